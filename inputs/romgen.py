@@ -1,0 +1,364 @@
+"""ROM construction -- the one-time CPU input-generation step (north_star).
+
+``BASELINE.json`` north_star: "The ROM construction (projection, CFL-extension
+perturbation) is a one-time CPU input-generation step that emits the reduced
+matrices both paths consume."  This module is that step.  Both the fp64 oracle
+(``oracle/``) and the CUDA path (``paper_1609_07114_b200``) read the matrices
+it emits; neither imports the other.  Everything here is fp64 NumPy/SciPy.
+
+Pipeline (citations are PAPER.md lines):
+  1. ``fine_system``  -- descriptor system of the fine region, eq:sys1a/b
+     (L286-292) with R^, F^, B^, L^ of eq:R, eq:F_f, eq:B, eq:L, eq:F11, eq:K
+     (L323-382); boundary rows with half lengths (eq:updateExS L217-222, L257).
+  2. ``collapse``     -- exact projection onto coarse-edge ports (R9):
+     the r fine boundary E nodes of one coarse edge are one degree of freedom
+     under eq:equalE (L608-611); ports become the nY coarse interface edges.
+  3. ``sprim``        -- SPRIM (L393): block Arnoldi on (G + s0 C)^{-1} C with
+     starting block (G + s0 C)^{-1} B, basis split into E / H rows and each part
+     orthonormalised, giving V = blkdiag(V1, V2) (eq:V L394-400; R10).
+  4. ``reduce``       -- congruence eq:R11_tilde ... eq:K_tilde (L431-447).
+  5. ``extend_cfl``   -- clip the singular values of R11~^-1/2 K~ R22~^-1/2 at
+     2/dt_target (eq:CFLgeneralized L741-745; R11/R12).
+
+Emitted model (dict, fp64, C order): bx, by, r, q1, q2, R11 (q1 x q1), R22
+(q2 x q2), F11 (q1 x q1), K (q1 x q2), L (q1 x nY) with nY = 2 bx + 2 by, ports
+ordered S (bx), N (bx), W (by), E (by).  B~ = L~ S_c is implied, S_c =
+diag(-dx, +dx, +dy, -dy) per side (eq:cond3rom L717 with eq:S L698-707,
+collapsed).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+C0 = 299792458.0
+MU0 = 4e-7 * math.pi
+EPS0 = 1.0 / (MU0 * C0 * C0)
+
+
+# --------------------------------------------------------------------------
+# 1. fine-region descriptor system
+# --------------------------------------------------------------------------
+def fine_system(bx, by, r, dx, dy, eps_r, sigma, mu_r=None):
+    """Assemble the fine-region system of Sec. II for a bx x by coarse block refined r times.
+
+    eps_r, sigma: per fine cell, shape (Ny, Nx) with Nx = bx r, Ny = by r.
+    Returns dict with diagonal vectors r11, f11 (nE), r22 (nH), sparse K (nE x nH),
+    B (nE x nP, E rows only), L (nE x nP selector), S (nP diag), plus sizes.
+    State order: Ex row-major (j outer), then Ey, then Hz.
+    """
+    Nx, Ny = bx * r, by * r
+    fdx, fdy = dx / r, dy / r
+    eps_r = np.asarray(eps_r, dtype=np.float64).reshape(Ny, Nx)
+    sigma = np.asarray(sigma, dtype=np.float64).reshape(Ny, Nx)
+    mu = MU0 * (np.ones((Ny, Nx)) if mu_r is None else np.asarray(mu_r, dtype=np.float64).reshape(Ny, Nx))
+    nEx, nEy, nH = Nx * (Ny + 1), (Nx + 1) * Ny, Nx * Ny
+    nE = nEx + nEy
+
+    def ex(i, j):
+        return j * Nx + i
+
+    def ey(i, j):
+        return nEx + j * (Nx + 1) + i
+
+    def hz(i, j):
+        return j * Nx + i
+
+    r11 = np.zeros(nE)
+    f11 = np.zeros(nE)
+    rows, cols, vals = [], [], []
+    # Ex nodes: eq:updateEx (interior) / eq:updateExS (S, N boundary: half dual length fdy/2)
+    for j in range(Ny + 1):
+        for i in range(Nx):
+            if j == 0:
+                e, s, lp = eps_r[0, i], sigma[0, i], fdy / 2
+            elif j == Ny:
+                e, s, lp = eps_r[Ny - 1, i], sigma[Ny - 1, i], fdy / 2
+            else:
+                e = 0.5 * (eps_r[j - 1, i] + eps_r[j, i])
+                s = 0.5 * (sigma[j - 1, i] + sigma[j, i])
+                lp = fdy
+            k = ex(i, j)
+            r11[k] = fdx * lp * EPS0 * e       # D_lx D_l'y D_eps_x (eq:R11)
+            f11[k] = fdx * lp * s / 2          # D_lx D_l'y D_sig_x / 2 (eq:F11)
+            if j < Ny:                          # + dx^ H_above (eq:updateEx)
+                rows.append(k); cols.append(hz(i, j)); vals.append(+fdx)
+            if j > 0:                           # - dx^ H_below
+                rows.append(k); cols.append(hz(i, j - 1)); vals.append(-fdx)
+    # Ey nodes: Ey analogue (L223), sign of eq:updateEymat: - dy^ (H_right - H_left)
+    for j in range(Ny):
+        for i in range(Nx + 1):
+            if i == 0:
+                e, s, lp = eps_r[j, 0], sigma[j, 0], fdx / 2
+            elif i == Nx:
+                e, s, lp = eps_r[j, Nx - 1], sigma[j, Nx - 1], fdx / 2
+            else:
+                e = 0.5 * (eps_r[j, i - 1] + eps_r[j, i])
+                s = 0.5 * (sigma[j, i - 1] + sigma[j, i])
+                lp = fdx
+            k = ey(i, j)
+            r11[k] = fdy * lp * EPS0 * e
+            f11[k] = fdy * lp * s / 2
+            if i < Nx:
+                rows.append(k); cols.append(hz(i, j)); vals.append(-fdy)
+            if i > 0:
+                rows.append(k); cols.append(hz(i - 1, j)); vals.append(+fdy)
+    K = sp.csr_matrix((vals, (rows, cols)), shape=(nE, nH))
+    r22 = fdx * fdy * mu.ravel()                  # D_A D_mu (R^22)
+    # ports S, N, W, E (eq:B, eq:L, eq:S; signs DESIGN.md R4)
+    port_node, port_sign, port_len = [], [], []
+    for i in range(Nx):
+        port_node.append(ex(i, 0)); port_sign.append(-1.0); port_len.append(fdx)
+    for i in range(Nx):
+        port_node.append(ex(i, Ny)); port_sign.append(+1.0); port_len.append(fdx)
+    for j in range(Ny):
+        port_node.append(ey(0, j)); port_sign.append(+1.0); port_len.append(fdy)
+    for j in range(Ny):
+        port_node.append(ey(Nx, j)); port_sign.append(-1.0); port_len.append(fdy)
+    nP = len(port_node)
+    pn = np.array(port_node)
+    S = np.array(port_sign) * np.array(port_len)
+    B = sp.csr_matrix((S, (pn, np.arange(nP))), shape=(nE, nP))
+    L = sp.csr_matrix((np.ones(nP), (pn, np.arange(nP))), shape=(nE, nP))
+    return dict(bx=bx, by=by, r=r, dx=dx, dy=dy, Nx=Nx, Ny=Ny, nE=nE, nH=nH, nP=nP,
+                r11=r11, f11=f11, r22=r22, K=K, B=B, L=L, S=S, port_node=pn)
+
+
+def full_order(sysf):
+    """Total state count nE + nH (the paper's 'order', e.g. 7,600 at N^=50, L840)."""
+    return sysf["nE"] + sysf["nH"]
+
+
+def descriptor_matrices(sysf, dt):
+    """Dense-free sparse R^, F^ of eq:R / eq:F_f (L323-338) at time step dt."""
+    nE, nH, K = sysf["nE"], sysf["nH"], sysf["K"]
+    R11 = sp.diags(sysf["r11"] / dt)
+    R22 = sp.diags(sysf["r22"] / dt)
+    R = sp.bmat([[R11, -0.5 * K], [-0.5 * K.T, R22]], format="csr")
+    F = sp.bmat([[sp.diags(sysf["f11"]), -0.5 * K], [0.5 * K.T, sp.csr_matrix((nH, nH))]], format="csr")
+    B = sp.vstack([sysf["B"], sp.csr_matrix((nH, sysf["nP"]))], format="csr")
+    L = sp.vstack([sysf["L"], sp.csr_matrix((nH, sysf["nP"]))], format="csr")
+    return R, F, B, L
+
+
+def fine_cfl_limit(sysf):
+    """dt_f = 2 / s_max(R^11^-1/2 K^ R^22^-1/2): the dt at which eq:cond1 fails (L708, R13)."""
+    X = sp.diags(1 / np.sqrt(sysf["r11"])) @ sysf["K"] @ sp.diags(1 / np.sqrt(sysf["r22"]))
+    smax = _smax(X)
+    return 2.0 / smax
+
+
+def _smax(X):
+    n = min(X.shape)
+    if n <= 400:
+        A = X.toarray() if sp.issparse(X) else np.asarray(X)
+        return float(np.linalg.svd(A, compute_uv=False)[0])
+    v = spla.svds(X, k=1, return_singular_vectors=False, tol=1e-12)
+    return float(v[0])
+
+
+# --------------------------------------------------------------------------
+# 2. collapse onto coarse-edge ports (R9)
+# --------------------------------------------------------------------------
+def collapse(sysf):
+    """Merge the r fine boundary E nodes of every coarse interface edge into one node.
+
+    Collapsed E ordering: the nY merged port nodes first (port order S,N,W,E), then the
+    interior E nodes.  Returns the collapsed system: diagonal r11c, f11c (nEc), r22,
+    Kc (nEc x nH), Sc (nY), plus the 0/1 map Pi (nE x nEc).
+    B_c = Pi^T B^ T = [diag(Sc); 0], L_c = Pi^T L^ T / r = [I; 0].
+    """
+    r, nE, nP = sysf["r"], sysf["nE"], sysf["nP"]
+    nY = nP // r
+    col = np.full(nE, -1, dtype=np.int64)
+    col[sysf["port_node"]] = np.arange(nP) // r          # fine port k -> coarse port k // r
+    interior = np.flatnonzero(col < 0)
+    col[interior] = nY + np.arange(interior.size)
+    nEc = nY + interior.size
+    Pi = sp.csr_matrix((np.ones(nE), (np.arange(nE), col)), shape=(nE, nEc))
+    r11c = Pi.T @ sysf["r11"]
+    f11c = Pi.T @ sysf["f11"]
+    Kc = (Pi.T @ sysf["K"]).tocsr()
+    Sc = np.array([sysf["S"][k * r: (k + 1) * r].sum() for k in range(nY)])  # = +-dx, +-dy
+    return dict(bx=sysf["bx"], by=sysf["by"], r=r, dx=sysf["dx"], dy=sysf["dy"], nY=nY, nEc=nEc,
+                nH=sysf["nH"], r11=r11c, f11=f11c, r22=sysf["r22"], K=Kc, Sc=Sc, Pi=Pi)
+
+
+def full_order_model(csys):
+    """V = I on the collapsed system: the exact (unreduced) embedded model."""
+    nEc, nY = csys["nEc"], csys["nY"]
+    L = np.zeros((nEc, nY))
+    L[np.arange(nY), np.arange(nY)] = 1.0
+    return dict(bx=csys["bx"], by=csys["by"], r=csys["r"], q1=nEc, q2=csys["nH"],
+                R11=np.diag(csys["r11"]), R22=np.diag(csys["r22"]), F11=np.diag(csys["f11"]),
+                K=csys["K"].toarray(), L=L, n_clipped=0)
+
+
+# --------------------------------------------------------------------------
+# 3. SPRIM (R10)
+# --------------------------------------------------------------------------
+def sprim_basis(csys, q, fmax, defl_tol=1e-10):
+    """Structure-preserving block Arnoldi basis V1 (nEc x q1), V2 (nH x q2).
+
+    Semi-discrete pencil of R(x'-x) + F(x'+x) = B u (eq:sys1a): C = blkdiag(R11, R22),
+    G = [[2 F11, -K], [K^T, 0]].  Krylov space of (G + s0 C)^{-1} C from (G + s0 C)^{-1} B,
+    real s0 = pi * fmax, C-inner product, modified Gram-Schmidt run twice, deflation
+    defl_tol.  m = ceil(q/2) vectors; the E and H rows are orthonormalised separately.
+    """
+    nEc, nH, nY = csys["nEc"], csys["nH"], csys["nY"]
+    s0 = math.pi * fmax
+    r11, f11, r22, K = csys["r11"], csys["f11"], csys["r22"], csys["K"]
+    # (G + s0 C) x = b, eliminating H: x_H = (b_H - K^T x_E) / (s0 r22)
+    schur = (sp.diags(2 * f11 + s0 * r11) + K @ sp.diags(1.0 / (s0 * r22)) @ K.T).tocsc()
+    lu = spla.splu(schur)
+
+    def solve(bE, bH):
+        xE = lu.solve(bE + K @ (bH / (s0 * r22)[:, None]))
+        xH = (bH - K.T @ xE) / (s0 * r22)[:, None]
+        return np.vstack([xE, xH])
+
+    cdiag = np.concatenate([r11, r22])
+
+    def cdot(u, v):
+        return float(np.dot(u * cdiag, v))
+
+    B0 = np.zeros((nEc, nY))
+    B0[np.arange(nY), np.arange(nY)] = csys["Sc"]
+    X0 = solve(B0, np.zeros((nH, nY)))
+    m = (q + 1) // 2
+    W = []
+
+    def add(v):
+        n0 = math.sqrt(cdot(v, v))
+        if n0 == 0.0:
+            return False
+        for _ in range(2):
+            for w in W:
+                v = v - cdot(w, v) * w
+        n1 = math.sqrt(cdot(v, v))
+        if n1 <= defl_tol * n0:
+            return False
+        W.append(v / n1)
+        return True
+
+    for c in range(nY):
+        if len(W) >= m:
+            break
+        add(X0[:, c])
+    j = 0
+    while len(W) < m and j < len(W):
+        y = solve((r11 * W[j][:nEc])[:, None], (r22 * W[j][nEc:])[:, None])[:, 0]  # M w = (G+s0C)^-1 C w
+        add(y)
+        j += 1
+    Wm = np.array(W).T
+    V1 = _orth(Wm[:nEc])
+    V2 = _orth(Wm[nEc:])
+    return V1, V2
+
+
+def _orth(A, tol=1e-12):
+    U, s, _ = np.linalg.svd(A, full_matrices=False)
+    k = int(np.sum(s > tol * s[0])) if s.size and s[0] > 0 else 0
+    return U[:, :k]
+
+
+# --------------------------------------------------------------------------
+# 4. congruence (eq:R11_tilde ... eq:K_tilde)
+# --------------------------------------------------------------------------
+def reduce(csys, V1, V2):
+    R11 = V1.T @ (csys["r11"][:, None] * V1)
+    R22 = V2.T @ (csys["r22"][:, None] * V2)
+    F11 = V1.T @ (csys["f11"][:, None] * V1)
+    K = V1.T @ (csys["K"] @ V2)
+    L = V1[: csys["nY"], :].T.copy()           # V1^T L_c with L_c = [I; 0]
+    sym = lambda A: 0.5 * (A + A.T)            # exact symmetry of congruences
+    return dict(bx=csys["bx"], by=csys["by"], r=csys["r"], q1=V1.shape[1], q2=V2.shape[1],
+                R11=sym(R11), R22=sym(R22), F11=sym(F11), K=np.ascontiguousarray(K),
+                L=np.ascontiguousarray(L), n_clipped=0)
+
+
+# --------------------------------------------------------------------------
+# 5. CFL extension (eq:CFLgeneralized)
+# --------------------------------------------------------------------------
+def _sqrtm_spd(A):
+    w, U = np.linalg.eigh(A)
+    if w.min() <= 1e-14 * w.max():
+        raise ValueError("matrix is not SPD (eigenvalue floor check)")
+    return (U * np.sqrt(w)) @ U.T, (U / np.sqrt(w)) @ U.T
+
+
+def generalized_singular_values(model):
+    """s_k of R11~^-1/2 K~ R22~^-1/2 (eq:CFLgeneralized), descending."""
+    _, i1 = _sqrtm_spd(model["R11"])
+    _, i2 = _sqrtm_spd(model["R22"])
+    return np.linalg.svd(i1 @ model["K"] @ i2, compute_uv=False)
+
+
+def rom_cfl_limit(model):
+    s = generalized_singular_values(model)
+    return 2.0 / s[0] if s.size and s[0] > 0 else math.inf
+
+
+def extend_cfl(model, dt_target, margin=1e-6):
+    """Clip s_k at (2/dt_target)(1 - margin); only K~ changes (L740-745, R11)."""
+    h1, i1 = _sqrtm_spd(model["R11"])
+    h2, i2 = _sqrtm_spd(model["R22"])
+    U, s, Wt = np.linalg.svd(i1 @ model["K"] @ i2, full_matrices=False)
+    cap = (2.0 / dt_target) * (1.0 - margin)
+    out = dict(model)
+    nclip = int(np.sum(s > cap))
+    out["n_clipped"] = nclip
+    if nclip == 0:
+        return out
+    out["K"] = np.ascontiguousarray(h1 @ (U * np.minimum(s, cap)) @ Wt @ h2)
+    return out
+
+
+def check_passivity(model, dt, tol=1e-12):
+    """eq:cond1rom-3rom (L713-719): returns (ok, min_eig_R, min_eig_FpFt)."""
+    q1, q2 = model["q1"], model["q2"]
+    Kt = model["K"]
+    R = np.block([[model["R11"] / dt, -0.5 * Kt], [-0.5 * Kt.T, model["R22"] / dt]])
+    F = np.block([[model["F11"], -0.5 * Kt], [0.5 * Kt.T, np.zeros((q2, q2))]])
+    # scale-free test: symmetric scaling by diag(R)^-1/2
+    d = 1 / np.sqrt(np.abs(np.diag(R)))
+    lamR = np.linalg.eigvalsh((R * d[:, None]) * d[None, :]).min()
+    FF = F + F.T
+    lamF = np.linalg.eigvalsh(FF).min() if q1 + q2 else 0.0
+    okF = lamF >= -tol * max(1e-300, np.abs(FF).max())
+    return bool(lamR > 0 and okF), float(lamR), float(lamF)
+
+
+# --------------------------------------------------------------------------
+# one-call driver
+# --------------------------------------------------------------------------
+def build_rom(bx, by, r, dx, dy, eps_r, sigma, q, fmax, dt_target=None, full=False):
+    """Fine assembly -> collapse -> SPRIM(q) -> reduce -> optional clip at dt_target."""
+    sysf = fine_system(bx, by, r, dx, dy, eps_r, sigma)
+    csys = collapse(sysf)
+    if full:
+        model = full_order_model(csys)
+    else:
+        V1, V2 = sprim_basis(csys, q, fmax)
+        model = reduce(csys, V1, V2)
+    model["natural_dt_limit"] = rom_cfl_limit(model) if not full else None
+    model["fine_dt_limit"] = fine_cfl_limit(sysf)
+    if dt_target is not None:
+        model = extend_cfl(model, dt_target)
+    return model
+
+
+def save_model(path, model):
+    np.savez(path, **{k: np.asarray(v) for k, v in model.items() if v is not None})
+
+
+def load_model(path):
+    z = np.load(path)
+    m = {k: z[k] for k in z.files}
+    for k in ("bx", "by", "r", "q1", "q2", "n_clipped"):
+        if k in m:
+            m[k] = int(m[k])
+    return m
