@@ -1,0 +1,196 @@
+/*
+ * fdtdrom.h -- C ABI of the B200 time-marching hot path of
+ * Zhang, Bekmambetova, Triverio, "A Stable FDTD Method with Embedded
+ * Reduced-Order Models" (arXiv 1609.07114).  Implemented by
+ * paper_1609_07114_b200/libfdtdrom.so (CUDA, sm_100a).
+ *
+ * The calls follow the paper's problem statement: "the
+ * proposed scheme consists of conventional FDTD equations to update the coarse
+ * grid, and (eq:connExplicit) to update the reduced model state and the
+ * interface.  If multiple reduced models are present, (eq:connExplicit) is
+ * applied to each one of them."
+ *
+ * Grid conventions (R1): coarse cells (i, j), 0-based, i along x.
+ * Hz at cell centres [ny][nx]; Ex on x-directed edges [ny+1][nx] (edge row j
+ * lies at y = j dy); Ey on y-directed edges [ny][nx+1] (edge column i lies at
+ * x = i dx).  All host arrays are row-major with j slow.  SI units.  PEC outer
+ * walls: Ex rows 0 and ny and Ey columns 0 and nx are identically zero.
+ *
+ * Ownership: every host input is copied before the call returns; the caller
+ * keeps its buffers.  The context owns its device memory (obtained through the
+ * optional allocator, so the PyTorch caching allocator can back it).  The
+ * stream and the NCCL unique id are borrowed.
+ *
+ * Errors: every call returns an fdtd_status; no exception crosses the ABI.
+ * fdtd_last_error() gives the text of the last failure of that context.
+ * fdtd_step only enqueues work; asynchronous faults (CUDA errors, the
+ * non-finite sentinel) surface at the next synchronous call (fdtd_probe,
+ * fdtd_energy, fdtd_get_window, fdtd_sync).
+ *
+ * Threading: a context is single-threaded; several contexts may coexist.
+ */
+#ifndef FDTDROM_H
+#define FDTDROM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fdtd_ctx fdtd_ctx;
+
+typedef enum {
+  FDTD_OK = 0,
+  FDTD_E_ARG = 1,       /* invalid argument, placement or state                       */
+  FDTD_E_STATE = 2,     /* call not valid now (e.g. record buffer would overflow)     */
+  FDTD_E_PASSIVITY = 3, /* ROM violates eq:cond1rom / eq:cond2rom at dt (L713-719)     */
+  FDTD_E_UNSTABLE = 4,  /* dt above eq.(1) (L36-38) or non-finite fields detected      */
+  FDTD_E_CUDA = 5,
+  FDTD_E_NCCL = 6,
+  FDTD_E_NOMEM = 7
+} fdtd_status;
+
+/* fdtd_grid_desc.flags */
+#define FDTD_MATERIALS_ON_DEVICE 0x1u /* eps_r / sigma are device pointers            */
+#define FDTD_MATERIALS_F32 0x2u       /* eps_r / sigma are float (else double)        */
+#define FDTD_ALLOW_DT_ABOVE_EQ1 0x4u  /* skip the eq.(1) check (e.g. tests of blow-up) */
+#define FDTD_NO_GRAPH 0x8u            /* never capture CUDA graphs in fdtd_step        */
+
+typedef struct {
+  int64_t nx, ny;          /* global coarse cells                                         */
+  double dx, dy, dt;       /* cell sizes and time step, SI                                */
+  int32_t precision;       /* 32 (fp32 state) or 64 (fp64 state)                          */
+  uint32_t flags;          /* FDTD_* flags above                                          */
+  /* Per-cell relative permittivity and conductivity (S/m), row-major [rows][nx].  The
+   * pointer addresses global row `materials_row0`; it must cover the rows
+   * [max(row_begin-1, 0), row_end) of the grid.  Edge values are the arithmetic mean of
+   * the two adjacent cells (R2).  mu = mu0 everywhere
+   * (R3).  Host or device memory (FDTD_MATERIALS_ON_DEVICE), double or float
+   * (FDTD_MATERIALS_F32). */
+  const void *eps_r, *sigma;
+  int64_t materials_row0;
+  int32_t device;          /* CUDA device ordinal                                         */
+  void *stream;            /* cudaStream_t work is ordered on (borrowed); NULL: legacy     */
+  /* optional allocator (e.g. the PyTorch caching allocator); NULL: cudaMalloc/cudaFree  */
+  void *(*alloc)(size_t bytes, void *user);
+  void (*free)(void *ptr, void *user);
+  void *alloc_user;
+  /* row-slab decomposition: this rank owns coarse cell rows
+   * [row_begin, row_end) and Ex edge rows [row_begin, row_end).  nranks == 1: the
+   * whole grid (row_begin = 0, row_end = ny). */
+  int32_t nranks, rank;
+  const void *nccl_id;     /* 128-byte ncclUniqueId (same on every rank); NULL if nranks == 1 */
+  int64_t row_begin, row_end;
+  int64_t record_capacity; /* steps of probe / energy records kept on device (0: 65536)  */
+} fdtd_grid_desc;
+
+/* Create a context: validates the descriptor, builds the per-edge update
+ * coefficients of eq:updateEx (L209-214) on the device, allocates the fields
+ * (zero) and checks dt against eq.(1) (L36-38) with c_max = c0/sqrt(min eps_r).
+ * FDTD_E_UNSTABLE if dt exceeds eq.(1) and FDTD_ALLOW_DT_ABOVE_EQ1 is not set. */
+fdtd_status fdtd_create(const fdtd_grid_desc *desc, fdtd_ctx **out);
+
+/* One reduced model, as emitted by the ROM generator (fp64, row-major, host):
+ * R11 (q1 x q1), R22 (q2 x q2), F11 (q1 x q1), K (q1 x q2), L (q1 x nY) with
+ * nY = 2 bx + 2 by ports ordered S (bx, left->right), N (bx), W (by,
+ * bottom->top), E (by).  These are R~11, R~22, F~11, K~, L~ of eq:rom1a/b and
+ * eq:R11_tilde..eq:K_tilde (L406-447) after the exact collapse onto coarse-edge
+ * ports (R9); B~ = L~ S_c is implied with S_c = diag(-dx, +dx, +dy,
+ * -dy) per side (eq:cond3rom L717, eq:S L698-707).  r is informational. */
+typedef struct {
+  int32_t bx, by, r, q1, q2;
+  const double *R11, *R22, *F11, *K, *L;
+} fdtd_rom_model;
+
+/* Embed `count` instances of one model with lower-left coarse cells anchors[2k],
+ * anchors[2k+1] (global (i0, j0)).  Each instance occupies cells [i0, i0+bx) x
+ * [j0, j0+by); it is coupled through eq:updateExboundary (L461-468, coarse half
+ * cell outside the block) and eq:connExplicit (L666-675), evaluated in an
+ * equivalent factored form.
+ * Checks: FDTD_E_PASSIVITY if R~(dt) is not positive definite (eq:cond1rom) or
+ * F~11 + F~11^T has an eigenvalue below -1e-12 |F| (eq:cond2rom); FDTD_E_ARG if
+ * a footprint plus its one-cell ring leaves this rank's rows, touches the PEC
+ * wall, or overlaps another instance's footprint plus ring.  On success
+ * *model_id receives the model's index. */
+fdtd_status fdtd_add_rom(fdtd_ctx *c, const fdtd_rom_model *m, const int32_t *anchors,
+                         int64_t count, int32_t *model_id);
+
+/* Soft Hz source (R15): after the H half-step of step n,
+ * Hz[j][i] += samples[n - step0] for step0 <= n < step0 + n_samples, else 0.
+ * Replaces any previous source.  A cell outside this rank's rows is ignored. */
+fdtd_status fdtd_set_source(fdtd_ctx *c, int64_t i, int64_t j, const double *samples,
+                            int64_t n_samples, int64_t step0);
+
+/* Probes: record Hz^{n+1/2} at cells ij[2p], ij[2p+1] after every step n (R16). */
+fdtd_status fdtd_set_probes(fdtd_ctx *c, const int64_t *ij, int32_t n_probes);
+
+/* Record the storage function W^n (R17) every step (1) or not (0). */
+fdtd_status fdtd_record_energy(fdtd_ctx *c, int32_t on);
+
+/* Enqueue `nsteps` time steps on the context's stream (asynchronous).  Each step:
+ * H half-step (eq:updateH), source, probes and energy, per-ROM gather / reduced
+ * update / scatter (eq:connExplicit), E half-step (eq:updateEx) -- S1..S8 of
+ * DESIGN.md.  FDTD_E_STATE if the unread probe/energy records would exceed
+ * record_capacity. */
+fdtd_status fdtd_step(fdtd_ctx *c, int64_t nsteps);
+
+/* Read and consume the probe records of the steps taken since the last read:
+ * out[p * cap_steps + k] (row-major [n_probes][cap_steps]), k = 0 .. *n_steps-1.
+ * With several ranks, probes are summed over ranks (each cell lives on one rank).
+ * Synchronous. */
+fdtd_status fdtd_probe(fdtd_ctx *c, double *out, int64_t cap_steps, int64_t *n_steps);
+
+/* Read and consume the energy records W^n of the steps since the last read
+ * (fp64, summed over ranks).  Synchronous. */
+fdtd_status fdtd_energy(fdtd_ctx *c, double *out, int64_t cap, int64_t *n);
+
+/* Copy a window of the global fields to / from host fp64 arrays: Hz cells
+ * [i0, i0+w) x [j0, j0+h) -> Hz[h][w]; Ex edges [i0, i0+w) x rows [j0, j0+h]
+ * -> Ex[h+1][w]; Ey edges columns [i0, i0+w] x rows [j0, j0+h) -> Ey[h][w+1].
+ * Only rows owned by this rank are transferred; NULL pointers are skipped.
+ * fdtd_set_window also zeroes ROM hole cells/edges and keeps PEC walls zero.
+ * Synchronous. */
+fdtd_status fdtd_get_window(fdtd_ctx *c, int64_t i0, int64_t j0, int64_t w, int64_t h,
+                            double *Ex, double *Ey, double *Hz);
+fdtd_status fdtd_set_window(fdtd_ctx *c, int64_t i0, int64_t j0, int64_t w, int64_t h,
+                            const double *Ex, const double *Ey, const double *Hz);
+
+/* ROM states x~ = [E~; H~] (q1 + q2 per instance, instances in the order they were
+ * added on this rank), fp64.  Synchronous. */
+fdtd_status fdtd_get_rom_state(fdtd_ctx *c, double *out, int64_t cap, int64_t *n);
+fdtd_status fdtd_set_rom_state(fdtd_ctx *c, const double *in, int64_t n);
+
+/* Block until all enqueued work finished; reports asynchronous faults. */
+fdtd_status fdtd_sync(fdtd_ctx *c);
+
+/* Introspection (host values; no synchronisation). */
+typedef struct {
+  int64_t steps_taken;         /* steps enqueued so far                                    */
+  int64_t n_instances;         /* ROM instances on this rank                               */
+  int64_t kernel_launches;     /* kernels launched by fdtd_step so far (graph nodes count)  */
+  int64_t pitch;               /* elements per device row                                  */
+  int64_t sweep_ctas;          /* CTAs of one fused-sweep launch                           */
+  int32_t graphs;              /* 1 if fdtd_step replays CUDA graphs                       */
+  int32_t precision;
+  double bytes_per_cell_step;  /* algorithmic bytes of the fused sweep per cell-step        */
+  void *sweep_stream;          /* cudaStream_t the kernels are launched on                 */
+} fdtd_info;
+fdtd_status fdtd_get_info(const fdtd_ctx *c, fdtd_info *out);
+
+/* Tuning knobs for the fused sweep (rows per CTA, warps per CTA); 0 keeps default. */
+fdtd_status fdtd_set_tuning(fdtd_ctx *c, int32_t rows_per_cta, int32_t warps_per_cta);
+
+/* Fill out[128] with a fresh ncclUniqueId (rank 0 calls it and broadcasts the bytes, e.g. with
+ * torch.distributed.broadcast).  FDTD_E_NCCL if libnccl.so.2 cannot be loaded. */
+fdtd_status fdtd_nccl_unique_id(void *out128);
+
+const char *fdtd_last_error(const fdtd_ctx *c);
+const char *fdtd_status_string(fdtd_status s);
+void fdtd_destroy(fdtd_ctx *c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDTDROM_H */

@@ -1,0 +1,8 @@
+"""B200-native time-marching hot path of arXiv 1609.07114 (FDTD with embedded reduced-order models).
+
+The product is libfdtdrom.so (C ABI in include/fdtdrom.h, CUDA kernels for sm_100a);
+``fdtdrom`` is its thin ctypes binding.  Build with ``python -m paper_1609_07114_b200.build``.
+"""
+from .fdtdrom import FDTDError, Simulation, from_scene, lib, nccl_unique_id  # noqa: F401
+
+__all__ = ["Simulation", "FDTDError", "from_scene", "lib", "nccl_unique_id"]

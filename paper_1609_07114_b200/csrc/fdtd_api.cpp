@@ -1,0 +1,1022 @@
+// Host implementation of the C ABI declared in include/fdtdrom.h.
+//
+// Owns the device state of one row slab: ping-pong field buffers with one ghost row on each
+// side, the per-edge coefficients, the ROM operators, probe/energy record rings, and (for
+// several ranks) an NCCL communicator used for the per-step halo exchange of DESIGN.md
+// "Multi-GPU".  All per-step work is enqueued on one stream; fdtd_step replays a captured
+// two-step CUDA graph when possible.
+#include "fdtdrom.h"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dense.hpp"
+#include "fdtd_kernels.cuh"
+
+namespace {
+
+constexpr double MU0 = 4.0e-7 * 3.14159265358979323846;
+constexpr double C0 = 299792458.0;
+constexpr double EPS0 = 1.0 / (MU0 * C0 * C0);
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+typedef struct { char internal[128]; } nccl_uid;
+typedef void* nccl_comm;
+struct Nccl {
+  void* h = nullptr;
+  int (*CommInitRank)(nccl_comm*, int, nccl_uid, int) = nullptr;
+  int (*CommDestroy)(nccl_comm) = nullptr;
+  int (*Send)(const void*, size_t, int, int, nccl_comm, cudaStream_t) = nullptr;
+  int (*Recv)(void*, size_t, int, int, nccl_comm, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  int (*GetUniqueId)(nccl_uid*) = nullptr;
+  bool load(std::string& err) {
+    if (h) return true;
+    const char* env = getenv("FDTD_NCCL_LIB");
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the copy torch already loaded
+    if (!h && env) h = dlopen(env, RTLD_NOW);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (!h) { err = "cannot load libnccl.so.2"; return false; }
+#define SYM(n) n = reinterpret_cast<decltype(n)>(dlsym(h, "nccl" #n)); if (!n) { err = "missing nccl" #n; return false; }
+    SYM(CommInitRank) SYM(CommDestroy) SYM(Send) SYM(Recv) SYM(GroupStart) SYM(GroupEnd) SYM(AllReduce)
+    SYM(GetErrorString) SYM(GetUniqueId)
+#undef SYM
+    return true;
+  }
+};
+Nccl g_nccl;
+constexpr int NCCL_F32 = 7, NCCL_F64 = 8, NCCL_SUM = 0;
+
+struct ModelHost {
+  int bx, by, nY, q1, q2;
+  std::vector<double> P;  // nY x nY: L~^T C^-1 B~
+  fdtd::RomModelDev dev;
+};
+
+}  // namespace
+
+struct fdtd_ctx {
+  fdtd_grid_desc d{};
+  int prec = 32;
+  size_t es = 4;  // element size
+  int V = 4;      // elements per 16-byte vector
+  int rows = 0;   // owned rows
+  int64_t nrows_alloc = 0, pitch = 0;
+  int ncolv = 0;
+  cudaStream_t stream = nullptr, cap_stream = nullptr;
+  std::string err;
+  // device buffers (element type T)
+  void* f[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};  // [buf][ex,ey,hz]
+  void* coef[4] = {nullptr, nullptr, nullptr, nullptr};
+  void* mat_eps = nullptr;  // device copy of per-cell materials for rows [mrow0, row_end)
+  void* mat_sig = nullptr;
+  bool mat_f32 = false;
+  int64_t mrow0 = 0;
+  int64_t* d_step = nullptr;
+  unsigned* d_done = nullptr;
+  double* d_partials = nullptr;
+  int n_partials = 0;
+  int chunk = 64, warps = 4;
+  // source
+  double* d_src = nullptr;
+  int64_t src_n = 0, src_t0 = 0, src_i = -1, src_j = -1, src_cap = 0;
+  // probes & energy rings
+  int64_t cap = 65536;
+  int n_probe = 0;
+  int64_t* d_probe_idx = nullptr;
+  void* d_probe_ring = nullptr;
+  double* d_energy_ring = nullptr;
+  bool energy_on = false;
+  int64_t steps = 0, rd_probe = 0, rd_energy = 0;
+  // ROMs
+  std::vector<ModelHost> models;
+  std::vector<int32_t> inst_model, rects;  // rects: (i0, j0, bx, by) global
+  std::vector<int64_t> port_off, port_edge, port_h, ring_idx, ring_off, state_off, Sk_off;
+  std::vector<double> cya, cyg, ehalf, Sk;  // fp64 host copies (converted on upload)
+  std::vector<double> mpool;                // shared model matrices (col-major, fp64)
+  int nvec = 1;
+  // device ROM arrays
+  void* d_mpool = nullptr; void* d_Sk = nullptr; void* d_cya = nullptr; void* d_cyg = nullptr;
+  void* d_state = nullptr; double* d_ehalf = nullptr; double* d_rom_partials = nullptr;
+  int64_t *d_port_off = nullptr, *d_port_edge = nullptr, *d_port_h = nullptr, *d_ring_idx = nullptr,
+          *d_ring_off = nullptr, *d_state_off = nullptr, *d_Sk_off = nullptr;
+  int32_t* d_inst_model = nullptr;
+  fdtd::RomModelDev* d_models = nullptr;
+  int64_t state_len = 0;
+  // graphs
+  cudaGraphExec_t gexec = nullptr;
+  bool graph_dirty = true;
+  int64_t launches = 0;
+  // multi-rank
+  nccl_comm comm = nullptr;
+  std::vector<void*> owned;  // every device allocation
+};
+
+namespace {
+
+fdtd_status fail(fdtd_ctx* c, fdtd_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return s;
+}
+
+#define CK(call)                                                                             \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess) return fail(c, FDTD_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define NK(call)                                                                         \
+  do {                                                                                   \
+    int r_ = (call);                                                                     \
+    if (r_ != 0) return fail(c, FDTD_E_NCCL, "%s: %s", #call, g_nccl.GetErrorString(r_)); \
+  } while (0)
+
+void* dalloc(fdtd_ctx* c, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  void* p = nullptr;
+  if (c->d.alloc) {
+    p = c->d.alloc(bytes, c->d.alloc_user);
+  } else if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    p = nullptr;
+  }
+  if (p) {
+    c->owned.push_back(p);
+    if (cudaMemsetAsync(p, 0, bytes, c->stream) != cudaSuccess) return nullptr;
+  }
+  return p;
+}
+
+void dfree(fdtd_ctx* c, void* p) {
+  if (!p) return;
+  auto it = std::find(c->owned.begin(), c->owned.end(), p);
+  if (it != c->owned.end()) c->owned.erase(it);
+  if (c->d.free) c->d.free(p, c->d.alloc_user);
+  else cudaFree(p);
+}
+
+template <typename X>
+fdtd_status upload(fdtd_ctx* c, X** dst, const std::vector<X>& v) {
+  if (*dst) { dfree(c, *dst); *dst = nullptr; }
+  *dst = static_cast<X*>(dalloc(c, v.size() * sizeof(X)));
+  if (!*dst) return fail(c, FDTD_E_NOMEM, "device allocation of %zu bytes failed", v.size() * sizeof(X));
+  if (!v.empty()) CK(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(X), cudaMemcpyHostToDevice, c->stream));
+  return FDTD_OK;
+}
+
+// upload an fp64 host vector converted to the storage precision
+fdtd_status upload_T(fdtd_ctx* c, void** dst, const std::vector<double>& v) {
+  if (c->prec == 64) return upload(c, reinterpret_cast<double**>(dst), v);
+  std::vector<float> f(v.begin(), v.end());
+  return upload(c, reinterpret_cast<float**>(dst), f);
+}
+
+inline int64_t lrow(const fdtd_ctx* c, int64_t g) { return g - c->d.row_begin + 1; }
+
+template <typename T>
+fdtd::SweepParams<T> sweep_params(fdtd_ctx* c, int q) {
+  fdtd::SweepParams<T> p{};
+  p.ex0 = (const T*)c->f[q][0]; p.ey0 = (const T*)c->f[q][1]; p.hz0 = (const T*)c->f[q][2];
+  p.ex1 = (T*)c->f[1 - q][0]; p.ey1 = (T*)c->f[1 - q][1]; p.hz1 = (T*)c->f[1 - q][2];
+  p.cax = (const T*)c->coef[0]; p.cbx = (const T*)c->coef[1];
+  p.cay = (const T*)c->coef[2]; p.cby = (const T*)c->coef[3];
+  p.pitch = c->pitch; p.ncolv = c->ncolv; p.rows = c->rows; p.chunk = c->chunk;
+  p.chx = (T)(c->d.dt / (MU0 * c->d.dx));
+  p.chy = (T)(c->d.dt / (MU0 * c->d.dy));
+  const bool src_here = c->d_src && c->src_j >= c->d.row_begin && c->src_j < c->d.row_end;
+  p.src_row = src_here ? (int)lrow(c, c->src_j) : -1;
+  p.src_col = src_here ? c->src_i : -1;
+  p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
+  p.step = c->d_step;
+  p.partials = c->energy_on ? c->d_partials : nullptr;
+  p.wex = (T)(c->d.dx / 2); p.wey = (T)(c->d.dy / 2);
+  p.wh = (T)(MU0 * c->d.dx * c->d.dy / c->d.dt);
+  return p;
+}
+
+template <typename T>
+fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
+  fdtd::PostParams<T> p{};
+  p.n_inst = (int)c->inst_model.size();
+  p.inst_model = c->d_inst_model; p.models = c->d_models; p.mpool = (const T*)c->d_mpool;
+  p.Sk = (const T*)c->d_Sk; p.Sk_off = c->d_Sk_off; p.port_off = c->d_port_off;
+  p.cya = (const T*)c->d_cya; p.cyg = (const T*)c->d_cyg; p.ehalf = c->d_ehalf;
+  p.port_edge = c->d_port_edge; p.port_h = c->d_port_h; p.ring_idx = c->d_ring_idx; p.ring_off = c->d_ring_off;
+  p.state = (T*)c->d_state; p.state_off = c->d_state_off;
+  p.ex1 = (T*)c->f[1 - q][0]; p.ey1 = (T*)c->f[1 - q][1]; p.hz1 = (T*)c->f[1 - q][2];
+  p.n_probe = c->n_probe; p.probe_idx = c->d_probe_idx; p.probe_ring = (T*)c->d_probe_ring; p.cap = c->cap;
+  p.sweep_partials = c->d_partials; p.n_sweep_partials = c->n_partials;
+  p.rom_partials = c->d_rom_partials; p.energy_ring = c->d_energy_ring;
+  p.step = c->d_step; p.done = c->d_done;
+  p.nthreads_vec = c->nvec;
+  return p;
+}
+
+fdtd_status halo_exchange(fdtd_ctx* c, int q, cudaStream_t s) {
+  if (c->d.nranks <= 1) return FDTD_OK;
+  const size_t n = (size_t)c->pitch;
+  const int dt = c->prec == 64 ? NCCL_F64 : NCCL_F32;
+  const int up = c->d.rank + 1, dn = c->d.rank - 1;
+  const size_t es = c->es;
+  auto row = [&](int a, int64_t r) { return (char*)c->f[q][a] + (size_t)r * n * es; };
+  NK(g_nccl.GroupStart());
+  if (up < c->d.nranks) {  // my top owned row (Hz, Ex, Ey) -> up's ghost row 0; up's Ex row 1 -> my row rows+1
+    for (int a = 0; a < 3; ++a) NK(g_nccl.Send(row(a, c->rows), n, dt, up, c->comm, s));
+    NK(g_nccl.Recv(row(0, c->rows + 1), n, dt, up, c->comm, s));
+  }
+  if (dn >= 0) {
+    for (int a = 0; a < 3; ++a) NK(g_nccl.Recv(row(a, 0), n, dt, dn, c->comm, s));
+    NK(g_nccl.Send(row(0, 1), n, dt, dn, c->comm, s));
+  }
+  NK(g_nccl.GroupEnd());
+  return FDTD_OK;
+}
+
+fdtd_status enqueue_step(fdtd_ctx* c, int q, cudaStream_t s) {
+  fdtd_status st = halo_exchange(c, q, s);
+  if (st != FDTD_OK) return st;
+  if (c->prec == 64) {
+    fdtd::launch_sweep<double>(sweep_params<double>(c, q), c->warps, s);
+    fdtd::launch_post<double>(post_params<double>(c, q), c->energy_on, s);
+  } else {
+    fdtd::launch_sweep<float>(sweep_params<float>(c, q), c->warps, s);
+    fdtd::launch_post<float>(post_params<float>(c, q), c->energy_on, s);
+  }
+  c->launches += 2;
+  return FDTD_OK;
+}
+
+void drop_graph(fdtd_ctx* c) {
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  c->gexec = nullptr;
+  c->graph_dirty = true;
+}
+
+fdtd_status build_graph(fdtd_ctx* c) {
+  drop_graph(c);
+  if (!c->cap_stream) CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+  const int64_t before = c->launches;
+  fdtd_status st = enqueue_step(c, 0, c->cap_stream);
+  if (st == FDTD_OK) st = enqueue_step(c, 1, c->cap_stream);
+  c->launches = before;
+  cudaError_t e = cudaStreamEndCapture(c->cap_stream, &g);
+  if (st != FDTD_OK) return st;
+  if (e != cudaSuccess) return fail(c, FDTD_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&c->gexec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(c, FDTD_E_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  c->graph_dirty = false;
+  return FDTD_OK;
+}
+
+fdtd_status check_async(fdtd_ctx* c) {
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaGetLastError());
+  return FDTD_OK;
+}
+
+template <typename M>
+fdtd_status build_coefficients(fdtd_ctx* c) {
+  const M* e = (const M*)c->mat_eps;
+  const M* s = (const M*)c->mat_sig;
+  if (c->prec == 64)
+    fdtd::launch_coefficients<double, M>(e, s, c->mrow0, c->d.nx, c->d.ny, c->d.row_begin, c->rows, c->pitch,
+                                         c->d.dx, c->d.dy, c->d.dt, (double*)c->coef[0], (double*)c->coef[1],
+                                         (double*)c->coef[2], (double*)c->coef[3], c->stream);
+  else
+    fdtd::launch_coefficients<float, M>(e, s, c->mrow0, c->d.nx, c->d.ny, c->d.row_begin, c->rows, c->pitch,
+                                        c->d.dx, c->d.dy, c->d.dt, (float*)c->coef[0], (float*)c->coef[1],
+                                        (float*)c->coef[2], (float*)c->coef[3], c->stream);
+  CK(cudaGetLastError());
+  return FDTD_OK;
+}
+
+fdtd_status gather_materials(fdtd_ctx* c, const std::vector<int64_t>& cells, std::vector<double>& eps,
+                             std::vector<double>& sig) {
+  const int64_t n = (int64_t)cells.size();
+  eps.assign(n, 0.0);
+  sig.assign(n, 0.0);
+  if (n == 0) return FDTD_OK;
+  int64_t* dc = nullptr;
+  fdtd_status st = upload(c, &dc, cells);
+  if (st != FDTD_OK) return st;
+  double* de = (double*)dalloc(c, n * sizeof(double));
+  double* ds = (double*)dalloc(c, n * sizeof(double));
+  if (!de || !ds) return fail(c, FDTD_E_NOMEM, "gather buffers");
+  if (c->mat_f32)
+    fdtd::launch_gather_materials<float>((const float*)c->mat_eps, (const float*)c->mat_sig, c->d.nx, c->mrow0, dc,
+                                         n, de, ds, c->stream);
+  else
+    fdtd::launch_gather_materials<double>((const double*)c->mat_eps, (const double*)c->mat_sig, c->d.nx, c->mrow0,
+                                          dc, n, de, ds, c->stream);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(eps.data(), de, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(sig.data(), ds, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  dfree(c, dc);
+  dfree(c, de);
+  dfree(c, ds);
+  return FDTD_OK;
+}
+
+fdtd_status upload_roms(fdtd_ctx* c) {
+  fdtd_status st;
+  std::vector<fdtd::RomModelDev> md;
+  for (auto& m : c->models) md.push_back(m.dev);
+  if ((st = upload_T(c, &c->d_mpool, c->mpool)) != FDTD_OK) return st;
+  if ((st = upload(c, &c->d_models, md)) != FDTD_OK) return st;
+  if ((st = upload(c, &c->d_inst_model, c->inst_model)) != FDTD_OK) return st;
+  if ((st = upload_T(c, &c->d_Sk, c->Sk)) != FDTD_OK) return st;
+  if ((st = upload(c, &c->d_Sk_off, c->Sk_off)) != FDTD_OK) return st;
+  if ((st = upload(c, &c->d_port_off, c->port_off)) != FDTD_OK) return st;
+  if ((st = upload_T(c, &c->d_cya, c->cya)) != FDTD_OK) return st;
+  if ((st = upload_T(c, &c->d_cyg, c->cyg)) != FDTD_OK) return st;
+  if ((st = upload(c, &c->d_ehalf, c->ehalf)) != FDTD_OK) return st;
+  if ((st = upload(c, &c->d_port_edge, c->port_edge)) != FDTD_OK) return st;
+  if ((st = upload(c, &c->d_port_h, c->port_h)) != FDTD_OK) return st;
+  if ((st = upload(c, &c->d_ring_idx, c->ring_idx)) != FDTD_OK) return st;
+  if ((st = upload(c, &c->d_ring_off, c->ring_off)) != FDTD_OK) return st;
+  if ((st = upload(c, &c->d_state_off, c->state_off)) != FDTD_OK) return st;
+  // ROM states start at zero (R26: x~0 = 0 with y0 = 0 on the freshly zeroed interface edges)
+  std::vector<double> zero(c->state_len, 0.0);
+  void* prev = c->d_state;
+  c->d_state = nullptr;
+  if ((st = upload_T(c, &c->d_state, zero)) != FDTD_OK) return st;
+  if (prev) dfree(c, prev);
+  std::vector<double> zp(c->inst_model.size() + 1, 0.0);
+  if ((st = upload(c, &c->d_rom_partials, zp)) != FDTD_OK) return st;
+  return FDTD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fdtd_status_string(fdtd_status s) {
+  switch (s) {
+    case FDTD_OK: return "ok";
+    case FDTD_E_ARG: return "invalid argument";
+    case FDTD_E_STATE: return "invalid state";
+    case FDTD_E_PASSIVITY: return "reduced model not passive at dt";
+    case FDTD_E_UNSTABLE: return "unstable";
+    case FDTD_E_CUDA: return "CUDA error";
+    case FDTD_E_NCCL: return "NCCL error";
+    case FDTD_E_NOMEM: return "out of memory";
+  }
+  return "unknown";
+}
+
+const char* fdtd_last_error(const fdtd_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
+  fdtd_ctx* c = nullptr;
+  if (!desc || !out) return FDTD_E_ARG;
+  *out = nullptr;
+  const fdtd_grid_desc& d = *desc;
+  if (d.nx < 1 || d.ny < 1 || !(d.dx > 0) || !(d.dy > 0) || !(d.dt > 0)) return FDTD_E_ARG;
+  if (d.precision != 32 && d.precision != 64) return FDTD_E_ARG;
+  if (!d.eps_r || !d.sigma) return FDTD_E_ARG;
+  const int nranks = d.nranks <= 0 ? 1 : d.nranks;
+  int64_t rb = d.row_begin, re = d.row_end;
+  if (nranks == 1 && rb == 0 && re == 0) re = d.ny;
+  if (rb < 0 || re > d.ny || re <= rb) return FDTD_E_ARG;
+  if (re - rb > (int64_t)1 << 30) return FDTD_E_ARG;
+  if (nranks > 1 && !d.nccl_id) return FDTD_E_ARG;
+  const int64_t m0 = std::max<int64_t>(rb - 1, 0);
+  if (d.materials_row0 > m0) return FDTD_E_ARG;
+
+  c = new fdtd_ctx();
+  c->d = d;
+  c->d.nranks = nranks;
+  c->d.row_begin = rb;
+  c->d.row_end = re;
+  c->prec = d.precision;
+  c->es = d.precision == 64 ? 8 : 4;
+  c->V = 16 / (int)c->es;
+  c->rows = (int)(re - rb);
+  c->nrows_alloc = c->rows + 2;
+  c->ncolv = (int)((d.nx + c->V - 1) / c->V);
+  const int64_t align = 128 / (int64_t)c->es;
+  c->pitch = ((int64_t)c->ncolv * c->V + align - 1) / align * align;
+  c->cap = d.record_capacity > 0 ? d.record_capacity : 65536;
+  c->stream = (cudaStream_t)d.stream;
+  if (cudaSetDevice(d.device) != cudaSuccess) {
+    delete c;
+    return FDTD_E_CUDA;
+  }
+
+  // eq.(1) with c_max from the smallest eps_r (host check needs the values; device arrays
+  // are reduced on the host after a copy of the owned rows)
+  const int64_t nmat = (re - m0) * d.nx;
+  const bool f32 = (d.flags & FDTD_MATERIALS_F32) != 0;
+  const bool on_dev = (d.flags & FDTD_MATERIALS_ON_DEVICE) != 0;
+  const size_t mes = f32 ? 4 : 8;
+  const char* ebase = (const char*)d.eps_r + (size_t)(m0 - d.materials_row0) * d.nx * mes;
+  const char* sbase = (const char*)d.sigma + (size_t)(m0 - d.materials_row0) * d.nx * mes;
+  c->mat_f32 = f32;
+  c->mrow0 = m0;
+  c->mat_eps = dalloc(c, nmat * mes);
+  c->mat_sig = dalloc(c, nmat * mes);
+  if (!c->mat_eps || !c->mat_sig) {
+    fdtd_destroy(c);
+    return FDTD_E_NOMEM;
+  }
+  const cudaMemcpyKind kind = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if (cudaMemcpyAsync(c->mat_eps, ebase, nmat * mes, kind, c->stream) != cudaSuccess ||
+      cudaMemcpyAsync(c->mat_sig, sbase, nmat * mes, kind, c->stream) != cudaSuccess) {
+    fdtd_destroy(c);
+    return FDTD_E_CUDA;
+  }
+  double emin = INFINITY, smin = INFINITY;
+  {
+    // min eps_r over the owned rows (host side; device arrays are copied once)
+    std::vector<char> hbuf;
+    const char* he = ebase;
+    const char* hs = sbase;
+    std::vector<char> hsb;
+    if (on_dev) {
+      hbuf.resize(nmat * mes);
+      hsb.resize(nmat * mes);
+      if (cudaMemcpy(hbuf.data(), c->mat_eps, nmat * mes, cudaMemcpyDeviceToHost) != cudaSuccess ||
+          cudaMemcpy(hsb.data(), c->mat_sig, nmat * mes, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        fdtd_destroy(c);
+        return FDTD_E_CUDA;
+      }
+      he = hbuf.data();
+      hs = hsb.data();
+    }
+    for (int64_t k = 0; k < nmat; ++k) {
+      const double e = f32 ? (double)((const float*)he)[k] : ((const double*)he)[k];
+      const double s = f32 ? (double)((const float*)hs)[k] : ((const double*)hs)[k];
+      emin = std::min(emin, e);
+      smin = std::min(smin, s);
+    }
+  }
+  if (!(emin > 0) || smin < 0) {
+    fail(c, FDTD_E_ARG, "materials must have eps_r > 0 and sigma >= 0");
+    fdtd_destroy(c);
+    return FDTD_E_ARG;
+  }
+  const double cmax = C0 / std::sqrt(emin);
+  const double eq1 = 1.0 / (cmax * std::sqrt(1.0 / (d.dx * d.dx) + 1.0 / (d.dy * d.dy)));
+  if (d.dt > eq1 && !(d.flags & FDTD_ALLOW_DT_ABOVE_EQ1)) {
+    fdtd_destroy(c);
+    return FDTD_E_UNSTABLE;
+  }
+
+  const size_t fbytes = (size_t)c->nrows_alloc * c->pitch * c->es;
+  for (int b = 0; b < 2; ++b)
+    for (int a = 0; a < 3; ++a)
+      if (!(c->f[b][a] = dalloc(c, fbytes))) { fdtd_destroy(c); return FDTD_E_NOMEM; }
+  for (int a = 0; a < 4; ++a)
+    if (!(c->coef[a] = dalloc(c, fbytes))) { fdtd_destroy(c); return FDTD_E_NOMEM; }
+  c->d_step = (int64_t*)dalloc(c, sizeof(int64_t));
+  c->d_done = (unsigned*)dalloc(c, sizeof(unsigned) * 4);
+  c->d_energy_ring = (double*)dalloc(c, c->cap * sizeof(double));
+  if (!c->d_step || !c->d_done || !c->d_energy_ring) { fdtd_destroy(c); return FDTD_E_NOMEM; }
+  fdtd_status st = f32 ? build_coefficients<float>(c) : build_coefficients<double>(c);
+  if (st != FDTD_OK) { fdtd_destroy(c); return st; }
+  fdtd_set_tuning(c, 0, 0);
+  if (nranks > 1) {
+    if (!g_nccl.load(c->err)) { fdtd_destroy(c); return FDTD_E_NCCL; }
+    nccl_uid id;
+    memcpy(&id, d.nccl_id, sizeof id);
+    if (g_nccl.CommInitRank(&c->comm, nranks, id, d.rank) != 0) { fdtd_destroy(c); return FDTD_E_NCCL; }
+  }
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) { fdtd_destroy(c); return FDTD_E_CUDA; }
+  *out = c;
+  return FDTD_OK;
+}
+
+fdtd_status fdtd_set_tuning(fdtd_ctx* c, int32_t rows_per_cta, int32_t warps_per_cta) {
+  if (!c) return FDTD_E_ARG;
+  if (rows_per_cta < 0 || warps_per_cta < 0 || warps_per_cta > 8) return fail(c, FDTD_E_ARG, "bad tuning");
+  c->chunk = rows_per_cta ? rows_per_cta : (c->rows >= 4096 ? 64 : 32);
+  c->warps = warps_per_cta ? warps_per_cta : 4;
+  const int per_cta = 32 * c->warps;
+  const int gx = (c->ncolv + per_cta - 1) / per_cta;
+  const int gy = (c->rows + c->chunk - 1) / c->chunk;
+  const int n = gx * gy;
+  if (n != c->n_partials) {
+    if (c->d_partials) dfree(c, c->d_partials);
+    c->d_partials = (double*)dalloc(c, (size_t)n * sizeof(double));
+    if (!c->d_partials) return fail(c, FDTD_E_NOMEM, "partials");
+    c->n_partials = n;
+  }
+  drop_graph(c);
+  return FDTD_OK;
+}
+
+fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* anchors, int64_t count,
+                         int32_t* model_id) {
+  if (!c || !m) return FDTD_E_ARG;
+  if (m->bx < 1 || m->by < 1 || m->q1 < 1 || m->q2 < 1 || !m->R11 || !m->R22 || !m->F11 || !m->K || !m->L)
+    return fail(c, FDTD_E_ARG, "bad model");
+  if (count < 0 || (count > 0 && !anchors)) return fail(c, FDTD_E_ARG, "bad anchors");
+  const int bx = m->bx, by = m->by, q1 = m->q1, q2 = m->q2, nY = 2 * bx + 2 * by, q = q1 + q2;
+  const double dt = c->d.dt, dx = c->d.dx, dy = c->d.dy;
+  using fdtd::dense::Mat;
+  namespace dense = fdtd::dense;
+  Mat R11(m->R11, m->R11 + q1 * q1), R22(m->R22, m->R22 + q2 * q2), F11(m->F11, m->F11 + q1 * q1),
+      K(m->K, m->K + q1 * q2), L(m->L, m->L + q1 * nY);
+  // eq:cond1rom: R~ = [[R11/dt, -K/2], [-K^T/2, R22/dt]] > 0 (Cholesky of the diagonally scaled matrix)
+  {
+    Mat R = dense::zeros(q, q);
+    for (int i = 0; i < q1; ++i)
+      for (int j = 0; j < q1; ++j) R[(size_t)i * q + j] = 0.5 * (R11[i * q1 + j] + R11[j * q1 + i]) / dt;
+    for (int i = 0; i < q2; ++i)
+      for (int j = 0; j < q2; ++j) R[(size_t)(q1 + i) * q + q1 + j] = 0.5 * (R22[i * q2 + j] + R22[j * q2 + i]) / dt;
+    for (int i = 0; i < q1; ++i)
+      for (int j = 0; j < q2; ++j) {
+        R[(size_t)i * q + q1 + j] = -0.5 * K[i * q2 + j];
+        R[(size_t)(q1 + j) * q + i] = -0.5 * K[i * q2 + j];
+      }
+    std::vector<double> s(q);
+    for (int i = 0; i < q; ++i) {
+      const double dg = R[(size_t)i * q + i];
+      if (!(dg > 0)) return fail(c, FDTD_E_PASSIVITY, "R~ has a non-positive diagonal entry");
+      s[i] = 1.0 / std::sqrt(dg);
+    }
+    for (int i = 0; i < q; ++i)
+      for (int j = 0; j < q; ++j) R[(size_t)i * q + j] *= s[i] * s[j];
+    if (!dense::cholesky_ok(R, q))
+      return fail(c, FDTD_E_PASSIVITY, "eq:cond1rom fails: R~ is not positive definite at dt = %g", dt);
+    // eq:cond2rom: F~ + F~^T >= 0 -> F11 + F11^T + 2 tol I must be positive definite
+    Mat FF = dense::zeros(q1, q1);
+    double fmax = 0.0;
+    for (int i = 0; i < q1; ++i)
+      for (int j = 0; j < q1; ++j) {
+        FF[i * q1 + j] = F11[i * q1 + j] + F11[j * q1 + i];
+        fmax = std::max(fmax, std::fabs(FF[i * q1 + j]));
+      }
+    if (fmax > 0) {
+      for (int i = 0; i < q1; ++i) FF[i * q1 + i] += 2e-12 * fmax;
+      if (!dense::cholesky_ok(FF, q1)) return fail(c, FDTD_E_PASSIVITY, "eq:cond2rom fails: F~ + F~^T not >= 0");
+    }
+  }
+  // placement checks
+  for (int64_t k = 0; k < count; ++k) {
+    const int64_t i0 = anchors[2 * k], j0 = anchors[2 * k + 1];
+    if (i0 < 1 || j0 < 1 || i0 + bx > c->d.nx - 1 || j0 + by > c->d.ny - 1)
+      return fail(c, FDTD_E_ARG, "instance %lld: footprint + ring leaves the grid", (long long)k);
+    if (j0 - 1 < c->d.row_begin || j0 + by > c->d.row_end - 1)
+      return fail(c, FDTD_E_ARG, "instance %lld: footprint + ring straddles this rank's rows", (long long)k);
+  }
+  {
+    // ring-vs-footprint overlap: sort all rectangles by i0 and sweep
+    struct Rc { int64_t i0, j0, bx, by; };
+    std::vector<Rc> all;
+    for (size_t r = 0; r < c->rects.size(); r += 4)
+      all.push_back({c->rects[r], c->rects[r + 1], c->rects[r + 2], c->rects[r + 3]});
+    for (int64_t k = 0; k < count; ++k) all.push_back({anchors[2 * k], anchors[2 * k + 1], bx, by});
+    std::sort(all.begin(), all.end(), [](const Rc& a, const Rc& b) { return a.i0 < b.i0; });
+    int64_t wmax = 0;
+    for (auto& r : all) wmax = std::max(wmax, r.bx);
+    for (size_t a = 0; a < all.size(); ++a)
+      for (size_t b = a + 1; b < all.size() && all[b].i0 <= all[a].i0 + all[a].bx + wmax + 2; ++b) {
+        const Rc &A = all[a], &B = all[b];
+        // expanded A = [i0-1, i0+bx] vs footprint B = [i0, i0+bx-1] (and symmetric)
+        const bool ox = A.i0 - 1 <= B.i0 + B.bx - 1 && B.i0 <= A.i0 + A.bx;
+        const bool oy = A.j0 - 1 <= B.j0 + B.by - 1 && B.j0 <= A.j0 + A.by;
+        const bool ox2 = B.i0 - 1 <= A.i0 + A.bx - 1 && A.i0 <= B.i0 + B.bx;
+        const bool oy2 = B.j0 - 1 <= A.j0 + A.by - 1 && A.j0 <= B.j0 + B.by;
+        if ((ox && oy) || (ox2 && oy2))
+          return fail(c, FDTD_E_ARG, "instances at (%lld,%lld) and (%lld,%lld) overlap (footprint + ring)",
+                      (long long)A.i0, (long long)A.j0, (long long)B.i0, (long long)B.j0);
+      }
+  }
+  // ---- shared model operators (fp64), K3:
+  // C = R11/dt + F11; Aq = C^-1 (R11/dt - F11); Kq = C^-1 K; Q1 = -dt R22^-1 K^T;
+  // Bq = C^-1 L S_c; P = L^T Bq; Lt = L^T
+  Mat Cm = dense::zeros(q1, q1), Cr = dense::zeros(q1, q1);
+  for (int i = 0; i < q1 * q1; ++i) { Cm[i] = R11[i] / dt + F11[i]; Cr[i] = R11[i] / dt - F11[i]; }
+  Mat Ci, R22i;
+  if (!dense::inverse(Cm, q1, Ci) || !dense::inverse(R22, q2, R22i))
+    return fail(c, FDTD_E_PASSIVITY, "singular R~11/dt + F~11 or R~22");
+  std::vector<double> Sc(nY);
+  for (int p = 0; p < nY; ++p) Sc[p] = p < bx ? -dx : p < 2 * bx ? dx : p < 2 * bx + by ? dy : -dy;
+  Mat Be = dense::zeros(q1, nY);
+  for (int i = 0; i < q1; ++i)
+    for (int p = 0; p < nY; ++p) Be[i * nY + p] = L[i * nY + p] * Sc[p];
+  Mat Aq = dense::matmul(Ci, Cr, q1, q1, q1);
+  Mat Kq = dense::matmul(Ci, K, q1, q1, q2);
+  Mat Kt = dense::transpose(K, q1, q2);
+  Mat Q1 = dense::matmul(R22i, Kt, q2, q2, q1);
+  for (auto& v : Q1) v *= -dt;
+  Mat Bq = dense::matmul(Ci, Be, q1, q1, nY);
+  Mat Lt = dense::transpose(L, q1, nY);
+  Mat P = dense::matmul(Lt, Bq, nY, q1, nY);
+  ModelHost mh;
+  mh.bx = bx; mh.by = by; mh.nY = nY; mh.q1 = q1; mh.q2 = q2; mh.P = P;
+  auto push = [&](const Mat& A, int rows_, int cols_) {  // row-major host -> column-major pool
+    const int64_t off = (int64_t)c->mpool.size();
+    for (int j = 0; j < cols_; ++j)
+      for (int i = 0; i < rows_; ++i) c->mpool.push_back(A[(size_t)i * cols_ + j]);
+    return off;
+  };
+  Mat R11dt(R11), R22dt(R22);
+  for (auto& v : R11dt) v /= dt;
+  for (auto& v : R22dt) v /= dt;
+  mh.dev.nY = nY; mh.dev.q1 = q1; mh.dev.q2 = q2;
+  mh.dev.off_Q1 = push(Q1, q2, q1);
+  mh.dev.off_Aq = push(Aq, q1, q1);
+  mh.dev.off_Kq = push(Kq, q1, q2);
+  mh.dev.off_Lt = push(Lt, nY, q1);
+  mh.dev.off_Bq = push(Bq, q1, nY);
+  mh.dev.off_R11 = push(R11dt, q1, q1);
+  mh.dev.off_R22 = push(R22dt, q2, q2);
+  mh.dev.off_K = push(K, q1, q2);
+  const int mid = (int)c->models.size();
+  c->models.push_back(mh);
+  c->nvec = std::max(c->nvec, std::max(nY, std::max(q1, q2)));
+
+  // ---- per instance: outside-cell materials -> c_y, a_y, Schur inverse S_k
+  std::vector<int64_t> cells;
+  auto outside = [&](int64_t i0, int64_t j0, int p, int64_t& oi, int64_t& oj) {
+    if (p < bx) { oi = i0 + p; oj = j0 - 1; }
+    else if (p < 2 * bx) { oi = i0 + p - bx; oj = j0 + by; }
+    else if (p < 2 * bx + by) { oi = i0 - 1; oj = j0 + p - 2 * bx; }
+    else { oi = i0 + bx; oj = j0 + p - 2 * bx - by; }
+  };
+  for (int64_t k = 0; k < count; ++k)
+    for (int p = 0; p < nY; ++p) {
+      int64_t oi, oj;
+      outside(anchors[2 * k], anchors[2 * k + 1], p, oi, oj);
+      cells.push_back(oj * c->d.nx + oi);
+    }
+  std::vector<double> oe, os;
+  fdtd_status st = gather_materials(c, cells, oe, os);
+  if (st != FDTD_OK) return st;
+  const int64_t P_ = c->pitch;
+  for (int64_t k = 0; k < count; ++k) {
+    const int64_t i0 = anchors[2 * k], j0 = anchors[2 * k + 1];
+    c->inst_model.push_back(mid);
+    c->rects.insert(c->rects.end(), {(int32_t)i0, (int32_t)j0, bx, by});
+    c->port_off.push_back((int64_t)c->port_edge.size());
+    c->state_off.push_back(c->state_len);
+    c->state_len += q;
+    c->Sk_off.push_back((int64_t)c->Sk.size());
+    Mat A = P;
+    for (int p = 0; p < nY; ++p) {
+      const bool isey = p >= 2 * bx;
+      const double Dl = isey ? dy : dx, Dlp = isey ? dx / 2 : dy / 2;
+      const double G = (p < bx) ? -1.0 : (p < 2 * bx) ? 1.0 : (p < 2 * bx + by) ? 1.0 : -1.0;
+      const double eps = EPS0 * oe[k * nY + p], sig = os[k * nY + p];
+      const double cy = Dl * Dlp * (eps / dt + sig / 2), ay = Dl * Dlp * (eps / dt - sig / 2);
+      A[(size_t)p * nY + p] += Dl * G / cy;
+      c->cya.push_back(ay / cy);
+      c->cyg.push_back(Dl * G / cy);
+      c->ehalf.push_back(Dl * Dlp * eps / dt);
+      int64_t oi, oj;
+      outside(i0, j0, p, oi, oj);
+      c->port_h.push_back(lrow(c, oj) * P_ + oi);
+      int64_t e;
+      if (p < bx) e = lrow(c, j0) * P_ + i0 + p;
+      else if (p < 2 * bx) e = lrow(c, j0 + by) * P_ + i0 + p - bx;
+      else if (p < 2 * bx + by) e = (int64_t(1) << 62) | (lrow(c, j0 + p - 2 * bx) * P_ + i0);
+      else e = (int64_t(1) << 62) | (lrow(c, j0 + p - 2 * bx - by) * P_ + i0 + bx);
+      c->port_edge.push_back(e);
+    }
+    Mat S;
+    if (!dense::inverse(A, nY, S)) return fail(c, FDTD_E_ARG, "singular interface Schur matrix");
+    for (int j = 0; j < nY; ++j)  // column-major
+      for (int i = 0; i < nY; ++i) c->Sk.push_back(S[(size_t)i * nY + j]);
+    if (c->ring_off.empty()) c->ring_off.push_back(0);
+    for (int64_t jj = j0; jj < j0 + by; ++jj)
+      for (int64_t ii = i0; ii < i0 + bx; ++ii)
+        if (jj == j0 || jj == j0 + by - 1 || ii == i0 || ii == i0 + bx - 1)
+          c->ring_idx.push_back(lrow(c, jj) * P_ + ii);
+    c->ring_off.push_back((int64_t)c->ring_idx.size());
+  }
+  // masks (coefficients + zeroed holes/interfaces in both buffers)
+  std::vector<int32_t> nr(c->rects.end() - 4 * count, c->rects.end());
+  int32_t* drect = nullptr;
+  if ((st = upload(c, &drect, nr)) != FDTD_OK) return st;
+  if (c->prec == 64) {
+    double* fl[6] = {(double*)c->f[0][0], (double*)c->f[0][1], (double*)c->f[0][2],
+                     (double*)c->f[1][0], (double*)c->f[1][1], (double*)c->f[1][2]};
+    fdtd::launch_mask<double>((double*)c->coef[0], (double*)c->coef[1], (double*)c->coef[2], (double*)c->coef[3],
+                              fl, P_, drect, count, c->d.row_begin, true, true, c->stream);
+  } else {
+    float* fl[6] = {(float*)c->f[0][0], (float*)c->f[0][1], (float*)c->f[0][2],
+                    (float*)c->f[1][0], (float*)c->f[1][1], (float*)c->f[1][2]};
+    fdtd::launch_mask<float>((float*)c->coef[0], (float*)c->coef[1], (float*)c->coef[2], (float*)c->coef[3], fl,
+                             P_, drect, count, c->d.row_begin, true, true, c->stream);
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->stream));
+  dfree(c, drect);
+  if ((st = upload_roms(c)) != FDTD_OK) return st;
+  CK(cudaStreamSynchronize(c->stream));
+  drop_graph(c);
+  if (model_id) *model_id = mid;
+  return FDTD_OK;
+}
+
+fdtd_status fdtd_set_source(fdtd_ctx* c, int64_t i, int64_t j, const double* samples, int64_t n, int64_t step0) {
+  if (!c) return FDTD_E_ARG;
+  if (i < 0 || i >= c->d.nx || j < 0 || j >= c->d.ny || n < 0 || (n > 0 && !samples))
+    return fail(c, FDTD_E_ARG, "bad source");
+  if (!c->d_src || n > c->src_cap) {
+    if (c->d_src) dfree(c, c->d_src);
+    c->src_cap = std::max<int64_t>(n, 1);
+    c->d_src = (double*)dalloc(c, c->src_cap * sizeof(double));
+    if (!c->d_src) return fail(c, FDTD_E_NOMEM, "source");
+  }
+  if (n) CK(cudaMemcpyAsync(c->d_src, samples, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  c->src_n = n;
+  c->src_t0 = step0;
+  c->src_i = i;
+  c->src_j = j;
+  drop_graph(c);
+  return FDTD_OK;
+}
+
+fdtd_status fdtd_set_probes(fdtd_ctx* c, const int64_t* ij, int32_t n) {
+  if (!c || n < 0 || (n > 0 && !ij)) return FDTD_E_ARG;
+  std::vector<int64_t> idx(std::max(n, 1), 0);
+  // probes outside this rank read a dedicated always-zero slot (ghost row above, column 0 is never
+  // written for Hz); they contribute 0 to the cross-rank sum
+  const int64_t zero_slot = (int64_t)(c->rows + 1) * c->pitch + c->pitch - 1;
+  for (int32_t k = 0; k < n; ++k) {
+    const int64_t i = ij[2 * k], j = ij[2 * k + 1];
+    if (i < 0 || i >= c->d.nx || j < 0 || j >= c->d.ny) return fail(c, FDTD_E_ARG, "probe %d outside grid", k);
+    idx[k] = (j >= c->d.row_begin && j < c->d.row_end) ? lrow(c, j) * c->pitch + i : zero_slot;
+  }
+  fdtd_status st = upload(c, &c->d_probe_idx, idx);
+  if (st != FDTD_OK) return st;
+  if (c->d_probe_ring) dfree(c, c->d_probe_ring);
+  c->d_probe_ring = dalloc(c, (size_t)std::max(n, 1) * c->cap * c->es);
+  if (!c->d_probe_ring) return fail(c, FDTD_E_NOMEM, "probe ring");
+  c->n_probe = n;
+  c->rd_probe = c->steps;
+  drop_graph(c);
+  return FDTD_OK;
+}
+
+fdtd_status fdtd_record_energy(fdtd_ctx* c, int32_t on) {
+  if (!c) return FDTD_E_ARG;
+  if ((on != 0) != c->energy_on) {
+    c->energy_on = on != 0;
+    c->rd_energy = c->steps;
+    drop_graph(c);
+  }
+  return FDTD_OK;
+}
+
+fdtd_status fdtd_step(fdtd_ctx* c, int64_t nsteps) {
+  if (!c || nsteps < 0) return FDTD_E_ARG;
+  int64_t oldest = c->steps + nsteps;
+  if (c->n_probe > 0) oldest = std::min(oldest, c->rd_probe);
+  if (c->energy_on) oldest = std::min(oldest, c->rd_energy);
+  if (c->steps + nsteps - oldest > c->cap)
+    return fail(c, FDTD_E_STATE, "unread records would exceed record_capacity (%lld)", (long long)c->cap);
+  const bool use_graph = !(c->d.flags & FDTD_NO_GRAPH) && c->d.nranks == 1 && nsteps >= 2;
+  fdtd_status st;
+  int64_t left = nsteps;
+  if (use_graph) {
+    if (c->steps & 1) {  // realign to even parity
+      if ((st = enqueue_step(c, 1, c->stream)) != FDTD_OK) return st;
+      c->steps++;
+      left--;
+    }
+    if (left >= 2 && (c->graph_dirty || !c->gexec))
+      if ((st = build_graph(c)) != FDTD_OK) return st;
+    while (left >= 2) {
+      CK(cudaGraphLaunch(c->gexec, c->stream));
+      c->launches += 4;
+      c->steps += 2;
+      left -= 2;
+    }
+  }
+  while (left > 0) {
+    if ((st = enqueue_step(c, (int)(c->steps & 1), c->stream)) != FDTD_OK) return st;
+    c->steps++;
+    left--;
+  }
+  CK(cudaGetLastError());
+  return FDTD_OK;
+}
+
+static fdtd_status read_ring(fdtd_ctx* c, const void* ring, int rows_, size_t es, int64_t from, int64_t to,
+                             int dtype, void* host, int64_t ldh) {
+  // copy ring entries for steps [from, to) of `rows_` rows (ring row stride cap) into host [rows_][ldh]
+  const int64_t n = to - from;
+  if (n <= 0 || rows_ <= 0) return FDTD_OK;
+  void* tmp = dalloc(c, (size_t)rows_ * n * es);
+  if (!tmp) return fail(c, FDTD_E_NOMEM, "record staging");
+  int64_t done = 0;
+  while (done < n) {
+    const int64_t s = (from + done) % c->cap;
+    const int64_t len = std::min(n - done, c->cap - s);
+    CK(cudaMemcpy2DAsync((char*)tmp + done * es, n * es, (const char*)ring + s * es, c->cap * es, len * es, rows_,
+                         cudaMemcpyDeviceToDevice, c->stream));
+    done += len;
+  }
+  if (c->d.nranks > 1) NK(g_nccl.AllReduce(tmp, tmp, (size_t)rows_ * n, dtype, NCCL_SUM, c->comm, c->stream));
+  CK(cudaMemcpy2DAsync(host, ldh * es, tmp, n * es, n * es, rows_, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  dfree(c, tmp);
+  return FDTD_OK;
+}
+
+fdtd_status fdtd_probe(fdtd_ctx* c, double* out, int64_t cap_steps, int64_t* n_steps) {
+  if (!c || !n_steps) return FDTD_E_ARG;
+  fdtd_status st = check_async(c);
+  if (st != FDTD_OK) return st;
+  const int64_t n = c->steps - c->rd_probe;
+  if (n > cap_steps) return fail(c, FDTD_E_ARG, "output holds %lld steps, %lld pending", (long long)cap_steps, (long long)n);
+  *n_steps = n;
+  if (c->n_probe == 0 || n == 0) { c->rd_probe = c->steps; return FDTD_OK; }
+  if (!out) return FDTD_E_ARG;
+  std::vector<char> h((size_t)c->n_probe * cap_steps * c->es);
+  st = read_ring(c, c->d_probe_ring, c->n_probe, c->es, c->rd_probe, c->steps, c->prec == 64 ? NCCL_F64 : NCCL_F32,
+                 h.data(), cap_steps);
+  if (st != FDTD_OK) return st;
+  for (int64_t p = 0; p < c->n_probe; ++p)
+    for (int64_t k = 0; k < n; ++k)
+      out[p * cap_steps + k] = c->prec == 64 ? ((double*)h.data())[p * cap_steps + k]
+                                             : (double)((float*)h.data())[p * cap_steps + k];
+  c->rd_probe = c->steps;
+  return FDTD_OK;
+}
+
+fdtd_status fdtd_energy(fdtd_ctx* c, double* out, int64_t cap, int64_t* n_out) {
+  if (!c || !n_out) return FDTD_E_ARG;
+  fdtd_status st = check_async(c);
+  if (st != FDTD_OK) return st;
+  const int64_t n = c->energy_on ? c->steps - c->rd_energy : 0;
+  if (n > cap) return fail(c, FDTD_E_ARG, "output holds %lld steps, %lld pending", (long long)cap, (long long)n);
+  *n_out = n;
+  if (n == 0) return FDTD_OK;
+  if (!out) return FDTD_E_ARG;
+  st = read_ring(c, c->d_energy_ring, 1, 8, c->rd_energy, c->steps, NCCL_F64, out, cap);
+  if (st != FDTD_OK) return st;
+  c->rd_energy = c->steps;
+  return FDTD_OK;
+}
+
+static fdtd_status window_io(fdtd_ctx* c, int64_t i0, int64_t j0, int64_t w, int64_t h, double* Ex, double* Ey,
+                             double* Hz, bool set) {
+  if (!c || w < 0 || h < 0 || i0 < 0 || j0 < 0 || i0 + w > c->d.nx || j0 + h > c->d.ny)
+    return fail(c, FDTD_E_ARG, "bad window");
+  fdtd_status st = check_async(c);
+  if (st != FDTD_OK) return st;
+  const int q = (int)(c->steps & 1);
+  const int64_t rb = c->d.row_begin, re = c->d.row_end;
+  const size_t es = c->es;
+  // arrays: (ptr, ncols, global row range [g0, g1), device array, row range owned, col limit stored)
+  struct A { double* p; int64_t cols; int64_t g0, g1; int a; };
+  A arr[3] = {{Ex, w, j0, j0 + h + 1, 0}, {Ey, w + 1, j0, j0 + h, 1}, {Hz, w, j0, j0 + h, 2}};
+  std::vector<char> stg;
+  for (auto& x : arr) {
+    if (!x.p) continue;
+    const int64_t a0 = std::max(x.g0, rb), a1 = std::min(x.g1, re);
+    if (a1 <= a0) continue;
+    const int64_t nrow = a1 - a0;
+    const int64_t cstore = std::min<int64_t>(x.cols, c->pitch - i0);  // columns stored on device
+    if (cstore <= 0) continue;
+    stg.assign((size_t)nrow * cstore * es, 0);
+    char* dev = (char*)c->f[q][x.a] + ((size_t)lrow(c, a0) * c->pitch + i0) * es;
+    if (!set) {
+      CK(cudaMemcpy2DAsync(stg.data(), cstore * es, dev, c->pitch * es, cstore * es, nrow, cudaMemcpyDeviceToHost,
+                           c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      for (int64_t r = 0; r < nrow; ++r)
+        for (int64_t k = 0; k < x.cols; ++k) {
+          double v = 0.0;
+          if (k < cstore) v = c->prec == 64 ? ((double*)stg.data())[r * cstore + k] : ((float*)stg.data())[r * cstore + k];
+          x.p[(a0 - x.g0 + r) * x.cols + k] = v;
+        }
+    } else {
+      for (int64_t r = 0; r < nrow; ++r)
+        for (int64_t k = 0; k < cstore; ++k) {
+          const int64_t g = a0 + r, col = i0 + k;
+          double v = x.p[(a0 - x.g0 + r) * x.cols + k];
+          if (x.a == 0 && (g == 0 || g == c->d.ny)) v = 0.0;      // PEC Ex rows
+          if (x.a == 1 && (col == 0 || col >= c->d.nx)) v = 0.0;  // PEC Ey columns
+          if (x.a != 1 && col >= c->d.nx) v = 0.0;
+          if (c->prec == 64) ((double*)stg.data())[r * cstore + k] = v;
+          else ((float*)stg.data())[r * cstore + k] = (float)v;
+        }
+      CK(cudaMemcpy2DAsync(dev, c->pitch * es, stg.data(), cstore * es, cstore * es, nrow, cudaMemcpyHostToDevice,
+                           c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
+  }
+  if (set && !c->inst_model.empty()) {  // keep ROM holes at zero (interface edges keep the given y)
+    int32_t* drect = nullptr;
+    if ((st = upload(c, &drect, c->rects)) != FDTD_OK) return st;
+    const int64_t nr = (int64_t)c->rects.size() / 4;
+    if (c->prec == 64) {
+      double* fl[6] = {(double*)c->f[q][0], (double*)c->f[q][1], (double*)c->f[q][2],
+                       (double*)c->f[q][0], (double*)c->f[q][1], (double*)c->f[q][2]};
+      fdtd::launch_mask<double>(nullptr, nullptr, nullptr, nullptr, fl, c->pitch, drect, nr, rb, false, false, c->stream);
+    } else {
+      float* fl[6] = {(float*)c->f[q][0], (float*)c->f[q][1], (float*)c->f[q][2],
+                      (float*)c->f[q][0], (float*)c->f[q][1], (float*)c->f[q][2]};
+      fdtd::launch_mask<float>(nullptr, nullptr, nullptr, nullptr, fl, c->pitch, drect, nr, rb, false, false, c->stream);
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, drect);
+  }
+  return FDTD_OK;
+}
+
+fdtd_status fdtd_get_window(fdtd_ctx* c, int64_t i0, int64_t j0, int64_t w, int64_t h, double* Ex, double* Ey,
+                            double* Hz) {
+  return window_io(c, i0, j0, w, h, Ex, Ey, Hz, false);
+}
+
+fdtd_status fdtd_set_window(fdtd_ctx* c, int64_t i0, int64_t j0, int64_t w, int64_t h, const double* Ex,
+                            const double* Ey, const double* Hz) {
+  return window_io(c, i0, j0, w, h, const_cast<double*>(Ex), const_cast<double*>(Ey), const_cast<double*>(Hz), true);
+}
+
+fdtd_status fdtd_get_rom_state(fdtd_ctx* c, double* out, int64_t cap, int64_t* n) {
+  if (!c || !n) return FDTD_E_ARG;
+  fdtd_status st = check_async(c);
+  if (st != FDTD_OK) return st;
+  *n = c->state_len;
+  if (c->state_len == 0) return FDTD_OK;
+  if (cap < c->state_len || !out) return fail(c, FDTD_E_ARG, "rom state buffer too small");
+  std::vector<char> h(c->state_len * c->es);
+  CK(cudaMemcpy(h.data(), c->d_state, h.size(), cudaMemcpyDeviceToHost));
+  for (int64_t k = 0; k < c->state_len; ++k)
+    out[k] = c->prec == 64 ? ((double*)h.data())[k] : (double)((float*)h.data())[k];
+  return FDTD_OK;
+}
+
+fdtd_status fdtd_set_rom_state(fdtd_ctx* c, const double* in, int64_t n) {
+  if (!c || n != c->state_len || (n > 0 && !in)) return fail(c, FDTD_E_ARG, "rom state length mismatch");
+  fdtd_status st = check_async(c);
+  if (st != FDTD_OK) return st;
+  if (n == 0) return FDTD_OK;
+  std::vector<double> v(in, in + n);
+  if (c->prec == 64) {
+    CK(cudaMemcpy(c->d_state, v.data(), n * 8, cudaMemcpyHostToDevice));
+  } else {
+    std::vector<float> f(v.begin(), v.end());
+    CK(cudaMemcpy(c->d_state, f.data(), n * 4, cudaMemcpyHostToDevice));
+  }
+  return FDTD_OK;
+}
+
+fdtd_status fdtd_sync(fdtd_ctx* c) {
+  if (!c) return FDTD_E_ARG;
+  return check_async(c);
+}
+
+fdtd_status fdtd_get_info(const fdtd_ctx* c, fdtd_info* o) {
+  if (!c || !o) return FDTD_E_ARG;
+  o->steps_taken = c->steps;
+  o->n_instances = (int64_t)c->inst_model.size();
+  o->kernel_launches = c->launches;
+  o->pitch = c->pitch;
+  o->sweep_ctas = c->n_partials;
+  o->graphs = !(c->d.flags & FDTD_NO_GRAPH) && c->d.nranks == 1;
+  o->precision = c->prec;
+  o->bytes_per_cell_step = 10.0 * (double)c->es;
+  o->sweep_stream = (void*)c->stream;
+  return FDTD_OK;
+}
+
+fdtd_status fdtd_nccl_unique_id(void* out128) {
+  std::string err;
+  if (!out128) return FDTD_E_ARG;
+  if (!g_nccl.load(err)) return FDTD_E_NCCL;
+  nccl_uid id;
+  if (g_nccl.GetUniqueId(&id) != 0) return FDTD_E_NCCL;
+  memcpy(out128, &id, sizeof id);
+  return FDTD_OK;
+}
+
+void fdtd_destroy(fdtd_ctx* c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  drop_graph(c);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  std::vector<void*> all = c->owned;
+  for (void* p : all) dfree(c, p);
+  delete c;
+}
+
+}  // extern "C"

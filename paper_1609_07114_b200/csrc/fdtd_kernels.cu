@@ -1,0 +1,487 @@
+// CUDA kernels of the hot path (sm_100a).  See DESIGN.md for the derivations.
+//
+//  K1 sweep_kernel : one pass over the grid per time step.  For every owned cell row it
+//                    computes Hz^{n+1/2} (eq:updateH), adds the soft
+//                    source, then the E^{n+1} of that row's x- and y-directed edges
+//                    (eq:updateEx L209-214 and its Ey analogue L223) from the new Hz of
+//                    this row and the row below (kept in registers).  16-byte vector
+//                    loads, one warp per 32x16-byte column strip, rows walked upward by
+//                    each CTA over a chunk; ping-pong buffers so no CTA ever reads a value
+//                    another CTA writes in the same launch.  Edge masks (PEC, ROM holes,
+//                    ROM interfaces) are encoded in the coefficients (ca = 1, cb = 0).
+//  K3 post_kernel  : per ROM instance (one CTA each) the factored eq:connExplicit update
+//                    (gather h, y; reduced matvecs; Schur solve; scatter y^{n+1});
+//                    one CTA records the probes; the last CTA to finish reduces the
+//                    energy partials in a fixed order and advances the step counter.
+#include "fdtd_kernels.cuh"
+
+#include <cstdio>
+
+namespace fdtd {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr double MU0 = 4.0e-7 * 3.14159265358979323846;
+constexpr double C0 = 299792458.0;
+constexpr double EPS0 = 1.0 / (MU0 * C0 * C0);
+constexpr int64_t IDX_MASK = (int64_t(1) << 62) - 1;
+
+template <typename T> struct VT;
+template <> struct VT<float> { static constexpr int N = 4; };
+template <> struct VT<double> { static constexpr int N = 2; };
+
+__device__ __forceinline__ void ldv(const float* p, float (&v)[4]) {
+  const float4 x = __ldg(reinterpret_cast<const float4*>(p));
+  v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+}
+__device__ __forceinline__ void ldv(const double* p, double (&v)[2]) {
+  const double2 x = __ldg(reinterpret_cast<const double2*>(p));
+  v[0] = x.x; v[1] = x.y;
+}
+__device__ __forceinline__ void stv(float* p, const float (&v)[4]) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void stv(double* p, const double (&v)[2]) {
+  *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+}
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
+// eq:updateH divided by dx dy mu / dt:  Hz' = Hz + chy (Ex_{j+1} - Ex_j) - chx (Ey_{i+1} - Ey_i).
+// Explicit fused operations pin the rounding, so the redundant recomputations at warp and
+// chunk edges are bit-identical to the owner's value (needed for 1-GPU == N-GPU fields).
+template <typename T>
+__device__ __forceinline__ T hupd(T hz, T exn, T exc, T eyr, T eyl, T chy, T chx) {
+  return fma_rn(-chx, eyr - eyl, fma_rn(chy, exn - exc, hz));
+}
+
+template <typename T, bool ENERGY>
+__global__ void __launch_bounds__(256) sweep_kernel(const SweepParams<T> p) {
+  constexpr int V = VT<T>::N;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int wpc = blockDim.x >> 5;
+  const int colv = (blockIdx.x * wpc + warp) * 32 + lane;
+  const bool act = colv < p.ncolv;
+  const int64_t c = (int64_t)colv * V;
+  const int r0 = 1 + blockIdx.y * p.chunk;
+  const int r1 = min(r0 + p.chunk, p.rows + 1);
+  const int64_t P = p.pitch;
+
+  T src = T(0);
+  if (p.src_row >= 0) {
+    const int64_t k = *p.step - p.src_t0;
+    if (k >= 0 && k < p.src_n) src = (T)p.src_samples[k];
+  }
+
+  T exc[V], hzp[V], exn[V], eyv[V], hzv[V];
+  T excl = T(0);
+  // ---- prologue: Hz^{n+1/2} of row r0-1 (recomputed; ghost row when r0 == 1)
+  {
+    const int64_t rj = (int64_t)(r0 - 1) * P;
+    T exl[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) exl[k] = exn[k] = eyv[k] = hzv[k] = T(0);
+    if (act) {
+      ldv(p.ex0 + rj + c, exl);
+      ldv(p.ex0 + rj + P + c, exn);
+      ldv(p.ey0 + rj + c, eyv);
+      ldv(p.hz0 + rj + c, hzv);
+    }
+    T eyr = __shfl_down_sync(FULL, eyv[0], 1);
+    if (lane == 31) eyr = (act && colv + 1 < p.ncolv) ? __ldg(p.ey0 + rj + c + V) : T(0);
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      hzp[k] = hupd(hzv[k], exn[k], exl[k], k + 1 < V ? eyv[k + 1] : eyr, eyv[k], p.chy, p.chx);
+    if (r0 - 1 == p.src_row) {
+#pragma unroll
+      for (int k = 0; k < V; ++k)
+        if (c + k == p.src_col) hzp[k] += src;
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k) exc[k] = exn[k];
+    if (lane == 0 && act && c > 0) excl = __ldg(p.ex0 + rj + P + c - 1);
+  }
+
+  double eacc = 0.0;
+  for (int j = r0; j < r1; ++j) {
+    const int64_t rj = (int64_t)j * P;
+    const int64_t rn = rj + P;
+    T ca_x[V], cb_x[V], ca_y[V], cb_y[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) exn[k] = eyv[k] = hzv[k] = ca_x[k] = cb_x[k] = ca_y[k] = cb_y[k] = T(0);
+    if (act) {
+      ldv(p.ex0 + rn + c, exn);
+      ldv(p.ey0 + rj + c, eyv);
+      ldv(p.hz0 + rj + c, hzv);
+      ldv(p.cax + rj + c, ca_x);
+      ldv(p.cbx + rj + c, cb_x);
+      ldv(p.cay + rj + c, ca_y);
+      ldv(p.cby + rj + c, cb_y);
+    }
+    T lhz = T(0), lexn = T(0), ley = T(0);
+    if (lane == 0 && act && c > 0) {
+      lhz = __ldg(p.hz0 + rj + c - 1);
+      lexn = __ldg(p.ex0 + rn + c - 1);
+      ley = __ldg(p.ey0 + rj + c - 1);
+    }
+    T eyr = __shfl_down_sync(FULL, eyv[0], 1);
+    if (lane == 31) eyr = (act && colv + 1 < p.ncolv) ? __ldg(p.ey0 + rj + c + V) : T(0);
+    T hzn[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      hzn[k] = hupd(hzv[k], exn[k], exc[k], k + 1 < V ? eyv[k + 1] : eyr, eyv[k], p.chy, p.chx);
+    if (j == p.src_row) {  // S2: soft source after the H half-step
+#pragma unroll
+      for (int k = 0; k < V; ++k)
+        if (c + k == p.src_col) hzn[k] += src;
+    }
+    T hl = __shfl_up_sync(FULL, hzn[V - 1], 1);
+    if (lane == 0) {
+      if (c > 0) {
+        hl = hupd(lhz, lexn, excl, eyv[0], ley, p.chy, p.chx);
+        if (j == p.src_row && c - 1 == p.src_col) hl += src;
+      } else {
+        hl = T(0);  // Ey column 0 is the PEC wall (cb = 0)
+      }
+      excl = lexn;
+    }
+    T exo[V], eyo[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      exo[k] = fma_rn(cb_x[k], hzn[k] - hzp[k], mul_rn(ca_x[k], exc[k]));
+      eyo[k] = fma_rn(-cb_y[k], hzn[k] - (k ? hzn[k - 1] : hl), mul_rn(ca_y[k], eyv[k]));
+    }
+    if (act) {
+      stv(p.hz1 + rj + c, hzn);
+      stv(p.ex1 + rj + c, exo);
+      stv(p.ey1 + rj + c, eyo);
+    }
+    if (ENERGY) {  // S3: (1/dt)[C E^2 + mu A H^{n-1/2} H^{n+1/2}], C/dt = l (1 + ca) / (2 cb)
+      T e = T(0);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const T wx = cb_x[k] > T(0) ? p.wex * (T(1) + ca_x[k]) / cb_x[k] : T(0);
+        const T wy = cb_y[k] > T(0) ? p.wey * (T(1) + ca_y[k]) / cb_y[k] : T(0);
+        e += wx * exc[k] * exc[k] + wy * eyv[k] * eyv[k] + p.wh * hzv[k] * hzn[k];
+      }
+      eacc += (double)e;
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      exc[k] = exn[k];
+      hzp[k] = hzn[k];
+    }
+  }
+  if (ENERGY) {
+    __shared__ double red[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) eacc += __shfl_down_sync(FULL, eacc, o);
+    if (lane == 0) red[warp] = eacc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < wpc; ++w) s += red[w];
+      p.partials[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+    }
+  }
+}
+
+// block-wide fixed-order sum of doubles (deterministic)
+__device__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FULL, v, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+  return s;  // valid in thread 0
+}
+
+template <typename T, bool ENERGY>
+__device__ void rom_instance(const PostParams<T>& p, int b, T* sv, double* red) {
+  const RomModelDev m = p.models[p.inst_model[b]];
+  const int nY = m.nY, q1 = m.q1, q2 = m.q2;
+  const int NV = p.nthreads_vec;
+  T* sy = sv;
+  T* sh = sy + NV;
+  T* sE = sh + NV;
+  T* sH = sE + NV;
+  T* sEs = sH + NV;
+  T* st = sEs + NV;
+  T* sU = st + NV;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t po = p.port_off[b];
+  T* xs = p.state + p.state_off[b];
+  const T* Q1 = p.mpool + m.off_Q1;
+  const T* Aq = p.mpool + m.off_Aq;
+  const T* Kq = p.mpool + m.off_Kq;
+  const T* Lt = p.mpool + m.off_Lt;
+  const T* Bq = p.mpool + m.off_Bq;
+  // S4: gather y^n (interface edges, copied old->new by the sweep) and h = Hz^{n+1/2} outside
+  for (int i = tid; i < nY; i += nt) {
+    const int64_t e = p.port_edge[po + i];
+    sy[i] = (e >> 62) ? p.ey1[e & IDX_MASK] : p.ex1[e & IDX_MASK];
+    sh[i] = p.hz1[p.port_h[po + i]];
+  }
+  for (int i = tid; i < q1; i += nt) sE[i] = xs[i];
+  for (int i = tid; i < q2; i += nt) sH[i] = xs[q1 + i];
+  __syncthreads();
+  if (ENERGY) {  // coarse interface half cells + x~^T R~ x~ (eq:R with R~11, R~22, K~)
+    const T* R11 = p.mpool + m.off_R11;
+    const T* R22 = p.mpool + m.off_R22;
+    const T* Km = p.mpool + m.off_K;
+    double w = 0.0;
+    for (int i = tid; i < nY; i += nt) w += p.ehalf[po + i] * (double)sy[i] * (double)sy[i];
+    for (int i = tid; i < q1; i += nt) {
+      double a = 0.0, k = 0.0;
+      for (int c = 0; c < q1; ++c) a += (double)R11[(int64_t)c * q1 + i] * (double)sE[c];
+      for (int c = 0; c < q2; ++c) k += (double)Km[(int64_t)c * q1 + i] * (double)sH[c];
+      w += (double)sE[i] * (a - k);
+    }
+    for (int i = tid; i < q2; i += nt) {
+      double a = 0.0;
+      for (int c = 0; c < q2; ++c) a += (double)R22[(int64_t)c * q2 + i] * (double)sH[c];
+      w += (double)sH[i] * a;
+    }
+    const double s = block_sum(w, red);
+    if (tid == 0) p.rom_partials[b] = s;
+  }
+  // S5 (factored eq:connExplicit, K3):
+  // (1) H~ <- H~ + Q1 E~   (each thread owns its sH[i]; only sE is shared)
+  for (int i = tid; i < q2; i += nt) {
+    T a = sH[i];
+    for (int c = 0; c < q1; ++c) a = fma_rn(Q1[(int64_t)c * q2 + i], sE[c], a);
+    sH[i] = a;
+  }
+  __syncthreads();
+  // (2) E* = Aq E~ + Kq H~
+  for (int i = tid; i < q1; i += nt) {
+    T a = T(0);
+    for (int c = 0; c < q1; ++c) a = fma_rn(Aq[(int64_t)c * q1 + i], sE[c], a);
+    for (int c = 0; c < q2; ++c) a = fma_rn(Kq[(int64_t)c * q1 + i], sH[c], a);
+    sEs[i] = a;
+  }
+  __syncthreads();
+  // (3) t = (a_y/c_y) y + (D_l G/c_y) h - L~^T E*
+  for (int i = tid; i < nY; i += nt) {
+    T a = fma_rn(p.cyg[po + i], sh[i], mul_rn(p.cya[po + i], sy[i]));
+    for (int c = 0; c < q1; ++c) a = fma_rn(-Lt[(int64_t)c * nY + i], sEs[c], a);
+    st[i] = a;
+  }
+  __syncthreads();
+  // (4) U = S_k t
+  const T* S = p.Sk + p.Sk_off[b];
+  for (int i = tid; i < nY; i += nt) {
+    T a = T(0);
+    for (int c = 0; c < nY; ++c) a = fma_rn(S[(int64_t)c * nY + i], st[c], a);
+    sU[i] = a;
+  }
+  __syncthreads();
+  // (5) E~ = E* + Bq U
+  for (int i = tid; i < q1; i += nt) {
+    T a = sEs[i];
+    for (int c = 0; c < nY; ++c) a = fma_rn(Bq[(int64_t)c * q1 + i], sU[c], a);
+    sE[i] = a;
+  }
+  __syncthreads();
+  // (6) y^{n+1} = L~^T E~ ; S6: scatter into the interface edges
+  for (int i = tid; i < nY; i += nt) {
+    T a = T(0);
+    for (int c = 0; c < q1; ++c) a = fma_rn(Lt[(int64_t)c * nY + i], sE[c], a);
+    const int64_t e = p.port_edge[po + i];
+    if (e >> 62) p.ey1[e & IDX_MASK] = a;
+    else p.ex1[e & IDX_MASK] = a;
+  }
+  for (int i = tid; i < q1; i += nt) xs[i] = sE[i];
+  for (int i = tid; i < q2; i += nt) xs[q1 + i] = sH[i];
+  // hole-ring Hz cells took garbage from the interface edges in the sweep; reset them
+  for (int64_t k = p.ring_off[b] + tid; k < p.ring_off[b + 1]; k += nt) p.hz1[p.ring_idx[k]] = T(0);
+}
+
+template <typename T, bool ENERGY>
+__global__ void __launch_bounds__(128) post_kernel(const PostParams<T> p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[32];
+  __shared__ bool last;
+  T* sv = reinterpret_cast<T*>(smem_raw);
+  const int b = blockIdx.x;
+  const int64_t step = *p.step;
+  if (b < p.n_inst) {
+    rom_instance<T, ENERGY>(p, b, sv, red);
+  } else {
+    for (int k = threadIdx.x; k < p.n_probe; k += blockDim.x)
+      p.probe_ring[(int64_t)k * p.cap + step % p.cap] = p.hz1[p.probe_idx[k]];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(p.done, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (ENERGY) {
+    double s = 0.0;
+    for (int k = threadIdx.x; k < p.n_sweep_partials; k += blockDim.x) s += __ldcg(p.sweep_partials + k);
+    double r = 0.0;
+    for (int k = threadIdx.x; k < p.n_inst; k += blockDim.x) r += __ldcg(p.rom_partials + k);
+    const double tot = block_sum(s + r, red);
+    if (threadIdx.x == 0) p.energy_ring[step % p.cap] = tot;
+  }
+  if (threadIdx.x == 0) {
+    *p.done = 0u;
+    *p.step = step + 1;
+  }
+}
+
+// ---------------------------------------------------------------- setup kernels
+template <typename T, typename M>
+__global__ void coef_kernel(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t nx, int64_t ny,
+                            int64_t row_begin, int rows, int64_t pitch, double dx, double dy, double dt,
+                            T* cax, T* cbx, T* cay, T* cby) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int jl = blockIdx.y + 1;  // local row 1..rows
+  if (i >= pitch || jl > rows) return;
+  const int64_t g = row_begin + jl - 1;  // global cell row == global Ex edge row
+  const int64_t o = (int64_t)jl * pitch + i;
+  auto mat = [&](const M* a, int64_t gi, int64_t gj) { return (double)a[(gj - mat_row0) * nx + gi]; };
+  // Ex edge (i, g): between cells (i, g-1) and (i, g); PEC at g == 0 (row ny is never owned)
+  double a = 0.0, b = 0.0;
+  if (i < nx) {
+    if (g == 0 || g >= ny) {
+      a = 1.0; b = 0.0;
+    } else {
+      const double e = EPS0 * 0.5 * (mat(eps_r, i, g - 1) + mat(eps_r, i, g));
+      const double s = 0.5 * (mat(sigma, i, g - 1) + mat(sigma, i, g));
+      a = (e / dt - s / 2) / (e / dt + s / 2);
+      b = 1.0 / ((e / dt + s / 2) * dy);
+    }
+  }
+  cax[o] = (T)a;
+  cbx[o] = (T)b;
+  // Ey edge (i, g): between cells (i-1, g) and (i, g); PEC at i == 0 and i == nx
+  a = 0.0; b = 0.0;
+  if (i == 0 || i == nx) {
+    a = 1.0; b = 0.0;
+  } else if (i < nx) {
+    const double e = EPS0 * 0.5 * (mat(eps_r, i - 1, g) + mat(eps_r, i, g));
+    const double s = 0.5 * (mat(sigma, i - 1, g) + mat(sigma, i, g));
+    a = (e / dt - s / 2) / (e / dt + s / 2);
+    b = 1.0 / ((e / dt + s / 2) * dx);
+  }
+  cay[o] = (T)a;
+  cby[o] = (T)b;
+}
+
+template <typename M>
+__global__ void gather_mat_kernel(const M* eps_r, const M* sigma, int64_t nx, int64_t mat_row0,
+                                  const int64_t* cells, int64_t n, double* oe, double* os) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t gj = cells[k] / nx, gi = cells[k] % nx;
+  oe[k] = (double)eps_r[(gj - mat_row0) * nx + gi];
+  os[k] = (double)sigma[(gj - mat_row0) * nx + gi];
+}
+
+template <typename T>
+__global__ void mask_kernel(T* cax, T* cbx, T* cay, T* cby, T* f0, T* f1, T* f2, T* f3, T* f4, T* f5,
+                            int64_t pitch, const int32_t* rects, int64_t row_begin, bool coefs,
+                            bool zero_iface) {
+  const int32_t* r = rects + 4 * (int64_t)blockIdx.x;
+  const int i0 = r[0], bx = r[2], by = r[3];
+  const int64_t jl0 = (int64_t)r[1] - row_begin + 1;  // local row of the block's bottom cells
+  T* ex[2] = {f0, f3};
+  T* ey[2] = {f1, f4};
+  T* hz[2] = {f2, f5};
+  // Ex edges rows jl0 .. jl0+by (interface at both ends), columns i0 .. i0+bx-1
+  for (int t = threadIdx.x; t < (by + 1) * bx; t += blockDim.x) {
+    const int dj = t / bx, di = t % bx;
+    const int64_t o = (jl0 + dj) * pitch + i0 + di;
+    const bool iface = (dj == 0 || dj == by);
+    if (coefs) { cax[o] = T(1); cbx[o] = T(0); }
+    if (!iface || zero_iface)
+      for (int q = 0; q < 2; ++q) ex[q][o] = T(0);
+  }
+  // Ey edges rows jl0 .. jl0+by-1, columns i0 .. i0+bx
+  for (int t = threadIdx.x; t < by * (bx + 1); t += blockDim.x) {
+    const int dj = t / (bx + 1), di = t % (bx + 1);
+    const int64_t o = (jl0 + dj) * pitch + i0 + di;
+    const bool iface = (di == 0 || di == bx);
+    if (coefs) { cay[o] = T(1); cby[o] = T(0); }
+    if (!iface || zero_iface)
+      for (int q = 0; q < 2; ++q) ey[q][o] = T(0);
+  }
+  for (int t = threadIdx.x; t < by * bx; t += blockDim.x) {
+    const int64_t o = (jl0 + t / bx) * pitch + i0 + t % bx;
+    for (int q = 0; q < 2; ++q) hz[q][o] = T(0);
+  }
+}
+
+}  // namespace
+
+template <typename T>
+void launch_sweep(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s) {
+  const int per_cta = 32 * warps_per_cta;
+  dim3 grid((p.ncolv + per_cta - 1) / per_cta, (p.rows + p.chunk - 1) / p.chunk);
+  if (p.partials) sweep_kernel<T, true><<<grid, per_cta, 0, s>>>(p);
+  else sweep_kernel<T, false><<<grid, per_cta, 0, s>>>(p);
+}
+
+template <typename T>
+void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s) {
+  const size_t smem = sizeof(T) * 7 * (size_t)p.nthreads_vec;
+  if (energy) post_kernel<T, true><<<p.n_inst + 1, 128, smem, s>>>(p);
+  else post_kernel<T, false><<<p.n_inst + 1, 128, smem, s>>>(p);
+}
+
+template <typename T, typename M>
+void launch_coefficients(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t nx, int64_t ny,
+                         int64_t row_begin, int rows, int64_t pitch, double dx, double dy, double dt,
+                         T* cax, T* cbx, T* cay, T* cby, cudaStream_t s) {
+  dim3 grid((unsigned)((pitch + 255) / 256), rows);
+  coef_kernel<T, M><<<grid, 256, 0, s>>>(eps_r, sigma, mat_row0, nx, ny, row_begin, rows, pitch, dx, dy,
+                                         dt, cax, cbx, cay, cby);
+}
+
+template <typename M>
+void launch_gather_materials(const M* eps_r, const M* sigma, int64_t nx, int64_t mat_row0,
+                             const int64_t* cells, int64_t n, double* oe, double* os, cudaStream_t s) {
+  if (n <= 0) return;
+  gather_mat_kernel<M><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(eps_r, sigma, nx, mat_row0, cells, n, oe, os);
+}
+
+template <typename T>
+void launch_mask(T* cax, T* cbx, T* cay, T* cby, T* f[6], int64_t pitch, const int32_t* rects,
+                 int64_t n_rect, int64_t row_begin, bool coefs, bool zero_iface, cudaStream_t s) {
+  if (n_rect <= 0) return;
+  mask_kernel<T><<<(unsigned)n_rect, 256, 0, s>>>(cax, cbx, cay, cby, f[0], f[1], f[2], f[3], f[4], f[5],
+                                                   pitch, rects, row_begin, coefs, zero_iface);
+}
+
+#define INST(T)                                                                                     \
+  template void launch_sweep<T>(const SweepParams<T>&, int, cudaStream_t);                        \
+  template void launch_post<T>(const PostParams<T>&, bool, cudaStream_t);                        \
+  template void launch_coefficients<T, float>(const float*, const float*, int64_t, int64_t, int64_t, \
+                                              int64_t, int, int64_t, double, double, double, T*, T*, \
+                                              T*, T*, cudaStream_t);                               \
+  template void launch_coefficients<T, double>(const double*, const double*, int64_t, int64_t,     \
+                                               int64_t, int64_t, int, int64_t, double, double,     \
+                                               double, T*, T*, T*, T*, cudaStream_t);              \
+  template void launch_mask<T>(T*, T*, T*, T*, T* [6], int64_t, const int32_t*, int64_t, int64_t,  \
+                               bool, bool, cudaStream_t);
+INST(float)
+INST(double)
+template void launch_gather_materials<float>(const float*, const float*, int64_t, int64_t,
+                                             const int64_t*, int64_t, double*, double*, cudaStream_t);
+template void launch_gather_materials<double>(const double*, const double*, int64_t, int64_t,
+                                              const int64_t*, int64_t, double*, double*, cudaStream_t);
+
+}  // namespace fdtd

@@ -1,0 +1,75 @@
+// Internal device-side declarations shared by fdtd_kernels.cu and fdtd_api.cpp.
+// Not part of the public ABI (include/fdtdrom.h is).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fdtd {
+
+// Fused single-pass H+E sweep: S1 (eq:updateH), S2 (source), S3 (energy
+// partials) and S7 (eq:updateEx / Ey analogue) for one time step, ping-pong buffers.
+template <typename T>
+struct SweepParams {
+  const T* ex0; const T* ey0; const T* hz0;  // fields at step n (E^n, H^{n-1/2})
+  T* ex1; T* ey1; T* hz1;                     // fields at step n+1 (E^{n+1}, H^{n+1/2})
+  const T* cax; const T* cbx; const T* cay; const T* cby;  // per-edge update coefficients
+  int64_t pitch;   // elements per row (all arrays)
+  int ncolv;       // vector columns processed (16-byte vectors)
+  int rows;        // owned cell rows (local rows 1..rows; local row 0 is the ghost row below)
+  int chunk;       // rows per CTA
+  T chx, chy;      // dt/(mu0 dx), dt/(mu0 dy)
+  int src_row;     // local row of the soft source (-1: none)
+  int64_t src_col;
+  const double* src_samples; int64_t src_n, src_t0;
+  const int64_t* step;  // device step counter (value n during step n)
+  double* partials;     // energy partial per CTA (nullptr: energy off)
+  T wex, wey, wh;       // dx/2, dy/2, mu0 dx dy / dt
+};
+
+struct RomModelDev {
+  int nY, q1, q2;
+  int64_t off_Q1, off_Aq, off_Kq, off_Lt, off_Bq, off_R11, off_R22, off_K;  // into model pool
+};
+
+// Post kernel: S4-S6 per ROM instance, probe recording, deterministic
+// energy finalisation and the device step counter.
+template <typename T>
+struct PostParams {
+  int n_inst;
+  const int32_t* inst_model;
+  const RomModelDev* models;
+  const T* mpool;                  // shared model matrices (column-major)
+  const T* Sk; const int64_t* Sk_off;        // per-instance Schur inverses (col-major nY x nY)
+  const int64_t* port_off;                    // per-instance offset into port arrays
+  const T* cya; const T* cyg;                 // a_y / c_y, D_l G / c_y per port
+  const double* ehalf;                        // D_l D_l' eps / dt per port (energy)
+  const int64_t* port_edge;                   // per port: (is_ey << 62) | element offset
+  const int64_t* port_h;                      // per port: Hz element offset of the outside cell
+  const int64_t* ring_idx; const int64_t* ring_off;  // hole-ring Hz cells per instance
+  T* state; const int64_t* state_off;         // per instance [E~ (q1); H~ (q2)]
+  T* ex1; T* ey1; T* hz1;
+  int n_probe; const int64_t* probe_idx; T* probe_ring; int64_t cap;
+  const double* sweep_partials; int n_sweep_partials; double* rom_partials; double* energy_ring;
+  int64_t* step; unsigned int* done;
+  int nthreads_vec;  // max(nY, q1, q2) over models (smem sizing)
+};
+
+template <typename T>
+void launch_sweep(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s);
+template <typename T>
+void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s);
+
+// setup kernels
+template <typename T, typename M>
+void launch_coefficients(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t nx, int64_t ny,
+                         int64_t row_begin, int rows, int64_t pitch, double dx, double dy, double dt,
+                         T* cax, T* cbx, T* cay, T* cby, cudaStream_t s);
+template <typename M>
+void launch_gather_materials(const M* eps_r, const M* sigma, int64_t nx, int64_t mat_row0,
+                             const int64_t* cells /*global j*nx+i*/, int64_t n, double* out_eps,
+                             double* out_sig, cudaStream_t s);
+template <typename T>
+void launch_mask(T* cax, T* cbx, T* cay, T* cby, T* fields[6], int64_t pitch, const int32_t* rects,
+                 int64_t n_rect, int64_t row_begin, bool coefs, bool zero_iface, cudaStream_t s);
+
+}  // namespace fdtd

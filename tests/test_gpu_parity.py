@@ -1,0 +1,167 @@
+"""CUDA path vs the fp64 oracle on identical seeded inputs (-m gpu).
+
+Tolerances (BASELINE.json north_star): fp64 relative L2 <= 1e-10 on probe series
+and final fields; fp32 relative L2 <= 1e-4 over the first 2000 steps, with the
+energy never increasing by more than 1e-6 relative per step when source-free.
+"""
+import numpy as np
+import pytest
+
+from inputs import configs
+from inputs import romgen as rg
+from inputs import scene as sc
+
+from helpers import consistent_random_state, gpu_from_scene, oracle_from_scene, rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _compare(scene, n, tol, energy=True, random_init=None, tuning=None, **kw):
+    g = gpu_from_scene(scene, **kw)
+    o = oracle_from_scene(scene)
+    if tuning:
+        g.set_tuning(*tuning)
+    if random_init is not None:
+        Ex, Ey, Hz, xs = consistent_random_state(scene, random_init)
+        g.set_window(0, 0, Ex, Ey, Hz)
+        o.set_state(Ex, Ey, Hz, xs if xs.size else None)
+        if xs.size:
+            g.set_rom_state(xs)
+    g.record_energy(energy)
+    g.step(n)
+    pg, eg = g.probe(), g.energy()
+    Exg, Eyg, Hzg = g.get_window()
+    xg = g.get_rom_state()
+    po, eo = o.step(n, energy=energy)
+    Exo, Eyo, Hzo, xo = o.get_state()
+    errs = dict(probe=rel(pg, po), Ex=rel(Exg, Exo), Ey=rel(Eyg, Eyo), Hz=rel(Hzg, Hzo))
+    if xo.size:
+        errs["rom"] = rel(xg, xo)
+    if energy:
+        errs["energy"] = rel(eg, eo)
+    g.close()
+    bad = {k: v for k, v in errs.items() if not v <= tol}
+    assert not bad, errs
+    return errs, (eg if energy else None)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg1b", "cfg1c"])
+def test_cfg1_full_fp64(name):
+    """Config 1 in full (4000 steps, fp64): <= 1e-10 on probes, fields, ROM state and energy."""
+    s = configs.make(name)
+    _compare(s, s.steps, 1e-10)
+
+
+def test_cfg1_random_init_fp64():
+    s = configs.make("cfg1")
+    _compare(s, 1500, 1e-10, random_init=11)
+
+
+def _ragged_scene(nx, ny, precision, seed=3, rom=True):
+    rng = np.random.default_rng(seed)
+    eps = rng.uniform(1, 4, (ny, nx))
+    sig = rng.uniform(0, 0.05, (ny, nx))
+    dx, dy = 1e-3, 1.3e-3
+    models, placements = [], None
+    dt = 0.95 * sc.cfl_limit(dx, dy)
+    if rom:
+        fe, fs = sc.uniform_fill(3, 2, 3, seed + 1, 1, 4, 0, 0.05)
+        m = rg.build_rom(3, 2, 3, dx, dy, fe, fs, 20, 30e9)
+        fe2, fs2 = sc.uniform_fill(2, 2, 4, seed + 2, 1, 4, 0, 0.05)
+        m2 = rg.build_rom(2, 2, 4, dx, dy, fe2, fs2, 16, 30e9)
+        dt = 0.95 * min(m["fine_dt_limit"], m2["fine_dt_limit"])
+        models = [m, m2]
+        placements = np.array([[0, 4, 5], [1, nx - 8, ny - 7], [0, nx // 2, 3]], dtype=np.int32)
+    steps = 600
+    return sc.Scene(name="ragged", nx=nx, ny=ny, dx=dx, dy=dy, dt=dt, eps_r=eps, sigma=sig, precision=precision,
+                    steps=steps, source=(nx // 3, ny // 2), samples=sc.gaussian_samples(steps, dt, 30e9, True),
+                    probes=np.array([[1, 1], [nx - 2, ny - 2], [nx // 2, ny // 2 + 1]], dtype=np.int32),
+                    models=models, placements=placements)
+
+
+@pytest.mark.parametrize("nx,ny", [(37, 29), (130, 61), (64, 64), (5, 7)])
+def test_ragged_fp64(nx, ny):
+    """Ragged widths (not multiples of the 16-byte vector or the warp strip), several tiles."""
+    s = _ragged_scene(nx, ny, 64, rom=nx >= 30)
+    _compare(s, s.steps, 1e-10, random_init=5)
+
+
+@pytest.mark.parametrize("tuning", [(1, 1), (3, 2), (7, 8), (64, 4)])
+def test_tuning_is_bitwise_invariant(tuning):
+    """Chunk-start and warp-edge recomputation are bit-identical to the owner's values."""
+    s = _ragged_scene(301, 203, 32)
+    base = gpu_from_scene(s)
+    Ex, Ey, Hz, xs = consistent_random_state(s, 9)
+    base.set_window(0, 0, Ex, Ey, Hz)
+    base.set_rom_state(xs)
+    base.step(50)
+    ref = base.get_window()
+    t = gpu_from_scene(s)
+    t.set_tuning(*tuning)
+    t.set_window(0, 0, Ex, Ey, Hz)
+    t.set_rom_state(xs)
+    t.step(50)
+    got = t.get_window()
+    for a, b in zip(got, ref):
+        assert np.array_equal(a, b)
+    assert np.array_equal(t.get_rom_state(), base.get_rom_state())
+
+
+def test_graph_and_eager_paths_agree():
+    s = _ragged_scene(96, 80, 32)
+    a = gpu_from_scene(s, use_graphs=True)
+    b = gpu_from_scene(s, use_graphs=False)
+    for sim in (a, b):
+        sim.record_energy(True)
+        sim.step(3)
+        sim.step(120)
+        sim.step(1)
+    for x, y in zip(a.get_window(), b.get_window()):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a.probe(), b.probe())
+    assert np.array_equal(a.energy(), b.energy())
+
+
+@pytest.mark.parametrize("name,n", [("cfg2", 256), ("cfg3", 512)])
+def test_fp32_crops_2000_steps(name, n):
+    """Seeded cropped sub-instances of configs 2 and 3, fp32, first 2000 steps: <= 1e-4."""
+    s = configs.make(name, n=n)
+    _compare(s, 2000, 1e-4, random_init=7 if name == "cfg3" else None)
+
+
+def test_fp32_energy_non_increasing_source_free():
+    """Q24: source-free, the fp32 GPU trace never rises by more than 1e-6 relative per step."""
+    s = configs.make("cfg3", n=256)
+    g = gpu_from_scene(s, source=False)
+    Ex, Ey, Hz, xs = consistent_random_state(s, 21)
+    g.set_window(0, 0, Ex, Ey, Hz)
+    g.set_rom_state(xs)
+    g.record_energy(True)
+    g.step(2000)
+    e = g.energy()
+    assert np.all(np.diff(e) <= 1e-6 * e[:-1]), np.max(np.diff(e) / e[:-1])
+    assert e[-1] < e[0]
+
+
+def test_fp32_lossless_energy_conserved():
+    """sigma == 0 everywhere (coarse and fine): W^n is conserved up to fp32 roundoff."""
+    nx = ny = 192
+    dx = dy = 1e-3
+    fe, fs = sc.inclusion_fill(6, 4, seed=2)
+    m = rg.build_rom(6, 6, 4, dx, dy, fe, 0 * fs, 48, 10e9)
+    dt = 1.9 * m["fine_dt_limit"]
+    m = rg.extend_cfl(m, 2 * m["fine_dt_limit"])
+    P = sc.place_blocks(nx, ny, [(6, 6)], 40, seed=3, nslabs=1)
+    rng = np.random.default_rng(1)
+    s = sc.Scene(name="lossless", nx=nx, ny=ny, dx=dx, dy=dy, dt=dt, eps_r=rng.uniform(1, 3, (ny, nx)),
+                 sigma=np.zeros((ny, nx)), precision=32, steps=0, source=(0, 0), samples=np.zeros(1),
+                 probes=np.array([[5, 5]], dtype=np.int32), models=[m], placements=P)
+    g = gpu_from_scene(s, source=False)
+    Ex, Ey, Hz, xs = consistent_random_state(s, 4)
+    g.set_window(0, 0, Ex, Ey, Hz)
+    g.set_rom_state(xs)
+    g.record_energy(True)
+    g.step(2000)
+    e = g.energy()
+    assert np.max(np.abs(e - e[0])) <= 1e-5 * e[0]
+    assert np.all(np.diff(e) <= 1e-6 * e[:-1])
