@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: coarse-grid cell-updates/s incl. ROMs (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg4]
+
+A "step" is one time step of the whole hot path (S1..S8 of DESIGN.md) over the
+workload.  Default workload: BASELINE config 4 (the metric's 1/2/4/8-GPU
+config): 32768^2 fp32 coarse grid, smooth random lossy medium, 4096 instances of
+one ROM (16x16 block, r = 4, q = 128), source, 64 probes and the energy trace
+recorded every step.  N > 1: launched by torchrun, one rank per GPU, row slabs
+of 32768/N rows with the per-step NCCL halo exchange (strong scaling).
+``--impl reference`` times the fp64 CPU oracle (the base contract's reference
+arm for this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "coarse-grid cell-updates/s incl. ROMs"
+UNIT = "cell-updates/s"
+WORKLOADS = {
+    "cfg4": "BASELINE config 4: 32768^2 fp32 coarse TEz grid, copula medium eps_r U[1,10] sigma U[0,0.1] l=32, "
+            "4096 instances of one ROM (16x16 coarse block, r=4, disc inclusion, q=128, clipped at 2 dt_f), "
+            "dt = 1.9 dt_f, Gaussian source, 64 probes, energy every step",
+    "cfg3": "BASELINE config 3: 8192^2 fp32, 1024 instances of one ROM (8x8 block, r=8, q=64), dt = 1.9 dt_f",
+    "cfg2": "BASELINE config 2: 8192^2 fp32 plain grid, no ROMs, dt = 0.99 eq.(1)",
+}
+SAMPLE_N = 1024  # bounded CPU sample: a seeded 1024^2 sub-instance of the same recipe
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    lrank = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return ws, rank, lrank
+
+
+# ------------------------------------------------------------------ CPU oracle timing
+def oracle_rate(workload, steps, max_seconds=None):
+    """Time the fp64 oracle (as it stands, single thread) on the bounded sample; cell-updates/s."""
+    import oracle as O
+    from inputs import configs
+
+    s = configs.make(workload, n=SAMPLE_N)
+    eps, sig = configs.to_numpy(s.eps_r), configs.to_numpy(s.sigma)
+    o = O.OracleSim(s.nx, s.ny, s.dx, s.dy, s.dt, eps, sig)
+    ninst = 0
+    if s.placements is not None:
+        for k, i0, j0 in s.placements:
+            o.add_rom(s.models[k], int(i0), int(j0))
+            ninst += 1
+    o.set_source(*s.source, s.samples)
+    o.set_probes(s.probes)
+    o.step(1)
+    t0 = time.perf_counter()
+    done = 0
+    while done < steps:
+        o.step(1)
+        done += 1
+        if max_seconds and time.perf_counter() - t0 > max_seconds:
+            break
+    dt = time.perf_counter() - t0
+    sample = "%s sub-instance %dx%d with %d ROM instances, %d steps (fp64 oracle, single thread)" % (
+        workload, s.nx, s.ny, ninst, done)
+    return s.nx * s.ny * done / dt, dt, done, sample
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    wl = args.workload
+    # warm-up steps then K timed steps, each a step of the bounded sample
+    oracle_rate(wl, max(args.warmup, 0), max_seconds=60)
+    v, dt, done, sample = oracle_rate(wl, args.steps, max_seconds=240)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": done,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(done, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl + " (bounded CPU sample)", "description": WORKLOADS.get(wl, wl),
+                       "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return None
+        time.sleep(0.15)
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows]
+        mx = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].strip().lower() == "active"})
+        load = [x for x in sm if x > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].strip() not in ("", "[N/A]"))}
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from inputs import configs
+    from paper_1609_07114_b200 import Simulation, nccl_unique_id
+
+    ws, rank, lrank = dist_env()
+    torch.cuda.set_device(lrank)
+    if ws > 1:
+        dist.init_process_group("gloo")
+    wl = args.workload
+    t_setup = time.perf_counter()
+    scene = configs.make(wl, device="cuda")
+    ny = scene.ny
+    rb, re = rank * ny // ws, (rank + 1) * ny // ws
+    nid = None
+    if ws > 1:
+        t = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            t = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8).clone()
+        dist.broadcast(t, 0)
+        nid = bytes(t.numpy().tobytes())
+    m0 = max(rb - 1, 0)
+    eps = scene.eps_r[m0:re].contiguous()
+    sig = scene.sigma[m0:re].contiguous()
+    sim = Simulation(scene.nx, scene.ny, scene.dx, scene.dy, scene.dt, eps, sig, precision=scene.precision,
+                     device=lrank, rank=rank, nranks=ws, nccl_id=nid, row_begin=rb, row_end=re,
+                     materials_row0=m0, record_capacity=max(4096, args.steps + args.warmup + 8))
+    del eps, sig
+    ninst = 0
+    if scene.placements is not None:
+        P = scene.placements
+        for k, m in enumerate(scene.models):
+            sel = P[(P[:, 0] == k) & (P[:, 2] - 1 >= rb) & (P[:, 2] + m["by"] <= re - 1)]
+            if len(sel):
+                sim.add_rom(m, sel[:, 1:3])
+                ninst += len(sel)
+    sim.set_source(*scene.source, scene.samples)
+    sim.set_probes(scene.probes)
+    sim.record_energy(not args.no_energy)
+    scene.eps_r = scene.sigma = None
+    torch.cuda.empty_cache()
+    setup_s = time.perf_counter() - t_setup
+    cells_rank = scene.nx * (re - rb)
+    cells_total = scene.nx * scene.ny
+    stream = sim.stream
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    # ---- warm-up
+    sim.step(args.warmup)
+    sim.sync()
+    sim.probe()
+    sim.energy()
+    # ---- timed region: K steps, per-kernel events (sweep / post) on the launching stream
+    clk = Clocks(lrank)
+    clk.start()
+    l0 = sim.info().kernel_launches
+    barrier()
+    torch.cuda.synchronize()
+    sim.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    sim.step(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    sweep_ms, post_ms, nl = sim.profile_read()
+    sim.profile(False)
+    clocks = clk.stop()
+    launches = sim.info().kernel_launches - l0
+    ms_all = ms
+    if ws > 1:
+        t = torch.tensor([ms, sweep_ms, post_ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_all, sweep_ms_max, post_ms_max = t.tolist()
+    value = cells_total * args.steps / (ms_all / 1e3)
+    pr = sim.probe()
+    en = sim.energy()
+    finite = bool(np.all(np.isfinite(pr)) and np.all(np.isfinite(en)))
+
+    # ---- end-to-end through the public API with host buffers (per step: H2D source sample,
+    #      D2H probe samples + energy)
+    e2e = None
+    if not args.no_e2e:
+        samples = np.ascontiguousarray(scene.samples, dtype=np.float64)
+        k_e2e = max(1, min(args.steps, args.e2e_steps))
+        start = sim.info().steps_taken
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(k_e2e):
+            n = start + k
+            sim.set_source(*scene.source, samples[n:n + 1], step0=n)
+            sim.step(1)
+            p = sim.probe()
+            e = sim.energy()
+        torch.cuda.synchronize()
+        barrier()
+        dt_e2e = time.perf_counter() - t0
+        if ws > 1:
+            t = torch.tensor([dt_e2e], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt_e2e = t.item()
+        es = 8 if scene.precision == 64 else 4
+        e2e = {"value": cells_total * k_e2e / dt_e2e, "unit": UNIT, "h2d_bytes_per_step": 8,
+               "d2h_bytes_per_step": len(scene.probes) * es + (0 if args.no_energy else 8),
+               "steps": k_e2e, "api": "fdtd_set_source + fdtd_step(1) + fdtd_probe + fdtd_energy per step"}
+        finite = finite and bool(np.all(np.isfinite(p)))
+    if rank != 0:
+        sim.close()
+        if ws > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (the fused sweep), rank 0's slab
+    pk = peaks()
+    es = 8 if scene.precision == 64 else 4
+    alg_bytes = 10 * es * cells_rank       # 40 B/cell-step fp32: read Ex,Ey,Hz,4 coefs; write Ex,Ey,Hz
+    sweep_avg_s = (sweep_ms / max(nl, 1)) / 1e3
+    achieved = alg_bytes / sweep_avg_s / 1e9
+    peak = pk.get("hbm_gbs", 6650.0)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "sweep_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            if tj.get("workload") == wl:
+                traffic = tj.get("bytes_per_launch_per_cell") * cells_rank
+        except Exception:
+            traffic = None
+    roof = {"kernel": "sweep_kernel<float> (fused H+E)", "bound": "hbm", "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in pk else "fallback",
+            "algorithmic_bytes_per_launch": alg_bytes, "sweep_ms_per_launch": sweep_avg_s * 1e3,
+            "post_ms_per_launch": post_ms / max(nl, 1), "sweep_share_of_step": sweep_ms / max(ms, 1e-9),
+            "frac_of_8TBs_nominal": achieved / 8000.0}
+    cpu = None
+    if ws == 1 and not args.no_cpu:
+        v, dt, done, sample = oracle_rate(wl, 10 ** 6, max_seconds=args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_all / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32" if scene.precision == 32 else "f64",
+            "data": "synthetic",
+            "config": {"workload": wl, "description": WORKLOADS.get(wl, wl), "nx": scene.nx, "ny": scene.ny,
+                       "rom_instances": int(len(scene.placements)) if scene.placements is not None else 0,
+                       "rom_instances_rank0": ninst, "steps_in_config": scene.steps,
+                       "parallelism": "row-slab x%d" % ws, "l2": "inputs larger than L2 (%.1f GB/step)" %
+                       (10 * es * cells_total / 1e9), "energy_recorded": not args.no_energy,
+                       "n_clipped": scene.meta.get("n_clipped"), "setup_s": setup_s, "finite": finite},
+            "roofline": roof, "cpu_baseline": cpu, "clocks": clocks, "e2e": e2e, "gpu_launches": launches}
+    print(json.dumps(line), flush=True)
+    sim.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-energy", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: at least 3 warm-up steps
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

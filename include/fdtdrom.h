@@ -179,6 +179,13 @@ typedef struct {
 } fdtd_info;
 fdtd_status fdtd_get_info(const fdtd_ctx *c, fdtd_info *out);
 
+/* Kernel timing (for bench.py's roofline): while on, fdtd_step launches eagerly and brackets
+ * every sweep and post launch with CUDA events on the context's stream.  fdtd_profile_read
+ * synchronises and returns the summed device milliseconds and the launch count since the
+ * last read. */
+fdtd_status fdtd_profile(fdtd_ctx *c, int32_t on);
+fdtd_status fdtd_profile_read(fdtd_ctx *c, double *sweep_ms, double *post_ms, int64_t *n_launches);
+
 /* Tuning knobs for the fused sweep (rows per CTA, warps per CTA); 0 keeps default. */
 fdtd_status fdtd_set_tuning(fdtd_ctx *c, int32_t rows_per_cta, int32_t warps_per_cta);
 

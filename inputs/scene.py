@@ -81,9 +81,10 @@ def place_blocks(nx, ny, sizes, count, seed, nslabs=8, forbid=(), max_tries=2_00
     Returns int32 array (count, 3): (model, i0, j0).
     """
     rng = np.random.default_rng(seed)
-    occ = np.zeros((ny + 2, nx + 2), dtype=bool)  # padded occupancy of expanded footprints
     slab = ny // nslabs if nslabs > 1 and ny % nslabs == 0 else ny
     forbid = [(int(i), int(j)) for i, j in forbid]
+    B = 64
+    buckets = {}  # (bi, bj) -> list of occupied rects [x0, x1) x [y0, y1) (expanded footprints)
     out = []
     tries = 0
     while len(out) < count:
@@ -96,12 +97,24 @@ def place_blocks(nx, ny, sizes, count, seed, nslabs=8, forbid=(), max_tries=2_00
         j0 = int(rng.integers(2, ny - by - 1))
         if (j0 - 1) // slab != (j0 + by) // slab:
             continue
-        # expanded footprint [i0-1, i0+bx] x [j0-1, j0+by] plus one more cell so rings never touch
-        if occ[j0 - 1: j0 + by + 3, i0 - 1: i0 + bx + 3].any():
+        # expanded footprint [i0-1, i0+bx] x [j0-1, j0+by], kept one extra cell apart so rings never touch
+        x0, x1, y0, y1 = i0 - 1, i0 + bx + 2, j0 - 1, j0 + by + 2
+        keys = [(a, b) for a in range(x0 // B, (x1 - 1) // B + 1) for b in range(y0 // B, (y1 - 1) // B + 1)]
+        hit = False
+        for k in keys:
+            for (u0, u1, v0, v1) in buckets.get(k, ()):
+                if u0 < x1 and x0 < u1 and v0 < y1 and y0 < v1:
+                    hit = True
+                    break
+            if hit:
+                break
+        if hit:
             continue
         if any(i0 - 1 <= fi <= i0 + bx and j0 - 1 <= fj <= j0 + by for fi, fj in forbid):
             continue
-        occ[j0: j0 + by + 2, i0: i0 + bx + 2] = True
+        rect = (i0 - 1, i0 + bx + 1, j0 - 1, j0 + by + 1)
+        for k in keys:
+            buckets.setdefault(k, []).append(rect)
         out.append((m, i0, j0))
     return np.array(out, dtype=np.int32).reshape(-1, 3)
 

@@ -117,6 +117,10 @@ struct fdtd_ctx {
   cudaGraphExec_t gexec = nullptr;
   bool graph_dirty = true;
   int64_t launches = 0;
+  // profiling (event pairs around each launch)
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev;
+  size_t ev_used = 0;
   // multi-rank
   nccl_comm comm = nullptr;
   std::vector<void*> owned;  // every device allocation
@@ -246,16 +250,30 @@ fdtd_status halo_exchange(fdtd_ctx* c, int q, cudaStream_t s) {
   return FDTD_OK;
 }
 
+cudaEvent_t next_event(fdtd_ctx* c) {
+  if (c->ev_used == c->ev.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev.push_back(e);
+  }
+  return c->ev[c->ev_used++];
+}
+
 fdtd_status enqueue_step(fdtd_ctx* c, int q, cudaStream_t s) {
   fdtd_status st = halo_exchange(c, q, s);
   if (st != FDTD_OK) return st;
-  if (c->prec == 64) {
-    fdtd::launch_sweep<double>(sweep_params<double>(c, q), c->warps, s);
-    fdtd::launch_post<double>(post_params<double>(c, q), c->energy_on, s);
-  } else {
-    fdtd::launch_sweep<float>(sweep_params<float>(c, q), c->warps, s);
-    fdtd::launch_post<float>(post_params<float>(c, q), c->energy_on, s);
+  const bool prof = c->profiling && s == c->stream;
+  cudaEvent_t e[3];
+  if (prof) {
+    for (auto& x : e) x = next_event(c);
+    CK(cudaEventRecord(e[0], s));
   }
+  if (c->prec == 64) fdtd::launch_sweep<double>(sweep_params<double>(c, q), c->warps, s);
+  else fdtd::launch_sweep<float>(sweep_params<float>(c, q), c->warps, s);
+  if (prof) CK(cudaEventRecord(e[1], s));
+  if (c->prec == 64) fdtd::launch_post<double>(post_params<double>(c, q), c->energy_on, s);
+  else fdtd::launch_post<float>(post_params<float>(c, q), c->energy_on, s);
+  if (prof) CK(cudaEventRecord(e[2], s));
   c->launches += 2;
   return FDTD_OK;
 }
@@ -445,28 +463,20 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
   }
   double emin = INFINITY, smin = INFINITY;
   {
-    // min eps_r over the owned rows (host side; device arrays are copied once)
-    std::vector<char> hbuf;
-    const char* he = ebase;
-    const char* hs = sbase;
-    std::vector<char> hsb;
-    if (on_dev) {
-      hbuf.resize(nmat * mes);
-      hsb.resize(nmat * mes);
-      if (cudaMemcpy(hbuf.data(), c->mat_eps, nmat * mes, cudaMemcpyDeviceToHost) != cudaSuccess ||
-          cudaMemcpy(hsb.data(), c->mat_sig, nmat * mes, cudaMemcpyDeviceToHost) != cudaSuccess) {
-        fdtd_destroy(c);
-        return FDTD_E_CUDA;
-      }
-      he = hbuf.data();
-      hs = hsb.data();
+    // min eps_r / sigma over the owned rows (+ ghost row), reduced on the device
+    const int nb = 1024;
+    double* dm = (double*)dalloc(c, 2 * nb * sizeof(double));
+    if (!dm) { fdtd_destroy(c); return FDTD_E_NOMEM; }
+    if (f32) fdtd::launch_min2<float>((const float*)c->mat_eps, (const float*)c->mat_sig, nmat, dm, nb, c->stream);
+    else fdtd::launch_min2<double>((const double*)c->mat_eps, (const double*)c->mat_sig, nmat, dm, nb, c->stream);
+    std::vector<double> hm(2 * nb);
+    if (cudaMemcpyAsync(hm.data(), dm, hm.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess) {
+      fdtd_destroy(c);
+      return FDTD_E_CUDA;
     }
-    for (int64_t k = 0; k < nmat; ++k) {
-      const double e = f32 ? (double)((const float*)he)[k] : ((const double*)he)[k];
-      const double s = f32 ? (double)((const float*)hs)[k] : ((const double*)hs)[k];
-      emin = std::min(emin, e);
-      smin = std::min(smin, s);
-    }
+    for (int k = 0; k < nb; ++k) { emin = std::min(emin, hm[2 * k]); smin = std::min(smin, hm[2 * k + 1]); }
+    dfree(c, dm);
   }
   if (!(emin > 0) || smin < 0) {
     fail(c, FDTD_E_ARG, "materials must have eps_r > 0 and sigma >= 0");
@@ -787,7 +797,7 @@ fdtd_status fdtd_step(fdtd_ctx* c, int64_t nsteps) {
   if (c->energy_on) oldest = std::min(oldest, c->rd_energy);
   if (c->steps + nsteps - oldest > c->cap)
     return fail(c, FDTD_E_STATE, "unread records would exceed record_capacity (%lld)", (long long)c->cap);
-  const bool use_graph = !(c->d.flags & FDTD_NO_GRAPH) && c->d.nranks == 1 && nsteps >= 2;
+  const bool use_graph = !(c->d.flags & FDTD_NO_GRAPH) && c->d.nranks == 1 && nsteps >= 2 && !c->profiling;
   fdtd_status st;
   int64_t left = nsteps;
   if (use_graph) {
@@ -979,6 +989,31 @@ fdtd_status fdtd_set_rom_state(fdtd_ctx* c, const double* in, int64_t n) {
   return FDTD_OK;
 }
 
+fdtd_status fdtd_profile(fdtd_ctx* c, int32_t on) {
+  if (!c) return FDTD_E_ARG;
+  c->profiling = on != 0;
+  c->ev_used = 0;
+  return FDTD_OK;
+}
+
+fdtd_status fdtd_profile_read(fdtd_ctx* c, double* sweep_ms, double* post_ms, int64_t* n) {
+  if (!c || !sweep_ms || !post_ms || !n) return FDTD_E_ARG;
+  CK(cudaStreamSynchronize(c->stream));
+  double a = 0.0, b = 0.0;
+  for (size_t k = 0; k + 3 <= c->ev_used; k += 3) {
+    float t1 = 0.f, t2 = 0.f;
+    CK(cudaEventElapsedTime(&t1, c->ev[k], c->ev[k + 1]));
+    CK(cudaEventElapsedTime(&t2, c->ev[k + 1], c->ev[k + 2]));
+    a += t1;
+    b += t2;
+  }
+  *sweep_ms = a;
+  *post_ms = b;
+  *n = (int64_t)(c->ev_used / 3);
+  c->ev_used = 0;
+  return FDTD_OK;
+}
+
 fdtd_status fdtd_sync(fdtd_ctx* c) {
   if (!c) return FDTD_E_ARG;
   return check_async(c);
@@ -1012,6 +1047,7 @@ void fdtd_destroy(fdtd_ctx* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
   drop_graph(c);
+  for (auto e : c->ev) cudaEventDestroy(e);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   std::vector<void*> all = c->owned;

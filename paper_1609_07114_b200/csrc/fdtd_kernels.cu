@@ -425,7 +425,36 @@ __global__ void mask_kernel(T* cax, T* cbx, T* cay, T* cby, T* f0, T* f1, T* f2,
   }
 }
 
+template <typename M>
+__global__ void min2_kernel(const M* a, const M* b, int64_t n, double* out) {
+  double ma = INFINITY, mb = INFINITY;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    ma = fmin(ma, (double)a[k]);
+    mb = fmin(mb, (double)b[k]);
+  }
+  __shared__ double ra[32], rb[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    ma = fmin(ma, __shfl_down_sync(FULL, ma, o));
+    mb = fmin(mb, __shfl_down_sync(FULL, mb, o));
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { ra[w] = ma; rb[w] = mb; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) { ma = fmin(ma, ra[k]); mb = fmin(mb, rb[k]); }
+    out[2 * blockIdx.x] = fmin(ma, ra[0]);
+    out[2 * blockIdx.x + 1] = fmin(mb, rb[0]);
+  }
+}
+
 }  // namespace
+
+template <typename M>
+void launch_min2(const M* a, const M* b, int64_t n, double* out, int nblocks, cudaStream_t s) {
+  min2_kernel<M><<<nblocks, 256, 0, s>>>(a, b, n, out);
+}
+template void launch_min2<float>(const float*, const float*, int64_t, double*, int, cudaStream_t);
+template void launch_min2<double>(const double*, const double*, int64_t, double*, int, cudaStream_t);
 
 template <typename T>
 void launch_sweep(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s) {

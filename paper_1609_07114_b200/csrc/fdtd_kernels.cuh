@@ -68,6 +68,8 @@ template <typename M>
 void launch_gather_materials(const M* eps_r, const M* sigma, int64_t nx, int64_t mat_row0,
                              const int64_t* cells /*global j*nx+i*/, int64_t n, double* out_eps,
                              double* out_sig, cudaStream_t s);
+template <typename M>
+void launch_min2(const M* a, const M* b, int64_t n, double* out /*2 per block*/, int nblocks, cudaStream_t s);
 template <typename T>
 void launch_mask(T* cax, T* cbx, T* cay, T* cby, T* fields[6], int64_t pitch, const int32_t* rects,
                  int64_t n_rect, int64_t row_begin, bool coefs, bool zero_iface, cudaStream_t s);

@@ -82,6 +82,8 @@ def lib():
         L.fdtd_sync.argtypes = [vp]
         L.fdtd_get_info.argtypes = [vp, C.POINTER(Info)]
         L.fdtd_set_tuning.argtypes = [vp, i32, i32]
+        L.fdtd_profile.argtypes = [vp, i32]
+        L.fdtd_profile_read.argtypes = [vp, dp, dp, C.POINTER(i64)]
         L.fdtd_nccl_unique_id.argtypes = [vp]
         L.fdtd_last_error.argtypes = [vp]
         L.fdtd_last_error.restype = C.c_char_p
@@ -90,7 +92,7 @@ def lib():
         L.fdtd_destroy.restype = None
         for n in ("create", "add_rom", "set_source", "set_probes", "record_energy", "step", "probe", "energy",
                   "get_window", "set_window", "get_rom_state", "set_rom_state", "sync", "get_info", "set_tuning",
-                  "nccl_unique_id"):
+                  "nccl_unique_id", "profile", "profile_read"):
             getattr(L, "fdtd_" + n).restype = C.c_int
         _lib = L
     return _lib
@@ -181,6 +183,7 @@ class Simulation:
         if st:
             raise FDTDError(st, "fdtd_create failed")
         self._h = h
+        self._mat = None  # copied by fdtd_create
         self.n_probe = 0
         self.rom_state_len = 0
 
@@ -283,6 +286,14 @@ class Simulation:
         o = Info()
         self._ck(lib().fdtd_get_info(self._h, C.byref(o)), "fdtd_get_info")
         return o
+
+    def profile(self, on=True):
+        self._ck(lib().fdtd_profile(self._h, 1 if on else 0), "fdtd_profile")
+
+    def profile_read(self):
+        a, b, n = C.c_double(0), C.c_double(0), C.c_int64(0)
+        self._ck(lib().fdtd_profile_read(self._h, C.byref(a), C.byref(b), C.byref(n)), "fdtd_profile_read")
+        return a.value, b.value, n.value
 
     def set_tuning(self, rows_per_cta=0, warps_per_cta=0):
         self._ck(lib().fdtd_set_tuning(self._h, int(rows_per_cta), int(warps_per_cta)), "fdtd_set_tuning")
