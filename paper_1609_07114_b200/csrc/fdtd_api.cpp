@@ -85,6 +85,7 @@ struct fdtd_ctx {
   int64_t* d_step = nullptr;
   unsigned* d_done = nullptr;
   double* d_partials = nullptr;
+  double* d_level1 = nullptr;
   int n_partials = 0;
   int chunk = 64, warps = 4;
   // source
@@ -105,6 +106,9 @@ struct fdtd_ctx {
   std::vector<double> cya, cyg, ehalf, Sk;  // fp64 host copies (converted on upload)
   std::vector<double> mpool;                // shared model matrices (col-major, fp64)
   int nvec = 1;
+  int rom_batch = 16;
+  std::vector<int32_t> batch_tab;  // (model, first instance, count)
+  int32_t* d_batch_tab = nullptr;
   // device ROM arrays
   void* d_mpool = nullptr; void* d_Sk = nullptr; void* d_cya = nullptr; void* d_cyg = nullptr;
   void* d_state = nullptr; double* d_ehalf = nullptr; double* d_rom_partials = nullptr;
@@ -227,6 +231,11 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
   p.rom_partials = c->d_rom_partials; p.energy_ring = c->d_energy_ring;
   p.step = c->d_step; p.done = c->d_done;
   p.nthreads_vec = c->nvec;
+  p.n_batch = (int)(c->batch_tab.size() / 3);
+  p.batch = c->rom_batch;
+  p.batch_tab = c->d_batch_tab;
+  p.block = 256;
+  p.level1 = c->d_level1;
   return p;
 }
 
@@ -360,6 +369,25 @@ fdtd_status upload_roms(fdtd_ctx* c) {
   if ((st = upload_T(c, &c->d_mpool, c->mpool)) != FDTD_OK) return st;
   if ((st = upload(c, &c->d_models, md)) != FDTD_OK) return st;
   if ((st = upload(c, &c->d_inst_model, c->inst_model)) != FDTD_OK) return st;
+  // batches of consecutive instances of one model (instances are stored grouped by model)
+  {
+    const char* env = getenv("FDTD_ROM_BATCH");
+    int B = env ? atoi(env) : 8;
+    B = std::max(4, std::min(64, (B + 3) / 4 * 4));
+    while (B > 4 && ((size_t)7 * c->nvec * B + 2 * (size_t)c->nvec * c->nvec) * c->es > 200 * 1024) B -= 4;
+    c->rom_batch = B;
+    c->batch_tab.clear();
+    const int n = (int)c->inst_model.size();
+    for (int k = 0; k < n;) {
+      int e = k;
+      while (e < n && e - k < B && c->inst_model[e] == c->inst_model[k]) ++e;
+      c->batch_tab.insert(c->batch_tab.end(), {c->inst_model[k], k, e - k});
+      k = e;
+    }
+    if ((st = upload(c, &c->d_batch_tab, c->batch_tab)) != FDTD_OK) return st;
+    std::vector<double> l1(c->batch_tab.size() / 3 + 1, 0.0);
+    if ((st = upload(c, &c->d_level1, l1)) != FDTD_OK) return st;
+  }
   if ((st = upload_T(c, &c->d_Sk, c->Sk)) != FDTD_OK) return st;
   if ((st = upload(c, &c->d_Sk_off, c->Sk_off)) != FDTD_OK) return st;
   if ((st = upload(c, &c->d_port_off, c->port_off)) != FDTD_OK) return st;
@@ -499,6 +527,7 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
   c->d_step = (int64_t*)dalloc(c, sizeof(int64_t));
   c->d_done = (unsigned*)dalloc(c, sizeof(unsigned) * 4);
   c->d_energy_ring = (double*)dalloc(c, c->cap * sizeof(double));
+  c->d_level1 = (double*)dalloc(c, 16 * sizeof(double));
   if (!c->d_step || !c->d_done || !c->d_energy_ring) { fdtd_destroy(c); return FDTD_E_NOMEM; }
   fdtd_status st = f32 ? build_coefficients<float>(c) : build_coefficients<double>(c);
   if (st != FDTD_OK) { fdtd_destroy(c); return st; }
@@ -635,6 +664,7 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
   ModelHost mh;
   mh.bx = bx; mh.by = by; mh.nY = nY; mh.q1 = q1; mh.q2 = q2; mh.P = P;
   auto push = [&](const Mat& A, int rows_, int cols_) {  // row-major host -> column-major pool
+    while (c->mpool.size() % 4) c->mpool.push_back(0.0);   // 16-byte aligned operators (cp.async)
     const int64_t off = (int64_t)c->mpool.size();
     for (int j = 0; j < cols_; ++j)
       for (int i = 0; i < rows_; ++i) c->mpool.push_back(A[(size_t)i * cols_ + j]);

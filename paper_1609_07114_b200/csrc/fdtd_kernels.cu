@@ -204,120 +204,234 @@ __device__ double block_sum(double v, double* red) {
   return s;  // valid in thread 0
 }
 
+// ---- asynchronous global -> shared copies (cp.async, sm_80+; SASS LDGSTS)
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Stage n elements (16-byte aligned source and destination) into shared memory; one commit group.
+template <typename T>
+__device__ __forceinline__ void stage(T* dst, const T* src, int n) {
+  constexpr int V = 16 / sizeof(T);
+  const int nv = n / V;
+  for (int k = threadIdx.x; k < nv; k += blockDim.x) cp_async16(dst + k * V, src + k * V);
+  for (int k = nv * V + threadIdx.x; k < n; k += blockDim.x) {
+    if (sizeof(T) == 8) cp_async8(dst + k, src + k);
+    else cp_async4(dst + k, src + k);
+  }
+  cp_commit();
+}
+
+// Y[i][b] += alpha * sum_c A[c*m + i] X[c][b] for i < m, b < B.  A is a shared model operator
+// staged in shared memory (column-major); X, Y in shared memory with row stride B (B % 4 == 0).
+// Each thread item owns one row i and IPI consecutive instances.
+template <typename T, int IPI>
+__device__ __forceinline__ void bgemm_ipi(const T* A, int m, int k, const T* X, T* Y, int B, T alpha) {
+  const int G = B / IPI;
+  for (int it = threadIdx.x; it < m * G; it += blockDim.x) {
+    const int i = it % m, g = (it / m) * IPI;
+    T acc[IPI];
+#pragma unroll
+    for (int u = 0; u < IPI; ++u) acc[u] = T(0);
+#pragma unroll 8
+    for (int c = 0; c < k; ++c) {
+      const T a = A[c * m + i];
+      const T* x = X + c * B + g;
+#pragma unroll
+      for (int u = 0; u < IPI; ++u) acc[u] = fma_rn(a, x[u], acc[u]);
+    }
+    T* y = Y + i * B + g;
+#pragma unroll
+    for (int u = 0; u < IPI; ++u) y[u] = fma_rn(alpha, acc[u], y[u]);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void bgemm(const T* A, int m, int k, const T* X, T* Y, int B, T alpha) {
+  if (m * (B / 4) >= (int)blockDim.x) bgemm_ipi<T, 4>(A, m, k, X, Y, B, alpha);
+  else if (m * (B / 2) >= (int)blockDim.x) bgemm_ipi<T, 2>(A, m, k, X, Y, B, alpha);
+  else bgemm_ipi<T, 1>(A, m, k, X, Y, B, alpha);
+}
+
+// One CTA = one batch of up to p.batch instances of one model (K3).  The shared
+// operators of the model are streamed through two shared-memory buffers (cp.async double
+// buffering): while phase p computes from one buffer, the operator of phase p+1 is in flight.
 template <typename T, bool ENERGY>
-__device__ void rom_instance(const PostParams<T>& p, int b, T* sv, double* red) {
-  const RomModelDev m = p.models[p.inst_model[b]];
+__device__ void rom_batch(const PostParams<T>& p, int bi, T* sv) {
+  const int model = p.batch_tab[3 * bi], first = p.batch_tab[3 * bi + 1], nb = p.batch_tab[3 * bi + 2];
+  const RomModelDev m = p.models[model];
   const int nY = m.nY, q1 = m.q1, q2 = m.q2;
-  const int NV = p.nthreads_vec;
-  T* sy = sv;
-  T* sh = sy + NV;
-  T* sE = sh + NV;
-  T* sH = sE + NV;
-  T* sEs = sH + NV;
-  T* st = sEs + NV;
-  T* sU = st + NV;
+  const int B = p.batch, NV = p.nthreads_vec;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int64_t po = p.port_off[b];
-  T* xs = p.state + p.state_off[b];
-  const T* Q1 = p.mpool + m.off_Q1;
-  const T* Aq = p.mpool + m.off_Aq;
-  const T* Kq = p.mpool + m.off_Kq;
-  const T* Lt = p.mpool + m.off_Lt;
-  const T* Bq = p.mpool + m.off_Bq;
-  // S4: gather y^n (interface edges, copied old->new by the sweep) and h = Hz^{n+1/2} outside
-  for (int i = tid; i < nY; i += nt) {
+  const int64_t S = (int64_t)NV * B;
+  T* sy = sv;
+  T* sh = sy + S;
+  T* sE = sh + S;
+  T* sH = sE + S;
+  T* sEs = sH + S;
+  T* st = sEs + S;
+  T* sU = st + S;
+  const int64_t NB = ((int64_t)NV * NV + 3) / 4 * 4;  // keep both buffers 16-byte aligned
+  T* buf[2] = {sU + S, sU + S + NB};
+  const T* mp = p.mpool;
+  // operator sequence (pointer, rows, cols)
+  const T* op[9];
+  int om[9], ok[9], nop = 0;
+  auto add = [&](int64_t off, int r, int c) { op[nop] = mp + off; om[nop] = r; ok[nop] = c; ++nop; };
+  if (ENERGY) { add(m.off_R11, q1, q1); add(m.off_R22, q2, q2); add(m.off_K, q1, q2); }
+  add(m.off_Q1, q2, q1); add(m.off_Aq, q1, q1); add(m.off_Kq, q1, q2); add(m.off_Lt, nY, q1);
+  add(m.off_Bq, q1, nY); add(m.off_Lt, nY, q1);
+  int ph = 0;
+  stage<T>(buf[0], op[0], om[0] * ok[0]);
+  // next(): start staging operator ph+1, wait for operator ph, return its buffer
+  auto next = [&]() -> const T* {
+    if (ph + 1 < nop) {
+      stage<T>(buf[(ph + 1) & 1], op[ph + 1], om[ph + 1] * ok[ph + 1]);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    return buf[ph & 1];
+  };
+  auto done = [&]() { __syncthreads(); ++ph; };
+
+  for (int64_t k = tid; k < 7 * S; k += nt) sv[k] = T(0);
+  __syncthreads();
+  // S4: gather y^n (interface edges, copied old->new by the sweep), h = Hz^{n+1/2} outside, state
+  for (int it = tid; it < nY * nb; it += nt) {
+    const int i = it % nY, b = it / nY;
+    const int64_t po = p.port_off[first + b];
     const int64_t e = p.port_edge[po + i];
-    sy[i] = (e >> 62) ? p.ey1[e & IDX_MASK] : p.ex1[e & IDX_MASK];
-    sh[i] = p.hz1[p.port_h[po + i]];
+    sy[i * B + b] = (e >> 62) ? p.ey1[e & IDX_MASK] : p.ex1[e & IDX_MASK];
+    sh[i * B + b] = p.hz1[p.port_h[po + i]];
   }
-  for (int i = tid; i < q1; i += nt) sE[i] = xs[i];
-  for (int i = tid; i < q2; i += nt) sH[i] = xs[q1 + i];
-  __syncthreads();
-  if (ENERGY) {  // coarse interface half cells + x~^T R~ x~ (eq:R with R~11, R~22, K~)
-    const T* R11 = p.mpool + m.off_R11;
-    const T* R22 = p.mpool + m.off_R22;
-    const T* Km = p.mpool + m.off_K;
-    double w = 0.0;
-    for (int i = tid; i < nY; i += nt) w += p.ehalf[po + i] * (double)sy[i] * (double)sy[i];
-    for (int i = tid; i < q1; i += nt) {
-      double a = 0.0, k = 0.0;
-      for (int c = 0; c < q1; ++c) a += (double)R11[(int64_t)c * q1 + i] * (double)sE[c];
-      for (int c = 0; c < q2; ++c) k += (double)Km[(int64_t)c * q1 + i] * (double)sH[c];
-      w += (double)sE[i] * (a - k);
-    }
-    for (int i = tid; i < q2; i += nt) {
-      double a = 0.0;
-      for (int c = 0; c < q2; ++c) a += (double)R22[(int64_t)c * q2 + i] * (double)sH[c];
-      w += (double)sH[i] * a;
-    }
-    const double s = block_sum(w, red);
-    if (tid == 0) p.rom_partials[b] = s;
-  }
-  // S5 (factored eq:connExplicit, K3):
-  // (1) H~ <- H~ + Q1 E~   (each thread owns its sH[i]; only sE is shared)
-  for (int i = tid; i < q2; i += nt) {
-    T a = sH[i];
-    for (int c = 0; c < q1; ++c) a = fma_rn(Q1[(int64_t)c * q2 + i], sE[c], a);
-    sH[i] = a;
+  for (int it = tid; it < (q1 + q2) * nb; it += nt) {
+    const int i = it % (q1 + q2), b = it / (q1 + q2);
+    const T v = p.state[p.state_off[first + b] + i];
+    if (i < q1) sE[i * B + b] = v;
+    else sH[(i - q1) * B + b] = v;
   }
   __syncthreads();
+  if (ENERGY) {  // W_rom = sum D_l D_l' eps/dt y^2 + E~^T (R~11/dt) E~ + H~^T (R~22/dt) H~ - E~^T K~ H~
+    const T* A = next();
+    bgemm<T>(A, q1, q1, sE, sEs, B, T(1));
+    done();
+    A = next();
+    bgemm<T>(A, q2, q2, sH, st, B, T(1));
+    done();
+    A = next();
+    bgemm<T>(A, q1, q2, sH, sEs, B, T(-1));
+    done();
+    const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+    for (int b = w; b < nb; b += nw) {
+      const int64_t po = p.port_off[first + b];
+      double acc = 0.0;
+      for (int i = lane; i < nY; i += 32) acc += p.ehalf[po + i] * (double)sy[i * B + b] * (double)sy[i * B + b];
+      for (int i = lane; i < q1; i += 32) acc += (double)sE[i * B + b] * (double)sEs[i * B + b];
+      for (int i = lane; i < q2; i += 32) acc += (double)sH[i * B + b] * (double)st[i * B + b];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
+      if (lane == 0) p.rom_partials[first + b] = acc;
+    }
+    __syncthreads();
+    for (int64_t k = tid; k < S; k += nt) { sEs[k] = T(0); st[k] = T(0); }
+  }
+  // S5 (factored eq:connExplicit):
+  // (1) H~ <- H~ + Q1 E~
+  const T* A = next();
+  bgemm<T>(A, q2, q1, sE, sH, B, T(1));
+  done();
   // (2) E* = Aq E~ + Kq H~
-  for (int i = tid; i < q1; i += nt) {
-    T a = T(0);
-    for (int c = 0; c < q1; ++c) a = fma_rn(Aq[(int64_t)c * q1 + i], sE[c], a);
-    for (int c = 0; c < q2; ++c) a = fma_rn(Kq[(int64_t)c * q1 + i], sH[c], a);
-    sEs[i] = a;
-  }
-  __syncthreads();
+  A = next();
+  bgemm<T>(A, q1, q1, sE, sEs, B, T(1));
+  done();
+  A = next();
+  bgemm<T>(A, q1, q2, sH, sEs, B, T(1));
+  done();
   // (3) t = (a_y/c_y) y + (D_l G/c_y) h - L~^T E*
-  for (int i = tid; i < nY; i += nt) {
-    T a = fma_rn(p.cyg[po + i], sh[i], mul_rn(p.cya[po + i], sy[i]));
-    for (int c = 0; c < q1; ++c) a = fma_rn(-Lt[(int64_t)c * nY + i], sEs[c], a);
-    st[i] = a;
+  for (int it = tid; it < nY * nb; it += nt) {
+    const int i = it % nY, b = it / nY;
+    const int64_t po = p.port_off[first + b];
+    st[i * B + b] = fma_rn(p.cyg[po + i], sh[i * B + b], mul_rn(p.cya[po + i], sy[i * B + b]));
   }
-  __syncthreads();
-  // (4) U = S_k t
-  const T* S = p.Sk + p.Sk_off[b];
-  for (int i = tid; i < nY; i += nt) {
+  A = next();  // (barrier inside)
+  bgemm<T>(A, nY, q1, sEs, st, B, T(-1));
+  done();
+  // (4) U = S_k t (per-instance Schur inverse, streamed from HBM; many loads in flight)
+  for (int it = tid; it < nY * nb; it += nt) {
+    const int i = it % nY, b = it / nY;
+    const T* Sk = p.Sk + p.Sk_off[first + b] + i;
     T a = T(0);
-    for (int c = 0; c < nY; ++c) a = fma_rn(S[(int64_t)c * nY + i], st[c], a);
-    sU[i] = a;
+#pragma unroll 16
+    for (int c = 0; c < nY; ++c) a = fma_rn(__ldg(Sk + (int64_t)c * nY), st[c * B + b], a);
+    sU[i * B + b] = a;
   }
-  __syncthreads();
+  for (int64_t k = tid; k < (int64_t)q1 * B; k += nt) sE[k] = sEs[k];
   // (5) E~ = E* + Bq U
-  for (int i = tid; i < q1; i += nt) {
-    T a = sEs[i];
-    for (int c = 0; c < nY; ++c) a = fma_rn(Bq[(int64_t)c * q1 + i], sU[c], a);
-    sE[i] = a;
+  A = next();
+  bgemm<T>(A, q1, nY, sU, sE, B, T(1));
+  done();
+  // (6) y^{n+1} = L~^T E~
+  for (int64_t k = tid; k < (int64_t)nY * B; k += nt) sy[k] = T(0);
+  A = next();
+  bgemm<T>(A, nY, q1, sE, sy, B, T(1));
+  done();
+  // S6: scatter y^{n+1}; store the state; reset the hole-ring Hz cells (they took garbage
+  // from the interface edges in the sweep and must not enter the next energy sum)
+  for (int it = tid; it < nY * nb; it += nt) {
+    const int i = it % nY, b = it / nY;
+    const int64_t e = p.port_edge[p.port_off[first + b] + i];
+    if (e >> 62) p.ey1[e & IDX_MASK] = sy[i * B + b];
+    else p.ex1[e & IDX_MASK] = sy[i * B + b];
   }
-  __syncthreads();
-  // (6) y^{n+1} = L~^T E~ ; S6: scatter into the interface edges
-  for (int i = tid; i < nY; i += nt) {
-    T a = T(0);
-    for (int c = 0; c < q1; ++c) a = fma_rn(Lt[(int64_t)c * nY + i], sE[c], a);
-    const int64_t e = p.port_edge[po + i];
-    if (e >> 62) p.ey1[e & IDX_MASK] = a;
-    else p.ex1[e & IDX_MASK] = a;
+  for (int it = tid; it < (q1 + q2) * nb; it += nt) {
+    const int i = it % (q1 + q2), b = it / (q1 + q2);
+    p.state[p.state_off[first + b] + i] = i < q1 ? sE[i * B + b] : sH[(i - q1) * B + b];
   }
-  for (int i = tid; i < q1; i += nt) xs[i] = sE[i];
-  for (int i = tid; i < q2; i += nt) xs[q1 + i] = sH[i];
-  // hole-ring Hz cells took garbage from the interface edges in the sweep; reset them
-  for (int64_t k = p.ring_off[b] + tid; k < p.ring_off[b + 1]; k += nt) p.hz1[p.ring_idx[k]] = T(0);
+  for (int b = 0; b < nb; ++b)
+    for (int64_t k = p.ring_off[first + b] + tid; k < p.ring_off[first + b + 1]; k += nt) p.hz1[p.ring_idx[k]] = T(0);
 }
 
 template <typename T, bool ENERGY>
-__global__ void __launch_bounds__(128) post_kernel(const PostParams<T> p) {
+__global__ void __launch_bounds__(256) post_kernel(const PostParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[32];
   __shared__ bool last;
   T* sv = reinterpret_cast<T*>(smem_raw);
   const int b = blockIdx.x;
   const int64_t step = *p.step;
-  if (b < p.n_inst) {
-    rom_instance<T, ENERGY>(p, b, sv, red);
+  if (b < p.n_batch) {
+    rom_batch<T, ENERGY>(p, b, sv);
   } else {
     for (int k = threadIdx.x; k < p.n_probe; k += blockDim.x)
       p.probe_ring[(int64_t)k * p.cap + step % p.cap] = p.hz1[p.probe_idx[k]];
+  }
+  if (ENERGY) {
+    // level 1 (every CTA, fixed slice): sweep partials [b*per, (b+1)*per) + this batch's ROM energies
+    const int per = (p.n_sweep_partials + gridDim.x - 1) / gridDim.x;
+    const int k0 = b * per, k1 = min(p.n_sweep_partials, k0 + per);
+    double v = 0.0;
+    for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) v += __ldcg(p.sweep_partials + k);
+    __syncthreads();  // rom_partials of this batch written (rom_batch ends with barriers)
+    if (b < p.n_batch) {
+      const int first = p.batch_tab[3 * b + 1], nb = p.batch_tab[3 * b + 2];
+      for (int k = threadIdx.x; k < nb; k += blockDim.x) v += p.rom_partials[first + k];
+    }
+    const double tot = block_sum(v, red);
+    if (threadIdx.x == 0) p.level1[b] = tot;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -328,12 +442,10 @@ __global__ void __launch_bounds__(128) post_kernel(const PostParams<T> p) {
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (ENERGY) {
+  if (ENERGY) {  // level 2: fixed-order sum of the per-CTA values (deterministic)
     double s = 0.0;
-    for (int k = threadIdx.x; k < p.n_sweep_partials; k += blockDim.x) s += __ldcg(p.sweep_partials + k);
-    double r = 0.0;
-    for (int k = threadIdx.x; k < p.n_inst; k += blockDim.x) r += __ldcg(p.rom_partials + k);
-    const double tot = block_sum(s + r, red);
+    for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) s += __ldcg(p.level1 + k);
+    const double tot = block_sum(s, red);
     if (threadIdx.x == 0) p.energy_ring[step % p.cap] = tot;
   }
   if (threadIdx.x == 0) {
@@ -466,9 +578,14 @@ void launch_sweep(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s) {
 
 template <typename T>
 void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s) {
-  const size_t smem = sizeof(T) * 7 * (size_t)p.nthreads_vec;
-  if (energy) post_kernel<T, true><<<p.n_inst + 1, 128, smem, s>>>(p);
-  else post_kernel<T, false><<<p.n_inst + 1, 128, smem, s>>>(p);
+  const size_t smem = sizeof(T) * ((size_t)7 * p.nthreads_vec * p.batch + 2 * (((size_t)p.nthreads_vec * p.nthreads_vec + 3) / 4 * 4));
+  if (energy) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(post_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    post_kernel<T, true><<<p.n_batch + 1, p.block, smem, s>>>(p);
+  } else {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(post_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    post_kernel<T, false><<<p.n_batch + 1, p.block, smem, s>>>(p);
+  }
 }
 
 template <typename T, typename M>

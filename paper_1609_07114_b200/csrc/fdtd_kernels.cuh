@@ -36,6 +36,9 @@ struct RomModelDev {
 template <typename T>
 struct PostParams {
   int n_inst;
+  int n_batch;                     // CTAs doing ROM work; batches of <= batch instances of one model
+  int batch;                       // instances per batch (multiple of 4)
+  const int32_t* batch_tab;        // per batch: (model, first instance, count)
   const int32_t* inst_model;
   const RomModelDev* models;
   const T* mpool;                  // shared model matrices (column-major)
@@ -50,8 +53,10 @@ struct PostParams {
   T* ex1; T* ey1; T* hz1;
   int n_probe; const int64_t* probe_idx; T* probe_ring; int64_t cap;
   const double* sweep_partials; int n_sweep_partials; double* rom_partials; double* energy_ring;
+  double* level1;                  // per post CTA energy partial (gridDim.x entries)
   int64_t* step; unsigned int* done;
   int nthreads_vec;  // max(nY, q1, q2) over models (smem sizing)
+  int block;         // threads per CTA
 };
 
 template <typename T>
