@@ -77,7 +77,7 @@ struct fdtd_ctx {
   std::string err;
   // device buffers (element type T)
   void* f[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};  // [buf][ex,ey,hz]
-  void* coef[4] = {nullptr, nullptr, nullptr, nullptr};
+  void* coef[2] = {nullptr, nullptr};  // per cell: mea = eps0 eps_r/(2 dt) (-1: hole/wall), msb = sigma/4
   void* mat_eps = nullptr;  // device copy of per-cell materials for rows [mrow0, row_end)
   void* mat_sig = nullptr;
   bool mat_f32 = false;
@@ -200,8 +200,7 @@ fdtd::SweepParams<T> sweep_params(fdtd_ctx* c, int q) {
   fdtd::SweepParams<T> p{};
   p.ex0 = (const T*)c->f[q][0]; p.ey0 = (const T*)c->f[q][1]; p.hz0 = (const T*)c->f[q][2];
   p.ex1 = (T*)c->f[1 - q][0]; p.ey1 = (T*)c->f[1 - q][1]; p.hz1 = (T*)c->f[1 - q][2];
-  p.cax = (const T*)c->coef[0]; p.cbx = (const T*)c->coef[1];
-  p.cay = (const T*)c->coef[2]; p.cby = (const T*)c->coef[3];
+  p.mea = (const T*)c->coef[0]; p.msb = (const T*)c->coef[1];
   p.pitch = c->pitch; p.ncolv = c->ncolv; p.rows = c->rows; p.chunk = c->chunk;
   p.chx = (T)(c->d.dt / (MU0 * c->d.dx));
   p.chy = (T)(c->d.dt / (MU0 * c->d.dy));
@@ -211,7 +210,8 @@ fdtd::SweepParams<T> sweep_params(fdtd_ctx* c, int q) {
   p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
   p.step = c->d_step;
   p.partials = c->energy_on ? c->d_partials : nullptr;
-  p.wex = (T)(c->d.dx / 2); p.wey = (T)(c->d.dy / 2);
+  p.idx = (T)(1.0 / c->d.dx); p.idy = (T)(1.0 / c->d.dy);
+  p.wxy = (T)(c->d.dx * c->d.dy);
   p.wh = (T)(MU0 * c->d.dx * c->d.dy / c->d.dt);
   return p;
 }
@@ -323,13 +323,11 @@ fdtd_status build_coefficients(fdtd_ctx* c) {
   const M* e = (const M*)c->mat_eps;
   const M* s = (const M*)c->mat_sig;
   if (c->prec == 64)
-    fdtd::launch_coefficients<double, M>(e, s, c->mrow0, c->d.nx, c->d.ny, c->d.row_begin, c->rows, c->pitch,
-                                         c->d.dx, c->d.dy, c->d.dt, (double*)c->coef[0], (double*)c->coef[1],
-                                         (double*)c->coef[2], (double*)c->coef[3], c->stream);
+    fdtd::launch_materials<double, M>(e, s, c->mrow0, c->d.nx, c->d.ny, c->d.row_begin, c->rows, c->pitch, c->d.dt,
+                                      (double*)c->coef[0], (double*)c->coef[1], c->stream);
   else
-    fdtd::launch_coefficients<float, M>(e, s, c->mrow0, c->d.nx, c->d.ny, c->d.row_begin, c->rows, c->pitch,
-                                        c->d.dx, c->d.dy, c->d.dt, (float*)c->coef[0], (float*)c->coef[1],
-                                        (float*)c->coef[2], (float*)c->coef[3], c->stream);
+    fdtd::launch_materials<float, M>(e, s, c->mrow0, c->d.nx, c->d.ny, c->d.row_begin, c->rows, c->pitch, c->d.dt,
+                                     (float*)c->coef[0], (float*)c->coef[1], c->stream);
   CK(cudaGetLastError());
   return FDTD_OK;
 }
@@ -522,7 +520,7 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
   for (int b = 0; b < 2; ++b)
     for (int a = 0; a < 3; ++a)
       if (!(c->f[b][a] = dalloc(c, fbytes))) { fdtd_destroy(c); return FDTD_E_NOMEM; }
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 2; ++a)
     if (!(c->coef[a] = dalloc(c, fbytes))) { fdtd_destroy(c); return FDTD_E_NOMEM; }
   c->d_step = (int64_t*)dalloc(c, sizeof(int64_t));
   c->d_done = (unsigned*)dalloc(c, sizeof(unsigned) * 4);
@@ -751,13 +749,11 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
   if (c->prec == 64) {
     double* fl[6] = {(double*)c->f[0][0], (double*)c->f[0][1], (double*)c->f[0][2],
                      (double*)c->f[1][0], (double*)c->f[1][1], (double*)c->f[1][2]};
-    fdtd::launch_mask<double>((double*)c->coef[0], (double*)c->coef[1], (double*)c->coef[2], (double*)c->coef[3],
-                              fl, P_, drect, count, c->d.row_begin, true, true, c->stream);
+    fdtd::launch_mask<double>((double*)c->coef[0], fl, P_, drect, count, c->d.row_begin, true, c->stream);
   } else {
     float* fl[6] = {(float*)c->f[0][0], (float*)c->f[0][1], (float*)c->f[0][2],
                     (float*)c->f[1][0], (float*)c->f[1][1], (float*)c->f[1][2]};
-    fdtd::launch_mask<float>((float*)c->coef[0], (float*)c->coef[1], (float*)c->coef[2], (float*)c->coef[3], fl,
-                             P_, drect, count, c->d.row_begin, true, true, c->stream);
+    fdtd::launch_mask<float>((float*)c->coef[0], fl, P_, drect, count, c->d.row_begin, true, c->stream);
   }
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(c->stream));
@@ -967,11 +963,11 @@ static fdtd_status window_io(fdtd_ctx* c, int64_t i0, int64_t j0, int64_t w, int
     if (c->prec == 64) {
       double* fl[6] = {(double*)c->f[q][0], (double*)c->f[q][1], (double*)c->f[q][2],
                        (double*)c->f[q][0], (double*)c->f[q][1], (double*)c->f[q][2]};
-      fdtd::launch_mask<double>(nullptr, nullptr, nullptr, nullptr, fl, c->pitch, drect, nr, rb, false, false, c->stream);
+      fdtd::launch_mask<double>(nullptr, fl, c->pitch, drect, nr, rb, false, c->stream);
     } else {
       float* fl[6] = {(float*)c->f[q][0], (float*)c->f[q][1], (float*)c->f[q][2],
                       (float*)c->f[q][0], (float*)c->f[q][1], (float*)c->f[q][2]};
-      fdtd::launch_mask<float>(nullptr, nullptr, nullptr, nullptr, fl, c->pitch, drect, nr, rb, false, false, c->stream);
+      fdtd::launch_mask<float>(nullptr, fl, c->pitch, drect, nr, rb, false, c->stream);
     }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
@@ -1058,7 +1054,7 @@ fdtd_status fdtd_get_info(const fdtd_ctx* c, fdtd_info* o) {
   o->sweep_ctas = c->n_partials;
   o->graphs = !(c->d.flags & FDTD_NO_GRAPH) && c->d.nranks == 1;
   o->precision = c->prec;
-  o->bytes_per_cell_step = 10.0 * (double)c->es;
+  o->bytes_per_cell_step = 8.0 * (double)c->es;  // read Ex, Ey, Hz, mea, msb; write Ex, Ey, Hz
   o->sweep_stream = (void*)c->stream;
   return FDTD_OK;
 }

@@ -58,6 +58,24 @@ __device__ __forceinline__ T hupd(T hz, T exn, T exc, T eyr, T eyl, T chy, T chx
   return fma_rn(-chx, eyr - eyl, fma_rn(chy, exn - exc, hz));
 }
 
+__device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
+__device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
+
+// E half-step of one edge from the two adjacent cells' material terms (eq:updateEx divided by
+// its left-hand coefficient):  E' = [(a - s) E + dH / l] / (a + s),  a = eps/dt, s = sigma/2 of
+// the edge (arithmetic means, R2), l = the dual length.  An edge next to a cell with a < 0
+// (ROM hole, PEC wall, padding) keeps its value (PEC edges stay 0; interface edges are
+// written by the ROM kernel).
+template <typename T>
+__device__ __forceinline__ T eupd(T e, T dh_over_l, T a0, T s0, T a1, T s1, bool& live, T& a) {
+  a = a0 + a1;
+  const T s = s0 + s1;
+  live = (a0 >= T(0)) & (a1 >= T(0));
+  const T r = rcp_rn(a + s);
+  const T v = mul_rn(r, fma_rn(a - s, e, dh_over_l));
+  return live ? v : e;
+}
+
 template <typename T, bool ENERGY>
 __global__ void __launch_bounds__(256) sweep_kernel(const SweepParams<T> p) {
   constexpr int V = VT<T>::N;
@@ -77,19 +95,22 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepParams<T> p) {
     if (k >= 0 && k < p.src_n) src = (T)p.src_samples[k];
   }
 
-  T exc[V], hzp[V], exn[V], eyv[V], hzv[V];
+  // carried between rows: Ex^n of edge row j, Hz^{n+1/2} of cell row j-1, materials of row j-1
+  T exc[V], hzp[V], mpa[V], mps[V], exn[V], eyv[V], hzv[V], ma[V], ms[V];
   T excl = T(0);
-  // ---- prologue: Hz^{n+1/2} of row r0-1 (recomputed; ghost row when r0 == 1)
+  // ---- prologue: row r0-1 (recomputed; the ghost row when r0 == 1)
   {
     const int64_t rj = (int64_t)(r0 - 1) * P;
     T exl[V];
 #pragma unroll
-    for (int k = 0; k < V; ++k) exl[k] = exn[k] = eyv[k] = hzv[k] = T(0);
+    for (int k = 0; k < V; ++k) exl[k] = exn[k] = eyv[k] = hzv[k] = mpa[k] = mps[k] = T(0);
     if (act) {
       ldv(p.ex0 + rj + c, exl);
       ldv(p.ex0 + rj + P + c, exn);
       ldv(p.ey0 + rj + c, eyv);
       ldv(p.hz0 + rj + c, hzv);
+      ldv(p.mea + rj + c, mpa);
+      ldv(p.msb + rj + c, mps);
     }
     T eyr = __shfl_down_sync(FULL, eyv[0], 1);
     if (lane == 31) eyr = (act && colv + 1 < p.ncolv) ? __ldg(p.ey0 + rj + c + V) : T(0);
@@ -110,23 +131,22 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepParams<T> p) {
   for (int j = r0; j < r1; ++j) {
     const int64_t rj = (int64_t)j * P;
     const int64_t rn = rj + P;
-    T ca_x[V], cb_x[V], ca_y[V], cb_y[V];
 #pragma unroll
-    for (int k = 0; k < V; ++k) exn[k] = eyv[k] = hzv[k] = ca_x[k] = cb_x[k] = ca_y[k] = cb_y[k] = T(0);
+    for (int k = 0; k < V; ++k) exn[k] = eyv[k] = hzv[k] = ma[k] = ms[k] = T(0);
     if (act) {
       ldv(p.ex0 + rn + c, exn);
       ldv(p.ey0 + rj + c, eyv);
       ldv(p.hz0 + rj + c, hzv);
-      ldv(p.cax + rj + c, ca_x);
-      ldv(p.cbx + rj + c, cb_x);
-      ldv(p.cay + rj + c, ca_y);
-      ldv(p.cby + rj + c, cb_y);
+      ldv(p.mea + rj + c, ma);
+      ldv(p.msb + rj + c, ms);
     }
-    T lhz = T(0), lexn = T(0), ley = T(0);
+    T lhz = T(0), lexn = T(0), ley = T(0), lma = T(-1), lms = T(0);
     if (lane == 0 && act && c > 0) {
       lhz = __ldg(p.hz0 + rj + c - 1);
       lexn = __ldg(p.ex0 + rn + c - 1);
       ley = __ldg(p.ey0 + rj + c - 1);
+      lma = __ldg(p.mea + rj + c - 1);
+      lms = __ldg(p.msb + rj + c - 1);
     }
     T eyr = __shfl_down_sync(FULL, eyv[0], 1);
     if (lane == 31) eyr = (act && colv + 1 < p.ncolv) ? __ldg(p.ey0 + rj + c + V) : T(0);
@@ -140,40 +160,48 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepParams<T> p) {
         if (c + k == p.src_col) hzn[k] += src;
     }
     T hl = __shfl_up_sync(FULL, hzn[V - 1], 1);
+    T la = __shfl_up_sync(FULL, ma[V - 1], 1);
+    T ls = __shfl_up_sync(FULL, ms[V - 1], 1);
     if (lane == 0) {
       if (c > 0) {
         hl = hupd(lhz, lexn, excl, eyv[0], ley, p.chy, p.chx);
         if (j == p.src_row && c - 1 == p.src_col) hl += src;
       } else {
-        hl = T(0);  // Ey column 0 is the PEC wall (cb = 0)
+        hl = T(0);  // Ey column 0 is the PEC wall (lma = -1 keeps it at 0)
       }
+      la = lma;
+      ls = lms;
       excl = lexn;
     }
     T exo[V], eyo[V];
+    T e = T(0);
 #pragma unroll
     for (int k = 0; k < V; ++k) {
-      exo[k] = fma_rn(cb_x[k], hzn[k] - hzp[k], mul_rn(ca_x[k], exc[k]));
-      eyo[k] = fma_rn(-cb_y[k], hzn[k] - (k ? hzn[k - 1] : hl), mul_rn(ca_y[k], eyv[k]));
+      bool lx, ly;
+      T ax, ay;
+      // Ex edge (row j, column c+k): cells (c+k, j-1) and (c+k, j)
+      exo[k] = eupd(exc[k], mul_rn(p.idy, hzn[k] - hzp[k]), mpa[k], mps[k], ma[k], ms[k], lx, ax);
+      // Ey edge (row j, column c+k): cells (c+k-1, j) and (c+k, j)
+      const T hleft = k ? hzn[k - 1] : hl;
+      eyo[k] = eupd(eyv[k], -mul_rn(p.idx, hzn[k] - hleft), k ? ma[k - 1] : la, k ? ms[k - 1] : ls, ma[k], ms[k],
+                    ly, ay);
+      if (ENERGY) {  // S3: (1/dt)[C E^2 + mu A H^{n-1/2} H^{n+1/2}], C/dt = dx dy a
+        e += p.wxy * ((lx ? ax * exc[k] * exc[k] : T(0)) + (ly ? ay * eyv[k] * eyv[k] : T(0)));
+        e += p.wh * hzv[k] * hzn[k];
+      }
     }
     if (act) {
       stv(p.hz1 + rj + c, hzn);
       stv(p.ex1 + rj + c, exo);
       stv(p.ey1 + rj + c, eyo);
     }
-    if (ENERGY) {  // S3: (1/dt)[C E^2 + mu A H^{n-1/2} H^{n+1/2}], C/dt = l (1 + ca) / (2 cb)
-      T e = T(0);
-#pragma unroll
-      for (int k = 0; k < V; ++k) {
-        const T wx = cb_x[k] > T(0) ? p.wex * (T(1) + ca_x[k]) / cb_x[k] : T(0);
-        const T wy = cb_y[k] > T(0) ? p.wey * (T(1) + ca_y[k]) / cb_y[k] : T(0);
-        e += wx * exc[k] * exc[k] + wy * eyv[k] * eyv[k] + p.wh * hzv[k] * hzn[k];
-      }
-      eacc += (double)e;
-    }
+    if (ENERGY) eacc += (double)e;
 #pragma unroll
     for (int k = 0; k < V; ++k) {
       exc[k] = exn[k];
       hzp[k] = hzn[k];
+      mpa[k] = ma[k];
+      mps[k] = ms[k];
     }
   }
   if (ENERGY) {
@@ -456,41 +484,21 @@ __global__ void __launch_bounds__(256) post_kernel(const PostParams<T> p) {
 
 // ---------------------------------------------------------------- setup kernels
 template <typename T, typename M>
-__global__ void coef_kernel(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t nx, int64_t ny,
-                            int64_t row_begin, int rows, int64_t pitch, double dx, double dy, double dt,
-                            T* cax, T* cbx, T* cay, T* cby) {
+__global__ void material_kernel(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t nx, int64_t ny,
+                                int64_t row_begin, int rows, int64_t pitch, double dt, T* mea, T* msb) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int jl = blockIdx.y + 1;  // local row 1..rows
+  const int jl = blockIdx.y;  // local row 0..rows (0: ghost row below)
   if (i >= pitch || jl > rows) return;
-  const int64_t g = row_begin + jl - 1;  // global cell row == global Ex edge row
+  const int64_t g = row_begin + jl - 1;
   const int64_t o = (int64_t)jl * pitch + i;
-  auto mat = [&](const M* a, int64_t gi, int64_t gj) { return (double)a[(gj - mat_row0) * nx + gi]; };
-  // Ex edge (i, g): between cells (i, g-1) and (i, g); PEC at g == 0 (row ny is never owned)
-  double a = 0.0, b = 0.0;
-  if (i < nx) {
-    if (g == 0 || g >= ny) {
-      a = 1.0; b = 0.0;
-    } else {
-      const double e = EPS0 * 0.5 * (mat(eps_r, i, g - 1) + mat(eps_r, i, g));
-      const double s = 0.5 * (mat(sigma, i, g - 1) + mat(sigma, i, g));
-      a = (e / dt - s / 2) / (e / dt + s / 2);
-      b = 1.0 / ((e / dt + s / 2) * dy);
-    }
+  if (g < 0 || g >= ny || i >= nx) {  // outside the grid: walls and padding (edges next to it stay put)
+    mea[o] = T(-1);
+    msb[o] = T(0);
+    return;
   }
-  cax[o] = (T)a;
-  cbx[o] = (T)b;
-  // Ey edge (i, g): between cells (i-1, g) and (i, g); PEC at i == 0 and i == nx
-  a = 0.0; b = 0.0;
-  if (i == 0 || i == nx) {
-    a = 1.0; b = 0.0;
-  } else if (i < nx) {
-    const double e = EPS0 * 0.5 * (mat(eps_r, i - 1, g) + mat(eps_r, i, g));
-    const double s = 0.5 * (mat(sigma, i - 1, g) + mat(sigma, i, g));
-    a = (e / dt - s / 2) / (e / dt + s / 2);
-    b = 1.0 / ((e / dt + s / 2) * dx);
-  }
-  cay[o] = (T)a;
-  cby[o] = (T)b;
+  const int64_t k = (g - mat_row0) * nx + i;
+  mea[o] = (T)(EPS0 * (double)eps_r[k] / (2.0 * dt));  // half of eps/dt: edge a = mea_a + mea_b
+  msb[o] = (T)((double)sigma[k] / 4.0);                 // quarter of sigma: edge s = sigma_edge / 2
 }
 
 template <typename M>
@@ -504,9 +512,8 @@ __global__ void gather_mat_kernel(const M* eps_r, const M* sigma, int64_t nx, in
 }
 
 template <typename T>
-__global__ void mask_kernel(T* cax, T* cbx, T* cay, T* cby, T* f0, T* f1, T* f2, T* f3, T* f4, T* f5,
-                            int64_t pitch, const int32_t* rects, int64_t row_begin, bool coefs,
-                            bool zero_iface) {
+__global__ void mask_kernel(T* mea, T* f0, T* f1, T* f2, T* f3, T* f4, T* f5, int64_t pitch, const int32_t* rects,
+                            int64_t row_begin, bool zero_iface) {
   const int32_t* r = rects + 4 * (int64_t)blockIdx.x;
   const int i0 = r[0], bx = r[2], by = r[3];
   const int64_t jl0 = (int64_t)r[1] - row_begin + 1;  // local row of the block's bottom cells
@@ -517,23 +524,21 @@ __global__ void mask_kernel(T* cax, T* cbx, T* cay, T* cby, T* f0, T* f1, T* f2,
   for (int t = threadIdx.x; t < (by + 1) * bx; t += blockDim.x) {
     const int dj = t / bx, di = t % bx;
     const int64_t o = (jl0 + dj) * pitch + i0 + di;
-    const bool iface = (dj == 0 || dj == by);
-    if (coefs) { cax[o] = T(1); cbx[o] = T(0); }
-    if (!iface || zero_iface)
+    if (!(dj == 0 || dj == by) || zero_iface)
       for (int q = 0; q < 2; ++q) ex[q][o] = T(0);
   }
   // Ey edges rows jl0 .. jl0+by-1, columns i0 .. i0+bx
   for (int t = threadIdx.x; t < by * (bx + 1); t += blockDim.x) {
     const int dj = t / (bx + 1), di = t % (bx + 1);
     const int64_t o = (jl0 + dj) * pitch + i0 + di;
-    const bool iface = (di == 0 || di == bx);
-    if (coefs) { cay[o] = T(1); cby[o] = T(0); }
-    if (!iface || zero_iface)
+    if (!(di == 0 || di == bx) || zero_iface)
       for (int q = 0; q < 2; ++q) ey[q][o] = T(0);
   }
+  // hole cells: zero fields; mark the material so every edge touching the block keeps its value
   for (int t = threadIdx.x; t < by * bx; t += blockDim.x) {
     const int64_t o = (jl0 + t / bx) * pitch + i0 + t % bx;
     for (int q = 0; q < 2; ++q) hz[q][o] = T(0);
+    if (mea) mea[o] = T(-1);
   }
 }
 
@@ -589,12 +594,10 @@ void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s) {
 }
 
 template <typename T, typename M>
-void launch_coefficients(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t nx, int64_t ny,
-                         int64_t row_begin, int rows, int64_t pitch, double dx, double dy, double dt,
-                         T* cax, T* cbx, T* cay, T* cby, cudaStream_t s) {
-  dim3 grid((unsigned)((pitch + 255) / 256), rows);
-  coef_kernel<T, M><<<grid, 256, 0, s>>>(eps_r, sigma, mat_row0, nx, ny, row_begin, rows, pitch, dx, dy,
-                                         dt, cax, cbx, cay, cby);
+void launch_materials(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t nx, int64_t ny,
+                      int64_t row_begin, int rows, int64_t pitch, double dt, T* mea, T* msb, cudaStream_t s) {
+  dim3 grid((unsigned)((pitch + 255) / 256), rows + 1);
+  material_kernel<T, M><<<grid, 256, 0, s>>>(eps_r, sigma, mat_row0, nx, ny, row_begin, rows, pitch, dt, mea, msb);
 }
 
 template <typename M>
@@ -605,24 +608,21 @@ void launch_gather_materials(const M* eps_r, const M* sigma, int64_t nx, int64_t
 }
 
 template <typename T>
-void launch_mask(T* cax, T* cbx, T* cay, T* cby, T* f[6], int64_t pitch, const int32_t* rects,
-                 int64_t n_rect, int64_t row_begin, bool coefs, bool zero_iface, cudaStream_t s) {
+void launch_mask(T* mea, T* f[6], int64_t pitch, const int32_t* rects, int64_t n_rect, int64_t row_begin,
+                 bool zero_iface, cudaStream_t s) {
   if (n_rect <= 0) return;
-  mask_kernel<T><<<(unsigned)n_rect, 256, 0, s>>>(cax, cbx, cay, cby, f[0], f[1], f[2], f[3], f[4], f[5],
-                                                   pitch, rects, row_begin, coefs, zero_iface);
+  mask_kernel<T><<<(unsigned)n_rect, 256, 0, s>>>(mea, f[0], f[1], f[2], f[3], f[4], f[5], pitch, rects, row_begin,
+                                                   zero_iface);
 }
 
 #define INST(T)                                                                                     \
   template void launch_sweep<T>(const SweepParams<T>&, int, cudaStream_t);                        \
   template void launch_post<T>(const PostParams<T>&, bool, cudaStream_t);                        \
-  template void launch_coefficients<T, float>(const float*, const float*, int64_t, int64_t, int64_t, \
-                                              int64_t, int, int64_t, double, double, double, T*, T*, \
-                                              T*, T*, cudaStream_t);                               \
-  template void launch_coefficients<T, double>(const double*, const double*, int64_t, int64_t,     \
-                                               int64_t, int64_t, int, int64_t, double, double,     \
-                                               double, T*, T*, T*, T*, cudaStream_t);              \
-  template void launch_mask<T>(T*, T*, T*, T*, T* [6], int64_t, const int32_t*, int64_t, int64_t,  \
-                               bool, bool, cudaStream_t);
+  template void launch_materials<T, float>(const float*, const float*, int64_t, int64_t, int64_t, int64_t, \
+                                           int, int64_t, double, T*, T*, cudaStream_t);                   \
+  template void launch_materials<T, double>(const double*, const double*, int64_t, int64_t, int64_t,      \
+                                            int64_t, int, int64_t, double, T*, T*, cudaStream_t);         \
+  template void launch_mask<T>(T*, T* [6], int64_t, const int32_t*, int64_t, int64_t, bool, cudaStream_t);
 INST(float)
 INST(double)
 template void launch_gather_materials<float>(const float*, const float*, int64_t, int64_t,

@@ -12,7 +12,7 @@ template <typename T>
 struct SweepParams {
   const T* ex0; const T* ey0; const T* hz0;  // fields at step n (E^n, H^{n-1/2})
   T* ex1; T* ey1; T* hz1;                     // fields at step n+1 (E^{n+1}, H^{n+1/2})
-  const T* cax; const T* cbx; const T* cay; const T* cby;  // per-edge update coefficients
+  const T* mea; const T* msb;  // per cell: eps0 eps_r / (2 dt) (< 0: hole / wall / dead) and sigma / 4
   int64_t pitch;   // elements per row (all arrays)
   int ncolv;       // vector columns processed (16-byte vectors)
   int rows;        // owned cell rows (local rows 1..rows; local row 0 is the ghost row below)
@@ -23,7 +23,8 @@ struct SweepParams {
   const double* src_samples; int64_t src_n, src_t0;
   const int64_t* step;  // device step counter (value n during step n)
   double* partials;     // energy partial per CTA (nullptr: energy off)
-  T wex, wey, wh;       // dx/2, dy/2, mu0 dx dy / dt
+  T idx, idy;           // 1/dx, 1/dy
+  T wxy, wh;            // dx dy, mu0 dx dy / dt (energy weights)
 };
 
 struct RomModelDev {
@@ -66,9 +67,8 @@ void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s);
 
 // setup kernels
 template <typename T, typename M>
-void launch_coefficients(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t nx, int64_t ny,
-                         int64_t row_begin, int rows, int64_t pitch, double dx, double dy, double dt,
-                         T* cax, T* cbx, T* cay, T* cby, cudaStream_t s);
+void launch_materials(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t nx, int64_t ny,
+                      int64_t row_begin, int rows, int64_t pitch, double dt, T* mea, T* msb, cudaStream_t s);
 template <typename M>
 void launch_gather_materials(const M* eps_r, const M* sigma, int64_t nx, int64_t mat_row0,
                              const int64_t* cells /*global j*nx+i*/, int64_t n, double* out_eps,
@@ -76,7 +76,7 @@ void launch_gather_materials(const M* eps_r, const M* sigma, int64_t nx, int64_t
 template <typename M>
 void launch_min2(const M* a, const M* b, int64_t n, double* out /*2 per block*/, int nblocks, cudaStream_t s);
 template <typename T>
-void launch_mask(T* cax, T* cbx, T* cay, T* cby, T* fields[6], int64_t pitch, const int32_t* rects,
-                 int64_t n_rect, int64_t row_begin, bool coefs, bool zero_iface, cudaStream_t s);
+void launch_mask(T* mea, T* fields[6], int64_t pitch, const int32_t* rects, int64_t n_rect, int64_t row_begin,
+                 bool zero_iface, cudaStream_t s);
 
 }  // namespace fdtd
