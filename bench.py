@@ -148,7 +148,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from inputs import configs
-    from paper_1609_07114_b200 import Simulation, nccl_unique_id
+    from paper_1609_07114_b200 import Simulation, nccl_unique_id, slabs
 
     ws, rank, lrank = dist_env()
     torch.cuda.set_device(lrank)
@@ -158,7 +158,7 @@ def run_ours(args):
     t_setup = time.perf_counter()
     scene = configs.make(wl, device="cuda")
     ny = scene.ny
-    rb, re = rank * ny // ws, (rank + 1) * ny // ws
+    rb, re = slabs.slab_rows(ny, ws, rank)
     nid = None
     if ws > 1:
         t = torch.zeros(128, dtype=torch.uint8)
@@ -175,9 +175,9 @@ def run_ours(args):
     del eps, sig
     ninst = 0
     if scene.placements is not None:
-        P = scene.placements
+        P = slabs.owned_placements(scene.placements, scene.models, rb, re)
         for k, m in enumerate(scene.models):
-            sel = P[(P[:, 0] == k) & (P[:, 2] - 1 >= rb) & (P[:, 2] + m["by"] <= re - 1)]
+            sel = P[P[:, 0] == k]
             if len(sel):
                 sim.add_rom(m, sel[:, 1:3])
                 ninst += len(sel)

@@ -57,6 +57,8 @@ typedef enum {
 #define FDTD_MATERIALS_F32 0x2u       /* eps_r / sigma are float (else double)        */
 #define FDTD_ALLOW_DT_ABOVE_EQ1 0x4u  /* skip the eq.(1) check (e.g. tests of blow-up) */
 #define FDTD_NO_GRAPH 0x8u            /* never capture CUDA graphs in fdtd_step        */
+#define FDTD_LOCAL_GROUP 0x10u        /* rank of an in-process slab group (no NCCL; see
+                                         fdtd_step_group)                               */
 
 typedef struct {
   int64_t nx, ny;          /* global coarse cells                                         */
@@ -135,6 +137,13 @@ fdtd_status fdtd_record_energy(fdtd_ctx *c, int32_t on);
  * DESIGN.md.  FDTD_E_STATE if the unread probe/energy records would exceed
  * record_capacity. */
 fdtd_status fdtd_step(fdtd_ctx *c, int64_t nsteps);
+
+/* In-process slab group (testing the decomposition on one device): contexts created with
+ * FDTD_LOCAL_GROUP, nranks = n, rank = k (k = 0..n-1, ctxs[k] has rank k), all on the same
+ * stream.  Enqueues `nsteps` steps of every slab; before each step the halo rows move by
+ * device copies following exactly the NCCL exchange plan of fdtd_step.  Probe and energy
+ * records stay per slab (the caller sums them). */
+fdtd_status fdtd_step_group(fdtd_ctx **ctxs, int32_t n, int64_t nsteps);
 
 /* Read and consume the probe records of the steps taken since the last read:
  * out[p * cap_steps + k] (row-major [n_probes][cap_steps]), k = 0 .. *n_steps-1.

@@ -204,7 +204,9 @@ fdtd::SweepParams<T> sweep_params(fdtd_ctx* c, int q) {
   p.pitch = c->pitch; p.ncolv = c->ncolv; p.rows = c->rows; p.chunk = c->chunk;
   p.chx = (T)(c->d.dt / (MU0 * c->d.dx));
   p.chy = (T)(c->d.dt / (MU0 * c->d.dy));
-  const bool src_here = c->d_src && c->src_j >= c->d.row_begin && c->src_j < c->d.row_end;
+  // the source row may also be the ghost row below: the first chunk recomputes that row's
+  // Hz^{n+1/2} and must add the source exactly as its owner does
+  const bool src_here = c->d_src && c->src_j >= c->d.row_begin - 1 && c->src_j < c->d.row_end;
   p.src_row = src_here ? (int)lrow(c, c->src_j) : -1;
   p.src_col = src_here ? c->src_i : -1;
   p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
@@ -239,23 +241,59 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
   return p;
 }
 
-fdtd_status halo_exchange(fdtd_ctx* c, int q, cudaStream_t s) {
-  if (c->d.nranks <= 1) return FDTD_OK;
-  const size_t n = (size_t)c->pitch;
-  const int dt = c->prec == 64 ? NCCL_F64 : NCCL_F32;
+// Halo plan: rank g sends its top owned row of (Ex, Ey, Hz) at step n
+// to g+1's ghost row 0, and its bottom owned Ex row to g-1's ghost Ex row rows+1.  Rows are
+// whole device rows (pitch elements).  Sends and receives are listed in the order both
+// transports pair them (per peer and direction, in list order).
+struct HaloRow { int a; int64_t row; int peer; };
+void halo_plan(const fdtd_ctx* c, std::vector<HaloRow>& sends, std::vector<HaloRow>& recvs) {
+  sends.clear();
+  recvs.clear();
   const int up = c->d.rank + 1, dn = c->d.rank - 1;
-  const size_t es = c->es;
-  auto row = [&](int a, int64_t r) { return (char*)c->f[q][a] + (size_t)r * n * es; };
-  NK(g_nccl.GroupStart());
-  if (up < c->d.nranks) {  // my top owned row (Hz, Ex, Ey) -> up's ghost row 0; up's Ex row 1 -> my row rows+1
-    for (int a = 0; a < 3; ++a) NK(g_nccl.Send(row(a, c->rows), n, dt, up, c->comm, s));
-    NK(g_nccl.Recv(row(0, c->rows + 1), n, dt, up, c->comm, s));
+  if (up < c->d.nranks) {
+    for (int a = 0; a < 3; ++a) sends.push_back({a, (int64_t)c->rows, up});
+    recvs.push_back({0, (int64_t)c->rows + 1, up});
   }
   if (dn >= 0) {
-    for (int a = 0; a < 3; ++a) NK(g_nccl.Recv(row(a, 0), n, dt, dn, c->comm, s));
-    NK(g_nccl.Send(row(0, 1), n, dt, dn, c->comm, s));
+    for (int a = 0; a < 3; ++a) recvs.push_back({a, 0, dn});
+    sends.push_back({0, 1, dn});
   }
+}
+
+inline char* dev_row(const fdtd_ctx* c, int q, int a, int64_t r) {
+  return (char*)c->f[q][a] + (size_t)r * c->pitch * c->es;
+}
+
+fdtd_status halo_exchange(fdtd_ctx* c, int q, cudaStream_t s) {
+  if (c->d.nranks <= 1 || (c->d.flags & FDTD_LOCAL_GROUP)) return FDTD_OK;
+  const size_t n = (size_t)c->pitch;
+  const int dt = c->prec == 64 ? NCCL_F64 : NCCL_F32;
+  std::vector<HaloRow> sends, recvs;
+  halo_plan(c, sends, recvs);
+  NK(g_nccl.GroupStart());
+  for (auto& x : sends) NK(g_nccl.Send(dev_row(c, q, x.a, x.row), n, dt, x.peer, c->comm, s));
+  for (auto& x : recvs) NK(g_nccl.Recv(dev_row(c, q, x.a, x.row), n, dt, x.peer, c->comm, s));
   NK(g_nccl.GroupEnd());
+  return FDTD_OK;
+}
+
+// Local transport for an in-process group: every receive pairs with the peer's sends to this
+// rank in plan order (the same pairing NCCL applies).
+fdtd_status halo_local(fdtd_ctx* const* g, int n, int k, int q, cudaStream_t s) {
+  fdtd_ctx* c = g[k];
+  std::vector<HaloRow> sends, recvs, psends, precvs;
+  halo_plan(c, sends, recvs);
+  for (int peer = 0; peer < n; ++peer) {
+    if (peer == k) continue;
+    halo_plan(g[peer], psends, precvs);
+    std::vector<HaloRow> in, out;
+    for (auto& x : recvs) if (x.peer == peer) in.push_back(x);
+    for (auto& x : psends) if (x.peer == k) out.push_back(x);
+    if (in.size() != out.size()) return fail(c, FDTD_E_STATE, "halo plans of ranks %d and %d do not pair", k, peer);
+    for (size_t i = 0; i < in.size(); ++i)
+      CK(cudaMemcpyAsync(dev_row(c, q, in[i].a, in[i].row), dev_row(g[peer], q, out[i].a, out[i].row),
+                         (size_t)c->pitch * c->es, cudaMemcpyDeviceToDevice, s));
+  }
   return FDTD_OK;
 }
 
@@ -441,7 +479,7 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
   if (nranks == 1 && rb == 0 && re == 0) re = d.ny;
   if (rb < 0 || re > d.ny || re <= rb) return FDTD_E_ARG;
   if (re - rb > (int64_t)1 << 30) return FDTD_E_ARG;
-  if (nranks > 1 && !d.nccl_id) return FDTD_E_ARG;
+  if (nranks > 1 && !d.nccl_id && !(d.flags & FDTD_LOCAL_GROUP)) return FDTD_E_ARG;
   const int64_t m0 = std::max<int64_t>(rb - 1, 0);
   if (d.materials_row0 > m0) return FDTD_E_ARG;
 
@@ -530,7 +568,7 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
   fdtd_status st = f32 ? build_coefficients<float>(c) : build_coefficients<double>(c);
   if (st != FDTD_OK) { fdtd_destroy(c); return st; }
   fdtd_set_tuning(c, 0, 0);
-  if (nranks > 1) {
+  if (nranks > 1 && !(d.flags & FDTD_LOCAL_GROUP)) {
     if (!g_nccl.load(c->err)) { fdtd_destroy(c); return FDTD_E_NCCL; }
     nccl_uid id;
     memcpy(&id, d.nccl_id, sizeof id);
@@ -823,6 +861,7 @@ fdtd_status fdtd_step(fdtd_ctx* c, int64_t nsteps) {
   if (c->energy_on) oldest = std::min(oldest, c->rd_energy);
   if (c->steps + nsteps - oldest > c->cap)
     return fail(c, FDTD_E_STATE, "unread records would exceed record_capacity (%lld)", (long long)c->cap);
+  if (c->d.flags & FDTD_LOCAL_GROUP) return fail(c, FDTD_E_STATE, "members of a local group step with fdtd_step_group");
   const bool use_graph = !(c->d.flags & FDTD_NO_GRAPH) && c->d.nranks == 1 && nsteps >= 2 && !c->profiling;
   fdtd_status st;
   int64_t left = nsteps;
@@ -865,7 +904,7 @@ static fdtd_status read_ring(fdtd_ctx* c, const void* ring, int rows_, size_t es
                          cudaMemcpyDeviceToDevice, c->stream));
     done += len;
   }
-  if (c->d.nranks > 1) NK(g_nccl.AllReduce(tmp, tmp, (size_t)rows_ * n, dtype, NCCL_SUM, c->comm, c->stream));
+  if (c->d.nranks > 1 && c->comm) NK(g_nccl.AllReduce(tmp, tmp, (size_t)rows_ * n, dtype, NCCL_SUM, c->comm, c->stream));
   CK(cudaMemcpy2DAsync(host, ldh * es, tmp, n * es, n * es, rows_, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   dfree(c, tmp);
@@ -1012,6 +1051,37 @@ fdtd_status fdtd_set_rom_state(fdtd_ctx* c, const double* in, int64_t n) {
     std::vector<float> f(v.begin(), v.end());
     CK(cudaMemcpy(c->d_state, f.data(), n * 4, cudaMemcpyHostToDevice));
   }
+  return FDTD_OK;
+}
+
+fdtd_status fdtd_step_group(fdtd_ctx** g, int32_t n, int64_t nsteps) {
+  if (!g || n < 1 || nsteps < 0) return FDTD_E_ARG;
+  for (int k = 0; k < n; ++k) {
+    fdtd_ctx* c = g[k];
+    if (!c || c->d.rank != k || c->d.nranks != n || !(c->d.flags & FDTD_LOCAL_GROUP) || c->stream != g[0]->stream ||
+        c->steps != g[0]->steps || c->prec != g[0]->prec || c->pitch != g[0]->pitch)
+      return c ? fail(c, FDTD_E_ARG, "context %d is not rank %d of a local group of %d on one stream", k, k, n)
+               : FDTD_E_ARG;
+    int64_t oldest = c->steps + nsteps;
+    if (c->n_probe > 0) oldest = std::min(oldest, c->rd_probe);
+    if (c->energy_on) oldest = std::min(oldest, c->rd_energy);
+    if (c->steps + nsteps - oldest > c->cap) return fail(c, FDTD_E_STATE, "unread records would overflow");
+  }
+  cudaStream_t s = g[0]->stream;
+  for (int64_t t = 0; t < nsteps; ++t) {
+    const int q = (int)(g[0]->steps & 1);
+    for (int k = 0; k < n; ++k) {
+      fdtd_status st = halo_local(g, n, k, q, s);
+      if (st != FDTD_OK) return st;
+    }
+    for (int k = 0; k < n; ++k) {
+      fdtd_status st = enqueue_step(g[k], q, s);
+      if (st != FDTD_OK) return st;
+      g[k]->steps++;
+    }
+  }
+  fdtd_ctx* c = g[0];
+  CK(cudaGetLastError());
   return FDTD_OK;
 }
 

@@ -19,6 +19,7 @@ FDTD_MATERIALS_ON_DEVICE = 0x1
 FDTD_MATERIALS_F32 = 0x2
 FDTD_ALLOW_DT_ABOVE_EQ1 = 0x4
 FDTD_NO_GRAPH = 0x8
+FDTD_LOCAL_GROUP = 0x10
 
 STATUS = {0: "FDTD_OK", 1: "FDTD_E_ARG", 2: "FDTD_E_STATE", 3: "FDTD_E_PASSIVITY", 4: "FDTD_E_UNSTABLE",
           5: "FDTD_E_CUDA", 6: "FDTD_E_NCCL", 7: "FDTD_E_NOMEM"}
@@ -73,6 +74,7 @@ def lib():
         L.fdtd_set_probes.argtypes = [vp, vp, i32]
         L.fdtd_record_energy.argtypes = [vp, i32]
         L.fdtd_step.argtypes = [vp, i64]
+        L.fdtd_step_group.argtypes = [C.POINTER(vp), i32, i64]
         L.fdtd_probe.argtypes = [vp, vp, i64, C.POINTER(i64)]
         L.fdtd_energy.argtypes = [vp, vp, i64, C.POINTER(i64)]
         L.fdtd_get_window.argtypes = [vp, i64, i64, i64, i64, vp, vp, vp]
@@ -92,7 +94,7 @@ def lib():
         L.fdtd_destroy.restype = None
         for n in ("create", "add_rom", "set_source", "set_probes", "record_energy", "step", "probe", "energy",
                   "get_window", "set_window", "get_rom_state", "set_rom_state", "sync", "get_info", "set_tuning",
-                  "nccl_unique_id", "profile", "profile_read"):
+                  "nccl_unique_id", "profile", "profile_read", "step_group"):
             getattr(L, "fdtd_" + n).restype = C.c_int
         _lib = L
     return _lib
@@ -126,7 +128,7 @@ class Simulation:
 
     def __init__(self, nx, ny, dx, dy, dt, eps_r, sigma, precision=32, device=0, stream=None, rank=0,
                  nranks=1, nccl_id=None, row_begin=0, row_end=None, materials_row0=0, record_capacity=0,
-                 allow_unstable=False, use_graphs=True, torch_allocator=True):
+                 allow_unstable=False, use_graphs=True, torch_allocator=True, local_group=False):
         import torch
 
         if not torch.cuda.is_available():
@@ -156,6 +158,8 @@ class Simulation:
             flags |= FDTD_ALLOW_DT_ABOVE_EQ1
         if not use_graphs:
             flags |= FDTD_NO_GRAPH
+        if local_group:
+            flags |= FDTD_LOCAL_GROUP
         d = GridDesc()
         d.nx, d.ny, d.dx, d.dy, d.dt = self.nx, self.ny, self.dx, self.dy, self.dt
         d.precision, d.flags = self.precision, flags
@@ -297,6 +301,15 @@ class Simulation:
 
     def set_tuning(self, rows_per_cta=0, warps_per_cta=0):
         self._ck(lib().fdtd_set_tuning(self._h, int(rows_per_cta), int(warps_per_cta)), "fdtd_set_tuning")
+
+
+def step_group(sims, n):
+    """Advance an in-process slab group (contexts created with local_group=True on one stream)."""
+    arr = (C.c_void_p * len(sims))(*[s._h.value for s in sims])
+    st = lib().fdtd_step_group(arr, len(sims), int(n))
+    if st:
+        msgs = [lib().fdtd_last_error(s._h).decode() for s in sims]
+        raise FDTDError(st, "fdtd_step_group: %s" % [m for m in msgs if m])
 
 
 def from_scene(scene, device=0, torch_materials=None, **kw):

@@ -1,0 +1,111 @@
+"""Row-slab decomposition on one device (-m gpu): N in-process slab contexts exchanging halo rows
+with the same plan as the NCCL path must reproduce the single-context fields bit for bit."""
+import numpy as np
+import pytest
+
+from inputs import romgen as rg
+from inputs import scene as sc
+from paper_1609_07114_b200 import slabs
+
+from helpers import consistent_random_state, gpu_from_scene, ordered_instances
+
+pytestmark = pytest.mark.gpu
+
+
+def slab_scene(precision=32):
+    nx, ny = 203, 240
+    rng = np.random.default_rng(12)
+    dx = dy = 1e-3
+    fe, fs = sc.uniform_fill(3, 2, 3, 1, 1, 4, 0, 0.05)
+    m1 = rg.build_rom(3, 2, 3, dx, dy, fe, fs, 20, 30e9)
+    fe, fs = sc.uniform_fill(2, 2, 4, 2, 1, 4, 0, 0.05)
+    m2 = rg.build_rom(2, 2, 4, dx, dy, fe, fs, 16, 30e9)
+    dt = 0.95 * min(m1["fine_dt_limit"], m2["fine_dt_limit"])
+    src = (50, 119)
+    probes = np.array([[50, 120], [50, 119], [10, 60], [150, 179], [100, 180], [5, 239]], dtype=np.int32)
+    # slab-compatible for 2, 3 and 4 slabs: footprints + rings stay inside 20-row bands
+    P = sc.place_blocks(nx, ny, [(3, 2), (2, 2)], 14, seed=5, nslabs=12,
+                        forbid=[src] + [tuple(p) for p in probes])
+    return sc.Scene(name="slabs", nx=nx, ny=ny, dx=dx, dy=dy, dt=dt, eps_r=rng.uniform(1, 4, (ny, nx)),
+                    sigma=rng.uniform(0, 0.05, (ny, nx)), precision=precision, steps=400, source=src,
+                    samples=sc.gaussian_samples(400, dt, 30e9, True), probes=probes, models=[m1, m2],
+                    placements=P)
+
+
+def run_single(s, n, init):
+    g = gpu_from_scene(s)
+    Ex, Ey, Hz, xs = init
+    g.set_window(0, 0, Ex, Ey, Hz)
+    g.set_rom_state(xs)
+    g.record_energy(True)
+    g.step(n)
+    out = g.get_window(), g.get_rom_state(), g.probe(), g.energy()
+    g.close()
+    return out
+
+
+def run_group(s, n, init, nslab):
+    import torch
+
+    from paper_1609_07114_b200 import Simulation, step_group
+
+    Ex, Ey, Hz, xs = init
+    glob = ordered_instances(s)
+    offs = np.cumsum([0] + [m["q1"] + m["q2"] for m, _, _ in glob])
+    stream = torch.cuda.Stream()
+    sims, local = [], []
+    for k in range(nslab):
+        rb, re = slabs.slab_rows(s.ny, nslab, k)
+        m0 = max(rb - 1, 0)
+        sim = Simulation(s.nx, s.ny, s.dx, s.dy, s.dt, s.eps_r[m0:re], s.sigma[m0:re], precision=s.precision,
+                         stream=stream, rank=k, nranks=nslab, row_begin=rb, row_end=re, materials_row0=m0,
+                         local_group=True)
+        mine = []
+        own = slabs.owned_placements(s.placements, s.models, rb, re)
+        for mk, m in enumerate(s.models):
+            sel = own[own[:, 0] == mk]
+            if len(sel):
+                sim.add_rom(m, sel[:, 1:3])
+                mine += [(m, int(i0), int(j0)) for _, i0, j0 in sel]
+        sim.set_source(*s.source, s.samples)
+        sim.set_probes(s.probes)
+        sim.record_energy(True)
+        sim.set_window(0, 0, Ex, Ey, Hz)
+        idx = [next(t for t, (mm, a, b) in enumerate(glob) if (a, b) == (i0, j0)) for _, i0, j0 in mine]
+        if idx:
+            sim.set_rom_state(np.concatenate([xs[offs[t]:offs[t + 1]] for t in idx]))
+        sims.append(sim)
+        local.append(idx)
+    step_group(sims, n)
+    F = [np.zeros((s.ny + 1, s.nx)), np.zeros((s.ny, s.nx + 1)), np.zeros((s.ny, s.nx))]
+    xs_out = np.zeros_like(xs)
+    pr, en = 0, 0
+    for sim, idx in zip(sims, local):
+        w = sim.get_window()
+        for a, b in zip(F, w):
+            a += b  # each row is owned by exactly one slab (other rows come back as zeros)
+        st = sim.get_rom_state()
+        o = 0
+        for t in idx:
+            q = offs[t + 1] - offs[t]
+            xs_out[offs[t]:offs[t + 1]] = st[o:o + q]
+            o += q
+        pr = pr + sim.probe()
+        en = en + sim.energy()
+        sim.close()
+    return tuple(F), xs_out, pr, en
+
+
+@pytest.mark.parametrize("nslab", [2, 3, 4])
+@pytest.mark.parametrize("precision", [32, 64])
+def test_slabs_bitwise_equal_single(nslab, precision):
+    s = slab_scene(precision)
+    assert slabs.check_partition(s.placements, s.models, s.ny, nslab)
+    init = consistent_random_state(s, 3)
+    (W1, x1, p1, e1) = run_single(s, 300, init)
+    (W2, x2, p2, e2) = run_group(s, 300, init, nslab)
+    for a, b in zip(W1, W2):
+        assert np.array_equal(a, b)
+    assert np.array_equal(x1, x2)
+    assert np.array_equal(p1, p2)
+    np.testing.assert_allclose(e2, e1, rtol=1e-12 if precision == 64 else 1e-6)
