@@ -82,3 +82,50 @@ def consistent_random_state(scene, seed, lossless_scale=1.0):
         Ey[j0:j0 + by, i0 + bx] = y[2 * bx + by:]
         xs.append(xt)
     return Ex, Ey, Hz, (np.concatenate(xs) if xs else np.zeros(0))
+
+
+# ------------------------------------------------------------------ light-cone windows
+def instance_boxes(scene):
+    """(i0-1, j0-1, i0+bx+1, j0+by+1) footprint + ring boxes (half-open), in placement order."""
+    out = []
+    if scene.placements is None:
+        return out
+    for k, i0, j0 in scene.placements:
+        m = scene.models[k]
+        out.append((int(i0) - 1, int(j0) - 1, int(i0) + m["bx"] + 1, int(j0) + m["by"] + 1))
+    return out
+
+
+def _inter(a, b):
+    return a[0] < b[2] and b[0] < a[2] and a[1] < b[3] and b[1] < a[3]
+
+
+def _union(a, b):
+    return (min(a[0], b[0]), min(a[1], b[1]), max(a[2], b[2]), max(a[3], b[3]))
+
+
+def cone_window(scene, box, nsteps, margin=3):
+    """A window (half-open cell box) that contains the backward dependency cone of `box` over
+    `nsteps` steps: one cell per half-step pair, plus a whole ROM footprint + ring whenever the
+    cone touches it (a ROM couples all its ports within one step).  Instances touching the
+    window are included whole."""
+    inst = instance_boxes(scene)
+    B = box
+    for _ in range(nsteps + 1):
+        B = (B[0] - 1, B[1] - 1, B[2] + 1, B[3] + 1)
+        changed = True
+        while changed:
+            changed = False
+            for r in inst:
+                if _inter(B, r) and _union(B, r) != B:
+                    B = _union(B, r)
+                    changed = True
+    W = (B[0] - margin, B[1] - margin, B[2] + margin, B[3] + margin)
+    changed = True
+    while changed:
+        changed = False
+        for r in inst:
+            if _inter(W, r) and _union(W, r) != W:
+                W = _union(W, r)
+                changed = True
+    return (max(W[0], 0), max(W[1], 0), min(W[2], scene.nx), min(W[3], scene.ny))

@@ -1,0 +1,133 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (-m gpu).
+
+The GPU runs the whole 8192^2 / 32768^2 grid (all ROM instances, default tuning, CUDA graphs);
+the fp64 oracle recomputes sampled outputs one window at a time: each sample box is advanced in a
+window that contains its backward dependency cone (helpers.cone_window), so the window's PEC edge
+cannot reach the samples.  Initial state: random live fields inside the windows (holes and
+interface edges zero, ROM states zero, R26), zero elsewhere; the source stays on.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from inputs import configs
+
+from helpers import cone_window, instance_boxes, rel
+
+pytestmark = pytest.mark.gpu
+NSTEPS = 16
+
+
+def _boxes(scene):
+    n = scene.nx
+    cx, cy = scene.source
+    boxes = [(cx - 16, cy - 16, cx + 16, cy + 16),          # the source
+             (0, 0, 24, 24),                                  # the south-west PEC corner
+             (n - 24, n - 24, n, n),                          # the north-east corner (last warp strip)
+             (n // 3, 2 * n // 3, n // 3 + 24, 2 * n // 3 + 24)]
+    ib = instance_boxes(scene)
+    if ib:  # a ROM instance far from the others, with some margin
+        r = ib[len(ib) // 2]
+        boxes.append((r[0] - 4, r[1] - 4, r[2] + 4, r[3] + 4))
+    return boxes
+
+
+def _random_window(rng, W, holes):
+    a0, b0, a1, b1 = W
+    w, h = a1 - a0, b1 - b0
+    Ex = rng.standard_normal((h + 1, w))
+    Ey = rng.standard_normal((h, w + 1))
+    Hz = rng.standard_normal((h, w)) / 377.0
+    return Ex, Ey, Hz
+
+
+def _zero_rom_parts(scene, W, Ex, Ey, Hz, nx, ny):
+    """Holes, interface edges and PEC walls inside window W set to zero (R26 with x~ = 0)."""
+    a0, b0 = W[0], W[1]
+    if a0 == 0:
+        Ey[:, 0] = 0
+    if W[2] == nx:
+        Ey[:, -1] = 0
+    if b0 == 0:
+        Ex[0] = 0
+    if W[3] == ny:
+        Ex[-1] = 0
+    for k, i0, j0 in (scene.placements if scene.placements is not None else []):
+        m = scene.models[k]
+        bx, by = m["bx"], m["by"]
+        if not (i0 + bx >= a0 and i0 <= W[2] and j0 + by >= b0 and j0 <= W[3]):
+            continue
+        for jj in range(j0, j0 + by + 1):        # Ex edges of the block (interface rows included)
+            for ii in range(i0, i0 + bx):
+                if 0 <= jj - b0 < Ex.shape[0] and 0 <= ii - a0 < Ex.shape[1]:
+                    Ex[jj - b0, ii - a0] = 0
+        for jj in range(j0, j0 + by):
+            for ii in range(i0, i0 + bx + 1):
+                if 0 <= jj - b0 < Ey.shape[0] and 0 <= ii - a0 < Ey.shape[1]:
+                    Ey[jj - b0, ii - a0] = 0
+            for ii in range(i0, i0 + bx):
+                if 0 <= jj - b0 < Hz.shape[0] and 0 <= ii - a0 < Hz.shape[1]:
+                    Hz[jj - b0, ii - a0] = 0
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4"])
+def test_full_size_sampled_parity(name):
+    import torch
+
+    from paper_1609_07114_b200 import Simulation
+
+    scene = configs.make(name, device="cuda")
+    sim = Simulation(scene.nx, scene.ny, scene.dx, scene.dy, scene.dt, scene.eps_r, scene.sigma,
+                     precision=scene.precision)
+    if scene.placements is not None:
+        for k, m in enumerate(scene.models):
+            sel = scene.placements[scene.placements[:, 0] == k]
+            sim.add_rom(m, sel[:, 1:3])
+    sim.set_source(*scene.source, scene.samples)
+    rng = np.random.default_rng(77)
+    boxes = _boxes(scene)
+    wins = [cone_window(scene, b, NSTEPS) for b in boxes]
+    for i in range(len(wins)):
+        for j in range(i + 1, len(wins)):
+            a, b = wins[i], wins[j]
+            assert not (a[0] < b[2] and b[0] < a[2] and a[1] < b[3] and b[1] < a[3]), "windows overlap"
+    n_rom_windows = 0
+    inits = []
+    for W in wins:
+        Ex, Ey, Hz = _random_window(rng, W, None)
+        _zero_rom_parts(scene, W, Ex, Ey, Hz, scene.nx, scene.ny)
+        sim.set_window(W[0], W[1], Ex, Ey, Hz)
+        inits.append((Ex, Ey, Hz))
+    sim.step(NSTEPS)
+    for b, W, (Ex, Ey, Hz) in zip(boxes, wins, inits):
+        a0, b0, a1, b1 = W
+        eps = scene.eps_r[b0:b1, a0:a1].double().cpu().numpy()
+        sig = scene.sigma[b0:b1, a0:a1].double().cpu().numpy()
+        o = O.OracleSim(a1 - a0, b1 - b0, scene.dx, scene.dy, scene.dt, eps, sig)
+        nrom = 0
+        for k, m in enumerate(scene.models):
+            for kk, i0, j0 in (scene.placements if scene.placements is not None else []):
+                if kk == k and a0 <= i0 - 1 and i0 + m["bx"] + 1 <= a1 and b0 <= j0 - 1 and j0 + m["by"] + 1 <= b1:
+                    o.add_rom(m, int(i0) - a0, int(j0) - b0)
+                    nrom += 1
+        n_rom_windows += nrom > 0
+        sx, sy = scene.source
+        if a0 <= sx < a1 and b0 <= sy < b1:
+            o.set_source(sx - a0, sy - b0, scene.samples)
+        o.set_state(Ex, Ey, Hz)
+        o.step(NSTEPS, probes=False, energy=False)
+        Exo, Eyo, Hzo, _ = o.get_state()
+        i0, j0, i1, j1 = max(b[0], 0), max(b[1], 0), min(b[2], scene.nx), min(b[3], scene.ny)
+        gEx, gEy, gHz = sim.get_window(i0, j0, i1 - i0, j1 - j0)
+        sl = (slice(j0 - b0, j1 - b0), slice(i0 - a0, i1 - a0))
+        e = [rel(gHz, Hzo[sl]),
+             rel(gEx, Exo[j0 - b0:j1 - b0 + 1, i0 - a0:i1 - a0]),
+             rel(gEy, Eyo[j0 - b0:j1 - b0, i0 - a0:i1 - a0 + 1])]
+        print("%s box %s window %s roms %d rel-L2 Hz/Ex/Ey %s |Hz| %.3g" % (name, b, W, nrom, e, np.linalg.norm(Hzo[sl])))
+        assert np.linalg.norm(Hzo[sl]) > 0
+        assert max(e) <= 1e-4, (name, b, W, e)
+    if scene.placements is not None:
+        assert n_rom_windows >= 1
+    sim.close()
+    del scene
+    torch.cuda.empty_cache()
