@@ -244,15 +244,21 @@ def sprim_basis(csys, q, fmax, defl_tol=1e-10):
         W.append(v / n1)
         return True
 
-    for c in range(nY):
-        if len(W) >= m:
+    # block Arnoldi: the next block is M applied to the whole previous block (one multi-RHS
+    # solve per block), then Gram-Schmidt column by column; the Krylov space is unchanged.
+    block = [X0[:, c] for c in range(nY)]
+    while len(W) < m and block:
+        nxt = []
+        for v in block:
+            if len(W) >= m:
+                break
+            if add(v):
+                nxt.append(W[-1])
+        if len(W) >= m or not nxt:
             break
-        add(X0[:, c])
-    j = 0
-    while len(W) < m and j < len(W):
-        y = solve((r11 * W[j][:nEc])[:, None], (r22 * W[j][nEc:])[:, None])[:, 0]  # M w = (G+s0C)^-1 C w
-        add(y)
-        j += 1
+        Wb = np.array(nxt).T
+        Y = solve(r11[:, None] * Wb[:nEc], r22[:, None] * Wb[nEc:])  # M w = (G+s0C)^-1 C w
+        block = [Y[:, c] for c in range(Y.shape[1])]
     Wm = np.array(W).T
     V1 = _orth(Wm[:nEc])
     V2 = _orth(Wm[nEc:])
