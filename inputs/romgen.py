@@ -229,19 +229,23 @@ def sprim_basis(csys, q, fmax, defl_tol=1e-10):
     B0[np.arange(nY), np.arange(nY)] = csys["Sc"]
     X0 = solve(B0, np.zeros((nH, nY)))
     m = (q + 1) // 2
+    Wmat = np.zeros((nEc + nH, m))
     W = []
 
     def add(v):
+        """Classical Gram-Schmidt in the C-inner product, run twice (CGS2), with deflation."""
         n0 = math.sqrt(cdot(v, v))
         if n0 == 0.0:
             return False
+        k = len(W)
         for _ in range(2):
-            for w in W:
-                v = v - cdot(w, v) * w
+            if k:
+                v = v - Wmat[:, :k] @ (Wmat[:, :k].T @ (cdiag * v))
         n1 = math.sqrt(cdot(v, v))
         if n1 <= defl_tol * n0:
             return False
-        W.append(v / n1)
+        Wmat[:, k] = v / n1
+        W.append(Wmat[:, k])
         return True
 
     # block Arnoldi: the next block is M applied to the whole previous block (one multi-RHS
@@ -259,7 +263,7 @@ def sprim_basis(csys, q, fmax, defl_tol=1e-10):
         Wb = np.array(nxt).T
         Y = solve(r11[:, None] * Wb[:nEc], r22[:, None] * Wb[nEc:])  # M w = (G+s0C)^-1 C w
         block = [Y[:, c] for c in range(Y.shape[1])]
-    Wm = np.array(W).T
+    Wm = Wmat[:, :len(W)]
     V1 = _orth(Wm[:nEc])
     V2 = _orth(Wm[nEc:])
     return V1, V2

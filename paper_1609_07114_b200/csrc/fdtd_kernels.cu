@@ -76,6 +76,12 @@ __device__ __forceinline__ T eupd(T e, T dh_over_l, T a0, T s0, T a1, T s1, bool
   return live ? v : e;
 }
 
+// Cells outside the live grid (ROM hole, ghost row below the grid, padding) keep their Hz.
+template <typename T>
+__device__ __forceinline__ T hmask(T mea_cell, T hold, T hnew) {
+  return mea_cell < T(0) ? hold : hnew;
+}
+
 template <typename T, bool ENERGY>
 __global__ void __launch_bounds__(256) sweep_kernel(const SweepParams<T> p) {
   constexpr int V = VT<T>::N;
@@ -116,7 +122,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepParams<T> p) {
     if (lane == 31) eyr = (act && colv + 1 < p.ncolv) ? __ldg(p.ey0 + rj + c + V) : T(0);
 #pragma unroll
     for (int k = 0; k < V; ++k)
-      hzp[k] = hupd(hzv[k], exn[k], exl[k], k + 1 < V ? eyv[k + 1] : eyr, eyv[k], p.chy, p.chx);
+      hzp[k] = hmask(mpa[k], hzv[k], hupd(hzv[k], exn[k], exl[k], k + 1 < V ? eyv[k + 1] : eyr, eyv[k], p.chy, p.chx));
     if (r0 - 1 == p.src_row) {
 #pragma unroll
       for (int k = 0; k < V; ++k)
@@ -153,7 +159,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepParams<T> p) {
     T hzn[V];
 #pragma unroll
     for (int k = 0; k < V; ++k)
-      hzn[k] = hupd(hzv[k], exn[k], exc[k], k + 1 < V ? eyv[k + 1] : eyr, eyv[k], p.chy, p.chx);
+      hzn[k] = hmask(ma[k], hzv[k], hupd(hzv[k], exn[k], exc[k], k + 1 < V ? eyv[k + 1] : eyr, eyv[k], p.chy, p.chx));
     if (j == p.src_row) {  // S2: soft source after the H half-step
 #pragma unroll
       for (int k = 0; k < V; ++k)
@@ -164,7 +170,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepParams<T> p) {
     T ls = __shfl_up_sync(FULL, ms[V - 1], 1);
     if (lane == 0) {
       if (c > 0) {
-        hl = hupd(lhz, lexn, excl, eyv[0], ley, p.chy, p.chx);
+        hl = hmask(lma, lhz, hupd(lhz, lexn, excl, eyv[0], ley, p.chy, p.chx));
         if (j == p.src_row && c - 1 == p.src_col) hl += src;
       } else {
         hl = T(0);  // Ey column 0 is the PEC wall (lma = -1 keeps it at 0)
@@ -214,6 +220,190 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepParams<T> p) {
       double s = 0.0;
       for (int w = 0; w < wpc; ++w) s += red[w];
       p.partials[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+    }
+  }
+}
+
+// K1b: two time steps per pass.  At row j the warp advances
+// step n on row j and step n+1 on row j-1 entirely in registers, so each field and material
+// byte crosses HBM once per two steps.  Lanes 0 and 31 are redundant halo lanes (their
+// leftmost / rightmost values may be wrong after the first step, which only they use); lanes
+// 1..30 store.  Interface edges are treated as frozen (masked) in both steps; the fix-up
+// kernel (post2) repairs the cells and edges next to every ROM instance.
+template <typename T, bool ENERGY>
+__global__ void __launch_bounds__(128) sweep2_kernel(const SweepParams<T> p) {
+  constexpr int V = VT<T>::N;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int wpc = blockDim.x >> 5;
+  const int colv = (blockIdx.x * wpc + warp) * 30 + lane - 1;
+  const bool act = colv >= 0 && colv < p.ncolv;
+  const bool out = act && lane >= 1 && lane <= 30;
+  const int64_t c = (int64_t)colv * V;
+  const int r0 = 1 + blockIdx.y * p.chunk;
+  const int r1 = min(r0 + p.chunk, p.rows + 1);
+  const int64_t P = p.pitch;
+
+  T g0 = T(0), g1 = T(0);
+  if (p.src_row >= 0) {
+    const int64_t k = *p.step - p.src_t0;
+    if (k >= 0 && k < p.src_n) g0 = (T)p.src_samples[k];
+    if (k + 1 >= 0 && k + 1 < p.src_n) g1 = (T)p.src_samples[k + 1];
+  }
+  auto load_row = [&](const T* a, int row, T (&v)[V], T fill) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) v[k] = fill;
+    if (act && row >= 0) ldv(a + (int64_t)row * P + c, v);
+  };
+
+  T exc[V], h1p[V], ma1[V], ms1[V], ma2[V], ms2[V], e1c[V], y1c[V], h2p[V];
+  // ---- prologue: step n on rows r0-2 (Hz only) and r0-1 (Hz, Ex, Ey)
+  {
+    T hA[V], exA[V], eyA[V], hB[V], exB[V], eyB[V], exC[V];
+    load_row(p.hz0, r0 - 2, hA, T(0));
+    load_row(p.ex0, r0 - 2, exA, T(0));
+    load_row(p.ey0, r0 - 2, eyA, T(0));
+    load_row(p.mea, r0 - 2, ma2, T(-1));
+    load_row(p.msb, r0 - 2, ms2, T(0));
+    load_row(p.hz0, r0 - 1, hB, T(0));
+    load_row(p.ex0, r0 - 1, exB, T(0));
+    load_row(p.ey0, r0 - 1, eyB, T(0));
+    load_row(p.mea, r0 - 1, ma1, T(-1));
+    load_row(p.msb, r0 - 1, ms1, T(0));
+    load_row(p.ex0, r0, exC, T(0));
+    T rA = __shfl_down_sync(FULL, eyA[0], 1);
+    T rB = __shfl_down_sync(FULL, eyB[0], 1);
+    T h1a[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      h1a[k] = hmask(ma2[k], hA[k], hupd(hA[k], exB[k], exA[k], k + 1 < V ? eyA[k + 1] : rA, eyA[k], p.chy, p.chx));
+      h1p[k] = hmask(ma1[k], hB[k], hupd(hB[k], exC[k], exB[k], k + 1 < V ? eyB[k + 1] : rB, eyB[k], p.chy, p.chx));
+    }
+    if (r0 - 2 == p.src_row) {
+#pragma unroll
+      for (int k = 0; k < V; ++k)
+        if (c + k == p.src_col) h1a[k] += g0;
+    }
+    if (r0 - 1 == p.src_row) {
+#pragma unroll
+      for (int k = 0; k < V; ++k)
+        if (c + k == p.src_col) h1p[k] += g0;
+    }
+    const T hl = __shfl_up_sync(FULL, h1p[V - 1], 1);
+    const T la = __shfl_up_sync(FULL, ma1[V - 1], 1);
+    const T ls = __shfl_up_sync(FULL, ms1[V - 1], 1);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      bool l;
+      T a;
+      e1c[k] = eupd(exB[k], mul_rn(p.idy, h1p[k] - h1a[k]), ma2[k], ms2[k], ma1[k], ms1[k], l, a);
+      const T left = k ? h1p[k - 1] : hl;
+      y1c[k] = eupd(eyB[k], -mul_rn(p.idx, h1p[k] - left), k ? ma1[k - 1] : la, k ? ms1[k - 1] : ls, ma1[k], ms1[k],
+                    l, a);
+      exc[k] = exC[k];
+      h2p[k] = T(0);
+    }
+  }
+
+  double eacc0 = 0.0, eacc1 = 0.0;
+  for (int j = r0; j <= r1; ++j) {
+    T exn[V], eyv[V], hzv[V], ma[V], ms[V];
+    load_row(p.ex0, j + 1, exn, T(0));
+    load_row(p.ey0, j, eyv, T(0));
+    load_row(p.hz0, j, hzv, T(0));
+    load_row(p.mea, j, ma, T(-1));
+    load_row(p.msb, j, ms, T(0));
+    // ---- step n on row j
+    const T eyr = __shfl_down_sync(FULL, eyv[0], 1);
+    T h1[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      h1[k] = hmask(ma[k], hzv[k], hupd(hzv[k], exn[k], exc[k], k + 1 < V ? eyv[k + 1] : eyr, eyv[k], p.chy, p.chx));
+    if (j == p.src_row) {
+#pragma unroll
+      for (int k = 0; k < V; ++k)
+        if (c + k == p.src_col) h1[k] += g0;
+    }
+    const T hl = __shfl_up_sync(FULL, h1[V - 1], 1);
+    const T la = __shfl_up_sync(FULL, ma[V - 1], 1);
+    const T ls = __shfl_up_sync(FULL, ms[V - 1], 1);
+    T e1[V], y1[V];
+    T en = T(0);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      bool lx, ly;
+      T ax, ay;
+      e1[k] = eupd(exc[k], mul_rn(p.idy, h1[k] - h1p[k]), ma1[k], ms1[k], ma[k], ms[k], lx, ax);
+      const T left = k ? h1[k - 1] : hl;
+      y1[k] = eupd(eyv[k], -mul_rn(p.idx, h1[k] - left), k ? ma[k - 1] : la, k ? ms[k - 1] : ls, ma[k], ms[k], ly, ay);
+      if (ENERGY) {
+        en += p.wxy * ((lx ? ax * exc[k] * exc[k] : T(0)) + (ly ? ay * eyv[k] * eyv[k] : T(0)));
+        en += p.wh * hzv[k] * h1[k];
+      }
+    }
+    if (ENERGY && out && j < r1) eacc0 += (double)en;
+    // ---- step n+1 on row j-1
+    const T y1r = __shfl_down_sync(FULL, y1c[0], 1);
+    T h2[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      h2[k] = hmask(ma1[k], h1p[k], hupd(h1p[k], e1[k], e1c[k], k + 1 < V ? y1c[k + 1] : y1r, y1c[k], p.chy, p.chx));
+    if (j - 1 == p.src_row) {
+#pragma unroll
+      for (int k = 0; k < V; ++k)
+        if (c + k == p.src_col) h2[k] += g1;
+    }
+    const T hl2 = __shfl_up_sync(FULL, h2[V - 1], 1);
+    const T la1 = __shfl_up_sync(FULL, ma1[V - 1], 1);
+    const T ls1 = __shfl_up_sync(FULL, ms1[V - 1], 1);
+    T e2[V], y2[V];
+    T en1 = T(0);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      bool lx, ly;
+      T ax, ay;
+      e2[k] = eupd(e1c[k], mul_rn(p.idy, h2[k] - h2p[k]), ma2[k], ms2[k], ma1[k], ms1[k], lx, ax);
+      const T left = k ? h2[k - 1] : hl2;
+      y2[k] = eupd(y1c[k], -mul_rn(p.idx, h2[k] - left), k ? ma1[k - 1] : la1, k ? ms1[k - 1] : ls1, ma1[k], ms1[k],
+                   ly, ay);
+      if (ENERGY) {
+        en1 += p.wxy * ((lx ? ax * e1c[k] * e1c[k] : T(0)) + (ly ? ay * y1c[k] * y1c[k] : T(0)));
+        en1 += p.wh * h1p[k] * h2[k];
+      }
+    }
+    if (out && j > r0) {
+      const int64_t rs = (int64_t)(j - 1) * P + c;
+      stv(p.hz1 + rs, h2);
+      stv(p.ex1 + rs, e2);
+      stv(p.ey1 + rs, y2);
+      if (ENERGY) eacc1 += (double)en1;
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      ma2[k] = ma1[k]; ms2[k] = ms1[k];
+      ma1[k] = ma[k]; ms1[k] = ms[k];
+      exc[k] = exn[k];
+      h2p[k] = h2[k];
+      h1p[k] = h1[k];
+      e1c[k] = e1[k];
+      y1c[k] = y1[k];
+    }
+  }
+  if (ENERGY) {
+    __shared__ double red0[32], red1[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      eacc0 += __shfl_down_sync(FULL, eacc0, o);
+      eacc1 += __shfl_down_sync(FULL, eacc1, o);
+    }
+    if (lane == 0) { red0[warp] = eacc0; red1[warp] = eacc1; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s0 = 0.0, s1 = 0.0;
+      for (int w = 0; w < wpc; ++w) { s0 += red0[w]; s1 += red1[w]; }
+      const int64_t b = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+      p.partials[b] = s0;
+      p.partials2[b] = s1;
     }
   }
 }
@@ -293,13 +483,15 @@ __device__ __forceinline__ void bgemm(const T* A, int m, int k, const T* X, T* Y
   else bgemm_ipi<T, 1>(A, m, k, X, Y, B, alpha);
 }
 
-// One CTA = one batch of up to p.batch instances of one model (K3).  The shared
-// operators of the model are streamed through two shared-memory buffers (cp.async double
+// One ROM step for a batch of nb (<= B) instances of one model (K3).  On entry sy (y^n),
+// sh (h = Hz^{n+1/2} of the outside cells), sE, sH (x~^n) hold the batch's vectors in shared
+// memory (row stride B, zero padding for b >= nb).  On exit sy holds y^{n+1} and sE, sH hold
+// x~^{n+1}; with ENERGY the ROM part of W^n (coarse half cells + x~^T R~ x~) of instance b is in
+// eout[b].  The model operators are streamed through two shared-memory buffers (cp.async double
 // buffering): while phase p computes from one buffer, the operator of phase p+1 is in flight.
 template <typename T, bool ENERGY>
-__device__ void rom_batch(const PostParams<T>& p, int bi, T* sv) {
-  const int model = p.batch_tab[3 * bi], first = p.batch_tab[3 * bi + 1], nb = p.batch_tab[3 * bi + 2];
-  const RomModelDev m = p.models[model];
+__device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first, int nb, T* sv, T* const* buf,
+                         double* eout) {
   const int nY = m.nY, q1 = m.q1, q2 = m.q2;
   const int B = p.batch, NV = p.nthreads_vec;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -311,10 +503,7 @@ __device__ void rom_batch(const PostParams<T>& p, int bi, T* sv) {
   T* sEs = sH + S;
   T* st = sEs + S;
   T* sU = st + S;
-  const int64_t NB = ((int64_t)NV * NV + 3) / 4 * 4;  // keep both buffers 16-byte aligned
-  T* buf[2] = {sU + S, sU + S + NB};
   const T* mp = p.mpool;
-  // operator sequence (pointer, rows, cols)
   const T* op[9];
   int om[9], ok[9], nop = 0;
   auto add = [&](int64_t off, int r, int c) { op[nop] = mp + off; om[nop] = r; ok[nop] = c; ++nop; };
@@ -323,8 +512,7 @@ __device__ void rom_batch(const PostParams<T>& p, int bi, T* sv) {
   add(m.off_Bq, q1, nY); add(m.off_Lt, nY, q1);
   int ph = 0;
   stage<T>(buf[0], op[0], om[0] * ok[0]);
-  // next(): start staging operator ph+1, wait for operator ph, return its buffer
-  auto next = [&]() -> const T* {
+  auto next = [&]() -> const T* {  // start staging operator ph+1, wait for operator ph
     if (ph + 1 < nop) {
       stage<T>(buf[(ph + 1) & 1], op[ph + 1], om[ph + 1] * ok[ph + 1]);
       cp_wait<1>();
@@ -335,23 +523,7 @@ __device__ void rom_batch(const PostParams<T>& p, int bi, T* sv) {
     return buf[ph & 1];
   };
   auto done = [&]() { __syncthreads(); ++ph; };
-
-  for (int64_t k = tid; k < 7 * S; k += nt) sv[k] = T(0);
-  __syncthreads();
-  // S4: gather y^n (interface edges, copied old->new by the sweep), h = Hz^{n+1/2} outside, state
-  for (int it = tid; it < nY * nb; it += nt) {
-    const int i = it % nY, b = it / nY;
-    const int64_t po = p.port_off[first + b];
-    const int64_t e = p.port_edge[po + i];
-    sy[i * B + b] = (e >> 62) ? p.ey1[e & IDX_MASK] : p.ex1[e & IDX_MASK];
-    sh[i * B + b] = p.hz1[p.port_h[po + i]];
-  }
-  for (int it = tid; it < (q1 + q2) * nb; it += nt) {
-    const int i = it % (q1 + q2), b = it / (q1 + q2);
-    const T v = p.state[p.state_off[first + b] + i];
-    if (i < q1) sE[i * B + b] = v;
-    else sH[(i - q1) * B + b] = v;
-  }
+  for (int64_t k = tid; k < 3 * S; k += nt) sEs[k] = T(0);  // sEs, st, sU
   __syncthreads();
   if (ENERGY) {  // W_rom = sum D_l D_l' eps/dt y^2 + E~^T (R~11/dt) E~ + H~^T (R~22/dt) H~ - E~^T K~ H~
     const T* A = next();
@@ -372,7 +544,7 @@ __device__ void rom_batch(const PostParams<T>& p, int bi, T* sv) {
       for (int i = lane; i < q2; i += 32) acc += (double)sH[i * B + b] * (double)st[i * B + b];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
-      if (lane == 0) p.rom_partials[first + b] = acc;
+      if (lane == 0) eout[b] = acc;
     }
     __syncthreads();
     for (int64_t k = tid; k < S; k += nt) { sEs[k] = T(0); st[k] = T(0); }
@@ -417,20 +589,76 @@ __device__ void rom_batch(const PostParams<T>& p, int bi, T* sv) {
   A = next();
   bgemm<T>(A, nY, q1, sE, sy, B, T(1));
   done();
-  // S6: scatter y^{n+1}; store the state; reset the hole-ring Hz cells (they took garbage
-  // from the interface edges in the sweep and must not enter the next energy sum)
-  for (int it = tid; it < nY * nb; it += nt) {
-    const int i = it % nY, b = it / nY;
+}
+
+template <typename T>
+__device__ __forceinline__ T* rom_buffers(const PostParams<T>& p, T* sv, T** buf) {
+  const int64_t S = (int64_t)p.nthreads_vec * p.batch;
+  const int64_t NB = ((int64_t)p.nthreads_vec * p.nthreads_vec + 3) / 4 * 4;  // 16-byte aligned
+  buf[0] = sv + 7 * S;
+  buf[1] = buf[0] + NB;
+  return buf[1] + NB;  // first free element after the ROM area
+}
+
+template <typename T>
+__device__ void load_rom_state(const PostParams<T>& p, const RomModelDev& m, int first, int nb, T* sv) {
+  const int B = p.batch;
+  const int64_t S = (int64_t)p.nthreads_vec * B;
+  T* sE = sv + 2 * S;
+  T* sH = sv + 3 * S;
+  for (int it = threadIdx.x; it < (m.q1 + m.q2) * nb; it += blockDim.x) {
+    const int i = it % (m.q1 + m.q2), b = it / (m.q1 + m.q2);
+    const T v = p.state[p.state_off[first + b] + i];
+    if (i < m.q1) sE[i * B + b] = v;
+    else sH[(i - m.q1) * B + b] = v;
+  }
+}
+
+template <typename T>
+__device__ void store_rom(const PostParams<T>& p, const RomModelDev& m, int first, int nb, const T* sv, T* ex,
+                          T* ey) {
+  const int B = p.batch;
+  const int64_t S = (int64_t)p.nthreads_vec * B;
+  const T* sy = sv;
+  const T* sE = sv + 2 * S;
+  const T* sH = sv + 3 * S;
+  for (int it = threadIdx.x; it < m.nY * nb; it += blockDim.x) {  // S6: scatter y^{n+1}
+    const int i = it % m.nY, b = it / m.nY;
     const int64_t e = p.port_edge[p.port_off[first + b] + i];
-    if (e >> 62) p.ey1[e & IDX_MASK] = sy[i * B + b];
-    else p.ex1[e & IDX_MASK] = sy[i * B + b];
+    if (e >> 62) ey[e & IDX_MASK] = sy[i * B + b];
+    else ex[e & IDX_MASK] = sy[i * B + b];
   }
-  for (int it = tid; it < (q1 + q2) * nb; it += nt) {
-    const int i = it % (q1 + q2), b = it / (q1 + q2);
-    p.state[p.state_off[first + b] + i] = i < q1 ? sE[i * B + b] : sH[(i - q1) * B + b];
+  for (int it = threadIdx.x; it < (m.q1 + m.q2) * nb; it += blockDim.x) {
+    const int i = it % (m.q1 + m.q2), b = it / (m.q1 + m.q2);
+    p.state[p.state_off[first + b] + i] = i < m.q1 ? sE[i * B + b] : sH[(i - m.q1) * B + b];
   }
-  for (int b = 0; b < nb; ++b)
-    for (int64_t k = p.ring_off[first + b] + tid; k < p.ring_off[first + b + 1]; k += nt) p.hz1[p.ring_idx[k]] = T(0);
+}
+
+// One-step post kernel body for one batch: gather, ROM step, scatter.
+template <typename T, bool ENERGY>
+__device__ void rom_batch(const PostParams<T>& p, int bi, T* sv) {
+  const int model = p.batch_tab[3 * bi], first = p.batch_tab[3 * bi + 1], nb = p.batch_tab[3 * bi + 2];
+  const RomModelDev m = p.models[model];
+  const int B = p.batch;
+  const int64_t S = (int64_t)p.nthreads_vec * B;
+  T* buf[2];
+  rom_buffers(p, sv, buf);
+  for (int64_t k = threadIdx.x; k < 7 * S; k += blockDim.x) sv[k] = T(0);
+  __syncthreads();
+  T* sy = sv;
+  T* sh = sv + S;
+  // S4: gather y^n (interface edges, copied old->new by the sweep), h = Hz^{n+1/2} outside, state
+  for (int it = threadIdx.x; it < m.nY * nb; it += blockDim.x) {
+    const int i = it % m.nY, b = it / m.nY;
+    const int64_t po = p.port_off[first + b];
+    const int64_t e = p.port_edge[po + i];
+    sy[i * B + b] = (e >> 62) ? p.ey1[e & IDX_MASK] : p.ex1[e & IDX_MASK];
+    sh[i * B + b] = p.hz1[p.port_h[po + i]];
+  }
+  load_rom_state(p, m, first, nb, sv);
+  __syncthreads();
+  rom_step<T, ENERGY>(p, m, first, nb, sv, buf, p.rom_partials + first);
+  store_rom(p, m, first, nb, sv, p.ex1, p.ey1);
 }
 
 template <typename T, bool ENERGY>
@@ -582,6 +810,13 @@ void launch_sweep(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s) {
 }
 
 template <typename T>
+void launch_sweep2(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s) {
+  dim3 grid(sweep2_ctas_x(p.ncolv, warps_per_cta), (p.rows + p.chunk - 1) / p.chunk);
+  if (p.partials) sweep2_kernel<T, true><<<grid, 32 * warps_per_cta, 0, s>>>(p);
+  else sweep2_kernel<T, false><<<grid, 32 * warps_per_cta, 0, s>>>(p);
+}
+
+template <typename T>
 void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s) {
   const size_t smem = sizeof(T) * ((size_t)7 * p.nthreads_vec * p.batch + 2 * (((size_t)p.nthreads_vec * p.nthreads_vec + 3) / 4 * 4));
   if (energy) {
@@ -617,6 +852,7 @@ void launch_mask(T* mea, T* f[6], int64_t pitch, const int32_t* rects, int64_t n
 
 #define INST(T)                                                                                     \
   template void launch_sweep<T>(const SweepParams<T>&, int, cudaStream_t);                        \
+  template void launch_sweep2<T>(const SweepParams<T>&, int, cudaStream_t);                       \
   template void launch_post<T>(const PostParams<T>&, bool, cudaStream_t);                        \
   template void launch_materials<T, float>(const float*, const float*, int64_t, int64_t, int64_t, int64_t, \
                                            int, int64_t, double, T*, T*, cudaStream_t);                   \

@@ -23,6 +23,7 @@ struct SweepParams {
   const double* src_samples; int64_t src_n, src_t0;
   const int64_t* step;  // device step counter (value n during step n)
   double* partials;     // energy partial per CTA (nullptr: energy off)
+  double* partials2;    // two-step sweep: partials of the second step
   T idx, idy;           // 1/dx, 1/dy
   T wxy, wh;            // dx dy, mu0 dx dy / dt (energy weights)
 };
@@ -62,6 +63,13 @@ struct PostParams {
 
 template <typename T>
 void launch_sweep(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s);
+// two time steps per pass (temporal blocking; 30 output lanes per warp)
+template <typename T>
+void launch_sweep2(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s);
+inline int sweep2_ctas_x(int ncolv, int warps_per_cta) {
+  const int nw = (ncolv + 29) / 30;
+  return (nw + warps_per_cta - 1) / warps_per_cta;
+}
 template <typename T>
 void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s);
 
