@@ -183,7 +183,8 @@ typedef struct {
   int64_t sweep_ctas;          /* CTAs of one fused-sweep launch                           */
   int32_t graphs;              /* 1 if fdtd_step replays CUDA graphs                       */
   int32_t precision;
-  double bytes_per_cell_step;  /* algorithmic bytes of the fused sweep per cell-step        */
+  double bytes_per_cell_step;  /* HBM bytes of the sweep per cell-step as implemented       */
+  int32_t steps_per_pass;      /* 2 when the two-step (temporally blocked) sweep is active  */
   void *sweep_stream;          /* cudaStream_t the kernels are launched on                 */
 } fdtd_info;
 fdtd_status fdtd_get_info(const fdtd_ctx *c, fdtd_info *out);
@@ -194,6 +195,13 @@ fdtd_status fdtd_get_info(const fdtd_ctx *c, fdtd_info *out);
  * last read. */
 fdtd_status fdtd_profile(fdtd_ctx *c, int32_t on);
 fdtd_status fdtd_profile_read(fdtd_ctx *c, double *sweep_ms, double *post_ms, int64_t *n_launches);
+
+/* Time steps per sweep pass: 1, or 2 (default; temporal blocking with a per-instance fix-up,
+ * DESIGN.md K1b/K3b).  Two-step mode is used only on one rank and when every ROM instance's
+ * [i0-2, i0+bx+2) x [j0-2, j0+by+2) region is inside the grid and free of other instances'
+ * outside cells; otherwise fdtd_step silently runs one step per pass.  Results are
+ * bit-identical either way. */
+fdtd_status fdtd_set_time_blocking(fdtd_ctx *c, int32_t steps_per_pass);
 
 /* Tuning knobs for the fused sweep (rows per CTA, warps per CTA); 0 keeps default. */
 fdtd_status fdtd_set_tuning(fdtd_ctx *c, int32_t rows_per_cta, int32_t warps_per_cta);

@@ -71,7 +71,7 @@ struct fdtd_ctx {
   size_t es = 4;  // element size
   int V = 4;      // elements per 16-byte vector
   int rows = 0;   // owned rows
-  int64_t nrows_alloc = 0, pitch = 0;
+  int64_t nrows_alloc = 0, pitch = 0;  // rows + 3: ghost row below, two ghost rows above
   int ncolv = 0;
   cudaStream_t stream = nullptr, cap_stream = nullptr;
   std::string err;
@@ -85,7 +85,9 @@ struct fdtd_ctx {
   int64_t* d_step = nullptr;
   unsigned* d_done = nullptr;
   double* d_partials = nullptr;
+  double* d_partials2 = nullptr;
   double* d_level1 = nullptr;
+  double* d_level1b = nullptr;
   int n_partials = 0;
   int chunk = 64, warps = 4;
   // source
@@ -99,6 +101,12 @@ struct fdtd_ctx {
   double* d_energy_ring = nullptr;
   bool energy_on = false;
   int64_t steps = 0, rd_probe = 0, rd_energy = 0;
+  int cur = 0;  // buffer holding the current state (E^n, H^{n-1/2})
+  // two-step mode (sweep2 + post2): wanted by the user (default on) and valid for the placements
+  bool tb2_want = true, tb2_ok = true;
+  int region_stride = 4;
+  int32_t* d_rects = nullptr;
+  double* d_rom_partials2 = nullptr;
   // ROMs
   std::vector<ModelHost> models;
   std::vector<int32_t> inst_model, rects;  // rects: (i0, j0, bx, by) global
@@ -120,9 +128,11 @@ struct fdtd_ctx {
   // graphs
   cudaGraphExec_t gexec = nullptr;
   bool graph_dirty = true;
+  int graph_steps = 2;
   int64_t launches = 0;
   // profiling (event pairs around each launch)
   bool profiling = false;
+  int64_t prof_pairs = 0;  // two-step launches among the profiled ones
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
   // multi-rank
@@ -212,6 +222,7 @@ fdtd::SweepParams<T> sweep_params(fdtd_ctx* c, int q) {
   p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
   p.step = c->d_step;
   p.partials = c->energy_on ? c->d_partials : nullptr;
+  p.partials2 = c->energy_on ? c->d_partials2 : nullptr;
   p.idx = (T)(1.0 / c->d.dx); p.idy = (T)(1.0 / c->d.dy);
   p.wxy = (T)(c->d.dx * c->d.dy);
   p.wh = (T)(MU0 * c->d.dx * c->d.dy / c->d.dt);
@@ -219,7 +230,7 @@ fdtd::SweepParams<T> sweep_params(fdtd_ctx* c, int q) {
 }
 
 template <typename T>
-fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
+fdtd::PostParams<T> post_params(fdtd_ctx* c, int q, bool pair = false) {
   fdtd::PostParams<T> p{};
   p.n_inst = (int)c->inst_model.size();
   p.inst_model = c->d_inst_model; p.models = c->d_models; p.mpool = (const T*)c->d_mpool;
@@ -229,7 +240,12 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
   p.state = (T*)c->d_state; p.state_off = c->d_state_off;
   p.ex1 = (T*)c->f[1 - q][0]; p.ey1 = (T*)c->f[1 - q][1]; p.hz1 = (T*)c->f[1 - q][2];
   p.n_probe = c->n_probe; p.probe_idx = c->d_probe_idx; p.probe_ring = (T*)c->d_probe_ring; p.cap = c->cap;
-  p.sweep_partials = c->d_partials; p.n_sweep_partials = c->n_partials;
+  {  // exactly the partials the matching sweep launch wrote
+    const int per_cta = 32 * c->warps;
+    const int gx = pair ? fdtd::sweep2_ctas_x(c->ncolv, c->warps) : (c->ncolv + per_cta - 1) / per_cta;
+    p.sweep_partials = c->d_partials;
+    p.n_sweep_partials = gx * ((c->rows + c->chunk - 1) / c->chunk);
+  }
   p.rom_partials = c->d_rom_partials; p.energy_ring = c->d_energy_ring;
   p.step = c->d_step; p.done = c->d_done;
   p.nthreads_vec = c->nvec;
@@ -238,6 +254,23 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
   p.batch_tab = c->d_batch_tab;
   p.block = 256;
   p.level1 = c->d_level1;
+  p.level1b = c->d_level1b;
+  p.rects = c->d_rects;
+  p.row_begin = c->d.row_begin;
+  p.pitch = c->pitch;
+  p.ex0 = (const T*)c->f[q][0]; p.ey0 = (const T*)c->f[q][1]; p.hz0 = (const T*)c->f[q][2];
+  p.mea = (const T*)c->coef[0]; p.msb = (const T*)c->coef[1];
+  p.chx = (T)(c->d.dt / (MU0 * c->d.dx));
+  p.chy = (T)(c->d.dt / (MU0 * c->d.dy));
+  p.idx = (T)(1.0 / c->d.dx); p.idy = (T)(1.0 / c->d.dy);
+  p.wh = (T)(MU0 * c->d.dx * c->d.dy / c->d.dt);
+  const bool src_here = c->d_src && c->src_j >= c->d.row_begin && c->src_j < c->d.row_end;
+  p.src_row = src_here ? (int)lrow(c, c->src_j) : -1;
+  p.src_col = src_here ? c->src_i : -1;
+  p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
+  p.sweep_partials2 = c->d_partials2;
+  p.rom_partials2 = c->d_rom_partials2;
+  p.region_stride = c->region_stride;
   return p;
 }
 
@@ -325,20 +358,44 @@ fdtd_status enqueue_step(fdtd_ctx* c, int q, cudaStream_t s) {
   return FDTD_OK;
 }
 
+bool tb2_active(const fdtd_ctx* c) { return c->tb2_want && c->tb2_ok && c->d.nranks == 1; }
+
+// two steps in one pass: sweep2 (q -> 1-q) then the ROM fix-up / probes / energy of both steps
+fdtd_status enqueue_pair(fdtd_ctx* c, int q, cudaStream_t s) {
+  const bool prof = c->profiling && s == c->stream;
+  cudaEvent_t e[3];
+  if (prof) {
+    for (auto& x : e) x = next_event(c);
+    CK(cudaEventRecord(e[0], s));
+  }
+  if (c->prec == 64) fdtd::launch_sweep2<double>(sweep_params<double>(c, q), c->warps, s);
+  else fdtd::launch_sweep2<float>(sweep_params<float>(c, q), c->warps, s);
+  if (prof) CK(cudaEventRecord(e[1], s));
+  if (c->prec == 64) fdtd::launch_post2<double>(post_params<double>(c, q, true), c->energy_on, s);
+  else fdtd::launch_post2<float>(post_params<float>(c, q, true), c->energy_on, s);
+  if (prof) CK(cudaEventRecord(e[2], s));
+  c->launches += 2;
+  c->prof_pairs += prof ? 1 : 0;
+  return FDTD_OK;
+}
+
 void drop_graph(fdtd_ctx* c) {
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   c->gexec = nullptr;
   c->graph_dirty = true;
 }
 
+// Captures one "period" starting from buffer 0: two single steps (0 -> 1 -> 0) or, in two-step
+// mode, two pairs (4 steps, 0 -> 1 -> 0).
 fdtd_status build_graph(fdtd_ctx* c) {
   drop_graph(c);
   if (!c->cap_stream) CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
   const int64_t before = c->launches;
-  fdtd_status st = enqueue_step(c, 0, c->cap_stream);
-  if (st == FDTD_OK) st = enqueue_step(c, 1, c->cap_stream);
+  const bool pairs = tb2_active(c);
+  fdtd_status st = pairs ? enqueue_pair(c, 0, c->cap_stream) : enqueue_step(c, 0, c->cap_stream);
+  if (st == FDTD_OK) st = pairs ? enqueue_pair(c, 1, c->cap_stream) : enqueue_step(c, 1, c->cap_stream);
   c->launches = before;
   cudaError_t e = cudaStreamEndCapture(c->cap_stream, &g);
   if (st != FDTD_OK) return st;
@@ -346,6 +403,7 @@ fdtd_status build_graph(fdtd_ctx* c) {
   e = cudaGraphInstantiate(&c->gexec, g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return fail(c, FDTD_E_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  c->graph_steps = pairs ? 4 : 2;
   c->graph_dirty = false;
   return FDTD_OK;
 }
@@ -361,10 +419,10 @@ fdtd_status build_coefficients(fdtd_ctx* c) {
   const M* e = (const M*)c->mat_eps;
   const M* s = (const M*)c->mat_sig;
   if (c->prec == 64)
-    fdtd::launch_materials<double, M>(e, s, c->mrow0, c->d.nx, c->d.ny, c->d.row_begin, c->rows, c->pitch, c->d.dt,
+    fdtd::launch_materials<double, M>(e, s, c->mrow0, c->d.row_end, c->d.nx, c->d.ny, c->d.row_begin, c->rows, c->pitch, c->d.dt,
                                       (double*)c->coef[0], (double*)c->coef[1], c->stream);
   else
-    fdtd::launch_materials<float, M>(e, s, c->mrow0, c->d.nx, c->d.ny, c->d.row_begin, c->rows, c->pitch, c->d.dt,
+    fdtd::launch_materials<float, M>(e, s, c->mrow0, c->d.row_end, c->d.nx, c->d.ny, c->d.row_begin, c->rows, c->pitch, c->d.dt,
                                      (float*)c->coef[0], (float*)c->coef[1], c->stream);
   CK(cudaGetLastError());
   return FDTD_OK;
@@ -405,12 +463,53 @@ fdtd_status upload_roms(fdtd_ctx* c) {
   if ((st = upload_T(c, &c->d_mpool, c->mpool)) != FDTD_OK) return st;
   if ((st = upload(c, &c->d_models, md)) != FDTD_OK) return st;
   if ((st = upload(c, &c->d_inst_model, c->inst_model)) != FDTD_OK) return st;
-  // batches of consecutive instances of one model (instances are stored grouped by model)
+  // two-step mode needs, per instance, the region [i0-2, i0+bx+2) x [j0-2, j0+by+2) inside the grid,
+  // and no other instance's outside cells inside that region (K3b)
+  {
+    c->region_stride = 4;
+    for (auto& m : c->models) {
+      const int Wr = m.bx + 4, Hr = m.by + 4;
+      int rs = 4 * Hr * Wr + (Hr + 1) * Wr + Hr * (Wr + 1);
+      c->region_stride = std::max(c->region_stride, (rs + 3) / 4 * 4);
+    }
+    bool ok = true;
+    struct Rc { int64_t i0, j0, bx, by; };
+    std::vector<Rc> all;
+    for (size_t r = 0; r < c->rects.size(); r += 4) {
+      Rc x{c->rects[r], c->rects[r + 1], c->rects[r + 2], c->rects[r + 3]};
+      if (x.i0 - 2 < 0 || x.j0 - 2 < 0 || x.i0 + x.bx + 2 > c->d.nx || x.j0 + x.by + 2 > c->d.ny ||
+          x.j0 - 2 < c->d.row_begin || x.j0 + x.by + 2 > c->d.row_end)
+        ok = false;
+      all.push_back(x);
+    }
+    std::sort(all.begin(), all.end(), [](const Rc& a, const Rc& b) { return a.i0 < b.i0; });
+    int64_t wmax = 0;
+    for (auto& r : all) wmax = std::max(wmax, r.bx);
+    for (size_t a = 0; ok && a < all.size(); ++a)
+      for (size_t b = a + 1; ok && b < all.size() && all[b].i0 <= all[a].i0 + all[a].bx + wmax + 4; ++b) {
+        const Rc &A = all[a], &Bq = all[b];
+        auto hit = [](const Rc& X, const Rc& Y) {  // region of X vs ring box of Y
+          return X.i0 - 2 <= Y.i0 + Y.bx && Y.i0 - 1 <= X.i0 + X.bx + 1 && X.j0 - 2 <= Y.j0 + Y.by &&
+                 Y.j0 - 1 <= X.j0 + X.by + 1;
+        };
+        if (hit(A, Bq) || hit(Bq, A)) ok = false;
+      }
+    c->tb2_ok = ok;
+  }
+  // batches of consecutive instances of one model (instances are stored grouped by model); the
+  // batch size keeps the two-step fix-up kernel at <= ~110 KB of shared memory when possible
   {
     const char* env = getenv("FDTD_ROM_BATCH");
-    int B = env ? atoi(env) : 8;
-    B = std::max(4, std::min(64, (B + 3) / 4 * 4));
-    while (B > 4 && ((size_t)7 * c->nvec * B + 2 * (size_t)c->nvec * c->nvec) * c->es > 200 * 1024) B -= 4;
+    int B = env ? std::max(1, std::min(64, atoi(env))) : 8;
+    auto fits = [&](int b, size_t lim) {
+      return fdtd::post2_smem_bytes(c->es, c->nvec, b, c->region_stride) <= lim &&
+             fdtd::post_smem_bytes(c->es, c->nvec, b) <= lim;
+    };
+    while (B > 1 && !fits(B, 110 * 1024)) B = B > 4 ? B - 4 : B / 2;
+    if (!fits(B, 110 * 1024)) {
+      while (B > 1 && !fits(B, 220 * 1024)) B /= 2;
+      if (!fits(B, 220 * 1024)) c->tb2_ok = false;
+    }
     c->rom_batch = B;
     c->batch_tab.clear();
     const int n = (int)c->inst_model.size();
@@ -423,6 +522,8 @@ fdtd_status upload_roms(fdtd_ctx* c) {
     if ((st = upload(c, &c->d_batch_tab, c->batch_tab)) != FDTD_OK) return st;
     std::vector<double> l1(c->batch_tab.size() / 3 + 1, 0.0);
     if ((st = upload(c, &c->d_level1, l1)) != FDTD_OK) return st;
+    if ((st = upload(c, &c->d_level1b, l1)) != FDTD_OK) return st;
+    if ((st = upload(c, &c->d_rects, c->rects)) != FDTD_OK) return st;
   }
   if ((st = upload_T(c, &c->d_Sk, c->Sk)) != FDTD_OK) return st;
   if ((st = upload(c, &c->d_Sk_off, c->Sk_off)) != FDTD_OK) return st;
@@ -443,6 +544,7 @@ fdtd_status upload_roms(fdtd_ctx* c) {
   if (prev) dfree(c, prev);
   std::vector<double> zp(c->inst_model.size() + 1, 0.0);
   if ((st = upload(c, &c->d_rom_partials, zp)) != FDTD_OK) return st;
+  if ((st = upload(c, &c->d_rom_partials2, zp)) != FDTD_OK) return st;
   return FDTD_OK;
 }
 
@@ -492,7 +594,7 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
   c->es = d.precision == 64 ? 8 : 4;
   c->V = 16 / (int)c->es;
   c->rows = (int)(re - rb);
-  c->nrows_alloc = c->rows + 2;
+  c->nrows_alloc = c->rows + 3;
   c->ncolv = (int)((d.nx + c->V - 1) / c->V);
   const int64_t align = 128 / (int64_t)c->es;
   c->pitch = ((int64_t)c->ncolv * c->V + align - 1) / align * align;
@@ -564,6 +666,8 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
   c->d_done = (unsigned*)dalloc(c, sizeof(unsigned) * 4);
   c->d_energy_ring = (double*)dalloc(c, c->cap * sizeof(double));
   c->d_level1 = (double*)dalloc(c, 16 * sizeof(double));
+  c->d_level1b = (double*)dalloc(c, 16 * sizeof(double));
+  if (const char* e = getenv("FDTD_TB2")) c->tb2_want = atoi(e) != 0;
   if (!c->d_step || !c->d_done || !c->d_energy_ring) { fdtd_destroy(c); return FDTD_E_NOMEM; }
   fdtd_status st = f32 ? build_coefficients<float>(c) : build_coefficients<double>(c);
   if (st != FDTD_OK) { fdtd_destroy(c); return st; }
@@ -585,13 +689,15 @@ fdtd_status fdtd_set_tuning(fdtd_ctx* c, int32_t rows_per_cta, int32_t warps_per
   c->chunk = rows_per_cta ? rows_per_cta : (c->rows >= 4096 ? 64 : 32);
   c->warps = warps_per_cta ? warps_per_cta : 4;
   const int per_cta = 32 * c->warps;
-  const int gx = (c->ncolv + per_cta - 1) / per_cta;
+  const int gx = std::max((c->ncolv + per_cta - 1) / per_cta, fdtd::sweep2_ctas_x(c->ncolv, c->warps));
   const int gy = (c->rows + c->chunk - 1) / c->chunk;
   const int n = gx * gy;
-  if (n != c->n_partials) {
+  if (n > c->n_partials) {
     if (c->d_partials) dfree(c, c->d_partials);
+    if (c->d_partials2) dfree(c, c->d_partials2);
     c->d_partials = (double*)dalloc(c, (size_t)n * sizeof(double));
-    if (!c->d_partials) return fail(c, FDTD_E_NOMEM, "partials");
+    c->d_partials2 = (double*)dalloc(c, (size_t)n * sizeof(double));
+    if (!c->d_partials || !c->d_partials2) return fail(c, FDTD_E_NOMEM, "partials");
     c->n_partials = n;
   }
   drop_graph(c);
@@ -862,28 +968,31 @@ fdtd_status fdtd_step(fdtd_ctx* c, int64_t nsteps) {
   if (c->steps + nsteps - oldest > c->cap)
     return fail(c, FDTD_E_STATE, "unread records would exceed record_capacity (%lld)", (long long)c->cap);
   if (c->d.flags & FDTD_LOCAL_GROUP) return fail(c, FDTD_E_STATE, "members of a local group step with fdtd_step_group");
-  const bool use_graph = !(c->d.flags & FDTD_NO_GRAPH) && c->d.nranks == 1 && nsteps >= 2 && !c->profiling;
+  const bool use_graph = !(c->d.flags & FDTD_NO_GRAPH) && c->d.nranks == 1 && !c->profiling;
+  const bool pairs = tb2_active(c);
   fdtd_status st;
   int64_t left = nsteps;
-  if (use_graph) {
-    if (c->steps & 1) {  // realign to even parity
-      if ((st = enqueue_step(c, 1, c->stream)) != FDTD_OK) return st;
-      c->steps++;
-      left--;
-    }
-    if (left >= 2 && (c->graph_dirty || !c->gexec))
-      if ((st = build_graph(c)) != FDTD_OK) return st;
-    while (left >= 2) {
+  while (left > 0) {
+    const int per = pairs ? 4 : 2;
+    if (use_graph && c->cur == 0 && left >= per) {
+      if (c->graph_dirty || !c->gexec || c->graph_steps != per)
+        if ((st = build_graph(c)) != FDTD_OK) return st;
       CK(cudaGraphLaunch(c->gexec, c->stream));
-      c->launches += 4;
+      c->launches += 4;  // two sweep + two post launches per graph period
+      c->steps += per;
+      left -= per;
+      continue;
+    }
+    if (pairs && left >= 2) {
+      if ((st = enqueue_pair(c, c->cur, c->stream)) != FDTD_OK) return st;
       c->steps += 2;
       left -= 2;
+    } else {
+      if ((st = enqueue_step(c, c->cur, c->stream)) != FDTD_OK) return st;
+      c->steps += 1;
+      left -= 1;
     }
-  }
-  while (left > 0) {
-    if ((st = enqueue_step(c, (int)(c->steps & 1), c->stream)) != FDTD_OK) return st;
-    c->steps++;
-    left--;
+    c->cur ^= 1;
   }
   CK(cudaGetLastError());
   return FDTD_OK;
@@ -953,7 +1062,7 @@ static fdtd_status window_io(fdtd_ctx* c, int64_t i0, int64_t j0, int64_t w, int
     return fail(c, FDTD_E_ARG, "bad window");
   fdtd_status st = check_async(c);
   if (st != FDTD_OK) return st;
-  const int q = (int)(c->steps & 1);
+  const int q = c->cur;
   const int64_t rb = c->d.row_begin, re = c->d.row_end;
   const size_t es = c->es;
   // arrays: (ptr, ncols, global row range [g0, g1), device array, row range owned, col limit stored)
@@ -1059,7 +1168,7 @@ fdtd_status fdtd_step_group(fdtd_ctx** g, int32_t n, int64_t nsteps) {
   for (int k = 0; k < n; ++k) {
     fdtd_ctx* c = g[k];
     if (!c || c->d.rank != k || c->d.nranks != n || !(c->d.flags & FDTD_LOCAL_GROUP) || c->stream != g[0]->stream ||
-        c->steps != g[0]->steps || c->prec != g[0]->prec || c->pitch != g[0]->pitch)
+        c->steps != g[0]->steps || c->cur != g[0]->cur || c->prec != g[0]->prec || c->pitch != g[0]->pitch)
       return c ? fail(c, FDTD_E_ARG, "context %d is not rank %d of a local group of %d on one stream", k, k, n)
                : FDTD_E_ARG;
     int64_t oldest = c->steps + nsteps;
@@ -1069,7 +1178,7 @@ fdtd_status fdtd_step_group(fdtd_ctx** g, int32_t n, int64_t nsteps) {
   }
   cudaStream_t s = g[0]->stream;
   for (int64_t t = 0; t < nsteps; ++t) {
-    const int q = (int)(g[0]->steps & 1);
+    const int q = g[0]->cur;
     for (int k = 0; k < n; ++k) {
       fdtd_status st = halo_local(g, n, k, q, s);
       if (st != FDTD_OK) return st;
@@ -1078,6 +1187,7 @@ fdtd_status fdtd_step_group(fdtd_ctx** g, int32_t n, int64_t nsteps) {
       fdtd_status st = enqueue_step(g[k], q, s);
       if (st != FDTD_OK) return st;
       g[k]->steps++;
+      g[k]->cur ^= 1;
     }
   }
   fdtd_ctx* c = g[0];
@@ -1085,10 +1195,18 @@ fdtd_status fdtd_step_group(fdtd_ctx** g, int32_t n, int64_t nsteps) {
   return FDTD_OK;
 }
 
+fdtd_status fdtd_set_time_blocking(fdtd_ctx* c, int32_t steps_per_pass) {
+  if (!c || (steps_per_pass != 1 && steps_per_pass != 2)) return FDTD_E_ARG;
+  c->tb2_want = steps_per_pass == 2;
+  drop_graph(c);
+  return FDTD_OK;
+}
+
 fdtd_status fdtd_profile(fdtd_ctx* c, int32_t on) {
   if (!c) return FDTD_E_ARG;
   c->profiling = on != 0;
   c->ev_used = 0;
+  c->prof_pairs = 0;
   return FDTD_OK;
 }
 
@@ -1107,6 +1225,7 @@ fdtd_status fdtd_profile_read(fdtd_ctx* c, double* sweep_ms, double* post_ms, in
   *post_ms = b;
   *n = (int64_t)(c->ev_used / 3);
   c->ev_used = 0;
+  c->prof_pairs = 0;
   return FDTD_OK;
 }
 
@@ -1124,7 +1243,9 @@ fdtd_status fdtd_get_info(const fdtd_ctx* c, fdtd_info* o) {
   o->sweep_ctas = c->n_partials;
   o->graphs = !(c->d.flags & FDTD_NO_GRAPH) && c->d.nranks == 1;
   o->precision = c->prec;
-  o->bytes_per_cell_step = 8.0 * (double)c->es;  // read Ex, Ey, Hz, mea, msb; write Ex, Ey, Hz
+  o->steps_per_pass = tb2_active(c) ? 2 : 1;
+  // read Ex, Ey, Hz, mea, msb and write Ex, Ey, Hz once per pass
+  o->bytes_per_cell_step = 8.0 * (double)c->es / o->steps_per_pass;
   o->sweep_stream = (void*)c->stream;
   return FDTD_OK;
 }

@@ -58,7 +58,13 @@ __device__ __forceinline__ T hupd(T hz, T exn, T exc, T eyr, T eyl, T chy, T chx
   return fma_rn(-chx, eyr - eyl, fma_rn(chy, exn - exc, hz));
 }
 
-__device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
+// Reciprocal of an edge's (eps/dt + sigma/2): fp32 uses the single-instruction MUFU
+// approximation (max relative error ~2^-23, deterministic); fp64 the correctly rounded one.
+__device__ __forceinline__ float rcp_rn(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
 
 // E half-step of one edge from the two adjacent cells' material terms (eq:updateEx divided by
@@ -231,7 +237,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepParams<T> p) {
 // 1..30 store.  Interface edges are treated as frozen (masked) in both steps; the fix-up
 // kernel (post2) repairs the cells and edges next to every ROM instance.
 template <typename T, bool ENERGY>
-__global__ void __launch_bounds__(128) sweep2_kernel(const SweepParams<T> p) {
+__global__ void __launch_bounds__(256) sweep2_kernel(const SweepParams<T> p) {
   constexpr int V = VT<T>::N;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -306,13 +312,26 @@ __global__ void __launch_bounds__(128) sweep2_kernel(const SweepParams<T> p) {
   }
 
   double eacc0 = 0.0, eacc1 = 0.0;
+  // software pipeline: the loads of row j+1 are in flight while row j computes
+  T nexn[V], neyv[V], nhzv[V], nma[V], nms[V];
+  load_row(p.ex0, r0 + 1, nexn, T(0));
+  load_row(p.ey0, r0, neyv, T(0));
+  load_row(p.hz0, r0, nhzv, T(0));
+  load_row(p.mea, r0, nma, T(-1));
+  load_row(p.msb, r0, nms, T(0));
   for (int j = r0; j <= r1; ++j) {
     T exn[V], eyv[V], hzv[V], ma[V], ms[V];
-    load_row(p.ex0, j + 1, exn, T(0));
-    load_row(p.ey0, j, eyv, T(0));
-    load_row(p.hz0, j, hzv, T(0));
-    load_row(p.mea, j, ma, T(-1));
-    load_row(p.msb, j, ms, T(0));
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      exn[k] = nexn[k]; eyv[k] = neyv[k]; hzv[k] = nhzv[k]; ma[k] = nma[k]; ms[k] = nms[k];
+    }
+    if (j < r1) {
+      load_row(p.ex0, j + 2, nexn, T(0));
+      load_row(p.ey0, j + 1, neyv, T(0));
+      load_row(p.hz0, j + 1, nhzv, T(0));
+      load_row(p.mea, j + 1, nma, T(-1));
+      load_row(p.msb, j + 1, nms, T(0));
+    }
     // ---- step n on row j
     const T eyr = __shfl_down_sync(FULL, eyv[0], 1);
     T h1[V];
@@ -661,6 +680,306 @@ __device__ void rom_batch(const PostParams<T>& p, int bi, T* sv) {
   store_rom(p, m, first, nb, sv, p.ex1, p.ey1);
 }
 
+// Two-step fix-up for one batch (K3b).  sweep2 advanced every cell two steps with the
+// interface edges frozen at y^n; here, per instance, step n is recomputed in the region
+// [i0-2, i0+bx+2) x [j0-2, j0+by+2) from the input buffer (bit-identical to the sweep's own
+// arithmetic), the ROM takes step n (y^{n+1}), the outside cells' Hz^{n+3/2} and their
+// non-interface edges' E^{n+2} are recomputed with the correct y^{n+1}, the ROM takes step n+1
+// (y^{n+2}), and the corrected values are written over the sweep's output.  The energy of
+// step n+1 is corrected by mu A/dt H^{n+1/2} (H_correct - H_sweep) on the outside cells.
+template <typename T, bool ENERGY>
+__device__ void rom_batch2(const PostParams<T>& p, int bi, T* sv, T g0, T g1, double* sdelta) {
+  const int model = p.batch_tab[3 * bi], first = p.batch_tab[3 * bi + 1], nb = p.batch_tab[3 * bi + 2];
+  const RomModelDev m = p.models[model];
+  const int B = p.batch, nY = m.nY;
+  const int64_t S = (int64_t)p.nthreads_vec * B;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  T* buf[2];
+  T* reg = rom_buffers(p, sv, buf);
+  const int64_t P = p.pitch;
+  for (int64_t k = tid; k < 7 * S; k += nt) sv[k] = T(0);
+  if (tid < B) sdelta[tid] = 0.0;  // B <= 64
+  T* sy = sv;
+  T* sh = sv + S;
+  // region geometry of slot b
+  auto geo = [&](int b, int& i0, int& j0, int& bx, int& by) {
+    const int32_t* r = p.rects + 4 * (int64_t)(first + b);
+    i0 = r[0]; j0 = r[1]; bx = r[2]; by = r[3];
+  };
+  // layout of one region: H1, H2, MA, MS [Hr][Wr]; EX [Hr+1][Wr]; EY [Hr][Wr+1]
+  auto arrays = [&](int b, int bx, int by, T*& H1, T*& H2, T*& MA, T*& MS, T*& EX, T*& EY) {
+    const int Wr = bx + 4, Hr = by + 4;
+    H1 = reg + (int64_t)b * p.region_stride;
+    H2 = H1 + Hr * Wr;
+    MA = H2 + Hr * Wr;
+    MS = MA + Hr * Wr;
+    EX = MS + Hr * Wr;
+    EY = EX + (Hr + 1) * Wr;
+  };
+  auto goff = [&](int gi, int gj) { return ((int64_t)gj - p.row_begin + 1) * P + gi; };
+  const bool src_on = p.src_row >= 0;
+  const int64_t src_off = src_on ? (int64_t)p.src_row * P + p.src_col : -1;
+  // ---- R1: load the region (materials, E^n, the sweep's Hz^{n+3/2} into H2)
+  for (int b = 0; b < nb; ++b) {
+    int i0, j0, bx, by;
+    geo(b, i0, j0, bx, by);
+    T *H1, *H2, *MA, *MS, *EX, *EY;
+    arrays(b, bx, by, H1, H2, MA, MS, EX, EY);
+    const int Wr = bx + 4, Hr = by + 4;
+    for (int t = tid; t < Hr * Wr; t += nt) {
+      const int u = t % Wr, v = t / Wr;
+      const int64_t o = goff(i0 - 2 + u, j0 - 2 + v);
+      MA[t] = p.mea[o];
+      MS[t] = p.msb[o];
+      H2[t] = p.hz1[o];
+    }
+    for (int t = tid; t < (Hr + 1) * Wr; t += nt) EX[t] = p.ex0[goff(i0 - 2 + t % Wr, j0 - 2 + t / Wr)];
+    for (int t = tid; t < Hr * (Wr + 1); t += nt) EY[t] = p.ey0[goff(i0 - 2 + t % (Wr + 1), j0 - 2 + t / (Wr + 1))];
+  }
+  load_rom_state(p, m, first, nb, sv);
+  __syncthreads();
+  // ---- R2: Hz^{n+1/2} on the region (same arithmetic as the sweep)
+  for (int b = 0; b < nb; ++b) {
+    int i0, j0, bx, by;
+    geo(b, i0, j0, bx, by);
+    T *H1, *H2, *MA, *MS, *EX, *EY;
+    arrays(b, bx, by, H1, H2, MA, MS, EX, EY);
+    const int Wr = bx + 4, Hr = by + 4;
+    for (int t = tid; t < Hr * Wr; t += nt) {
+      const int u = t % Wr, v = t / Wr;
+      const int64_t o = goff(i0 - 2 + u, j0 - 2 + v);
+      const T hz = p.hz0[o];
+      T h = hmask(MA[t], hz, hupd(hz, EX[(v + 1) * Wr + u], EX[v * Wr + u], EY[v * (Wr + 1) + u + 1],
+                                  EY[v * (Wr + 1) + u], p.chy, p.chx));
+      if (o == src_off) h += g0;
+      H1[t] = h;
+    }
+  }
+  __syncthreads();
+  // ---- R3: E^{n+1} on the region's interior edges (in place); gather y^n and h^{n+1/2}
+  for (int b = 0; b < nb; ++b) {
+    int i0, j0, bx, by;
+    geo(b, i0, j0, bx, by);
+    T *H1, *H2, *MA, *MS, *EX, *EY;
+    arrays(b, bx, by, H1, H2, MA, MS, EX, EY);
+    const int Wr = bx + 4, Hr = by + 4;
+    bool l;
+    T a;
+    for (int t = tid; t < (Hr - 1) * Wr; t += nt) {  // Ex edge rows v = 1 .. Hr-1
+      const int u = t % Wr, v = t / Wr + 1;
+      const int cb = v * Wr + u, ca = cb - Wr;
+      EX[v * Wr + u] = eupd(EX[v * Wr + u], mul_rn(p.idy, H1[cb] - H1[ca]), MA[ca], MS[ca], MA[cb], MS[cb], l, a);
+    }
+    for (int t = tid; t < Hr * (Wr - 1); t += nt) {  // Ey edge columns u = 1 .. Wr-1
+      const int u = t % (Wr - 1) + 1, v = t / (Wr - 1);
+      const int cb = v * Wr + u, ca = cb - 1;
+      EY[v * (Wr + 1) + u] =
+          eupd(EY[v * (Wr + 1) + u], -mul_rn(p.idx, H1[cb] - H1[ca]), MA[ca], MS[ca], MA[cb], MS[cb], l, a);
+    }
+    for (int i = tid; i < nY; i += nt) {
+      int eidx, hidx;  // interface edge (EX or EY index) and outside cell, region coordinates
+      bool isy;
+      if (i < bx) { isy = false; eidx = 2 * Wr + 2 + i; hidx = 1 * Wr + 2 + i; }
+      else if (i < 2 * bx) { isy = false; eidx = (2 + by) * Wr + 2 + (i - bx); hidx = (2 + by) * Wr + 2 + (i - bx); }
+      else if (i < 2 * bx + by) { isy = true; eidx = (2 + i - 2 * bx) * (Wr + 1) + 2; hidx = (2 + i - 2 * bx) * Wr + 1; }
+      else { isy = true; eidx = (2 + i - 2 * bx - by) * (Wr + 1) + 2 + bx; hidx = (2 + i - 2 * bx - by) * Wr + 2 + bx; }
+      sy[i * B + b] = isy ? EY[eidx] : EX[eidx];  // y^n (interface edges are frozen copies)
+      sh[i * B + b] = H1[hidx];
+    }
+  }
+  __syncthreads();
+  // ---- ROM step n: y^{n+1}, x~^{n+1}; ROM energy of W^n
+  rom_step<T, ENERGY>(p, m, first, nb, sv, buf, p.rom_partials + first);
+  // ---- R4: y^{n+1} into the interface edges; Hz^{n+3/2} of the outside cells
+  for (int b = 0; b < nb; ++b) {
+    int i0, j0, bx, by;
+    geo(b, i0, j0, bx, by);
+    T *H1, *H2, *MA, *MS, *EX, *EY;
+    arrays(b, bx, by, H1, H2, MA, MS, EX, EY);
+    const int Wr = bx + 4;
+    for (int i = tid; i < nY; i += nt) {
+      if (i < bx) EX[2 * Wr + 2 + i] = sy[i * B + b];
+      else if (i < 2 * bx) EX[(2 + by) * Wr + 2 + (i - bx)] = sy[i * B + b];
+      else if (i < 2 * bx + by) EY[(2 + i - 2 * bx) * (Wr + 1) + 2] = sy[i * B + b];
+      else EY[(2 + i - 2 * bx - by) * (Wr + 1) + 2 + bx] = sy[i * B + b];
+    }
+  }
+  __syncthreads();
+  auto port_cell = [&](int i, int bx, int by, int& u, int& v) {  // outside cell of port i
+    if (i < bx) { u = 2 + i; v = 1; }
+    else if (i < 2 * bx) { u = 2 + i - bx; v = 2 + by; }
+    else if (i < 2 * bx + by) { u = 1; v = 2 + i - 2 * bx; }
+    else { u = 2 + bx; v = 2 + i - 2 * bx - by; }
+  };
+  for (int b = 0; b < nb; ++b) {  // corrected Hz^{n+3/2} of the outside cells -> sh
+    int i0, j0, bx, by;
+    geo(b, i0, j0, bx, by);
+    T *H1, *H2, *MA, *MS, *EX, *EY;
+    arrays(b, bx, by, H1, H2, MA, MS, EX, EY);
+    const int Wr = bx + 4;
+    for (int i = tid; i < nY; i += nt) {
+      int u, v;
+      port_cell(i, bx, by, u, v);
+      const int t = v * Wr + u;
+      T h = hmask(MA[t], H1[t], hupd(H1[t], EX[(v + 1) * Wr + u], EX[v * Wr + u], EY[v * (Wr + 1) + u + 1],
+                                     EY[v * (Wr + 1) + u], p.chy, p.chx));
+      if (goff(i0 - 2 + u, j0 - 2 + v) == src_off) h += g1;
+      sh[i * B + b] = h;
+    }
+  }
+  __syncthreads();
+  {  // energy correction of W^{n+1} (fixed order: one warp per instance), then H2 <- corrected
+    const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+    for (int b = w; b < nb; b += nw) {
+      int i0, j0, bx, by;
+      geo(b, i0, j0, bx, by);
+      T *H1, *H2, *MA, *MS, *EX, *EY;
+      arrays(b, bx, by, H1, H2, MA, MS, EX, EY);
+      double d = 0.0;
+      for (int i = lane; i < nY; i += 32) {
+        int u, v;
+        port_cell(i, bx, by, u, v);
+        const int t = v * (bx + 4) + u;
+        d += (double)(p.wh * H1[t] * sh[i * B + b]) - (double)(p.wh * H1[t] * H2[t]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_down_sync(FULL, d, o);
+      if (lane == 0) sdelta[b] = d;
+    }
+  }
+  __syncthreads();
+  for (int b = 0; b < nb; ++b) {
+    int i0, j0, bx, by;
+    geo(b, i0, j0, bx, by);
+    T *H1, *H2, *MA, *MS, *EX, *EY;
+    arrays(b, bx, by, H1, H2, MA, MS, EX, EY);
+    for (int i = tid; i < nY; i += nt) {
+      int u, v;
+      port_cell(i, bx, by, u, v);
+      H2[v * (bx + 4) + u] = sh[i * B + b];
+    }
+  }
+  __syncthreads();
+  // ---- ROM step n+1: y^{n+2}, x~^{n+2}; ROM energy of W^{n+1}
+  rom_step<T, ENERGY>(p, m, first, nb, sv, buf, p.rom_partials2 + first);
+  // ---- R5: E^{n+2} of the outside cells' non-interface edges, the outside cells' Hz, y^{n+2}
+  for (int b = 0; b < nb; ++b) {
+    int i0, j0, bx, by;
+    geo(b, i0, j0, bx, by);
+    T *H1, *H2, *MA, *MS, *EX, *EY;
+    arrays(b, bx, by, H1, H2, MA, MS, EX, EY);
+    const int Wr = bx + 4, Hr = by + 4;
+    auto hole = [&](int u, int v) { return u >= 2 && u < 2 + bx && v >= 2 && v < 2 + by; };
+    auto outside = [&](int u, int v) {
+      return ((v == 1 || v == 2 + by) && u >= 2 && u < 2 + bx) || ((u == 1 || u == 2 + bx) && v >= 2 && v < 2 + by);
+    };
+    bool l;
+    T a;
+    for (int t = tid; t < (Hr - 1) * Wr; t += nt) {
+      const int u = t % Wr, v = t / Wr + 1;
+      if (!(outside(u, v - 1) || outside(u, v)) || hole(u, v - 1) || hole(u, v)) continue;
+      const int cb = v * Wr + u, ca = cb - Wr;
+      p.ex1[goff(i0 - 2 + u, j0 - 2 + v)] =
+          eupd(EX[v * Wr + u], mul_rn(p.idy, H2[cb] - H2[ca]), MA[ca], MS[ca], MA[cb], MS[cb], l, a);
+    }
+    for (int t = tid; t < Hr * (Wr - 1); t += nt) {
+      const int u = t % (Wr - 1) + 1, v = t / (Wr - 1);
+      if (!(outside(u - 1, v) || outside(u, v)) || hole(u - 1, v) || hole(u, v)) continue;
+      const int cb = v * Wr + u, ca = cb - 1;
+      p.ey1[goff(i0 - 2 + u, j0 - 2 + v)] =
+          eupd(EY[v * (Wr + 1) + u], -mul_rn(p.idx, H2[cb] - H2[ca]), MA[ca], MS[ca], MA[cb], MS[cb], l, a);
+    }
+    for (int i = tid; i < nY; i += nt) {
+      int u, v;
+      port_cell(i, bx, by, u, v);
+      p.hz1[goff(i0 - 2 + u, j0 - 2 + v)] = H2[v * Wr + u];
+    }
+  }
+  store_rom(p, m, first, nb, sv, p.ex1, p.ey1);
+  __syncthreads();
+  if (ENERGY && tid < nb) p.rom_partials2[first + tid] += sdelta[tid];
+}
+
+template <typename T, bool ENERGY>
+__global__ void __launch_bounds__(256) post2_kernel(const PostParams<T> p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[32];
+  __shared__ double sdelta[64];
+  __shared__ bool last;
+  T* sv = reinterpret_cast<T*>(smem_raw);
+  const int b = blockIdx.x;
+  const int64_t step = *p.step;
+  T g0 = T(0), g1 = T(0);
+  if (p.src_row >= 0) {
+    const int64_t k = step - p.src_t0;
+    if (k >= 0 && k < p.src_n) g0 = (T)p.src_samples[k];
+    if (k + 1 >= 0 && k + 1 < p.src_n) g1 = (T)p.src_samples[k + 1];
+  }
+  if (b < p.n_batch) {
+    rom_batch2<T, ENERGY>(p, b, sv, g0, g1, sdelta);
+  } else {  // probes: Hz^{n+1/2} recomputed from the input buffer, Hz^{n+3/2} from the output
+    const int64_t P = p.pitch;
+    const int64_t src_off = p.src_row >= 0 ? (int64_t)p.src_row * P + p.src_col : -1;
+    for (int k = threadIdx.x; k < p.n_probe; k += blockDim.x) {
+      const int64_t o = p.probe_idx[k];
+      const T hz = p.hz0[o];
+      T h = hmask(p.mea[o], hz, hupd(hz, p.ex0[o + P], p.ex0[o], p.ey0[o + 1], p.ey0[o], p.chy, p.chx));
+      if (o == src_off) h += g0;
+      p.probe_ring[(int64_t)k * p.cap + step % p.cap] = h;
+      p.probe_ring[(int64_t)k * p.cap + (step + 1) % p.cap] = p.hz1[o];
+    }
+  }
+  if (ENERGY) {
+    const int per = (p.n_sweep_partials + gridDim.x - 1) / gridDim.x;
+    const int k0 = b * per, k1 = min(p.n_sweep_partials, k0 + per);
+    double v0 = 0.0, v1 = 0.0;
+    for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+      v0 += __ldcg(p.sweep_partials + k);
+      v1 += __ldcg(p.sweep_partials2 + k);
+    }
+    __syncthreads();
+    if (b < p.n_batch) {
+      const int first = p.batch_tab[3 * b + 1], nb = p.batch_tab[3 * b + 2];
+      for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+        v0 += p.rom_partials[first + k];
+        v1 += p.rom_partials2[first + k];
+      }
+    }
+    const double t0 = block_sum(v0, red);
+    const double t1 = block_sum(v1, red);
+    if (threadIdx.x == 0) {
+      p.level1[b] = t0;
+      p.level1b[b] = t1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(p.done, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (ENERGY) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) {
+      s0 += __ldcg(p.level1 + k);
+      s1 += __ldcg(p.level1b + k);
+    }
+    const double t0 = block_sum(s0, red);
+    const double t1 = block_sum(s1, red);
+    if (threadIdx.x == 0) {
+      p.energy_ring[step % p.cap] = t0;
+      p.energy_ring[(step + 1) % p.cap] = t1;
+    }
+  }
+  if (threadIdx.x == 0) {
+    *p.done = 0u;
+    *p.step = step + 2;
+  }
+}
+
 template <typename T, bool ENERGY>
 __global__ void __launch_bounds__(256) post_kernel(const PostParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -712,15 +1031,15 @@ __global__ void __launch_bounds__(256) post_kernel(const PostParams<T> p) {
 
 // ---------------------------------------------------------------- setup kernels
 template <typename T, typename M>
-__global__ void material_kernel(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t nx, int64_t ny,
-                                int64_t row_begin, int rows, int64_t pitch, double dt, T* mea, T* msb) {
+__global__ void material_kernel(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t mat_row_end, int64_t nx,
+                                int64_t ny, int64_t row_begin, int rows, int64_t pitch, double dt, T* mea, T* msb) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int jl = blockIdx.y;  // local row 0..rows (0: ghost row below)
-  if (i >= pitch || jl > rows) return;
+  const int jl = blockIdx.y;  // local row 0..rows+1 (0: ghost row below, rows+1: ghost row above)
+  if (i >= pitch || jl > rows + 1) return;
   const int64_t g = row_begin + jl - 1;
   const int64_t o = (int64_t)jl * pitch + i;
-  if (g < 0 || g >= ny || i >= nx) {  // outside the grid: walls and padding (edges next to it stay put)
-    mea[o] = T(-1);
+  if (g < 0 || g >= ny || i >= nx || g < mat_row0 || g >= mat_row_end) {
+    mea[o] = T(-1);  // outside the grid / not provided: walls and padding (edges next to it stay put)
     msb[o] = T(0);
     return;
   }
@@ -816,9 +1135,28 @@ void launch_sweep2(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s) {
   else sweep2_kernel<T, false><<<grid, 32 * warps_per_cta, 0, s>>>(p);
 }
 
+size_t post_smem_bytes(size_t es, int nvec, int batch) {
+  return es * ((size_t)7 * nvec * batch + 2 * (((size_t)nvec * nvec + 3) / 4 * 4));
+}
+size_t post2_smem_bytes(size_t es, int nvec, int batch, int region_stride) {
+  return post_smem_bytes(es, nvec, batch) + es * (size_t)batch * region_stride;
+}
+
+template <typename T>
+void launch_post2(const PostParams<T>& p, bool energy, cudaStream_t s) {
+  const size_t smem = post2_smem_bytes(sizeof(T), p.nthreads_vec, p.batch, p.region_stride);
+  if (energy) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(post2_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    post2_kernel<T, true><<<p.n_batch + 1, p.block, smem, s>>>(p);
+  } else {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(post2_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    post2_kernel<T, false><<<p.n_batch + 1, p.block, smem, s>>>(p);
+  }
+}
+
 template <typename T>
 void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s) {
-  const size_t smem = sizeof(T) * ((size_t)7 * p.nthreads_vec * p.batch + 2 * (((size_t)p.nthreads_vec * p.nthreads_vec + 3) / 4 * 4));
+  const size_t smem = post_smem_bytes(sizeof(T), p.nthreads_vec, p.batch);
   if (energy) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(post_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     post_kernel<T, true><<<p.n_batch + 1, p.block, smem, s>>>(p);
@@ -829,10 +1167,11 @@ void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s) {
 }
 
 template <typename T, typename M>
-void launch_materials(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t nx, int64_t ny,
+void launch_materials(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t mat_row_end, int64_t nx, int64_t ny,
                       int64_t row_begin, int rows, int64_t pitch, double dt, T* mea, T* msb, cudaStream_t s) {
-  dim3 grid((unsigned)((pitch + 255) / 256), rows + 1);
-  material_kernel<T, M><<<grid, 256, 0, s>>>(eps_r, sigma, mat_row0, nx, ny, row_begin, rows, pitch, dt, mea, msb);
+  dim3 grid((unsigned)((pitch + 255) / 256), rows + 2);
+  material_kernel<T, M><<<grid, 256, 0, s>>>(eps_r, sigma, mat_row0, mat_row_end, nx, ny, row_begin, rows, pitch, dt,
+                                             mea, msb);
 }
 
 template <typename M>
@@ -854,10 +1193,11 @@ void launch_mask(T* mea, T* f[6], int64_t pitch, const int32_t* rects, int64_t n
   template void launch_sweep<T>(const SweepParams<T>&, int, cudaStream_t);                        \
   template void launch_sweep2<T>(const SweepParams<T>&, int, cudaStream_t);                       \
   template void launch_post<T>(const PostParams<T>&, bool, cudaStream_t);                        \
+  template void launch_post2<T>(const PostParams<T>&, bool, cudaStream_t);                       \
   template void launch_materials<T, float>(const float*, const float*, int64_t, int64_t, int64_t, int64_t, \
-                                           int, int64_t, double, T*, T*, cudaStream_t);                   \
+                                           int64_t, int, int64_t, double, T*, T*, cudaStream_t);          \
   template void launch_materials<T, double>(const double*, const double*, int64_t, int64_t, int64_t,      \
-                                            int64_t, int, int64_t, double, T*, T*, cudaStream_t);         \
+                                            int64_t, int64_t, int, int64_t, double, T*, T*, cudaStream_t);\
   template void launch_mask<T>(T*, T* [6], int64_t, const int32_t*, int64_t, int64_t, bool, cudaStream_t);
 INST(float)
 INST(double)

@@ -59,6 +59,15 @@ struct PostParams {
   int64_t* step; unsigned int* done;
   int nthreads_vec;  // max(nY, q1, q2) over models (smem sizing)
   int block;         // threads per CTA
+  // ---- two-step mode (post2): fix-up around every instance after sweep2 (K3b)
+  const int32_t* rects;            // per instance (i0, j0, bx, by), global
+  int64_t row_begin, pitch;
+  const T* ex0; const T* ey0; const T* hz0;  // fields at step n (the sweep's input buffer)
+  const T* mea; const T* msb;
+  T chx, chy, idx, idy, wh;
+  int src_row; int64_t src_col; const double* src_samples; int64_t src_n, src_t0;
+  const double* sweep_partials2; double* rom_partials2; double* level1b;
+  int region_stride;               // shared-memory elements per instance region
 };
 
 template <typename T>
@@ -72,10 +81,15 @@ inline int sweep2_ctas_x(int ncolv, int warps_per_cta) {
 }
 template <typename T>
 void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s);
+template <typename T>
+void launch_post2(const PostParams<T>& p, bool energy, cudaStream_t s);
+// shared-memory bytes of the two kernels for a given batch (host-side sizing)
+size_t post_smem_bytes(size_t es, int nvec, int batch);
+size_t post2_smem_bytes(size_t es, int nvec, int batch, int region_stride);
 
 // setup kernels
 template <typename T, typename M>
-void launch_materials(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t nx, int64_t ny,
+void launch_materials(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t mat_row_end, int64_t nx, int64_t ny,
                       int64_t row_begin, int rows, int64_t pitch, double dt, T* mea, T* msb, cudaStream_t s);
 template <typename M>
 void launch_gather_materials(const M* eps_r, const M* sigma, int64_t nx, int64_t mat_row0,

@@ -47,7 +47,8 @@ class RomModel(C.Structure):
 class Info(C.Structure):
     _fields_ = [("steps_taken", C.c_int64), ("n_instances", C.c_int64), ("kernel_launches", C.c_int64),
                 ("pitch", C.c_int64), ("sweep_ctas", C.c_int64), ("graphs", C.c_int32),
-                ("precision", C.c_int32), ("bytes_per_cell_step", C.c_double), ("sweep_stream", C.c_void_p)]
+                ("precision", C.c_int32), ("bytes_per_cell_step", C.c_double), ("steps_per_pass", C.c_int32),
+                ("sweep_stream", C.c_void_p)]
 
 
 class FDTDError(RuntimeError):
@@ -85,6 +86,7 @@ def lib():
         L.fdtd_get_info.argtypes = [vp, C.POINTER(Info)]
         L.fdtd_set_tuning.argtypes = [vp, i32, i32]
         L.fdtd_profile.argtypes = [vp, i32]
+        L.fdtd_set_time_blocking.argtypes = [vp, i32]
         L.fdtd_profile_read.argtypes = [vp, dp, dp, C.POINTER(i64)]
         L.fdtd_nccl_unique_id.argtypes = [vp]
         L.fdtd_last_error.argtypes = [vp]
@@ -94,7 +96,7 @@ def lib():
         L.fdtd_destroy.restype = None
         for n in ("create", "add_rom", "set_source", "set_probes", "record_energy", "step", "probe", "energy",
                   "get_window", "set_window", "get_rom_state", "set_rom_state", "sync", "get_info", "set_tuning",
-                  "nccl_unique_id", "profile", "profile_read", "step_group"):
+                  "nccl_unique_id", "profile", "profile_read", "step_group", "set_time_blocking"):
             getattr(L, "fdtd_" + n).restype = C.c_int
         _lib = L
     return _lib
@@ -290,6 +292,9 @@ class Simulation:
         o = Info()
         self._ck(lib().fdtd_get_info(self._h, C.byref(o)), "fdtd_get_info")
         return o
+
+    def set_time_blocking(self, steps_per_pass=2):
+        self._ck(lib().fdtd_set_time_blocking(self._h, int(steps_per_pass)), "fdtd_set_time_blocking")
 
     def profile(self, on=True):
         self._ck(lib().fdtd_profile(self._h, 1 if on else 0), "fdtd_profile")
