@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepParams<T> p) {
 // 1..30 store.  Interface edges are treated as frozen (masked) in both steps; the fix-up
 // kernel (post2) repairs the cells and edges next to every ROM instance.
 template <typename T, bool ENERGY>
-__global__ void __launch_bounds__(256) sweep2_kernel(const SweepParams<T> p) {
+__global__ void __maxnreg__(96) sweep2_kernel(const SweepParams<T> p) {
   constexpr int V = VT<T>::N;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
