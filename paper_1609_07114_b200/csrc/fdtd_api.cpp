@@ -137,6 +137,8 @@ struct fdtd_ctx {
   size_t ev_used = 0;
   // multi-rank
   nccl_comm comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
   std::vector<void*> owned;  // every device allocation
 };
 
@@ -339,17 +341,51 @@ cudaEvent_t next_event(fdtd_ctx* c) {
   return c->ev[c->ev_used++];
 }
 
+template <typename T>
+void sweep_split(fdtd_ctx* c, int q, cudaStream_t s, int begin, int count) {
+  fdtd::launch_sweep<T>(sweep_params<T>(c, q), c->warps, s, begin, count);
+}
+
+// One time step.  With several ranks the sweep is split: the interior row chunks (which read no
+// ghost row) run on the compute stream while the NCCL halo exchange runs on a side stream; the
+// first and last chunks follow once the ghost rows have arrived.
 fdtd_status enqueue_step(fdtd_ctx* c, int q, cudaStream_t s) {
-  fdtd_status st = halo_exchange(c, q, s);
-  if (st != FDTD_OK) return st;
   const bool prof = c->profiling && s == c->stream;
+  const int nch = (c->rows + c->chunk - 1) / c->chunk;
+  const bool split = c->d.nranks > 1 && nch >= 3;
+  const bool nccl_overlap = split && c->comm && c->comm_stream;
+  auto sweep = [&](int b, int n) {
+    if (c->prec == 64) sweep_split<double>(c, q, s, b, n);
+    else sweep_split<float>(c, q, s, b, n);
+  };
   cudaEvent_t e[3];
   if (prof) {
     for (auto& x : e) x = next_event(c);
     CK(cudaEventRecord(e[0], s));
   }
-  if (c->prec == 64) fdtd::launch_sweep<double>(sweep_params<double>(c, q), c->warps, s);
-  else fdtd::launch_sweep<float>(sweep_params<float>(c, q), c->warps, s);
+  if (nccl_overlap) {
+    CK(cudaEventRecord(c->ev_ready, s));
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
+    fdtd_status st = halo_exchange(c, q, c->comm_stream);
+    if (st != FDTD_OK) return st;
+    CK(cudaEventRecord(c->ev_halo, c->comm_stream));
+    sweep(1, nch - 2);                             // interior chunks: no ghost rows needed
+    CK(cudaStreamWaitEvent(s, c->ev_halo, 0));
+    sweep(0, 1);
+    sweep(nch - 1, 1);
+    c->launches += 2;
+  } else {
+    fdtd_status st = halo_exchange(c, q, s);
+    if (st != FDTD_OK) return st;
+    if (split) {  // local groups: same split launches (their halo copies precede on this stream)
+      sweep(1, nch - 2);
+      sweep(0, 1);
+      sweep(nch - 1, 1);
+      c->launches += 2;
+    } else {
+      sweep(0, nch);
+    }
+  }
   if (prof) CK(cudaEventRecord(e[1], s));
   if (c->prec == 64) fdtd::launch_post<double>(post_params<double>(c, q), c->energy_on, s);
   else fdtd::launch_post<float>(post_params<float>(c, q), c->energy_on, s);
@@ -677,6 +713,12 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
     nccl_uid id;
     memcpy(&id, d.nccl_id, sizeof id);
     if (g_nccl.CommInitRank(&c->comm, nranks, id, d.rank) != 0) { fdtd_destroy(c); return FDTD_E_NCCL; }
+    if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming) != cudaSuccess) {
+      fdtd_destroy(c);
+      return FDTD_E_CUDA;
+    }
   }
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) { fdtd_destroy(c); return FDTD_E_CUDA; }
   *out = c;
@@ -1267,6 +1309,9 @@ void fdtd_destroy(fdtd_ctx* c) {
   for (auto e : c->ev) cudaEventDestroy(e);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
   std::vector<void*> all = c->owned;
   for (void* p : all) dfree(c, p);
   delete c;

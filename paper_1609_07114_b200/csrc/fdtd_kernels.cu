@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepParams<T> p) {
   const int colv = (blockIdx.x * wpc + warp) * 32 + lane;
   const bool act = colv < p.ncolv;
   const int64_t c = (int64_t)colv * V;
-  const int r0 = 1 + blockIdx.y * p.chunk;
+  const int cy = p.chunk0 + blockIdx.y;  // row chunk
+  const int r0 = 1 + cy * p.chunk;
   const int r1 = min(r0 + p.chunk, p.rows + 1);
   const int64_t P = p.pitch;
 
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepParams<T> p) {
     if (threadIdx.x == 0) {
       double s = 0.0;
       for (int w = 0; w < wpc; ++w) s += red[w];
-      p.partials[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+      p.partials[(int64_t)cy * gridDim.x + blockIdx.x] = s;
     }
   }
 }
@@ -1121,11 +1122,16 @@ template void launch_min2<float>(const float*, const float*, int64_t, double*, i
 template void launch_min2<double>(const double*, const double*, int64_t, double*, int, cudaStream_t);
 
 template <typename T>
-void launch_sweep(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s) {
+void launch_sweep(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s, int chunk_begin, int chunk_count) {
   const int per_cta = 32 * warps_per_cta;
-  dim3 grid((p.ncolv + per_cta - 1) / per_cta, (p.rows + p.chunk - 1) / p.chunk);
-  if (p.partials) sweep_kernel<T, true><<<grid, per_cta, 0, s>>>(p);
-  else sweep_kernel<T, false><<<grid, per_cta, 0, s>>>(p);
+  const int nch = (p.rows + p.chunk - 1) / p.chunk;
+  if (chunk_count < 0) chunk_count = nch - chunk_begin;
+  if (chunk_count <= 0) return;
+  SweepParams<T> q = p;
+  q.chunk0 = chunk_begin;
+  dim3 grid((p.ncolv + per_cta - 1) / per_cta, chunk_count);
+  if (p.partials) sweep_kernel<T, true><<<grid, per_cta, 0, s>>>(q);
+  else sweep_kernel<T, false><<<grid, per_cta, 0, s>>>(q);
 }
 
 template <typename T>
@@ -1190,7 +1196,7 @@ void launch_mask(T* mea, T* f[6], int64_t pitch, const int32_t* rects, int64_t n
 }
 
 #define INST(T)                                                                                     \
-  template void launch_sweep<T>(const SweepParams<T>&, int, cudaStream_t);                        \
+  template void launch_sweep<T>(const SweepParams<T>&, int, cudaStream_t, int, int);              \
   template void launch_sweep2<T>(const SweepParams<T>&, int, cudaStream_t);                       \
   template void launch_post<T>(const PostParams<T>&, bool, cudaStream_t);                        \
   template void launch_post2<T>(const PostParams<T>&, bool, cudaStream_t);                       \

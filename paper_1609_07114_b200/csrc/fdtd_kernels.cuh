@@ -17,6 +17,7 @@ struct SweepParams {
   int ncolv;       // vector columns processed (16-byte vectors)
   int rows;        // owned cell rows (local rows 1..rows; local row 0 is the ghost row below)
   int chunk;       // rows per CTA
+  int chunk0;      // first row chunk of this launch (split launches overlap the halo exchange)
   T chx, chy;      // dt/(mu0 dx), dt/(mu0 dy)
   int src_row;     // local row of the soft source (-1: none)
   int64_t src_col;
@@ -71,7 +72,8 @@ struct PostParams {
 };
 
 template <typename T>
-void launch_sweep(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s);
+void launch_sweep(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s, int chunk_begin = 0,
+                  int chunk_count = -1);
 // two time steps per pass (temporal blocking; 30 output lanes per warp)
 template <typename T>
 void launch_sweep2(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s);
