@@ -51,6 +51,7 @@ def _model(kind, b, r, q, fmax, seed, dt_target_factor):
 
 
 def model(kind, b, r, q, fmax, seed, dt_target=None):
+    """A cached ROM of the given fill kind (see _model), optionally clipped at dt_target."""
     m = dict(_model(kind, b, r, q, fmax, seed, None))
     if dt_target is not None:
         m = rg.extend_cfl(m, dt_target)
@@ -110,24 +111,31 @@ def _grid_scene(name, N, n, device, steps, rom=None, count=0, seed=100):
                     meta=dict(full_n=N, n_clipped=[m["n_clipped"] for m in models]))
 
 
-def _cfg5(n, device, seed=500):
-    N = 49152
-    n = N if n is None else int(n)
-    eps, sig = _medium(n, seed, device)
+CFG5_SEED = 500
+
+
+def cfg5_specs(seed=CFG5_SEED):
+    """The 32 (b, r, q) model specs of config 5 (b ~ U{4..32}, r ~ U{4..10}, q ~ U{32,64,128,256})."""
     rng = np.random.default_rng(seed)
     specs = []
-    for k in range(32):
+    for _ in range(32):
         b = int(rng.integers(4, 33))
         r = int(rng.integers(4, 11))
         q = int(rng.choice([32, 64, 128, 256]))
         specs.append((b, r, q))
-    cnt = max(1, int(round(8192 * (n / N) ** 2)))
-    # smaller sub-instances use only models that fit comfortably
-    use = [k for k, (b, r, q) in enumerate(specs) if b <= max(4, n // 16)]
-    models = []
-    for k in use:
-        b, r, q = specs[k]
-        models.append(model("uniform112", b, r, q, 10e9, seed + 10 + k))
+    return specs
+
+
+def _cfg5(n, device, seed=CFG5_SEED, max_fine=None, min_count=0):
+    """Config 5.  Sub-instances may restrict the models to fine grids of at most max_fine cells per
+    side (fast to build) and place at least min_count instances."""
+    N = 49152
+    n = N if n is None else int(n)
+    eps, sig = _medium(n, seed, device)
+    specs = cfg5_specs(seed)
+    cnt = max(min_count, int(round(8192 * (n / N) ** 2)))
+    use = [k for k, (b, r, q) in enumerate(specs) if (max_fine is None or b * r <= max_fine) and b <= max(4, n // 16)]
+    models = [model("uniform112", *specs[k], 10e9, seed + 10 + k) for k in use]
     dtf = min(m["fine_dt_limit"] for m in models)
     dt = min(1.9 * dtf, 0.99 * sc.cfl_limit(DX, DY))
     models = [rg.extend_cfl(m, dt / 0.95) for m in models]
@@ -139,10 +147,11 @@ def _cfg5(n, device, seed=500):
     samples = sc.gaussian_samples(steps, dt, 10e9)
     return sc.Scene(name="cfg5", nx=n, ny=n, dx=DX, dy=DY, dt=dt, eps_r=eps, sigma=sig, precision=32,
                     steps=steps, source=src, samples=samples, probes=probes, models=models,
-                    placements=placements, meta=dict(full_n=N, n_clipped=[m["n_clipped"] for m in models]))
+                    placements=placements, meta=dict(full_n=N, n_clipped=[m["n_clipped"] for m in models],
+                                                     model_specs=[specs[k] for k in use]))
 
 
-def make(name, n=None, device="cpu"):
+def make(name, n=None, device="cpu", **kw):
     if name in ("cfg1", "cfg1b", "cfg1c"):
         return _cfg1({"cfg1": "a", "cfg1b": "b", "cfg1c": "c"}[name])
     if name == "cfg2":
@@ -152,7 +161,7 @@ def make(name, n=None, device="cpu"):
     if name == "cfg4":
         return _grid_scene("cfg4", 32768, n, device, 5000, rom=(16, 4, 128), count=4096, seed=400)
     if name == "cfg5":
-        return _cfg5(n, device)
+        return _cfg5(n, device, **kw)
     raise KeyError(name)
 
 

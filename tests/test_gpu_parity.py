@@ -200,3 +200,35 @@ def test_two_step_sweep_bitwise_equals_one_step(which):
     assert np.array_equal(x1, x2)
     assert np.array_equal(p1, p2)
     np.testing.assert_allclose(e2, e1, rtol=1e-12 if s.precision == 64 else 2e-6)
+
+
+def _cfg5_sub():
+    return configs.make("cfg5", n=1024, max_fine=100, min_count=24)
+
+
+def test_cfg5_subinstance_fp32_2000_steps():
+    """Config 5 recipe (12 distinct ROM models, q 32..256, nY up to 64): <= 1e-4 over 2000 steps."""
+    s = _cfg5_sub()
+    assert len({(m["bx"], m["q1"]) for m in s.models}) >= 8
+    _compare(s, 2000, 1e-4, random_init=17)
+
+
+def test_cfg5_two_step_bitwise_and_energy():
+    s = _cfg5_sub()
+    out = []
+    for spp in (1, 2):
+        g = gpu_from_scene(s, source=False)
+        g.set_time_blocking(spp)
+        Ex, Ey, Hz, xs = consistent_random_state(s, 19)
+        g.set_window(0, 0, Ex, Ey, Hz)
+        g.set_rom_state(xs)
+        g.record_energy(True)
+        g.step(301)
+        assert g.info().steps_per_pass == spp
+        out.append((g.get_window(), g.get_rom_state(), g.energy()))
+        g.close()
+    for a, b in zip(out[0][0], out[1][0]):
+        assert np.array_equal(a, b)
+    assert np.array_equal(out[0][1], out[1][1])
+    e = out[1][2]
+    assert np.all(np.diff(e) <= 1e-6 * e[:-1])
