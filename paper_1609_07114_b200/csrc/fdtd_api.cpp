@@ -115,6 +115,7 @@ struct fdtd_ctx {
   std::vector<double> mpool;                // shared model matrices (col-major, fp64)
   int nvec = 1;
   int rom_batch = 16;
+  bool rom_staged = true;
   std::vector<int32_t> batch_tab;  // (model, first instance, count)
   int32_t* d_batch_tab = nullptr;
   // device ROM arrays
@@ -255,6 +256,7 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q, bool pair = false) {
   p.batch = c->rom_batch;
   p.batch_tab = c->d_batch_tab;
   p.block = 256;
+  p.staged = c->rom_staged ? 1 : 0;
   p.level1 = c->d_level1;
   p.level1b = c->d_level1b;
   p.rects = c->d_rects;
@@ -537,9 +539,12 @@ fdtd_status upload_roms(fdtd_ctx* c) {
   {
     const char* env = getenv("FDTD_ROM_BATCH");
     int B = env ? std::max(1, std::min(64, atoi(env))) : 8;
+    // operators are staged in shared memory when two of them fit next to the batch vectors
+    c->rom_staged = fdtd::post_smem_bytes(c->es, c->nvec, 1, true) <= 200 * 1024;
+    const bool stg = c->rom_staged;
     auto fits = [&](int b, size_t lim) {
-      return fdtd::post2_smem_bytes(c->es, c->nvec, b, c->region_stride) <= lim &&
-             fdtd::post_smem_bytes(c->es, c->nvec, b) <= lim;
+      return fdtd::post2_smem_bytes(c->es, c->nvec, b, c->region_stride, stg) <= lim &&
+             fdtd::post_smem_bytes(c->es, c->nvec, b, stg) <= lim;
     };
     while (B > 1 && !fits(B, 110 * 1024)) B = B > 4 ? B - 4 : B / 2;
     if (!fits(B, 110 * 1024)) {

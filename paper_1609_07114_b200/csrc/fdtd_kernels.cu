@@ -531,8 +531,13 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first
   add(m.off_Q1, q2, q1); add(m.off_Aq, q1, q1); add(m.off_Kq, q1, q2); add(m.off_Lt, nY, q1);
   add(m.off_Bq, q1, nY); add(m.off_Lt, nY, q1);
   int ph = 0;
-  stage<T>(buf[0], op[0], om[0] * ok[0]);
+  const bool staged = p.staged != 0;
+  if (staged) stage<T>(buf[0], op[0], om[0] * ok[0]);
   auto next = [&]() -> const T* {  // start staging operator ph+1, wait for operator ph
+    if (!staged) {                   // large models: operators stay in L2/global memory
+      __syncthreads();
+      return op[ph];
+    }
     if (ph + 1 < nop) {
       stage<T>(buf[(ph + 1) & 1], op[ph + 1], om[ph + 1] * ok[ph + 1]);
       cp_wait<1>();
@@ -614,7 +619,7 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first
 template <typename T>
 __device__ __forceinline__ T* rom_buffers(const PostParams<T>& p, T* sv, T** buf) {
   const int64_t S = (int64_t)p.nthreads_vec * p.batch;
-  const int64_t NB = ((int64_t)p.nthreads_vec * p.nthreads_vec + 3) / 4 * 4;  // 16-byte aligned
+  const int64_t NB = p.staged ? ((int64_t)p.nthreads_vec * p.nthreads_vec + 3) / 4 * 4 : 0;  // 16-byte aligned
   buf[0] = sv + 7 * S;
   buf[1] = buf[0] + NB;
   return buf[1] + NB;  // first free element after the ROM area
@@ -1141,16 +1146,16 @@ void launch_sweep2(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s) {
   else sweep2_kernel<T, false><<<grid, 32 * warps_per_cta, 0, s>>>(p);
 }
 
-size_t post_smem_bytes(size_t es, int nvec, int batch) {
-  return es * ((size_t)7 * nvec * batch + 2 * (((size_t)nvec * nvec + 3) / 4 * 4));
+size_t post_smem_bytes(size_t es, int nvec, int batch, bool staged) {
+  return es * ((size_t)7 * nvec * batch + (staged ? 2 * (((size_t)nvec * nvec + 3) / 4 * 4) : 0));
 }
-size_t post2_smem_bytes(size_t es, int nvec, int batch, int region_stride) {
-  return post_smem_bytes(es, nvec, batch) + es * (size_t)batch * region_stride;
+size_t post2_smem_bytes(size_t es, int nvec, int batch, int region_stride, bool staged) {
+  return post_smem_bytes(es, nvec, batch, staged) + es * (size_t)batch * region_stride;
 }
 
 template <typename T>
 void launch_post2(const PostParams<T>& p, bool energy, cudaStream_t s) {
-  const size_t smem = post2_smem_bytes(sizeof(T), p.nthreads_vec, p.batch, p.region_stride);
+  const size_t smem = post2_smem_bytes(sizeof(T), p.nthreads_vec, p.batch, p.region_stride, p.staged != 0);
   if (energy) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(post2_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     post2_kernel<T, true><<<p.n_batch + 1, p.block, smem, s>>>(p);
@@ -1162,7 +1167,7 @@ void launch_post2(const PostParams<T>& p, bool energy, cudaStream_t s) {
 
 template <typename T>
 void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s) {
-  const size_t smem = post_smem_bytes(sizeof(T), p.nthreads_vec, p.batch);
+  const size_t smem = post_smem_bytes(sizeof(T), p.nthreads_vec, p.batch, p.staged != 0);
   if (energy) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(post_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     post_kernel<T, true><<<p.n_batch + 1, p.block, smem, s>>>(p);

@@ -60,6 +60,7 @@ struct PostParams {
   int64_t* step; unsigned int* done;
   int nthreads_vec;  // max(nY, q1, q2) over models (smem sizing)
   int block;         // threads per CTA
+  int staged;        // 1: operators streamed through shared memory; 0: read from global (large q)
   // ---- two-step mode (post2): fix-up around every instance after sweep2 (K3b)
   const int32_t* rects;            // per instance (i0, j0, bx, by), global
   int64_t row_begin, pitch;
@@ -86,8 +87,8 @@ void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s);
 template <typename T>
 void launch_post2(const PostParams<T>& p, bool energy, cudaStream_t s);
 // shared-memory bytes of the two kernels for a given batch (host-side sizing)
-size_t post_smem_bytes(size_t es, int nvec, int batch);
-size_t post2_smem_bytes(size_t es, int nvec, int batch, int region_stride);
+size_t post_smem_bytes(size_t es, int nvec, int batch, bool staged = true);
+size_t post2_smem_bytes(size_t es, int nvec, int batch, int region_stride, bool staged = true);
 
 // setup kernels
 template <typename T, typename M>

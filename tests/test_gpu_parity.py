@@ -232,3 +232,30 @@ def test_cfg5_two_step_bitwise_and_energy():
     assert np.array_equal(out[0][1], out[1][1])
     e = out[1][2]
     assert np.all(np.diff(e) <= 1e-6 * e[:-1])
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_large_rom_order_unstaged_operators(precision):
+    """q = 600 (q1 = q2 = 300): the shared operators no longer fit in shared memory and are read
+    from L2; parity with the oracle and two-step bit-equality still hold."""
+    nx = ny = 64
+    dx = dy = 1e-3
+    fe, fs = sc.uniform_fill(6, 6, 5, 31, 1, 4, 0, 0.05)
+    m = rg.build_rom(6, 6, 5, dx, dy, fe, fs, 600, 30e9)
+    assert m["q1"] == 300 and m["q2"] == 300
+    dt = 0.95 * m["fine_dt_limit"]
+    rng = np.random.default_rng(2)
+    s = sc.Scene(name="bigq", nx=nx, ny=ny, dx=dx, dy=dy, dt=dt, eps_r=rng.uniform(1, 3, (ny, nx)),
+                 sigma=rng.uniform(0, 0.05, (ny, nx)), precision=precision, steps=800, source=(10, 10),
+                 samples=sc.gaussian_samples(800, dt, 30e9, True), probes=np.array([[50, 50], [30, 12]], np.int32),
+                 models=[m], placements=np.array([[0, 29, 30]], np.int32))
+    _compare(s, 800, 1e-10 if precision == 64 else 1e-4, random_init=3)
+    outs = []
+    for spp in (1, 2):
+        g = gpu_from_scene(s)
+        g.set_time_blocking(spp)
+        g.step(101)
+        outs.append(g.get_window() + (g.get_rom_state(),))
+        g.close()
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
