@@ -201,12 +201,28 @@ def full_order_model(csys):
 # 3. SPRIM (R10)
 # --------------------------------------------------------------------------
 def sprim_basis(csys, q, fmax, defl_tol=1e-10):
-    """Structure-preserving block Arnoldi basis V1 (nEc x q1), V2 (nH x q2).
+    """SPRIM basis with q1 = ceil(q/2), q2 = floor(q/2) where the Krylov space allows it.
+
+    The E and H parts of an m-vector Krylov basis can have rank < m, so m grows until both parts
+    reach their share (or the space is exhausted); each part keeps its leading directions.
+    """
+    q1w, q2w = (q + 1) // 2, q // 2
+    m = q1w
+    for _ in range(8):
+        V1, V2 = _sprim_basis_m(csys, m, fmax, defl_tol)
+        if (V1.shape[1] >= q1w and V2.shape[1] >= q2w) or m >= csys["nEc"] + csys["nH"]:
+            break
+        m = int(m + max(q1w - V1.shape[1], q2w - V2.shape[1], 1) * 1.5)
+    return V1[:, :q1w], V2[:, :q2w]
+
+
+def _sprim_basis_m(csys, m, fmax, defl_tol=1e-10):
+    """Structure-preserving block Arnoldi basis V1 (nEc x q1), V2 (nH x q2) from m Krylov vectors.
 
     Semi-discrete pencil of R(x'-x) + F(x'+x) = B u (eq:sys1a): C = blkdiag(R11, R22),
     G = [[2 F11, -K], [K^T, 0]].  Krylov space of (G + s0 C)^{-1} C from (G + s0 C)^{-1} B,
-    real s0 = pi * fmax, C-inner product, modified Gram-Schmidt run twice, deflation
-    defl_tol.  m = ceil(q/2) vectors; the E and H rows are orthonormalised separately.
+    real s0 = pi * fmax, C-inner product, Gram-Schmidt run twice, deflation defl_tol; the E and
+    H rows of the m vectors are orthonormalised separately (directions ordered by singular value).
     """
     nEc, nH, nY = csys["nEc"], csys["nH"], csys["nY"]
     s0 = math.pi * fmax
@@ -228,7 +244,7 @@ def sprim_basis(csys, q, fmax, defl_tol=1e-10):
     B0 = np.zeros((nEc, nY))
     B0[np.arange(nY), np.arange(nY)] = csys["Sc"]
     X0 = solve(B0, np.zeros((nH, nY)))
-    m = (q + 1) // 2
+    m = min(m, nEc + nH)
     Wmat = np.zeros((nEc + nH, m))
     W = []
 
