@@ -340,3 +340,34 @@ def test_scheme_stability_and_cfl_extension():
     mc = rg.extend_cfl(m, 2 * dtf)
     assert mc["n_clipped"] > 0
     assert radius(mc, 1.9 * dtf) <= 1 + 1e-10
+
+
+@pytest.mark.slow
+def test_rom_converges_to_subgridding_as_q_grows():
+    """SPRIM ROMs approach the full-order (direct subgridding) solution as q grows (SURVEY Appendix A:
+    8.3e-2 / 1.9e-2 / 1.4e-4 at q = 24 / 48 / 96 for this setup).  Pins the construction quality of
+    the emitted models; the paper's own accuracy figures (Figs. 5/7/9) remain unpinned (no data)."""
+    from inputs import configs
+    nx = ny = 40
+    dx = dy = 1e-3
+    fe, fs = sc.uniform_fill(4, 4, 5, 11, 1, 4, 0, 0.05)
+    sysf = rg.fine_system(4, 4, 5, dx, dy, fe, fs)
+    dt = 0.95 * rg.fine_cfl_limit(sysf)
+    n = 6000
+    g = sc.gaussian_samples(n, dt, 10e9, derivative=True)
+
+    def run(add):
+        s = O.OracleSim(nx, ny, dx, dy, dt, 1.0, 0.0)
+        add(s)
+        s.set_source(8, 8, g)
+        s.set_probes([(30, 30)])
+        return s.step(n, energy=False)[0][0]
+
+    ref = run(lambda s: s.add_subgrid(18, 18, 4, 4, 5, fe, fs))
+    errs = []
+    for q in (24, 48, 96):
+        m = rg.build_rom(4, 4, 5, dx, dy, fe, fs, q, 10e9)
+        p = run(lambda s: s.add_rom(m, 18, 18))
+        errs.append(np.linalg.norm(p - ref) / np.linalg.norm(ref))
+    assert errs[0] > errs[1] > errs[2]
+    assert errs[2] < 1e-2, errs
