@@ -34,7 +34,7 @@ def build(force: bool = False) -> str:
     """Compile the plain-C oracle (gcc, -O2, no fast-math)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + ".tmp%d" % os.getpid()
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fno-fast-math", "-ffp-contract=off",
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fno-fast-math", "-ffp-contract=off", "-fopenmp",
                                "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
@@ -59,6 +59,8 @@ def lib():
         L.osim_step.argtypes = [C.c_void_p, C.c_int64, _dp, C.c_int64, _dp]
         L.osim_get_state.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp]
         L.osim_set_state.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp]
+        L.osim_set_threads.argtypes = [C.c_int]
+        L.osim_get_threads.restype = C.c_int
         L.osim_steps_taken.restype = C.c_int64
         L.osim_steps_taken.argtypes = [C.c_void_p]
         _lib = L
@@ -71,6 +73,15 @@ def _p(a):
 
 def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def set_threads(n):
+    """Host threads for the oracle's row loops (0: all cores).  Results do not depend on it."""
+    lib().osim_set_threads(int(n))
+
+
+def get_threads():
+    return lib().osim_get_threads()
 
 
 class OracleSim:

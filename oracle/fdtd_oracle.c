@@ -28,6 +28,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #define O_C0 299792458.0
 #define O_MU0 (4.0e-7 * 3.14159265358979323846)
@@ -328,12 +331,31 @@ void osim_set_probes(osim *s, const int *ij, int n) {
 /* ------------------------------------------------------------------ */
 /* one time step                                                       */
 /* ------------------------------------------------------------------ */
+/* Row loops may run on several host threads (OpenMP, rows are independent; results do not
+ * depend on the thread count).  osim_set_threads(1) gives the plain single-threaded oracle. */
+void osim_set_threads(int n) {
+#ifdef _OPENMP
+  omp_set_num_threads(n > 0 ? n : omp_get_num_procs());
+#else
+  (void)n;
+#endif
+}
+
+int osim_get_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
 static void coarse_h(osim *s) {
   /* eq:updateH (L267-273) at coarse resolution:
    * dx dy mu/dt H^{n+1/2} = dx dy mu/dt H^{n-1/2} - dx Ex_j + dx Ex_{j+1} + dy Ey_i - dy Ey_{i+1} */
   const int nx = s->nx, ny = s->ny;
   const double dx = s->dx, dy = s->dy, dt = s->dt, mu = O_MU0;
   memcpy(s->Hold, s->Hz, (size_t)nx * ny * sizeof(double));
+#pragma omp parallel for schedule(static) if (ny >= 256)
   for (int j = 0; j < ny; ++j)
     for (int i = 0; i < nx; ++i) {
       if (CELL(s, kc, i, j) == K_HOLE) continue;
@@ -352,6 +374,7 @@ static void coarse_e(osim *s) {
    *   dy dx (eps/dt + sig/2) Ey^{n+1} = dy dx (eps/dt - sig/2) Ey^n - dy (Hz_{i+1/2} - Hz_{i-1/2}). */
   const int nx = s->nx, ny = s->ny;
   const double dx = s->dx, dy = s->dy, dt = s->dt;
+#pragma omp parallel for schedule(static) if (ny >= 256)
   for (int j = 1; j < ny; ++j)
     for (int i = 0; i < nx; ++i) {
       if (s->kx[(size_t)j * nx + i] != K_NORMAL) continue;
@@ -361,6 +384,7 @@ static void coarse_e(osim *s) {
       double rhs = dx * dy * (eps / dt - sig / 2) * EX(s, i, j) + dx * HZ(s, i, j) - dx * HZ(s, i, j - 1);
       EX(s, i, j) = rhs / lhs;
     }
+#pragma omp parallel for schedule(static) if (ny >= 256)
   for (int j = 0; j < ny; ++j)
     for (int i = 1; i < nx; ++i) {
       if (s->ky[(size_t)j * (nx + 1) + i] != K_NORMAL) continue;
@@ -378,21 +402,33 @@ static void coarse_e(osim *s) {
 static double energy(const osim *s) {
   const int nx = s->nx, ny = s->ny;
   const double dx = s->dx, dy = s->dy, dt = s->dt;
+  /* per-row partial sums (fixed order, so the value does not depend on the thread count) */
+  double *row = (double *)calloc((size_t)ny + 1, sizeof(double));
+#pragma omp parallel for schedule(static) if (ny >= 256)
+  for (int j = 0; j <= ny; ++j) {
+    double w = 0.0;
+    if (j >= 1 && j < ny)
+      for (int i = 0; i < nx; ++i) {
+        if (s->kx[(size_t)j * nx + i] != K_NORMAL) continue;
+        double eps = O_EPS0 * 0.5 * (CELL(s, eps_r, i, j - 1) + CELL(s, eps_r, i, j));
+        w += dx * dy * eps * EX(s, i, j) * EX(s, i, j);
+      }
+    if (j < ny) {
+      for (int i = 1; i < nx; ++i) {
+        if (s->ky[(size_t)j * (nx + 1) + i] != K_NORMAL) continue;
+        double eps = O_EPS0 * 0.5 * (CELL(s, eps_r, i - 1, j) + CELL(s, eps_r, i, j));
+        w += dx * dy * eps * EY(s, i, j) * EY(s, i, j);
+      }
+      for (int i = 0; i < nx; ++i) {
+        size_t c = (size_t)j * nx + i;
+        if (s->kc[c] != K_HOLE) w += O_MU0 * dx * dy * s->Hold[c] * s->Hz[c];
+      }
+    }
+    row[j] = w;
+  }
   double w = 0.0;
-  for (int j = 1; j < ny; ++j)
-    for (int i = 0; i < nx; ++i) {
-      if (s->kx[(size_t)j * nx + i] != K_NORMAL) continue;
-      double eps = O_EPS0 * 0.5 * (CELL(s, eps_r, i, j - 1) + CELL(s, eps_r, i, j));
-      w += dx * dy * eps * EX(s, i, j) * EX(s, i, j);
-    }
-  for (int j = 0; j < ny; ++j)
-    for (int i = 1; i < nx; ++i) {
-      if (s->ky[(size_t)j * (nx + 1) + i] != K_NORMAL) continue;
-      double eps = O_EPS0 * 0.5 * (CELL(s, eps_r, i - 1, j) + CELL(s, eps_r, i, j));
-      w += dx * dy * eps * EY(s, i, j) * EY(s, i, j);
-    }
-  for (size_t c = 0; c < (size_t)nx * ny; ++c)
-    if (s->kc[c] != K_HOLE) w += O_MU0 * dx * dy * s->Hold[c] * s->Hz[c];
+  for (int j = 0; j <= ny; ++j) w += row[j];
+  free(row);
   for (int r = 0; r < s->nrom; ++r) {
     const orom *m = &s->roms[r];
     for (int p = 0; p < m->nY; ++p) {
@@ -580,7 +616,8 @@ void osim_step(osim *s, int64_t nsteps, double *probe_out, int64_t ldp, double *
     if (energy_out) energy_out[t] = energy(s);            /* S3: W^n */
     if (probe_out)
       for (int p = 0; p < s->nprobe; ++p) probe_out[(size_t)p * ldp + t] = s->Hz[s->probe[p]];
-    for (int r = 0; r < s->nrom; ++r) rom_step(s, &s->roms[r]); /* S4-S5 */
+#pragma omp parallel for schedule(dynamic) if (s->nrom >= 8)
+    for (int r = 0; r < s->nrom; ++r) rom_step(s, &s->roms[r]); /* S4-S5 (ROMs are independent) */
     for (int r = 0; r < s->nsub; ++r) subgrid_step(s, &s->subs[r]); /* reference only */
     coarse_e(s);                                          /* S7 */
     for (int r = 0; r < s->nrom; ++r) {                   /* S6 */

@@ -131,3 +131,40 @@ def test_full_size_sampled_parity(name):
     sim.close()
     del scene
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name", ["cfg3"])
+def test_full_grid_first_200_steps(name):
+    """Config 3 in full (8192^2, all 1024 ROM instances) for the first 200 steps from a random
+    consistent state, every cell and every ROM state compared (config 2 is the same
+    stencil without ROMs and is covered at full size by the sampled-window test)."""
+    import torch
+
+    from helpers import consistent_random_state, gpu_from_scene, oracle_from_scene
+
+    scene = configs.make(name, device="cuda")
+    scene.eps_r = scene.eps_r.double().cpu().numpy()
+    scene.sigma = scene.sigma.double().cpu().numpy()
+    O.set_threads(0)
+    g = gpu_from_scene(scene)
+    o = oracle_from_scene(scene)
+    Ex, Ey, Hz, xs = consistent_random_state(scene, 23)
+    g.set_window(0, 0, Ex, Ey, Hz)
+    o.set_state(Ex, Ey, Hz, xs if xs.size else None)
+    if xs.size:
+        g.set_rom_state(xs)
+    del Ex, Ey, Hz
+    g.record_energy(True)
+    g.step(200)
+    po, eo = o.step(200)
+    pg, eg = g.probe(), g.energy()
+    Exg, Eyg, Hzg = g.get_window()
+    Exo, Eyo, Hzo, xo = o.get_state()
+    errs = dict(probe=rel(pg, po), Ex=rel(Exg, Exo), Ey=rel(Eyg, Eyo), Hz=rel(Hzg, Hzo), energy=rel(eg, eo))
+    if xo.size:
+        errs["rom"] = rel(g.get_rom_state(), xo)
+    print(name, errs)
+    assert max(errs.values()) <= 1e-4, errs
+    g.close()
+    o.close()
+    torch.cuda.empty_cache()
