@@ -171,9 +171,9 @@ def run_ours(args):
             t = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8).clone()
         dist.broadcast(t, 0)
         nid = bytes(t.numpy().tobytes())
-    m0 = max(rb - 1, 0)
-    eps = scene.eps_r[m0:re].contiguous()
-    sig = scene.sigma[m0:re].contiguous()
+    m0, m1 = max(rb - 2, 0), min(re + 1, ny)  # materials of rows [rb-2, re+1): the 2-step halo
+    eps = scene.eps_r[m0:m1].contiguous()
+    sig = scene.sigma[m0:m1].contiguous()
     sim = Simulation(scene.nx, scene.ny, scene.dx, scene.dy, scene.dt, eps, sig, precision=scene.precision,
                      device=lrank, rank=rank, nranks=ws, nccl_id=nid, row_begin=rb, row_end=re,
                      materials_row0=m0, record_capacity=max(4096, args.steps + args.warmup + 8))

@@ -67,7 +67,8 @@ typedef struct {
   uint32_t flags;          /* FDTD_* flags above                                          */
   /* Per-cell relative permittivity and conductivity (S/m), row-major [rows][nx].  The
    * pointer addresses global row `materials_row0`; it must cover the rows
-   * [max(row_begin-1, 0), row_end) of the grid.  Edge values are the arithmetic mean of
+   * [max(row_begin-2, 0), min(row_end+1, ny)) of the grid (the slab plus the ghost rows the
+   * two-step sweep reads).  Edge values are the arithmetic mean of
    * the two adjacent cells (R2).  mu = mu0 everywhere
    * (R3).  Host or device memory (FDTD_MATERIALS_ON_DEVICE), double or float
    * (FDTD_MATERIALS_F32). */
@@ -197,10 +198,11 @@ fdtd_status fdtd_profile(fdtd_ctx *c, int32_t on);
 fdtd_status fdtd_profile_read(fdtd_ctx *c, double *sweep_ms, double *post_ms, int64_t *n_launches);
 
 /* Time steps per sweep pass: 1, or 2 (default; temporal blocking with a per-instance fix-up,
- * DESIGN.md K1b/K3b).  Two-step mode is used only on one rank and when every ROM instance's
- * [i0-2, i0+bx+2) x [j0-2, j0+by+2) region is inside the grid and free of other instances'
- * outside cells; otherwise fdtd_step silently runs one step per pass.  Results are
- * bit-identical either way. */
+ * DESIGN.md K1b/K3b).  Two-step mode is used when every ROM instance's
+ * [i0-2, i0+bx+2) x [j0-2, j0+by+2) region is inside this rank's rows and free of other
+ * instances' outside cells -- on every rank (agreed collectively at the first fdtd_step after a
+ * configuration change; then the halo exchange is two rows deep); otherwise fdtd_step runs one
+ * step per pass.  Results are bit-identical either way. */
 fdtd_status fdtd_set_time_blocking(fdtd_ctx *c, int32_t steps_per_pass);
 
 /* Tuning knobs for the fused sweep (rows per CTA, warps per CTA); 0 keeps default. */

@@ -75,8 +75,8 @@ def place_blocks(nx, ny, sizes, count, seed, nslabs=8, forbid=(), max_tries=2_00
 
     sizes: list of (bx, by) per model; the model of each placement is drawn uniformly.
     Every footprint plus its one-cell ring stays inside the grid without touching the PEC
-    wall, the expanded footprints are pairwise disjoint, and the rows j0-1 .. j0+by stay
-    inside one of ``nslabs`` equal row slabs.  ``forbid``: cells (i, j) that must stay
+    wall, the expanded footprints are pairwise disjoint, and the rows j0-2 .. j0+by+1 stay
+    inside one of ``nslabs`` equal row slabs (the two-step fix-up region of DESIGN.md K3b).  ``forbid``: cells (i, j) that must stay
     outside every footprint (source, probes).
     Returns int32 array (count, 3): (model, i0, j0).
     """
@@ -95,7 +95,7 @@ def place_blocks(nx, ny, sizes, count, seed, nslabs=8, forbid=(), max_tries=2_00
         bx, by = sizes[m]
         i0 = int(rng.integers(2, nx - bx - 1))
         j0 = int(rng.integers(2, ny - by - 1))
-        if (j0 - 1) // slab != (j0 + by) // slab:
+        if (j0 - 2) // slab != (j0 + by + 1) // slab:  # footprint + 2 rows inside one slab (R19)
             continue
         # expanded footprint [i0-1, i0+bx] x [j0-1, j0+by], kept one extra cell apart so rings never touch
         x0, x1, y0, y1 = i0 - 1, i0 + bx + 2, j0 - 1, j0 + by + 2

@@ -22,6 +22,7 @@
 
 namespace {
 
+constexpr int ROW0 = 2;  // local row of the first owned row (two ghost rows below: 2-step halos)
 constexpr double MU0 = 4.0e-7 * 3.14159265358979323846;
 constexpr double C0 = 299792458.0;
 constexpr double EPS0 = 1.0 / (MU0 * C0 * C0);
@@ -55,7 +56,7 @@ struct Nccl {
   }
 };
 Nccl g_nccl;
-constexpr int NCCL_F32 = 7, NCCL_F64 = 8, NCCL_SUM = 0;
+constexpr int NCCL_I32 = 2, NCCL_F32 = 7, NCCL_F64 = 8, NCCL_SUM = 0, NCCL_MIN = 3;
 
 struct ModelHost {
   int bx, by, nY, q1, q2;
@@ -71,7 +72,7 @@ struct fdtd_ctx {
   size_t es = 4;  // element size
   int V = 4;      // elements per 16-byte vector
   int rows = 0;   // owned rows
-  int64_t nrows_alloc = 0, pitch = 0;  // rows + 3: ghost row below, two ghost rows above
+  int64_t nrows_alloc = 0, pitch = 0;  // rows + 5: two ghost rows below, three above
   int ncolv = 0;
   cudaStream_t stream = nullptr, cap_stream = nullptr;
   std::string err;
@@ -81,7 +82,7 @@ struct fdtd_ctx {
   void* mat_eps = nullptr;  // device copy of per-cell materials for rows [mrow0, row_end)
   void* mat_sig = nullptr;
   bool mat_f32 = false;
-  int64_t mrow0 = 0;
+  int64_t mrow0 = 0, mrow_end = 0;
   int64_t* d_step = nullptr;
   unsigned* d_done = nullptr;
   double* d_partials = nullptr;
@@ -103,7 +104,7 @@ struct fdtd_ctx {
   int64_t steps = 0, rd_probe = 0, rd_energy = 0;
   int cur = 0;  // buffer holding the current state (E^n, H^{n-1/2})
   // two-step mode (sweep2 + post2): wanted by the user (default on) and valid for the placements
-  bool tb2_want = true, tb2_ok = true;
+  bool tb2_want = true, tb2_ok = true, tb2_all = true, tb2_dirty = true;
   int region_stride = 4;
   int32_t* d_rects = nullptr;
   double* d_rom_partials2 = nullptr;
@@ -206,7 +207,7 @@ fdtd_status upload_T(fdtd_ctx* c, void** dst, const std::vector<double>& v) {
   return upload(c, reinterpret_cast<float**>(dst), f);
 }
 
-inline int64_t lrow(const fdtd_ctx* c, int64_t g) { return g - c->d.row_begin + 1; }
+inline int64_t lrow(const fdtd_ctx* c, int64_t g) { return g - c->d.row_begin + ROW0; }
 
 template <typename T>
 fdtd::SweepParams<T> sweep_params(fdtd_ctx* c, int q) {
@@ -214,12 +215,12 @@ fdtd::SweepParams<T> sweep_params(fdtd_ctx* c, int q) {
   p.ex0 = (const T*)c->f[q][0]; p.ey0 = (const T*)c->f[q][1]; p.hz0 = (const T*)c->f[q][2];
   p.ex1 = (T*)c->f[1 - q][0]; p.ey1 = (T*)c->f[1 - q][1]; p.hz1 = (T*)c->f[1 - q][2];
   p.mea = (const T*)c->coef[0]; p.msb = (const T*)c->coef[1];
-  p.pitch = c->pitch; p.ncolv = c->ncolv; p.rows = c->rows; p.chunk = c->chunk;
+  p.pitch = c->pitch; p.ncolv = c->ncolv; p.rows = c->rows; p.chunk = c->chunk; p.row0 = ROW0;
   p.chx = (T)(c->d.dt / (MU0 * c->d.dx));
   p.chy = (T)(c->d.dt / (MU0 * c->d.dy));
-  // the source row may also be the ghost row below: the first chunk recomputes that row's
-  // Hz^{n+1/2} and must add the source exactly as its owner does
-  const bool src_here = c->d_src && c->src_j >= c->d.row_begin - 1 && c->src_j < c->d.row_end;
+  // the source row may also be a ghost row (below: the first chunk recomputes it; above: the
+  // two-step sweep advances row_end once): those recomputations add the source as its owner does
+  const bool src_here = c->d_src && c->src_j >= c->d.row_begin - 2 && c->src_j <= c->d.row_end;
   p.src_row = src_here ? (int)lrow(c, c->src_j) : -1;
   p.src_col = src_here ? c->src_i : -1;
   p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
@@ -261,6 +262,7 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q, bool pair = false) {
   p.level1b = c->d_level1b;
   p.rects = c->d_rects;
   p.row_begin = c->d.row_begin;
+  p.row0 = ROW0;
   p.pitch = c->pitch;
   p.ex0 = (const T*)c->f[q][0]; p.ey0 = (const T*)c->f[q][1]; p.hz0 = (const T*)c->f[q][2];
   p.mea = (const T*)c->coef[0]; p.msb = (const T*)c->coef[1];
@@ -283,17 +285,33 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q, bool pair = false) {
 // whole device rows (pitch elements).  Sends and receives are listed in the order both
 // transports pair them (per peer and direction, in list order).
 struct HaloRow { int a; int64_t row; int peer; };
-void halo_plan(const fdtd_ctx* c, std::vector<HaloRow>& sends, std::vector<HaloRow>& recvs) {
+// depth 1 (one-step passes): rank g sends its top owned row of (Ex, Ey, Hz) to g+1's ghost row
+// below and its bottom Ex row to g-1's ghost Ex row above.  depth 2 (two-step passes): the top two
+// rows of (Ex, Ey, Hz) go up; the bottom row's (Ex, Ey, Hz) and the second Ex row go down.
+void halo_plan(const fdtd_ctx* c, int depth, std::vector<HaloRow>& sends, std::vector<HaloRow>& recvs) {
   sends.clear();
   recvs.clear();
   const int up = c->d.rank + 1, dn = c->d.rank - 1;
+  const int64_t top = ROW0 + c->rows;  // first row above the slab
+  auto down_list = [&](int64_t base, int peer, std::vector<HaloRow>& v) {  // rows the lower rank needs
+    if (depth == 1) {
+      v.push_back({0, base, peer});
+    } else {
+      v.push_back({0, base, peer});
+      v.push_back({1, base, peer});
+      v.push_back({2, base, peer});
+      v.push_back({0, base + 1, peer});
+    }
+  };
   if (up < c->d.nranks) {
-    for (int a = 0; a < 3; ++a) sends.push_back({a, (int64_t)c->rows, up});
-    recvs.push_back({0, (int64_t)c->rows + 1, up});
+    for (int64_t r = top - depth; r < top; ++r)
+      for (int a = 0; a < 3; ++a) sends.push_back({a, r, up});
+    down_list(top, up, recvs);  // rows above the slab come from rank g+1's bottom rows
   }
   if (dn >= 0) {
-    for (int a = 0; a < 3; ++a) recvs.push_back({a, 0, dn});
-    sends.push_back({0, 1, dn});
+    for (int64_t r = ROW0 - depth; r < ROW0; ++r)
+      for (int a = 0; a < 3; ++a) recvs.push_back({a, r, dn});
+    down_list(ROW0, dn, sends);
   }
 }
 
@@ -301,12 +319,12 @@ inline char* dev_row(const fdtd_ctx* c, int q, int a, int64_t r) {
   return (char*)c->f[q][a] + (size_t)r * c->pitch * c->es;
 }
 
-fdtd_status halo_exchange(fdtd_ctx* c, int q, cudaStream_t s) {
+fdtd_status halo_exchange(fdtd_ctx* c, int q, cudaStream_t s, int depth) {
   if (c->d.nranks <= 1 || (c->d.flags & FDTD_LOCAL_GROUP)) return FDTD_OK;
   const size_t n = (size_t)c->pitch;
   const int dt = c->prec == 64 ? NCCL_F64 : NCCL_F32;
   std::vector<HaloRow> sends, recvs;
-  halo_plan(c, sends, recvs);
+  halo_plan(c, depth, sends, recvs);
   NK(g_nccl.GroupStart());
   for (auto& x : sends) NK(g_nccl.Send(dev_row(c, q, x.a, x.row), n, dt, x.peer, c->comm, s));
   for (auto& x : recvs) NK(g_nccl.Recv(dev_row(c, q, x.a, x.row), n, dt, x.peer, c->comm, s));
@@ -316,13 +334,13 @@ fdtd_status halo_exchange(fdtd_ctx* c, int q, cudaStream_t s) {
 
 // Local transport for an in-process group: every receive pairs with the peer's sends to this
 // rank in plan order (the same pairing NCCL applies).
-fdtd_status halo_local(fdtd_ctx* const* g, int n, int k, int q, cudaStream_t s) {
+fdtd_status halo_local(fdtd_ctx* const* g, int n, int k, int q, cudaStream_t s, int depth) {
   fdtd_ctx* c = g[k];
   std::vector<HaloRow> sends, recvs, psends, precvs;
-  halo_plan(c, sends, recvs);
+  halo_plan(c, depth, sends, recvs);
   for (int peer = 0; peer < n; ++peer) {
     if (peer == k) continue;
-    halo_plan(g[peer], psends, precvs);
+    halo_plan(g[peer], depth, psends, precvs);
     std::vector<HaloRow> in, out;
     for (auto& x : recvs) if (x.peer == peer) in.push_back(x);
     for (auto& x : psends) if (x.peer == k) out.push_back(x);
@@ -368,7 +386,7 @@ fdtd_status enqueue_step(fdtd_ctx* c, int q, cudaStream_t s) {
   if (nccl_overlap) {
     CK(cudaEventRecord(c->ev_ready, s));
     CK(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
-    fdtd_status st = halo_exchange(c, q, c->comm_stream);
+    fdtd_status st = halo_exchange(c, q, c->comm_stream, 1);
     if (st != FDTD_OK) return st;
     CK(cudaEventRecord(c->ev_halo, c->comm_stream));
     sweep(1, nch - 2);                             // interior chunks: no ghost rows needed
@@ -377,7 +395,7 @@ fdtd_status enqueue_step(fdtd_ctx* c, int q, cudaStream_t s) {
     sweep(nch - 1, 1);
     c->launches += 2;
   } else {
-    fdtd_status st = halo_exchange(c, q, s);
+    fdtd_status st = halo_exchange(c, q, s, 1);
     if (st != FDTD_OK) return st;
     if (split) {  // local groups: same split launches (their halo copies precede on this stream)
       sweep(1, nch - 2);
@@ -396,18 +414,76 @@ fdtd_status enqueue_step(fdtd_ctx* c, int q, cudaStream_t s) {
   return FDTD_OK;
 }
 
-bool tb2_active(const fdtd_ctx* c) { return c->tb2_want && c->tb2_ok && c->d.nranks == 1; }
+// Two-step passes are used when this rank wants and can (tb2_ok) -- and, with several ranks, when
+// every rank can (the halo depth must agree): agreed once per configuration (agree_tb2).
+bool tb2_active(const fdtd_ctx* c) {
+  if (!c->tb2_want || !c->tb2_ok) return false;
+  return c->d.nranks == 1 || c->tb2_all;
+}
 
-// two steps in one pass: sweep2 (q -> 1-q) then the ROM fix-up / probes / energy of both steps
+fdtd_status agree_tb2(fdtd_ctx* c) {
+  if (!c->tb2_dirty) return FDTD_OK;
+  c->tb2_dirty = false;
+  c->tb2_all = c->tb2_want && c->tb2_ok;
+  if (c->d.nranks > 1 && c->comm) {  // collective min over ranks (all ranks reach this call together)
+    int32_t* d = (int32_t*)dalloc(c, sizeof(int32_t));
+    if (!d) return fail(c, FDTD_E_NOMEM, "agree");
+    const int32_t mine = c->tb2_all ? 1 : 0;
+    CK(cudaMemcpyAsync(d, &mine, sizeof mine, cudaMemcpyHostToDevice, c->stream));
+    NK(g_nccl.AllReduce(d, d, 1, NCCL_I32, NCCL_MIN, c->comm, c->stream));
+    int32_t all = 0;
+    CK(cudaMemcpyAsync(&all, d, sizeof all, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, d);
+    c->tb2_all = all != 0;
+  }
+  return FDTD_OK;
+}
+
+template <typename T>
+void sweep2_split(fdtd_ctx* c, int q, cudaStream_t s, int begin, int count) {
+  fdtd::launch_sweep2<T>(sweep_params<T>(c, q), c->warps, s, begin, count);
+}
+
+// two steps in one pass: sweep2 (q -> 1-q) then the ROM fix-up / probes / energy of both steps.
+// With several ranks the two-row-deep halo exchange overlaps the interior row chunks.
 fdtd_status enqueue_pair(fdtd_ctx* c, int q, cudaStream_t s) {
   const bool prof = c->profiling && s == c->stream;
+  const int nch = (c->rows + c->chunk - 1) / c->chunk;
+  const bool split = c->d.nranks > 1 && nch >= 3 && c->chunk >= 2;
+  const bool nccl_overlap = split && c->comm && c->comm_stream;
+  auto sweep = [&](int b, int n) {
+    if (c->prec == 64) sweep2_split<double>(c, q, s, b, n);
+    else sweep2_split<float>(c, q, s, b, n);
+  };
   cudaEvent_t e[3];
   if (prof) {
     for (auto& x : e) x = next_event(c);
     CK(cudaEventRecord(e[0], s));
   }
-  if (c->prec == 64) fdtd::launch_sweep2<double>(sweep_params<double>(c, q), c->warps, s);
-  else fdtd::launch_sweep2<float>(sweep_params<float>(c, q), c->warps, s);
+  if (nccl_overlap) {
+    CK(cudaEventRecord(c->ev_ready, s));
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
+    fdtd_status st = halo_exchange(c, q, c->comm_stream, 2);
+    if (st != FDTD_OK) return st;
+    CK(cudaEventRecord(c->ev_halo, c->comm_stream));
+    sweep(1, nch - 2);  // interior chunks read no ghost row (chunk >= 2)
+    CK(cudaStreamWaitEvent(s, c->ev_halo, 0));
+    sweep(0, 1);
+    sweep(nch - 1, 1);
+    c->launches += 2;
+  } else {
+    fdtd_status st = halo_exchange(c, q, s, 2);
+    if (st != FDTD_OK) return st;
+    if (split) {
+      sweep(1, nch - 2);
+      sweep(0, 1);
+      sweep(nch - 1, 1);
+      c->launches += 2;
+    } else {
+      sweep(0, nch);
+    }
+  }
   if (prof) CK(cudaEventRecord(e[1], s));
   if (c->prec == 64) fdtd::launch_post2<double>(post_params<double>(c, q, true), c->energy_on, s);
   else fdtd::launch_post2<float>(post_params<float>(c, q, true), c->energy_on, s);
@@ -421,6 +497,7 @@ void drop_graph(fdtd_ctx* c) {
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   c->gexec = nullptr;
   c->graph_dirty = true;
+  c->tb2_dirty = true;
 }
 
 // Captures one "period" starting from buffer 0: two single steps (0 -> 1 -> 0) or, in two-step
@@ -457,10 +534,10 @@ fdtd_status build_coefficients(fdtd_ctx* c) {
   const M* e = (const M*)c->mat_eps;
   const M* s = (const M*)c->mat_sig;
   if (c->prec == 64)
-    fdtd::launch_materials<double, M>(e, s, c->mrow0, c->d.row_end, c->d.nx, c->d.ny, c->d.row_begin, c->rows, c->pitch, c->d.dt,
+    fdtd::launch_materials<double, M>(e, s, c->mrow0, c->mrow_end, c->d.nx, c->d.ny, c->d.row_begin, ROW0, (int)c->nrows_alloc, c->pitch, c->d.dt,
                                       (double*)c->coef[0], (double*)c->coef[1], c->stream);
   else
-    fdtd::launch_materials<float, M>(e, s, c->mrow0, c->d.row_end, c->d.nx, c->d.ny, c->d.row_begin, c->rows, c->pitch, c->d.dt,
+    fdtd::launch_materials<float, M>(e, s, c->mrow0, c->mrow_end, c->d.nx, c->d.ny, c->d.row_begin, ROW0, (int)c->nrows_alloc, c->pitch, c->d.dt,
                                      (float*)c->coef[0], (float*)c->coef[1], c->stream);
   CK(cudaGetLastError());
   return FDTD_OK;
@@ -623,7 +700,9 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
   if (rb < 0 || re > d.ny || re <= rb) return FDTD_E_ARG;
   if (re - rb > (int64_t)1 << 30) return FDTD_E_ARG;
   if (nranks > 1 && !d.nccl_id && !(d.flags & FDTD_LOCAL_GROUP)) return FDTD_E_ARG;
-  const int64_t m0 = std::max<int64_t>(rb - 1, 0);
+  // materials of rows [rb-2, re+1) (clipped to the grid): the two-step sweep reads two ghost rows
+  // below and one above the slab
+  const int64_t m0 = std::max<int64_t>(rb - 2, 0), m1 = std::min<int64_t>(re + 1, d.ny);
   if (d.materials_row0 > m0) return FDTD_E_ARG;
 
   c = new fdtd_ctx();
@@ -635,7 +714,7 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
   c->es = d.precision == 64 ? 8 : 4;
   c->V = 16 / (int)c->es;
   c->rows = (int)(re - rb);
-  c->nrows_alloc = c->rows + 3;
+  c->nrows_alloc = c->rows + 5;
   c->ncolv = (int)((d.nx + c->V - 1) / c->V);
   const int64_t align = 128 / (int64_t)c->es;
   c->pitch = ((int64_t)c->ncolv * c->V + align - 1) / align * align;
@@ -648,7 +727,8 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
 
   // eq.(1) with c_max from the smallest eps_r (host check needs the values; device arrays
   // are reduced on the host after a copy of the owned rows)
-  const int64_t nmat = (re - m0) * d.nx;
+  const int64_t nmat = (m1 - m0) * d.nx;
+  c->mrow_end = m1;
   const bool f32 = (d.flags & FDTD_MATERIALS_F32) != 0;
   const bool on_dev = (d.flags & FDTD_MATERIALS_ON_DEVICE) != 0;
   const size_t mes = f32 ? 4 : 8;
@@ -940,11 +1020,11 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
   if (c->prec == 64) {
     double* fl[6] = {(double*)c->f[0][0], (double*)c->f[0][1], (double*)c->f[0][2],
                      (double*)c->f[1][0], (double*)c->f[1][1], (double*)c->f[1][2]};
-    fdtd::launch_mask<double>((double*)c->coef[0], fl, P_, drect, count, c->d.row_begin, true, c->stream);
+    fdtd::launch_mask<double>((double*)c->coef[0], fl, P_, drect, count, c->d.row_begin, ROW0, true, c->stream);
   } else {
     float* fl[6] = {(float*)c->f[0][0], (float*)c->f[0][1], (float*)c->f[0][2],
                     (float*)c->f[1][0], (float*)c->f[1][1], (float*)c->f[1][2]};
-    fdtd::launch_mask<float>((float*)c->coef[0], fl, P_, drect, count, c->d.row_begin, true, c->stream);
+    fdtd::launch_mask<float>((float*)c->coef[0], fl, P_, drect, count, c->d.row_begin, ROW0, true, c->stream);
   }
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(c->stream));
@@ -980,7 +1060,7 @@ fdtd_status fdtd_set_probes(fdtd_ctx* c, const int64_t* ij, int32_t n) {
   std::vector<int64_t> idx(std::max(n, 1), 0);
   // probes outside this rank read a dedicated always-zero slot (ghost row above, column 0 is never
   // written for Hz); they contribute 0 to the cross-rank sum
-  const int64_t zero_slot = (int64_t)(c->rows + 1) * c->pitch + c->pitch - 1;
+  const int64_t zero_slot = (int64_t)(ROW0 + c->rows + 1) * c->pitch + c->pitch - 1;  // Hz never written there
   for (int32_t k = 0; k < n; ++k) {
     const int64_t i = ij[2 * k], j = ij[2 * k + 1];
     if (i < 0 || i >= c->d.nx || j < 0 || j >= c->d.ny) return fail(c, FDTD_E_ARG, "probe %d outside grid", k);
@@ -1016,6 +1096,10 @@ fdtd_status fdtd_step(fdtd_ctx* c, int64_t nsteps) {
     return fail(c, FDTD_E_STATE, "unread records would exceed record_capacity (%lld)", (long long)c->cap);
   if (c->d.flags & FDTD_LOCAL_GROUP) return fail(c, FDTD_E_STATE, "members of a local group step with fdtd_step_group");
   const bool use_graph = !(c->d.flags & FDTD_NO_GRAPH) && c->d.nranks == 1 && !c->profiling;
+  {
+    fdtd_status st0 = agree_tb2(c);
+    if (st0 != FDTD_OK) return st0;
+  }
   const bool pairs = tb2_active(c);
   fdtd_status st;
   int64_t left = nsteps;
@@ -1158,11 +1242,11 @@ static fdtd_status window_io(fdtd_ctx* c, int64_t i0, int64_t j0, int64_t w, int
     if (c->prec == 64) {
       double* fl[6] = {(double*)c->f[q][0], (double*)c->f[q][1], (double*)c->f[q][2],
                        (double*)c->f[q][0], (double*)c->f[q][1], (double*)c->f[q][2]};
-      fdtd::launch_mask<double>(nullptr, fl, c->pitch, drect, nr, rb, false, c->stream);
+      fdtd::launch_mask<double>(nullptr, fl, c->pitch, drect, nr, rb, ROW0, false, c->stream);
     } else {
       float* fl[6] = {(float*)c->f[q][0], (float*)c->f[q][1], (float*)c->f[q][2],
                       (float*)c->f[q][0], (float*)c->f[q][1], (float*)c->f[q][2]};
-      fdtd::launch_mask<float>(nullptr, fl, c->pitch, drect, nr, rb, false, c->stream);
+      fdtd::launch_mask<float>(nullptr, fl, c->pitch, drect, nr, rb, ROW0, false, c->stream);
     }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
@@ -1224,18 +1308,28 @@ fdtd_status fdtd_step_group(fdtd_ctx** g, int32_t n, int64_t nsteps) {
     if (c->steps + nsteps - oldest > c->cap) return fail(c, FDTD_E_STATE, "unread records would overflow");
   }
   cudaStream_t s = g[0]->stream;
-  for (int64_t t = 0; t < nsteps; ++t) {
+  bool pairs = true;  // two-step passes only if every slab can
+  for (int k = 0; k < n; ++k) {
+    g[k]->tb2_dirty = false;
+    g[k]->tb2_all = g[k]->tb2_want && g[k]->tb2_ok;
+    pairs = pairs && g[k]->tb2_all;
+  }
+  for (int k = 0; k < n; ++k) g[k]->tb2_all = pairs;
+  int64_t left = nsteps;
+  while (left > 0) {
+    const bool pr = pairs && left >= 2;
     const int q = g[0]->cur;
     for (int k = 0; k < n; ++k) {
-      fdtd_status st = halo_local(g, n, k, q, s);
+      fdtd_status st = halo_local(g, n, k, q, s, pr ? 2 : 1);
       if (st != FDTD_OK) return st;
     }
     for (int k = 0; k < n; ++k) {
-      fdtd_status st = enqueue_step(g[k], q, s);
+      fdtd_status st = pr ? enqueue_pair(g[k], q, s) : enqueue_step(g[k], q, s);
       if (st != FDTD_OK) return st;
-      g[k]->steps++;
+      g[k]->steps += pr ? 2 : 1;
       g[k]->cur ^= 1;
     }
+    left -= pr ? 2 : 1;
   }
   fdtd_ctx* c = g[0];
   CK(cudaGetLastError());

@@ -98,8 +98,8 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepParams<T> p) {
   const bool act = colv < p.ncolv;
   const int64_t c = (int64_t)colv * V;
   const int cy = p.chunk0 + blockIdx.y;  // row chunk
-  const int r0 = 1 + cy * p.chunk;
-  const int r1 = min(r0 + p.chunk, p.rows + 1);
+  const int r0 = p.row0 + cy * p.chunk;
+  const int r1 = min(r0 + p.chunk, p.row0 + p.rows);
   const int64_t P = p.pitch;
 
   T src = T(0);
@@ -247,8 +247,9 @@ __global__ void __maxnreg__(96) sweep2_kernel(const SweepParams<T> p) {
   const bool act = colv >= 0 && colv < p.ncolv;
   const bool out = act && lane >= 1 && lane <= 30;
   const int64_t c = (int64_t)colv * V;
-  const int r0 = 1 + blockIdx.y * p.chunk;
-  const int r1 = min(r0 + p.chunk, p.rows + 1);
+  const int cy = p.chunk0 + blockIdx.y;  // row chunk
+  const int r0 = p.row0 + cy * p.chunk;
+  const int r1 = min(r0 + p.chunk, p.row0 + p.rows);
   const int64_t P = p.pitch;
 
   T g0 = T(0), g1 = T(0);
@@ -421,7 +422,7 @@ __global__ void __maxnreg__(96) sweep2_kernel(const SweepParams<T> p) {
     if (threadIdx.x == 0) {
       double s0 = 0.0, s1 = 0.0;
       for (int w = 0; w < wpc; ++w) { s0 += red0[w]; s1 += red1[w]; }
-      const int64_t b = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+      const int64_t b = (int64_t)cy * gridDim.x + blockIdx.x;
       p.partials[b] = s0;
       p.partials2[b] = s1;
     }
@@ -722,7 +723,7 @@ __device__ void rom_batch2(const PostParams<T>& p, int bi, T* sv, T g0, T g1, do
     EX = MS + Hr * Wr;
     EY = EX + (Hr + 1) * Wr;
   };
-  auto goff = [&](int gi, int gj) { return ((int64_t)gj - p.row_begin + 1) * P + gi; };
+  auto goff = [&](int gi, int gj) { return ((int64_t)gj - p.row_begin + p.row0) * P + gi; };
   const bool src_on = p.src_row >= 0;
   const int64_t src_off = src_on ? (int64_t)p.src_row * P + p.src_col : -1;
   // ---- R1: load the region (materials, E^n, the sweep's Hz^{n+3/2} into H2)
@@ -1038,11 +1039,12 @@ __global__ void __launch_bounds__(256) post_kernel(const PostParams<T> p) {
 // ---------------------------------------------------------------- setup kernels
 template <typename T, typename M>
 __global__ void material_kernel(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t mat_row_end, int64_t nx,
-                                int64_t ny, int64_t row_begin, int rows, int64_t pitch, double dt, T* mea, T* msb) {
+                                int64_t ny, int64_t row_begin, int row0, int nrows_alloc, int64_t pitch, double dt,
+                                T* mea, T* msb) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int jl = blockIdx.y;  // local row 0..rows+1 (0: ghost row below, rows+1: ghost row above)
-  if (i >= pitch || jl > rows + 1) return;
-  const int64_t g = row_begin + jl - 1;
+  const int jl = blockIdx.y;  // every local row, ghost rows included
+  if (i >= pitch || jl >= nrows_alloc) return;
+  const int64_t g = row_begin + jl - row0;
   const int64_t o = (int64_t)jl * pitch + i;
   if (g < 0 || g >= ny || i >= nx || g < mat_row0 || g >= mat_row_end) {
     mea[o] = T(-1);  // outside the grid / not provided: walls and padding (edges next to it stay put)
@@ -1066,10 +1068,10 @@ __global__ void gather_mat_kernel(const M* eps_r, const M* sigma, int64_t nx, in
 
 template <typename T>
 __global__ void mask_kernel(T* mea, T* f0, T* f1, T* f2, T* f3, T* f4, T* f5, int64_t pitch, const int32_t* rects,
-                            int64_t row_begin, bool zero_iface) {
+                            int64_t row_begin, int row0, bool zero_iface) {
   const int32_t* r = rects + 4 * (int64_t)blockIdx.x;
   const int i0 = r[0], bx = r[2], by = r[3];
-  const int64_t jl0 = (int64_t)r[1] - row_begin + 1;  // local row of the block's bottom cells
+  const int64_t jl0 = (int64_t)r[1] - row_begin + row0;  // local row of the block's bottom cells
   T* ex[2] = {f0, f3};
   T* ey[2] = {f1, f4};
   T* hz[2] = {f2, f5};
@@ -1140,10 +1142,15 @@ void launch_sweep(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s, in
 }
 
 template <typename T>
-void launch_sweep2(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s) {
-  dim3 grid(sweep2_ctas_x(p.ncolv, warps_per_cta), (p.rows + p.chunk - 1) / p.chunk);
-  if (p.partials) sweep2_kernel<T, true><<<grid, 32 * warps_per_cta, 0, s>>>(p);
-  else sweep2_kernel<T, false><<<grid, 32 * warps_per_cta, 0, s>>>(p);
+void launch_sweep2(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s, int chunk_begin, int chunk_count) {
+  const int nch = (p.rows + p.chunk - 1) / p.chunk;
+  if (chunk_count < 0) chunk_count = nch - chunk_begin;
+  if (chunk_count <= 0) return;
+  SweepParams<T> q = p;
+  q.chunk0 = chunk_begin;
+  dim3 grid(sweep2_ctas_x(p.ncolv, warps_per_cta), chunk_count);
+  if (p.partials) sweep2_kernel<T, true><<<grid, 32 * warps_per_cta, 0, s>>>(q);
+  else sweep2_kernel<T, false><<<grid, 32 * warps_per_cta, 0, s>>>(q);
 }
 
 size_t post_smem_bytes(size_t es, int nvec, int batch, bool staged) {
@@ -1179,10 +1186,11 @@ void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s) {
 
 template <typename T, typename M>
 void launch_materials(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t mat_row_end, int64_t nx, int64_t ny,
-                      int64_t row_begin, int rows, int64_t pitch, double dt, T* mea, T* msb, cudaStream_t s) {
-  dim3 grid((unsigned)((pitch + 255) / 256), rows + 2);
-  material_kernel<T, M><<<grid, 256, 0, s>>>(eps_r, sigma, mat_row0, mat_row_end, nx, ny, row_begin, rows, pitch, dt,
-                                             mea, msb);
+                      int64_t row_begin, int row0, int nrows_alloc, int64_t pitch, double dt, T* mea, T* msb,
+                      cudaStream_t s) {
+  dim3 grid((unsigned)((pitch + 255) / 256), nrows_alloc);
+  material_kernel<T, M><<<grid, 256, 0, s>>>(eps_r, sigma, mat_row0, mat_row_end, nx, ny, row_begin, row0,
+                                             nrows_alloc, pitch, dt, mea, msb);
 }
 
 template <typename M>
@@ -1193,23 +1201,24 @@ void launch_gather_materials(const M* eps_r, const M* sigma, int64_t nx, int64_t
 }
 
 template <typename T>
-void launch_mask(T* mea, T* f[6], int64_t pitch, const int32_t* rects, int64_t n_rect, int64_t row_begin,
+void launch_mask(T* mea, T* f[6], int64_t pitch, const int32_t* rects, int64_t n_rect, int64_t row_begin, int row0,
                  bool zero_iface, cudaStream_t s) {
   if (n_rect <= 0) return;
   mask_kernel<T><<<(unsigned)n_rect, 256, 0, s>>>(mea, f[0], f[1], f[2], f[3], f[4], f[5], pitch, rects, row_begin,
-                                                   zero_iface);
+                                                   row0, zero_iface);
 }
 
 #define INST(T)                                                                                     \
   template void launch_sweep<T>(const SweepParams<T>&, int, cudaStream_t, int, int);              \
-  template void launch_sweep2<T>(const SweepParams<T>&, int, cudaStream_t);                       \
+  template void launch_sweep2<T>(const SweepParams<T>&, int, cudaStream_t, int, int);             \
   template void launch_post<T>(const PostParams<T>&, bool, cudaStream_t);                        \
   template void launch_post2<T>(const PostParams<T>&, bool, cudaStream_t);                       \
   template void launch_materials<T, float>(const float*, const float*, int64_t, int64_t, int64_t, int64_t, \
-                                           int64_t, int, int64_t, double, T*, T*, cudaStream_t);          \
+                                           int64_t, int, int, int64_t, double, T*, T*, cudaStream_t);     \
   template void launch_materials<T, double>(const double*, const double*, int64_t, int64_t, int64_t,      \
-                                            int64_t, int64_t, int, int64_t, double, T*, T*, cudaStream_t);\
-  template void launch_mask<T>(T*, T* [6], int64_t, const int32_t*, int64_t, int64_t, bool, cudaStream_t);
+                                            int64_t, int64_t, int, int, int64_t, double, T*, T*,          \
+                                            cudaStream_t);                                                \
+  template void launch_mask<T>(T*, T* [6], int64_t, const int32_t*, int64_t, int64_t, int, bool, cudaStream_t);
 INST(float)
 INST(double)
 template void launch_gather_materials<float>(const float*, const float*, int64_t, int64_t,

@@ -15,7 +15,8 @@ struct SweepParams {
   const T* mea; const T* msb;  // per cell: eps0 eps_r / (2 dt) (< 0: hole / wall / dead) and sigma / 4
   int64_t pitch;   // elements per row (all arrays)
   int ncolv;       // vector columns processed (16-byte vectors)
-  int rows;        // owned cell rows (local rows 1..rows; local row 0 is the ghost row below)
+  int rows;        // owned cell rows: local rows row0 .. row0+rows-1
+  int row0;        // local row of the first owned row (ROW0 = 2: two ghost rows below)
   int chunk;       // rows per CTA
   int chunk0;      // first row chunk of this launch (split launches overlap the halo exchange)
   T chx, chy;      // dt/(mu0 dx), dt/(mu0 dy)
@@ -64,6 +65,7 @@ struct PostParams {
   // ---- two-step mode (post2): fix-up around every instance after sweep2 (K3b)
   const int32_t* rects;            // per instance (i0, j0, bx, by), global
   int64_t row_begin, pitch;
+  int row0;                        // local row of global row row_begin
   const T* ex0; const T* ey0; const T* hz0;  // fields at step n (the sweep's input buffer)
   const T* mea; const T* msb;
   T chx, chy, idx, idy, wh;
@@ -77,7 +79,8 @@ void launch_sweep(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s, in
                   int chunk_count = -1);
 // two time steps per pass (temporal blocking; 30 output lanes per warp)
 template <typename T>
-void launch_sweep2(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s);
+void launch_sweep2(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s, int chunk_begin = 0,
+                   int chunk_count = -1);
 inline int sweep2_ctas_x(int ncolv, int warps_per_cta) {
   const int nw = (ncolv + 29) / 30;
   return (nw + warps_per_cta - 1) / warps_per_cta;
@@ -93,7 +96,8 @@ size_t post2_smem_bytes(size_t es, int nvec, int batch, int region_stride, bool 
 // setup kernels
 template <typename T, typename M>
 void launch_materials(const M* eps_r, const M* sigma, int64_t mat_row0, int64_t mat_row_end, int64_t nx, int64_t ny,
-                      int64_t row_begin, int rows, int64_t pitch, double dt, T* mea, T* msb, cudaStream_t s);
+                      int64_t row_begin, int row0, int nrows_alloc, int64_t pitch, double dt, T* mea, T* msb,
+                      cudaStream_t s);
 template <typename M>
 void launch_gather_materials(const M* eps_r, const M* sigma, int64_t nx, int64_t mat_row0,
                              const int64_t* cells /*global j*nx+i*/, int64_t n, double* out_eps,
@@ -102,6 +106,6 @@ template <typename M>
 void launch_min2(const M* a, const M* b, int64_t n, double* out /*2 per block*/, int nblocks, cudaStream_t s);
 template <typename T>
 void launch_mask(T* mea, T* fields[6], int64_t pitch, const int32_t* rects, int64_t n_rect, int64_t row_begin,
-                 bool zero_iface, cudaStream_t s);
+                 int row0, bool zero_iface, cudaStream_t s);
 
 }  // namespace fdtd

@@ -14,7 +14,7 @@ def slab_rows(ny, nranks, rank):
 
 
 def owned_placements(placements, models, row_begin, row_end):
-    """Placements (model, i0, j0) whose rows j0-1 .. j0+by lie in [row_begin, row_end)."""
+    """Placements (model, i0, j0) whose footprint + ring rows j0-1 .. j0+by lie in [row_begin, row_end)."""
     if placements is None or len(placements) == 0:
         return np.zeros((0, 3), dtype=np.int32)
     P = np.asarray(placements)

@@ -44,7 +44,7 @@ def run_single(s, n, init):
     return out
 
 
-def run_group(s, n, init, nslab):
+def run_group(s, n, init, nslab, spp=2):
     import torch
 
     from paper_1609_07114_b200 import Simulation, step_group
@@ -56,8 +56,8 @@ def run_group(s, n, init, nslab):
     sims, local = [], []
     for k in range(nslab):
         rb, re = slabs.slab_rows(s.ny, nslab, k)
-        m0 = max(rb - 1, 0)
-        sim = Simulation(s.nx, s.ny, s.dx, s.dy, s.dt, s.eps_r[m0:re], s.sigma[m0:re], precision=s.precision,
+        m0, m1 = max(rb - 2, 0), min(re + 1, s.ny)
+        sim = Simulation(s.nx, s.ny, s.dx, s.dy, s.dt, s.eps_r[m0:m1], s.sigma[m0:m1], precision=s.precision,
                          stream=stream, rank=k, nranks=nslab, row_begin=rb, row_end=re, materials_row0=m0,
                          local_group=True)
         mine = []
@@ -70,6 +70,7 @@ def run_group(s, n, init, nslab):
         sim.set_source(*s.source, s.samples)
         sim.set_probes(s.probes)
         sim.record_energy(True)
+        sim.set_time_blocking(spp)
         sim.set_window(0, 0, Ex, Ey, Hz)
         idx = [next(t for t, (mm, a, b) in enumerate(glob) if (a, b) == (i0, j0)) for _, i0, j0 in mine]
         if idx:
@@ -77,6 +78,7 @@ def run_group(s, n, init, nslab):
         sims.append(sim)
         local.append(idx)
     step_group(sims, n)
+    assert all(sim.info().steps_per_pass == spp for sim in sims)
     F = [np.zeros((s.ny + 1, s.nx)), np.zeros((s.ny, s.nx + 1)), np.zeros((s.ny, s.nx))]
     xs_out = np.zeros_like(xs)
     pr, en = 0, 0
@@ -96,14 +98,16 @@ def run_group(s, n, init, nslab):
     return tuple(F), xs_out, pr, en
 
 
+@pytest.mark.parametrize("spp", [1, 2])
 @pytest.mark.parametrize("nslab", [2, 3, 4])
 @pytest.mark.parametrize("precision", [32, 64])
-def test_slabs_bitwise_equal_single(nslab, precision):
+def test_slabs_bitwise_equal_single(nslab, precision, spp):
+    """spp = 1: one-step passes with 1-row halos; spp = 2: two-step passes with 2-row halos."""
     s = slab_scene(precision)
     assert slabs.check_partition(s.placements, s.models, s.ny, nslab)
     init = consistent_random_state(s, 3)
-    (W1, x1, p1, e1) = run_single(s, 300, init)
-    (W2, x2, p2, e2) = run_group(s, 300, init, nslab)
+    (W1, x1, p1, e1) = run_single(s, 301, init)
+    (W2, x2, p2, e2) = run_group(s, 301, init, nslab, spp)
     for a, b in zip(W1, W2):
         assert np.array_equal(a, b)
     assert np.array_equal(x1, x2)
