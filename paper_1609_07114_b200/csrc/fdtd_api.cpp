@@ -116,7 +116,6 @@ struct fdtd_ctx {
   std::vector<double> mpool;                // shared model matrices (col-major, fp64)
   int nvec = 1;
   int rom_batch = 16;
-  bool rom_staged = true;
   std::vector<int32_t> batch_tab;  // (model, first instance, count)
   int32_t* d_batch_tab = nullptr;
   // device ROM arrays
@@ -257,7 +256,6 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q, bool pair = false) {
   p.batch = c->rom_batch;
   p.batch_tab = c->d_batch_tab;
   p.block = 256;
-  p.staged = c->rom_staged ? 1 : 0;
   p.level1 = c->d_level1;
   p.level1b = c->d_level1b;
   p.rects = c->d_rects;
@@ -616,12 +614,9 @@ fdtd_status upload_roms(fdtd_ctx* c) {
   {
     const char* env = getenv("FDTD_ROM_BATCH");
     int B = env ? std::max(1, std::min(64, atoi(env))) : 8;
-    // operators are staged in shared memory when two of them fit next to the batch vectors
-    c->rom_staged = fdtd::post_smem_bytes(c->es, c->nvec, 1, true) <= 200 * 1024;
-    const bool stg = c->rom_staged;
     auto fits = [&](int b, size_t lim) {
-      return fdtd::post2_smem_bytes(c->es, c->nvec, b, c->region_stride, stg) <= lim &&
-             fdtd::post_smem_bytes(c->es, c->nvec, b, stg) <= lim;
+      return fdtd::post2_smem_bytes(c->es, c->nvec, b, c->region_stride) <= lim &&
+             fdtd::post_smem_bytes(c->es, c->nvec, b) <= lim;
     };
     while (B > 1 && !fits(B, 110 * 1024)) B = B > 4 ? B - 4 : B / 2;
     if (!fits(B, 110 * 1024)) {
@@ -942,18 +937,48 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
   Mat R11dt(R11), R22dt(R22);
   for (auto& v : R11dt) v /= dt;
   for (auto& v : R22dt) v /= dt;
+  // fused operators (K3): x = [E~; H~]
+  //   M1 = [[Q1, I], [Aq', Kq], [-Lt Aq', -Lt Kq]] with Aq' = Aq + Kq Q1;  M2 = [Bq; Lt Bq];  Rt = R~
+  const int nxs = q1 + q2, m1 = q2 + q1 + nY, m2 = q1 + nY;
+  Mat Aqp = dense::matmul(Kq, Q1, q1, q2, q1);
+  for (int i = 0; i < q1 * q1; ++i) Aqp[i] += Aq[i];
+  Mat LtAqp = dense::matmul(Lt, Aqp, nY, q1, q1);
+  Mat LtKq = dense::matmul(Lt, Kq, nY, q1, q2);
+  Mat M1 = dense::zeros(m1, nxs);
+  for (int i = 0; i < q2; ++i) {
+    for (int j = 0; j < q1; ++j) M1[(size_t)i * nxs + j] = Q1[(size_t)i * q1 + j];
+    M1[(size_t)i * nxs + q1 + i] = 1.0;
+  }
+  for (int i = 0; i < q1; ++i) {
+    for (int j = 0; j < q1; ++j) M1[(size_t)(q2 + i) * nxs + j] = Aqp[(size_t)i * q1 + j];
+    for (int j = 0; j < q2; ++j) M1[(size_t)(q2 + i) * nxs + q1 + j] = Kq[(size_t)i * q2 + j];
+  }
+  for (int i = 0; i < nY; ++i) {
+    for (int j = 0; j < q1; ++j) M1[(size_t)(q2 + q1 + i) * nxs + j] = -LtAqp[(size_t)i * q1 + j];
+    for (int j = 0; j < q2; ++j) M1[(size_t)(q2 + q1 + i) * nxs + q1 + j] = -LtKq[(size_t)i * q2 + j];
+  }
+  Mat M2 = dense::zeros(m2, nY);
+  for (int i = 0; i < q1; ++i)
+    for (int j = 0; j < nY; ++j) M2[(size_t)i * nY + j] = Bq[(size_t)i * nY + j];
+  for (int i = 0; i < nY; ++i)
+    for (int j = 0; j < nY; ++j) M2[(size_t)(q1 + i) * nY + j] = P[(size_t)i * nY + j];
+  Mat Rt = dense::zeros(nxs, nxs);
+  for (int i = 0; i < q1; ++i)
+    for (int j = 0; j < q1; ++j) Rt[(size_t)i * nxs + j] = R11dt[(size_t)i * q1 + j];
+  for (int i = 0; i < q2; ++i)
+    for (int j = 0; j < q2; ++j) Rt[(size_t)(q1 + i) * nxs + q1 + j] = R22dt[(size_t)i * q2 + j];
+  for (int i = 0; i < q1; ++i)
+    for (int j = 0; j < q2; ++j) {
+      Rt[(size_t)i * nxs + q1 + j] = -0.5 * K[(size_t)i * q2 + j];
+      Rt[(size_t)(q1 + j) * nxs + i] = -0.5 * K[(size_t)i * q2 + j];
+    }
   mh.dev.nY = nY; mh.dev.q1 = q1; mh.dev.q2 = q2;
-  mh.dev.off_Q1 = push(Q1, q2, q1);
-  mh.dev.off_Aq = push(Aq, q1, q1);
-  mh.dev.off_Kq = push(Kq, q1, q2);
-  mh.dev.off_Lt = push(Lt, nY, q1);
-  mh.dev.off_Bq = push(Bq, q1, nY);
-  mh.dev.off_R11 = push(R11dt, q1, q1);
-  mh.dev.off_R22 = push(R22dt, q2, q2);
-  mh.dev.off_K = push(K, q1, q2);
+  mh.dev.off_M1 = push(M1, m1, nxs);
+  mh.dev.off_M2 = push(M2, m2, nY);
+  mh.dev.off_Rt = push(Rt, nxs, nxs);
   const int mid = (int)c->models.size();
   c->models.push_back(mh);
-  c->nvec = std::max(c->nvec, std::max(nY, std::max(q1, q2)));
+  c->nvec = std::max(c->nvec, q1 + q2 + nY);
 
   // ---- per instance: outside-cell materials -> c_y, a_y, Schur inverse S_k
   std::vector<int64_t> cells;

@@ -443,50 +443,20 @@ __device__ double block_sum(double v, double* red) {
   return s;  // valid in thread 0
 }
 
-// ---- asynchronous global -> shared copies (cp.async, sm_80+; SASS LDGSTS)
-__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-// Stage n elements (16-byte aligned source and destination) into shared memory; one commit group.
-template <typename T>
-__device__ __forceinline__ void stage(T* dst, const T* src, int n) {
-  constexpr int V = 16 / sizeof(T);
-  const int nv = n / V;
-  for (int k = threadIdx.x; k < nv; k += blockDim.x) cp_async16(dst + k * V, src + k * V);
-  for (int k = nv * V + threadIdx.x; k < n; k += blockDim.x) {
-    if (sizeof(T) == 8) cp_async8(dst + k, src + k);
-    else cp_async4(dst + k, src + k);
-  }
-  cp_commit();
-}
-
 // Y[i][b] += alpha * sum_c A[c*m + i] X[c][b] for i < m, b < B.  A is a shared model operator
-// staged in shared memory (column-major); X, Y in shared memory with row stride B (B % 4 == 0).
-// Each thread item owns one row i and IPI consecutive instances.
+// (column-major, L2-resident: one coalesced 128-byte row of A per warp and column, reused for the
+// IPI instances of a thread's item); X, Y in shared memory with row stride B.
 template <typename T, int IPI>
-__device__ __forceinline__ void bgemm_ipi(const T* A, int m, int k, const T* X, T* Y, int B, T alpha) {
+__device__ __forceinline__ void bgemm_ipi(const T* __restrict__ A, int m, int k, const T* X, T* Y, int B, T alpha) {
   const int G = B / IPI;
   for (int it = threadIdx.x; it < m * G; it += blockDim.x) {
     const int i = it % m, g = (it / m) * IPI;
     T acc[IPI];
 #pragma unroll
     for (int u = 0; u < IPI; ++u) acc[u] = T(0);
-#pragma unroll 8
+#pragma unroll 16
     for (int c = 0; c < k; ++c) {
-      const T a = A[c * m + i];
+      const T a = __ldg(A + (int64_t)c * m + i);
       const T* x = X + c * B + g;
 #pragma unroll
       for (int u = 0; u < IPI; ++u) acc[u] = fma_rn(a, x[u], acc[u]);
@@ -504,139 +474,96 @@ __device__ __forceinline__ void bgemm(const T* A, int m, int k, const T* X, T* Y
   else bgemm_ipi<T, 1>(A, m, k, X, Y, B, alpha);
 }
 
-// One ROM step for a batch of nb (<= B) instances of one model (K3).  On entry sy (y^n),
-// sh (h = Hz^{n+1/2} of the outside cells), sE, sH (x~^n) hold the batch's vectors in shared
-// memory (row stride B, zero padding for b >= nb).  On exit sy holds y^{n+1} and sE, sH hold
-// x~^{n+1}; with ENERGY the ROM part of W^n (coarse half cells + x~^T R~ x~) of instance b is in
-// eout[b].  The model operators are streamed through two shared-memory buffers (cp.async double
-// buffering): while phase p computes from one buffer, the operator of phase p+1 is in flight.
+// Shared-memory vectors of a batch (row stride B, NV rows each):
+//   sx = [E~; H~] (q1 + q2), sy = y (nY), sh = h (nY), so = M1 x (q2 + q1 + nY),
+//   st = t (nY), sU = U (nY), so2 = [E~; y] (q1 + nY)
+template <typename T>
+struct RomVec {
+  T *sx, *sy, *sh, *so, *st, *sU, *so2;
+  __device__ RomVec(T* sv, int64_t S) : sx(sv), sy(sv + S), sh(sv + 2 * S), so(sv + 3 * S), st(sv + 4 * S),
+                                         sU(sv + 5 * S), so2(sv + 6 * S) {}
+};
+
+// One ROM step for a batch of nb (<= B) instances of one model (eq:connExplicit, K3).
+// On entry sx (x~^n), sy (y^n), sh (h = Hz^{n+1/2} of the outside cells) hold the batch's vectors
+// (zero padding for b >= nb).  On exit sx holds x~^{n+1} and sy holds y^{n+1}; with ENERGY the ROM
+// part of W^n (coarse half cells + x~^T R~ x~) of instance b is in eout[b].
 template <typename T, bool ENERGY>
-__device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first, int nb, T* sv, T* const* buf,
-                         double* eout) {
-  const int nY = m.nY, q1 = m.q1, q2 = m.q2;
-  const int B = p.batch, NV = p.nthreads_vec;
+__device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first, int nb, T* sv, double* eout) {
+  const int nY = m.nY, q1 = m.q1, q2 = m.q2, nx = q1 + q2, m1 = q2 + q1 + nY, m2 = q1 + nY;
+  const int B = p.batch;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int64_t S = (int64_t)NV * B;
-  T* sy = sv;
-  T* sh = sy + S;
-  T* sE = sh + S;
-  T* sH = sE + S;
-  T* sEs = sH + S;
-  T* st = sEs + S;
-  T* sU = st + S;
+  const int64_t S = (int64_t)p.nthreads_vec * B;
+  RomVec<T> v(sv, S);
   const T* mp = p.mpool;
-  const T* op[9];
-  int om[9], ok[9], nop = 0;
-  auto add = [&](int64_t off, int r, int c) { op[nop] = mp + off; om[nop] = r; ok[nop] = c; ++nop; };
-  if (ENERGY) { add(m.off_R11, q1, q1); add(m.off_R22, q2, q2); add(m.off_K, q1, q2); }
-  add(m.off_Q1, q2, q1); add(m.off_Aq, q1, q1); add(m.off_Kq, q1, q2); add(m.off_Lt, nY, q1);
-  add(m.off_Bq, q1, nY); add(m.off_Lt, nY, q1);
-  int ph = 0;
-  const bool staged = p.staged != 0;
-  if (staged) stage<T>(buf[0], op[0], om[0] * ok[0]);
-  auto next = [&]() -> const T* {  // start staging operator ph+1, wait for operator ph
-    if (!staged) {                   // large models: operators stay in L2/global memory
-      __syncthreads();
-      return op[ph];
-    }
-    if (ph + 1 < nop) {
-      stage<T>(buf[(ph + 1) & 1], op[ph + 1], om[ph + 1] * ok[ph + 1]);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncthreads();
-    return buf[ph & 1];
-  };
-  auto done = [&]() { __syncthreads(); ++ph; };
-  for (int64_t k = tid; k < 3 * S; k += nt) sEs[k] = T(0);  // sEs, st, sU
+  for (int64_t k = tid; k < S; k += nt) { v.so[k] = T(0); v.so2[k] = T(0); }
   __syncthreads();
-  if (ENERGY) {  // W_rom = sum D_l D_l' eps/dt y^2 + E~^T (R~11/dt) E~ + H~^T (R~22/dt) H~ - E~^T K~ H~
-    const T* A = next();
-    bgemm<T>(A, q1, q1, sE, sEs, B, T(1));
-    done();
-    A = next();
-    bgemm<T>(A, q2, q2, sH, st, B, T(1));
-    done();
-    A = next();
-    bgemm<T>(A, q1, q2, sH, sEs, B, T(-1));
-    done();
+  if (ENERGY) {  // x~^T Rt x~ + sum D_l D_l' eps/dt y^2
+    bgemm<T>(mp + m.off_Rt, nx, nx, v.sx, v.so, B, T(1));
+    __syncthreads();
     const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
     for (int b = w; b < nb; b += nw) {
       const int64_t po = p.port_off[first + b];
       double acc = 0.0;
-      for (int i = lane; i < nY; i += 32) acc += p.ehalf[po + i] * (double)sy[i * B + b] * (double)sy[i * B + b];
-      for (int i = lane; i < q1; i += 32) acc += (double)sE[i * B + b] * (double)sEs[i * B + b];
-      for (int i = lane; i < q2; i += 32) acc += (double)sH[i * B + b] * (double)st[i * B + b];
+      for (int i = lane; i < nY; i += 32) acc += p.ehalf[po + i] * (double)v.sy[i * B + b] * (double)v.sy[i * B + b];
+      for (int i = lane; i < nx; i += 32) acc += (double)v.sx[i * B + b] * (double)v.so[i * B + b];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
       if (lane == 0) eout[b] = acc;
     }
     __syncthreads();
-    for (int64_t k = tid; k < S; k += nt) { sEs[k] = T(0); st[k] = T(0); }
+    for (int64_t k = tid; k < S; k += nt) v.so[k] = T(0);
+    __syncthreads();
   }
-  // S5 (factored eq:connExplicit):
-  // (1) H~ <- H~ + Q1 E~
-  const T* A = next();
-  bgemm<T>(A, q2, q1, sE, sH, B, T(1));
-  done();
-  // (2) E* = Aq E~ + Kq H~
-  A = next();
-  bgemm<T>(A, q1, q1, sE, sEs, B, T(1));
-  done();
-  A = next();
-  bgemm<T>(A, q1, q2, sH, sEs, B, T(1));
-  done();
-  // (3) t = (a_y/c_y) y + (D_l G/c_y) h - L~^T E*
+  // [H~^{n+1}; E*; -L~^T E*] = M1 x~^n
+  bgemm<T>(mp + m.off_M1, m1, nx, v.sx, v.so, B, T(1));
+  __syncthreads();
+  // t = (a_y/c_y) y + (D_l G/c_y) h - L~^T E*
   for (int it = tid; it < nY * nb; it += nt) {
     const int i = it % nY, b = it / nY;
     const int64_t po = p.port_off[first + b];
-    st[i * B + b] = fma_rn(p.cyg[po + i], sh[i * B + b], mul_rn(p.cya[po + i], sy[i * B + b]));
+    v.st[i * B + b] = v.so[(q2 + q1 + i) * B + b] +
+                      fma_rn(p.cyg[po + i], v.sh[i * B + b], mul_rn(p.cya[po + i], v.sy[i * B + b]));
   }
-  A = next();  // (barrier inside)
-  bgemm<T>(A, nY, q1, sEs, st, B, T(-1));
-  done();
-  // (4) U = S_k t (per-instance Schur inverse, streamed from HBM; many loads in flight)
+  __syncthreads();
+  // U = S_k t (per-instance Schur inverse, streamed from HBM); [E*; -L~^T E*] as the base of M2 U
   for (int it = tid; it < nY * nb; it += nt) {
     const int i = it % nY, b = it / nY;
     const T* Sk = p.Sk + p.Sk_off[first + b] + i;
     T a = T(0);
 #pragma unroll 16
-    for (int c = 0; c < nY; ++c) a = fma_rn(__ldg(Sk + (int64_t)c * nY), st[c * B + b], a);
-    sU[i * B + b] = a;
+    for (int c = 0; c < nY; ++c) a = fma_rn(__ldg(Sk + (int64_t)c * nY), v.st[c * B + b], a);
+    v.sU[i * B + b] = a;
   }
-  for (int64_t k = tid; k < (int64_t)q1 * B; k += nt) sE[k] = sEs[k];
-  // (5) E~ = E* + Bq U
-  A = next();
-  bgemm<T>(A, q1, nY, sU, sE, B, T(1));
-  done();
-  // (6) y^{n+1} = L~^T E~
-  for (int64_t k = tid; k < (int64_t)nY * B; k += nt) sy[k] = T(0);
-  A = next();
-  bgemm<T>(A, nY, q1, sE, sy, B, T(1));
-  done();
+  for (int64_t k = tid; k < (int64_t)m2 * B; k += nt) {
+    const int64_t r = k / B;
+    v.so2[k] = r < q1 ? v.so[(q2 + r) * B + k % B] : -v.so[(q2 + r) * B + k % B];
+  }
+  __syncthreads();
+  // [E~^{n+1}; y^{n+1}] = [E*; L~^T E*] + M2 U
+  bgemm<T>(mp + m.off_M2, m2, nY, v.sU, v.so2, B, T(1));
+  __syncthreads();
+  for (int64_t k = tid; k < (int64_t)nx * B; k += nt) {
+    const int64_t r = k / B;
+    v.sx[k] = r < q1 ? v.so2[k] : v.so[(r - q1) * B + k % B];  // E~ from so2, H~ from so rows 0..q2
+  }
+  for (int64_t k = tid; k < (int64_t)nY * B; k += nt) v.sy[k] = v.so2[(int64_t)q1 * B + k];
+  __syncthreads();
 }
 
 template <typename T>
-__device__ __forceinline__ T* rom_buffers(const PostParams<T>& p, T* sv, T** buf) {
-  const int64_t S = (int64_t)p.nthreads_vec * p.batch;
-  const int64_t NB = p.staged ? ((int64_t)p.nthreads_vec * p.nthreads_vec + 3) / 4 * 4 : 0;  // 16-byte aligned
-  buf[0] = sv + 7 * S;
-  buf[1] = buf[0] + NB;
-  return buf[1] + NB;  // first free element after the ROM area
+__device__ __forceinline__ T* rom_end(const PostParams<T>& p, T* sv) {
+  return sv + 7 * (int64_t)p.nthreads_vec * p.batch;  // first free element after the ROM vectors
 }
 
 template <typename T>
 __device__ void load_rom_state(const PostParams<T>& p, const RomModelDev& m, int first, int nb, T* sv) {
   const int B = p.batch;
-  const int64_t S = (int64_t)p.nthreads_vec * B;
-  T* sE = sv + 2 * S;
-  T* sH = sv + 3 * S;
-  for (int it = threadIdx.x; it < (m.q1 + m.q2) * nb; it += blockDim.x) {
-    const int i = it % (m.q1 + m.q2), b = it / (m.q1 + m.q2);
-    const T v = p.state[p.state_off[first + b] + i];
-    if (i < m.q1) sE[i * B + b] = v;
-    else sH[(i - m.q1) * B + b] = v;
+  T* sx = sv;
+  const int nx = m.q1 + m.q2;
+  for (int it = threadIdx.x; it < nx * nb; it += blockDim.x) {
+    const int i = it % nx, b = it / nx;
+    sx[i * B + b] = p.state[p.state_off[first + b] + i];
   }
 }
 
@@ -645,18 +572,18 @@ __device__ void store_rom(const PostParams<T>& p, const RomModelDev& m, int firs
                           T* ey) {
   const int B = p.batch;
   const int64_t S = (int64_t)p.nthreads_vec * B;
-  const T* sy = sv;
-  const T* sE = sv + 2 * S;
-  const T* sH = sv + 3 * S;
+  const T* sx = sv;
+  const T* sy = sv + S;
   for (int it = threadIdx.x; it < m.nY * nb; it += blockDim.x) {  // S6: scatter y^{n+1}
     const int i = it % m.nY, b = it / m.nY;
     const int64_t e = p.port_edge[p.port_off[first + b] + i];
     if (e >> 62) ey[e & IDX_MASK] = sy[i * B + b];
     else ex[e & IDX_MASK] = sy[i * B + b];
   }
-  for (int it = threadIdx.x; it < (m.q1 + m.q2) * nb; it += blockDim.x) {
-    const int i = it % (m.q1 + m.q2), b = it / (m.q1 + m.q2);
-    p.state[p.state_off[first + b] + i] = i < m.q1 ? sE[i * B + b] : sH[(i - m.q1) * B + b];
+  const int nx = m.q1 + m.q2;
+  for (int it = threadIdx.x; it < nx * nb; it += blockDim.x) {
+    const int i = it % nx, b = it / nx;
+    p.state[p.state_off[first + b] + i] = sx[i * B + b];
   }
 }
 
@@ -667,12 +594,10 @@ __device__ void rom_batch(const PostParams<T>& p, int bi, T* sv) {
   const RomModelDev m = p.models[model];
   const int B = p.batch;
   const int64_t S = (int64_t)p.nthreads_vec * B;
-  T* buf[2];
-  rom_buffers(p, sv, buf);
   for (int64_t k = threadIdx.x; k < 7 * S; k += blockDim.x) sv[k] = T(0);
   __syncthreads();
-  T* sy = sv;
-  T* sh = sv + S;
+  T* sy = sv + S;
+  T* sh = sv + 2 * S;
   // S4: gather y^n (interface edges, copied old->new by the sweep), h = Hz^{n+1/2} outside, state
   for (int it = threadIdx.x; it < m.nY * nb; it += blockDim.x) {
     const int i = it % m.nY, b = it / m.nY;
@@ -683,7 +608,7 @@ __device__ void rom_batch(const PostParams<T>& p, int bi, T* sv) {
   }
   load_rom_state(p, m, first, nb, sv);
   __syncthreads();
-  rom_step<T, ENERGY>(p, m, first, nb, sv, buf, p.rom_partials + first);
+  rom_step<T, ENERGY>(p, m, first, nb, sv, p.rom_partials + first);
   store_rom(p, m, first, nb, sv, p.ex1, p.ey1);
 }
 
@@ -701,13 +626,12 @@ __device__ void rom_batch2(const PostParams<T>& p, int bi, T* sv, T g0, T g1, do
   const int B = p.batch, nY = m.nY;
   const int64_t S = (int64_t)p.nthreads_vec * B;
   const int tid = threadIdx.x, nt = blockDim.x;
-  T* buf[2];
-  T* reg = rom_buffers(p, sv, buf);
+  T* reg = rom_end(p, sv);
   const int64_t P = p.pitch;
   for (int64_t k = tid; k < 7 * S; k += nt) sv[k] = T(0);
   if (tid < B) sdelta[tid] = 0.0;  // B <= 64
-  T* sy = sv;
-  T* sh = sv + S;
+  T* sy = sv + S;
+  T* sh = sv + 2 * S;
   // region geometry of slot b
   auto geo = [&](int b, int& i0, int& j0, int& bx, int& by) {
     const int32_t* r = p.rects + 4 * (int64_t)(first + b);
@@ -796,7 +720,7 @@ __device__ void rom_batch2(const PostParams<T>& p, int bi, T* sv, T g0, T g1, do
   }
   __syncthreads();
   // ---- ROM step n: y^{n+1}, x~^{n+1}; ROM energy of W^n
-  rom_step<T, ENERGY>(p, m, first, nb, sv, buf, p.rom_partials + first);
+  rom_step<T, ENERGY>(p, m, first, nb, sv, p.rom_partials + first);
   // ---- R4: y^{n+1} into the interface edges; Hz^{n+3/2} of the outside cells
   for (int b = 0; b < nb; ++b) {
     int i0, j0, bx, by;
@@ -868,7 +792,7 @@ __device__ void rom_batch2(const PostParams<T>& p, int bi, T* sv, T g0, T g1, do
   }
   __syncthreads();
   // ---- ROM step n+1: y^{n+2}, x~^{n+2}; ROM energy of W^{n+1}
-  rom_step<T, ENERGY>(p, m, first, nb, sv, buf, p.rom_partials2 + first);
+  rom_step<T, ENERGY>(p, m, first, nb, sv, p.rom_partials2 + first);
   // ---- R5: E^{n+2} of the outside cells' non-interface edges, the outside cells' Hz, y^{n+2}
   for (int b = 0; b < nb; ++b) {
     int i0, j0, bx, by;
@@ -1153,16 +1077,14 @@ void launch_sweep2(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s, i
   else sweep2_kernel<T, false><<<grid, 32 * warps_per_cta, 0, s>>>(q);
 }
 
-size_t post_smem_bytes(size_t es, int nvec, int batch, bool staged) {
-  return es * ((size_t)7 * nvec * batch + (staged ? 2 * (((size_t)nvec * nvec + 3) / 4 * 4) : 0));
-}
-size_t post2_smem_bytes(size_t es, int nvec, int batch, int region_stride, bool staged) {
-  return post_smem_bytes(es, nvec, batch, staged) + es * (size_t)batch * region_stride;
+size_t post_smem_bytes(size_t es, int nvec, int batch) { return es * (size_t)7 * nvec * batch; }
+size_t post2_smem_bytes(size_t es, int nvec, int batch, int region_stride) {
+  return post_smem_bytes(es, nvec, batch) + es * (size_t)batch * region_stride;
 }
 
 template <typename T>
 void launch_post2(const PostParams<T>& p, bool energy, cudaStream_t s) {
-  const size_t smem = post2_smem_bytes(sizeof(T), p.nthreads_vec, p.batch, p.region_stride, p.staged != 0);
+  const size_t smem = post2_smem_bytes(sizeof(T), p.nthreads_vec, p.batch, p.region_stride);
   if (energy) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(post2_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     post2_kernel<T, true><<<p.n_batch + 1, p.block, smem, s>>>(p);
@@ -1174,7 +1096,7 @@ void launch_post2(const PostParams<T>& p, bool energy, cudaStream_t s) {
 
 template <typename T>
 void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s) {
-  const size_t smem = post_smem_bytes(sizeof(T), p.nthreads_vec, p.batch, p.staged != 0);
+  const size_t smem = post_smem_bytes(sizeof(T), p.nthreads_vec, p.batch);
   if (energy) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(post_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     post_kernel<T, true><<<p.n_batch + 1, p.block, smem, s>>>(p);

@@ -30,9 +30,14 @@ struct SweepParams {
   T wxy, wh;            // dx dy, mu0 dx dy / dt (energy weights)
 };
 
+// Fused per-model operators (column-major, in the model pool), with x = [E~; H~] (q1 + q2):
+//   M1 ((q2 + q1 + nY) x (q1 + q2)) = [[Q1, I], [Aq', Kq], [-L~^T Aq', -L~^T Kq]],  Aq' = Aq + Kq Q1
+//      -> [H~^{n+1}; E*; -L~^T E*] in one product (K3)
+//   M2 ((q1 + nY) x nY) = [Bq; L~^T Bq]  -> [E~ - E*; y - L~^T E*] from U
+//   Rt ((q1 + q2) x (q1 + q2)) = [[R~11/dt, -K~/2], [-K~^T/2, R~22/dt]]  (storage function)
 struct RomModelDev {
   int nY, q1, q2;
-  int64_t off_Q1, off_Aq, off_Kq, off_Lt, off_Bq, off_R11, off_R22, off_K;  // into model pool
+  int64_t off_M1, off_M2, off_Rt;
 };
 
 // Post kernel: S4-S6 per ROM instance, probe recording, deterministic
@@ -59,9 +64,8 @@ struct PostParams {
   const double* sweep_partials; int n_sweep_partials; double* rom_partials; double* energy_ring;
   double* level1;                  // per post CTA energy partial (gridDim.x entries)
   int64_t* step; unsigned int* done;
-  int nthreads_vec;  // max(nY, q1, q2) over models (smem sizing)
+  int nthreads_vec;  // max(q1 + q2 + nY) over models: shared-memory vector stride
   int block;         // threads per CTA
-  int staged;        // 1: operators streamed through shared memory; 0: read from global (large q)
   // ---- two-step mode (post2): fix-up around every instance after sweep2 (K3b)
   const int32_t* rects;            // per instance (i0, j0, bx, by), global
   int64_t row_begin, pitch;
@@ -90,8 +94,8 @@ void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s);
 template <typename T>
 void launch_post2(const PostParams<T>& p, bool energy, cudaStream_t s);
 // shared-memory bytes of the two kernels for a given batch (host-side sizing)
-size_t post_smem_bytes(size_t es, int nvec, int batch, bool staged = true);
-size_t post2_smem_bytes(size_t es, int nvec, int batch, int region_stride, bool staged = true);
+size_t post_smem_bytes(size_t es, int nvec, int batch);
+size_t post2_smem_bytes(size_t es, int nvec, int batch, int region_stride);
 
 // setup kernels
 template <typename T, typename M>
