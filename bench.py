@@ -171,7 +171,7 @@ def run_ours(args):
             t = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8).clone()
         dist.broadcast(t, 0)
         nid = bytes(t.numpy().tobytes())
-    m0, m1 = max(rb - 2, 0), min(re + 1, ny)  # materials of rows [rb-2, re+1): the 2-step halo
+    m0, m1 = max(rb - 4, 0), min(re + 4, ny)  # materials of rows [rb-4, re+4): the 4-step halo
     eps = scene.eps_r[m0:m1].contiguous()
     sig = scene.sigma[m0:m1].contiguous()
     sim = Simulation(scene.nx, scene.ny, scene.dx, scene.dy, scene.dt, eps, sig, precision=scene.precision,
@@ -235,11 +235,11 @@ def run_ours(args):
 
     # ---- end-to-end through the public API with host buffers: every call advances E2E_CHUNK steps
     #      and copies exactly those steps' inputs in (source samples, host -> device) and their
-    #      results out (probe samples + energy, device -> host); E2E_CHUNK = 2 = one two-step pass
+    #      results out (probe samples + energy, device -> host); chunk = two K-step passes
     e2e = None
     if not args.no_e2e:
         samples = np.ascontiguousarray(scene.samples, dtype=np.float64)
-        chunk = 2
+        chunk = 2 * sim.info().steps_per_pass
         k_e2e = max(chunk, min(args.steps, args.e2e_steps) // chunk * chunk)
         start = sim.info().steps_taken
         barrier()
@@ -262,7 +262,8 @@ def run_ours(args):
         e2e = {"value": cells_total * k_e2e / dt_e2e, "unit": UNIT, "h2d_bytes_per_step": 8,
                "d2h_bytes_per_step": len(scene.probes) * es + (0 if args.no_energy else 8),
                "steps": k_e2e, "steps_per_call": chunk,
-               "api": "per call: fdtd_set_source(host samples) + fdtd_step(2) + fdtd_probe + fdtd_energy (host)"}
+               "api": "per call: fdtd_set_source(host samples) + fdtd_step(%d) + fdtd_probe + fdtd_energy (host)"
+                      % chunk}
         finite = finite and bool(np.all(np.isfinite(p)))
     if rank != 0:
         sim.close()
@@ -274,7 +275,7 @@ def run_ours(args):
     pk = peaks()
     es = 8 if scene.precision == 64 else 4
     info = sim.info()
-    spp = info.steps_per_pass              # time steps advanced by one sweep launch (1 or 2)
+    spp = info.steps_per_pass              # time steps advanced by one sweep pass (1, 2 or 4)
     # algorithmic bytes: 40 B per cell-step fp32 -- read Ex, Ey, Hz and the per-edge
     # (ca, cb) pairs, write Ex, Ey, Hz -- times the cell-steps one launch advances
     alg_bytes = 10 * es * cells_rank * spp
@@ -290,8 +291,8 @@ def run_ours(args):
                 traffic = tj.get("bytes_per_launch_per_cell") * cells_rank
         except Exception:
             traffic = None
-    kname = "sweep2_kernel<float> (fused H+E, two time steps per pass)" if spp == 2 else \
-        "sweep_kernel<float> (fused H+E)"
+    kname = "sweepk_kernel<%s, K=%d> (fused H+E, %d time step%s per HBM pass)" % (
+        "float" if es == 4 else "double", spp, spp, "s" if spp > 1 else "")
     roof = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": peak,
             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in pk else "fallback",

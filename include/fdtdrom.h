@@ -67,8 +67,8 @@ typedef struct {
   uint32_t flags;          /* FDTD_* flags above                                          */
   /* Per-cell relative permittivity and conductivity (S/m), row-major [rows][nx].  The
    * pointer addresses global row `materials_row0`; it must cover the rows
-   * [max(row_begin-2, 0), min(row_end+1, ny)) of the grid (the slab plus the ghost rows the
-   * two-step sweep reads).  Edge values are the arithmetic mean of
+   * [max(row_begin-4, 0), min(row_end+4, ny)) of the grid (the slab plus the ghost rows a
+   * four-step pass recomputes).  Edge values are the arithmetic mean of
    * the two adjacent cells (R2).  mu = mu0 everywhere
    * (R3).  Host or device memory (FDTD_MATERIALS_ON_DEVICE), double or float
    * (FDTD_MATERIALS_F32). */
@@ -126,7 +126,8 @@ fdtd_status fdtd_add_rom(fdtd_ctx *c, const fdtd_rom_model *m, const int32_t *an
 fdtd_status fdtd_set_source(fdtd_ctx *c, int64_t i, int64_t j, const double *samples,
                             int64_t n_samples, int64_t step0);
 
-/* Probes: record Hz^{n+1/2} at cells ij[2p], ij[2p+1] after every step n (R16). */
+/* Probes: record Hz^{n+1/2} at cells ij[2p], ij[2p+1] after every step n (R16).  Replaces any
+ * previous set; the record of a probe in another rank's rows reads 0 on this rank. */
 fdtd_status fdtd_set_probes(fdtd_ctx *c, const int64_t *ij, int32_t n_probes);
 
 /* Record the storage function W^n (R17) every step (1) or not (0). */
@@ -185,7 +186,7 @@ typedef struct {
   int32_t graphs;              /* 1 if fdtd_step replays CUDA graphs                       */
   int32_t precision;
   double bytes_per_cell_step;  /* HBM bytes of the sweep per cell-step as implemented       */
-  int32_t steps_per_pass;      /* 2 when the two-step (temporally blocked) sweep is active  */
+  int32_t steps_per_pass;      /* time steps per sweep pass in use (1, 2 or 4)              */
   void *sweep_stream;          /* cudaStream_t the kernels are launched on                 */
 } fdtd_info;
 fdtd_status fdtd_get_info(const fdtd_ctx *c, fdtd_info *out);
@@ -197,12 +198,15 @@ fdtd_status fdtd_get_info(const fdtd_ctx *c, fdtd_info *out);
 fdtd_status fdtd_profile(fdtd_ctx *c, int32_t on);
 fdtd_status fdtd_profile_read(fdtd_ctx *c, double *sweep_ms, double *post_ms, int64_t *n_launches);
 
-/* Time steps per sweep pass: 1, or 2 (default; temporal blocking with a per-instance fix-up,
- * DESIGN.md K1b/K3b).  Two-step mode is used when every ROM instance's
- * [i0-2, i0+bx+2) x [j0-2, j0+by+2) region is inside this rank's rows and free of other
- * instances' outside cells -- on every rank (agreed collectively at the first fdtd_step after a
- * configuration change; then the halo exchange is two rows deep); otherwise fdtd_step runs one
- * step per pass.  Results are bit-identical either way. */
+/* Time steps per sweep pass K: 1, 2 or 4 (temporal blocking with a per-instance fix-up,
+ * DESIGN.md K1/K3; default: 4 in fp32, 2 in fp64 -- a 16-byte vector must hold K columns).
+ * K-step passes are used when every ROM instance's fix-up region [i0-(2K-1), i0+bx+2K-1) x
+ * [j0-(2K-1), j0+by+2K-1) lies inside the grid columns and this rank's rows, and no two
+ * instances' [i0-K, i0+bx+K) x [j0-K, j0+by+K) rectangles meet -- on every rank (agreed
+ * collectively at the first fdtd_step after a configuration change; the halo exchange is then K
+ * rows deep); otherwise the deepest valid K below is used.  A step count that is not a multiple
+ * of K ends with shallower passes.  Fields, ROM states and probes are bit-identical for every
+ * K; the energy trace agrees up to summation order. */
 fdtd_status fdtd_set_time_blocking(fdtd_ctx *c, int32_t steps_per_pass);
 
 /* Tuning knobs for the fused sweep (rows per CTA, warps per CTA); 0 keeps default. */

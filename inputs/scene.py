@@ -70,16 +70,19 @@ def gaussian_samples(n, dt, fmax, derivative=False, t0=None):
 
 
 # ---------------------------------------------------------------- placements
-def place_blocks(nx, ny, sizes, count, seed, nslabs=8, forbid=(), max_tries=2_000_000):
+def place_blocks(nx, ny, sizes, count, seed, nslabs=8, forbid=(), max_tries=2_000_000, margin=7, clear=4):
     """Seeded non-overlapping placements (R19).
 
     sizes: list of (bx, by) per model; the model of each placement is drawn uniformly.
-    Every footprint plus its one-cell ring stays inside the grid without touching the PEC
-    wall, the expanded footprints are pairwise disjoint, and the rows j0-2 .. j0+by+1 stay
-    inside one of ``nslabs`` equal row slabs (the two-step fix-up region of DESIGN.md K3b).  ``forbid``: cells (i, j) that must stay
-    outside every footprint (source, probes).
+    Every footprint stays ``margin`` cells away from the PEC walls and from the boundaries of
+    ``nslabs`` equal row slabs, and the footprints expanded by ``clear`` cells are pairwise
+    disjoint.  The defaults (7, 4) are what four-step passes need (K3: fix-up region =
+    block + 2K-1 cells inside the slab, block + K rectangles disjoint); every placement also
+    satisfies the one-cell-ring rule of fdtd_add_rom.  ``forbid``: cells (i, j) that must stay
+    outside every footprint plus ring (source, probes).
     Returns int32 array (count, 3): (model, i0, j0).
     """
+    assert margin >= 2 and clear >= 1
     rng = np.random.default_rng(seed)
     slab = ny // nslabs if nslabs > 1 and ny % nslabs == 0 else ny
     forbid = [(int(i), int(j)) for i, j in forbid]
@@ -93,12 +96,13 @@ def place_blocks(nx, ny, sizes, count, seed, nslabs=8, forbid=(), max_tries=2_00
             raise RuntimeError("placement failed after %d tries (%d placed)" % (tries, len(out)))
         m = int(rng.integers(len(sizes)))
         bx, by = sizes[m]
-        i0 = int(rng.integers(2, nx - bx - 1))
-        j0 = int(rng.integers(2, ny - by - 1))
-        if (j0 - 2) // slab != (j0 + by + 1) // slab:  # footprint + 2 rows inside one slab (R19)
+        if nx - bx - margin <= margin or ny - by - margin <= margin:
+            raise RuntimeError("grid too small for a %dx%d block with margin %d" % (bx, by, margin))
+        i0 = int(rng.integers(margin, nx - bx - margin + 1))
+        j0 = int(rng.integers(margin, ny - by - margin + 1))
+        if (j0 - margin) // slab != (j0 + by + margin - 1) // slab:  # inside one slab with its margin
             continue
-        # expanded footprint [i0-1, i0+bx] x [j0-1, j0+by], kept one extra cell apart so rings never touch
-        x0, x1, y0, y1 = i0 - 1, i0 + bx + 2, j0 - 1, j0 + by + 2
+        x0, x1, y0, y1 = i0 - clear, i0 + bx + clear, j0 - clear, j0 + by + clear
         keys = [(a, b) for a in range(x0 // B, (x1 - 1) // B + 1) for b in range(y0 // B, (y1 - 1) // B + 1)]
         hit = False
         for k in keys:
@@ -112,7 +116,7 @@ def place_blocks(nx, ny, sizes, count, seed, nslabs=8, forbid=(), max_tries=2_00
             continue
         if any(i0 - 1 <= fi <= i0 + bx and j0 - 1 <= fj <= j0 + by for fi, fj in forbid):
             continue
-        rect = (i0 - 1, i0 + bx + 1, j0 - 1, j0 + by + 1)
+        rect = (x0, x1, y0, y1)
         for k in keys:
             buckets.setdefault(k, []).append(rect)
         out.append((m, i0, j0))

@@ -1,15 +1,16 @@
 // Host implementation of the C ABI declared in include/fdtdrom.h.
 //
-// Owns the device state of one row slab: ping-pong field buffers with one ghost row on each
-// side, the per-edge coefficients, the ROM operators, probe/energy record rings, and (for
-// several ranks) an NCCL communicator used for the per-step halo exchange of DESIGN.md
-// "Multi-GPU".  All per-step work is enqueued on one stream; fdtd_step replays a captured
-// two-step CUDA graph when possible.
+// Owns the device state of one row slab: ping-pong field buffers with ghost rows on each side,
+// the per-cell material terms, the ROM operators, probe/energy record rings, and (for several
+// ranks) an NCCL communicator used for the per-pass halo exchange of DESIGN.md "Multi-GPU".  All
+// work is enqueued on one stream; fdtd_step replays a captured CUDA graph of two K-step passes
+// when possible.
 #include "fdtdrom.h"
 
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -22,7 +23,10 @@
 
 namespace {
 
-constexpr int ROW0 = 2;  // local row of the first owned row (two ghost rows below: 2-step halos)
+using fdtd::KMAX;
+constexpr int ROW0 = 2 * KMAX;  // local row of the first owned row: the K-step sweep's first chunk
+                                // reads K halo rows below it and stage rows down to r0 - 2K
+constexpr int GHOST_UP = KMAX;  // ghost rows above the slab (Ex edge rows up to row_end + K - 1)
 constexpr double MU0 = 4.0e-7 * 3.14159265358979323846;
 constexpr double C0 = 299792458.0;
 constexpr double EPS0 = 1.0 / (MU0 * C0 * C0);
@@ -72,7 +76,7 @@ struct fdtd_ctx {
   size_t es = 4;  // element size
   int V = 4;      // elements per 16-byte vector
   int rows = 0;   // owned rows
-  int64_t nrows_alloc = 0, pitch = 0;  // rows + 5: two ghost rows below, three above
+  int64_t nrows_alloc = 0, pitch = 0;  // rows + ROW0 + GHOST_UP
   int ncolv = 0;
   cudaStream_t stream = nullptr, cap_stream = nullptr;
   std::string err;
@@ -85,10 +89,8 @@ struct fdtd_ctx {
   int64_t mrow0 = 0, mrow_end = 0;
   int64_t* d_step = nullptr;
   unsigned* d_done = nullptr;
-  double* d_partials = nullptr;
-  double* d_partials2 = nullptr;
-  double* d_level1 = nullptr;
-  double* d_level1b = nullptr;
+  double* d_partials = nullptr;   // [KMAX][n_partials] sweep energy partials
+  double* d_level1 = nullptr;     // [KMAX][post grid]
   int n_partials = 0;
   int chunk = 64, warps = 4;
   // source
@@ -97,43 +99,49 @@ struct fdtd_ctx {
   // probes & energy rings
   int64_t cap = 65536;
   int n_probe = 0;
-  int64_t* d_probe_idx = nullptr;
+  std::vector<int64_t> probe_ij;   // global (i, j) per probe
+  int2* d_probe_rows = nullptr;    // per local row: (first, count) into d_probe_list
+  int2* d_probe_list = nullptr;    // (column, probe index), owned probes sorted by row, column
   void* d_probe_ring = nullptr;
   double* d_energy_ring = nullptr;
   bool energy_on = false;
   int64_t steps = 0, rd_probe = 0, rd_energy = 0;
   int cur = 0;  // buffer holding the current state (E^n, H^{n-1/2})
-  // two-step mode (sweep2 + post2): wanted by the user (default on) and valid for the placements
-  bool tb2_want = true, tb2_ok = true, tb2_all = true, tb2_dirty = true;
+  // K-step passes (K1/K3): k_want requested, k_ok the deepest this rank can do,
+  // kz the depth in use (agreed over ranks; the zone marks in msb are for kz)
+  int k_want = 4, k_ok = 1, kz = 1, kz_marked = 1;
+  bool kz_dirty = true;
   int region_stride = 4;
   int32_t* d_rects = nullptr;
-  double* d_rom_partials2 = nullptr;
+  std::vector<int32_t> zp_off, zp;  // zone probes per instance (gi, gj, probe index)
+  int32_t* d_zp_off = nullptr;
+  int32_t* d_zp = nullptr;
   // ROMs
   std::vector<ModelHost> models;
   std::vector<int32_t> inst_model, rects;  // rects: (i0, j0, bx, by) global
-  std::vector<int64_t> port_off, port_edge, port_h, ring_idx, ring_off, state_off, Sk_off;
+  std::vector<int64_t> port_off, port_edge, state_off, Sk_off;
   std::vector<double> cya, cyg, ehalf, Sk;  // fp64 host copies (converted on upload)
   std::vector<double> mpool;                // shared model matrices (col-major, fp64)
   int nvec = 1;
   int rom_batch = 16;
   std::vector<int32_t> batch_tab;  // (model, first instance, count)
   int32_t* d_batch_tab = nullptr;
+  int post_grid = 1;
   // device ROM arrays
   void* d_mpool = nullptr; void* d_Sk = nullptr; void* d_cya = nullptr; void* d_cyg = nullptr;
   void* d_state = nullptr; double* d_ehalf = nullptr; double* d_rom_partials = nullptr;
-  int64_t *d_port_off = nullptr, *d_port_edge = nullptr, *d_port_h = nullptr, *d_ring_idx = nullptr,
-          *d_ring_off = nullptr, *d_state_off = nullptr, *d_Sk_off = nullptr;
+  int64_t *d_port_off = nullptr, *d_port_edge = nullptr, *d_state_off = nullptr, *d_Sk_off = nullptr;
   int32_t* d_inst_model = nullptr;
   fdtd::RomModelDev* d_models = nullptr;
   int64_t state_len = 0;
   // graphs
   cudaGraphExec_t gexec = nullptr;
   bool graph_dirty = true;
-  int graph_steps = 2;
+  int graph_steps = 0;
+  int64_t graph_launches = 0;
   int64_t launches = 0;
   // profiling (event pairs around each launch)
   bool profiling = false;
-  int64_t prof_pairs = 0;  // two-step launches among the profiled ones
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
   // multi-rank
@@ -217,88 +225,85 @@ fdtd::SweepParams<T> sweep_params(fdtd_ctx* c, int q) {
   p.pitch = c->pitch; p.ncolv = c->ncolv; p.rows = c->rows; p.chunk = c->chunk; p.row0 = ROW0;
   p.chx = (T)(c->d.dt / (MU0 * c->d.dx));
   p.chy = (T)(c->d.dt / (MU0 * c->d.dy));
-  // the source row may also be a ghost row (below: the first chunk recomputes it; above: the
-  // two-step sweep advances row_end once): those recomputations add the source as its owner does
-  const bool src_here = c->d_src && c->src_j >= c->d.row_begin - 2 && c->src_j <= c->d.row_end;
+  // the source row may also be a ghost row: the chunks next to the slab edges recompute up to
+  // KMAX rows beyond it, adding the source as its owner does
+  const bool src_here = c->d_src && c->src_j >= c->d.row_begin - KMAX && c->src_j < c->d.row_end + KMAX;
   p.src_row = src_here ? (int)lrow(c, c->src_j) : -1;
   p.src_col = src_here ? c->src_i : -1;
   p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
   p.step = c->d_step;
   p.partials = c->energy_on ? c->d_partials : nullptr;
-  p.partials2 = c->energy_on ? c->d_partials2 : nullptr;
+  p.pstride = c->n_partials;
+  p.probe_rows = c->d_probe_rows; p.probe_list = c->d_probe_list;
+  p.probe_ring = (T*)c->d_probe_ring; p.cap = c->cap;
   p.idx = (T)(1.0 / c->d.dx); p.idy = (T)(1.0 / c->d.dy);
   p.wxy = (T)(c->d.dx * c->d.dy);
   p.wh = (T)(MU0 * c->d.dx * c->d.dy / c->d.dt);
   return p;
 }
 
+int sweep_gx(const fdtd_ctx* c) { return fdtd::sweep_ctas_x(c->ncolv, c->warps); }
+
 template <typename T>
-fdtd::PostParams<T> post_params(fdtd_ctx* c, int q, bool pair = false) {
+fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
   fdtd::PostParams<T> p{};
   p.n_inst = (int)c->inst_model.size();
-  p.inst_model = c->d_inst_model; p.models = c->d_models; p.mpool = (const T*)c->d_mpool;
+  p.models = c->d_models; p.mpool = (const T*)c->d_mpool;
   p.Sk = (const T*)c->d_Sk; p.Sk_off = c->d_Sk_off; p.port_off = c->d_port_off;
   p.cya = (const T*)c->d_cya; p.cyg = (const T*)c->d_cyg; p.ehalf = c->d_ehalf;
-  p.port_edge = c->d_port_edge; p.port_h = c->d_port_h; p.ring_idx = c->d_ring_idx; p.ring_off = c->d_ring_off;
+  p.port_edge = c->d_port_edge;
   p.state = (T*)c->d_state; p.state_off = c->d_state_off;
   p.ex1 = (T*)c->f[1 - q][0]; p.ey1 = (T*)c->f[1 - q][1]; p.hz1 = (T*)c->f[1 - q][2];
-  p.n_probe = c->n_probe; p.probe_idx = c->d_probe_idx; p.probe_ring = (T*)c->d_probe_ring; p.cap = c->cap;
-  {  // exactly the partials the matching sweep launch wrote
-    const int per_cta = 32 * c->warps;
-    const int gx = pair ? fdtd::sweep2_ctas_x(c->ncolv, c->warps) : (c->ncolv + per_cta - 1) / per_cta;
-    p.sweep_partials = c->d_partials;
-    p.n_sweep_partials = gx * ((c->rows + c->chunk - 1) / c->chunk);
-  }
-  p.rom_partials = c->d_rom_partials; p.energy_ring = c->d_energy_ring;
+  p.ex0 = (const T*)c->f[q][0]; p.ey0 = (const T*)c->f[q][1]; p.hz0 = (const T*)c->f[q][2];
+  p.mea = (const T*)c->coef[0]; p.msb = (const T*)c->coef[1];
+  p.pitch = c->pitch; p.row_begin = c->d.row_begin; p.row0 = ROW0;
+  p.Kz = c->kz;
+  p.rects = c->d_rects;
+  p.zp_off = c->d_zp_off; p.zp = c->d_zp;
+  p.probe_ring = (T*)c->d_probe_ring; p.cap = c->cap;
+  p.chx = (T)(c->d.dt / (MU0 * c->d.dx));
+  p.chy = (T)(c->d.dt / (MU0 * c->d.dy));
+  p.idx = (T)(1.0 / c->d.dx); p.idy = (T)(1.0 / c->d.dy);
+  p.wxy = (T)(c->d.dx * c->d.dy);
+  p.wh = (T)(MU0 * c->d.dx * c->d.dy / c->d.dt);
+  const bool src_here = c->d_src && c->src_j >= c->d.row_begin - KMAX && c->src_j < c->d.row_end + KMAX;
+  p.src_row = src_here ? (int)lrow(c, c->src_j) : -1;
+  p.src_col = src_here ? c->src_i : -1;
+  p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
+  p.sweep_partials = c->d_partials;  // exactly the partials the matching sweep launches wrote
+  p.n_sweep_partials = (int64_t)sweep_gx(c) * ((c->rows + c->chunk - 1) / c->chunk);
+  p.pstride = c->n_partials;
+  p.rom_partials = c->d_rom_partials;
+  p.level1 = c->d_level1;
+  p.energy_ring = c->d_energy_ring;
   p.step = c->d_step; p.done = c->d_done;
   p.nthreads_vec = c->nvec;
   p.n_batch = (int)(c->batch_tab.size() / 3);
   p.batch = c->rom_batch;
   p.batch_tab = c->d_batch_tab;
   p.block = 256;
-  p.level1 = c->d_level1;
-  p.level1b = c->d_level1b;
-  p.rects = c->d_rects;
-  p.row_begin = c->d.row_begin;
-  p.row0 = ROW0;
-  p.pitch = c->pitch;
-  p.ex0 = (const T*)c->f[q][0]; p.ey0 = (const T*)c->f[q][1]; p.hz0 = (const T*)c->f[q][2];
-  p.mea = (const T*)c->coef[0]; p.msb = (const T*)c->coef[1];
-  p.chx = (T)(c->d.dt / (MU0 * c->d.dx));
-  p.chy = (T)(c->d.dt / (MU0 * c->d.dy));
-  p.idx = (T)(1.0 / c->d.dx); p.idy = (T)(1.0 / c->d.dy);
-  p.wh = (T)(MU0 * c->d.dx * c->d.dy / c->d.dt);
-  const bool src_here = c->d_src && c->src_j >= c->d.row_begin && c->src_j < c->d.row_end;
-  p.src_row = src_here ? (int)lrow(c, c->src_j) : -1;
-  p.src_col = src_here ? c->src_i : -1;
-  p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
-  p.sweep_partials2 = c->d_partials2;
-  p.rom_partials2 = c->d_rom_partials2;
   p.region_stride = c->region_stride;
   return p;
 }
 
-// Halo plan: rank g sends its top owned row of (Ex, Ey, Hz) at step n
-// to g+1's ghost row 0, and its bottom owned Ex row to g-1's ghost Ex row rows+1.  Rows are
-// whole device rows (pitch elements).  Sends and receives are listed in the order both
-// transports pair them (per peer and direction, in list order).
+// Halo plan of a K-step pass: rank g owns cell rows and Ex edge rows
+// [row_begin, row_end).  Its sweep reads rows [row_begin - K, row_end + K): all three fields of
+// the K rows below (the top K rows of rank g-1), Ex of the K edge rows above and Ey / Hz of the
+// K-1 cell rows above (the bottom rows of rank g+1).  Rows are whole device rows (pitch
+// elements); sends and receives are listed in the order both transports pair them.
 struct HaloRow { int a; int64_t row; int peer; };
-// depth 1 (one-step passes): rank g sends its top owned row of (Ex, Ey, Hz) to g+1's ghost row
-// below and its bottom Ex row to g-1's ghost Ex row above.  depth 2 (two-step passes): the top two
-// rows of (Ex, Ey, Hz) go up; the bottom row's (Ex, Ey, Hz) and the second Ex row go down.
 void halo_plan(const fdtd_ctx* c, int depth, std::vector<HaloRow>& sends, std::vector<HaloRow>& recvs) {
   sends.clear();
   recvs.clear();
   const int up = c->d.rank + 1, dn = c->d.rank - 1;
   const int64_t top = ROW0 + c->rows;  // first row above the slab
   auto down_list = [&](int64_t base, int peer, std::vector<HaloRow>& v) {  // rows the lower rank needs
-    if (depth == 1) {
-      v.push_back({0, base, peer});
-    } else {
-      v.push_back({0, base, peer});
-      v.push_back({1, base, peer});
-      v.push_back({2, base, peer});
-      v.push_back({0, base + 1, peer});
+    for (int64_t r = 0; r < depth; ++r) {
+      v.push_back({0, base + r, peer});
+      if (r + 1 < depth) {
+        v.push_back({1, base + r, peer});
+        v.push_back({2, base + r, peer});
+      }
     }
   };
   if (up < c->d.nranks) {
@@ -359,22 +364,24 @@ cudaEvent_t next_event(fdtd_ctx* c) {
   return c->ev[c->ev_used++];
 }
 
-template <typename T>
-void sweep_split(fdtd_ctx* c, int q, cudaStream_t s, int begin, int count) {
-  fdtd::launch_sweep<T>(sweep_params<T>(c, q), c->warps, s, begin, count);
-}
-
-// One time step.  With several ranks the sweep is split: the interior row chunks (which read no
-// ghost row) run on the compute stream while the NCCL halo exchange runs on a side stream; the
-// first and last chunks follow once the ghost rows have arrived.
-fdtd_status enqueue_step(fdtd_ctx* c, int q, cudaStream_t s) {
+// One pass of K time steps (K1 sweep q -> 1-q, then the K3 fix-up).  With several ranks the sweep
+// is split: the interior row chunks (which read no ghost row) run on the compute stream while the
+// NCCL halo exchange runs on a side stream; the chunks next to the slab edges follow once the
+// ghost rows have arrived.
+fdtd_status enqueue_pass(fdtd_ctx* c, int q, cudaStream_t s, int K) {
   const bool prof = c->profiling && s == c->stream;
   const int nch = (c->rows + c->chunk - 1) / c->chunk;
-  const bool split = c->d.nranks > 1 && nch >= 3;
+  // chunks [lo, hi) read only owned rows: a chunk reads rows [r0 - K, r1 + K)
+  int lo = 0, hi = nch;
+  while (lo < nch && lo * c->chunk - K < 0) ++lo;
+  while (hi > lo && std::min((hi) * c->chunk, c->rows) + K > c->rows) --hi;
+  const bool split = c->d.nranks > 1 && hi > lo;
   const bool nccl_overlap = split && c->comm && c->comm_stream;
   auto sweep = [&](int b, int n) {
-    if (c->prec == 64) sweep_split<double>(c, q, s, b, n);
-    else sweep_split<float>(c, q, s, b, n);
+    if (n <= 0) return;
+    if (c->prec == 64) fdtd::launch_sweep<double>(sweep_params<double>(c, q), K, c->warps, s, b, n);
+    else fdtd::launch_sweep<float>(sweep_params<float>(c, q), K, c->warps, s, b, n);
+    c->launches += 1;
   };
   cudaEvent_t e[3];
   if (prof) {
@@ -384,110 +391,29 @@ fdtd_status enqueue_step(fdtd_ctx* c, int q, cudaStream_t s) {
   if (nccl_overlap) {
     CK(cudaEventRecord(c->ev_ready, s));
     CK(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
-    fdtd_status st = halo_exchange(c, q, c->comm_stream, 1);
+    fdtd_status st = halo_exchange(c, q, c->comm_stream, K);
     if (st != FDTD_OK) return st;
     CK(cudaEventRecord(c->ev_halo, c->comm_stream));
-    sweep(1, nch - 2);                             // interior chunks: no ghost rows needed
+    sweep(lo, hi - lo);  // interior chunks: no ghost rows needed
     CK(cudaStreamWaitEvent(s, c->ev_halo, 0));
-    sweep(0, 1);
-    sweep(nch - 1, 1);
-    c->launches += 2;
+    sweep(0, lo);
+    sweep(hi, nch - hi);
   } else {
-    fdtd_status st = halo_exchange(c, q, s, 1);
+    fdtd_status st = halo_exchange(c, q, s, K);
     if (st != FDTD_OK) return st;
     if (split) {  // local groups: same split launches (their halo copies precede on this stream)
-      sweep(1, nch - 2);
-      sweep(0, 1);
-      sweep(nch - 1, 1);
-      c->launches += 2;
+      sweep(lo, hi - lo);
+      sweep(0, lo);
+      sweep(hi, nch - hi);
     } else {
       sweep(0, nch);
     }
   }
   if (prof) CK(cudaEventRecord(e[1], s));
-  if (c->prec == 64) fdtd::launch_post<double>(post_params<double>(c, q), c->energy_on, s);
-  else fdtd::launch_post<float>(post_params<float>(c, q), c->energy_on, s);
+  if (c->prec == 64) fdtd::launch_post<double>(post_params<double>(c, q), K, c->energy_on, s);
+  else fdtd::launch_post<float>(post_params<float>(c, q), K, c->energy_on, s);
   if (prof) CK(cudaEventRecord(e[2], s));
-  c->launches += 2;
-  return FDTD_OK;
-}
-
-// Two-step passes are used when this rank wants and can (tb2_ok) -- and, with several ranks, when
-// every rank can (the halo depth must agree): agreed once per configuration (agree_tb2).
-bool tb2_active(const fdtd_ctx* c) {
-  if (!c->tb2_want || !c->tb2_ok) return false;
-  return c->d.nranks == 1 || c->tb2_all;
-}
-
-fdtd_status agree_tb2(fdtd_ctx* c) {
-  if (!c->tb2_dirty) return FDTD_OK;
-  c->tb2_dirty = false;
-  c->tb2_all = c->tb2_want && c->tb2_ok;
-  if (c->d.nranks > 1 && c->comm) {  // collective min over ranks (all ranks reach this call together)
-    int32_t* d = (int32_t*)dalloc(c, sizeof(int32_t));
-    if (!d) return fail(c, FDTD_E_NOMEM, "agree");
-    const int32_t mine = c->tb2_all ? 1 : 0;
-    CK(cudaMemcpyAsync(d, &mine, sizeof mine, cudaMemcpyHostToDevice, c->stream));
-    NK(g_nccl.AllReduce(d, d, 1, NCCL_I32, NCCL_MIN, c->comm, c->stream));
-    int32_t all = 0;
-    CK(cudaMemcpyAsync(&all, d, sizeof all, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    dfree(c, d);
-    c->tb2_all = all != 0;
-  }
-  return FDTD_OK;
-}
-
-template <typename T>
-void sweep2_split(fdtd_ctx* c, int q, cudaStream_t s, int begin, int count) {
-  fdtd::launch_sweep2<T>(sweep_params<T>(c, q), c->warps, s, begin, count);
-}
-
-// two steps in one pass: sweep2 (q -> 1-q) then the ROM fix-up / probes / energy of both steps.
-// With several ranks the two-row-deep halo exchange overlaps the interior row chunks.
-fdtd_status enqueue_pair(fdtd_ctx* c, int q, cudaStream_t s) {
-  const bool prof = c->profiling && s == c->stream;
-  const int nch = (c->rows + c->chunk - 1) / c->chunk;
-  const bool split = c->d.nranks > 1 && nch >= 3 && c->chunk >= 2;
-  const bool nccl_overlap = split && c->comm && c->comm_stream;
-  auto sweep = [&](int b, int n) {
-    if (c->prec == 64) sweep2_split<double>(c, q, s, b, n);
-    else sweep2_split<float>(c, q, s, b, n);
-  };
-  cudaEvent_t e[3];
-  if (prof) {
-    for (auto& x : e) x = next_event(c);
-    CK(cudaEventRecord(e[0], s));
-  }
-  if (nccl_overlap) {
-    CK(cudaEventRecord(c->ev_ready, s));
-    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
-    fdtd_status st = halo_exchange(c, q, c->comm_stream, 2);
-    if (st != FDTD_OK) return st;
-    CK(cudaEventRecord(c->ev_halo, c->comm_stream));
-    sweep(1, nch - 2);  // interior chunks read no ghost row (chunk >= 2)
-    CK(cudaStreamWaitEvent(s, c->ev_halo, 0));
-    sweep(0, 1);
-    sweep(nch - 1, 1);
-    c->launches += 2;
-  } else {
-    fdtd_status st = halo_exchange(c, q, s, 2);
-    if (st != FDTD_OK) return st;
-    if (split) {
-      sweep(1, nch - 2);
-      sweep(0, 1);
-      sweep(nch - 1, 1);
-      c->launches += 2;
-    } else {
-      sweep(0, nch);
-    }
-  }
-  if (prof) CK(cudaEventRecord(e[1], s));
-  if (c->prec == 64) fdtd::launch_post2<double>(post_params<double>(c, q, true), c->energy_on, s);
-  else fdtd::launch_post2<float>(post_params<float>(c, q, true), c->energy_on, s);
-  if (prof) CK(cudaEventRecord(e[2], s));
-  c->launches += 2;
-  c->prof_pairs += prof ? 1 : 0;
+  c->launches += 1;
   return FDTD_OK;
 }
 
@@ -495,20 +421,18 @@ void drop_graph(fdtd_ctx* c) {
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   c->gexec = nullptr;
   c->graph_dirty = true;
-  c->tb2_dirty = true;
 }
 
-// Captures one "period" starting from buffer 0: two single steps (0 -> 1 -> 0) or, in two-step
-// mode, two pairs (4 steps, 0 -> 1 -> 0).
+// Captures one "period" starting from buffer 0: two K-step passes (0 -> 1 -> 0).
 fdtd_status build_graph(fdtd_ctx* c) {
   drop_graph(c);
   if (!c->cap_stream) CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
   const int64_t before = c->launches;
-  const bool pairs = tb2_active(c);
-  fdtd_status st = pairs ? enqueue_pair(c, 0, c->cap_stream) : enqueue_step(c, 0, c->cap_stream);
-  if (st == FDTD_OK) st = pairs ? enqueue_pair(c, 1, c->cap_stream) : enqueue_step(c, 1, c->cap_stream);
+  fdtd_status st = enqueue_pass(c, 0, c->cap_stream, c->kz);
+  if (st == FDTD_OK) st = enqueue_pass(c, 1, c->cap_stream, c->kz);
+  c->graph_launches = c->launches - before;
   c->launches = before;
   cudaError_t e = cudaStreamEndCapture(c->cap_stream, &g);
   if (st != FDTD_OK) return st;
@@ -516,7 +440,7 @@ fdtd_status build_graph(fdtd_ctx* c) {
   e = cudaGraphInstantiate(&c->gexec, g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return fail(c, FDTD_E_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
-  c->graph_steps = pairs ? 4 : 2;
+  c->graph_steps = 2 * c->kz;
   c->graph_dirty = false;
   return FDTD_OK;
 }
@@ -575,69 +499,7 @@ fdtd_status upload_roms(fdtd_ctx* c) {
   for (auto& m : c->models) md.push_back(m.dev);
   if ((st = upload_T(c, &c->d_mpool, c->mpool)) != FDTD_OK) return st;
   if ((st = upload(c, &c->d_models, md)) != FDTD_OK) return st;
-  if ((st = upload(c, &c->d_inst_model, c->inst_model)) != FDTD_OK) return st;
-  // two-step mode needs, per instance, the region [i0-2, i0+bx+2) x [j0-2, j0+by+2) inside the grid,
-  // and no other instance's outside cells inside that region (K3b)
-  {
-    c->region_stride = 4;
-    for (auto& m : c->models) {
-      const int Wr = m.bx + 4, Hr = m.by + 4;
-      int rs = 4 * Hr * Wr + (Hr + 1) * Wr + Hr * (Wr + 1);
-      c->region_stride = std::max(c->region_stride, (rs + 3) / 4 * 4);
-    }
-    bool ok = true;
-    struct Rc { int64_t i0, j0, bx, by; };
-    std::vector<Rc> all;
-    for (size_t r = 0; r < c->rects.size(); r += 4) {
-      Rc x{c->rects[r], c->rects[r + 1], c->rects[r + 2], c->rects[r + 3]};
-      if (x.i0 - 2 < 0 || x.j0 - 2 < 0 || x.i0 + x.bx + 2 > c->d.nx || x.j0 + x.by + 2 > c->d.ny ||
-          x.j0 - 2 < c->d.row_begin || x.j0 + x.by + 2 > c->d.row_end)
-        ok = false;
-      all.push_back(x);
-    }
-    std::sort(all.begin(), all.end(), [](const Rc& a, const Rc& b) { return a.i0 < b.i0; });
-    int64_t wmax = 0;
-    for (auto& r : all) wmax = std::max(wmax, r.bx);
-    for (size_t a = 0; ok && a < all.size(); ++a)
-      for (size_t b = a + 1; ok && b < all.size() && all[b].i0 <= all[a].i0 + all[a].bx + wmax + 4; ++b) {
-        const Rc &A = all[a], &Bq = all[b];
-        auto hit = [](const Rc& X, const Rc& Y) {  // region of X vs ring box of Y
-          return X.i0 - 2 <= Y.i0 + Y.bx && Y.i0 - 1 <= X.i0 + X.bx + 1 && X.j0 - 2 <= Y.j0 + Y.by &&
-                 Y.j0 - 1 <= X.j0 + X.by + 1;
-        };
-        if (hit(A, Bq) || hit(Bq, A)) ok = false;
-      }
-    c->tb2_ok = ok;
-  }
-  // batches of consecutive instances of one model (instances are stored grouped by model); the
-  // batch size keeps the two-step fix-up kernel at <= ~110 KB of shared memory when possible
-  {
-    const char* env = getenv("FDTD_ROM_BATCH");
-    int B = env ? std::max(1, std::min(64, atoi(env))) : 8;
-    auto fits = [&](int b, size_t lim) {
-      return fdtd::post2_smem_bytes(c->es, c->nvec, b, c->region_stride) <= lim &&
-             fdtd::post_smem_bytes(c->es, c->nvec, b) <= lim;
-    };
-    while (B > 1 && !fits(B, 110 * 1024)) B = B > 4 ? B - 4 : B / 2;
-    if (!fits(B, 110 * 1024)) {
-      while (B > 1 && !fits(B, 220 * 1024)) B /= 2;
-      if (!fits(B, 220 * 1024)) c->tb2_ok = false;
-    }
-    c->rom_batch = B;
-    c->batch_tab.clear();
-    const int n = (int)c->inst_model.size();
-    for (int k = 0; k < n;) {
-      int e = k;
-      while (e < n && e - k < B && c->inst_model[e] == c->inst_model[k]) ++e;
-      c->batch_tab.insert(c->batch_tab.end(), {c->inst_model[k], k, e - k});
-      k = e;
-    }
-    if ((st = upload(c, &c->d_batch_tab, c->batch_tab)) != FDTD_OK) return st;
-    std::vector<double> l1(c->batch_tab.size() / 3 + 1, 0.0);
-    if ((st = upload(c, &c->d_level1, l1)) != FDTD_OK) return st;
-    if ((st = upload(c, &c->d_level1b, l1)) != FDTD_OK) return st;
-    if ((st = upload(c, &c->d_rects, c->rects)) != FDTD_OK) return st;
-  }
+  if ((st = upload(c, &c->d_rects, c->rects)) != FDTD_OK) return st;
   if ((st = upload_T(c, &c->d_Sk, c->Sk)) != FDTD_OK) return st;
   if ((st = upload(c, &c->d_Sk_off, c->Sk_off)) != FDTD_OK) return st;
   if ((st = upload(c, &c->d_port_off, c->port_off)) != FDTD_OK) return st;
@@ -645,9 +507,6 @@ fdtd_status upload_roms(fdtd_ctx* c) {
   if ((st = upload_T(c, &c->d_cyg, c->cyg)) != FDTD_OK) return st;
   if ((st = upload(c, &c->d_ehalf, c->ehalf)) != FDTD_OK) return st;
   if ((st = upload(c, &c->d_port_edge, c->port_edge)) != FDTD_OK) return st;
-  if ((st = upload(c, &c->d_port_h, c->port_h)) != FDTD_OK) return st;
-  if ((st = upload(c, &c->d_ring_idx, c->ring_idx)) != FDTD_OK) return st;
-  if ((st = upload(c, &c->d_ring_off, c->ring_off)) != FDTD_OK) return st;
   if ((st = upload(c, &c->d_state_off, c->state_off)) != FDTD_OK) return st;
   // ROM states start at zero (R26: x~0 = 0 with y0 = 0 on the freshly zeroed interface edges)
   std::vector<double> zero(c->state_len, 0.0);
@@ -655,9 +514,143 @@ fdtd_status upload_roms(fdtd_ctx* c) {
   c->d_state = nullptr;
   if ((st = upload_T(c, &c->d_state, zero)) != FDTD_OK) return st;
   if (prev) dfree(c, prev);
-  std::vector<double> zp(c->inst_model.size() + 1, 0.0);
+  std::vector<double> zp((size_t)KMAX * (c->inst_model.size() + 1), 0.0);
   if ((st = upload(c, &c->d_rom_partials, zp)) != FDTD_OK) return st;
-  if ((st = upload(c, &c->d_rom_partials2, zp)) != FDTD_OK) return st;
+  c->kz_dirty = true;
+  return FDTD_OK;
+}
+
+// Can this rank run K-step passes (K3)?  Every instance's fix-up region (block + 2K-1
+// cells) must lie inside the grid columns and inside this slab's rows, and the (block + K)
+// rectangles of two instances must not meet (so the fix-up of one never needs the other's ROM and
+// the zones are disjoint).
+bool passes_valid(const fdtd_ctx* c, int K) {
+  if (K > c->V) return false;  // a halo lane of V columns covers at most V steps of error spread
+  if (K == 1) return true;
+  const int64_t M = 2 * K - 1;
+  struct Rc { int64_t i0, j0, bx, by; };
+  std::vector<Rc> all;
+  for (size_t r = 0; r < c->rects.size(); r += 4) {
+    Rc x{c->rects[r], c->rects[r + 1], c->rects[r + 2], c->rects[r + 3]};
+    if (x.i0 - M < 0 || x.i0 + x.bx + M > c->d.nx || x.j0 - M < c->d.row_begin || x.j0 + x.by + M > c->d.row_end)
+      return false;
+    all.push_back(x);
+  }
+  std::sort(all.begin(), all.end(), [](const Rc& a, const Rc& b) { return a.i0 < b.i0; });
+  int64_t wmax = 0;
+  for (auto& r : all) wmax = std::max(wmax, r.bx);
+  for (size_t a = 0; a < all.size(); ++a)
+    for (size_t b = a + 1; b < all.size() && all[b].i0 <= all[a].i0 + all[a].bx + wmax + 2 * K; ++b) {
+      const Rc &A = all[a], &B = all[b];
+      const bool ox = A.i0 - K < B.i0 + B.bx + K && B.i0 - K < A.i0 + A.bx + K;
+      const bool oy = A.j0 - K < B.j0 + B.by + K && B.j0 - K < A.j0 + A.by + K;
+      if (ox && oy) return false;
+    }
+  return true;
+}
+
+fdtd_status apply_passes(fdtd_ctx* c, int k);
+
+// Zone depth, zone marks, fix-up batches and zone probes for passes of depth kz (all ranks agree
+// on kz: one NCCL min-reduction).  Runs at the first fdtd_step after a configuration change.
+fdtd_status configure_passes(fdtd_ctx* c) {
+  if (!c->kz_dirty) return FDTD_OK;
+  fdtd_status st;
+  int want = std::max(1, std::min(c->k_want, c->V));
+  int k = want >= 4 ? 4 : want >= 2 ? 2 : 1;
+  while (k > 1 && !passes_valid(c, k)) k /= 2;
+  // the fix-up kernel's shared memory: regions of margin 2k-1 plus the ROM vectors of a batch
+  auto stride_for = [&](int kk) {
+    int rs = 4;
+    for (auto& m : c->models) rs = std::max(rs, fdtd::region_elems(m.bx, m.by, 2 * kk - 1));
+    return (rs + 3) / 4 * 4;
+  };
+  auto fits = [&](int b, int rs, size_t lim) { return fdtd::post_smem_bytes(c->es, c->nvec, b, rs) <= lim; };
+  while (k > 1 && !fits(1, stride_for(k), 220 * 1024)) k /= 2;
+  c->k_ok = k;
+  if (c->d.nranks > 1 && c->comm) {  // collective min over ranks (all ranks reach this call together)
+    int32_t* d = (int32_t*)dalloc(c, sizeof(int32_t));
+    if (!d) return fail(c, FDTD_E_NOMEM, "agree");
+    const int32_t mine = k;
+    CK(cudaMemcpyAsync(d, &mine, sizeof mine, cudaMemcpyHostToDevice, c->stream));
+    NK(g_nccl.AllReduce(d, d, 1, NCCL_I32, NCCL_MIN, c->comm, c->stream));
+    int32_t all = 0;
+    CK(cudaMemcpyAsync(&all, d, sizeof all, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, d);
+    k = all;
+  }
+  return apply_passes(c, k);
+}
+
+fdtd_status apply_passes(fdtd_ctx* c, int k) {
+  fdtd_status st;
+  const int64_t n_rect = (int64_t)c->rects.size() / 4;
+  // zone marks: clear those of the previous depth, set those of the new one
+  if (n_rect > 0 && c->kz_marked != k) {
+    if (c->prec == 64) {
+      fdtd::launch_zone<double>((double*)c->coef[1], (const double*)c->coef[0], c->pitch, c->d_rects, n_rect,
+                                c->d.row_begin, ROW0, c->kz_marked, false, c->stream);
+      fdtd::launch_zone<double>((double*)c->coef[1], (const double*)c->coef[0], c->pitch, c->d_rects, n_rect,
+                                c->d.row_begin, ROW0, k, true, c->stream);
+    } else {
+      fdtd::launch_zone<float>((float*)c->coef[1], (const float*)c->coef[0], c->pitch, c->d_rects, n_rect,
+                               c->d.row_begin, ROW0, c->kz_marked, false, c->stream);
+      fdtd::launch_zone<float>((float*)c->coef[1], (const float*)c->coef[0], c->pitch, c->d_rects, n_rect,
+                               c->d.row_begin, ROW0, k, true, c->stream);
+    }
+    CK(cudaGetLastError());
+  }
+  c->kz_marked = k;
+  c->kz = k;
+  // batches of consecutive instances of one model (instances are stored grouped by model); the
+  // batch size keeps the fix-up kernel at <= ~200 KB of shared memory
+  {
+    int rs = 4;
+    for (auto& m : c->models) rs = std::max(rs, fdtd::region_elems(m.bx, m.by, 2 * k - 1));
+    c->region_stride = (rs + 3) / 4 * 4;
+    const char* env = getenv("FDTD_ROM_BATCH");
+    int B = env ? std::max(1, std::min(64, atoi(env))) : 8;
+    while (B > 1 && fdtd::post_smem_bytes(c->es, c->nvec, B, c->region_stride) > 200 * 1024) B = B > 4 ? B - 4 : B / 2;
+    c->rom_batch = B;
+    c->batch_tab.clear();
+    const int n = (int)c->inst_model.size();
+    for (int i = 0; i < n;) {
+      int e = i;
+      while (e < n && e - i < B && c->inst_model[e] == c->inst_model[i]) ++e;
+      c->batch_tab.insert(c->batch_tab.end(), {c->inst_model[i], i, e - i});
+      i = e;
+    }
+    if ((st = upload(c, &c->d_batch_tab, c->batch_tab)) != FDTD_OK) return st;
+    c->post_grid = std::max<int>(1, (int)(c->batch_tab.size() / 3));
+    std::vector<double> l1((size_t)KMAX * c->post_grid, 0.0);
+    if ((st = upload(c, &c->d_level1, l1)) != FDTD_OK) return st;
+  }
+  // zone probes: probes inside an instance's zone are recorded by its fix-up
+  {
+    const int n = (int)c->inst_model.size();
+    c->zp_off.assign(n + 1, 0);
+    c->zp.clear();
+    for (int i = 0; i < n; ++i) {
+      c->zp_off[i] = (int32_t)(c->zp.size() / 3);
+      if (k >= 2) {
+        const int64_t i0 = c->rects[4 * i], j0 = c->rects[4 * i + 1], bx = c->rects[4 * i + 2], by = c->rects[4 * i + 3];
+        for (int pr = 0; pr < c->n_probe; ++pr) {
+          const int64_t pi = c->probe_ij[2 * pr], pj = c->probe_ij[2 * pr + 1];
+          const bool hole = pi >= i0 && pi < i0 + bx && pj >= j0 && pj < j0 + by;
+          if (!hole && pi >= i0 - (k - 1) && pi < i0 + bx + k && pj >= j0 - (k - 1) && pj < j0 + by + k)
+            c->zp.insert(c->zp.end(), {(int32_t)pi, (int32_t)pj, pr});
+        }
+      }
+    }
+    c->zp_off[n] = (int32_t)(c->zp.size() / 3);
+    if (c->zp.empty()) c->zp.assign(3, 0);
+    if ((st = upload(c, &c->d_zp_off, c->zp_off)) != FDTD_OK) return st;
+    if ((st = upload(c, &c->d_zp, c->zp)) != FDTD_OK) return st;
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  c->kz_dirty = false;
+  drop_graph(c);
   return FDTD_OK;
 }
 
@@ -695,9 +688,9 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
   if (rb < 0 || re > d.ny || re <= rb) return FDTD_E_ARG;
   if (re - rb > (int64_t)1 << 30) return FDTD_E_ARG;
   if (nranks > 1 && !d.nccl_id && !(d.flags & FDTD_LOCAL_GROUP)) return FDTD_E_ARG;
-  // materials of rows [rb-2, re+1) (clipped to the grid): the two-step sweep reads two ghost rows
-  // below and one above the slab
-  const int64_t m0 = std::max<int64_t>(rb - 2, 0), m1 = std::min<int64_t>(re + 1, d.ny);
+  // materials of rows [rb-KMAX, re+KMAX) (clipped to the grid): a K-step sweep computes up to K
+  // ghost rows on each side of the slab
+  const int64_t m0 = std::max<int64_t>(rb - KMAX, 0), m1 = std::min<int64_t>(re + KMAX, d.ny);
   if (d.materials_row0 > m0) return FDTD_E_ARG;
 
   c = new fdtd_ctx();
@@ -709,10 +702,11 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
   c->es = d.precision == 64 ? 8 : 4;
   c->V = 16 / (int)c->es;
   c->rows = (int)(re - rb);
-  c->nrows_alloc = c->rows + 5;
+  c->nrows_alloc = c->rows + ROW0 + GHOST_UP;
   c->ncolv = (int)((d.nx + c->V - 1) / c->V);
   const int64_t align = 128 / (int64_t)c->es;
-  c->pitch = ((int64_t)c->ncolv * c->V + align - 1) / align * align;
+  // at least one column past the grid: the east PEC wall Ey[j][nx] (always 0) is read by the fix-up
+  c->pitch = (std::max<int64_t>((int64_t)c->ncolv * c->V, d.nx + 1) + align - 1) / align * align;
   c->cap = d.record_capacity > 0 ? d.record_capacity : 65536;
   c->stream = (cudaStream_t)d.stream;
   if (cudaSetDevice(d.device) != cudaSuccess) {
@@ -772,7 +766,9 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
     return FDTD_E_UNSTABLE;
   }
 
-  const size_t fbytes = (size_t)c->nrows_alloc * c->pitch * c->es;
+  // + a tail: the sweep's lanes past the last vector column load unconditionally (their values are
+  // never stored), reaching up to 31 vectors beyond the last row of an array
+  const size_t fbytes = (size_t)c->nrows_alloc * c->pitch * c->es + 32 * 1024;
   for (int b = 0; b < 2; ++b)
     for (int a = 0; a < 3; ++a)
       if (!(c->f[b][a] = dalloc(c, fbytes))) { fdtd_destroy(c); return FDTD_E_NOMEM; }
@@ -781,9 +777,9 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
   c->d_step = (int64_t*)dalloc(c, sizeof(int64_t));
   c->d_done = (unsigned*)dalloc(c, sizeof(unsigned) * 4);
   c->d_energy_ring = (double*)dalloc(c, c->cap * sizeof(double));
-  c->d_level1 = (double*)dalloc(c, 16 * sizeof(double));
-  c->d_level1b = (double*)dalloc(c, 16 * sizeof(double));
-  if (const char* e = getenv("FDTD_TB2")) c->tb2_want = atoi(e) != 0;
+  c->d_level1 = (double*)dalloc(c, KMAX * sizeof(double));
+  c->k_want = c->V;  // deepest pass the vector width allows (4 in fp32, 2 in fp64)
+  if (const char* e = getenv("FDTD_K")) c->k_want = std::max(1, atoi(e));
   if (!c->d_step || !c->d_done || !c->d_energy_ring) { fdtd_destroy(c); return FDTD_E_NOMEM; }
   fdtd_status st = f32 ? build_coefficients<float>(c) : build_coefficients<double>(c);
   if (st != FDTD_OK) { fdtd_destroy(c); return st; }
@@ -808,18 +804,15 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
 fdtd_status fdtd_set_tuning(fdtd_ctx* c, int32_t rows_per_cta, int32_t warps_per_cta) {
   if (!c) return FDTD_E_ARG;
   if (rows_per_cta < 0 || warps_per_cta < 0 || warps_per_cta > 8) return fail(c, FDTD_E_ARG, "bad tuning");
-  c->chunk = rows_per_cta ? rows_per_cta : (c->rows >= 4096 ? 64 : 32);
+  c->chunk = rows_per_cta ? rows_per_cta : (c->rows >= 4096 ? 128 : 32);
   c->warps = warps_per_cta ? warps_per_cta : 4;
-  const int per_cta = 32 * c->warps;
-  const int gx = std::max((c->ncolv + per_cta - 1) / per_cta, fdtd::sweep2_ctas_x(c->ncolv, c->warps));
+  const int gx = sweep_gx(c);
   const int gy = (c->rows + c->chunk - 1) / c->chunk;
   const int n = gx * gy;
   if (n > c->n_partials) {
     if (c->d_partials) dfree(c, c->d_partials);
-    if (c->d_partials2) dfree(c, c->d_partials2);
-    c->d_partials = (double*)dalloc(c, (size_t)n * sizeof(double));
-    c->d_partials2 = (double*)dalloc(c, (size_t)n * sizeof(double));
-    if (!c->d_partials || !c->d_partials2) return fail(c, FDTD_E_NOMEM, "partials");
+    c->d_partials = (double*)dalloc(c, (size_t)KMAX * n * sizeof(double));
+    if (!c->d_partials) return fail(c, FDTD_E_NOMEM, "partials");
     c->n_partials = n;
   }
   drop_graph(c);
@@ -1017,9 +1010,6 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
       c->cya.push_back(ay / cy);
       c->cyg.push_back(Dl * G / cy);
       c->ehalf.push_back(Dl * Dlp * eps / dt);
-      int64_t oi, oj;
-      outside(i0, j0, p, oi, oj);
-      c->port_h.push_back(lrow(c, oj) * P_ + oi);
       int64_t e;
       if (p < bx) e = lrow(c, j0) * P_ + i0 + p;
       else if (p < 2 * bx) e = lrow(c, j0 + by) * P_ + i0 + p - bx;
@@ -1031,12 +1021,6 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
     if (!dense::inverse(A, nY, S)) return fail(c, FDTD_E_ARG, "singular interface Schur matrix");
     for (int j = 0; j < nY; ++j)  // column-major
       for (int i = 0; i < nY; ++i) c->Sk.push_back(S[(size_t)i * nY + j]);
-    if (c->ring_off.empty()) c->ring_off.push_back(0);
-    for (int64_t jj = j0; jj < j0 + by; ++jj)
-      for (int64_t ii = i0; ii < i0 + bx; ++ii)
-        if (jj == j0 || jj == j0 + by - 1 || ii == i0 || ii == i0 + bx - 1)
-          c->ring_idx.push_back(lrow(c, jj) * P_ + ii);
-    c->ring_off.push_back((int64_t)c->ring_idx.size());
   }
   // masks (coefficients + zeroed holes/interfaces in both buffers)
   std::vector<int32_t> nr(c->rects.end() - 4 * count, c->rects.end());
@@ -1082,22 +1066,32 @@ fdtd_status fdtd_set_source(fdtd_ctx* c, int64_t i, int64_t j, const double* sam
 
 fdtd_status fdtd_set_probes(fdtd_ctx* c, const int64_t* ij, int32_t n) {
   if (!c || n < 0 || (n > 0 && !ij)) return FDTD_E_ARG;
-  std::vector<int64_t> idx(std::max(n, 1), 0);
-  // probes outside this rank read a dedicated always-zero slot (ghost row above, column 0 is never
-  // written for Hz); they contribute 0 to the cross-rank sum
-  const int64_t zero_slot = (int64_t)(ROW0 + c->rows + 1) * c->pitch + c->pitch - 1;  // Hz never written there
+  // S3: the sweep records the probes of its own rows (a per-row table); probes of other ranks are
+  // never written here and contribute 0 to the cross-rank sum
+  std::vector<std::array<int64_t, 3>> own;  // (local row, column, probe index)
+  c->probe_ij.assign(ij, ij + 2 * (int64_t)n);
   for (int32_t k = 0; k < n; ++k) {
     const int64_t i = ij[2 * k], j = ij[2 * k + 1];
     if (i < 0 || i >= c->d.nx || j < 0 || j >= c->d.ny) return fail(c, FDTD_E_ARG, "probe %d outside grid", k);
-    idx[k] = (j >= c->d.row_begin && j < c->d.row_end) ? lrow(c, j) * c->pitch + i : zero_slot;
+    if (j >= c->d.row_begin && j < c->d.row_end) own.push_back({lrow(c, j), i, k});
   }
-  fdtd_status st = upload(c, &c->d_probe_idx, idx);
+  std::sort(own.begin(), own.end());
+  std::vector<int2> rows_tab((size_t)c->nrows_alloc, int2{0, 0}), list(std::max<size_t>(own.size(), 1), int2{0, 0});
+  for (size_t t = 0; t < own.size(); ++t) {
+    list[t] = int2{(int)own[t][1], (int)own[t][2]};
+    int2& r = rows_tab[own[t][0]];
+    if (r.y == 0) r.x = (int)t;
+    r.y += 1;
+  }
+  fdtd_status st = upload(c, &c->d_probe_rows, rows_tab);
   if (st != FDTD_OK) return st;
+  if ((st = upload(c, &c->d_probe_list, list)) != FDTD_OK) return st;
   if (c->d_probe_ring) dfree(c, c->d_probe_ring);
   c->d_probe_ring = dalloc(c, (size_t)std::max(n, 1) * c->cap * c->es);
   if (!c->d_probe_ring) return fail(c, FDTD_E_NOMEM, "probe ring");
   c->n_probe = n;
   c->rd_probe = c->steps;
+  c->kz_dirty = true;  // zone probes
   drop_graph(c);
   return FDTD_OK;
 }
@@ -1121,33 +1115,25 @@ fdtd_status fdtd_step(fdtd_ctx* c, int64_t nsteps) {
     return fail(c, FDTD_E_STATE, "unread records would exceed record_capacity (%lld)", (long long)c->cap);
   if (c->d.flags & FDTD_LOCAL_GROUP) return fail(c, FDTD_E_STATE, "members of a local group step with fdtd_step_group");
   const bool use_graph = !(c->d.flags & FDTD_NO_GRAPH) && c->d.nranks == 1 && !c->profiling;
-  {
-    fdtd_status st0 = agree_tb2(c);
-    if (st0 != FDTD_OK) return st0;
-  }
-  const bool pairs = tb2_active(c);
-  fdtd_status st;
+  fdtd_status st = configure_passes(c);
+  if (st != FDTD_OK) return st;
   int64_t left = nsteps;
   while (left > 0) {
-    const int per = pairs ? 4 : 2;
+    const int per = 2 * c->kz;
     if (use_graph && c->cur == 0 && left >= per) {
       if (c->graph_dirty || !c->gexec || c->graph_steps != per)
         if ((st = build_graph(c)) != FDTD_OK) return st;
       CK(cudaGraphLaunch(c->gexec, c->stream));
-      c->launches += 4;  // two sweep + two post launches per graph period
+      c->launches += c->graph_launches;
       c->steps += per;
       left -= per;
       continue;
     }
-    if (pairs && left >= 2) {
-      if ((st = enqueue_pair(c, c->cur, c->stream)) != FDTD_OK) return st;
-      c->steps += 2;
-      left -= 2;
-    } else {
-      if ((st = enqueue_step(c, c->cur, c->stream)) != FDTD_OK) return st;
-      c->steps += 1;
-      left -= 1;
-    }
+    // passes of depth kz; a remainder with shallower passes (the zone marks stay those of kz)
+    const int K = left >= c->kz ? c->kz : left >= 2 ? 2 : 1;
+    if ((st = enqueue_pass(c, c->cur, c->stream, K)) != FDTD_OK) return st;
+    c->steps += K;
+    left -= K;
     c->cur ^= 1;
   }
   CK(cudaGetLastError());
@@ -1333,28 +1319,39 @@ fdtd_status fdtd_step_group(fdtd_ctx** g, int32_t n, int64_t nsteps) {
     if (c->steps + nsteps - oldest > c->cap) return fail(c, FDTD_E_STATE, "unread records would overflow");
   }
   cudaStream_t s = g[0]->stream;
-  bool pairs = true;  // two-step passes only if every slab can
-  for (int k = 0; k < n; ++k) {
-    g[k]->tb2_dirty = false;
-    g[k]->tb2_all = g[k]->tb2_want && g[k]->tb2_ok;
-    pairs = pairs && g[k]->tb2_all;
+  int k = KMAX;  // pass depth: the deepest every slab can do
+  for (int r = 0; r < n; ++r) {
+    fdtd_ctx* c = g[r];
+    if (c->kz_dirty) {
+      int want = std::max(1, std::min(c->k_want, c->V));
+      int kk = want >= 4 ? 4 : want >= 2 ? 2 : 1;
+      while (kk > 1 && !passes_valid(c, kk)) kk /= 2;
+      c->k_ok = kk;
+    } else {
+      c->k_ok = c->kz;
+    }
+    k = std::min(k, c->k_ok);
   }
-  for (int k = 0; k < n; ++k) g[k]->tb2_all = pairs;
+  for (int r = 0; r < n; ++r)
+    if (g[r]->kz_dirty || g[r]->kz != k) {
+      fdtd_status st = apply_passes(g[r], k);
+      if (st != FDTD_OK) return st;
+    }
   int64_t left = nsteps;
   while (left > 0) {
-    const bool pr = pairs && left >= 2;
+    const int K = left >= k ? k : left >= 2 ? 2 : 1;
     const int q = g[0]->cur;
-    for (int k = 0; k < n; ++k) {
-      fdtd_status st = halo_local(g, n, k, q, s, pr ? 2 : 1);
+    for (int r = 0; r < n; ++r) {
+      fdtd_status st = halo_local(g, n, r, q, s, K);
       if (st != FDTD_OK) return st;
     }
-    for (int k = 0; k < n; ++k) {
-      fdtd_status st = pr ? enqueue_pair(g[k], q, s) : enqueue_step(g[k], q, s);
+    for (int r = 0; r < n; ++r) {
+      fdtd_status st = enqueue_pass(g[r], q, s, K);
       if (st != FDTD_OK) return st;
-      g[k]->steps += pr ? 2 : 1;
-      g[k]->cur ^= 1;
+      g[r]->steps += K;
+      g[r]->cur ^= 1;
     }
-    left -= pr ? 2 : 1;
+    left -= K;
   }
   fdtd_ctx* c = g[0];
   CK(cudaGetLastError());
@@ -1362,8 +1359,9 @@ fdtd_status fdtd_step_group(fdtd_ctx** g, int32_t n, int64_t nsteps) {
 }
 
 fdtd_status fdtd_set_time_blocking(fdtd_ctx* c, int32_t steps_per_pass) {
-  if (!c || (steps_per_pass != 1 && steps_per_pass != 2)) return FDTD_E_ARG;
-  c->tb2_want = steps_per_pass == 2;
+  if (!c || (steps_per_pass != 1 && steps_per_pass != 2 && steps_per_pass != 4)) return FDTD_E_ARG;
+  c->k_want = steps_per_pass;
+  c->kz_dirty = true;
   drop_graph(c);
   return FDTD_OK;
 }
@@ -1372,7 +1370,6 @@ fdtd_status fdtd_profile(fdtd_ctx* c, int32_t on) {
   if (!c) return FDTD_E_ARG;
   c->profiling = on != 0;
   c->ev_used = 0;
-  c->prof_pairs = 0;
   return FDTD_OK;
 }
 
@@ -1391,7 +1388,6 @@ fdtd_status fdtd_profile_read(fdtd_ctx* c, double* sweep_ms, double* post_ms, in
   *post_ms = b;
   *n = (int64_t)(c->ev_used / 3);
   c->ev_used = 0;
-  c->prof_pairs = 0;
   return FDTD_OK;
 }
 
@@ -1409,7 +1405,7 @@ fdtd_status fdtd_get_info(const fdtd_ctx* c, fdtd_info* o) {
   o->sweep_ctas = c->n_partials;
   o->graphs = !(c->d.flags & FDTD_NO_GRAPH) && c->d.nranks == 1;
   o->precision = c->prec;
-  o->steps_per_pass = tb2_active(c) ? 2 : 1;
+  o->steps_per_pass = c->kz;
   // read Ex, Ey, Hz, mea, msb and write Ex, Ey, Hz once per pass
   o->bytes_per_cell_step = 8.0 * (double)c->es / o->steps_per_pass;
   o->sweep_stream = (void*)c->stream;

@@ -15,6 +15,7 @@
 //                    energy partials in a fixed order and advances the step counter.
 #include "fdtd_kernels.cuh"
 
+#include <climits>
 #include <cstdio>
 
 namespace fdtd {
@@ -45,6 +46,16 @@ __device__ __forceinline__ void stv(float* p, const float (&v)[4]) {
 __device__ __forceinline__ void stv(double* p, const double (&v)[2]) {
   *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
 }
+__device__ __forceinline__ void ldv_s(const float* p, float (&v)[4]) {
+  const float4 x = *reinterpret_cast<const float4*>(p);
+  v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+}
+__device__ __forceinline__ void ldv_s(const double* p, double (&v)[2]) {
+  const double2 x = *reinterpret_cast<const double2*>(p);
+  v[0] = x.x; v[1] = x.y;
+}
+__device__ __forceinline__ void stv_s(float* p, const float (&v)[4]) { stv(p, v); }
+__device__ __forceinline__ void stv_s(double* p, const double (&v)[2]) { stv(p, v); }
 __device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 __device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
@@ -67,364 +78,325 @@ __device__ __forceinline__ float rcp_rn(float x) {
 }
 __device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
 
-// E half-step of one edge from the two adjacent cells' material terms (eq:updateEx divided by
-// its left-hand coefficient):  E' = [(a - s) E + dH / l] / (a + s),  a = eps/dt, s = sigma/2 of
-// the edge (arithmetic means, R2), l = the dual length.  An edge next to a cell with a < 0
-// (ROM hole, PEC wall, padding) keeps its value (PEC edges stay 0; interface edges are
-// written by the ROM kernel).
+// Coefficients of one edge of eq:updateEx (and its Ey analogue) divided by its left-hand
+// coefficient, from the two adjacent cells' material terms (arithmetic means, R2):
+//   E' = ca E + cb dH,  ca = (a - s)/(a + s) = 1 - 2s/(a + s),  cb = il/(a + s),
+// a = eps/dt, s = sigma/2 of the edge, il = 1/dy (Ex, dH = H - H_below) or -1/dx (Ey,
+// dH = H - H_left).  An edge next to a cell with a < 0 (ROM hole, PEC wall, padding) is dead:
+// ca = 1, cb = 0 keeps its value exactly (PEC edges stay 0; interface edges belong to the ROM).
+// The sign bit of s0 / s1 marks fix-up zone cells and is ignored here.
 template <typename T>
-__device__ __forceinline__ T eupd(T e, T dh_over_l, T a0, T s0, T a1, T s1, bool& live, T& a) {
+__device__ __forceinline__ void edge_coef(T a0, T s0, T a1, T s1, T il, T& ca, T& cb, T& a, bool& live) {
   a = a0 + a1;
-  const T s = s0 + s1;
+  const T s = fabs(s0) + fabs(s1);
   live = (a0 >= T(0)) & (a1 >= T(0));
   const T r = rcp_rn(a + s);
-  const T v = mul_rn(r, fma_rn(a - s, e, dh_over_l));
-  return live ? v : e;
+  // ca = 1 - 2 s r: exactly 1 on lossless edges whatever the rounding of r (an approximate
+  // reciprocal only perturbs the small loss term and the curl gain, so a lossless grid stays
+  // lossless instead of decaying by ~1 ulp per step)
+  ca = live ? fma_rn(T(-2) * s, r, T(1)) : T(1);
+  cb = live ? mul_rn(r, il) : T(0);
 }
 
-// Cells outside the live grid (ROM hole, ghost row below the grid, padding) keep their Hz.
 template <typename T>
-__device__ __forceinline__ T hmask(T mea_cell, T hold, T hnew) {
-  return mea_cell < T(0) ? hold : hnew;
+__device__ __forceinline__ T eupd(T e, T ca, T cb, T dh) {
+  return fma_rn(ca, e, mul_rn(cb, dh));
 }
 
-template <typename T, bool ENERGY>
-__global__ void __launch_bounds__(256) sweep_kernel(const SweepParams<T> p) {
-  constexpr int V = VT<T>::N;
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int wpc = blockDim.x >> 5;
-  const int colv = (blockIdx.x * wpc + warp) * 32 + lane;
-  const bool act = colv < p.ncolv;
-  const int64_t c = (int64_t)colv * V;
-  const int cy = p.chunk0 + blockIdx.y;  // row chunk
-  const int r0 = p.row0 + cy * p.chunk;
-  const int r1 = min(r0 + p.chunk, p.row0 + p.rows);
-  const int64_t P = p.pitch;
+// Storage-function partial (eq:R, R17) of one cell at the start of a step, accumulated into acc:
+// (1/dt)[C E^2 of the cell's bottom Ex and left Ey edge + mu A H^{n-1/2} H^{n+1/2}] with the
+// weights wx, wy = dx dy a of live edges (C/dt = dx dy eps/dt), hw = mu0 dx dy / dt.
+template <typename T>
+__device__ __forceinline__ T cell_energy(T acc, T ex, T ey, T h0, T h1, T wx, T wy, T hw) {
+  return fma_rn(mul_rn(hw, h0), h1, fma_rn(mul_rn(wy, ey), ey, fma_rn(mul_rn(wx, ex), ex, acc)));
+}
 
-  T src = T(0);
-  if (p.src_row >= 0) {
-    const int64_t k = *p.step - p.src_t0;
-    if (k >= 0 && k < p.src_n) src = (T)p.src_samples[k];
-  }
+// Per-cell coefficient set of one row of a warp strip (K1): the cell's bottom Ex edge
+// (cax, cbx), left Ey edge (cay, cby), the energy weights of those edges (wx, wy; 0 if dead or a
+// zone cell) and hw = mu0 dx dy/dt (+0 on zone cells: the fix-up adds their energy; -0 on dead
+// cells, whose Hz is kept).  Built once per pass at stage 0 and reused by stages 1..K-1.
+template <typename T, int V>
+struct RowCoef {
+  T cax[V], cbx[V], cay[V], cby[V], wx[V], wy[V], hw[V];
+};
+constexpr int NCOEF = 7;
 
-  // carried between rows: Ex^n of edge row j, Hz^{n+1/2} of cell row j-1, materials of row j-1
-  T exc[V], hzp[V], mpa[V], mps[V], exn[V], eyv[V], hzv[V], ma[V], ms[V];
-  T excl = T(0);
-  // ---- prologue: row r0-1 (recomputed; the ghost row when r0 == 1)
-  {
-    const int64_t rj = (int64_t)(r0 - 1) * P;
-    T exl[V];
+template <typename T, int V>
+__device__ __forceinline__ void row_coef(const T (&ma)[V], const T (&ms)[V], const T (&mb)[V], const T (&sb)[V],
+                                         T idx, T idy, T wxy, T wh, RowCoef<T, V>& cf) {
+  const T la = __shfl_up_sync(FULL, ma[V - 1], 1);
+  const T ls = __shfl_up_sync(FULL, ms[V - 1], 1);
 #pragma unroll
-    for (int k = 0; k < V; ++k) exl[k] = exn[k] = eyv[k] = hzv[k] = mpa[k] = mps[k] = T(0);
-    if (act) {
-      ldv(p.ex0 + rj + c, exl);
-      ldv(p.ex0 + rj + P + c, exn);
-      ldv(p.ey0 + rj + c, eyv);
-      ldv(p.hz0 + rj + c, hzv);
-      ldv(p.mea + rj + c, mpa);
-      ldv(p.msb + rj + c, mps);
-    }
-    T eyr = __shfl_down_sync(FULL, eyv[0], 1);
-    if (lane == 31) eyr = (act && colv + 1 < p.ncolv) ? __ldg(p.ey0 + rj + c + V) : T(0);
+  for (int k = 0; k < V; ++k) {
+    bool lx, ly;
+    T ax, ay;
+    edge_coef(mb[k], sb[k], ma[k], ms[k], idy, cf.cax[k], cf.cbx[k], ax, lx);
+    edge_coef(k ? ma[k - 1] : la, k ? ms[k - 1] : ls, ma[k], ms[k], -idx, cf.cay[k], cf.cby[k], ay, ly);
+    const bool z = signbit(ms[k]);
+    cf.wx[k] = (lx && !z) ? mul_rn(wxy, ax) : T(0);
+    cf.wy[k] = (ly && !z) ? mul_rn(wxy, ay) : T(0);
+    cf.hw[k] = ma[k] < T(0) ? T(-0.0) : (z ? T(0) : wh);
+  }
+}
+
+// One Yee step on one row r of a warp's column strip (K1): Hz^{new} of row r from
+// (Ex edge rows r and r+1, Ey and Hz of row r), the soft source, then Ex of edge row r and Ey of
+// row r from Hz^{new} of rows r and r-1 (hb).  Column neighbours come from warp shuffles (lane 0 /
+// 31 of a strip get wrong outermost values; they are redundant halo lanes).  All lanes call it.
+// Returns the row's storage-function partial of W at the step's start (zone cells excluded).
+template <typename T, int V, bool ENERGY>
+__device__ __forceinline__ T yee_row(const T (&exb)[V], const T (&ext)[V], const T (&ey)[V], const T (&hz)[V],
+                                     const T (&hb)[V], const RowCoef<T, V>& cf, const SweepParams<T>& p, T gsrc,
+                                     bool srow, int src_k, T (&hn)[V], T (&exo)[V], T (&eyo)[V]) {
+  const T eyr = __shfl_down_sync(FULL, ey[0], 1);
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const T hu = hupd(hz[k], ext[k], exb[k], k + 1 < V ? ey[k + 1] : eyr, ey[k], p.chy, p.chx);
+    hn[k] = signbit(cf.hw[k]) ? hz[k] : hu;  // dead cells keep their Hz
+  }
+  if (srow) {  // S2: soft source after the H half-step (this lane holds the source column)
 #pragma unroll
     for (int k = 0; k < V; ++k)
-      hzp[k] = hmask(mpa[k], hzv[k], hupd(hzv[k], exn[k], exl[k], k + 1 < V ? eyv[k + 1] : eyr, eyv[k], p.chy, p.chx));
-    if (r0 - 1 == p.src_row) {
-#pragma unroll
-      for (int k = 0; k < V; ++k)
-        if (c + k == p.src_col) hzp[k] += src;
-    }
-#pragma unroll
-    for (int k = 0; k < V; ++k) exc[k] = exn[k];
-    if (lane == 0 && act && c > 0) excl = __ldg(p.ex0 + rj + P + c - 1);
+      if (k == src_k) hn[k] += gsrc;
   }
+  const T hl = __shfl_up_sync(FULL, hn[V - 1], 1);
+  T en = T(0);
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    exo[k] = eupd(exb[k], cf.cax[k], cf.cbx[k], hn[k] - hb[k]);
+    eyo[k] = eupd(ey[k], cf.cay[k], cf.cby[k], hn[k] - (k ? hn[k - 1] : hl));
+    if (ENERGY) en = cell_energy(en, exb[k], ey[k], hz[k], hn[k], cf.wx[k], cf.wy[k], cf.hw[k]);
+  }
+  return en;
+}
 
-  double eacc = 0.0;
-  for (int j = r0; j < r1; ++j) {
-    const int64_t rj = (int64_t)j * P;
-    const int64_t rn = rj + P;
+// S3 probes: record Hz^{n+s+1/2} of the probes in row r owned by this lane (sorted per row).
+template <typename T, int V, typename X>
+__device__ __forceinline__ void record_probes(const SweepParams<T>& p, int r, int64_t, const T (&h)[V], int64_t slot,
+                                              const X& x) {
+  if (!p.probe_rows) return;
+  const int2 pr = __ldg(p.probe_rows + r);
+  if (pr.y == 0) return;
+  const int64_t c = x.pex - p.ex0;  // this lane's first column
+  for (int i = 0; i < pr.y; ++i) {
+    const int2 e = __ldg(p.probe_list + pr.x + i);
+    const int64_t d = (int64_t)e.x - c;
+    if (d >= 0 && d < V) {
+      T v = h[0];
 #pragma unroll
-    for (int k = 0; k < V; ++k) exn[k] = eyv[k] = hzv[k] = ma[k] = ms[k] = T(0);
-    if (act) {
-      ldv(p.ex0 + rn + c, exn);
-      ldv(p.ey0 + rj + c, eyv);
-      ldv(p.hz0 + rj + c, hzv);
-      ldv(p.mea + rj + c, ma);
-      ldv(p.msb + rj + c, ms);
-    }
-    T lhz = T(0), lexn = T(0), ley = T(0), lma = T(-1), lms = T(0);
-    if (lane == 0 && act && c > 0) {
-      lhz = __ldg(p.hz0 + rj + c - 1);
-      lexn = __ldg(p.ex0 + rn + c - 1);
-      ley = __ldg(p.ey0 + rj + c - 1);
-      lma = __ldg(p.mea + rj + c - 1);
-      lms = __ldg(p.msb + rj + c - 1);
-    }
-    T eyr = __shfl_down_sync(FULL, eyv[0], 1);
-    if (lane == 31) eyr = (act && colv + 1 < p.ncolv) ? __ldg(p.ey0 + rj + c + V) : T(0);
-    T hzn[V];
-#pragma unroll
-    for (int k = 0; k < V; ++k)
-      hzn[k] = hmask(ma[k], hzv[k], hupd(hzv[k], exn[k], exc[k], k + 1 < V ? eyv[k + 1] : eyr, eyv[k], p.chy, p.chx));
-    if (j == p.src_row) {  // S2: soft source after the H half-step
-#pragma unroll
-      for (int k = 0; k < V; ++k)
-        if (c + k == p.src_col) hzn[k] += src;
-    }
-    T hl = __shfl_up_sync(FULL, hzn[V - 1], 1);
-    T la = __shfl_up_sync(FULL, ma[V - 1], 1);
-    T ls = __shfl_up_sync(FULL, ms[V - 1], 1);
-    if (lane == 0) {
-      if (c > 0) {
-        hl = hmask(lma, lhz, hupd(lhz, lexn, excl, eyv[0], ley, p.chy, p.chx));
-        if (j == p.src_row && c - 1 == p.src_col) hl += src;
-      } else {
-        hl = T(0);  // Ey column 0 is the PEC wall (lma = -1 keeps it at 0)
-      }
-      la = lma;
-      ls = lms;
-      excl = lexn;
-    }
-    T exo[V], eyo[V];
-    T e = T(0);
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      bool lx, ly;
-      T ax, ay;
-      // Ex edge (row j, column c+k): cells (c+k, j-1) and (c+k, j)
-      exo[k] = eupd(exc[k], mul_rn(p.idy, hzn[k] - hzp[k]), mpa[k], mps[k], ma[k], ms[k], lx, ax);
-      // Ey edge (row j, column c+k): cells (c+k-1, j) and (c+k, j)
-      const T hleft = k ? hzn[k - 1] : hl;
-      eyo[k] = eupd(eyv[k], -mul_rn(p.idx, hzn[k] - hleft), k ? ma[k - 1] : la, k ? ms[k - 1] : ls, ma[k], ms[k],
-                    ly, ay);
-      if (ENERGY) {  // S3: (1/dt)[C E^2 + mu A H^{n-1/2} H^{n+1/2}], C/dt = dx dy a
-        e += p.wxy * ((lx ? ax * exc[k] * exc[k] : T(0)) + (ly ? ay * eyv[k] * eyv[k] : T(0)));
-        e += p.wh * hzv[k] * hzn[k];
-      }
-    }
-    if (act) {
-      stv(p.hz1 + rj + c, hzn);
-      stv(p.ex1 + rj + c, exo);
-      stv(p.ey1 + rj + c, eyo);
-    }
-    if (ENERGY) eacc += (double)e;
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      exc[k] = exn[k];
-      hzp[k] = hzn[k];
-      mpa[k] = ma[k];
-      mps[k] = ms[k];
-    }
-  }
-  if (ENERGY) {
-    __shared__ double red[32];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) eacc += __shfl_down_sync(FULL, eacc, o);
-    if (lane == 0) red[warp] = eacc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int w = 0; w < wpc; ++w) s += red[w];
-      p.partials[(int64_t)cy * gridDim.x + blockIdx.x] = s;
+      for (int k = 1; k < V; ++k)
+        if (d == k) v = h[k];
+      p.probe_ring[(int64_t)e.y * p.cap + slot] = v;
     }
   }
 }
 
-// K1b: two time steps per pass.  At row j the warp advances
-// step n on row j and step n+1 on row j-1 entirely in registers, so each field and material
-// byte crosses HBM once per two steps.  Lanes 0 and 31 are redundant halo lanes (their
-// leftmost / rightmost values may be wrong after the first step, which only they use); lanes
-// 1..30 store.  Interface edges are treated as frozen (masked) in both steps; the fix-up
-// kernel (post2) repairs the cells and edges next to every ROM instance.
-template <typename T, bool ENERGY>
-__global__ void __maxnreg__(96) sweep2_kernel(const SweepParams<T> p) {
+// per-warp shared-memory ring of K rows of coefficient sets (lane-private 16-byte vectors)
+template <typename T, int V>
+__device__ __forceinline__ void ring_store(T* ring, int slot, int lane, const RowCoef<T, V>& cf) {
+  T* b = ring + ((int64_t)slot * NCOEF * 32 + lane) * V;
+  stv_s(b + 0 * 32 * V, cf.cax); stv_s(b + 1 * 32 * V, cf.cbx); stv_s(b + 2 * 32 * V, cf.cay);
+  stv_s(b + 3 * 32 * V, cf.cby); stv_s(b + 4 * 32 * V, cf.wx); stv_s(b + 5 * 32 * V, cf.wy);
+  stv_s(b + 6 * 32 * V, cf.hw);
+}
+template <typename T, int V>
+__device__ __forceinline__ void ring_load(const T* ring, int slot, int lane, RowCoef<T, V>& cf) {
+  const T* b = ring + ((int64_t)slot * NCOEF * 32 + lane) * V;
+  ldv_s(b + 0 * 32 * V, cf.cax); ldv_s(b + 1 * 32 * V, cf.cbx); ldv_s(b + 2 * 32 * V, cf.cay);
+  ldv_s(b + 3 * 32 * V, cf.cby); ldv_s(b + 4 * 32 * V, cf.wx); ldv_s(b + 5 * 32 * V, cf.wy);
+  ldv_s(b + 6 * 32 * V, cf.hw);
+}
+
+// Row data of one stage-0 row j (loaded from HBM): Ex of edge row j+1, Ey / Hz / materials of row j
+template <typename T, int V>
+struct RowIn {
+  T ext[V], ey[V], hz[V], ma[V], ms[V];
+};
+// Outputs of every stage at one stage-0 row j: stage s's Hz^{n+s+1/2}, Ex^{n+s+1}, Ey^{n+s+1} of row j-s
+template <typename T, int V, int K>
+struct StageOut {
+  T h[K][V], x[K][V], y[K][V];
+};
+
+template <typename T, int V, int K>
+struct SweepCtx {
+  const T *pex, *pey, *phz, *pma, *pms;  // this lane's column in row 0 of each input array
+  T* ring;
+  int lane, r0, r1, src_r, src_k;
+  bool out;
+  int64_t step, P;
+  T g[K];
+};
+
+// One stage-0 row j of the K-step sweep: X holds row j's data, Y row j-1's (and receives row
+// j+1's once stage 0 is done), A the stage outputs of row j-1, B receives those of row j.
+// Naming the two buffers statically (the caller alternates them) keeps every carried value in
+// place: no register moves.
+template <typename T, int V, int K, bool ENERGY, bool CHK, bool PROBES>
+__device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCtx<T, V, K>& x, int j, int je,
+                                          const RowIn<T, V>& X, RowIn<T, V>& Y, const StageOut<T, V, K>& A,
+                                          StageOut<T, V, K>& B, double (&eacc)[K]) {
+  // CHK: some stage rows may lie outside the chunk [r0, r1) (energy, probes and stores skip them);
+  // without CHK every stage row is the chunk's own.  PROBES: look up the per-row probe table.
+  {  // ---- stage 0: step n on row j
+    RowCoef<T, V> cf;
+    row_coef<T, V>(X.ma, X.ms, Y.ma, Y.ms, p.idx, p.idy, p.wxy, p.wh, cf);
+    if (K > 1) ring_store<T, V>(x.ring, j & (K - 1), x.lane, cf);
+    const T en = yee_row<T, V, ENERGY>(Y.ext, X.ext, X.ey, X.hz, A.h[0], cf, p, x.g[0], j == x.src_r, x.src_k,
+                                       B.h[0], B.x[0], B.y[0]);
+    const bool own = !CHK || (j >= x.r0 && j < x.r1);
+    if (ENERGY && own) eacc[0] += (double)en;
+    if (PROBES && own && x.out) record_probes<T, V>(p, j, (int64_t)0, B.h[0], x.step % p.cap, x);
+  }
+  if (j + 1 < je) {  // row j+1 into the buffer of row j-1 (consumed above)
+    const int64_t o = (int64_t)(j + 1) * x.P;
+    ldv(x.pex + o + x.P, Y.ext);
+    ldv(x.pey + o, Y.ey);
+    ldv(x.phz + o, Y.hz);
+    ldv(x.pma + o, Y.ma);
+    ldv(x.pms + o, Y.ms);
+  }
+  // ---- stage s: step n+s on row j-s, from stage s-1's outputs of rows j-s (A) and j-s+1 (B)
+#pragma unroll
+  for (int s = 1; s < K; ++s) {
+    const int r = j - s;
+    RowCoef<T, V> cf;
+    ring_load<T, V>(x.ring, r & (K - 1), x.lane, cf);
+    const T en = yee_row<T, V, ENERGY>(A.x[s - 1], B.x[s - 1], A.y[s - 1], A.h[s - 1], A.h[s], cf, p, x.g[s],
+                                       r == x.src_r, x.src_k, B.h[s], B.x[s], B.y[s]);
+    const bool own = !CHK || (r >= x.r0 && r < x.r1);
+    if (ENERGY && own) eacc[s] += (double)en;
+    if (PROBES && own && x.out) record_probes<T, V>(p, r, (int64_t)0, B.h[s], (x.step + s) % p.cap, x);
+  }
+  // stage K-1's outputs are the fields at step n+K of row j-K+1
+  const int rs = j - (K - 1);
+  if (x.out && (!CHK || (rs >= x.r0 && rs < x.r1))) {
+    const int64_t o = (int64_t)rs * x.P + (x.pex - p.ex0);
+    stv(p.hz1 + o, B.h[K - 1]);
+    stv(p.ex1 + o, B.x[K - 1]);
+    stv(p.ey1 + o, B.y[K - 1]);
+  }
+}
+
+// K1: K time steps per pass (temporal blocking).  At stage-0 row j a warp advances step n on row
+// j, step n+1 on row j-1, ..., step n+K-1 on row j-K+1, entirely in registers, so every field and
+// material byte crosses HBM once per K steps (32/K B per cell-step in fp32).  Lanes 0 and 31 are
+// redundant halo lanes (a 16-byte vector holds V >= K columns, so after K steps only they carry
+// wrong values); lanes 1..30 store.  A row chunk starts K rows early (recomputed, never stored).
+// Stage 0 builds the row's edge coefficients once (row_coef) and parks them in a per-warp
+// shared-memory ring of K rows, where stages 1..K-1 find them.  Interface edges are dead (frozen)
+// in every step; the fix-up kernel repairs the zone around every ROM instance.  The arrays are
+// padded so that every lane loads unconditionally.
+#ifndef FDTD_SWEEP_THREADS
+#define FDTD_SWEEP_THREADS 256
+#endif
+#ifndef FDTD_SWEEP_MINB
+#define FDTD_SWEEP_MINB 1
+#endif
+template <typename T, int K, bool ENERGY>
+__global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_kernel(const SweepParams<T> p) {
   constexpr int V = VT<T>::N;
-  const int lane = threadIdx.x & 31;
+  static_assert(K <= V, "one halo lane covers at most V columns of error spread");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SweepCtx<T, V, K> x;
+  x.lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int wpc = blockDim.x >> 5;
-  const int colv = (blockIdx.x * wpc + warp) * 30 + lane - 1;
-  const bool act = colv >= 0 && colv < p.ncolv;
-  const bool out = act && lane >= 1 && lane <= 30;
+  x.ring = reinterpret_cast<T*>(smem_raw) + (int64_t)warp * K * NCOEF * 32 * V;
+  const int colv = (blockIdx.x * wpc + warp) * 30 + x.lane - 1;
+  x.out = colv >= 0 && colv < p.ncolv && x.lane >= 1 && x.lane <= 30;
   const int64_t c = (int64_t)colv * V;
   const int cy = p.chunk0 + blockIdx.y;  // row chunk
-  const int r0 = p.row0 + cy * p.chunk;
-  const int r1 = min(r0 + p.chunk, p.row0 + p.rows);
-  const int64_t P = p.pitch;
-
-  T g0 = T(0), g1 = T(0);
-  if (p.src_row >= 0) {
-    const int64_t k = *p.step - p.src_t0;
-    if (k >= 0 && k < p.src_n) g0 = (T)p.src_samples[k];
-    if (k + 1 >= 0 && k + 1 < p.src_n) g1 = (T)p.src_samples[k + 1];
-  }
-  auto load_row = [&](const T* a, int row, T (&v)[V], T fill) {
+  x.r0 = p.row0 + cy * p.chunk;
+  x.r1 = min(x.r0 + p.chunk, p.row0 + p.rows);
+  x.P = p.pitch;
+  x.step = *p.step;
+  x.pex = p.ex0 + c; x.pey = p.ey0 + c; x.phz = p.hz0 + c; x.pma = p.mea + c; x.pms = p.msb + c;
+  const bool src_lane = p.src_row >= 0 && p.src_col >= c && p.src_col < c + V;
+  x.src_k = src_lane ? (int)(p.src_col - c) : -1;
+  x.src_r = src_lane ? p.src_row : INT_MIN;
 #pragma unroll
-    for (int k = 0; k < V; ++k) v[k] = fill;
-    if (act && row >= 0) ldv(a + (int64_t)row * P + c, v);
-  };
-
-  T exc[V], h1p[V], ma1[V], ms1[V], ma2[V], ms2[V], e1c[V], y1c[V], h2p[V];
-  // ---- prologue: step n on rows r0-2 (Hz only) and r0-1 (Hz, Ex, Ey)
+  for (int s = 0; s < K; ++s) {
+    x.g[s] = T(0);
+    if (p.src_row >= 0) {
+      const int64_t k = x.step + s - p.src_t0;
+      if (k >= 0 && k < p.src_n) x.g[s] = (T)p.src_samples[k];
+    }
+  }
+  const int jb = x.r0 - K, je = x.r1 + K - 1;  // stage-0 rows [jb, je); jb - 1 >= 0 (ROW0 = 2 KMAX)
+  RowIn<T, V> R0, R1;  // rows jb-1 (only Ex of edge row jb and the materials are used) and jb
   {
-    T hA[V], exA[V], eyA[V], hB[V], exB[V], eyB[V], exC[V];
-    load_row(p.hz0, r0 - 2, hA, T(0));
-    load_row(p.ex0, r0 - 2, exA, T(0));
-    load_row(p.ey0, r0 - 2, eyA, T(0));
-    load_row(p.mea, r0 - 2, ma2, T(-1));
-    load_row(p.msb, r0 - 2, ms2, T(0));
-    load_row(p.hz0, r0 - 1, hB, T(0));
-    load_row(p.ex0, r0 - 1, exB, T(0));
-    load_row(p.ey0, r0 - 1, eyB, T(0));
-    load_row(p.mea, r0 - 1, ma1, T(-1));
-    load_row(p.msb, r0 - 1, ms1, T(0));
-    load_row(p.ex0, r0, exC, T(0));
-    T rA = __shfl_down_sync(FULL, eyA[0], 1);
-    T rB = __shfl_down_sync(FULL, eyB[0], 1);
-    T h1a[V];
+    const int64_t o = (int64_t)(jb - 1) * x.P;
+    ldv(x.pex + o + x.P, R0.ext);
+    ldv(x.pma + o, R0.ma);
+    ldv(x.pms + o, R0.ms);
+    const int64_t o1 = o + x.P;
+    ldv(x.pex + o1 + x.P, R1.ext);
+    ldv(x.pey + o1, R1.ey);
+    ldv(x.phz + o1, R1.hz);
+    ldv(x.pma + o1, R1.ma);
+    ldv(x.pms + o1, R1.ms);
+  }
+  StageOut<T, V, K> O0, O1;
 #pragma unroll
-    for (int k = 0; k < V; ++k) {
-      h1a[k] = hmask(ma2[k], hA[k], hupd(hA[k], exB[k], exA[k], k + 1 < V ? eyA[k + 1] : rA, eyA[k], p.chy, p.chx));
-      h1p[k] = hmask(ma1[k], hB[k], hupd(hB[k], exC[k], exB[k], k + 1 < V ? eyB[k + 1] : rB, eyB[k], p.chy, p.chx));
+  for (int s = 0; s < K; ++s)
+#pragma unroll
+    for (int k = 0; k < V; ++k) O0.h[s][k] = O0.x[s][k] = O0.y[s][k] = T(0);
+  double eacc[K];
+#pragma unroll
+  for (int s = 0; s < K; ++s) eacc[s] = 0.0;
+  // does the chunk hold a probe row?  (one warp scans the per-row table once)
+  __shared__ int chunk_probes;
+  if (threadIdx.x < 32) {
+    bool any = false;
+    if (p.probe_rows)
+      for (int r = x.r0 + x.lane; r < x.r1; r += 32) any |= __ldg(p.probe_rows + r).y > 0;
+    any = __any_sync(FULL, any);
+    if (threadIdx.x == 0) chunk_probes = any;
+  }
+  __syncthreads();
+  // rows [jb, jm): the first stages' rows precede the chunk; [jm, jend): every stage row is the
+  // chunk's own; [jend, je): the last rows.  Boundaries keep even offsets (ping-pong parity).
+  const int jm = min(jb + ((x.r0 + K - 1 - jb + 1) & ~1), je);
+  const int jend = jm + (max(x.r1 - jm, 0) & ~1);
+  int j = jb;
+  for (; j < jm; j += 2) {
+    sweep_row<T, V, K, ENERGY, true, true>(p, x, j, je, R1, R0, O0, O1, eacc);
+    if (j + 1 < je) sweep_row<T, V, K, ENERGY, true, true>(p, x, j + 1, je, R0, R1, O1, O0, eacc);
+  }
+  if (chunk_probes) {
+    for (; j < jend; j += 2) {
+      sweep_row<T, V, K, ENERGY, false, true>(p, x, j, je, R1, R0, O0, O1, eacc);
+      sweep_row<T, V, K, ENERGY, false, true>(p, x, j + 1, je, R0, R1, O1, O0, eacc);
     }
-    if (r0 - 2 == p.src_row) {
-#pragma unroll
-      for (int k = 0; k < V; ++k)
-        if (c + k == p.src_col) h1a[k] += g0;
-    }
-    if (r0 - 1 == p.src_row) {
-#pragma unroll
-      for (int k = 0; k < V; ++k)
-        if (c + k == p.src_col) h1p[k] += g0;
-    }
-    const T hl = __shfl_up_sync(FULL, h1p[V - 1], 1);
-    const T la = __shfl_up_sync(FULL, ma1[V - 1], 1);
-    const T ls = __shfl_up_sync(FULL, ms1[V - 1], 1);
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      bool l;
-      T a;
-      e1c[k] = eupd(exB[k], mul_rn(p.idy, h1p[k] - h1a[k]), ma2[k], ms2[k], ma1[k], ms1[k], l, a);
-      const T left = k ? h1p[k - 1] : hl;
-      y1c[k] = eupd(eyB[k], -mul_rn(p.idx, h1p[k] - left), k ? ma1[k - 1] : la, k ? ms1[k - 1] : ls, ma1[k], ms1[k],
-                    l, a);
-      exc[k] = exC[k];
-      h2p[k] = T(0);
+  } else {
+    for (; j < jend; j += 2) {
+      sweep_row<T, V, K, ENERGY, false, false>(p, x, j, je, R1, R0, O0, O1, eacc);
+      sweep_row<T, V, K, ENERGY, false, false>(p, x, j + 1, je, R0, R1, O1, O0, eacc);
     }
   }
-
-  double eacc0 = 0.0, eacc1 = 0.0;
-  // software pipeline: the loads of row j+1 are in flight while row j computes
-  T nexn[V], neyv[V], nhzv[V], nma[V], nms[V];
-  load_row(p.ex0, r0 + 1, nexn, T(0));
-  load_row(p.ey0, r0, neyv, T(0));
-  load_row(p.hz0, r0, nhzv, T(0));
-  load_row(p.mea, r0, nma, T(-1));
-  load_row(p.msb, r0, nms, T(0));
-  for (int j = r0; j <= r1; ++j) {
-    T exn[V], eyv[V], hzv[V], ma[V], ms[V];
+  for (; j < je; j += 2) {
+    sweep_row<T, V, K, ENERGY, true, true>(p, x, j, je, R1, R0, O0, O1, eacc);
+    if (j + 1 < je) sweep_row<T, V, K, ENERGY, true, true>(p, x, j + 1, je, R0, R1, O1, O0, eacc);
+  }
+  if (!x.out) {
 #pragma unroll
-    for (int k = 0; k < V; ++k) {
-      exn[k] = nexn[k]; eyv[k] = neyv[k]; hzv[k] = nhzv[k]; ma[k] = nma[k]; ms[k] = nms[k];
-    }
-    if (j < r1) {
-      load_row(p.ex0, j + 2, nexn, T(0));
-      load_row(p.ey0, j + 1, neyv, T(0));
-      load_row(p.hz0, j + 1, nhzv, T(0));
-      load_row(p.mea, j + 1, nma, T(-1));
-      load_row(p.msb, j + 1, nms, T(0));
-    }
-    // ---- step n on row j
-    const T eyr = __shfl_down_sync(FULL, eyv[0], 1);
-    T h1[V];
-#pragma unroll
-    for (int k = 0; k < V; ++k)
-      h1[k] = hmask(ma[k], hzv[k], hupd(hzv[k], exn[k], exc[k], k + 1 < V ? eyv[k + 1] : eyr, eyv[k], p.chy, p.chx));
-    if (j == p.src_row) {
-#pragma unroll
-      for (int k = 0; k < V; ++k)
-        if (c + k == p.src_col) h1[k] += g0;
-    }
-    const T hl = __shfl_up_sync(FULL, h1[V - 1], 1);
-    const T la = __shfl_up_sync(FULL, ma[V - 1], 1);
-    const T ls = __shfl_up_sync(FULL, ms[V - 1], 1);
-    T e1[V], y1[V];
-    T en = T(0);
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      bool lx, ly;
-      T ax, ay;
-      e1[k] = eupd(exc[k], mul_rn(p.idy, h1[k] - h1p[k]), ma1[k], ms1[k], ma[k], ms[k], lx, ax);
-      const T left = k ? h1[k - 1] : hl;
-      y1[k] = eupd(eyv[k], -mul_rn(p.idx, h1[k] - left), k ? ma[k - 1] : la, k ? ms[k - 1] : ls, ma[k], ms[k], ly, ay);
-      if (ENERGY) {
-        en += p.wxy * ((lx ? ax * exc[k] * exc[k] : T(0)) + (ly ? ay * eyv[k] * eyv[k] : T(0)));
-        en += p.wh * hzv[k] * h1[k];
-      }
-    }
-    if (ENERGY && out && j < r1) eacc0 += (double)en;
-    // ---- step n+1 on row j-1
-    const T y1r = __shfl_down_sync(FULL, y1c[0], 1);
-    T h2[V];
-#pragma unroll
-    for (int k = 0; k < V; ++k)
-      h2[k] = hmask(ma1[k], h1p[k], hupd(h1p[k], e1[k], e1c[k], k + 1 < V ? y1c[k + 1] : y1r, y1c[k], p.chy, p.chx));
-    if (j - 1 == p.src_row) {
-#pragma unroll
-      for (int k = 0; k < V; ++k)
-        if (c + k == p.src_col) h2[k] += g1;
-    }
-    const T hl2 = __shfl_up_sync(FULL, h2[V - 1], 1);
-    const T la1 = __shfl_up_sync(FULL, ma1[V - 1], 1);
-    const T ls1 = __shfl_up_sync(FULL, ms1[V - 1], 1);
-    T e2[V], y2[V];
-    T en1 = T(0);
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      bool lx, ly;
-      T ax, ay;
-      e2[k] = eupd(e1c[k], mul_rn(p.idy, h2[k] - h2p[k]), ma2[k], ms2[k], ma1[k], ms1[k], lx, ax);
-      const T left = k ? h2[k - 1] : hl2;
-      y2[k] = eupd(y1c[k], -mul_rn(p.idx, h2[k] - left), k ? ma1[k - 1] : la1, k ? ms1[k - 1] : ls1, ma1[k], ms1[k],
-                   ly, ay);
-      if (ENERGY) {
-        en1 += p.wxy * ((lx ? ax * e1c[k] * e1c[k] : T(0)) + (ly ? ay * y1c[k] * y1c[k] : T(0)));
-        en1 += p.wh * h1p[k] * h2[k];
-      }
-    }
-    if (out && j > r0) {
-      const int64_t rs = (int64_t)(j - 1) * P + c;
-      stv(p.hz1 + rs, h2);
-      stv(p.ex1 + rs, e2);
-      stv(p.ey1 + rs, y2);
-      if (ENERGY) eacc1 += (double)en1;
-    }
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      ma2[k] = ma1[k]; ms2[k] = ms1[k];
-      ma1[k] = ma[k]; ms1[k] = ms[k];
-      exc[k] = exn[k];
-      h2p[k] = h2[k];
-      h1p[k] = h1[k];
-      e1c[k] = e1[k];
-      y1c[k] = y1[k];
-    }
+    for (int s = 0; s < K; ++s) eacc[s] = 0.0;
   }
   if (ENERGY) {
-    __shared__ double red0[32], red1[32];
+    __shared__ double red[K][32];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      eacc0 += __shfl_down_sync(FULL, eacc0, o);
-      eacc1 += __shfl_down_sync(FULL, eacc1, o);
+    for (int s = 0; s < K; ++s) {
+      double v = eacc[s];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FULL, v, o);
+      if (x.lane == 0) red[s][warp] = v;
     }
-    if (lane == 0) { red0[warp] = eacc0; red1[warp] = eacc1; }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double s0 = 0.0, s1 = 0.0;
-      for (int w = 0; w < wpc; ++w) { s0 += red0[w]; s1 += red1[w]; }
-      const int64_t b = (int64_t)cy * gridDim.x + blockIdx.x;
-      p.partials[b] = s0;
-      p.partials2[b] = s1;
+    if (threadIdx.x < K) {
+      double t = 0.0;
+      for (int w = 0; w < wpc; ++w) t += red[threadIdx.x][w];
+      p.partials[threadIdx.x * p.pstride + (int64_t)cy * gridDim.x + blockIdx.x] = t;
     }
   }
 }
@@ -587,357 +559,221 @@ __device__ void store_rom(const PostParams<T>& p, const RomModelDev& m, int firs
   }
 }
 
-// One-step post kernel body for one batch: gather, ROM step, scatter.
-template <typename T, bool ENERGY>
-__device__ void rom_batch(const PostParams<T>& p, int bi, T* sv) {
-  const int model = p.batch_tab[3 * bi], first = p.batch_tab[3 * bi + 1], nb = p.batch_tab[3 * bi + 2];
-  const RomModelDev m = p.models[model];
-  const int B = p.batch;
-  const int64_t S = (int64_t)p.nthreads_vec * B;
-  for (int64_t k = threadIdx.x; k < 7 * S; k += blockDim.x) sv[k] = T(0);
-  __syncthreads();
-  T* sy = sv + S;
-  T* sh = sv + 2 * S;
-  // S4: gather y^n (interface edges, copied old->new by the sweep), h = Hz^{n+1/2} outside, state
-  for (int it = threadIdx.x; it < m.nY * nb; it += blockDim.x) {
-    const int i = it % m.nY, b = it / m.nY;
-    const int64_t po = p.port_off[first + b];
-    const int64_t e = p.port_edge[po + i];
-    sy[i * B + b] = (e >> 62) ? p.ey1[e & IDX_MASK] : p.ex1[e & IDX_MASK];
-    sh[i * B + b] = p.hz1[p.port_h[po + i]];
-  }
-  load_rom_state(p, m, first, nb, sv);
-  __syncthreads();
-  rom_step<T, ENERGY>(p, m, first, nb, sv, p.rom_partials + first);
-  store_rom(p, m, first, nb, sv, p.ex1, p.ey1);
-}
-
-// Two-step fix-up for one batch (K3b).  sweep2 advanced every cell two steps with the
-// interface edges frozen at y^n; here, per instance, step n is recomputed in the region
-// [i0-2, i0+bx+2) x [j0-2, j0+by+2) from the input buffer (bit-identical to the sweep's own
-// arithmetic), the ROM takes step n (y^{n+1}), the outside cells' Hz^{n+3/2} and their
-// non-interface edges' E^{n+2} are recomputed with the correct y^{n+1}, the ROM takes step n+1
-// (y^{n+2}), and the corrected values are written over the sweep's output.  The energy of
-// step n+1 is corrected by mu A/dt H^{n+1/2} (H_correct - H_sweep) on the outside cells.
-template <typename T, bool ENERGY>
-__device__ void rom_batch2(const PostParams<T>& p, int bi, T* sv, T g0, T g1, double* sdelta) {
+// K3: the K-step fix-up of one batch (instances of one model).  The sweep advanced every cell K
+// steps with the interface edges frozen at y^n; here, per instance, the K steps are recomputed
+// on the region [i0-M, i0+bx+M) x [j0-M, j0+by+M), M = Kz + K - 1, from the pass's input buffer
+// with the sweep's own arithmetic (yee_row's device functions), and between the H and E half
+// steps the ROM takes its step (S4 gather, S5 eq:connExplicit, S6 scatter).  Values in the
+// region go wrong from its border inwards by one cell per step, so after K steps every cell
+// within Kz of the block is exact.  Written back: the zone cells (block + Kz - 1 rings, + one
+// more column / row on the right / top, holes excluded) with their bottom Ex and left Ey edges;
+// y^{n+K}; the ROM state.  Their energy (which the sweep skipped) and the zone probes are
+// recorded here for every step of the pass.
+template <typename T, int K, bool ENERGY>
+__device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[K], int64_t step, double* zsum) {
   const int model = p.batch_tab[3 * bi], first = p.batch_tab[3 * bi + 1], nb = p.batch_tab[3 * bi + 2];
   const RomModelDev m = p.models[model];
   const int B = p.batch, nY = m.nY;
   const int64_t S = (int64_t)p.nthreads_vec * B;
   const int tid = threadIdx.x, nt = blockDim.x;
   T* reg = rom_end(p, sv);
+  const int Kz = p.Kz, M = Kz + K - 1;
   const int64_t P = p.pitch;
   for (int64_t k = tid; k < 7 * S; k += nt) sv[k] = T(0);
-  if (tid < B) sdelta[tid] = 0.0;  // B <= 64
   T* sy = sv + S;
   T* sh = sv + 2 * S;
-  // region geometry of slot b
-  auto geo = [&](int b, int& i0, int& j0, int& bx, int& by) {
+  struct Geo {
+    int i0, j0, bx, by, Wr, Hr, zu0, zu1, zv0, zv1;
+    T *H, *MA, *MS, *ZE, *EX, *EY;
+  };
+  auto geo = [&](int b) {
+    Geo q;
     const int32_t* r = p.rects + 4 * (int64_t)(first + b);
-    i0 = r[0]; j0 = r[1]; bx = r[2]; by = r[3];
-  };
-  // layout of one region: H1, H2, MA, MS [Hr][Wr]; EX [Hr+1][Wr]; EY [Hr][Wr+1]
-  auto arrays = [&](int b, int bx, int by, T*& H1, T*& H2, T*& MA, T*& MS, T*& EX, T*& EY) {
-    const int Wr = bx + 4, Hr = by + 4;
-    H1 = reg + (int64_t)b * p.region_stride;
-    H2 = H1 + Hr * Wr;
-    MA = H2 + Hr * Wr;
-    MS = MA + Hr * Wr;
-    EX = MS + Hr * Wr;
-    EY = EX + (Hr + 1) * Wr;
-  };
-  auto goff = [&](int gi, int gj) { return ((int64_t)gj - p.row_begin + p.row0) * P + gi; };
-  const bool src_on = p.src_row >= 0;
-  const int64_t src_off = src_on ? (int64_t)p.src_row * P + p.src_col : -1;
-  // ---- R1: load the region (materials, E^n, the sweep's Hz^{n+3/2} into H2)
-  for (int b = 0; b < nb; ++b) {
-    int i0, j0, bx, by;
-    geo(b, i0, j0, bx, by);
-    T *H1, *H2, *MA, *MS, *EX, *EY;
-    arrays(b, bx, by, H1, H2, MA, MS, EX, EY);
-    const int Wr = bx + 4, Hr = by + 4;
-    for (int t = tid; t < Hr * Wr; t += nt) {
-      const int u = t % Wr, v = t / Wr;
-      const int64_t o = goff(i0 - 2 + u, j0 - 2 + v);
-      MA[t] = p.mea[o];
-      MS[t] = p.msb[o];
-      H2[t] = p.hz1[o];
+    q.i0 = r[0]; q.j0 = r[1]; q.bx = r[2]; q.by = r[3];
+    q.Wr = q.bx + 2 * M; q.Hr = q.by + 2 * M;
+    if (Kz >= 2) {  // zone rectangle in region coordinates
+      q.zu0 = M - (Kz - 1); q.zu1 = M + q.bx + Kz; q.zv0 = M - (Kz - 1); q.zv1 = M + q.by + Kz;
+    } else {
+      q.zu0 = q.zu1 = q.zv0 = q.zv1 = 0;
     }
-    for (int t = tid; t < (Hr + 1) * Wr; t += nt) EX[t] = p.ex0[goff(i0 - 2 + t % Wr, j0 - 2 + t / Wr)];
-    for (int t = tid; t < Hr * (Wr + 1); t += nt) EY[t] = p.ey0[goff(i0 - 2 + t % (Wr + 1), j0 - 2 + t / (Wr + 1))];
+    const int n = q.Hr * q.Wr;
+    q.H = reg + (int64_t)b * p.region_stride;
+    q.MA = q.H + n; q.MS = q.MA + n; q.ZE = q.MS + n; q.EX = q.ZE + n; q.EY = q.EX + n + q.Wr;
+    return q;
+  };
+  auto goff = [&](const Geo& q, int u, int v) {
+    return ((int64_t)q.j0 - M + v - p.row_begin + p.row0) * P + q.i0 - M + u;
+  };
+  const int64_t src_off = p.src_row >= 0 ? (int64_t)p.src_row * P + p.src_col : -1;
+  // ---- load the region: materials and the fields at step n
+  for (int b = 0; b < nb; ++b) {
+    const Geo q = geo(b);
+    for (int t = tid; t < q.Hr * q.Wr; t += nt) {
+      const int64_t o = goff(q, t % q.Wr, t / q.Wr);
+      q.MA[t] = p.mea[o];
+      q.MS[t] = p.msb[o];
+      q.H[t] = p.hz0[o];
+    }
+    for (int t = tid; t < (q.Hr + 1) * q.Wr; t += nt) q.EX[t] = p.ex0[goff(q, t % q.Wr, t / q.Wr)];
+    for (int t = tid; t < q.Hr * (q.Wr + 1); t += nt) q.EY[t] = p.ey0[goff(q, t % (q.Wr + 1), t / (q.Wr + 1))];
   }
   load_rom_state(p, m, first, nb, sv);
   __syncthreads();
-  // ---- R2: Hz^{n+1/2} on the region (same arithmetic as the sweep)
-  for (int b = 0; b < nb; ++b) {
-    int i0, j0, bx, by;
-    geo(b, i0, j0, bx, by);
-    T *H1, *H2, *MA, *MS, *EX, *EY;
-    arrays(b, bx, by, H1, H2, MA, MS, EX, EY);
-    const int Wr = bx + 4, Hr = by + 4;
-    for (int t = tid; t < Hr * Wr; t += nt) {
-      const int u = t % Wr, v = t / Wr;
-      const int64_t o = goff(i0 - 2 + u, j0 - 2 + v);
-      const T hz = p.hz0[o];
-      T h = hmask(MA[t], hz, hupd(hz, EX[(v + 1) * Wr + u], EX[v * Wr + u], EY[v * (Wr + 1) + u + 1],
-                                  EY[v * (Wr + 1) + u], p.chy, p.chx));
-      if (o == src_off) h += g0;
-      H1[t] = h;
-    }
-  }
-  __syncthreads();
-  // ---- R3: E^{n+1} on the region's interior edges (in place); gather y^n and h^{n+1/2}
-  for (int b = 0; b < nb; ++b) {
-    int i0, j0, bx, by;
-    geo(b, i0, j0, bx, by);
-    T *H1, *H2, *MA, *MS, *EX, *EY;
-    arrays(b, bx, by, H1, H2, MA, MS, EX, EY);
-    const int Wr = bx + 4, Hr = by + 4;
-    bool l;
-    T a;
-    for (int t = tid; t < (Hr - 1) * Wr; t += nt) {  // Ex edge rows v = 1 .. Hr-1
-      const int u = t % Wr, v = t / Wr + 1;
-      const int cb = v * Wr + u, ca = cb - Wr;
-      EX[v * Wr + u] = eupd(EX[v * Wr + u], mul_rn(p.idy, H1[cb] - H1[ca]), MA[ca], MS[ca], MA[cb], MS[cb], l, a);
-    }
-    for (int t = tid; t < Hr * (Wr - 1); t += nt) {  // Ey edge columns u = 1 .. Wr-1
-      const int u = t % (Wr - 1) + 1, v = t / (Wr - 1);
-      const int cb = v * Wr + u, ca = cb - 1;
-      EY[v * (Wr + 1) + u] =
-          eupd(EY[v * (Wr + 1) + u], -mul_rn(p.idx, H1[cb] - H1[ca]), MA[ca], MS[ca], MA[cb], MS[cb], l, a);
-    }
-    for (int i = tid; i < nY; i += nt) {
-      int eidx, hidx;  // interface edge (EX or EY index) and outside cell, region coordinates
-      bool isy;
-      if (i < bx) { isy = false; eidx = 2 * Wr + 2 + i; hidx = 1 * Wr + 2 + i; }
-      else if (i < 2 * bx) { isy = false; eidx = (2 + by) * Wr + 2 + (i - bx); hidx = (2 + by) * Wr + 2 + (i - bx); }
-      else if (i < 2 * bx + by) { isy = true; eidx = (2 + i - 2 * bx) * (Wr + 1) + 2; hidx = (2 + i - 2 * bx) * Wr + 1; }
-      else { isy = true; eidx = (2 + i - 2 * bx - by) * (Wr + 1) + 2 + bx; hidx = (2 + i - 2 * bx - by) * Wr + 2 + bx; }
-      sy[i * B + b] = isy ? EY[eidx] : EX[eidx];  // y^n (interface edges are frozen copies)
-      sh[i * B + b] = H1[hidx];
-    }
-  }
-  __syncthreads();
-  // ---- ROM step n: y^{n+1}, x~^{n+1}; ROM energy of W^n
-  rom_step<T, ENERGY>(p, m, first, nb, sv, p.rom_partials + first);
-  // ---- R4: y^{n+1} into the interface edges; Hz^{n+3/2} of the outside cells
-  for (int b = 0; b < nb; ++b) {
-    int i0, j0, bx, by;
-    geo(b, i0, j0, bx, by);
-    T *H1, *H2, *MA, *MS, *EX, *EY;
-    arrays(b, bx, by, H1, H2, MA, MS, EX, EY);
-    const int Wr = bx + 4;
-    for (int i = tid; i < nY; i += nt) {
-      if (i < bx) EX[2 * Wr + 2 + i] = sy[i * B + b];
-      else if (i < 2 * bx) EX[(2 + by) * Wr + 2 + (i - bx)] = sy[i * B + b];
-      else if (i < 2 * bx + by) EY[(2 + i - 2 * bx) * (Wr + 1) + 2] = sy[i * B + b];
-      else EY[(2 + i - 2 * bx - by) * (Wr + 1) + 2 + bx] = sy[i * B + b];
-    }
-  }
-  __syncthreads();
-  auto port_cell = [&](int i, int bx, int by, int& u, int& v) {  // outside cell of port i
-    if (i < bx) { u = 2 + i; v = 1; }
-    else if (i < 2 * bx) { u = 2 + i - bx; v = 2 + by; }
-    else if (i < 2 * bx + by) { u = 1; v = 2 + i - 2 * bx; }
-    else { u = 2 + bx; v = 2 + i - 2 * bx - by; }
-  };
-  for (int b = 0; b < nb; ++b) {  // corrected Hz^{n+3/2} of the outside cells -> sh
-    int i0, j0, bx, by;
-    geo(b, i0, j0, bx, by);
-    T *H1, *H2, *MA, *MS, *EX, *EY;
-    arrays(b, bx, by, H1, H2, MA, MS, EX, EY);
-    const int Wr = bx + 4;
-    for (int i = tid; i < nY; i += nt) {
-      int u, v;
-      port_cell(i, bx, by, u, v);
-      const int t = v * Wr + u;
-      T h = hmask(MA[t], H1[t], hupd(H1[t], EX[(v + 1) * Wr + u], EX[v * Wr + u], EY[v * (Wr + 1) + u + 1],
-                                     EY[v * (Wr + 1) + u], p.chy, p.chx));
-      if (goff(i0 - 2 + u, j0 - 2 + v) == src_off) h += g1;
-      sh[i * B + b] = h;
-    }
-  }
-  __syncthreads();
-  {  // energy correction of W^{n+1} (fixed order: one warp per instance), then H2 <- corrected
-    const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
-    for (int b = w; b < nb; b += nw) {
-      int i0, j0, bx, by;
-      geo(b, i0, j0, bx, by);
-      T *H1, *H2, *MA, *MS, *EX, *EY;
-      arrays(b, bx, by, H1, H2, MA, MS, EX, EY);
-      double d = 0.0;
-      for (int i = lane; i < nY; i += 32) {
-        int u, v;
-        port_cell(i, bx, by, u, v);
-        const int t = v * (bx + 4) + u;
-        d += (double)(p.wh * H1[t] * sh[i * B + b]) - (double)(p.wh * H1[t] * H2[t]);
+#pragma unroll 1
+  for (int s = 0; s < K; ++s) {
+    // ---- H half-step (+ source, + zone-cell energy of W^{n+s})
+    for (int b = 0; b < nb; ++b) {
+      const Geo q = geo(b);
+      const int W1 = q.Wr + 1;
+      for (int t = tid; t < q.Hr * q.Wr; t += nt) {
+        const int u = t % q.Wr, v = t / q.Wr;
+        const T h0 = q.H[t];
+        const T hu = hupd(h0, q.EX[t + q.Wr], q.EX[t], q.EY[v * W1 + u + 1], q.EY[v * W1 + u], p.chy, p.chx);
+        T h = q.MA[t] < T(0) ? h0 : hu;  // dead cells keep their Hz (as in yee_row)
+        if (goff(q, u, v) == src_off) h += g[s];
+        if (ENERGY && u >= q.zu0 && u < q.zu1 && v >= q.zv0 && v < q.zv1) {
+          // the zone cell's full storage-function term (row_coef's weights without the zone mask)
+          bool lx, ly;
+          T ax, ay, ca, cb;
+          edge_coef(q.MA[t - q.Wr], q.MS[t - q.Wr], q.MA[t], q.MS[t], p.idy, ca, cb, ax, lx);
+          edge_coef(q.MA[t - 1], q.MS[t - 1], q.MA[t], q.MS[t], -p.idx, ca, cb, ay, ly);
+          const T wx = lx ? mul_rn(p.wxy, ax) : T(0), wy = ly ? mul_rn(p.wxy, ay) : T(0);
+          const T hw = q.MA[t] < T(0) ? T(0) : p.wh;
+          q.ZE[(v - q.zv0) * (q.zu1 - q.zu0) + u - q.zu0] = cell_energy(T(0), q.EX[t], q.EY[v * W1 + u], h0, h, wx, wy, hw);
+        }
+        q.H[t] = h;
       }
+    }
+    __syncthreads();
+    // ---- zone probes; S4 gather of y^{n+s} (interface edges) and h = Hz^{n+s+1/2} (outside cells)
+    for (int b = 0; b < nb; ++b) {
+      const Geo q = geo(b);
+      const int z0 = p.zp_off[first + b], z1 = p.zp_off[first + b + 1];
+      for (int z = z0 + tid; z < z1; z += nt) {
+        const int u = p.zp[3 * z] - (q.i0 - M), v = p.zp[3 * z + 1] - (q.j0 - M);
+        p.probe_ring[(int64_t)p.zp[3 * z + 2] * p.cap + (step + s) % p.cap] = q.H[v * q.Wr + u];
+      }
+      const int W1 = q.Wr + 1;
+      for (int i = tid; i < nY; i += nt) {
+        T y, h;
+        if (i < q.bx) {  // S side: Ex edge row M, outside cell row M-1
+          y = q.EX[M * q.Wr + M + i]; h = q.H[(M - 1) * q.Wr + M + i];
+        } else if (i < 2 * q.bx) {  // N side: Ex edge row M+by, outside cell row M+by
+          y = q.EX[(M + q.by) * q.Wr + M + i - q.bx]; h = q.H[(M + q.by) * q.Wr + M + i - q.bx];
+        } else if (i < 2 * q.bx + q.by) {  // W side: Ey edge column M, outside cell column M-1
+          const int v = M + i - 2 * q.bx;
+          y = q.EY[v * W1 + M]; h = q.H[v * q.Wr + M - 1];
+        } else {  // E side: Ey edge column M+bx, outside cell column M+bx
+          const int v = M + i - 2 * q.bx - q.by;
+          y = q.EY[v * W1 + M + q.bx]; h = q.H[v * q.Wr + M + q.bx];
+        }
+        sy[i * B + b] = y;
+        sh[i * B + b] = h;
+      }
+    }
+    if (ENERGY) {  // zone energy per instance, fixed order (one warp per instance)
+      const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+      for (int b = w; b < nb; b += nw) {
+        const Geo q = geo(b);
+        const int nz = (q.zu1 - q.zu0) * (q.zv1 - q.zv0);
+        double acc = 0.0;
+        for (int i = lane; i < nz; i += 32) acc += (double)q.ZE[i];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) d += __shfl_down_sync(FULL, d, o);
-      if (lane == 0) sdelta[b] = d;
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
+        if (lane == 0) zsum[b] = acc;
+      }
     }
+    __syncthreads();
+    // ---- S5: ROM step n+s -> y^{n+s+1}, x~^{n+s+1}; ROM energy of W^{n+s}
+    double* eout = p.rom_partials + (int64_t)s * p.n_inst + first;
+    rom_step<T, ENERGY>(p, m, first, nb, sv, eout);
+    if (ENERGY && tid < nb) eout[tid] += zsum[tid];
+    // ---- E half-step on the region's interior edges (frozen edges keep their value)
+    for (int b = 0; b < nb; ++b) {
+      const Geo q = geo(b);
+      const int W1 = q.Wr + 1;
+      for (int t = q.Wr + tid; t < q.Hr * q.Wr; t += nt) {  // Ex edge rows 1 .. Hr-1
+        bool l;
+        T a, ca, cb;
+        edge_coef(q.MA[t - q.Wr], q.MS[t - q.Wr], q.MA[t], q.MS[t], p.idy, ca, cb, a, l);
+        q.EX[t] = eupd(q.EX[t], ca, cb, q.H[t] - q.H[t - q.Wr]);
+      }
+      for (int t = tid; t < q.Hr * (q.Wr - 1); t += nt) {  // Ey edge columns 1 .. Wr-1
+        const int u = t % (q.Wr - 1) + 1, v = t / (q.Wr - 1);
+        const int c = v * q.Wr + u;
+        bool l;
+        T a, ca, cb;
+        edge_coef(q.MA[c - 1], q.MS[c - 1], q.MA[c], q.MS[c], -p.idx, ca, cb, a, l);
+        q.EY[v * W1 + u] = eupd(q.EY[v * W1 + u], ca, cb, q.H[c] - q.H[c - 1]);
+      }
+    }
+    __syncthreads();
+    // ---- S6: y^{n+s+1} into the region's interface edges
+    for (int b = 0; b < nb; ++b) {
+      const Geo q = geo(b);
+      const int W1 = q.Wr + 1;
+      for (int i = tid; i < nY; i += nt) {
+        const T y = sy[i * B + b];
+        if (i < q.bx) q.EX[M * q.Wr + M + i] = y;
+        else if (i < 2 * q.bx) q.EX[(M + q.by) * q.Wr + M + i - q.bx] = y;
+        else if (i < 2 * q.bx + q.by) q.EY[(M + i - 2 * q.bx) * W1 + M] = y;
+        else q.EY[(M + i - 2 * q.bx - q.by) * W1 + M + q.bx] = y;
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
+  // ---- write back the zone: Hz of the live zone cells, their bottom Ex and left Ey edges
   for (int b = 0; b < nb; ++b) {
-    int i0, j0, bx, by;
-    geo(b, i0, j0, bx, by);
-    T *H1, *H2, *MA, *MS, *EX, *EY;
-    arrays(b, bx, by, H1, H2, MA, MS, EX, EY);
-    for (int i = tid; i < nY; i += nt) {
-      int u, v;
-      port_cell(i, bx, by, u, v);
-      H2[v * (bx + 4) + u] = sh[i * B + b];
-    }
-  }
-  __syncthreads();
-  // ---- ROM step n+1: y^{n+2}, x~^{n+2}; ROM energy of W^{n+1}
-  rom_step<T, ENERGY>(p, m, first, nb, sv, p.rom_partials2 + first);
-  // ---- R5: E^{n+2} of the outside cells' non-interface edges, the outside cells' Hz, y^{n+2}
-  for (int b = 0; b < nb; ++b) {
-    int i0, j0, bx, by;
-    geo(b, i0, j0, bx, by);
-    T *H1, *H2, *MA, *MS, *EX, *EY;
-    arrays(b, bx, by, H1, H2, MA, MS, EX, EY);
-    const int Wr = bx + 4, Hr = by + 4;
-    auto hole = [&](int u, int v) { return u >= 2 && u < 2 + bx && v >= 2 && v < 2 + by; };
-    auto outside = [&](int u, int v) {
-      return ((v == 1 || v == 2 + by) && u >= 2 && u < 2 + bx) || ((u == 1 || u == 2 + bx) && v >= 2 && v < 2 + by);
-    };
-    bool l;
-    T a;
-    for (int t = tid; t < (Hr - 1) * Wr; t += nt) {
-      const int u = t % Wr, v = t / Wr + 1;
-      if (!(outside(u, v - 1) || outside(u, v)) || hole(u, v - 1) || hole(u, v)) continue;
-      const int cb = v * Wr + u, ca = cb - Wr;
-      p.ex1[goff(i0 - 2 + u, j0 - 2 + v)] =
-          eupd(EX[v * Wr + u], mul_rn(p.idy, H2[cb] - H2[ca]), MA[ca], MS[ca], MA[cb], MS[cb], l, a);
-    }
-    for (int t = tid; t < Hr * (Wr - 1); t += nt) {
-      const int u = t % (Wr - 1) + 1, v = t / (Wr - 1);
-      if (!(outside(u - 1, v) || outside(u, v)) || hole(u - 1, v) || hole(u, v)) continue;
-      const int cb = v * Wr + u, ca = cb - 1;
-      p.ey1[goff(i0 - 2 + u, j0 - 2 + v)] =
-          eupd(EY[v * (Wr + 1) + u], -mul_rn(p.idx, H2[cb] - H2[ca]), MA[ca], MS[ca], MA[cb], MS[cb], l, a);
-    }
-    for (int i = tid; i < nY; i += nt) {
-      int u, v;
-      port_cell(i, bx, by, u, v);
-      p.hz1[goff(i0 - 2 + u, j0 - 2 + v)] = H2[v * Wr + u];
+    const Geo q = geo(b);
+    const int zw = q.zu1 - q.zu0, nz = zw * (q.zv1 - q.zv0);
+    for (int i = tid; i < nz; i += nt) {
+      const int u = q.zu0 + i % zw, v = q.zv0 + i / zw;
+      const int t = v * q.Wr + u;
+      if (!(q.MA[t] >= T(0))) continue;
+      const int64_t o = goff(q, u, v);
+      p.hz1[o] = q.H[t];
+      p.ex1[o] = q.EX[t];
+      p.ey1[o] = q.EY[v * (q.Wr + 1) + u];
     }
   }
   store_rom(p, m, first, nb, sv, p.ex1, p.ey1);
-  __syncthreads();
-  if (ENERGY && tid < nb) p.rom_partials2[first + tid] += sdelta[tid];
 }
 
-template <typename T, bool ENERGY>
-__global__ void __launch_bounds__(256) post2_kernel(const PostParams<T> p) {
+template <typename T, int K, bool ENERGY>
+__global__ void __launch_bounds__(256) postk_kernel(const PostParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[32];
-  __shared__ double sdelta[64];
+  __shared__ double zsum[64];
   __shared__ bool last;
   T* sv = reinterpret_cast<T*>(smem_raw);
   const int b = blockIdx.x;
   const int64_t step = *p.step;
-  T g0 = T(0), g1 = T(0);
-  if (p.src_row >= 0) {
-    const int64_t k = step - p.src_t0;
-    if (k >= 0 && k < p.src_n) g0 = (T)p.src_samples[k];
-    if (k + 1 >= 0 && k + 1 < p.src_n) g1 = (T)p.src_samples[k + 1];
-  }
-  if (b < p.n_batch) {
-    rom_batch2<T, ENERGY>(p, b, sv, g0, g1, sdelta);
-  } else {  // probes: Hz^{n+1/2} recomputed from the input buffer, Hz^{n+3/2} from the output
-    const int64_t P = p.pitch;
-    const int64_t src_off = p.src_row >= 0 ? (int64_t)p.src_row * P + p.src_col : -1;
-    for (int k = threadIdx.x; k < p.n_probe; k += blockDim.x) {
-      const int64_t o = p.probe_idx[k];
-      const T hz = p.hz0[o];
-      T h = hmask(p.mea[o], hz, hupd(hz, p.ex0[o + P], p.ex0[o], p.ey0[o + 1], p.ey0[o], p.chy, p.chx));
-      if (o == src_off) h += g0;
-      p.probe_ring[(int64_t)k * p.cap + step % p.cap] = h;
-      p.probe_ring[(int64_t)k * p.cap + (step + 1) % p.cap] = p.hz1[o];
+  T g[K];
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    g[s] = T(0);
+    if (p.src_row >= 0) {
+      const int64_t k = step + s - p.src_t0;
+      if (k >= 0 && k < p.src_n) g[s] = (T)p.src_samples[k];
     }
   }
-  if (ENERGY) {
-    const int per = (p.n_sweep_partials + gridDim.x - 1) / gridDim.x;
-    const int k0 = b * per, k1 = min(p.n_sweep_partials, k0 + per);
-    double v0 = 0.0, v1 = 0.0;
-    for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-      v0 += __ldcg(p.sweep_partials + k);
-      v1 += __ldcg(p.sweep_partials2 + k);
-    }
-    __syncthreads();
-    if (b < p.n_batch) {
-      const int first = p.batch_tab[3 * b + 1], nb = p.batch_tab[3 * b + 2];
-      for (int k = threadIdx.x; k < nb; k += blockDim.x) {
-        v0 += p.rom_partials[first + k];
-        v1 += p.rom_partials2[first + k];
-      }
-    }
-    const double t0 = block_sum(v0, red);
-    const double t1 = block_sum(v1, red);
-    if (threadIdx.x == 0) {
-      p.level1[b] = t0;
-      p.level1b[b] = t1;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned t = atomicAdd(p.done, 1u);
-    last = (t == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  if (ENERGY) {
-    double s0 = 0.0, s1 = 0.0;
-    for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) {
-      s0 += __ldcg(p.level1 + k);
-      s1 += __ldcg(p.level1b + k);
-    }
-    const double t0 = block_sum(s0, red);
-    const double t1 = block_sum(s1, red);
-    if (threadIdx.x == 0) {
-      p.energy_ring[step % p.cap] = t0;
-      p.energy_ring[(step + 1) % p.cap] = t1;
-    }
-  }
-  if (threadIdx.x == 0) {
-    *p.done = 0u;
-    *p.step = step + 2;
-  }
-}
-
-template <typename T, bool ENERGY>
-__global__ void __launch_bounds__(256) post_kernel(const PostParams<T> p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ double red[32];
-  __shared__ bool last;
-  T* sv = reinterpret_cast<T*>(smem_raw);
-  const int b = blockIdx.x;
-  const int64_t step = *p.step;
-  if (b < p.n_batch) {
-    rom_batch<T, ENERGY>(p, b, sv);
-  } else {
-    for (int k = threadIdx.x; k < p.n_probe; k += blockDim.x)
-      p.probe_ring[(int64_t)k * p.cap + step % p.cap] = p.hz1[p.probe_idx[k]];
-  }
+  if (b < p.n_batch) fixup_batch<T, K, ENERGY>(p, b, sv, g, step, zsum);
   if (ENERGY) {
     // level 1 (every CTA, fixed slice): sweep partials [b*per, (b+1)*per) + this batch's ROM energies
-    const int per = (p.n_sweep_partials + gridDim.x - 1) / gridDim.x;
-    const int k0 = b * per, k1 = min(p.n_sweep_partials, k0 + per);
-    double v = 0.0;
-    for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) v += __ldcg(p.sweep_partials + k);
-    __syncthreads();  // rom_partials of this batch written (rom_batch ends with barriers)
-    if (b < p.n_batch) {
-      const int first = p.batch_tab[3 * b + 1], nb = p.batch_tab[3 * b + 2];
-      for (int k = threadIdx.x; k < nb; k += blockDim.x) v += p.rom_partials[first + k];
+    const int64_t per = (p.n_sweep_partials + gridDim.x - 1) / gridDim.x;
+    const int64_t k0 = b * per, k1 = min(p.n_sweep_partials, k0 + per);
+    __syncthreads();  // rom_partials of this batch written (fixup_batch ends with barriers)
+#pragma unroll 1
+    for (int s = 0; s < K; ++s) {
+      double v = 0.0;
+      for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) v += __ldcg(p.sweep_partials + s * p.pstride + k);
+      if (b < p.n_batch) {
+        const int first = p.batch_tab[3 * b + 1], nb = p.batch_tab[3 * b + 2];
+        for (int k = threadIdx.x; k < nb; k += blockDim.x) v += p.rom_partials[(int64_t)s * p.n_inst + first + k];
+      }
+      const double tot = block_sum(v, red);
+      if (threadIdx.x == 0) p.level1[(int64_t)s * gridDim.x + b] = tot;
     }
-    const double tot = block_sum(v, red);
-    if (threadIdx.x == 0) p.level1[b] = tot;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -949,14 +785,17 @@ __global__ void __launch_bounds__(256) post_kernel(const PostParams<T> p) {
   if (!last) return;
   __threadfence();
   if (ENERGY) {  // level 2: fixed-order sum of the per-CTA values (deterministic)
-    double s = 0.0;
-    for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) s += __ldcg(p.level1 + k);
-    const double tot = block_sum(s, red);
-    if (threadIdx.x == 0) p.energy_ring[step % p.cap] = tot;
+#pragma unroll 1
+    for (int s = 0; s < K; ++s) {
+      double v = 0.0;
+      for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) v += __ldcg(p.level1 + (int64_t)s * gridDim.x + k);
+      const double tot = block_sum(v, red);
+      if (threadIdx.x == 0) p.energy_ring[(step + s) % p.cap] = tot;
+    }
   }
   if (threadIdx.x == 0) {
     *p.done = 0u;
-    *p.step = step + 1;
+    *p.step = step + K;
   }
 }
 
@@ -1021,6 +860,21 @@ __global__ void mask_kernel(T* mea, T* f0, T* f1, T* f2, T* f3, T* f4, T* f5, in
   }
 }
 
+// Zone marks (K3): the sign bit of msb on every live cell of an instance's zone
+// [i0-(Kz-1), i0+bx+Kz) x [j0-(Kz-1), j0+by+Kz) (Kz >= 2; empty for Kz = 1).
+template <typename T>
+__global__ void zone_kernel(T* msb, const T* mea, int64_t pitch, const int32_t* rects, int64_t row_begin, int row0,
+                            int Kz, bool set) {
+  if (Kz < 2) return;
+  const int32_t* r = rects + 4 * (int64_t)blockIdx.x;
+  const int u0 = r[0] - (Kz - 1), v0 = r[1] - (Kz - 1);
+  const int w = r[2] + 2 * Kz - 1, h = r[3] + 2 * Kz - 1;
+  for (int t = threadIdx.x; t < w * h; t += blockDim.x) {
+    const int64_t o = ((int64_t)v0 + t / w - row_begin + row0) * pitch + u0 + t % w;
+    if (mea[o] >= T(0)) msb[o] = set ? -fabs(msb[o]) : fabs(msb[o]);
+  }
+}
+
 template <typename M>
 __global__ void min2_kernel(const M* a, const M* b, int64_t n, double* out) {
   double ma = INFINITY, mb = INFINITY;
@@ -1052,58 +906,60 @@ void launch_min2(const M* a, const M* b, int64_t n, double* out, int nblocks, cu
 template void launch_min2<float>(const float*, const float*, int64_t, double*, int, cudaStream_t);
 template void launch_min2<double>(const double*, const double*, int64_t, double*, int, cudaStream_t);
 
+template <typename T, int K>
+void sweepk_launch(const SweepParams<T>& q, dim3 grid, int threads, cudaStream_t s) {
+  constexpr int V = VT<T>::N;
+  const size_t smem = K > 1 ? (size_t)(threads / 32) * K * NCOEF * 32 * V * sizeof(T) : 0;
+  if (q.partials) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(sweepk_kernel<T, K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sweepk_kernel<T, K, true><<<grid, threads, smem, s>>>(q);
+  } else {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(sweepk_kernel<T, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sweepk_kernel<T, K, false><<<grid, threads, smem, s>>>(q);
+  }
+}
+
 template <typename T>
-void launch_sweep(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s, int chunk_begin, int chunk_count) {
-  const int per_cta = 32 * warps_per_cta;
+void launch_sweep(const SweepParams<T>& p, int K, int warps_per_cta, cudaStream_t s, int chunk_begin,
+                  int chunk_count) {
   const int nch = (p.rows + p.chunk - 1) / p.chunk;
   if (chunk_count < 0) chunk_count = nch - chunk_begin;
   if (chunk_count <= 0) return;
   SweepParams<T> q = p;
   q.chunk0 = chunk_begin;
-  dim3 grid((p.ncolv + per_cta - 1) / per_cta, chunk_count);
-  if (p.partials) sweep_kernel<T, true><<<grid, per_cta, 0, s>>>(q);
-  else sweep_kernel<T, false><<<grid, per_cta, 0, s>>>(q);
+  dim3 grid(sweep_ctas_x(p.ncolv, warps_per_cta), chunk_count);
+  const int nt = 32 * warps_per_cta;
+  if (K == 1) sweepk_launch<T, 1>(q, grid, nt, s);
+  else if (K == 2) sweepk_launch<T, 2>(q, grid, nt, s);
+  else if constexpr (VT<T>::N >= 4) sweepk_launch<T, 4>(q, grid, nt, s);
 }
 
-template <typename T>
-void launch_sweep2(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s, int chunk_begin, int chunk_count) {
-  const int nch = (p.rows + p.chunk - 1) / p.chunk;
-  if (chunk_count < 0) chunk_count = nch - chunk_begin;
-  if (chunk_count <= 0) return;
-  SweepParams<T> q = p;
-  q.chunk0 = chunk_begin;
-  dim3 grid(sweep2_ctas_x(p.ncolv, warps_per_cta), chunk_count);
-  if (p.partials) sweep2_kernel<T, true><<<grid, 32 * warps_per_cta, 0, s>>>(q);
-  else sweep2_kernel<T, false><<<grid, 32 * warps_per_cta, 0, s>>>(q);
+size_t post_smem_bytes(size_t es, int nvec, int batch, int region_stride) {
+  return es * ((size_t)7 * nvec * batch + (size_t)batch * region_stride);
 }
 
-size_t post_smem_bytes(size_t es, int nvec, int batch) { return es * (size_t)7 * nvec * batch; }
-size_t post2_smem_bytes(size_t es, int nvec, int batch, int region_stride) {
-  return post_smem_bytes(es, nvec, batch) + es * (size_t)batch * region_stride;
-}
-
-template <typename T>
-void launch_post2(const PostParams<T>& p, bool energy, cudaStream_t s) {
-  const size_t smem = post2_smem_bytes(sizeof(T), p.nthreads_vec, p.batch, p.region_stride);
+template <typename T, int K>
+void postk_launch(const PostParams<T>& p, bool energy, cudaStream_t s) {
+  const size_t smem = post_smem_bytes(sizeof(T), p.nthreads_vec, p.batch, p.region_stride);
+  const int grid = p.n_batch > 0 ? p.n_batch : 1;
   if (energy) {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(post2_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    post2_kernel<T, true><<<p.n_batch + 1, p.block, smem, s>>>(p);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(postk_kernel<T, K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    postk_kernel<T, K, true><<<grid, p.block, smem, s>>>(p);
   } else {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(post2_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    post2_kernel<T, false><<<p.n_batch + 1, p.block, smem, s>>>(p);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(postk_kernel<T, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    postk_kernel<T, K, false><<<grid, p.block, smem, s>>>(p);
   }
 }
 
 template <typename T>
-void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s) {
-  const size_t smem = post_smem_bytes(sizeof(T), p.nthreads_vec, p.batch);
-  if (energy) {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(post_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    post_kernel<T, true><<<p.n_batch + 1, p.block, smem, s>>>(p);
-  } else {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(post_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    post_kernel<T, false><<<p.n_batch + 1, p.block, smem, s>>>(p);
-  }
+void launch_post(const PostParams<T>& p, int K, bool energy, cudaStream_t s) {
+  if (K == 1) postk_launch<T, 1>(p, energy, s);
+  else if (K == 2) postk_launch<T, 2>(p, energy, s);
+  else if constexpr (VT<T>::N >= 4) postk_launch<T, 4>(p, energy, s);
 }
 
 template <typename T, typename M>
@@ -1130,16 +986,23 @@ void launch_mask(T* mea, T* f[6], int64_t pitch, const int32_t* rects, int64_t n
                                                    row0, zero_iface);
 }
 
+template <typename T>
+void launch_zone(T* msb, const T* mea, int64_t pitch, const int32_t* rects, int64_t n_rect, int64_t row_begin,
+                 int row0, int Kz, bool set, cudaStream_t s) {
+  if (n_rect <= 0 || Kz < 2) return;
+  zone_kernel<T><<<(unsigned)n_rect, 256, 0, s>>>(msb, mea, pitch, rects, row_begin, row0, Kz, set);
+}
+
 #define INST(T)                                                                                     \
-  template void launch_sweep<T>(const SweepParams<T>&, int, cudaStream_t, int, int);              \
-  template void launch_sweep2<T>(const SweepParams<T>&, int, cudaStream_t, int, int);             \
-  template void launch_post<T>(const PostParams<T>&, bool, cudaStream_t);                        \
-  template void launch_post2<T>(const PostParams<T>&, bool, cudaStream_t);                       \
+  template void launch_sweep<T>(const SweepParams<T>&, int, int, cudaStream_t, int, int);         \
+  template void launch_post<T>(const PostParams<T>&, int, bool, cudaStream_t);                   \
   template void launch_materials<T, float>(const float*, const float*, int64_t, int64_t, int64_t, int64_t, \
                                            int64_t, int, int, int64_t, double, T*, T*, cudaStream_t);     \
   template void launch_materials<T, double>(const double*, const double*, int64_t, int64_t, int64_t,      \
                                             int64_t, int64_t, int, int, int64_t, double, T*, T*,          \
                                             cudaStream_t);                                                \
+  template void launch_zone<T>(T*, const T*, int64_t, const int32_t*, int64_t, int64_t, int, int, bool,   \
+                               cudaStream_t);                                                             \
   template void launch_mask<T>(T*, T* [6], int64_t, const int32_t*, int64_t, int64_t, int, bool, cudaStream_t);
 INST(float)
 INST(double)

@@ -6,26 +6,35 @@
 
 namespace fdtd {
 
-// Fused single-pass H+E sweep: S1 (eq:updateH), S2 (source), S3 (energy
-// partials) and S7 (eq:updateEx / Ey analogue) for one time step, ping-pong buffers.
+// K-step sweep: K time steps per pass over the grid (temporal blocking; K = 1
+// is the plain fused one-step sweep).  Each step is S1 (eq:updateH), S2 (source), S3 (probes,
+// energy partials of the non-zone cells) and S7 (eq:updateEx / Ey analogue); ping-pong buffers.
+// ROM interface edges are frozen for the whole pass; the fix-up kernel repairs the zone around
+// every instance.
+constexpr int KMAX = 4;  // deepest pass (ghost rows on each side of a slab)
 template <typename T>
 struct SweepParams {
   const T* ex0; const T* ey0; const T* hz0;  // fields at step n (E^n, H^{n-1/2})
-  T* ex1; T* ey1; T* hz1;                     // fields at step n+1 (E^{n+1}, H^{n+1/2})
-  const T* mea; const T* msb;  // per cell: eps0 eps_r / (2 dt) (< 0: hole / wall / dead) and sigma / 4
+  T* ex1; T* ey1; T* hz1;                     // fields at step n+K (E^{n+K}, H^{n+K-1/2})
+  // per cell: mea = eps0 eps_r / (2 dt) (< 0: hole / wall / dead), msb = sigma / 4 with the sign
+  // bit set on fix-up zone cells (their energy is added by the fix-up kernel)
+  const T* mea; const T* msb;
   int64_t pitch;   // elements per row (all arrays)
   int ncolv;       // vector columns processed (16-byte vectors)
   int rows;        // owned cell rows: local rows row0 .. row0+rows-1
-  int row0;        // local row of the first owned row (ROW0 = 2: two ghost rows below)
+  int row0;        // local row of the first owned row (KMAX ghost rows below)
   int chunk;       // rows per CTA
   int chunk0;      // first row chunk of this launch (split launches overlap the halo exchange)
   T chx, chy;      // dt/(mu0 dx), dt/(mu0 dy)
   int src_row;     // local row of the soft source (-1: none)
   int64_t src_col;
   const double* src_samples; int64_t src_n, src_t0;
-  const int64_t* step;  // device step counter (value n during step n)
-  double* partials;     // energy partial per CTA (nullptr: energy off)
-  double* partials2;    // two-step sweep: partials of the second step
+  const int64_t* step;  // device step counter (value n during the pass starting at step n)
+  double* partials;     // energy partial per CTA and step: partials[s * pstride + cta] (nullptr: off)
+  int64_t pstride;
+  const int2* probe_rows;  // per local row: (first, count) into probe_list (count 0: none)
+  const int2* probe_list;  // (column, probe index), sorted by row then column
+  T* probe_ring; int64_t cap;
   T idx, idy;           // 1/dx, 1/dy
   T wxy, wh;            // dx dy, mu0 dx dy / dt (energy weights)
 };
@@ -40,15 +49,17 @@ struct RomModelDev {
   int64_t off_M1, off_M2, off_Rt;
 };
 
-// Post kernel: S4-S6 per ROM instance, probe recording, deterministic
-// energy finalisation and the device step counter.
+// Fix-up kernel: per ROM instance, the K steps of the pass are recomputed on
+// the region [i0-M, i0+bx+M) x [j0-M, j0+by+M) (M = Kz + K - 1) from the pass's input buffer,
+// with the ROM update (S4-S6, eq:connExplicit) between them; the zone cells (the ones the sweep
+// may have got wrong and whose energy it skipped) are written back.  Also: zone probes, the
+// deterministic energy finalisation and the device step counter.
 template <typename T>
 struct PostParams {
   int n_inst;
   int n_batch;                     // CTAs doing ROM work; batches of <= batch instances of one model
   int batch;                       // instances per batch (multiple of 4)
   const int32_t* batch_tab;        // per batch: (model, first instance, count)
-  const int32_t* inst_model;
   const RomModelDev* models;
   const T* mpool;                  // shared model matrices (column-major)
   const T* Sk; const int64_t* Sk_off;        // per-instance Schur inverses (col-major nY x nY)
@@ -56,46 +67,44 @@ struct PostParams {
   const T* cya; const T* cyg;                 // a_y / c_y, D_l G / c_y per port
   const double* ehalf;                        // D_l D_l' eps / dt per port (energy)
   const int64_t* port_edge;                   // per port: (is_ey << 62) | element offset
-  const int64_t* port_h;                      // per port: Hz element offset of the outside cell
-  const int64_t* ring_idx; const int64_t* ring_off;  // hole-ring Hz cells per instance
   T* state; const int64_t* state_off;         // per instance [E~ (q1); H~ (q2)]
-  T* ex1; T* ey1; T* hz1;
-  int n_probe; const int64_t* probe_idx; T* probe_ring; int64_t cap;
-  const double* sweep_partials; int n_sweep_partials; double* rom_partials; double* energy_ring;
-  double* level1;                  // per post CTA energy partial (gridDim.x entries)
+  T* ex1; T* ey1; T* hz1;                     // output buffer (the sweep's)
+  const T* ex0; const T* ey0; const T* hz0;   // input buffer (state at step n)
+  const T* mea; const T* msb;
+  int64_t pitch, row_begin;
+  int row0;                        // local row of global row row_begin
+  int Kz;                          // zone depth of the material marks (>= K)
+  const int32_t* rects;            // per instance (i0, j0, bx, by), global
+  const int32_t* zp_off; const int32_t* zp;  // zone probes per instance: (gi, gj, probe index)
+  T* probe_ring; int64_t cap;
+  T chx, chy, idx, idy, wxy, wh;
+  int src_row; int64_t src_col; const double* src_samples; int64_t src_n, src_t0;
+  const double* sweep_partials; int64_t n_sweep_partials, pstride;  // [s * pstride + cta]
+  double* rom_partials;            // [s * n_inst + instance]: ROM + zone energy of step n+s
+  double* level1;                  // [s * gridDim.x + cta]
+  double* energy_ring;             // W^n per step (fp64 ring of cap entries)
   int64_t* step; unsigned int* done;
   int nthreads_vec;  // max(q1 + q2 + nY) over models: shared-memory vector stride
   int block;         // threads per CTA
-  // ---- two-step mode (post2): fix-up around every instance after sweep2 (K3b)
-  const int32_t* rects;            // per instance (i0, j0, bx, by), global
-  int64_t row_begin, pitch;
-  int row0;                        // local row of global row row_begin
-  const T* ex0; const T* ey0; const T* hz0;  // fields at step n (the sweep's input buffer)
-  const T* mea; const T* msb;
-  T chx, chy, idx, idy, wh;
-  int src_row; int64_t src_col; const double* src_samples; int64_t src_n, src_t0;
-  const double* sweep_partials2; double* rom_partials2; double* level1b;
-  int region_stride;               // shared-memory elements per instance region
+  int region_stride; // shared-memory elements per instance region
 };
 
 template <typename T>
-void launch_sweep(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s, int chunk_begin = 0,
+void launch_sweep(const SweepParams<T>& p, int K, int warps_per_cta, cudaStream_t s, int chunk_begin = 0,
                   int chunk_count = -1);
-// two time steps per pass (temporal blocking; 30 output lanes per warp)
-template <typename T>
-void launch_sweep2(const SweepParams<T>& p, int warps_per_cta, cudaStream_t s, int chunk_begin = 0,
-                   int chunk_count = -1);
-inline int sweep2_ctas_x(int ncolv, int warps_per_cta) {
+inline int sweep_ctas_x(int ncolv, int warps_per_cta) {  // 30 output lanes per warp
   const int nw = (ncolv + 29) / 30;
   return (nw + warps_per_cta - 1) / warps_per_cta;
 }
 template <typename T>
-void launch_post(const PostParams<T>& p, bool energy, cudaStream_t s);
-template <typename T>
-void launch_post2(const PostParams<T>& p, bool energy, cudaStream_t s);
-// shared-memory bytes of the two kernels for a given batch (host-side sizing)
-size_t post_smem_bytes(size_t es, int nvec, int batch);
-size_t post2_smem_bytes(size_t es, int nvec, int batch, int region_stride);
+void launch_post(const PostParams<T>& p, int K, bool energy, cudaStream_t s);
+// shared-memory bytes of the fix-up kernel for a given batch (host-side sizing)
+size_t post_smem_bytes(size_t es, int nvec, int batch, int region_stride);
+// elements of one instance region for zone depth Kz and pass depth K (<= Kz)
+inline int region_elems(int bx, int by, int M) {
+  const int Wr = bx + 2 * M, Hr = by + 2 * M;
+  return 3 * Hr * Wr + (Hr + 1) * Wr + Hr * (Wr + 1) + (bx + 2 * M) * (by + 2 * M);
+}
 
 // setup kernels
 template <typename T, typename M>
@@ -111,5 +120,9 @@ void launch_min2(const M* a, const M* b, int64_t n, double* out /*2 per block*/,
 template <typename T>
 void launch_mask(T* mea, T* fields[6], int64_t pitch, const int32_t* rects, int64_t n_rect, int64_t row_begin,
                  int row0, bool zero_iface, cudaStream_t s);
+// sign bit of msb on the zone cells of every instance (depth Kz; set or clear), holes excluded
+template <typename T>
+void launch_zone(T* msb, const T* mea, int64_t pitch, const int32_t* rects, int64_t n_rect, int64_t row_begin,
+                 int row0, int Kz, bool set, cudaStream_t s);
 
 }  // namespace fdtd

@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfdtdrom.so")
+# FDTD_LIB: an alternative in-tree build of the same library (kernel tuning experiments)
+LIB_PATH = os.environ.get("FDTD_LIB") or os.path.join(_HERE, "libfdtdrom.so")
 
 FDTD_MATERIALS_ON_DEVICE = 0x1
 FDTD_MATERIALS_F32 = 0x2
@@ -293,7 +294,7 @@ class Simulation:
         self._ck(lib().fdtd_get_info(self._h, C.byref(o)), "fdtd_get_info")
         return o
 
-    def set_time_blocking(self, steps_per_pass=2):
+    def set_time_blocking(self, steps_per_pass=4):
         self._ck(lib().fdtd_set_time_blocking(self._h, int(steps_per_pass)), "fdtd_set_time_blocking")
 
     def profile(self, on=True):
