@@ -222,7 +222,7 @@ fdtd::SweepParams<T> sweep_params(fdtd_ctx* c, int q) {
   p.ex0 = (const T*)c->f[q][0]; p.ey0 = (const T*)c->f[q][1]; p.hz0 = (const T*)c->f[q][2];
   p.ex1 = (T*)c->f[1 - q][0]; p.ey1 = (T*)c->f[1 - q][1]; p.hz1 = (T*)c->f[1 - q][2];
   p.mea = (const T*)c->coef[0]; p.msb = (const T*)c->coef[1];
-  p.pitch = c->pitch; p.ncolv = c->ncolv; p.rows = c->rows; p.chunk = c->chunk; p.row0 = ROW0;
+  p.pitch = c->pitch; p.nx = c->d.nx; p.rows = c->rows; p.chunk = c->chunk; p.row0 = ROW0;
   p.chx = (T)(c->d.dt / (MU0 * c->d.dx));
   p.chy = (T)(c->d.dt / (MU0 * c->d.dy));
   // the source row may also be a ghost row: the chunks next to the slab edges recompute up to
@@ -242,10 +242,15 @@ fdtd::SweepParams<T> sweep_params(fdtd_ctx* c, int q) {
   return p;
 }
 
-int sweep_gx(const fdtd_ctx* c) { return fdtd::sweep_ctas_x(c->ncolv, c->warps); }
+int sweep_gx(const fdtd_ctx* c, int K) { return fdtd::sweep_ctas_x(c->d.nx, (int)c->es, K, c->warps); }
+int sweep_gx_max(const fdtd_ctx* c) {
+  int g = 1;
+  for (int K = 1; K <= KMAX; K *= 2) g = std::max(g, sweep_gx(c, K));
+  return g;
+}
 
 template <typename T>
-fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
+fdtd::PostParams<T> post_params(fdtd_ctx* c, int q, int K) {
   fdtd::PostParams<T> p{};
   p.n_inst = (int)c->inst_model.size();
   p.models = c->d_models; p.mpool = (const T*)c->d_mpool;
@@ -271,7 +276,7 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
   p.src_col = src_here ? c->src_i : -1;
   p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
   p.sweep_partials = c->d_partials;  // exactly the partials the matching sweep launches wrote
-  p.n_sweep_partials = (int64_t)sweep_gx(c) * ((c->rows + c->chunk - 1) / c->chunk);
+  p.n_sweep_partials = (int64_t)sweep_gx(c, K) * ((c->rows + c->chunk - 1) / c->chunk);
   p.pstride = c->n_partials;
   p.rom_partials = c->d_rom_partials;
   p.level1 = c->d_level1;
@@ -410,8 +415,8 @@ fdtd_status enqueue_pass(fdtd_ctx* c, int q, cudaStream_t s, int K) {
     }
   }
   if (prof) CK(cudaEventRecord(e[1], s));
-  if (c->prec == 64) fdtd::launch_post<double>(post_params<double>(c, q), K, c->energy_on, s);
-  else fdtd::launch_post<float>(post_params<float>(c, q), K, c->energy_on, s);
+  if (c->prec == 64) fdtd::launch_post<double>(post_params<double>(c, q, K), K, c->energy_on, s);
+  else fdtd::launch_post<float>(post_params<float>(c, q, K), K, c->energy_on, s);
   if (prof) CK(cudaEventRecord(e[2], s));
   c->launches += 1;
   return FDTD_OK;
@@ -806,7 +811,7 @@ fdtd_status fdtd_set_tuning(fdtd_ctx* c, int32_t rows_per_cta, int32_t warps_per
   if (rows_per_cta < 0 || warps_per_cta < 0 || warps_per_cta > 8) return fail(c, FDTD_E_ARG, "bad tuning");
   c->chunk = rows_per_cta ? rows_per_cta : (c->rows >= 4096 ? 128 : 32);
   c->warps = warps_per_cta ? warps_per_cta : 4;
-  const int gx = sweep_gx(c);
+  const int gx = sweep_gx_max(c);
   const int gy = (c->rows + c->chunk - 1) / c->chunk;
   const int n = gx * gy;
   if (n > c->n_partials) {

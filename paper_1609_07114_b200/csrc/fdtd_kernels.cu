@@ -28,14 +28,23 @@ constexpr double C0 = 299792458.0;
 constexpr double EPS0 = 1.0 / (MU0 * C0 * C0);
 constexpr int64_t IDX_MASK = (int64_t(1) << 62) - 1;
 
-template <typename T> struct VT;
-template <> struct VT<float> { static constexpr int N = 4; };
-template <> struct VT<double> { static constexpr int N = 2; };
 
 __device__ __forceinline__ void ldv(const float* p, float (&v)[4]) {
   const float4 x = __ldg(reinterpret_cast<const float4*>(p));
   v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
 }
+__device__ __forceinline__ void ldv(const float* p, float (&v)[2]) {
+  const float2 x = __ldg(reinterpret_cast<const float2*>(p));
+  v[0] = x.x; v[1] = x.y;
+}
+__device__ __forceinline__ void stv(float* p, const float (&v)[2]) {
+  *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+}
+__device__ __forceinline__ void ldv_s(const float* p, float (&v)[2]) {
+  const float2 x = *reinterpret_cast<const float2*>(p);
+  v[0] = x.x; v[1] = x.y;
+}
+__device__ __forceinline__ void stv_s(float* p, const float (&v)[2]) { stv(p, v); }
 __device__ __forceinline__ void ldv(const double* p, double (&v)[2]) {
   const double2 x = __ldg(reinterpret_cast<const double2*>(p));
   v[0] = x.x; v[1] = x.y;
@@ -287,24 +296,24 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
 // shared-memory ring of K rows, where stages 1..K-1 find them.  Interface edges are dead (frozen)
 // in every step; the fix-up kernel repairs the zone around every ROM instance.  The arrays are
 // padded so that every lane loads unconditionally.
-#ifndef FDTD_SWEEP_THREADS
+#ifndef FDTD_SWEEP_THREADS  // at most 8 warps per CTA (fdtd_set_tuning)
 #define FDTD_SWEEP_THREADS 256
 #endif
-#ifndef FDTD_SWEEP_MINB
-#define FDTD_SWEEP_MINB 1
+#ifndef FDTD_SWEEP_MINB  // 2 x 256 threads: <= 128 registers, 16 resident warps per SM
+#define FDTD_SWEEP_MINB 2
 #endif
-template <typename T, int K, bool ENERGY>
+template <typename T, int K, int V, bool ENERGY>
 __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_kernel(const SweepParams<T> p) {
-  constexpr int V = VT<T>::N;
-  static_assert(K <= V, "one halo lane covers at most V columns of error spread");
+  constexpr int HL = (K + V - 1) / V;  // halo lanes at each end of a warp (sweep_halo)
+  constexpr int NOUT = 32 - 2 * HL;    // storing lanes per warp
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SweepCtx<T, V, K> x;
   x.lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int wpc = blockDim.x >> 5;
   x.ring = reinterpret_cast<T*>(smem_raw) + (int64_t)warp * K * NCOEF * 32 * V;
-  const int colv = (blockIdx.x * wpc + warp) * 30 + x.lane - 1;
-  x.out = colv >= 0 && colv < p.ncolv && x.lane >= 1 && x.lane <= 30;
+  const int64_t colv = (int64_t)(blockIdx.x * wpc + warp) * NOUT + x.lane - HL;
+  x.out = colv >= 0 && colv < (p.nx + V - 1) / V && x.lane >= HL && x.lane < 32 - HL;
   const int64_t c = (int64_t)colv * V;
   const int cy = p.chunk0 + blockIdx.y;  // row chunk
   x.r0 = p.row0 + cy * p.chunk;
@@ -908,16 +917,16 @@ template void launch_min2<double>(const double*, const double*, int64_t, double*
 
 template <typename T, int K>
 void sweepk_launch(const SweepParams<T>& q, dim3 grid, int threads, cudaStream_t s) {
-  constexpr int V = VT<T>::N;
+  constexpr int V = (sizeof(T) == 4 && K < 4) ? 4 : 2;  // sweep_width
   const size_t smem = K > 1 ? (size_t)(threads / 32) * K * NCOEF * 32 * V * sizeof(T) : 0;
   if (q.partials) {
     if (smem > 48 * 1024)
-      cudaFuncSetAttribute(sweepk_kernel<T, K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sweepk_kernel<T, K, true><<<grid, threads, smem, s>>>(q);
+      cudaFuncSetAttribute(sweepk_kernel<T, K, V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sweepk_kernel<T, K, V, true><<<grid, threads, smem, s>>>(q);
   } else {
     if (smem > 48 * 1024)
-      cudaFuncSetAttribute(sweepk_kernel<T, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sweepk_kernel<T, K, false><<<grid, threads, smem, s>>>(q);
+      cudaFuncSetAttribute(sweepk_kernel<T, K, V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sweepk_kernel<T, K, V, false><<<grid, threads, smem, s>>>(q);
   }
 }
 
@@ -929,11 +938,11 @@ void launch_sweep(const SweepParams<T>& p, int K, int warps_per_cta, cudaStream_
   if (chunk_count <= 0) return;
   SweepParams<T> q = p;
   q.chunk0 = chunk_begin;
-  dim3 grid(sweep_ctas_x(p.ncolv, warps_per_cta), chunk_count);
+  dim3 grid(sweep_ctas_x(p.nx, (int)sizeof(T), K, warps_per_cta), chunk_count);
   const int nt = 32 * warps_per_cta;
   if (K == 1) sweepk_launch<T, 1>(q, grid, nt, s);
   else if (K == 2) sweepk_launch<T, 2>(q, grid, nt, s);
-  else if constexpr (VT<T>::N >= 4) sweepk_launch<T, 4>(q, grid, nt, s);
+  else if constexpr (sizeof(T) == 4) sweepk_launch<T, 4>(q, grid, nt, s);
 }
 
 size_t post_smem_bytes(size_t es, int nvec, int batch, int region_stride) {
@@ -959,7 +968,7 @@ template <typename T>
 void launch_post(const PostParams<T>& p, int K, bool energy, cudaStream_t s) {
   if (K == 1) postk_launch<T, 1>(p, energy, s);
   else if (K == 2) postk_launch<T, 2>(p, energy, s);
-  else if constexpr (VT<T>::N >= 4) postk_launch<T, 4>(p, energy, s);
+  else if constexpr (sizeof(T) == 4) postk_launch<T, 4>(p, energy, s);
 }
 
 template <typename T, typename M>

@@ -20,7 +20,7 @@ struct SweepParams {
   // bit set on fix-up zone cells (their energy is added by the fix-up kernel)
   const T* mea; const T* msb;
   int64_t pitch;   // elements per row (all arrays)
-  int ncolv;       // vector columns processed (16-byte vectors)
+  int64_t nx;      // grid columns (the sweep processes ceil(nx / W) lane vectors per row)
   int rows;        // owned cell rows: local rows row0 .. row0+rows-1
   int row0;        // local row of the first owned row (KMAX ghost rows below)
   int chunk;       // rows per CTA
@@ -92,9 +92,15 @@ struct PostParams {
 template <typename T>
 void launch_sweep(const SweepParams<T>& p, int K, int warps_per_cta, cudaStream_t s, int chunk_begin = 0,
                   int chunk_count = -1);
-inline int sweep_ctas_x(int ncolv, int warps_per_cta) {  // 30 output lanes per warp
-  const int nw = (ncolv + 29) / 30;
-  return (nw + warps_per_cta - 1) / warps_per_cta;
+// Lane geometry of a K-step sweep: every lane holds W consecutive columns (one 8- or 16-byte
+// vector per array); errors from a warp's outermost columns spread one column per step, so the
+// HL = ceil(K / W) lanes at each end are redundant halo lanes and 32 - 2 HL lanes store.
+inline int sweep_width(int elem_bytes, int K) { return elem_bytes == 4 ? (K >= 4 ? 2 : 4) : 2; }
+inline int sweep_halo(int K, int W) { return (K + W - 1) / W; }
+inline int sweep_ctas_x(int64_t nx, int elem_bytes, int K, int warps_per_cta) {
+  const int W = sweep_width(elem_bytes, K), HL = sweep_halo(K, W);
+  const int64_t nvec = (nx + W - 1) / W, nw = (nvec + 32 - 2 * HL - 1) / (32 - 2 * HL);
+  return (int)((nw + warps_per_cta - 1) / warps_per_cta);
 }
 template <typename T>
 void launch_post(const PostParams<T>& p, int K, bool energy, cudaStream_t s);
