@@ -70,6 +70,38 @@ __device__ __forceinline__ double fma_rn(double a, double b, double c) { return 
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 
+// Packed fp32 pairs (sm_100a FADD2 / FMUL2 / FFMA2: two lanes of work per issue slot).  Each
+// element is rounded exactly as the scalar fadd / fmul / fma of the same operands, so packed and
+// scalar code paths (sweep vs fix-up) stay bit-identical.
+struct F2 {
+  float x, y;
+};
+__device__ __forceinline__ F2 add2(F2 a, F2 b) {
+  F2 r;
+  asm("{.reg .b64 ra, rb, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n add.rn.f32x2 rd, ra, rb;\n"
+      " mov.b64 {%0,%1}, rd;}" : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ F2 sub2(F2 a, F2 b) {
+  F2 r;
+  asm("{.reg .b64 ra, rb, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n sub.rn.f32x2 rd, ra, rb;\n"
+      " mov.b64 {%0,%1}, rd;}" : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ F2 mul2(F2 a, F2 b) {
+  F2 r;
+  asm("{.reg .b64 ra, rb, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n mul.rn.f32x2 rd, ra, rb;\n"
+      " mov.b64 {%0,%1}, rd;}" : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
+  F2 r;
+  asm("{.reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n mov.b64 rc, {%6,%7};\n"
+      " fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0,%1}, rd;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+
 // eq:updateH divided by dx dy mu / dt:  Hz' = Hz + chy (Ex_{j+1} - Ex_j) - chx (Ey_{i+1} - Ey_i).
 // Explicit fused operations pin the rounding, so the redundant recomputations at warp and
 // chunk edges are bit-identical to the owner's value (needed for 1-GPU == N-GPU fields).
@@ -148,20 +180,48 @@ __device__ __forceinline__ void row_coef(const T (&ma)[V], const T (&ms)[V], con
   }
 }
 
+// Coefficient sources for yee_row: registers (stage 0 just built them) or the warp's shared-memory
+// ring (stages 1..K-1), read lazily so that only the vectors in use occupy registers.
+template <typename T, int V>
+struct CoefRegs {
+  const RowCoef<T, V>& c;
+  __device__ __forceinline__ void hw(T (&o)[V]) const { for (int k = 0; k < V; ++k) o[k] = c.hw[k]; }
+  __device__ __forceinline__ void ex(T (&a)[V], T (&b)[V]) const {
+    for (int k = 0; k < V; ++k) { a[k] = c.cax[k]; b[k] = c.cbx[k]; }
+  }
+  __device__ __forceinline__ void ey(T (&a)[V], T (&b)[V]) const {
+    for (int k = 0; k < V; ++k) { a[k] = c.cay[k]; b[k] = c.cby[k]; }
+  }
+  __device__ __forceinline__ void w(T (&a)[V], T (&b)[V]) const {
+    for (int k = 0; k < V; ++k) { a[k] = c.wx[k]; b[k] = c.wy[k]; }
+  }
+};
+template <typename T, int V>
+struct CoefRing {
+  const T* b;  // this lane's slot: component i at b + i * 32 * V
+  __device__ __forceinline__ void hw(T (&o)[V]) const { ldv_s(b + 6 * 32 * V, o); }
+  __device__ __forceinline__ void ex(T (&a)[V], T (&c)[V]) const { ldv_s(b, a); ldv_s(b + 32 * V, c); }
+  __device__ __forceinline__ void ey(T (&a)[V], T (&c)[V]) const { ldv_s(b + 2 * 32 * V, a); ldv_s(b + 3 * 32 * V, c); }
+  __device__ __forceinline__ void w(T (&a)[V], T (&c)[V]) const { ldv_s(b + 4 * 32 * V, a); ldv_s(b + 5 * 32 * V, c); }
+};
+
 // One Yee step on one row r of a warp's column strip (K1): Hz^{new} of row r from
 // (Ex edge rows r and r+1, Ey and Hz of row r), the soft source, then Ex of edge row r and Ey of
-// row r from Hz^{new} of rows r and r-1 (hb).  Column neighbours come from warp shuffles (lane 0 /
-// 31 of a strip get wrong outermost values; they are redundant halo lanes).  All lanes call it.
-// Returns the row's storage-function partial of W at the step's start (zone cells excluded).
-template <typename T, int V, bool ENERGY>
+// row r from Hz^{new} of rows r and r-1 (hb).  Column neighbours come from warp shuffles (the
+// outermost lanes of a strip get wrong outermost values; they are redundant halo lanes).  All
+// lanes call it.  Returns the row's storage-function partial of W at the step's start (zone cells
+// excluded).
+template <typename T, int V, bool ENERGY, typename CS>
 __device__ __forceinline__ T yee_row(const T (&exb)[V], const T (&ext)[V], const T (&ey)[V], const T (&hz)[V],
-                                     const T (&hb)[V], const RowCoef<T, V>& cf, const SweepParams<T>& p, T gsrc,
+                                     const T (&hb)[V], const CS& cs, const SweepParams<T>& p, T gsrc,
                                      bool srow, int src_k, T (&hn)[V], T (&exo)[V], T (&eyo)[V]) {
   const T eyr = __shfl_down_sync(FULL, ey[0], 1);
+  T hw[V];
+  cs.hw(hw);
 #pragma unroll
   for (int k = 0; k < V; ++k) {
     const T hu = hupd(hz[k], ext[k], exb[k], k + 1 < V ? ey[k + 1] : eyr, ey[k], p.chy, p.chx);
-    hn[k] = signbit(cf.hw[k]) ? hz[k] : hu;  // dead cells keep their Hz
+    hn[k] = signbit(hw[k]) ? hz[k] : hu;  // dead cells keep their Hz
   }
   if (srow) {  // S2: soft source after the H half-step (this lane holds the source column)
 #pragma unroll
@@ -169,35 +229,119 @@ __device__ __forceinline__ T yee_row(const T (&exb)[V], const T (&ext)[V], const
       if (k == src_k) hn[k] += gsrc;
   }
   const T hl = __shfl_up_sync(FULL, hn[V - 1], 1);
-  T en = T(0);
+  {
+    T ca[V], cb[V];
+    cs.ex(ca, cb);
 #pragma unroll
-  for (int k = 0; k < V; ++k) {
-    exo[k] = eupd(exb[k], cf.cax[k], cf.cbx[k], hn[k] - hb[k]);
-    eyo[k] = eupd(ey[k], cf.cay[k], cf.cby[k], hn[k] - (k ? hn[k - 1] : hl));
-    if (ENERGY) en = cell_energy(en, exb[k], ey[k], hz[k], hn[k], cf.wx[k], cf.wy[k], cf.hw[k]);
+    for (int k = 0; k < V; ++k) exo[k] = eupd(exb[k], ca[k], cb[k], hn[k] - hb[k]);
+  }
+  {
+    T ca[V], cb[V];
+    cs.ey(ca, cb);
+#pragma unroll
+    for (int k = 0; k < V; ++k) eyo[k] = eupd(ey[k], ca[k], cb[k], hn[k] - (k ? hn[k - 1] : hl));
+  }
+  T en = T(0);
+  if (ENERGY) {
+    T wx[V], wy[V];
+    cs.w(wx, wy);
+#pragma unroll
+    for (int k = 0; k < V; ++k) en = cell_energy(en, exb[k], ey[k], hz[k], hn[k], wx[k], wy[k], hw[k]);
+  }
+  return en;
+}
+
+// yee_row for fp32 with the column pairs of a lane in packed FADD2 / FMUL2 / FFMA2 (the same
+// per-element operations as the generic version, in the same order).
+template <int V, bool ENERGY, typename CS>
+__device__ __forceinline__ float yee_row_f2(const float (&exb)[V], const float (&ext)[V], const float (&ey)[V],
+                                            const float (&hz)[V], const float (&hb)[V], const CS& cs,
+                                            const SweepParams<float>& p, float gsrc, bool srow, int src_k,
+                                            float (&hn)[V], float (&exo)[V], float (&eyo)[V]) {
+  static_assert(V % 2 == 0, "pairs");
+  const float eyr = __shfl_down_sync(FULL, ey[0], 1);
+  float hw[V];
+  cs.hw(hw);
+  const F2 chy{p.chy, p.chy}, mchx{-p.chx, -p.chx};
+#pragma unroll
+  for (int k = 0; k < V; k += 2) {
+    const F2 dex = sub2(F2{ext[k], ext[k + 1]}, F2{exb[k], exb[k + 1]});
+    const F2 dey = sub2(F2{ey[k + 1], k + 2 < V ? ey[k + 2] : eyr}, F2{ey[k], ey[k + 1]});
+    const F2 hu = fma2(mchx, dey, fma2(chy, dex, F2{hz[k], hz[k + 1]}));
+    hn[k] = signbit(hw[k]) ? hz[k] : hu.x;  // dead cells keep their Hz
+    hn[k + 1] = signbit(hw[k + 1]) ? hz[k + 1] : hu.y;
+  }
+  if (srow) {  // S2: soft source after the H half-step (this lane holds the source column)
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      if (k == src_k) hn[k] += gsrc;
+  }
+  const float hl = __shfl_up_sync(FULL, hn[V - 1], 1);
+  {
+    float ca[V], cb[V];
+    cs.ex(ca, cb);
+#pragma unroll
+    for (int k = 0; k < V; k += 2) {
+      const F2 t = mul2(F2{cb[k], cb[k + 1]}, sub2(F2{hn[k], hn[k + 1]}, F2{hb[k], hb[k + 1]}));
+      const F2 e = fma2(F2{ca[k], ca[k + 1]}, F2{exb[k], exb[k + 1]}, t);
+      exo[k] = e.x; exo[k + 1] = e.y;
+    }
+  }
+  {
+    float ca[V], cb[V];
+    cs.ey(ca, cb);
+#pragma unroll
+    for (int k = 0; k < V; k += 2) {
+      const F2 t = mul2(F2{cb[k], cb[k + 1]}, sub2(F2{hn[k], hn[k + 1]}, F2{k ? hn[k - 1] : hl, hn[k]}));
+      const F2 e = fma2(F2{ca[k], ca[k + 1]}, F2{ey[k], ey[k + 1]}, t);
+      eyo[k] = e.x; eyo[k + 1] = e.y;
+    }
+  }
+  float en = 0.f;
+  if (ENERGY) {
+    float wx[V], wy[V];
+    cs.w(wx, wy);
+    F2 acc{0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < V; k += 2) {
+      const F2 ex2{exb[k], exb[k + 1]}, ey2{ey[k], ey[k + 1]};
+      acc = fma2(mul2(F2{wx[k], wx[k + 1]}, ex2), ex2, acc);
+      acc = fma2(mul2(F2{wy[k], wy[k + 1]}, ey2), ey2, acc);
+      acc = fma2(mul2(F2{hw[k], hw[k + 1]}, F2{hz[k], hz[k + 1]}), F2{hn[k], hn[k + 1]}, acc);
+    }
+    en = acc.x + acc.y;
   }
   return en;
 }
 
 // S3 probes: record Hz^{n+s+1/2} of the probes in row r owned by this lane (sorted per row).
-template <typename T, int V, typename X>
-__device__ __forceinline__ void record_probes(const SweepParams<T>& p, int r, int64_t, const T (&h)[V], int64_t slot,
-                                              const X& x) {
+// Out of line: only the few row chunks holding a probe row take this path.
+template <typename T, int V>
+struct VecV {
+  T v[V];
+};
+template <typename T, int V>
+__device__ __forceinline__ void record_probes_v(const SweepParams<T>& p, int r, VecV<T, V> h, int64_t slot, int64_t c) {
   if (!p.probe_rows) return;
   const int2 pr = __ldg(p.probe_rows + r);
-  if (pr.y == 0) return;
-  const int64_t c = x.pex - p.ex0;  // this lane's first column
   for (int i = 0; i < pr.y; ++i) {
     const int2 e = __ldg(p.probe_list + pr.x + i);
     const int64_t d = (int64_t)e.x - c;
     if (d >= 0 && d < V) {
-      T v = h[0];
+      T v = h.v[0];
 #pragma unroll
       for (int k = 1; k < V; ++k)
-        if (d == k) v = h[k];
+        if (d == k) v = h.v[k];
       p.probe_ring[(int64_t)e.y * p.cap + slot] = v;
     }
   }
+}
+template <typename T, int V>
+__device__ __forceinline__ void record_probes(const SweepParams<T>& p, int r, const T (&h)[V], int64_t slot, int64_t c) {
+  VecV<T, V> hv;
+#pragma unroll
+  for (int k = 0; k < V; ++k) hv.v[k] = h[k];
+  record_probes_v<T, V>(p, r, hv, slot, c);
 }
 
 // per-warp shared-memory ring of K rows of coefficient sets (lane-private 16-byte vectors)
@@ -241,21 +385,32 @@ struct SweepCtx {
 // j+1's once stage 0 is done), A the stage outputs of row j-1, B receives those of row j.
 // Naming the two buffers statically (the caller alternates them) keeps every carried value in
 // place: no register moves.
-template <typename T, int V, int K, bool ENERGY, bool CHK, bool PROBES>
+// fp32: packed pairs; fp64: the generic scalar row
+template <typename T, int V, bool ENERGY, typename CS>
+__device__ __forceinline__ T yee_any(const T (&exb)[V], const T (&ext)[V], const T (&ey)[V], const T (&hz)[V],
+                                     const T (&hb)[V], const CS& cs, const SweepParams<T>& p, T gsrc, bool srow,
+                                     int src_k, T (&hn)[V], T (&exo)[V], T (&eyo)[V]) {
+  if constexpr (sizeof(T) == 4 && V % 2 == 0)
+    return yee_row_f2<V, ENERGY>(exb, ext, ey, hz, hb, cs, p, gsrc, srow, src_k, hn, exo, eyo);
+  else
+    return yee_row<T, V, ENERGY>(exb, ext, ey, hz, hb, cs, p, gsrc, srow, src_k, hn, exo, eyo);
+}
+
+template <typename T, int V, int K, bool ENERGY, bool CHK>
 __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCtx<T, V, K>& x, int j, int je,
                                           const RowIn<T, V>& X, RowIn<T, V>& Y, const StageOut<T, V, K>& A,
                                           StageOut<T, V, K>& B, double (&eacc)[K]) {
-  // CHK: some stage rows may lie outside the chunk [r0, r1) (energy, probes and stores skip them);
-  // without CHK every stage row is the chunk's own.  PROBES: look up the per-row probe table.
-  {  // ---- stage 0: step n on row j
+  // CHK: some stage rows may lie outside the chunk [r0, r1) (energy, probes and stores skip them)
+  // and the probe table is consulted; without CHK every stage row is the chunk's own, probe-free.
+  {  // ---- stage 0: step n on row j (builds the row's coefficients and parks them in the ring)
     RowCoef<T, V> cf;
     row_coef<T, V>(X.ma, X.ms, Y.ma, Y.ms, p.idx, p.idy, p.wxy, p.wh, cf);
     if (K > 1) ring_store<T, V>(x.ring, j & (K - 1), x.lane, cf);
-    const T en = yee_row<T, V, ENERGY>(Y.ext, X.ext, X.ey, X.hz, A.h[0], cf, p, x.g[0], j == x.src_r, x.src_k,
-                                       B.h[0], B.x[0], B.y[0]);
+    const T en = yee_any<T, V, ENERGY>(Y.ext, X.ext, X.ey, X.hz, A.h[0], CoefRegs<T, V>{cf}, p, x.g[0],
+                                       j == x.src_r, x.src_k, B.h[0], B.x[0], B.y[0]);
     const bool own = !CHK || (j >= x.r0 && j < x.r1);
     if (ENERGY && own) eacc[0] += (double)en;
-    if (PROBES && own && x.out) record_probes<T, V>(p, j, (int64_t)0, B.h[0], x.step % p.cap, x);
+    if (CHK && own && x.out) record_probes<T, V>(p, j, B.h[0], x.step % p.cap, x.pex - p.ex0);
   }
   if (j + 1 < je) {  // row j+1 into the buffer of row j-1 (consumed above)
     const int64_t o = (int64_t)(j + 1) * x.P;
@@ -269,13 +424,12 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
 #pragma unroll
   for (int s = 1; s < K; ++s) {
     const int r = j - s;
-    RowCoef<T, V> cf;
-    ring_load<T, V>(x.ring, r & (K - 1), x.lane, cf);
-    const T en = yee_row<T, V, ENERGY>(A.x[s - 1], B.x[s - 1], A.y[s - 1], A.h[s - 1], A.h[s], cf, p, x.g[s],
+    const CoefRing<T, V> cr{x.ring + ((int64_t)(r & (K - 1)) * NCOEF * 32 + x.lane) * V};
+    const T en = yee_any<T, V, ENERGY>(A.x[s - 1], B.x[s - 1], A.y[s - 1], A.h[s - 1], A.h[s], cr, p, x.g[s],
                                        r == x.src_r, x.src_k, B.h[s], B.x[s], B.y[s]);
     const bool own = !CHK || (r >= x.r0 && r < x.r1);
     if (ENERGY && own) eacc[s] += (double)en;
-    if (PROBES && own && x.out) record_probes<T, V>(p, r, (int64_t)0, B.h[s], (x.step + s) % p.cap, x);
+    if (CHK && own && x.out) record_probes<T, V>(p, r, B.h[s], (x.step + s) % p.cap, x.pex - p.ex0);
   }
   // stage K-1's outputs are the fields at step n+K of row j-K+1
   const int rs = j - (K - 1);
@@ -365,28 +519,18 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   }
   __syncthreads();
   // rows [jb, jm): the first stages' rows precede the chunk; [jm, jend): every stage row is the
-  // chunk's own; [jend, je): the last rows.  Boundaries keep even offsets (ping-pong parity).
+  // chunk's own (the fast body, unless the chunk holds a probe row); [jend, je): the last rows.
+  // Pairs of rows keep the ping-pong parity; the generic body checks rows at run time.
   const int jm = min(jb + ((x.r0 + K - 1 - jb + 1) & ~1), je);
-  const int jend = jm + (max(x.r1 - jm, 0) & ~1);
-  int j = jb;
-  for (; j < jm; j += 2) {
-    sweep_row<T, V, K, ENERGY, true, true>(p, x, j, je, R1, R0, O0, O1, eacc);
-    if (j + 1 < je) sweep_row<T, V, K, ENERGY, true, true>(p, x, j + 1, je, R0, R1, O1, O0, eacc);
-  }
-  if (chunk_probes) {
-    for (; j < jend; j += 2) {
-      sweep_row<T, V, K, ENERGY, false, true>(p, x, j, je, R1, R0, O0, O1, eacc);
-      sweep_row<T, V, K, ENERGY, false, true>(p, x, j + 1, je, R0, R1, O1, O0, eacc);
+  const int jend = chunk_probes ? jm : jm + (max(x.r1 - jm, 0) & ~1);
+  for (int j = jb; j < je; j += 2) {
+    if (j >= jm && j < jend) {
+      sweep_row<T, V, K, ENERGY, false>(p, x, j, je, R1, R0, O0, O1, eacc);
+      sweep_row<T, V, K, ENERGY, false>(p, x, j + 1, je, R0, R1, O1, O0, eacc);
+    } else {
+      sweep_row<T, V, K, ENERGY, true>(p, x, j, je, R1, R0, O0, O1, eacc);
+      if (j + 1 < je) sweep_row<T, V, K, ENERGY, true>(p, x, j + 1, je, R0, R1, O1, O0, eacc);
     }
-  } else {
-    for (; j < jend; j += 2) {
-      sweep_row<T, V, K, ENERGY, false, false>(p, x, j, je, R1, R0, O0, O1, eacc);
-      sweep_row<T, V, K, ENERGY, false, false>(p, x, j + 1, je, R0, R1, O1, O0, eacc);
-    }
-  }
-  for (; j < je; j += 2) {
-    sweep_row<T, V, K, ENERGY, true, true>(p, x, j, je, R1, R0, O0, O1, eacc);
-    if (j + 1 < je) sweep_row<T, V, K, ENERGY, true, true>(p, x, j + 1, je, R0, R1, O1, O0, eacc);
   }
   if (!x.out) {
 #pragma unroll
