@@ -379,6 +379,7 @@ struct SweepCtx {
   bool out;
   int64_t step, P;
   T g[K];
+  int64_t slot[K];  // probe-ring slot of each stage's step
 };
 
 // One stage-0 row j of the K-step sweep: X holds row j's data, Y row j-1's (and receives row
@@ -410,7 +411,7 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
                                        j == x.src_r, x.src_k, B.h[0], B.x[0], B.y[0]);
     const bool own = !CHK || (j >= x.r0 && j < x.r1);
     if (ENERGY && own) eacc[0] += (double)en;
-    if (CHK && own && x.out) record_probes<T, V>(p, j, B.h[0], x.step % p.cap, x.pex - p.ex0);
+    if (CHK && own && x.out) record_probes<T, V>(p, j, B.h[0], x.slot[0], x.pex - p.ex0);
   }
   if (j + 1 < je) {  // row j+1 into the buffer of row j-1 (consumed above)
     const int64_t o = (int64_t)(j + 1) * x.P;
@@ -429,7 +430,7 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
                                        r == x.src_r, x.src_k, B.h[s], B.x[s], B.y[s]);
     const bool own = !CHK || (r >= x.r0 && r < x.r1);
     if (ENERGY && own) eacc[s] += (double)en;
-    if (CHK && own && x.out) record_probes<T, V>(p, r, B.h[s], (x.step + s) % p.cap, x.pex - p.ex0);
+    if (CHK && own && x.out) record_probes<T, V>(p, r, B.h[s], x.slot[s], x.pex - p.ex0);
   }
   // stage K-1's outputs are the fields at step n+K of row j-K+1
   const int rs = j - (K - 1);
@@ -485,6 +486,7 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
       const int64_t k = x.step + s - p.src_t0;
       if (k >= 0 && k < p.src_n) x.g[s] = (T)p.src_samples[k];
     }
+    x.slot[s] = (x.step + s) % p.cap;
   }
   const int jb = x.r0 - K, je = x.r1 + K - 1;  // stage-0 rows [jb, je); jb - 1 >= 0 (ROW0 = 2 KMAX)
   RowIn<T, V> R0, R1;  // rows jb-1 (only Ex of edge row jb and the materials are used) and jb
@@ -508,21 +510,24 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   double eacc[K];
 #pragma unroll
   for (int s = 0; s < K; ++s) eacc[s] = 0.0;
-  // does the chunk hold a probe row?  (one warp scans the per-row table once)
-  __shared__ int chunk_probes;
-  if (threadIdx.x < 32) {
-    bool any = false;
-    if (p.probe_rows)
-      for (int r = x.r0 + x.lane; r < x.r1; r += 32) any |= __ldg(p.probe_rows + r).y > 0;
-    any = __any_sync(FULL, any);
-    if (threadIdx.x == 0) chunk_probes = any;
+  // does this warp's strip hold a probe in the chunk's rows?  (scanned once per warp)
+  bool warp_probes = false;
+  if (p.probe_rows) {
+    const int64_t c_lo = (colv - x.lane + HL) * V, c_hi = c_lo + (int64_t)NOUT * V;  // stored columns
+    for (int r = x.r0 + x.lane; r < x.r1; r += 32) {
+      const int2 pr = __ldg(p.probe_rows + r);
+      for (int i = 0; i < pr.y; ++i) {
+        const int col = __ldg(p.probe_list + pr.x + i).x;
+        warp_probes |= col >= c_lo && col < c_hi;
+      }
+    }
+    warp_probes = __any_sync(FULL, warp_probes);
   }
-  __syncthreads();
   // rows [jb, jm): the first stages' rows precede the chunk; [jm, jend): every stage row is the
   // chunk's own (the fast body, unless the chunk holds a probe row); [jend, je): the last rows.
   // Pairs of rows keep the ping-pong parity; the generic body checks rows at run time.
   const int jm = min(jb + ((x.r0 + K - 1 - jb + 1) & ~1), je);
-  const int jend = chunk_probes ? jm : jm + (max(x.r1 - jm, 0) & ~1);
+  const int jend = warp_probes ? jm : jm + (max(x.r1 - jm, 0) & ~1);
   for (int j = jb; j < je; j += 2) {
     if (j >= jm && j < jend) {
       sweep_row<T, V, K, ENERGY, false>(p, x, j, je, R1, R0, O0, O1, eacc);
