@@ -809,8 +809,12 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
 fdtd_status fdtd_set_tuning(fdtd_ctx* c, int32_t rows_per_cta, int32_t warps_per_cta) {
   if (!c) return FDTD_E_ARG;
   if (rows_per_cta < 0 || warps_per_cta < 0 || warps_per_cta > 8) return fail(c, FDTD_E_ARG, "bad tuning");
-  c->chunk = rows_per_cta ? rows_per_cta : (c->rows >= 4096 ? 128 : 32);
+  c->chunk = rows_per_cta ? rows_per_cta : (c->rows >= 4096 ? 256 : 32);
   c->warps = warps_per_cta ? warps_per_cta : 4;
+  if (!rows_per_cta)
+    if (const char* e = getenv("FDTD_CHUNK")) c->chunk = std::max(1, atoi(e));  // tuning experiments
+  if (!warps_per_cta)
+    if (const char* e = getenv("FDTD_WARPS")) c->warps = std::max(1, std::min(8, atoi(e)));
   const int gx = sweep_gx_max(c);
   const int gy = (c->rows + c->chunk - 1) / c->chunk;
   const int n = gx * gy;
