@@ -773,6 +773,12 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
 
   // + a tail: the sweep's lanes past the last vector column load unconditionally (their values are
   // never stored), reaching up to 31 vectors beyond the last row of an array
+  if ((double)c->nrows_alloc * (double)c->pitch >= 4294967296.0) {  // the sweep indexes rows with 32-bit offsets
+    fail(c, FDTD_E_ARG, "a slab of %lld x %lld elements per array exceeds 2^32; use more row slabs",
+         (long long)c->nrows_alloc, (long long)c->pitch);
+    fdtd_destroy(c);
+    return FDTD_E_ARG;
+  }
   const size_t fbytes = (size_t)c->nrows_alloc * c->pitch * c->es + 32 * 1024;
   for (int b = 0; b < 2; ++b)
     for (int a = 0; a < 3; ++a)

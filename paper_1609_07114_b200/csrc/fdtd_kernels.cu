@@ -346,15 +346,15 @@ __device__ __forceinline__ void record_probes(const SweepParams<T>& p, int r, co
 
 // per-warp shared-memory ring of K rows of coefficient sets (lane-private 16-byte vectors)
 template <typename T, int V>
-__device__ __forceinline__ void ring_store(T* ring, int slot, int lane, const RowCoef<T, V>& cf) {
-  T* b = ring + ((int64_t)slot * NCOEF * 32 + lane) * V;
+__device__ __forceinline__ void ring_store(T* ring, int slot, const RowCoef<T, V>& cf) {  // ring: this lane's base
+  T* b = ring + slot * (NCOEF * 32 * V);
   stv_s(b + 0 * 32 * V, cf.cax); stv_s(b + 1 * 32 * V, cf.cbx); stv_s(b + 2 * 32 * V, cf.cay);
   stv_s(b + 3 * 32 * V, cf.cby); stv_s(b + 4 * 32 * V, cf.wx); stv_s(b + 5 * 32 * V, cf.wy);
   stv_s(b + 6 * 32 * V, cf.hw);
 }
 template <typename T, int V>
-__device__ __forceinline__ void ring_load(const T* ring, int slot, int lane, RowCoef<T, V>& cf) {
-  const T* b = ring + ((int64_t)slot * NCOEF * 32 + lane) * V;
+__device__ __forceinline__ void ring_load(const T* ring, int slot, RowCoef<T, V>& cf) {
+  const T* b = ring + slot * (NCOEF * 32 * V);
   ldv_s(b + 0 * 32 * V, cf.cax); ldv_s(b + 1 * 32 * V, cf.cbx); ldv_s(b + 2 * 32 * V, cf.cay);
   ldv_s(b + 3 * 32 * V, cf.cby); ldv_s(b + 4 * 32 * V, cf.wx); ldv_s(b + 5 * 32 * V, cf.wy);
   ldv_s(b + 6 * 32 * V, cf.hw);
@@ -374,6 +374,7 @@ struct StageOut {
 template <typename T, int V, int K>
 struct SweepCtx {
   const T *pex, *pey, *phz, *pma, *pms;  // this lane's column in row 0 of each input array
+  T *pex1, *pey1, *phz1;                 // ... and of each output array
   T* ring;
   int lane, r0, r1, src_r, src_k;
   bool out;
@@ -406,15 +407,15 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
   {  // ---- stage 0: step n on row j (builds the row's coefficients and parks them in the ring)
     RowCoef<T, V> cf;
     row_coef<T, V>(X.ma, X.ms, Y.ma, Y.ms, p.idx, p.idy, p.wxy, p.wh, cf);
-    if (K > 1) ring_store<T, V>(x.ring, j & (K - 1), x.lane, cf);
+    if (K > 1) ring_store<T, V>(x.ring, j & (K - 1), cf);
     const T en = yee_any<T, V, ENERGY>(Y.ext, X.ext, X.ey, X.hz, A.h[0], CoefRegs<T, V>{cf}, p, x.g[0],
-                                       j == x.src_r, x.src_k, B.h[0], B.x[0], B.y[0]);
+                                       CHK && j == x.src_r, x.src_k, B.h[0], B.x[0], B.y[0]);
     const bool own = !CHK || (j >= x.r0 && j < x.r1);
     if (ENERGY && own) eacc[0] += (double)en;
     if (CHK && own && x.out) record_probes<T, V>(p, j, B.h[0], x.slot[0], x.pex - p.ex0);
   }
   if (j + 1 < je) {  // row j+1 into the buffer of row j-1 (consumed above)
-    const int64_t o = (int64_t)(j + 1) * x.P;
+    const uint32_t o = (uint32_t)(j + 1) * (uint32_t)x.P;  // arrays hold < 2^32 elements (fdtd_create)
     ldv(x.pex + o + x.P, Y.ext);
     ldv(x.pey + o, Y.ey);
     ldv(x.phz + o, Y.hz);
@@ -425,9 +426,9 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
 #pragma unroll
   for (int s = 1; s < K; ++s) {
     const int r = j - s;
-    const CoefRing<T, V> cr{x.ring + ((int64_t)(r & (K - 1)) * NCOEF * 32 + x.lane) * V};
+    const CoefRing<T, V> cr{x.ring + (r & (K - 1)) * (NCOEF * 32 * V)};
     const T en = yee_any<T, V, ENERGY>(A.x[s - 1], B.x[s - 1], A.y[s - 1], A.h[s - 1], A.h[s], cr, p, x.g[s],
-                                       r == x.src_r, x.src_k, B.h[s], B.x[s], B.y[s]);
+                                       CHK && r == x.src_r, x.src_k, B.h[s], B.x[s], B.y[s]);
     const bool own = !CHK || (r >= x.r0 && r < x.r1);
     if (ENERGY && own) eacc[s] += (double)en;
     if (CHK && own && x.out) record_probes<T, V>(p, r, B.h[s], x.slot[s], x.pex - p.ex0);
@@ -435,10 +436,10 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
   // stage K-1's outputs are the fields at step n+K of row j-K+1
   const int rs = j - (K - 1);
   if (x.out && (!CHK || (rs >= x.r0 && rs < x.r1))) {
-    const int64_t o = (int64_t)rs * x.P + (x.pex - p.ex0);
-    stv(p.hz1 + o, B.h[K - 1]);
-    stv(p.ex1 + o, B.x[K - 1]);
-    stv(p.ey1 + o, B.y[K - 1]);
+    const uint32_t o = (uint32_t)rs * (uint32_t)x.P;
+    stv(x.phz1 + o, B.h[K - 1]);
+    stv(x.pex1 + o, B.x[K - 1]);
+    stv(x.pey1 + o, B.y[K - 1]);
   }
 }
 
@@ -466,7 +467,7 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   x.lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int wpc = blockDim.x >> 5;
-  x.ring = reinterpret_cast<T*>(smem_raw) + (int64_t)warp * K * NCOEF * 32 * V;
+  x.ring = reinterpret_cast<T*>(smem_raw) + (int64_t)warp * K * NCOEF * 32 * V + x.lane * V;
   const int64_t colv = (int64_t)(blockIdx.x * wpc + warp) * NOUT + x.lane - HL;
   x.out = colv >= 0 && colv < (p.nx + V - 1) / V && x.lane >= HL && x.lane < 32 - HL;
   const int64_t c = (int64_t)colv * V;
@@ -476,6 +477,7 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   x.P = p.pitch;
   x.step = *p.step;
   x.pex = p.ex0 + c; x.pey = p.ey0 + c; x.phz = p.hz0 + c; x.pma = p.mea + c; x.pms = p.msb + c;
+  x.pex1 = p.ex1 + c; x.pey1 = p.ey1 + c; x.phz1 = p.hz1 + c;
   const bool src_lane = p.src_row >= 0 && p.src_col >= c && p.src_col < c + V;
   x.src_k = src_lane ? (int)(p.src_col - c) : -1;
   x.src_r = src_lane ? p.src_row : INT_MIN;
@@ -523,11 +525,14 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
     }
     warp_probes = __any_sync(FULL, warp_probes);
   }
+  // the soft source (S2) is applied only by the generic row body: a warp whose strip (halo lanes
+  // included) holds the source column takes it for the whole chunk
+  const bool warp_source = __any_sync(FULL, x.src_k >= 0) && p.src_row >= jb - K && p.src_row < je;
   // rows [jb, jm): the first stages' rows precede the chunk; [jm, jend): every stage row is the
   // chunk's own (the fast body, unless the chunk holds a probe row); [jend, je): the last rows.
   // Pairs of rows keep the ping-pong parity; the generic body checks rows at run time.
   const int jm = min(jb + ((x.r0 + K - 1 - jb + 1) & ~1), je);
-  const int jend = warp_probes ? jm : jm + (max(x.r1 - jm, 0) & ~1);
+  const int jend = (warp_probes || warp_source) ? jm : jm + (max(x.r1 - jm, 0) & ~1);
   for (int j = jb; j < je; j += 2) {
     if (j >= jm && j < jend) {
       sweep_row<T, V, K, ENERGY, false>(p, x, j, je, R1, R0, O0, O1, eacc);
