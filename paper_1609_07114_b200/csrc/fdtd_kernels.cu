@@ -102,6 +102,13 @@ __device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
   return r;
 }
 
+// one element global -> shared, asynchronously (LDGSTS); completed by cp.async.wait_all
+template <typename T>
+__device__ __forceinline__ void cp_async_el(T* dst, const T* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src),
+               "n"(sizeof(T)) : "memory");
+}
+
 // eq:updateH divided by dx dy mu / dt:  Hz' = Hz + chy (Ex_{j+1} - Ex_j) - chx (Ey_{i+1} - Ey_i).
 // Explicit fused operations pin the rounding, so the redundant recomputations at warp and
 // chunk edges are bit-identical to the owner's value (needed for 1-GPU == N-GPU fields).
@@ -768,19 +775,22 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     return ((int64_t)q.j0 - M + v - p.row_begin + p.row0) * P + q.i0 - M + u;
   };
   const int64_t src_off = p.src_row >= 0 ? (int64_t)p.src_row * P + p.src_col : -1;
-  // ---- load the region: materials and the fields at step n
+  // ---- load the region: materials and the fields at step n (asynchronous element copies, all in
+  // flight at once: the region rows are not 16-byte aligned)
   for (int b = 0; b < nb; ++b) {
     const Geo q = geo(b);
     for (int t = tid; t < q.Hr * q.Wr; t += nt) {
       const int64_t o = goff(q, t % q.Wr, t / q.Wr);
-      q.MA[t] = p.mea[o];
-      q.MS[t] = p.msb[o];
-      q.H[t] = p.hz0[o];
+      cp_async_el(q.MA + t, p.mea + o);
+      cp_async_el(q.MS + t, p.msb + o);
+      cp_async_el(q.H + t, p.hz0 + o);
     }
-    for (int t = tid; t < (q.Hr + 1) * q.Wr; t += nt) q.EX[t] = p.ex0[goff(q, t % q.Wr, t / q.Wr)];
-    for (int t = tid; t < q.Hr * (q.Wr + 1); t += nt) q.EY[t] = p.ey0[goff(q, t % (q.Wr + 1), t / (q.Wr + 1))];
+    for (int t = tid; t < (q.Hr + 1) * q.Wr; t += nt) cp_async_el(q.EX + t, p.ex0 + goff(q, t % q.Wr, t / q.Wr));
+    for (int t = tid; t < q.Hr * (q.Wr + 1); t += nt)
+      cp_async_el(q.EY + t, p.ey0 + goff(q, t % (q.Wr + 1), t / (q.Wr + 1)));
   }
   load_rom_state(p, m, first, nb, sv);
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
 #pragma unroll 1
   for (int s = 0; s < K; ++s) {
