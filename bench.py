@@ -35,6 +35,9 @@ WORKLOADS = {
             "dt = 1.9 dt_f, Gaussian source, 64 probes, energy every step",
     "cfg3": "BASELINE config 3: 8192^2 fp32, 1024 instances of one ROM (8x8 block, r=8, q=64), dt = 1.9 dt_f",
     "cfg2": "BASELINE config 2: 8192^2 fp32 plain grid, no ROMs, dt = 0.99 eq.(1)",
+    "cfg5": "BASELINE config 5: 49152^2 fp32, copula medium, 32 distinct ROM models (b 4..32, r 4..10, "
+            "q in {32,64,128,256}, uniform fills eps_r U[1,12] sigma U[0,0.2]), 8192 placements, dt = 1.9 min dt_f "
+            "(the 8-GPU config, run here on the GPUs given)",
 }
 SAMPLE_N = 1024  # bounded CPU sample: a seeded 1024^2 sub-instance of the same recipe
 

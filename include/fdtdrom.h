@@ -105,6 +105,12 @@ fdtd_status fdtd_create(const fdtd_grid_desc *desc, fdtd_ctx **out);
 typedef struct {
   int32_t bx, by, r, q1, q2;
   const double *R11, *R22, *F11, *K, *L;
+  /* 0: collapsed ports (L is q1 x nY, R9).  1: the paper-literal coupling (NEXT-1):
+   * L is q1 x nP with nP = r nY fine hanging variables in the same side order (fine port k on
+   * coarse port k / r), B~ = L~ S_f with S_f = S_c / r, coupled by eq:sysform with T and 1/r
+   * (eq:equalE, eq:averH L613-616); FDTD_E_ARG if that A1 is singular (the E basis
+   * must span the nP port directions, which needs q1 >= nP). */
+  int32_t literal;
 } fdtd_rom_model;
 
 /* Embed `count` instances of one model with lower-left coarse cells anchors[2k],

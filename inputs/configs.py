@@ -33,7 +33,7 @@ DX = DY = 1e-3  # R21
 
 
 @functools.lru_cache(maxsize=64)
-def _model(kind, b, r, q, fmax, seed, dt_target_factor):
+def _model(kind, b, r, q, fmax, seed, dt_target_factor, literal=False):
     if kind == "uniform14":
         fe, fs = sc.uniform_fill(b, b, r, seed, 1.0, 4.0, 0.0, 0.05)
     elif kind == "uniform112":
@@ -41,8 +41,10 @@ def _model(kind, b, r, q, fmax, seed, dt_target_factor):
     else:
         fe, fs = sc.inclusion_fill(b, r, seed)
     sysf = rg.fine_system(b, b, r, DX, DY, fe, fs)
-    csys = rg.collapse(sysf)
+    csys = rg.literal_system(sysf) if literal else rg.collapse(sysf)
     V1, V2 = rg.sprim_basis(csys, q, fmax)
+    if literal:  # the E basis must hold the nP port directions (q1 >= nP)
+        V1 = rg.with_port_directions(V1, csys["nY"])[:, : csys["nY"] + (q + 1) // 2]
     m = rg.reduce(csys, V1, V2)
     m["natural_dt_limit"] = rg.rom_cfl_limit(m)
     m["fine_dt_limit"] = rg.fine_cfl_limit(sysf)
@@ -50,20 +52,23 @@ def _model(kind, b, r, q, fmax, seed, dt_target_factor):
     return m
 
 
-def model(kind, b, r, q, fmax, seed, dt_target=None):
-    """A cached ROM of the given fill kind (see _model), optionally clipped at dt_target."""
-    m = dict(_model(kind, b, r, q, fmax, seed, None))
+def model(kind, b, r, q, fmax, seed, dt_target=None, literal=False):
+    """A cached ROM of the given fill kind (see _model), optionally clipped at dt_target.
+    literal: the paper's own nP-port coupling (NEXT-1) instead of the collapsed ports (R9)."""
+    m = dict(_model(kind, b, r, q, fmax, seed, None, literal))
     if dt_target is not None:
         m = rg.extend_cfl(m, dt_target)
     return m
 
 
 def _cfg1(variant, n=None):
+    """Config 1; variants b (dt = 0.95 dt_f), c (q = 48, active clip) and lit (the paper-literal
+    coupling through the nP = 80 fine hanging variables, NEXT-1: q = 24 + 80 port directions)."""
     nx = ny = 40
     eps = np.ones((ny, nx))
     sig = np.zeros((ny, nx))
     q = 48 if variant == "c" else 24
-    m = model("uniform14", 4, 5, q, 30e9, 11)
+    m = model("uniform14", 4, 5, q, 30e9, 11, literal=(variant == "lit"))
     dtc = sc.cfl_limit(DX, DY)
     if variant == "b":
         dt = 0.95 * m["fine_dt_limit"]
@@ -152,8 +157,8 @@ def _cfg5(n, device, seed=CFG5_SEED, max_fine=None, min_count=0):
 
 
 def make(name, n=None, device="cpu", **kw):
-    if name in ("cfg1", "cfg1b", "cfg1c"):
-        return _cfg1({"cfg1": "a", "cfg1b": "b", "cfg1c": "c"}[name])
+    if name in ("cfg1", "cfg1b", "cfg1c", "cfg1lit"):
+        return _cfg1({"cfg1": "a", "cfg1b": "b", "cfg1c": "c", "cfg1lit": "lit"}[name])
     if name == "cfg2":
         return _grid_scene("cfg2", 8192, n, device, 10000)
     if name == "cfg3":

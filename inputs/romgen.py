@@ -24,7 +24,9 @@ Emitted model (dict, fp64, C order): bx, by, r, q1, q2, R11 (q1 x q1), R22
 (q2 x q2), F11 (q1 x q1), K (q1 x q2), L (q1 x nY) with nY = 2 bx + 2 by, ports
 ordered S (bx), N (bx), W (by), E (by).  B~ = L~ S_c is implied, S_c =
 diag(-dx, +dx, +dy, -dy) per side (eq:cond3rom L717 with eq:S L698-707,
-collapsed).
+collapsed).  literal=True (NEXT-1): L is q1 x nP with the nP = r nY fine ports in
+the same side order, B~ = L~ diag(-dx/r, +dx/r, +dy/r, -dy/r per side) and the
+coupling is the paper's own eq:sysform with T and 1/r (eq:equalE, eq:averH).
 """
 from __future__ import annotations
 
@@ -188,13 +190,39 @@ def collapse(sysf):
 
 
 def full_order_model(csys):
-    """V = I on the collapsed system: the exact (unreduced) embedded model."""
+    """V = I on the collapsed (or literal) system: the exact (unreduced) embedded model."""
     nEc, nY = csys["nEc"], csys["nY"]
     L = np.zeros((nEc, nY))
     L[np.arange(nY), np.arange(nY)] = 1.0
     return dict(bx=csys["bx"], by=csys["by"], r=csys["r"], q1=nEc, q2=csys["nH"],
                 R11=np.diag(csys["r11"]), R22=np.diag(csys["r22"]), F11=np.diag(csys["f11"]),
-                K=csys["K"].toarray(), L=L, n_clipped=0)
+                K=csys["K"].toarray(), L=L, n_clipped=0, literal=bool(csys.get("literal", False)))
+
+
+# --------------------------------------------------------------------------
+# 2b. the paper-literal port set (NEXT-1): nP fine boundary nodes, no collapse
+# --------------------------------------------------------------------------
+def literal_system(sysf):
+    """The uncollapsed fine system with its E nodes reordered port nodes first (port order
+    S, N, W, E; nP = r nY of them), in the dict layout `sprim_basis` / `reduce` consume: the
+    ports are the nP fine hanging-variable nodes of eq:equalE / eq:averH (L608-616) and
+    B^ = L^ S with S the signed fine lengths (eq:B, eq:S)."""
+    nE, nP = sysf["nE"], sysf["nP"]
+    perm = np.concatenate([sysf["port_node"], np.setdiff1d(np.arange(nE), sysf["port_node"])])
+    Pm = sp.csr_matrix((np.ones(nE), (perm, np.arange(nE))), shape=(nE, nE))  # old -> new
+    return dict(bx=sysf["bx"], by=sysf["by"], r=sysf["r"], dx=sysf["dx"], dy=sysf["dy"], nY=nP, nEc=nE,
+                nH=sysf["nH"], r11=sysf["r11"][perm], f11=sysf["f11"][perm], r22=sysf["r22"],
+                K=(Pm.T @ sysf["K"]).tocsr(), Sc=sysf["S"].copy(), Pi=Pm, literal=True)
+
+
+def with_port_directions(V1, nP):
+    """Make the E basis contain the nP port-node unit vectors (ports are the first nP rows):
+    the literal coupling needs L~^T = V1[:nP] of full row rank (A1 regular, R9)."""
+    P = np.zeros((V1.shape[0], nP))
+    P[np.arange(nP), np.arange(nP)] = 1.0
+    rest = V1 - P @ (P.T @ V1)
+    U = _orth(rest)
+    return np.hstack([P, U])
 
 
 # --------------------------------------------------------------------------
@@ -299,11 +327,11 @@ def reduce(csys, V1, V2):
     R22 = V2.T @ (csys["r22"][:, None] * V2)
     F11 = V1.T @ (csys["f11"][:, None] * V1)
     K = V1.T @ (csys["K"] @ V2)
-    L = V1[: csys["nY"], :].T.copy()           # V1^T L_c with L_c = [I; 0]
+    L = V1[: csys["nY"], :].T.copy()           # V1^T L_c with L_c = [I; 0] (ports first)
     sym = lambda A: 0.5 * (A + A.T)            # exact symmetry of congruences
     return dict(bx=csys["bx"], by=csys["by"], r=csys["r"], q1=V1.shape[1], q2=V2.shape[1],
                 R11=sym(R11), R22=sym(R22), F11=sym(F11), K=np.ascontiguousarray(K),
-                L=np.ascontiguousarray(L), n_clipped=0)
+                L=np.ascontiguousarray(L), n_clipped=0, literal=bool(csys.get("literal", False)))
 
 
 # --------------------------------------------------------------------------
@@ -361,14 +389,19 @@ def check_passivity(model, dt, tol=1e-12):
 # --------------------------------------------------------------------------
 # one-call driver
 # --------------------------------------------------------------------------
-def build_rom(bx, by, r, dx, dy, eps_r, sigma, q, fmax, dt_target=None, full=False):
-    """Fine assembly -> collapse -> SPRIM(q) -> reduce -> optional clip at dt_target."""
+def build_rom(bx, by, r, dx, dy, eps_r, sigma, q, fmax, dt_target=None, full=False, literal=False):
+    """Fine assembly -> collapse (or the literal nP-port set) -> SPRIM(q) -> reduce -> optional
+    clip at dt_target.  literal: the paper's own port set (nP = r nY fine hanging variables,
+    eq:equalE / eq:averH); the E basis then holds the nP port directions plus ceil(q/2) SPRIM
+    directions (q1 = nP + ceil(q/2), q2 = floor(q/2))."""
     sysf = fine_system(bx, by, r, dx, dy, eps_r, sigma)
-    csys = collapse(sysf)
+    csys = literal_system(sysf) if literal else collapse(sysf)
     if full:
         model = full_order_model(csys)
     else:
         V1, V2 = sprim_basis(csys, q, fmax)
+        if literal:
+            V1 = with_port_directions(V1, csys["nY"])[:, : csys["nY"] + (q + 1) // 2]
         model = reduce(csys, V1, V2)
     model["natural_dt_limit"] = rom_cfl_limit(model) if not full else None
     model["fine_dt_limit"] = fine_cfl_limit(sysf)
@@ -387,4 +420,6 @@ def load_model(path):
     for k in ("bx", "by", "r", "q1", "q2", "n_clipped"):
         if k in m:
             m[k] = int(m[k])
+    if "literal" in m:
+        m["literal"] = bool(m["literal"])
     return m

@@ -51,7 +51,7 @@ def lib():
         L.osim_create.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, _dp, _dp]
         L.osim_destroy.argtypes = [C.c_void_p]
         L.osim_add_rom.restype = C.c_int
-        L.osim_add_rom.argtypes = [C.c_void_p] + [C.c_int] * 6 + [_dp] * 5
+        L.osim_add_rom.argtypes = [C.c_void_p] + [C.c_int] * 6 + [_dp] * 5 + [C.c_int, C.c_int]
         L.osim_add_subgrid.restype = C.c_int
         L.osim_add_subgrid.argtypes = [C.c_void_p] + [C.c_int] * 5 + [_dp, _dp]
         L.osim_set_source.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int64, C.c_int64]
@@ -109,11 +109,16 @@ class OracleSim:
             pass
 
     def add_rom(self, model, i0, j0):
-        """Embed one instance of a reduced model (dict with R11,R22,F11,K,L,bx,by)."""
+        """Embed one instance of a reduced model (dict with R11,R22,F11,K,L,bx,by[,r,literal]).
+
+        literal models couple through the r nY fine hanging variables of the paper's eq:sysform
+        (T, 1/r; L is q1 x r nY); the default is the collapsed reading (R9)."""
         R11, R22, F11, K, L = (_f64(model[k]) for k in ("R11", "R22", "F11", "K", "L"))
         q1, q2 = R11.shape[0], R22.shape[0]
+        literal = bool(model.get("literal", False))
         rc = lib().osim_add_rom(self._h, int(i0), int(j0), int(model["bx"]), int(model["by"]), q1, q2,
-                                _p(R11), _p(R22), _p(F11), _p(K), _p(L))
+                                _p(R11), _p(R22), _p(F11), _p(K), _p(L), int(model.get("r", 1)),
+                                1 if literal else 0)
         if rc < 0:
             raise ValueError("osim_add_rom failed with code %d" % rc)
         self.rom_q.append(q1 + q2)

@@ -41,11 +41,12 @@ enum { K_NORMAL = 0, K_PEC = 1, K_HOLE = 2, K_IFACE = 3 };
 
 typedef struct {
   int i0, j0, bx, by, q1, q2, nY, q, nz;
-  double *R11, *R22, *F11, *K, *L; /* row-major copies, L is q1 x nY */
+  int r, nU, xoff;                 /* hanging variables: nU = nY (collapsed) or r nY (literal); xt at z[xoff] */
+  double *R11, *R22, *F11, *K, *L; /* row-major copies, L is q1 x nU */
   double *A1;                      /* LU factors of A1 (nz x nz), row-major */
   int *piv;
   double *A2;                      /* dense nz x nz */
-  double *z;                       /* [y; U; xt], length nz */
+  double *z;                       /* [y (nY); U or u^ (nU); xt (q)], length nz */
   double *DlG;                     /* D_l G per port */
   double *eps_half;                /* D_l D_l' eps (coarse half cell) per port */
   int *port_is_ey;                 /* 0: Ex edge, 1: Ey edge */
@@ -191,8 +192,8 @@ void osim_destroy(osim *s) {
 /* dx/2 (L603).  G signs: DESIGN.md R5.                                */
 /* ------------------------------------------------------------------ */
 int osim_add_rom(osim *s, int i0, int j0, int bx, int by, int q1, int q2, const double *R11,
-                 const double *R22, const double *F11, const double *K, const double *L) {
-  if (bx < 1 || by < 1 || q1 < 1 || q2 < 0) return -1;
+                 const double *R22, const double *F11, const double *K, const double *L, int r, int literal) {
+  if (bx < 1 || by < 1 || q1 < 1 || q2 < 0 || r < 1) return -1;
   if (i0 < 1 || j0 < 1 || i0 + bx > s->nx - 1 || j0 + by > s->ny - 1) return -2;
   /* footprint + ring must not touch another block */
   for (int j = j0 - 1; j <= j0 + by; ++j)
@@ -202,8 +203,13 @@ int osim_add_rom(osim *s, int i0, int j0, int bx, int by, int q1, int q2, const 
   orom *m = &s->roms[s->nrom];
   memset(m, 0, sizeof(*m));
   m->i0 = i0; m->j0 = j0; m->bx = bx; m->by = by; m->q1 = q1; m->q2 = q2;
-  int nY = 2 * bx + 2 * by, q = q1 + q2, nz = 2 * nY + q;
-  m->nY = nY; m->q = q; m->nz = nz;
+  int nY = 2 * bx + 2 * by, q = q1 + q2;
+  /* literal (the paper's own Sec. IV, NEXT-1): nU = r nY fine hanging variables u^ tied to the
+   * coarse edges by T (eq:equalE: fine port k sits on coarse port k / r, the side order being
+   * the same) and averaged by 1/r T^T (eq:averH).  Collapsed (R9): T -> I, 1/r -> 1. */
+  int nU = literal ? r * nY : nY, nz = nY + nU + q;
+  m->nY = nY; m->q = q; m->nz = nz; m->r = literal ? r : 1; m->nU = nU; m->xoff = nY + nU;
+  const int X = nY + nU;
 #define DUP(dst, src, cnt)                                      \
   do {                                                          \
     dst = (double *)malloc((size_t)(cnt) * sizeof(double) + 8); \
@@ -213,7 +219,7 @@ int osim_add_rom(osim *s, int i0, int j0, int bx, int by, int q1, int q2, const 
   DUP(m->R22, R22, q2 * q2);
   DUP(m->F11, F11, q1 * q1);
   DUP(m->K, K, q1 * q2);
-  DUP(m->L, L, q1 * nY);
+  DUP(m->L, L, q1 * nU);
 #undef DUP
   m->DlG = (double *)calloc(nY, sizeof(double));
   m->eps_half = (double *)calloc(nY, sizeof(double));
@@ -247,43 +253,48 @@ int osim_add_rom(osim *s, int i0, int j0, int bx, int by, int q1, int q2, const 
     m->port_edge[p] = edge;
     m->port_h[p] = oj * nx + oi;
   }
-  /* A1 and A2 of eq:sysform (L649-664), collapsed: T -> I, 1/r -> 1.
-   * z = [y (nY); U (nY); xt (q)], xt = [E~ (q1); H~ (q2)].
+  /* A1 and A2 of eq:sysform (L649-664).
+   * z = [y (nY); u (nU); xt (q)], xt = [E~ (q1); H~ (q2)].
    * R~ + F~ = [[R11/dt + F11, -K], [0, R22/dt]]       (eq:R, eq:F_f, L416-425)
    * R~ - F~ = [[R11/dt - F11, 0], [-K^T, R22/dt]]
-   * B~ = L~ S_c, S_c = diag(-dx (S), +dx (N), +dy (W), -dy (E))  (eq:cond3rom, eq:S) */
+   * B~ = L~ S, S = diag(-dx (S), +dx (N), +dy (W), -dy (E)) per coarse port (collapsed) or the
+   * same divided by r per fine port (literal)  (eq:B, eq:cond3rom, eq:S) */
+  const int rr = m->r;
   double *A1 = (double *)calloc((size_t)nz * nz, sizeof(double));
   double *A2 = (double *)calloc((size_t)nz * nz, sizeof(double));
-#define A1_(r, cc) A1[(size_t)(r) * nz + (cc)]
-#define A2_(r, cc) A2[(size_t)(r) * nz + (cc)]
+#define A1_(r_, cc) A1[(size_t)(r_) * nz + (cc)]
+#define A2_(r_, cc) A2[(size_t)(r_) * nz + (cc)]
   for (int p = 0; p < nY; ++p) {
-    /* row block 1: D_l D_l'(D_eps/dt + D_sig/2) y' + D_l G^T U = ... (eq:updateEBC) */
+    /* row block 1: D_l D_l'(D_eps/dt + D_sig/2) y' + (1/r) D_l G^T T^T u = ... (eq:updateEBC2) */
     A1_(p, p) = c[p];
-    A1_(p, nY + p) = m->DlG[p];
+    for (int k = p * rr; k < (p + 1) * rr; ++k) A1_(p, nY + k) = m->DlG[p] / rr;
     A2_(p, p) = a[p];
-    /* row block 2: y' - L~^T xt' = 0 (eq:yandxt with transpose, R6) */
-    A1_(nY + p, p) = 1.0;
-    for (int e = 0; e < q1; ++e) A1_(nY + p, 2 * nY + e) = -L[(size_t)e * nY + p];
+  }
+  for (int k = 0; k < nU; ++k) {
+    /* row block 2: T y' - L~^T xt' = 0 (eq:yandxt with transpose, R6) */
+    A1_(nY + k, k / rr) = 1.0;
+    for (int e = 0; e < q1; ++e) A1_(nY + k, X + e) = -L[(size_t)e * nU + k];
   }
   for (int e = 0; e < q1; ++e) {
-    int row = 2 * nY + e;
-    for (int p = 0; p < nY; ++p) {
+    int row = X + e;
+    for (int k = 0; k < nU; ++k) {
+      const int p = k / rr;  /* coarse port of (fine) port k */
       double Sc = (p < bx) ? -dx : (p < 2 * bx) ? dx : (p < 2 * bx + by) ? dy : -dy;
-      A1_(row, nY + p) = -L[(size_t)e * nY + p] * Sc; /* -B~ */
+      A1_(row, nY + k) = -L[(size_t)e * nU + k] * Sc / rr; /* -B~ */
     }
     for (int f = 0; f < q1; ++f) {
-      A1_(row, 2 * nY + f) = R11[(size_t)e * q1 + f] / dt + F11[(size_t)e * q1 + f];
-      A2_(row, 2 * nY + f) = R11[(size_t)e * q1 + f] / dt - F11[(size_t)e * q1 + f];
+      A1_(row, X + f) = R11[(size_t)e * q1 + f] / dt + F11[(size_t)e * q1 + f];
+      A2_(row, X + f) = R11[(size_t)e * q1 + f] / dt - F11[(size_t)e * q1 + f];
     }
-    for (int h = 0; h < q2; ++h) A1_(row, 2 * nY + q1 + h) = -K[(size_t)e * q2 + h];
+    for (int h = 0; h < q2; ++h) A1_(row, X + q1 + h) = -K[(size_t)e * q2 + h];
   }
   for (int h = 0; h < q2; ++h) {
-    int row = 2 * nY + q1 + h;
+    int row = X + q1 + h;
     for (int g = 0; g < q2; ++g) {
-      A1_(row, 2 * nY + q1 + g) = R22[(size_t)h * q2 + g] / dt;
-      A2_(row, 2 * nY + q1 + g) = R22[(size_t)h * q2 + g] / dt;
+      A1_(row, X + q1 + g) = R22[(size_t)h * q2 + g] / dt;
+      A2_(row, X + q1 + g) = R22[(size_t)h * q2 + g] / dt;
     }
-    for (int e = 0; e < q1; ++e) A2_(row, 2 * nY + e) = -K[(size_t)e * q2 + h];
+    for (int e = 0; e < q1; ++e) A2_(row, X + e) = -K[(size_t)e * q2 + h];
   }
 #undef A1_
 #undef A2_
@@ -439,7 +450,7 @@ static double energy(const osim *s) {
   w /= dt;
   for (int r = 0; r < s->nrom; ++r) {
     const orom *m = &s->roms[r];
-    const double *E = m->z + 2 * m->nY, *H = E + m->q1;
+    const double *E = m->z + m->xoff, *H = E + m->q1;
     double e11 = 0, e22 = 0, ek = 0;
     for (int a = 0; a < m->q1; ++a)
       for (int b = 0; b < m->q1; ++b) e11 += E[a] * m->R11[(size_t)a * m->q1 + b] * E[b];
@@ -641,7 +652,7 @@ void osim_get_state(const osim *s, double *Ex, double *Ey, double *Hz, double *r
     size_t off = 0;
     for (int r = 0; r < s->nrom; ++r) {
       const orom *m = &s->roms[r];
-      memcpy(rom_state + off, m->z + 2 * m->nY, (size_t)m->q * sizeof(double));
+      memcpy(rom_state + off, m->z + m->xoff, (size_t)m->q * sizeof(double));
       off += m->q;
     }
   }
@@ -657,7 +668,7 @@ void osim_set_state(osim *s, const double *Ex, const double *Ey, const double *H
     size_t off = 0;
     for (int r = 0; r < s->nrom; ++r) {
       orom *m = &s->roms[r];
-      memcpy(m->z + 2 * m->nY, rom_state + off, (size_t)m->q * sizeof(double));
+      memcpy(m->z + m->xoff, rom_state + off, (size_t)m->q * sizeof(double));
       off += m->q;
     }
   }

@@ -64,7 +64,10 @@ constexpr int NCCL_I32 = 2, NCCL_F32 = 7, NCCL_F64 = 8, NCCL_SUM = 0, NCCL_MIN =
 
 struct ModelHost {
   int bx, by, nY, q1, q2;
-  std::vector<double> P;  // nY x nY: L~^T C^-1 B~
+  bool literal = false;
+  // per-instance Schur base (nY x nY): collapsed L~^T C^-1 B~ (S_k = (P + diag(D_l G / c_y))^-1);
+  // literal Psi = (1/r) D_l G T^T P_f^-1 T (S_k = (diag(c_y) + Psi)^-1)
+  std::vector<double> P;
   fdtd::RomModelDev dev;
 };
 
@@ -841,11 +844,14 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
     return fail(c, FDTD_E_ARG, "bad model");
   if (count < 0 || (count > 0 && !anchors)) return fail(c, FDTD_E_ARG, "bad anchors");
   const int bx = m->bx, by = m->by, q1 = m->q1, q2 = m->q2, nY = 2 * bx + 2 * by, q = q1 + q2;
+  const bool literal = m->literal != 0;
+  const int rr = literal ? m->r : 1, nU = rr * nY;  // ports of L: nY coarse edges or r nY fine nodes
+  if (literal && m->r < 1) return fail(c, FDTD_E_ARG, "literal model needs r >= 1");
   const double dt = c->d.dt, dx = c->d.dx, dy = c->d.dy;
   using fdtd::dense::Mat;
   namespace dense = fdtd::dense;
   Mat R11(m->R11, m->R11 + q1 * q1), R22(m->R22, m->R22 + q2 * q2), F11(m->F11, m->F11 + q1 * q1),
-      K(m->K, m->K + q1 * q2), L(m->L, m->L + q1 * nY);
+      K(m->K, m->K + q1 * q2), L(m->L, m->L + (size_t)q1 * nU);
   // eq:cond1rom: R~ = [[R11/dt, -K/2], [-K^T/2, R22/dt]] > 0 (Cholesky of the diagonally scaled matrix)
   {
     Mat R = dense::zeros(q, q);
@@ -920,21 +926,47 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
   Mat Ci, R22i;
   if (!dense::inverse(Cm, q1, Ci) || !dense::inverse(R22, q2, R22i))
     return fail(c, FDTD_E_PASSIVITY, "singular R~11/dt + F~11 or R~22");
-  std::vector<double> Sc(nY);
-  for (int p = 0; p < nY; ++p) Sc[p] = p < bx ? -dx : p < 2 * bx ? dx : p < 2 * bx + by ? dy : -dy;
-  Mat Be = dense::zeros(q1, nY);
+  std::vector<double> Sc(nY), DlGm(nY);
+  for (int p = 0; p < nY; ++p) {
+    Sc[p] = p < bx ? -dx : p < 2 * bx ? dx : p < 2 * bx + by ? dy : -dy;
+    DlGm[p] = p < bx ? -dx : p < 2 * bx ? dx : p < 2 * bx + by ? dy : -dy;  // D_l G (R5): same numbers
+  }
+  // B~ = L~ S over the ports of L (S_f = S_c / r on the literal fine ports)
+  Mat Be = dense::zeros(q1, nU);
   for (int i = 0; i < q1; ++i)
-    for (int p = 0; p < nY; ++p) Be[i * nY + p] = L[i * nY + p] * Sc[p];
+    for (int k = 0; k < nU; ++k) Be[(size_t)i * nU + k] = L[(size_t)i * nU + k] * Sc[k / rr] / rr;
   Mat Aq = dense::matmul(Ci, Cr, q1, q1, q1);
   Mat Kq = dense::matmul(Ci, K, q1, q1, q2);
   Mat Kt = dense::transpose(K, q1, q2);
   Mat Q1 = dense::matmul(R22i, Kt, q2, q2, q1);
   for (auto& v : Q1) v *= -dt;
-  Mat Bq = dense::matmul(Ci, Be, q1, q1, nY);
-  Mat Lt = dense::transpose(L, q1, nY);
-  Mat P = dense::matmul(Lt, Bq, nY, q1, nY);
+  Mat Bq = dense::matmul(Ci, Be, q1, q1, nU);
+  Mat Lt = dense::transpose(L, q1, nU);
+  Mat P = dense::matmul(Lt, Bq, nU, q1, nU);
   ModelHost mh;
-  mh.bx = bx; mh.by = by; mh.nY = nY; mh.q1 = q1; mh.q2 = q2; mh.P = P;
+  mh.bx = bx; mh.by = by; mh.nY = nY; mh.q1 = q1; mh.q2 = q2; mh.literal = literal;
+  // literal coupling (eq:sysform with T, 1/r; K3): with P_f = L~^T C^-1 B~ (nP x nP),
+  //   u^ = P_f^-1 (T y' - L~^T E*),  (diag(c_y) + Psi) y' = a_y y + D_l G h + W1 E*,
+  //   E~' = (I - Z L~^T) E* + Z T y',  Z = C^-1 B~ P_f^-1,  Psi = (1/r) D_l G T^T P_f^-1 T,
+  //   W1 = (1/r) D_l G T^T P_f^-1 L~^T
+  Mat Zl, Wl, Psi;
+  if (literal) {
+    Mat Pfi;
+    if (!dense::inverse(P, nU, Pfi))
+      return fail(c, FDTD_E_ARG, "literal coupling: A1 is singular (the ROM's E basis must span the %d port "
+                  "directions; q1 = %d)", nU, q1);
+    Zl = dense::matmul(Bq, Pfi, q1, nU, nU);
+    Mat TtPfi = dense::zeros(nY, nU);  // (1/r) D_l G T^T P_f^-1
+    for (int k = 0; k < nU; ++k)
+      for (int j = 0; j < nU; ++j) TtPfi[(size_t)(k / rr) * nU + j] += DlGm[k / rr] / rr * Pfi[(size_t)k * nU + j];
+    Psi = dense::zeros(nY, nY);
+    for (int p = 0; p < nY; ++p)
+      for (int j = 0; j < nU; ++j) Psi[(size_t)p * nY + j / rr] += TtPfi[(size_t)p * nU + j];
+    Wl = dense::matmul(TtPfi, Lt, nY, nU, q1);
+    mh.P = Psi;
+  } else {
+    mh.P = P;
+  }
   auto push = [&](const Mat& A, int rows_, int cols_) {  // row-major host -> column-major pool
     while (c->mpool.size() % 4) c->mpool.push_back(0.0);   // 16-byte aligned operators (cp.async)
     const int64_t off = (int64_t)c->mpool.size();
@@ -946,30 +978,50 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
   for (auto& v : R11dt) v /= dt;
   for (auto& v : R22dt) v /= dt;
   // fused operators (K3): x = [E~; H~]
-  //   M1 = [[Q1, I], [Aq', Kq], [-Lt Aq', -Lt Kq]] with Aq' = Aq + Kq Q1;  M2 = [Bq; Lt Bq];  Rt = R~
+  //   collapsed: M1 = [[Q1, I], [Aq', Kq], [-Lt Aq', -Lt Kq]] with Aq' = Aq + Kq Q1;  M2 = [Bq; Lt Bq]
+  //   literal:   M1 = [[Q1, I], [(I - Z Lt)[Aq', Kq]], [W1 [Aq', Kq]]];             M2 = [Z T; I]
   const int nxs = q1 + q2, m1 = q2 + q1 + nY, m2 = q1 + nY;
   Mat Aqp = dense::matmul(Kq, Q1, q1, q2, q1);
   for (int i = 0; i < q1 * q1; ++i) Aqp[i] += Aq[i];
-  Mat LtAqp = dense::matmul(Lt, Aqp, nY, q1, q1);
-  Mat LtKq = dense::matmul(Lt, Kq, nY, q1, q2);
+  Mat EA = Aqp, EK = Kq, TA, TK;  // E* rows and t rows of M1
+  if (literal) {
+    Mat ZL = dense::matmul(Zl, Lt, q1, nU, q1);  // Z L~^T
+    for (int i = 0; i < q1; ++i)
+      for (int j = 0; j < q1; ++j) ZL[(size_t)i * q1 + j] = (i == j ? 1.0 : 0.0) - ZL[(size_t)i * q1 + j];
+    EA = dense::matmul(ZL, Aqp, q1, q1, q1);
+    EK = dense::matmul(ZL, Kq, q1, q1, q2);
+    TA = dense::matmul(Wl, Aqp, nY, q1, q1);
+    TK = dense::matmul(Wl, Kq, nY, q1, q2);
+  } else {
+    TA = dense::matmul(Lt, Aqp, nY, q1, q1);
+    TK = dense::matmul(Lt, Kq, nY, q1, q2);
+    for (auto& v : TA) v = -v;
+    for (auto& v : TK) v = -v;
+  }
   Mat M1 = dense::zeros(m1, nxs);
   for (int i = 0; i < q2; ++i) {
     for (int j = 0; j < q1; ++j) M1[(size_t)i * nxs + j] = Q1[(size_t)i * q1 + j];
     M1[(size_t)i * nxs + q1 + i] = 1.0;
   }
   for (int i = 0; i < q1; ++i) {
-    for (int j = 0; j < q1; ++j) M1[(size_t)(q2 + i) * nxs + j] = Aqp[(size_t)i * q1 + j];
-    for (int j = 0; j < q2; ++j) M1[(size_t)(q2 + i) * nxs + q1 + j] = Kq[(size_t)i * q2 + j];
+    for (int j = 0; j < q1; ++j) M1[(size_t)(q2 + i) * nxs + j] = EA[(size_t)i * q1 + j];
+    for (int j = 0; j < q2; ++j) M1[(size_t)(q2 + i) * nxs + q1 + j] = EK[(size_t)i * q2 + j];
   }
   for (int i = 0; i < nY; ++i) {
-    for (int j = 0; j < q1; ++j) M1[(size_t)(q2 + q1 + i) * nxs + j] = -LtAqp[(size_t)i * q1 + j];
-    for (int j = 0; j < q2; ++j) M1[(size_t)(q2 + q1 + i) * nxs + q1 + j] = -LtKq[(size_t)i * q2 + j];
+    for (int j = 0; j < q1; ++j) M1[(size_t)(q2 + q1 + i) * nxs + j] = TA[(size_t)i * q1 + j];
+    for (int j = 0; j < q2; ++j) M1[(size_t)(q2 + q1 + i) * nxs + q1 + j] = TK[(size_t)i * q2 + j];
   }
   Mat M2 = dense::zeros(m2, nY);
-  for (int i = 0; i < q1; ++i)
-    for (int j = 0; j < nY; ++j) M2[(size_t)i * nY + j] = Bq[(size_t)i * nY + j];
-  for (int i = 0; i < nY; ++i)
-    for (int j = 0; j < nY; ++j) M2[(size_t)(q1 + i) * nY + j] = P[(size_t)i * nY + j];
+  if (literal) {
+    for (int i = 0; i < q1; ++i)
+      for (int k = 0; k < nU; ++k) M2[(size_t)i * nY + k / rr] += Zl[(size_t)i * nU + k];  // Z T
+    for (int i = 0; i < nY; ++i) M2[(size_t)(q1 + i) * nY + i] = 1.0;
+  } else {
+    for (int i = 0; i < q1; ++i)
+      for (int j = 0; j < nY; ++j) M2[(size_t)i * nY + j] = Bq[(size_t)i * nY + j];
+    for (int i = 0; i < nY; ++i)
+      for (int j = 0; j < nY; ++j) M2[(size_t)(q1 + i) * nY + j] = P[(size_t)i * nY + j];
+  }
   Mat Rt = dense::zeros(nxs, nxs);
   for (int i = 0; i < q1; ++i)
     for (int j = 0; j < q1; ++j) Rt[(size_t)i * nxs + j] = R11dt[(size_t)i * q1 + j];
@@ -980,7 +1032,7 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
       Rt[(size_t)i * nxs + q1 + j] = -0.5 * K[(size_t)i * q2 + j];
       Rt[(size_t)(q1 + j) * nxs + i] = -0.5 * K[(size_t)i * q2 + j];
     }
-  mh.dev.nY = nY; mh.dev.q1 = q1; mh.dev.q2 = q2;
+  mh.dev.nY = nY; mh.dev.q1 = q1; mh.dev.q2 = q2; mh.dev.literal = literal ? 1 : 0;
   mh.dev.off_M1 = push(M1, m1, nxs);
   mh.dev.off_M2 = push(M2, m2, nY);
   mh.dev.off_Rt = push(Rt, nxs, nxs);
@@ -1014,16 +1066,22 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
     c->state_off.push_back(c->state_len);
     c->state_len += q;
     c->Sk_off.push_back((int64_t)c->Sk.size());
-    Mat A = P;
+    Mat A = mh.P;
     for (int p = 0; p < nY; ++p) {
       const bool isey = p >= 2 * bx;
       const double Dl = isey ? dy : dx, Dlp = isey ? dx / 2 : dy / 2;
       const double G = (p < bx) ? -1.0 : (p < 2 * bx) ? 1.0 : (p < 2 * bx + by) ? 1.0 : -1.0;
       const double eps = EPS0 * oe[k * nY + p], sig = os[k * nY + p];
       const double cy = Dl * Dlp * (eps / dt + sig / 2), ay = Dl * Dlp * (eps / dt - sig / 2);
-      A[(size_t)p * nY + p] += Dl * G / cy;
-      c->cya.push_back(ay / cy);
-      c->cyg.push_back(Dl * G / cy);
+      if (literal) {  // (diag(c_y) + Psi) y' = a_y y + D_l G h + W1 E*
+        A[(size_t)p * nY + p] += cy;
+        c->cya.push_back(ay);
+        c->cyg.push_back(Dl * G);
+      } else {        // (P + diag(D_l G / c_y)) U = (a_y/c_y) y + (D_l G/c_y) h - L~^T E*
+        A[(size_t)p * nY + p] += Dl * G / cy;
+        c->cya.push_back(ay / cy);
+        c->cyg.push_back(Dl * G / cy);
+      }
       c->ehalf.push_back(Dl * Dlp * eps / dt);
       int64_t e;
       if (p < bx) e = lrow(c, j0) * P_ + i0 + p;

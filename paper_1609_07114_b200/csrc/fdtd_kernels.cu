@@ -679,7 +679,7 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first
   }
   for (int64_t k = tid; k < (int64_t)m2 * B; k += nt) {
     const int64_t r = k / B;
-    v.so2[k] = r < q1 ? v.so[(q2 + r) * B + k % B] : -v.so[(q2 + r) * B + k % B];
+    v.so2[k] = r < q1 ? v.so[(q2 + r) * B + k % B] : (m.literal ? T(0) : -v.so[(q2 + r) * B + k % B]);
   }
   __syncthreads();
   // [E~^{n+1}; y^{n+1}] = [E*; L~^T E*] + M2 U

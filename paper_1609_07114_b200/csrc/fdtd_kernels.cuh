@@ -46,6 +46,7 @@ struct SweepParams {
 //   Rt ((q1 + q2) x (q1 + q2)) = [[R~11/dt, -K~/2], [-K~^T/2, R~22/dt]]  (storage function)
 struct RomModelDev {
   int nY, q1, q2;
+  int literal;  // paper-literal coupling: U is y^{n+1} itself and M2 = [Z T; I] (K3)
   int64_t off_M1, off_M2, off_Rt;
 };
 

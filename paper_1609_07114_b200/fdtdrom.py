@@ -42,7 +42,7 @@ class GridDesc(C.Structure):
 class RomModel(C.Structure):
     _fields_ = [("bx", C.c_int32), ("by", C.c_int32), ("r", C.c_int32), ("q1", C.c_int32), ("q2", C.c_int32),
                 ("R11", C.c_void_p), ("R22", C.c_void_p), ("F11", C.c_void_p), ("K", C.c_void_p),
-                ("L", C.c_void_p)]
+                ("L", C.c_void_p), ("literal", C.c_int32)]
 
 
 class Info(C.Structure):
@@ -221,7 +221,8 @@ class Simulation:
     def add_rom(self, model, anchors):
         R11, R22, F11, K, L = (_f64(model[k]) for k in ("R11", "R22", "F11", "K", "L"))
         m = RomModel(int(model["bx"]), int(model["by"]), int(model.get("r", 1)), R11.shape[0], R22.shape[0],
-                     R11.ctypes.data, R22.ctypes.data, F11.ctypes.data, K.ctypes.data, L.ctypes.data)
+                     R11.ctypes.data, R22.ctypes.data, F11.ctypes.data, K.ctypes.data, L.ctypes.data,
+                     1 if model.get("literal", False) else 0)
         a = np.ascontiguousarray(np.asarray(anchors, dtype=np.int32).reshape(-1, 2))
         mid = C.c_int32(-1)
         self._ck(lib().fdtd_add_rom(self._h, C.byref(m), _ptr(a), a.shape[0], C.byref(mid)), "fdtd_add_rom")

@@ -75,7 +75,9 @@ def consistent_random_state(scene, seed, lossless_scale=1.0):
         Ey[j0:j0 + by, i0 + 1:i0 + bx] = 0
         xt = rng.standard_normal(q1 + q2)
         xt[q1:] /= 377.0
-        y = m["L"].T @ xt[:q1]
+        if m.get("literal", False):  # T y = L~^T E~ would constrain E~; start the ROM at rest
+            xt[:] = 0.0
+        y = (m["L"].T @ xt[:q1])[: 2 * bx + 2 * by]
         Ex[j0, i0:i0 + bx] = y[:bx]
         Ex[j0 + by, i0:i0 + bx] = y[bx:2 * bx]
         Ey[j0:j0 + by, i0] = y[2 * bx:2 * bx + by]

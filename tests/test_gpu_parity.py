@@ -265,3 +265,51 @@ def test_large_rom_order_unstaged_operators(precision):
     for o in outs[1:]:
         for a, b in zip(outs[0], o):
             assert np.array_equal(a, b)
+
+
+# ----------------------------------------------------------------- paper-literal coupling (NEXT-1)
+def test_cfg1_literal_fp64():
+    """Config 1 with the paper's own nP-port coupling (eq:sysform with T and 1/r; nP = 80, q1 = 92):
+    the factored GPU update matches the oracle's LU of the literal A1 to 1e-10 over 4000 steps."""
+    s = configs.make("cfg1lit")
+    assert s.models[0]["literal"] and s.models[0]["L"].shape[1] == 80
+    _compare(s, s.steps, 1e-10)
+
+
+def _literal_scene(precision, n=128, seed=21):
+    rng = np.random.default_rng(seed)
+    dx = dy = 1e-3
+    fe, fs = sc.uniform_fill(4, 4, 3, seed, 1, 4, 0, 0.05)
+    m = rg.build_rom(4, 4, 3, dx, dy, fe, fs, 16, 30e9, literal=True)   # nP = 48, q1 = 56, q2 = 8
+    dt = 0.95 * m["fine_dt_limit"]
+    P = sc.place_blocks(n, n, [(4, 4)], 12, seed=seed, nslabs=1)
+    return sc.Scene(name="literal", nx=n, ny=n, dx=dx, dy=dy, dt=dt, eps_r=rng.uniform(1, 3, (n, n)),
+                    sigma=rng.uniform(0, 0.05, (n, n)), precision=precision, steps=1000, source=(n // 2, n // 2),
+                    samples=sc.gaussian_samples(1000, dt, 30e9, True),
+                    probes=np.array([[5, 9], [n - 7, n - 12]], np.int32), models=[m], placements=P)
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_literal_rom_instances_parity(precision):
+    """12 literal ROM instances in a lossy medium: <= 1e-10 (fp64) / 1e-4 (fp32) vs the oracle."""
+    s = _literal_scene(precision)
+    _compare(s, 1000, 1e-10 if precision == 64 else 1e-4, random_init=5)
+
+
+def test_literal_rom_k_step_bitwise():
+    """K = 1, 2, 4 steps per pass agree bit for bit with literal ROMs (fix-up with the literal update)."""
+    s = _literal_scene(32)
+    outs = []
+    for spp in (1, 2, 4):
+        g = gpu_from_scene(s)
+        g.set_time_blocking(spp)
+        Ex, Ey, Hz, xs = consistent_random_state(s, 8)
+        g.set_window(0, 0, Ex, Ey, Hz)
+        g.set_rom_state(xs)
+        g.step(203)
+        assert g.info().steps_per_pass == spp
+        outs.append(g.get_window() + (g.get_rom_state(), g.probe()))
+        g.close()
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)

@@ -371,3 +371,65 @@ def test_rom_converges_to_subgridding_as_q_grows():
         errs.append(np.linalg.norm(p - ref) / np.linalg.norm(ref))
     assert errs[0] > errs[1] > errs[2]
     assert errs[2] < 1e-2, errs
+
+
+# ----------------------------------------------------------------- paper-literal coupling (NEXT-1)
+@pytest.mark.parametrize("r", [2, 3])
+def test_literal_full_order_rom_equals_direct_subgridding(r):
+    """The paper's own coupling (eq:sysform with T and 1/r, nP = r nY fine hanging variables) at
+    full order reproduces the brute-force subgridded solution (1.2e-15)."""
+    rng, nx, ny, dx, dy, eps, sig = _scene(3)
+    i0, j0, bx, by = 3, 3, 3, 2
+    fe, fs = rng.uniform(1, 4, (by * r, bx * r)), rng.uniform(0, 0.05, (by * r, bx * r))
+    dt = 0.9 / (C0 * math.sqrt(1 / (dx / r) ** 2 + 1 / (dy / r) ** 2))
+    m = rg.build_rom(bx, by, r, dx, dy, fe, fs, 0, 1e10, full=True, literal=True)
+    assert m["literal"] and m["L"].shape[1] == r * (2 * bx + 2 * by)
+    b = O.OracleSim(nx, ny, dx, dy, dt, eps, sig)
+    b.add_rom(m, i0, j0)
+    pb, sb, _ = _run(b, 1500)
+    g = O.OracleSim(nx, ny, dx, dy, dt, eps, sig)
+    g.add_subgrid(i0, j0, bx, by, r, fe, fs)
+    pg, sg, _ = _run(g, 1500)
+    assert np.abs(pb - pg).max() <= 1e-12 * np.abs(pg).max()
+    for x, y in zip(sb[:3], sg[:3]):
+        assert np.abs(x - y).max() <= 1e-12 * np.abs(y).max()
+
+
+def test_literal_coupling_singular_below_port_count():
+    """SURVEY finding 1 / DESIGN R9: the literal A1 is singular when the ROM's E basis does not span
+    the nP port directions (q1 < nP); with the port directions in the basis it is regular."""
+    r, bx, by = 3, 3, 3
+    nY, nP = 2 * bx + 2 * by, 3 * (2 * bx + 2 * by)
+    rng, nx, ny, dx, dy, eps, sig = _scene(5, nx=12, ny=12)
+    fe, fs = rng.uniform(1, 4, (by * r, bx * r)), np.zeros((by * r, bx * r))
+    dt = 0.9 / (C0 * math.sqrt(1 / (dx / r) ** 2 + 1 / (dy / r) ** 2))
+    lsys = rg.literal_system(rg.fine_system(bx, by, r, dx, dy, fe, fs))
+    V1, V2 = rg.sprim_basis(lsys, 24, 30e9)
+    bad = rg.reduce(lsys, V1, V2)                        # q1 = 12 < nP = 36
+    assert bad["q1"] < nP and bad["literal"]
+    o = O.OracleSim(nx, ny, dx, dy, dt, eps, sig)
+    with pytest.raises(ValueError):
+        o.add_rom(bad, 4, 4)
+    good = rg.build_rom(bx, by, r, dx, dy, fe, fs, 24, 30e9, literal=True)
+    assert good["q1"] >= nP
+    O.OracleSim(nx, ny, dx, dy, dt, eps, sig).add_rom(good, 4, 4)
+
+
+def test_literal_reduced_rom_energy_conserved():
+    """Lossless scene with a reduced literal ROM (q1 >= nP): the storage function is conserved."""
+    rng, nx, ny, dx, dy, eps, sig = _scene(6)
+    r, i0, j0, bx, by = 2, 3, 3, 3, 2
+    fe = rng.uniform(1, 4, (by * r, bx * r))
+    dt = 0.9 / (C0 * math.sqrt(1 / (dx / r) ** 2 + 1 / (dy / r) ** 2))
+    m = rg.build_rom(bx, by, r, dx, dy, fe, 0 * fe, 48, 30e9, literal=True)
+    s = O.OracleSim(nx, ny, dx, dy, dt, eps, 0 * sig)
+    s.add_rom(m, i0, j0)
+    Ex = rng.standard_normal((ny + 1, nx)); Ey = rng.standard_normal((ny, nx + 1))
+    Hz = rng.standard_normal((ny, nx)) / 377.0
+    Ex[0] = Ex[ny] = 0; Ey[:, 0] = Ey[:, nx] = 0
+    Hz[j0:j0 + by, i0:i0 + bx] = 0                       # hole; interface y = 0 = L~^T 0 (R26)
+    Ex[j0:j0 + by + 1, i0:i0 + bx] = 0
+    Ey[j0:j0 + by, i0:i0 + bx + 1] = 0
+    s.set_state(Ex, Ey, Hz, np.zeros(m["q1"] + m["q2"]))
+    _, en = s.step(1500, probes=False)
+    assert np.abs(en - en[0]).max() <= 1e-11 * en[0]
