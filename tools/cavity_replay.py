@@ -5,7 +5,9 @@ cells, R14) refined r = 5 (N^ = 50, full order 7,600, L840) reduced to
 (q1 = q2 = 600) with SPRIM at f_max = 0.5 GHz, CFL limit extended 2x by the clip (L840), run at
 1.98 x the fine-grid limit (L842 "1.98%" = 1.98x), empty (vacuum) cavity, Gaussian pulse of
 0.5 GHz bandwidth at (0.089, 0.089) m, probe at (0.933, 0.933) m (read off the schematic TikZ,
-L776-779), 10^6 steps in fp64.  Coupling: the collapsed reading R9.
+L776-779), 10^6 steps in fp64.  Coupling: the collapsed reading R9, or with --literal the paper's own
+eq:sysform through the nP = 200 fine hanging variables (T, 1/r; NEXT-1): the E basis holds the 200
+port directions plus 500 SPRIM directions, q1 = 700, q2 = 500 (order 1,200 as in L840).
 
 Reports: the fp64 parity of the first `--check` steps against the oracle, the boundedness of the
 probe (max over the last 10 % vs the first 10 %, SPEC.md criterion 6), the storage-function drift
@@ -28,7 +30,7 @@ from inputs import romgen as rg  # noqa: E402
 from inputs import scene as sc  # noqa: E402
 
 
-def build(steps):
+def build(steps, literal=False):
     nx = ny = 500
     dx = dy = 2e-3
     b, r = 10, 5
@@ -37,8 +39,13 @@ def build(steps):
     fs = np.zeros_like(fe)
     sysf = rg.fine_system(b, b, r, dx, dy, fe, fs)
     assert rg.full_order(sysf) == 7600
-    cs = rg.collapse(sysf)
-    V1, V2 = rg.sprim_basis(cs, 1200, 0.5e9)
+    if literal:
+        cs = rg.literal_system(sysf)
+        V1, V2 = rg.sprim_basis(cs, 1000, 0.5e9)
+        V1 = rg.with_port_directions(V1, cs["nY"])[:, : cs["nY"] + 500]
+    else:
+        cs = rg.collapse(sysf)
+        V1, V2 = rg.sprim_basis(cs, 1200, 0.5e9)
     m = rg.reduce(cs, V1, V2)
     dtf = rg.fine_cfl_limit(sysf)
     m["natural_dt_limit"] = rg.rom_cfl_limit(m)
@@ -58,15 +65,18 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=1_000_000)
     ap.add_argument("--check", type=int, default=2000)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_cavity_replay.json"))
+    ap.add_argument("--literal", action="store_true")
+    ap.add_argument("--out", default=None)
     args = ap.parse_args()
+    if args.out is None:
+        args.out = os.path.join(ROOT, "profiles", "r01_cavity_replay%s.json" % ("_literal" if args.literal else ""))
     import torch
 
     import oracle as O
     from paper_1609_07114_b200 import Simulation
 
     t0 = time.time()
-    s = build(args.steps)
+    s = build(args.steps, args.literal)
     t_build = time.time() - t0
     m = s.models[0]
     sim = Simulation(s.nx, s.ny, s.dx, s.dy, s.dt, s.eps_r, s.sigma, precision=64,
@@ -115,7 +125,8 @@ def main():
     k_off = int(np.ceil((4.5 * tau + 6 * tau) / s.dt))
     e_after = e[k_off:] if k_off < len(e) else e[-1:]
     out = dict(
-        experiment="PAPER.md Sec. VI-A cavity (Fig. 4), collapsed coupling (R9)",
+        experiment="PAPER.md Sec. VI-A cavity (Fig. 4), %s" % (
+            "paper-literal coupling (eq:sysform with T, 1/r; nP = 200)" if args.literal else "collapsed coupling (R9)"),
         grid=[s.nx, s.ny], dx=s.dx, block=[245, 245, 10, 10], r=5, full_order=7600,
         reduced_order=int(m["q1"] + m["q2"]), q1q2=[int(m["q1"]), int(m["q2"])],
         dt=s.dt, dt_over_fine_limit=s.dt / s.meta["dt_f"], natural_rom_limit_over_fine=m["natural_dt_limit"] /
