@@ -114,7 +114,7 @@ struct fdtd_ctx {
   // kz the depth in use (agreed over ranks; the zone marks in msb are for kz)
   int k_want = 4, k_ok = 1, kz = 1, kz_marked = 1;
   bool kz_dirty = true;
-  int region_stride = 4;
+  size_t post_smem = 0;  // dynamic shared memory of the fix-up launch
   int32_t* d_rects = nullptr;
   std::vector<int32_t> zp_off, zp;  // zone probes per instance (gi, gj, probe index)
   int32_t* d_zp_off = nullptr;
@@ -126,8 +126,7 @@ struct fdtd_ctx {
   std::vector<double> cya, cyg, ehalf, Sk;  // fp64 host copies (converted on upload)
   std::vector<double> mpool;                // shared model matrices (col-major, fp64)
   int nvec = 1;
-  int rom_batch = 16;
-  std::vector<int32_t> batch_tab;  // (model, first instance, count)
+  std::vector<int32_t> batch_tab;  // (model, first instance, count, slots B, region stride)
   int32_t* d_batch_tab = nullptr;
   int post_grid = 1;
   // device ROM arrays
@@ -285,12 +284,10 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q, int K) {
   p.level1 = c->d_level1;
   p.energy_ring = c->d_energy_ring;
   p.step = c->d_step; p.done = c->d_done;
-  p.nthreads_vec = c->nvec;
-  p.n_batch = (int)(c->batch_tab.size() / 3);
-  p.batch = c->rom_batch;
+  p.n_batch = c->inst_model.empty() ? 0 : (int)(c->batch_tab.size() / 5);
   p.batch_tab = c->d_batch_tab;
   p.block = 256;
-  p.region_stride = c->region_stride;
+  p.smem_bytes = c->post_smem;
   return p;
 }
 
@@ -611,26 +608,41 @@ fdtd_status apply_passes(fdtd_ctx* c, int k) {
   }
   c->kz_marked = k;
   c->kz = k;
-  // batches of consecutive instances of one model (instances are stored grouped by model); the
-  // batch size keeps the fix-up kernel at <= ~200 KB of shared memory
+  // batches of consecutive instances of one model (instances are stored grouped by model).  Every
+  // model gets its own region stride and batch size under one shared-memory budget per CTA
+  // (~100 KB: two fix-up CTAs per SM), so small models are batched 8 at a time and the largest
+  // still fits; the launch uses the largest batch footprint.
   {
-    int rs = 4;
-    for (auto& m : c->models) rs = std::max(rs, fdtd::region_elems(m.bx, m.by, 2 * k - 1));
-    c->region_stride = (rs + 3) / 4 * 4;
     const char* env = getenv("FDTD_ROM_BATCH");
-    int B = env ? std::max(1, std::min(64, atoi(env))) : 8;
-    while (B > 1 && fdtd::post_smem_bytes(c->es, c->nvec, B, c->region_stride) > 200 * 1024) B = B > 4 ? B - 4 : B / 2;
-    c->rom_batch = B;
+    const int Bmax = env ? std::max(1, std::min(64, atoi(env))) : 8;
+    const size_t budget = 100 * 1024;
+    struct Shape { int B, stride; size_t per; };
+    std::vector<Shape> shp;
+    size_t need1 = 0;
+    for (auto& m : c->models) {
+      const int rs = (fdtd::region_elems(m.bx, m.by, 2 * k - 1) + 3) / 4 * 4;
+      const size_t per = fdtd::post_smem_bytes(c->es, m.q1 + m.q2 + m.nY, 1, rs);
+      shp.push_back({1, rs, per});
+      need1 = std::max(need1, per);
+    }
+    const size_t cap = std::max(budget, need1);
+    c->post_smem = 16;
+    for (auto& x : shp) {
+      x.B = (int)std::max<size_t>(1, std::min<size_t>(Bmax, cap / x.per));
+      c->post_smem = std::max(c->post_smem, x.B * x.per);
+    }
     c->batch_tab.clear();
     const int n = (int)c->inst_model.size();
     for (int i = 0; i < n;) {
+      const Shape& x = shp[c->inst_model[i]];
       int e = i;
-      while (e < n && e - i < B && c->inst_model[e] == c->inst_model[i]) ++e;
-      c->batch_tab.insert(c->batch_tab.end(), {c->inst_model[i], i, e - i});
+      while (e < n && e - i < x.B && c->inst_model[e] == c->inst_model[i]) ++e;
+      c->batch_tab.insert(c->batch_tab.end(), {c->inst_model[i], i, e - i, x.B, x.stride});
       i = e;
     }
+    if (c->batch_tab.empty()) c->batch_tab.assign(5, 0);
     if ((st = upload(c, &c->d_batch_tab, c->batch_tab)) != FDTD_OK) return st;
-    c->post_grid = std::max<int>(1, (int)(c->batch_tab.size() / 3));
+    c->post_grid = n > 0 ? (int)(c->batch_tab.size() / 5) : 1;
     std::vector<double> l1((size_t)KMAX * c->post_grid, 0.0);
     if ((st = upload(c, &c->d_level1, l1)) != FDTD_OK) return st;
   }
@@ -1033,9 +1045,16 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
       Rt[(size_t)(q1 + j) * nxs + i] = -0.5 * K[(size_t)i * q2 + j];
     }
   mh.dev.nY = nY; mh.dev.q1 = q1; mh.dev.q2 = q2; mh.dev.literal = literal ? 1 : 0;
-  mh.dev.off_M1 = push(M1, m1, nxs);
+  {  // [M1; R~] as one column-major operator (the kernel's first GEMM phase also yields R~ x~)
+    Mat M1R = dense::zeros(m1 + nxs, nxs);
+    for (int i = 0; i < m1; ++i)
+      for (int j = 0; j < nxs; ++j) M1R[(size_t)i * nxs + j] = M1[(size_t)i * nxs + j];
+    for (int i = 0; i < nxs; ++i)
+      for (int j = 0; j < nxs; ++j) M1R[(size_t)(m1 + i) * nxs + j] = Rt[(size_t)i * nxs + j];
+    mh.dev.off_M1 = push(M1R, m1 + nxs, nxs);
+  }
   mh.dev.off_M2 = push(M2, m2, nY);
-  mh.dev.off_Rt = push(Rt, nxs, nxs);
+  mh.dev.off_Rt = mh.dev.off_M1 + m1;
   const int mid = (int)c->models.size();
   c->models.push_back(mh);
   c->nvec = std::max(c->nvec, q1 + q2 + nY);

@@ -589,7 +589,8 @@ __device__ double block_sum(double v, double* red) {
 // (column-major, L2-resident: one coalesced 128-byte row of A per warp and column, reused for the
 // IPI instances of a thread's item); X, Y in shared memory with row stride B.
 template <typename T, int IPI>
-__device__ __forceinline__ void bgemm_ipi(const T* __restrict__ A, int m, int k, const T* X, T* Y, int B, T alpha) {
+__device__ __forceinline__ void bgemm_ipi(const T* __restrict__ A, int m, int lda, int k, const T* X, T* Y, int B,
+                                          T alpha) {
   const int G = B / IPI;
   for (int it = threadIdx.x; it < m * G; it += blockDim.x) {
     const int i = it % m, g = (it / m) * IPI;
@@ -598,7 +599,7 @@ __device__ __forceinline__ void bgemm_ipi(const T* __restrict__ A, int m, int k,
     for (int u = 0; u < IPI; ++u) acc[u] = T(0);
 #pragma unroll 16
     for (int c = 0; c < k; ++c) {
-      const T a = __ldg(A + (int64_t)c * m + i);
+      const T a = __ldg(A + (int64_t)c * lda + i);
       const T* x = X + c * B + g;
 #pragma unroll
       for (int u = 0; u < IPI; ++u) acc[u] = fma_rn(a, x[u], acc[u]);
@@ -610,20 +611,21 @@ __device__ __forceinline__ void bgemm_ipi(const T* __restrict__ A, int m, int k,
 }
 
 template <typename T>
-__device__ __forceinline__ void bgemm(const T* A, int m, int k, const T* X, T* Y, int B, T alpha) {
-  if (m * (B / 4) >= (int)blockDim.x) bgemm_ipi<T, 4>(A, m, k, X, Y, B, alpha);
-  else if (m * (B / 2) >= (int)blockDim.x) bgemm_ipi<T, 2>(A, m, k, X, Y, B, alpha);
-  else bgemm_ipi<T, 1>(A, m, k, X, Y, B, alpha);
+__device__ __forceinline__ void bgemm(const T* A, int m, int lda, int k, const T* X, T* Y, int B, T alpha) {
+  if (m * (B / 4) >= (int)blockDim.x) bgemm_ipi<T, 4>(A, m, lda, k, X, Y, B, alpha);
+  else if (m * (B / 2) >= (int)blockDim.x) bgemm_ipi<T, 2>(A, m, lda, k, X, Y, B, alpha);
+  else bgemm_ipi<T, 1>(A, m, lda, k, X, Y, B, alpha);
 }
 
 // Shared-memory vectors of a batch (row stride B, NV rows each):
-//   sx = [E~; H~] (q1 + q2), sy = y (nY), sh = h (nY), so = M1 x (q2 + q1 + nY),
-//   st = t (nY), sU = U (nY), so2 = [E~; y] (q1 + nY)
+//   sx = [E~; H~] (q1 + q2), sy = y (nY), sh = h (nY), so = [M1; R~] x (q2 + q1 + nY + q1 + q2, two
+//   slots), st = t (nY), sU = U (nY), so2 = [E~; y] (q1 + nY)
+constexpr int NROMVEC = 8;  // vector slots of one batch (stride S = (q1 + q2 + nY) x B each)
 template <typename T>
 struct RomVec {
   T *sx, *sy, *sh, *so, *st, *sU, *so2;
-  __device__ RomVec(T* sv, int64_t S) : sx(sv), sy(sv + S), sh(sv + 2 * S), so(sv + 3 * S), st(sv + 4 * S),
-                                         sU(sv + 5 * S), so2(sv + 6 * S) {}
+  __device__ RomVec(T* sv, int64_t S) : sx(sv), sy(sv + S), sh(sv + 2 * S), so(sv + 3 * S), st(sv + 5 * S),
+                                         sU(sv + 6 * S), so2(sv + 7 * S) {}
 };
 
 // One ROM step for a batch of nb (<= B) instances of one model (eq:connExplicit, K3).
@@ -631,35 +633,31 @@ struct RomVec {
 // (zero padding for b >= nb).  On exit sx holds x~^{n+1} and sy holds y^{n+1}; with ENERGY the ROM
 // part of W^n (coarse half cells + x~^T R~ x~) of instance b is in eout[b].
 template <typename T, bool ENERGY>
-__device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first, int nb, T* sv, double* eout) {
+__device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first, int nb, int B, int64_t S, T* sv,
+                         double* eout) {
   const int nY = m.nY, q1 = m.q1, q2 = m.q2, nx = q1 + q2, m1 = q2 + q1 + nY, m2 = q1 + nY;
-  const int B = p.batch;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int64_t S = (int64_t)p.nthreads_vec * B;
   RomVec<T> v(sv, S);
   const T* mp = p.mpool;
-  for (int64_t k = tid; k < S; k += nt) { v.so[k] = T(0); v.so2[k] = T(0); }
+  for (int64_t k = tid; k < 2 * S; k += nt) v.so[k] = T(0);
+  for (int64_t k = tid; k < S; k += nt) v.so2[k] = T(0);
   __syncthreads();
-  if (ENERGY) {  // x~^T Rt x~ + sum D_l D_l' eps/dt y^2
-    bgemm<T>(mp + m.off_Rt, nx, nx, v.sx, v.so, B, T(1));
-    __syncthreads();
+  // [H~^{n+1}; E*; -L~^T E*] = M1 x~^n, and with ENERGY also R~ x~^n (R~ is stored after M1 as
+  // q1 + q2 further rows of the same column-major operator: one GEMM phase)
+  bgemm<T>(mp + m.off_M1, ENERGY ? m1 + nx : m1, m1 + nx, nx, v.sx, v.so, B, T(1));
+  __syncthreads();
+  if (ENERGY) {  // x~^T R~ x~ + sum D_l D_l' eps/dt y^2 (storage function, R17)
     const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
     for (int b = w; b < nb; b += nw) {
       const int64_t po = p.port_off[first + b];
       double acc = 0.0;
       for (int i = lane; i < nY; i += 32) acc += p.ehalf[po + i] * (double)v.sy[i * B + b] * (double)v.sy[i * B + b];
-      for (int i = lane; i < nx; i += 32) acc += (double)v.sx[i * B + b] * (double)v.so[i * B + b];
+      for (int i = lane; i < nx; i += 32) acc += (double)v.sx[i * B + b] * (double)v.so[(m1 + i) * B + b];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
       if (lane == 0) eout[b] = acc;
     }
-    __syncthreads();
-    for (int64_t k = tid; k < S; k += nt) v.so[k] = T(0);
-    __syncthreads();
   }
-  // [H~^{n+1}; E*; -L~^T E*] = M1 x~^n
-  bgemm<T>(mp + m.off_M1, m1, nx, v.sx, v.so, B, T(1));
-  __syncthreads();
   // t = (a_y/c_y) y + (D_l G/c_y) h - L~^T E*
   for (int it = tid; it < nY * nb; it += nt) {
     const int i = it % nY, b = it / nY;
@@ -683,7 +681,7 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first
   }
   __syncthreads();
   // [E~^{n+1}; y^{n+1}] = [E*; L~^T E*] + M2 U
-  bgemm<T>(mp + m.off_M2, m2, nY, v.sU, v.so2, B, T(1));
+  bgemm<T>(mp + m.off_M2, m2, m2, nY, v.sU, v.so2, B, T(1));
   __syncthreads();
   for (int64_t k = tid; k < (int64_t)nx * B; k += nt) {
     const int64_t r = k / B;
@@ -694,13 +692,12 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first
 }
 
 template <typename T>
-__device__ __forceinline__ T* rom_end(const PostParams<T>& p, T* sv) {
-  return sv + 7 * (int64_t)p.nthreads_vec * p.batch;  // first free element after the ROM vectors
+__device__ __forceinline__ T* rom_end(T* sv, int64_t S) {
+  return sv + NROMVEC * S;  // first free element after the ROM vectors
 }
 
 template <typename T>
-__device__ void load_rom_state(const PostParams<T>& p, const RomModelDev& m, int first, int nb, T* sv) {
-  const int B = p.batch;
+__device__ void load_rom_state(const PostParams<T>& p, const RomModelDev& m, int first, int nb, int B, T* sv) {
   T* sx = sv;
   const int nx = m.q1 + m.q2;
   for (int it = threadIdx.x; it < nx * nb; it += blockDim.x) {
@@ -710,10 +707,8 @@ __device__ void load_rom_state(const PostParams<T>& p, const RomModelDev& m, int
 }
 
 template <typename T>
-__device__ void store_rom(const PostParams<T>& p, const RomModelDev& m, int first, int nb, const T* sv, T* ex,
-                          T* ey) {
-  const int B = p.batch;
-  const int64_t S = (int64_t)p.nthreads_vec * B;
+__device__ void store_rom(const PostParams<T>& p, const RomModelDev& m, int first, int nb, int B, int64_t S,
+                          const T* sv, T* ex, T* ey) {
   const T* sx = sv;
   const T* sy = sv + S;
   for (int it = threadIdx.x; it < m.nY * nb; it += blockDim.x) {  // S6: scatter y^{n+1}
@@ -741,12 +736,13 @@ __device__ void store_rom(const PostParams<T>& p, const RomModelDev& m, int firs
 // recorded here for every step of the pass.
 template <typename T, int K, bool ENERGY>
 __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[K], int64_t step, double* zsum) {
-  const int model = p.batch_tab[3 * bi], first = p.batch_tab[3 * bi + 1], nb = p.batch_tab[3 * bi + 2];
+  const int* bt = p.batch_tab + 5 * bi;  // (model, first instance, count, slots B, region stride)
+  const int model = bt[0], first = bt[1], nb = bt[2], B = bt[3], rstride = bt[4];
   const RomModelDev m = p.models[model];
-  const int B = p.batch, nY = m.nY;
-  const int64_t S = (int64_t)p.nthreads_vec * B;
+  const int nY = m.nY;
+  const int64_t S = (int64_t)(m.q1 + m.q2 + nY) * B;  // vector stride of this batch's layout
   const int tid = threadIdx.x, nt = blockDim.x;
-  T* reg = rom_end(p, sv);
+  T* reg = rom_end(sv, S);
   const int Kz = p.Kz, M = Kz + K - 1;
   const int64_t P = p.pitch;
   for (int64_t k = tid; k < 7 * S; k += nt) sv[k] = T(0);
@@ -767,7 +763,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       q.zu0 = q.zu1 = q.zv0 = q.zv1 = 0;
     }
     const int n = q.Hr * q.Wr;
-    q.H = reg + (int64_t)b * p.region_stride;
+    q.H = reg + (int64_t)b * rstride;
     q.MA = q.H + n; q.MS = q.MA + n; q.ZE = q.MS + n; q.EX = q.ZE + n; q.EY = q.EX + n + q.Wr;
     return q;
   };
@@ -789,7 +785,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     for (int t = tid; t < q.Hr * (q.Wr + 1); t += nt)
       cp_async_el(q.EY + t, p.ey0 + goff(q, t % (q.Wr + 1), t / (q.Wr + 1)));
   }
-  load_rom_state(p, m, first, nb, sv);
+  load_rom_state(p, m, first, nb, B, sv);
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
 #pragma unroll 1
@@ -859,7 +855,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     __syncthreads();
     // ---- S5: ROM step n+s -> y^{n+s+1}, x~^{n+s+1}; ROM energy of W^{n+s}
     double* eout = p.rom_partials + (int64_t)s * p.n_inst + first;
-    rom_step<T, ENERGY>(p, m, first, nb, sv, eout);
+    rom_step<T, ENERGY>(p, m, first, nb, B, S, sv, eout);
     if (ENERGY && tid < nb) eout[tid] += zsum[tid];
     // ---- E half-step on the region's interior edges (frozen edges keep their value)
     for (int b = 0; b < nb; ++b) {
@@ -909,7 +905,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       p.ey1[o] = q.EY[v * (q.Wr + 1) + u];
     }
   }
-  store_rom(p, m, first, nb, sv, p.ex1, p.ey1);
+  store_rom(p, m, first, nb, B, S, sv, p.ex1, p.ey1);
 }
 
 template <typename T, int K, bool ENERGY>
@@ -941,7 +937,7 @@ __global__ void __launch_bounds__(256) postk_kernel(const PostParams<T> p) {
       double v = 0.0;
       for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) v += __ldcg(p.sweep_partials + s * p.pstride + k);
       if (b < p.n_batch) {
-        const int first = p.batch_tab[3 * b + 1], nb = p.batch_tab[3 * b + 2];
+        const int first = p.batch_tab[5 * b + 1], nb = p.batch_tab[5 * b + 2];
         for (int k = threadIdx.x; k < nb; k += blockDim.x) v += p.rom_partials[(int64_t)s * p.n_inst + first + k];
       }
       const double tot = block_sum(v, red);
@@ -1110,12 +1106,12 @@ void launch_sweep(const SweepParams<T>& p, int K, int warps_per_cta, cudaStream_
 }
 
 size_t post_smem_bytes(size_t es, int nvec, int batch, int region_stride) {
-  return es * ((size_t)7 * nvec * batch + (size_t)batch * region_stride);
+  return es * ((size_t)NROMVEC * nvec * batch + (size_t)batch * region_stride);
 }
 
 template <typename T, int K>
 void postk_launch(const PostParams<T>& p, bool energy, cudaStream_t s) {
-  const size_t smem = post_smem_bytes(sizeof(T), p.nthreads_vec, p.batch, p.region_stride);
+  const size_t smem = p.smem_bytes;
   const int grid = p.n_batch > 0 ? p.n_batch : 1;
   if (energy) {
     if (smem > 48 * 1024)

@@ -59,8 +59,7 @@ template <typename T>
 struct PostParams {
   int n_inst;
   int n_batch;                     // CTAs doing ROM work; batches of <= batch instances of one model
-  int batch;                       // instances per batch (multiple of 4)
-  const int32_t* batch_tab;        // per batch: (model, first instance, count)
+  const int32_t* batch_tab;        // per batch: (model, first instance, count, slots B, region stride)
   const RomModelDev* models;
   const T* mpool;                  // shared model matrices (column-major)
   const T* Sk; const int64_t* Sk_off;        // per-instance Schur inverses (col-major nY x nY)
@@ -85,9 +84,8 @@ struct PostParams {
   double* level1;                  // [s * gridDim.x + cta]
   double* energy_ring;             // W^n per step (fp64 ring of cap entries)
   int64_t* step; unsigned int* done;
-  int nthreads_vec;  // max(q1 + q2 + nY) over models: shared-memory vector stride
   int block;         // threads per CTA
-  int region_stride; // shared-memory elements per instance region
+  size_t smem_bytes; // dynamic shared memory of the launch (max over batches)
 };
 
 template <typename T>
