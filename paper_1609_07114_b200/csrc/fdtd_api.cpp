@@ -610,12 +610,12 @@ fdtd_status apply_passes(fdtd_ctx* c, int k) {
   c->kz = k;
   // batches of consecutive instances of one model (instances are stored grouped by model).  Every
   // model gets its own region stride and batch size under one shared-memory budget per CTA
-  // (~100 KB: two fix-up CTAs per SM), so small models are batched 8 at a time and the largest
+  // (~110 KB: two fix-up CTAs per SM), so small models are batched 8 at a time and the largest
   // still fits; the launch uses the largest batch footprint.
   {
     const char* env = getenv("FDTD_ROM_BATCH");
     const int Bmax = env ? std::max(1, std::min(64, atoi(env))) : 8;
-    const size_t budget = 100 * 1024;
+    const size_t budget = 110 * 1024;
     struct Shape { int B, stride; size_t per; };
     std::vector<Shape> shp;
     size_t need1 = 0;
