@@ -115,6 +115,7 @@ struct fdtd_ctx {
   int k_want = 4, k_ok = 1, kz = 1, kz_marked = 1;
   bool kz_dirty = true;
   size_t post_smem = 0;  // dynamic shared memory of the fix-up launch
+  int post_threads = 256;
   int32_t* d_rects = nullptr;
   std::vector<int32_t> zp_off, zp;  // zone probes per instance (gi, gj, probe index)
   int32_t* d_zp_off = nullptr;
@@ -286,7 +287,7 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q, int K) {
   p.step = c->d_step; p.done = c->d_done;
   p.n_batch = c->inst_model.empty() ? 0 : (int)(c->batch_tab.size() / 5);
   p.batch_tab = c->d_batch_tab;
-  p.block = 256;
+  p.block = c->post_threads;
   p.smem_bytes = c->post_smem;
   return p;
 }
@@ -836,6 +837,7 @@ fdtd_status fdtd_set_tuning(fdtd_ctx* c, int32_t rows_per_cta, int32_t warps_per
     if (const char* e = getenv("FDTD_CHUNK")) c->chunk = std::max(1, atoi(e));  // tuning experiments
   if (!warps_per_cta)
     if (const char* e = getenv("FDTD_WARPS")) c->warps = std::max(1, std::min(8, atoi(e)));
+  if (const char* e = getenv("FDTD_POST_THREADS")) c->post_threads = std::max(64, std::min(512, atoi(e) / 32 * 32));
   const int gx = sweep_gx_max(c);
   const int gy = (c->rows + c->chunk - 1) / c->chunk;
   const int n = gx * gy;

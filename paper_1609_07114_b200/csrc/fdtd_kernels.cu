@@ -909,7 +909,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
 }
 
 template <typename T, int K, bool ENERGY>
-__global__ void __launch_bounds__(256) postk_kernel(const PostParams<T> p) {
+__global__ void __launch_bounds__(512) postk_kernel(const PostParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[32];
   __shared__ double zsum[64];
