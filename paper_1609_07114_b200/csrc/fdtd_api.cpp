@@ -628,8 +628,10 @@ fdtd_status apply_passes(fdtd_ctx* c, int k) {
     }
     const size_t cap = std::max(budget, need1);
     c->post_smem = 16;
-    for (auto& x : shp) {
-      x.B = (int)std::max<size_t>(1, std::min<size_t>(Bmax, cap / x.per));
+    for (auto& x : shp) {  // a power of two: the batched GEMM splits B into groups of 4, 2 or 1
+      const int fit = (int)std::max<size_t>(1, std::min<size_t>(Bmax, cap / x.per));
+      x.B = 1;
+      while (x.B * 2 <= fit) x.B *= 2;
       c->post_smem = std::max(c->post_smem, x.B * x.per);
     }
     c->batch_tab.clear();

@@ -109,6 +109,12 @@ __device__ __forceinline__ void cp_async_el(T* dst, const T* src) {
                "n"(sizeof(T)) : "memory");
 }
 
+#ifndef FDTD_PFD
+#define FDTD_PFD 1  // sweep: row distance of the L2 prefetch beyond the register-prefetched row (measured best)
+#endif
+constexpr int PFD = FDTD_PFD;
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 // eq:updateH divided by dx dy mu / dt:  Hz' = Hz + chy (Ex_{j+1} - Ex_j) - chx (Ey_{i+1} - Ey_i).
 // Explicit fused operations pin the rounding, so the redundant recomputations at warp and
 // chunk edges are bit-identical to the owner's value (needed for 1-GPU == N-GPU fields).
@@ -429,6 +435,14 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
     ldv(x.pma + o, Y.ma);
     ldv(x.pms + o, Y.ms);
   }
+  if (PFD > 0 && j + 1 + PFD < je) {  // pull row j+1+PFD into L2 (no registers held)
+    const uint32_t o = (uint32_t)(j + 1 + PFD) * (uint32_t)x.P;
+    prefetch_l2(x.pex + o + x.P);
+    prefetch_l2(x.pey + o);
+    prefetch_l2(x.phz + o);
+    prefetch_l2(x.pma + o);
+    prefetch_l2(x.pms + o);
+  }
   // ---- stage s: step n+s on row j-s, from stage s-1's outputs of rows j-s (A) and j-s+1 (B)
 #pragma unroll
   for (int s = 1; s < K; ++s) {
@@ -610,6 +624,7 @@ __device__ __forceinline__ void bgemm_ipi(const T* __restrict__ A, int m, int ld
   }
 }
 
+// B (the batch's slot count) is a power of two (fdtd_api.cpp apply_passes), so B / IPI covers it
 template <typename T>
 __device__ __forceinline__ void bgemm(const T* A, int m, int lda, int k, const T* X, T* Y, int B, T alpha) {
   if (m * (B / 4) >= (int)blockDim.x) bgemm_ipi<T, 4>(A, m, lda, k, X, Y, B, alpha);
