@@ -833,7 +833,8 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
 fdtd_status fdtd_set_tuning(fdtd_ctx* c, int32_t rows_per_cta, int32_t warps_per_cta) {
   if (!c) return FDTD_E_ARG;
   if (rows_per_cta < 0 || warps_per_cta < 0 || warps_per_cta > 8) return fail(c, FDTD_E_ARG, "bad tuning");
-  c->chunk = rows_per_cta ? rows_per_cta : (c->rows >= 4096 ? 256 : 32);
+  // rows per CTA: long chunks amortise the K-row prologue, short ones keep enough CTAs for ~8 waves
+  c->chunk = rows_per_cta ? rows_per_cta : (c->rows >= 16384 ? 256 : c->rows >= 2048 ? 64 : 32);
   c->warps = warps_per_cta ? warps_per_cta : 4;
   if (!rows_per_cta)
     if (const char* e = getenv("FDTD_CHUNK")) c->chunk = std::max(1, atoi(e));  // tuning experiments
