@@ -313,3 +313,31 @@ def test_literal_rom_k_step_bitwise():
     for o in outs[1:]:
         for a, b in zip(outs[0], o):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("src", [(55, 31), (56, 32), (111, 64), (112, 63)])
+def test_source_and_probes_on_warp_and_chunk_seams(src):
+    """K = 4 strips store 28 lanes x 2 columns (seams at columns 56 w) and chunks of 32 rows: a source
+    and probes on / next to those seams are applied / recorded exactly once and match the one-step
+    path bit for bit and the oracle to 1e-4."""
+    n = 160
+    rng = np.random.default_rng(9)
+    dx = dy = 1e-3
+    dt = 0.95 * sc.cfl_limit(dx, dy)
+    probes = np.array([[src[0] + d, src[1] + e] for d in (-1, 0, 1) for e in (-1, 0, 1)] + [[56, 5], [55, 150]],
+                      np.int32)
+    s = sc.Scene(name="seams", nx=n, ny=n, dx=dx, dy=dy, dt=dt, eps_r=rng.uniform(1, 4, (n, n)),
+                 sigma=rng.uniform(0, 0.05, (n, n)), precision=32, steps=300, source=src,
+                 samples=sc.gaussian_samples(300, dt, 30e9, True), probes=probes, models=[], placements=None)
+    outs = []
+    for spp in (1, 4):
+        g = gpu_from_scene(s)
+        g.set_time_blocking(spp)
+        g.step(300)
+        assert g.info().steps_per_pass == spp
+        outs.append((g.get_window(), g.probe()))
+        g.close()
+    for a, b in zip(outs[0][0], outs[1][0]):
+        assert np.array_equal(a, b)
+    assert np.array_equal(outs[0][1], outs[1][1])
+    _compare(s, 300, 1e-4)
