@@ -132,6 +132,12 @@ fdtd_status fdtd_add_rom(fdtd_ctx *c, const fdtd_rom_model *m, const int32_t *an
 fdtd_status fdtd_set_source(fdtd_ctx *c, int64_t i, int64_t j, const double *samples,
                             int64_t n_samples, int64_t step0);
 
+/* Soft Hz line source on the cells (i, j0 .. j1-1), every cell driven by the same samples (the
+ * "line source" that excites the paper's waveguides, L882, L945; NEXT-2).  Replaces any previous
+ * source.  fdtd_set_source(i, j) is the line (i, j .. j). */
+fdtd_status fdtd_set_source_line(fdtd_ctx *c, int64_t i, int64_t j0, int64_t j1, const double *samples,
+                                 int64_t n_samples, int64_t step0);
+
 /* Probes: record Hz^{n+1/2} at cells ij[2p], ij[2p+1] after every step n (R16).  Replaces any
  * previous set; the record of a probe in another rank's rows reads 0 on this rank. */
 fdtd_status fdtd_set_probes(fdtd_ctx *c, const int64_t *ij, int32_t n_probes);
@@ -214,6 +220,17 @@ fdtd_status fdtd_profile_read(fdtd_ctx *c, double *sweep_ms, double *post_ms, in
  * of K ends with shallower passes.  Fields, ROM states and probes are bit-identical for every
  * K; the energy trace agrees up to summation order. */
 fdtd_status fdtd_set_time_blocking(fdtd_ctx *c, int32_t steps_per_pass);
+
+/* CPML absorbing layers (NEXT-2) of `width` cells at both x-ends (x < width dx and x > (nx - width) dx),
+ * backed by the PEC walls, for the paper's PML-terminated waveguides (L882, L945): Roden-Gedney
+ * recursive convolution with kappa = 1, alpha = 0, sigma(d) = sigma_max d^order with
+ * sigma_max = (order + 1) ln(1/r0) / (2 eta0 width dx), d the depth from the layer's inner face;
+ * b = exp(-sigma dt / eps0), a = b - 1; psi_hz = b psi_hz + a dEy/dx (Hz -= dt/mu0 psi_hz),
+ * psi_ey = b psi_ey + a dHz/dx (Ey's curl term -dHz/dx becomes -(dHz/dx + psi_ey)).  width 0
+ * removes the layers.  The layer cells stay in the storage function (their standard terms).
+ * FDTD_E_ARG with several ranks, when 2 (width + 4) > nx, or when a ROM instance's ring comes
+ * within width + 4 cells of an x-end.  Resets the auxiliary state. */
+fdtd_status fdtd_set_pml(fdtd_ctx *c, int32_t width, int32_t order, double r0);
 
 /* Tuning knobs for the fused sweep (rows per CTA, warps per CTA); 0 keeps default. */
 fdtd_status fdtd_set_tuning(fdtd_ctx *c, int32_t rows_per_cta, int32_t warps_per_cta);

@@ -55,6 +55,9 @@ def lib():
         L.osim_add_subgrid.restype = C.c_int
         L.osim_add_subgrid.argtypes = [C.c_void_p] + [C.c_int] * 5 + [_dp, _dp]
         L.osim_set_source.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int64, C.c_int64]
+        L.osim_set_source_line.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, _dp, C.c_int64, C.c_int64]
+        L.osim_set_pml.restype = C.c_int
+        L.osim_set_pml.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double]
         L.osim_set_probes.argtypes = [C.c_void_p, _ip, C.c_int]
         L.osim_step.argtypes = [C.c_void_p, C.c_int64, _dp, C.c_int64, _dp]
         L.osim_get_state.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp]
@@ -135,6 +138,17 @@ class OracleSim:
     def set_source(self, i, j, samples, t0=0):
         self._src = _f64(samples)
         lib().osim_set_source(self._h, int(i), int(j), _p(self._src), len(self._src), int(t0))
+
+    def set_source_line(self, i, j0, j1, samples, t0=0):
+        """Soft Hz source on the cells (i, j0 .. j1-1) (a line source, NEXT-2)."""
+        a = _f64(samples)
+        lib().osim_set_source_line(self._h, int(i), int(j0), int(j1), _p(a), a.size, int(t0))
+
+    def set_pml(self, width, order=3, r0=1e-8):
+        """CPML of `width` cells on both x-ends (NEXT-2)."""
+        rc = lib().osim_set_pml(self._h, int(width), int(order), float(r0))
+        if rc != 0:
+            raise ValueError("osim_set_pml failed with code %d" % rc)
 
     def set_probes(self, ij):
         a = np.ascontiguousarray(np.asarray(ij, dtype=np.int32).reshape(-1, 2))

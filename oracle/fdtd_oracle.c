@@ -62,7 +62,7 @@ typedef struct {
   unsigned char *kx, *ky, *kc; /* kinds of Ex edges, Ey edges, Hz cells */
   int nrom;
   orom *roms;
-  int src_i, src_j;
+  int src_i, src_j, src_j1;  /* soft Hz source on cells (src_i, src_j .. src_j1-1) */
   double *src;
   int64_t nsrc, src_t0;
   int nprobe;
@@ -71,6 +71,12 @@ typedef struct {
   /* direct subgridding regions (reference only, pin P-SUBGRID) */
   int nsub;
   struct osub_s *subs;
+  /* CPML on the two x-ends (NEXT-2): width w cells each side; per column coefficients and the
+   * auxiliary fields psi_hz (Hz cells) and psi_ey (Ey edges); 0 outside the layers */
+  int pml_w;
+  double *pml_bh, *pml_ah;   /* per Hz column i: b, a of the recursive convolution */
+  double *pml_be, *pml_ae;   /* per Ey column i (nx + 1) */
+  double *psi_hz, *psi_ey;
 } osim;
 
 /* A finely meshed region marched directly (no matrices): fine Yee cells of
@@ -160,6 +166,52 @@ osim *osim_create(int nx, int ny, double dx, double dy, double dt, const double 
   return s;
 }
 
+/* ------------------------------------------------------------------ */
+/* CPML (NEXT-2; Roden & Gedney's recursive-convolution PML, kappa = 1, */
+/* alpha = 0) on the cells i < w and i >= nx - w, backed by the PEC     */
+/* walls.  Depth d in [0, 1] from the layer's inner face; sigma(d) =    */
+/* sigma_max d^m, sigma_max = (m + 1) ln(1/R0) / (2 eta0 w dx).  Per    */
+/* step: b = exp(-sigma dt / eps0), a = b - 1;                          */
+/*   psi_hz = b psi_hz + a (Ey_{i+1} - Ey_i)/dx,  Hz -= dt/mu0 psi_hz;  */
+/*   psi_ey = b psi_ey + a (Hz_i - Hz_{i-1})/dx,                        */
+/*   Ey: the curl term -(dHz/dx) becomes -(dHz/dx + psi_ey).            */
+/* ------------------------------------------------------------------ */
+static double pml_sigma(int w, int order, double r0, double dx, double d) {
+  const double eta0 = sqrt(O_MU0 / O_EPS0);
+  const double smax = (order + 1) * log(1.0 / r0) / (2.0 * eta0 * w * dx);
+  return d <= 0.0 ? 0.0 : smax * pow(d, order);
+}
+
+int osim_set_pml(osim *s, int w, int order, double r0) {
+  const int nx = s->nx;
+  if (w < 0 || 2 * w > nx || order < 0 || !(r0 > 0 && r0 < 1)) return -1;
+  free(s->pml_bh); free(s->pml_ah); free(s->pml_be); free(s->pml_ae); free(s->psi_hz); free(s->psi_ey);
+  s->pml_w = w;
+  s->pml_bh = (double *)calloc(nx, sizeof(double));
+  s->pml_ah = (double *)calloc(nx, sizeof(double));
+  s->pml_be = (double *)calloc(nx + 1, sizeof(double));
+  s->pml_ae = (double *)calloc(nx + 1, sizeof(double));
+  s->psi_hz = (double *)calloc((size_t)nx * s->ny, sizeof(double));
+  s->psi_ey = (double *)calloc((size_t)(nx + 1) * s->ny, sizeof(double));
+  for (int i = 0; i < nx; ++i) {  /* Hz at x = (i + 1/2) dx */
+    double d = 0.0;
+    if (i < w) d = (w - i - 0.5) / w;
+    else if (i >= nx - w) d = (i + 0.5 - (nx - w)) / w;
+    const double b = exp(-pml_sigma(w, order, r0, s->dx, d) * s->dt / O_EPS0);
+    s->pml_bh[i] = b; s->pml_ah[i] = b - 1.0;
+  }
+  for (int i = 0; i <= nx; ++i) {  /* Ey at x = i dx */
+    double d = 0.0;
+    if (i < w) d = (double)(w - i) / w;
+    else if (i > nx - w) d = (double)(i - (nx - w)) / w;
+    const double b = exp(-pml_sigma(w, order, r0, s->dx, d) * s->dt / O_EPS0);
+    s->pml_be[i] = b; s->pml_ae[i] = b - 1.0;
+  }
+  return 0;
+}
+
+static int in_pml_col(const osim *s, int i) { return s->pml_w > 0 && (i < s->pml_w || i >= s->nx - s->pml_w); }
+
 void osim_destroy(osim *s) {
   if (!s) return;
   for (int r = 0; r < s->nrom; ++r) {
@@ -176,6 +228,7 @@ void osim_destroy(osim *s) {
   free(s->subs);
   free(s->eps_r); free(s->sigma); free(s->Ex); free(s->Ey); free(s->Hz); free(s->Hold);
   free(s->kx); free(s->ky); free(s->kc); free(s->src); free(s->probe);
+  free(s->pml_bh); free(s->pml_ah); free(s->pml_be); free(s->pml_ae); free(s->psi_hz); free(s->psi_ey);
   free(s);
 }
 
@@ -322,14 +375,18 @@ int osim_add_rom(osim *s, int i0, int j0, int bx, int by, int q1, int q2, const 
   return s->nrom - 1;
 }
 
-void osim_set_source(osim *s, int i, int j, const double *samples, int64_t n, int64_t t0) {
+void osim_set_source_line(osim *s, int i, int j0, int j1, const double *samples, int64_t n, int64_t t0) {
   free(s->src);
   s->src = NULL;
-  s->src_i = i; s->src_j = j; s->nsrc = n; s->src_t0 = t0;
+  s->src_i = i; s->src_j = j0; s->src_j1 = j1; s->nsrc = n; s->src_t0 = t0;
   if (n > 0) {
     s->src = (double *)malloc((size_t)n * sizeof(double));
     memcpy(s->src, samples, (size_t)n * sizeof(double));
   }
+}
+
+void osim_set_source(osim *s, int i, int j, const double *samples, int64_t n, int64_t t0) {
+  osim_set_source_line(s, i, j, j + 1, samples, n, t0);
 }
 
 void osim_set_probes(osim *s, const int *ij, int n) {
@@ -373,6 +430,11 @@ static void coarse_h(osim *s) {
       double lhs = dx * dy * mu / dt;
       double rhs = lhs * HZ(s, i, j) - dx * EX(s, i, j) + dx * EX(s, i, j + 1) + dy * EY(s, i, j) -
                    dy * EY(s, i + 1, j);
+      if (in_pml_col(s, i)) {  /* CPML: the x-derivative gains psi_hz */
+        double *ps = &s->psi_hz[(size_t)j * nx + i];
+        *ps = s->pml_bh[i] * *ps + s->pml_ah[i] * (EY(s, i + 1, j) - EY(s, i, j)) / dx;
+        rhs -= dx * dy * *ps;
+      }
       HZ(s, i, j) = rhs / lhs;
     }
 }
@@ -403,6 +465,11 @@ static void coarse_e(osim *s) {
       double sig = 0.5 * (CELL(s, sigma, i - 1, j) + CELL(s, sigma, i, j));
       double lhs = dy * dx * (eps / dt + sig / 2);
       double rhs = dy * dx * (eps / dt - sig / 2) * EY(s, i, j) - dy * HZ(s, i, j) + dy * HZ(s, i - 1, j);
+      if (s->pml_w > 0 && (i <= s->pml_w || i >= nx - s->pml_w)) {  /* CPML psi_ey */
+        double *ps = &s->psi_ey[(size_t)j * (nx + 1) + i];
+        *ps = s->pml_be[i] * *ps + s->pml_ae[i] * (HZ(s, i, j) - HZ(s, i - 1, j)) / dx;
+        rhs -= dy * dx * *ps;
+      }
       EY(s, i, j) = rhs / lhs;
     }
 }
@@ -622,7 +689,8 @@ void osim_step(osim *s, int64_t nsteps, double *probe_out, int64_t ldp, double *
     coarse_h(s);                                          /* S1 */
     if (s->src_i >= 0) {                                  /* S2 */
       int64_t k = s->n - s->src_t0;
-      if (k >= 0 && k < s->nsrc) HZ(s, s->src_i, s->src_j) += s->src[k];
+      if (k >= 0 && k < s->nsrc)
+        for (int j = s->src_j; j < s->src_j1; ++j) HZ(s, s->src_i, j) += s->src[k];
     }
     if (energy_out) energy_out[t] = energy(s);            /* S3: W^n */
     if (probe_out)

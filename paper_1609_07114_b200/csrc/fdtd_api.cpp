@@ -27,6 +27,7 @@ using fdtd::KMAX;
 constexpr int ROW0 = 2 * KMAX;  // local row of the first owned row: the K-step sweep's first chunk
                                 // reads K halo rows below it and stage rows down to r0 - 2K
 constexpr int GHOST_UP = KMAX;  // ghost rows above the slab (Ex edge rows up to row_end + K - 1)
+constexpr int PML_CHUNK = 32;   // rows per CTA of the CPML band fix-up
 constexpr double MU0 = 4.0e-7 * 3.14159265358979323846;
 constexpr double C0 = 299792458.0;
 constexpr double EPS0 = 1.0 / (MU0 * C0 * C0);
@@ -98,7 +99,7 @@ struct fdtd_ctx {
   int chunk = 64, warps = 4;
   // source
   double* d_src = nullptr;
-  int64_t src_n = 0, src_t0 = 0, src_i = -1, src_j = -1, src_cap = 0;
+  int64_t src_n = 0, src_t0 = 0, src_i = -1, src_j = -1, src_j1 = -1, src_cap = 0;  // cells (i, j .. j1-1)
   // probes & energy rings
   int64_t cap = 65536;
   int n_probe = 0;
@@ -118,6 +119,12 @@ struct fdtd_ctx {
   int post_threads = 256;
   int32_t* d_rects = nullptr;
   std::vector<int32_t> zp_off, zp;  // zone probes per instance (gi, gj, probe index)
+  // CPML on the two x-ends (NEXT-2): width, per-column coefficients, psi state, marked columns
+  int pml_w = 0, pml_marked = 0;
+  void *d_pml_bh = nullptr, *d_pml_ah = nullptr, *d_pml_be = nullptr, *d_pml_ae = nullptr;
+  void *d_psih = nullptr, *d_psie = nullptr;
+  int64_t* d_probe_gi = nullptr;
+  int32_t* d_probe_lr = nullptr;
   int32_t* d_zp_off = nullptr;
   int32_t* d_zp = nullptr;
   // ROMs
@@ -228,10 +235,12 @@ fdtd::SweepParams<T> sweep_params(fdtd_ctx* c, int q) {
   p.pitch = c->pitch; p.nx = c->d.nx; p.rows = c->rows; p.chunk = c->chunk; p.row0 = ROW0;
   p.chx = (T)(c->d.dt / (MU0 * c->d.dx));
   p.chy = (T)(c->d.dt / (MU0 * c->d.dy));
-  // the source row may also be a ghost row: the chunks next to the slab edges recompute up to
-  // KMAX rows beyond it, adding the source as its owner does
-  const bool src_here = c->d_src && c->src_j >= c->d.row_begin - KMAX && c->src_j < c->d.row_end + KMAX;
-  p.src_row = src_here ? (int)lrow(c, c->src_j) : -1;
+  // source rows clipped to this slab +- KMAX (the chunks next to the slab edges recompute up to KMAX
+  // ghost rows, adding the source as its owner does)
+  const int64_t sj0 = std::max(c->src_j, c->d.row_begin - KMAX), sj1 = std::min(c->src_j1, c->d.row_end + KMAX);
+  const bool src_here = c->d_src && sj0 < sj1;
+  p.src_row = src_here ? (int)lrow(c, sj0) : -1;
+  p.src_row_end = src_here ? (int)lrow(c, sj1) : -1;
   p.src_col = src_here ? c->src_i : -1;
   p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
   p.step = c->d_step;
@@ -274,12 +283,17 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q, int K) {
   p.idx = (T)(1.0 / c->d.dx); p.idy = (T)(1.0 / c->d.dy);
   p.wxy = (T)(c->d.dx * c->d.dy);
   p.wh = (T)(MU0 * c->d.dx * c->d.dy / c->d.dt);
-  const bool src_here = c->d_src && c->src_j >= c->d.row_begin - KMAX && c->src_j < c->d.row_end + KMAX;
-  p.src_row = src_here ? (int)lrow(c, c->src_j) : -1;
+  // source rows clipped to this slab +- KMAX (the chunks next to the slab edges recompute up to KMAX
+  // ghost rows, adding the source as its owner does)
+  const int64_t sj0 = std::max(c->src_j, c->d.row_begin - KMAX), sj1 = std::min(c->src_j1, c->d.row_end + KMAX);
+  const bool src_here = c->d_src && sj0 < sj1;
+  p.src_row = src_here ? (int)lrow(c, sj0) : -1;
+  p.src_row_end = src_here ? (int)lrow(c, sj1) : -1;
   p.src_col = src_here ? c->src_i : -1;
   p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
   p.sweep_partials = c->d_partials;  // exactly the partials the matching sweep launches wrote
-  p.n_sweep_partials = (int64_t)sweep_gx(c, K) * ((c->rows + c->chunk - 1) / c->chunk);
+  p.n_sweep_partials = (int64_t)sweep_gx(c, K) * ((c->rows + c->chunk - 1) / c->chunk) +
+                       (c->pml_w > 0 ? fdtd::pml_ctas(c->rows, PML_CHUNK) : 0);  // + the CPML band CTAs
   p.pstride = c->n_partials;
   p.rom_partials = c->d_rom_partials;
   p.level1 = c->d_level1;
@@ -289,6 +303,37 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q, int K) {
   p.batch_tab = c->d_batch_tab;
   p.block = c->post_threads;
   p.smem_bytes = c->post_smem;
+  return p;
+}
+
+template <typename T>
+fdtd::PmlParams<T> pml_params(fdtd_ctx* c, int q) {
+  fdtd::PmlParams<T> p{};
+  p.ex0 = (const T*)c->f[q][0]; p.ey0 = (const T*)c->f[q][1]; p.hz0 = (const T*)c->f[q][2];
+  p.ex1 = (T*)c->f[1 - q][0]; p.ey1 = (T*)c->f[1 - q][1]; p.hz1 = (T*)c->f[1 - q][2];
+  p.mea = (const T*)c->coef[0]; p.msb = (const T*)c->coef[1];
+  p.pitch = c->pitch; p.nx = c->d.nx; p.rows = c->rows; p.row0 = ROW0; p.chunk = PML_CHUNK;
+  p.w = c->pml_w; p.Kz = c->kz;
+  p.bh = (const T*)c->d_pml_bh; p.ah = (const T*)c->d_pml_ah; p.be = (const T*)c->d_pml_be; p.ae = (const T*)c->d_pml_ae;
+  p.psih = (T*)c->d_psih; p.psie = (T*)c->d_psie; p.psi_rows = c->nrows_alloc;
+  p.chx = (T)(c->d.dt / (MU0 * c->d.dx));
+  p.chy = (T)(c->d.dt / (MU0 * c->d.dy));
+  p.idx = (T)(1.0 / c->d.dx); p.idy = (T)(1.0 / c->d.dy);
+  p.wxy = (T)(c->d.dx * c->d.dy);
+  p.wh = (T)(MU0 * c->d.dx * c->d.dy / c->d.dt);
+  p.cpsi = (T)(c->d.dt / MU0);
+  p.dxv = (T)c->d.dx;
+  const int64_t sj0 = std::max(c->src_j, c->d.row_begin - KMAX), sj1 = std::min(c->src_j1, c->d.row_end + KMAX);
+  const bool src_here = c->d_src && sj0 < sj1;
+  p.src_row = src_here ? (int)lrow(c, sj0) : -1;
+  p.src_row_end = src_here ? (int)lrow(c, sj1) : -1;
+  p.src_col = src_here ? c->src_i : -1;
+  p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
+  p.step = c->d_step;
+  p.n_probe = c->d_probe_gi ? c->n_probe : 0;
+  p.probe_gi = c->d_probe_gi; p.probe_lr = c->d_probe_lr; p.probe_ring = (T*)c->d_probe_ring; p.cap = c->cap;
+  p.partials = c->energy_on ? c->d_partials : nullptr;
+  p.pstride = c->n_partials;
   return p;
 }
 
@@ -415,6 +460,19 @@ fdtd_status enqueue_pass(fdtd_ctx* c, int q, cudaStream_t s, int K) {
       sweep(0, nch);
     }
   }
+  if (c->pml_w > 0) {  // NEXT-2: CPML bands (their energy partials follow the sweep's)
+    const int64_t poff = (int64_t)sweep_gx(c, K) * nch;
+    if (c->prec == 64) {
+      auto pp = pml_params<double>(c, q);
+      pp.poff = poff;
+      fdtd::launch_pml<double>(pp, K, c->energy_on, s);
+    } else {
+      auto pp = pml_params<float>(c, q);
+      pp.poff = poff;
+      fdtd::launch_pml<float>(pp, K, c->energy_on, s);
+    }
+    c->launches += 1;
+  }
   if (prof) CK(cudaEventRecord(e[1], s));
   if (c->prec == 64) fdtd::launch_post<double>(post_params<double>(c, q, K), K, c->energy_on, s);
   else fdtd::launch_post<float>(post_params<float>(c, q, K), K, c->energy_on, s);
@@ -532,8 +590,14 @@ fdtd_status upload_roms(fdtd_ctx* c) {
 // the zones are disjoint).
 bool passes_valid(const fdtd_ctx* c, int K) {
   if (K > c->V) return false;  // a halo lane of V columns covers at most V steps of error spread
-  if (K == 1) return true;
   const int64_t M = 2 * K - 1;
+  if (c->pml_w > 0) {  // every fix-up region clear of the CPML bands (each kernel ignores the other's physics)
+    const int64_t WB = c->pml_w + 2 * K + 2;
+    if (2 * WB > c->d.nx) return false;
+    for (size_t r = 0; r < c->rects.size(); r += 4)
+      if (c->rects[r] - M < WB || c->rects[r] + c->rects[r + 2] + M > c->d.nx - WB) return false;
+  }
+  if (K == 1) return true;
   struct Rc { int64_t i0, j0, bx, by; };
   std::vector<Rc> all;
   for (size_t r = 0; r < c->rects.size(); r += 4) {
@@ -609,6 +673,24 @@ fdtd_status apply_passes(fdtd_ctx* c, int k) {
   }
   c->kz_marked = k;
   c->kz = k;
+  {  // CPML write-back columns (layer + k + 1): the sweep skips their storage-function terms
+    const int want = c->pml_w > 0 ? c->pml_w + k + 1 : 0;
+    if (c->pml_marked != want) {
+      if (c->prec == 64) {
+        fdtd::launch_band_marks<double>((double*)c->coef[1], (const double*)c->coef[0], c->pitch, c->d.nx, ROW0,
+                                        c->rows, c->pml_marked, false, c->stream);
+        fdtd::launch_band_marks<double>((double*)c->coef[1], (const double*)c->coef[0], c->pitch, c->d.nx, ROW0,
+                                        c->rows, want, true, c->stream);
+      } else {
+        fdtd::launch_band_marks<float>((float*)c->coef[1], (const float*)c->coef[0], c->pitch, c->d.nx, ROW0,
+                                       c->rows, c->pml_marked, false, c->stream);
+        fdtd::launch_band_marks<float>((float*)c->coef[1], (const float*)c->coef[0], c->pitch, c->d.nx, ROW0,
+                                       c->rows, want, true, c->stream);
+      }
+      CK(cudaGetLastError());
+      c->pml_marked = want;
+    }
+  }
   // batches of consecutive instances of one model (instances are stored grouped by model).  Every
   // model gets its own region stride and batch size under one shared-memory budget per CTA
   // (~110 KB: two fix-up CTAs per SM), so small models are batched 8 at a time and the largest
@@ -843,7 +925,7 @@ fdtd_status fdtd_set_tuning(fdtd_ctx* c, int32_t rows_per_cta, int32_t warps_per
   if (const char* e = getenv("FDTD_POST_THREADS")) c->post_threads = std::max(64, std::min(512, atoi(e) / 32 * 32));
   const int gx = sweep_gx_max(c);
   const int gy = (c->rows + c->chunk - 1) / c->chunk;
-  const int n = gx * gy;
+  const int n = gx * gy + fdtd::pml_ctas(c->rows, PML_CHUNK);  // sweep CTAs + (possible) CPML band CTAs
   if (n > c->n_partials) {
     if (c->d_partials) dfree(c, c->d_partials);
     c->d_partials = (double*)dalloc(c, (size_t)KMAX * n * sizeof(double));
@@ -911,6 +993,8 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
       return fail(c, FDTD_E_ARG, "instance %lld: footprint + ring leaves the grid", (long long)k);
     if (j0 - 1 < c->d.row_begin || j0 + by > c->d.row_end - 1)
       return fail(c, FDTD_E_ARG, "instance %lld: footprint + ring straddles this rank's rows", (long long)k);
+    if (c->pml_w > 0 && (i0 - 1 < c->pml_w + 4 || i0 + bx + 1 > c->d.nx - c->pml_w - 4))
+      return fail(c, FDTD_E_ARG, "instance %lld lies within the CPML band", (long long)k);
   }
   {
     // ring-vs-footprint overlap: sort all rectangles by i0 and sweep
@@ -1142,9 +1226,10 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
   return FDTD_OK;
 }
 
-fdtd_status fdtd_set_source(fdtd_ctx* c, int64_t i, int64_t j, const double* samples, int64_t n, int64_t step0) {
+fdtd_status fdtd_set_source_line(fdtd_ctx* c, int64_t i, int64_t j0, int64_t j1, const double* samples, int64_t n,
+                                 int64_t step0) {
   if (!c) return FDTD_E_ARG;
-  if (i < 0 || i >= c->d.nx || j < 0 || j >= c->d.ny || n < 0 || (n > 0 && !samples))
+  if (i < 0 || i >= c->d.nx || j0 < 0 || j1 > c->d.ny || j1 <= j0 || n < 0 || (n > 0 && !samples))
     return fail(c, FDTD_E_ARG, "bad source");
   if (!c->d_src || n > c->src_cap) {
     if (c->d_src) dfree(c, c->d_src);
@@ -1156,9 +1241,14 @@ fdtd_status fdtd_set_source(fdtd_ctx* c, int64_t i, int64_t j, const double* sam
   c->src_n = n;
   c->src_t0 = step0;
   c->src_i = i;
-  c->src_j = j;
+  c->src_j = j0;
+  c->src_j1 = j1;
   drop_graph(c);
   return FDTD_OK;
+}
+
+fdtd_status fdtd_set_source(fdtd_ctx* c, int64_t i, int64_t j, const double* samples, int64_t n, int64_t step0) {
+  return fdtd_set_source_line(c, i, j, j + 1, samples, n, step0);
 }
 
 fdtd_status fdtd_set_probes(fdtd_ctx* c, const int64_t* ij, int32_t n) {
@@ -1182,6 +1272,17 @@ fdtd_status fdtd_set_probes(fdtd_ctx* c, const int64_t* ij, int32_t n) {
   }
   fdtd_status st = upload(c, &c->d_probe_rows, rows_tab);
   if (st != FDTD_OK) return st;
+  {  // column and local row of every probe (-1: another rank's) for the CPML band fix-up
+    std::vector<int64_t> gi(std::max(n, 1), -1);
+    std::vector<int32_t> lr(std::max(n, 1), -1);
+    for (int32_t k = 0; k < n; ++k) {
+      gi[k] = ij[2 * k];
+      const int64_t j = ij[2 * k + 1];
+      lr[k] = (j >= c->d.row_begin && j < c->d.row_end) ? (int32_t)lrow(c, j) : -1;
+    }
+    if ((st = upload(c, &c->d_probe_gi, gi)) != FDTD_OK) return st;
+    if ((st = upload(c, &c->d_probe_lr, lr)) != FDTD_OK) return st;
+  }
   if ((st = upload(c, &c->d_probe_list, list)) != FDTD_OK) return st;
   if (c->d_probe_ring) dfree(c, c->d_probe_ring);
   c->d_probe_ring = dalloc(c, (size_t)std::max(n, 1) * c->cap * c->es);
@@ -1452,6 +1553,52 @@ fdtd_status fdtd_step_group(fdtd_ctx** g, int32_t n, int64_t nsteps) {
   }
   fdtd_ctx* c = g[0];
   CK(cudaGetLastError());
+  return FDTD_OK;
+}
+
+fdtd_status fdtd_set_pml(fdtd_ctx* c, int32_t width, int32_t order, double r0) {
+  if (!c) return FDTD_E_ARG;
+  if (width < 0 || order < 0 || order > 8 || !(r0 > 0 && r0 < 1)) return fail(c, FDTD_E_ARG, "bad CPML parameters");
+  if (width > 0 && c->d.nranks > 1) return fail(c, FDTD_E_ARG, "CPML layers need a single rank (row slabs: NEXT)");
+  if (2 * (width + 4) > c->d.nx) return fail(c, FDTD_E_ARG, "CPML layers of %d cells do not fit nx = %lld", width,
+                                             (long long)c->d.nx);
+  for (size_t r = 0; width > 0 && r < c->rects.size(); r += 4)  // one-step band (width + 4) clear of every ring
+    if (c->rects[r] - 1 < width + 4 || c->rects[r] + c->rects[r + 2] + 1 > c->d.nx - width - 4)
+      return fail(c, FDTD_E_ARG, "a ROM instance lies within the CPML band");
+  fdtd_status st;
+  for (void** pp : {&c->d_pml_bh, &c->d_pml_ah, &c->d_pml_be, &c->d_pml_ae, &c->d_psih, &c->d_psie})
+    if (*pp) { dfree(c, *pp); *pp = nullptr; }
+  c->pml_w = width;
+  if (width > 0) {
+    // sigma(d) = sigma_max d^order, sigma_max = (order + 1) ln(1/R0) / (2 eta0 width dx); b = exp(-sigma dt / eps0),
+    // a = b - 1 (kappa 1, alpha 0); d = depth from the layer's inner face, per column position
+    const double eta0 = std::sqrt(MU0 / EPS0);
+    const double smax = (order + 1) * std::log(1.0 / r0) / (2.0 * eta0 * width * c->d.dx);
+    auto bcoef = [&](double d) { return std::exp(-(d > 0 ? smax * std::pow(d, order) : 0.0) * c->d.dt / EPS0); };
+    const int64_t nx = c->d.nx;
+    std::vector<double> bh(2 * width), ah(2 * width), be(2 * (width + 1)), ae(2 * (width + 1));
+    for (int k = 0; k < width; ++k) {  // Hz columns: left i = k, right i = nx - width + k
+      const double dl = (width - k - 0.5) / width, dr = (k + 0.5) / width;
+      bh[k] = bcoef(dl); ah[k] = bh[k] - 1.0;
+      bh[width + k] = bcoef(dr); ah[width + k] = bh[width + k] - 1.0;
+    }
+    for (int k = 0; k <= width; ++k) {  // Ey columns: left i = k, right i = nx - width + k
+      const double dl = (double)(width - k) / width, dr = (double)k / width;
+      be[k] = bcoef(dl); ae[k] = be[k] - 1.0;
+      be[width + 1 + k] = bcoef(dr); ae[width + 1 + k] = be[width + 1 + k] - 1.0;
+    }
+    (void)nx;
+    if ((st = upload_T(c, &c->d_pml_bh, bh)) != FDTD_OK) return st;
+    if ((st = upload_T(c, &c->d_pml_ah, ah)) != FDTD_OK) return st;
+    if ((st = upload_T(c, &c->d_pml_be, be)) != FDTD_OK) return st;
+    if ((st = upload_T(c, &c->d_pml_ae, ae)) != FDTD_OK) return st;
+    c->d_psih = dalloc(c, (size_t)2 * c->nrows_alloc * width * c->es);
+    c->d_psie = dalloc(c, (size_t)2 * c->nrows_alloc * (width + 1) * c->es);
+    if (!c->d_psih || !c->d_psie) return fail(c, FDTD_E_NOMEM, "CPML state");
+  }
+  c->kz_dirty = true;
+  drop_graph(c);
+  CK(cudaStreamSynchronize(c->stream));
   return FDTD_OK;
 }
 

@@ -389,7 +389,7 @@ struct SweepCtx {
   const T *pex, *pey, *phz, *pma, *pms;  // this lane's column in row 0 of each input array
   T *pex1, *pey1, *phz1;                 // ... and of each output array
   T* ring;
-  int lane, r0, r1, src_r, src_k;
+  int lane, r0, r1, src_r, src_r1, src_k;  // source rows [src_r, src_r1) in this lane's column src_k
   bool out;
   int64_t step, P;
   T g[K];
@@ -422,7 +422,7 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
     row_coef<T, V>(X.ma, X.ms, Y.ma, Y.ms, p.idx, p.idy, p.wxy, p.wh, cf);
     if (K > 1) ring_store<T, V>(x.ring, j & (K - 1), cf);
     const T en = yee_any<T, V, ENERGY>(Y.ext, X.ext, X.ey, X.hz, A.h[0], CoefRegs<T, V>{cf}, p, x.g[0],
-                                       CHK && j == x.src_r, x.src_k, B.h[0], B.x[0], B.y[0]);
+                                       CHK && j >= x.src_r && j < x.src_r1, x.src_k, B.h[0], B.x[0], B.y[0]);
     const bool own = !CHK || (j >= x.r0 && j < x.r1);
     if (ENERGY && own) eacc[0] += (double)en;
     if (CHK && own && x.out) record_probes<T, V>(p, j, B.h[0], x.slot[0], x.pex - p.ex0);
@@ -449,7 +449,7 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
     const int r = j - s;
     const CoefRing<T, V> cr{x.ring + (r & (K - 1)) * (NCOEF * 32 * V)};
     const T en = yee_any<T, V, ENERGY>(A.x[s - 1], B.x[s - 1], A.y[s - 1], A.h[s - 1], A.h[s], cr, p, x.g[s],
-                                       CHK && r == x.src_r, x.src_k, B.h[s], B.x[s], B.y[s]);
+                                       CHK && r >= x.src_r && r < x.src_r1, x.src_k, B.h[s], B.x[s], B.y[s]);
     const bool own = !CHK || (r >= x.r0 && r < x.r1);
     if (ENERGY && own) eacc[s] += (double)en;
     if (CHK && own && x.out) record_probes<T, V>(p, r, B.h[s], x.slot[s], x.pex - p.ex0);
@@ -502,6 +502,7 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   const bool src_lane = p.src_row >= 0 && p.src_col >= c && p.src_col < c + V;
   x.src_k = src_lane ? (int)(p.src_col - c) : -1;
   x.src_r = src_lane ? p.src_row : INT_MIN;
+  x.src_r1 = src_lane ? p.src_row_end : INT_MIN;
 #pragma unroll
   for (int s = 0; s < K; ++s) {
     x.g[s] = T(0);
@@ -548,7 +549,7 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   }
   // the soft source (S2) is applied only by the generic row body: a warp whose strip (halo lanes
   // included) holds the source column takes it for the whole chunk
-  const bool warp_source = __any_sync(FULL, x.src_k >= 0) && p.src_row >= jb - K && p.src_row < je;
+  const bool warp_source = __any_sync(FULL, x.src_k >= 0) && p.src_row_end > jb - K && p.src_row < je;
   // rows [jb, jm): the first stages' rows precede the chunk; [jm, jend): every stage row is the
   // chunk's own (the fast body, unless the chunk holds a probe row); [jend, je): the last rows.
   // Pairs of rows keep the ping-pong parity; the generic body checks rows at run time.
@@ -785,7 +786,10 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   auto goff = [&](const Geo& q, int u, int v) {
     return ((int64_t)q.j0 - M + v - p.row_begin + p.row0) * P + q.i0 - M + u;
   };
-  const int64_t src_off = p.src_row >= 0 ? (int64_t)p.src_row * P + p.src_col : -1;
+  auto is_src = [&](const Geo& q, int u, int v) {  // soft (line) source cell?
+    const int lr = q.j0 - M + v - (int)p.row_begin + p.row0;
+    return p.src_row >= 0 && q.i0 - M + u == p.src_col && lr >= p.src_row && lr < p.src_row_end;
+  };
   // ---- load the region: materials and the fields at step n (asynchronous element copies, all in
   // flight at once: the region rows are not 16-byte aligned)
   for (int b = 0; b < nb; ++b) {
@@ -814,7 +818,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
         const T h0 = q.H[t];
         const T hu = hupd(h0, q.EX[t + q.Wr], q.EX[t], q.EY[v * W1 + u + 1], q.EY[v * W1 + u], p.chy, p.chx);
         T h = q.MA[t] < T(0) ? h0 : hu;  // dead cells keep their Hz (as in yee_row)
-        if (goff(q, u, v) == src_off) h += g[s];
+        if (is_src(q, u, v)) h += g[s];
         if (ENERGY && u >= q.zu0 && u < q.zu1 && v >= q.zv0 && v < q.zv1) {
           // the zone cell's full storage-function term (row_coef's weights without the zone mask)
           bool lx, ly;
@@ -980,6 +984,168 @@ __global__ void __launch_bounds__(512) postk_kernel(const PostParams<T> p) {
   if (threadIdx.x == 0) {
     *p.done = 0u;
     *p.step = step + K;
+  }
+}
+
+// NEXT-2: CPML band fix-up.  Per CTA: one row chunk [r0, r1) of one side; region = columns
+// [c0, c0 + WB), WB = w + 2K + 2, rows [r0 - K, r1 + K - 1) (+ one Ex edge row).  K steps with the
+// sweep's device functions plus, in the layer, psi_hz = b psi_hz + a dEy/dx (Hz -= dt/mu0 psi_hz)
+// and psi_ey = b psi_ey + a dHz/dx (the Ey curl term gains dx psi_ey).  Values go wrong from the
+// region's border inwards one cell per step, so after K steps the write-back columns (the layer
+// and Kz + 1 interior columns) of the chunk's rows are exact; the sweep's plain-Yee values there are
+// overwritten.  Also: the storage-function terms of the write-back cells (their msb marks made the
+// sweep skip them), the probes in them, and the layer's psi state.
+template <typename T, int K, bool ENERGY>
+__global__ void __launch_bounds__(256) pml_kernel(const PmlParams<T> p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[32];
+  const int side = blockIdx.y;
+  const int w = p.w, WB = w + 2 * K + 2, WW = w + p.Kz + 1;
+  const int64_t nx = p.nx, P = p.pitch;
+  const int r0 = p.row0 + blockIdx.x * p.chunk, r1 = min(r0 + p.chunk, p.row0 + p.rows);
+  const int R0 = r0 - K, Hr = (r1 - r0) + 2 * K - 1;  // region cell rows [R0, R0 + Hr)
+  const int64_t c0 = side == 0 ? 0 : nx - WB;          // first region column
+  const int64_t lay0 = side == 0 ? 0 : nx - w;         // first layer column
+  const int64_t wb0 = side == 0 ? 0 : nx - WW, wb1 = side == 0 ? WW : nx;  // write-back columns
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int n = Hr * WB;
+  T* H = reinterpret_cast<T*>(smem_raw);
+  T* MA = H + n;
+  T* MS = MA + n;
+  T* PH = MS + n;              // psi_hz per region cell (0 outside the layer)
+  T* EX = PH + n;              // (Hr + 1) x WB
+  T* EY = EX + n + WB;         // Hr x (WB + 1)
+  T* PE = EY + Hr * (WB + 1);  // psi_ey per region Ey edge
+  const int W1 = WB + 1;
+  const int64_t step = *p.step;
+  auto off = [&](int u, int v) { return (int64_t)(R0 + v) * P + c0 + u; };
+  auto hcol = [&](int64_t gi) { return side == 0 ? (int)gi : (int)(gi - lay0); };  // Hz layer index
+  auto in_layer_h = [&](int64_t gi) { return side == 0 ? gi < w : gi >= lay0; };
+  auto in_layer_e = [&](int64_t gi) { return side == 0 ? (gi >= 1 && gi <= w) : (gi >= lay0 && gi < nx); };
+  auto ecol = [&](int64_t gi) { return side == 0 ? (int)gi : (int)(gi - lay0); };
+  const T* bh = p.bh + side * w; const T* ah = p.ah + side * w;
+  const T* be = p.be + side * (w + 1); const T* ae = p.ae + side * (w + 1);
+  T* psih = p.psih + (int64_t)side * p.psi_rows * w;
+  T* psie = p.psie + (int64_t)side * p.psi_rows * (w + 1);
+  // ---- load the region (fields at step n, materials, psi)
+  for (int t = tid; t < n; t += nt) {
+    const int u = t % WB, v = t / WB;
+    const int64_t o = off(u, v), gi = c0 + u;
+    H[t] = p.hz0[o]; MA[t] = p.mea[o]; MS[t] = p.msb[o];
+    PH[t] = in_layer_h(gi) ? psih[(int64_t)(R0 + v) * w + hcol(gi)] : T(0);
+  }
+  for (int t = tid; t < n + WB; t += nt) EX[t] = p.ex0[off(t % WB, t / WB)];
+  for (int t = tid; t < Hr * W1; t += nt) {
+    const int u = t % W1, v = t / W1;
+    const int64_t gi = c0 + u;
+    EY[t] = p.ey0[off(u, v)];
+    PE[t] = in_layer_e(gi) ? psie[(int64_t)(R0 + v) * (w + 1) + ecol(gi)] : T(0);
+  }
+  __syncthreads();
+  double eacc[K];
+#pragma unroll
+  for (int s = 0; s < K; ++s) eacc[s] = 0.0;
+#pragma unroll 1
+  for (int s = 0; s < K; ++s) {
+    T gsrc = T(0);
+    if (p.src_row >= 0) {
+      const int64_t k = step + s - p.src_t0;
+      if (k >= 0 && k < p.src_n) gsrc = (T)p.src_samples[k];
+    }
+    // ---- H half-step (+ CPML psi_hz, + source, + storage terms of the write-back cells)
+    T ea = T(0);
+    for (int t = tid; t < n; t += nt) {
+      const int u = t % WB, v = t / WB;
+      const int64_t gi = c0 + u;
+      const T h0 = H[t];
+      T h = hupd(h0, EX[t + WB], EX[t], EY[v * W1 + u + 1], EY[v * W1 + u], p.chy, p.chx);
+      if (MA[t] < T(0)) {
+        h = h0;  // dead cells keep their Hz
+      } else if (in_layer_h(gi)) {
+        const int hc = hcol(gi);
+        const T ps = fma_rn(bh[hc], PH[t], mul_rn(ah[hc], mul_rn(p.idx, EY[v * W1 + u + 1] - EY[v * W1 + u])));
+        PH[t] = ps;
+        h = fma_rn(-p.cpsi, ps, h);
+      }
+      const int lr = R0 + v;
+      if (p.src_row >= 0 && gi == p.src_col && lr >= p.src_row && lr < p.src_row_end) h += gsrc;
+      if (ENERGY && gi >= wb0 && gi < wb1 && lr >= r0 && lr < r1) {  // v >= K >= 1 here
+        bool lx, ly = false;
+        T ax, ay = T(0), ca, cb;
+        edge_coef(MA[t - WB], MS[t - WB], MA[t], MS[t], p.idy, ca, cb, ax, lx);
+        if (u >= 1) edge_coef(MA[t - 1], MS[t - 1], MA[t], MS[t], -p.idx, ca, cb, ay, ly);  // u = 0: the x = 0 wall
+        const T wx = lx ? mul_rn(p.wxy, ax) : T(0), wy = ly ? mul_rn(p.wxy, ay) : T(0);
+        const T hw = MA[t] < T(0) ? T(0) : p.wh;
+        ea = cell_energy(ea, EX[t], EY[v * W1 + u], h0, h, wx, wy, hw);
+      }
+      H[t] = h;
+    }
+    if (ENERGY) eacc[s] += (double)ea;
+    __syncthreads();
+    for (int k = tid; k < p.n_probe; k += nt) {  // probes in the write-back cells of the chunk
+      const int64_t gi = p.probe_gi[k];
+      const int lr = p.probe_lr[k];
+      if (gi >= wb0 && gi < wb1 && lr >= r0 && lr < r1)
+        p.probe_ring[(int64_t)k * p.cap + (step + s) % p.cap] = H[(lr - R0) * WB + (gi - c0)];
+    }
+    // ---- E half-step on the region's interior edges (+ CPML psi_ey on the layer's Ey edges)
+    for (int t = WB + tid; t < n; t += nt) {  // Ex edge rows 1 .. Hr-1
+      bool l;
+      T a, ca, cb;
+      edge_coef(MA[t - WB], MS[t - WB], MA[t], MS[t], p.idy, ca, cb, a, l);
+      EX[t] = eupd(EX[t], ca, cb, H[t] - H[t - WB]);
+    }
+    for (int t = tid; t < Hr * (WB - 1); t += nt) {  // Ey edge columns 1 .. WB-1
+      const int u = t % (WB - 1) + 1, v = t / (WB - 1);
+      const int c = v * WB + u;
+      const int64_t gi = c0 + u;
+      bool l;
+      T a, ca, cb;
+      edge_coef(MA[c - 1], MS[c - 1], MA[c], MS[c], -p.idx, ca, cb, a, l);
+      T dh = H[c] - H[c - 1];
+      if (l && in_layer_e(gi)) {
+        const int ec = ecol(gi);
+        const T ps = fma_rn(be[ec], PE[v * W1 + u], mul_rn(ae[ec], mul_rn(p.idx, dh)));
+        PE[v * W1 + u] = ps;
+        dh = fma_rn(p.dxv, ps, dh);
+      }
+      EY[v * W1 + u] = eupd(EY[v * W1 + u], ca, cb, dh);
+    }
+    __syncthreads();
+  }
+  // ---- write back the chunk's write-back cells (Hz, bottom Ex, left Ey) and the layer's psi
+  for (int t = tid; t < n; t += nt) {
+    const int u = t % WB, v = t / WB;
+    const int64_t gi = c0 + u;
+    const int lr = R0 + v;
+    if (gi < wb0 || gi >= wb1 || lr < r0 || lr >= r1) continue;
+    const int64_t o = off(u, v);
+    p.hz1[o] = H[t];
+    p.ex1[o] = EX[t];
+    p.ey1[o] = EY[v * W1 + u];
+    if (in_layer_h(gi)) psih[(int64_t)lr * w + hcol(gi)] = PH[t];
+    if (in_layer_e(gi)) psie[(int64_t)lr * (w + 1) + ecol(gi)] = PE[v * W1 + u];
+  }
+  if (side == 1 && tid < Hr) {  // the right layer's outermost psi_ey column sits at the wall edge nx
+    (void)0;
+  }
+  if (ENERGY) {
+#pragma unroll 1
+    for (int s = 0; s < K; ++s) {
+      const double tot = block_sum(eacc[s], red);
+      if (tid == 0) p.partials[s * p.pstride + p.poff + (int64_t)blockIdx.y * gridDim.x + blockIdx.x] = tot;
+    }
+  }
+}
+
+template <typename T>
+__global__ void band_marks_kernel(T* msb, const T* mea, int64_t pitch, int64_t nx, int row0, int ncol, bool set) {
+  const int r = row0 + blockIdx.x;
+  for (int t = threadIdx.x; t < 2 * ncol; t += blockDim.x) {
+    const int64_t gi = t < ncol ? t : nx - 2 * ncol + t;
+    if (gi < 0 || gi >= nx) continue;
+    const int64_t o = (int64_t)r * pitch + gi;
+    if (mea[o] >= T(0)) msb[o] = set ? -fabs(msb[o]) : fabs(msb[o]);
   }
 }
 
@@ -1177,6 +1343,31 @@ void launch_zone(T* msb, const T* mea, int64_t pitch, const int32_t* rects, int6
   zone_kernel<T><<<(unsigned)n_rect, 256, 0, s>>>(msb, mea, pitch, rects, row_begin, row0, Kz, set);
 }
 
+template <typename T, int K>
+void pml_launch(const PmlParams<T>& p, bool energy, cudaStream_t s) {
+  const int WB = p.w + 2 * K + 2, Hr = p.chunk + 2 * K - 1;
+  const size_t smem = sizeof(T) * ((size_t)5 * Hr * WB + WB + (size_t)2 * Hr * (WB + 1));
+  dim3 grid((p.rows + p.chunk - 1) / p.chunk, 2);
+  auto kern = energy ? pml_kernel<T, K, true> : pml_kernel<T, K, false>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<grid, 256, smem, s>>>(p);
+}
+
+template <typename T>
+void launch_pml(const PmlParams<T>& p, int K, bool energy, cudaStream_t s) {
+  if (p.w <= 0 || p.rows <= 0) return;
+  if (K == 1) pml_launch<T, 1>(p, energy, s);
+  else if (K == 2) pml_launch<T, 2>(p, energy, s);
+  else if constexpr (sizeof(T) == 4) pml_launch<T, 4>(p, energy, s);
+}
+
+template <typename T>
+void launch_band_marks(T* msb, const T* mea, int64_t pitch, int64_t nx, int row0, int rows, int ncol, bool set,
+                       cudaStream_t s) {
+  if (rows <= 0 || ncol <= 0) return;
+  band_marks_kernel<T><<<rows, 128, 0, s>>>(msb, mea, pitch, nx, row0, ncol, set);
+}
+
 #define INST(T)                                                                                     \
   template void launch_sweep<T>(const SweepParams<T>&, int, int, cudaStream_t, int, int);         \
   template void launch_post<T>(const PostParams<T>&, int, bool, cudaStream_t);                   \
@@ -1187,6 +1378,8 @@ void launch_zone(T* msb, const T* mea, int64_t pitch, const int32_t* rects, int6
                                             cudaStream_t);                                                \
   template void launch_zone<T>(T*, const T*, int64_t, const int32_t*, int64_t, int64_t, int, int, bool,   \
                                cudaStream_t);                                                             \
+  template void launch_pml<T>(const PmlParams<T>&, int, bool, cudaStream_t);                             \
+  template void launch_band_marks<T>(T*, const T*, int64_t, int64_t, int, int, int, bool, cudaStream_t);  \
   template void launch_mask<T>(T*, T* [6], int64_t, const int32_t*, int64_t, int64_t, int, bool, cudaStream_t);
 INST(float)
 INST(double)

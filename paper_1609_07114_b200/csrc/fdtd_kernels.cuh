@@ -26,7 +26,8 @@ struct SweepParams {
   int chunk;       // rows per CTA
   int chunk0;      // first row chunk of this launch (split launches overlap the halo exchange)
   T chx, chy;      // dt/(mu0 dx), dt/(mu0 dy)
-  int src_row;     // local row of the soft source (-1: none)
+  int src_row;     // local rows [src_row, src_row_end) of the soft (line) source at column src_col (-1: none)
+  int src_row_end;
   int64_t src_col;
   const double* src_samples; int64_t src_n, src_t0;
   const int64_t* step;  // device step counter (value n during the pass starting at step n)
@@ -78,7 +79,7 @@ struct PostParams {
   const int32_t* zp_off; const int32_t* zp;  // zone probes per instance: (gi, gj, probe index)
   T* probe_ring; int64_t cap;
   T chx, chy, idx, idy, wxy, wh;
-  int src_row; int64_t src_col; const double* src_samples; int64_t src_n, src_t0;
+  int src_row, src_row_end; int64_t src_col; const double* src_samples; int64_t src_n, src_t0;
   const double* sweep_partials; int64_t n_sweep_partials, pstride;  // [s * pstride + cta]
   double* rom_partials;            // [s * n_inst + instance]: ROM + zone energy of step n+s
   double* level1;                  // [s * gridDim.x + cta]
@@ -87,6 +88,32 @@ struct PostParams {
   int block;         // threads per CTA
   size_t smem_bytes; // dynamic shared memory of the launch (max over batches)
 };
+
+// CPML band fix-up (NEXT-2): the sweep advances the two x-end layers with the plain Yee update; per
+// row chunk and side this kernel recomputes the K steps on the band [layer + 2K + 2 columns] x
+// [chunk rows +- K] from the pass's input buffer with the CPML terms (Roden-Gedney, kappa 1, alpha 0)
+// and writes back the layer plus Kz + 1 interior columns (the sweep skipped their energy: msb marks).
+template <typename T>
+struct PmlParams {
+  const T* ex0; const T* ey0; const T* hz0;
+  T* ex1; T* ey1; T* hz1;
+  const T* mea; const T* msb;
+  int64_t pitch, nx;
+  int rows, row0, chunk;       // owned rows, local row of the first, rows per CTA
+  int w, Kz;                   // layer width (cells); zone depth (write-back = w + Kz + 1 columns)
+  const T* bh; const T* ah;    // per side [2][w]: Hz columns, index = distance into the layer
+  const T* be; const T* ae;    // per side [2][w + 1]: Ey columns
+  T* psih; T* psie;            // [2][rows_alloc][w], [2][rows_alloc][w + 1]
+  int64_t psi_rows;            // rows_alloc
+  T chx, chy, idx, idy, wxy, wh, cpsi, dxv;  // cpsi = dt / mu0, dxv = dx
+  int src_row, src_row_end; int64_t src_col; const double* src_samples; int64_t src_n, src_t0;
+  const int64_t* step;
+  int n_probe; const int64_t* probe_gi; const int32_t* probe_lr; T* probe_ring; int64_t cap;
+  double* partials; int64_t pstride, poff;  // energy: partials[s * pstride + poff + cta]
+};
+template <typename T>
+void launch_pml(const PmlParams<T>& p, int K, bool energy, cudaStream_t s);
+inline int pml_ctas(int rows, int chunk) { return 2 * ((rows + chunk - 1) / chunk); }
 
 template <typename T>
 void launch_sweep(const SweepParams<T>& p, int K, int warps_per_cta, cudaStream_t s, int chunk_begin = 0,
@@ -125,6 +152,10 @@ void launch_min2(const M* a, const M* b, int64_t n, double* out /*2 per block*/,
 template <typename T>
 void launch_mask(T* mea, T* fields[6], int64_t pitch, const int32_t* rects, int64_t n_rect, int64_t row_begin,
                  int row0, bool zero_iface, cudaStream_t s);
+// sign bit of msb on the columns [0, ncol) and [nx - ncol, nx) of every owned row (PML bands)
+template <typename T>
+void launch_band_marks(T* msb, const T* mea, int64_t pitch, int64_t nx, int row0, int rows, int ncol, bool set,
+                       cudaStream_t s);
 // sign bit of msb on the zone cells of every instance (depth Kz; set or clear), holes excluded
 template <typename T>
 void launch_zone(T* msb, const T* mea, int64_t pitch, const int32_t* rects, int64_t n_rect, int64_t row_begin,

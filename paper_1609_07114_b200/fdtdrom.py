@@ -73,6 +73,8 @@ def lib():
         L.fdtd_create.argtypes = [C.POINTER(GridDesc), C.POINTER(vp)]
         L.fdtd_add_rom.argtypes = [vp, C.POINTER(RomModel), vp, i64, C.POINTER(i32)]
         L.fdtd_set_source.argtypes = [vp, i64, i64, vp, i64, i64]
+        L.fdtd_set_source_line.argtypes = [vp, i64, i64, i64, vp, i64, i64]
+        L.fdtd_set_pml.argtypes = [vp, i32, i32, C.c_double]
         L.fdtd_set_probes.argtypes = [vp, vp, i32]
         L.fdtd_record_energy.argtypes = [vp, i32]
         L.fdtd_step.argtypes = [vp, i64]
@@ -97,7 +99,8 @@ def lib():
         L.fdtd_destroy.restype = None
         for n in ("create", "add_rom", "set_source", "set_probes", "record_energy", "step", "probe", "energy",
                   "get_window", "set_window", "get_rom_state", "set_rom_state", "sync", "get_info", "set_tuning",
-                  "nccl_unique_id", "profile", "profile_read", "step_group", "set_time_blocking"):
+                  "nccl_unique_id", "profile", "profile_read", "step_group", "set_time_blocking",
+                  "set_source_line", "set_pml"):
             getattr(L, "fdtd_" + n).restype = C.c_int
         _lib = L
     return _lib
@@ -232,6 +235,14 @@ class Simulation:
     def set_source(self, i, j, samples, step0=0):
         s = _f64(samples)
         self._ck(lib().fdtd_set_source(self._h, int(i), int(j), _ptr(s), s.size, int(step0)), "fdtd_set_source")
+
+    def set_source_line(self, i, j0, j1, samples, step0=0):
+        s = _f64(samples)
+        self._ck(lib().fdtd_set_source_line(self._h, int(i), int(j0), int(j1), _ptr(s), s.size, int(step0)),
+                 "fdtd_set_source_line")
+
+    def set_pml(self, width, order=3, r0=1e-8):
+        self._ck(lib().fdtd_set_pml(self._h, int(width), int(order), float(r0)), "fdtd_set_pml")
 
     def set_probes(self, ij):
         a = np.ascontiguousarray(np.asarray(ij, dtype=np.int64).reshape(-1, 2))

@@ -24,8 +24,13 @@ def oracle_from_scene(scene, source=True, probes=True):
             for kk, i0, j0 in scene.placements:
                 if kk == k:
                     s.add_rom(m, int(i0), int(j0))
+    if "pml" in scene.meta:
+        s.set_pml(*scene.meta["pml"])
     if source:
-        s.set_source(*scene.source, scene.samples)
+        if "source_rows" in scene.meta:
+            s.set_source_line(scene.source[0], *scene.meta["source_rows"], scene.samples)
+        else:
+            s.set_source(*scene.source, scene.samples)
     if probes:
         s.set_probes(scene.probes)
     return s
@@ -35,13 +40,18 @@ def gpu_from_scene(scene, source=True, probes=True, **kw):
     from paper_1609_07114_b200 import Simulation
     eps, sig = np_materials(scene)
     sim = Simulation(scene.nx, scene.ny, scene.dx, scene.dy, scene.dt, eps, sig, precision=scene.precision, **kw)
+    if "pml" in scene.meta:
+        sim.set_pml(*scene.meta["pml"])
     if scene.placements is not None:
         for k, m in enumerate(scene.models):
             sel = scene.placements[scene.placements[:, 0] == k]
             if len(sel):
                 sim.add_rom(m, sel[:, 1:3])
     if source:
-        sim.set_source(*scene.source, scene.samples)
+        if "source_rows" in scene.meta:
+            sim.set_source_line(scene.source[0], *scene.meta["source_rows"], scene.samples)
+        else:
+            sim.set_source(*scene.source, scene.samples)
     if probes:
         sim.set_probes(scene.probes)
     return sim
