@@ -229,7 +229,8 @@ fdtd_status fdtd_set_time_blocking(fdtd_ctx *c, int32_t steps_per_pass);
  * psi_ey = b psi_ey + a dHz/dx (Ey's curl term -dHz/dx becomes -(dHz/dx + psi_ey)).  width 0
  * removes the layers.  The layer cells stay in the storage function (their standard terms).
  * FDTD_E_ARG with several ranks, when 2 (width + 4) > nx, or when a ROM instance's ring comes
- * within width + 4 cells of an x-end.  Resets the auxiliary state. */
+ * within 3 cells of a layer (K-step passes need 2K + 1; shallower passes are used otherwise).
+ * Resets the auxiliary state. */
 fdtd_status fdtd_set_pml(fdtd_ctx *c, int32_t width, int32_t order, double r0);
 
 /* Tuning knobs for the fused sweep (rows per CTA, warps per CTA); 0 keeps default. */

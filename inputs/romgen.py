@@ -314,7 +314,11 @@ def _sprim_basis_m(csys, m, fmax, defl_tol=1e-10):
 
 
 def _orth(A, tol=1e-12):
-    U, s, _ = np.linalg.svd(A, full_matrices=False)
+    try:
+        U, s, _ = np.linalg.svd(A, full_matrices=False)
+    except np.linalg.LinAlgError:  # gesdd can fail to converge on ill-scaled bases; gesvd does not
+        import scipy.linalg as sla
+        U, s, _ = sla.svd(A, full_matrices=False, lapack_driver="gesvd")
     k = int(np.sum(s > tol * s[0])) if s.size and s[0] > 0 else 0
     return U[:, :k]
 

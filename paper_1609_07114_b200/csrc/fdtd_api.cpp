@@ -591,11 +591,14 @@ fdtd_status upload_roms(fdtd_ctx* c) {
 bool passes_valid(const fdtd_ctx* c, int K) {
   if (K > c->V) return false;  // a halo lane of V columns covers at most V steps of error spread
   const int64_t M = 2 * K - 1;
-  if (c->pml_w > 0) {  // every fix-up region clear of the CPML bands (each kernel ignores the other's physics)
+  if (c->pml_w > 0) {  // ROM rings 2K + 1 cells clear of the CPML layers: neither fix-up then sees the
+                       // other's physics within the K steps (the band region may hold ROM edges it never
+                       // updates, the ROM region no layer cell)
     const int64_t WB = c->pml_w + 2 * K + 2;
     if (2 * WB > c->d.nx) return false;
     for (size_t r = 0; r < c->rects.size(); r += 4)
-      if (c->rects[r] - M < WB || c->rects[r] + c->rects[r + 2] + M > c->d.nx - WB) return false;
+      if (c->rects[r] - 1 < c->pml_w + 2 * K + 1 || c->rects[r] + c->rects[r + 2] + 1 > c->d.nx - c->pml_w - 2 * K - 1)
+        return false;
   }
   if (K == 1) return true;
   struct Rc { int64_t i0, j0, bx, by; };
@@ -993,7 +996,7 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
       return fail(c, FDTD_E_ARG, "instance %lld: footprint + ring leaves the grid", (long long)k);
     if (j0 - 1 < c->d.row_begin || j0 + by > c->d.row_end - 1)
       return fail(c, FDTD_E_ARG, "instance %lld: footprint + ring straddles this rank's rows", (long long)k);
-    if (c->pml_w > 0 && (i0 - 1 < c->pml_w + 4 || i0 + bx + 1 > c->d.nx - c->pml_w - 4))
+    if (c->pml_w > 0 && (i0 - 1 < c->pml_w + 3 || i0 + bx + 1 > c->d.nx - c->pml_w - 3))
       return fail(c, FDTD_E_ARG, "instance %lld lies within the CPML band", (long long)k);
   }
   {
@@ -1562,8 +1565,8 @@ fdtd_status fdtd_set_pml(fdtd_ctx* c, int32_t width, int32_t order, double r0) {
   if (width > 0 && c->d.nranks > 1) return fail(c, FDTD_E_ARG, "CPML layers need a single rank (row slabs: NEXT)");
   if (2 * (width + 4) > c->d.nx) return fail(c, FDTD_E_ARG, "CPML layers of %d cells do not fit nx = %lld", width,
                                              (long long)c->d.nx);
-  for (size_t r = 0; width > 0 && r < c->rects.size(); r += 4)  // one-step band (width + 4) clear of every ring
-    if (c->rects[r] - 1 < width + 4 || c->rects[r] + c->rects[r + 2] + 1 > c->d.nx - width - 4)
+  for (size_t r = 0; width > 0 && r < c->rects.size(); r += 4)  // rings 3 cells clear of the layers (K = 1)
+    if (c->rects[r] - 1 < width + 3 || c->rects[r] + c->rects[r + 2] + 1 > c->d.nx - width - 3)
       return fail(c, FDTD_E_ARG, "a ROM instance lies within the CPML band");
   fdtd_status st;
   for (void** pp : {&c->d_pml_bh, &c->d_pml_ah, &c->d_pml_be, &c->d_pml_ae, &c->d_psih, &c->d_psie})
