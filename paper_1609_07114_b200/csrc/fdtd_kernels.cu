@@ -109,6 +109,9 @@ __device__ __forceinline__ void cp_async_el(T* dst, const T* src) {
                "n"(sizeof(T)) : "memory");
 }
 
+#ifndef FDTD_REG_RING  // sweep: coefficient ring of K rows in registers (1) or shared memory (0)
+#define FDTD_REG_RING 0
+#endif
 #ifndef FDTD_PFD
 #define FDTD_PFD 1  // sweep: row distance of the L2 prefetch beyond the register-prefetched row (measured best)
 #endif
@@ -144,12 +147,13 @@ __device__ __forceinline__ void edge_coef(T a0, T s0, T a1, T s1, T il, T& ca, T
   a = a0 + a1;
   const T s = fabs(s0) + fabs(s1);
   live = (a0 >= T(0)) & (a1 >= T(0));
-  const T r = rcp_rn(a + s);
+  // r = 0 on a dead edge makes ca = 1 and cb = 0 (the edge keeps its value) with one select
+  const T r = live ? rcp_rn(a + s) : T(0);
   // ca = 1 - 2 s r: exactly 1 on lossless edges whatever the rounding of r (an approximate
   // reciprocal only perturbs the small loss term and the curl gain, so a lossless grid stays
   // lossless instead of decaying by ~1 ulp per step)
-  ca = live ? fma_rn(T(-2) * s, r, T(1)) : T(1);
-  cb = live ? mul_rn(r, il) : T(0);
+  ca = fma_rn(T(-2) * s, r, T(1));
+  cb = mul_rn(r, il);
 }
 
 template <typename T>
@@ -386,12 +390,13 @@ struct StageOut {
 
 template <typename T, int V, int K>
 struct SweepCtx {
-  const T *pex, *pey, *phz, *pma, *pms;  // this lane's column in row 0 of each input array
-  T *pex1, *pey1, *phz1;                 // ... and of each output array
+  uint32_t c, P;  // this lane's first column (row-0 element offset) and the row pitch: every array
+                  // holds < 2^32 elements (fdtd_create), so element offsets stay 32-bit and each
+                  // address is one wide multiply-add on the array's base pointer
   T* ring;
   int lane, r0, r1, src_r, src_r1, src_k;  // source rows [src_r, src_r1) in this lane's column src_k
   bool out;
-  int64_t step, P;
+  int64_t step;
   T g[K];
   int64_t slot[K];  // probe-ring slot of each stage's step
 };
@@ -411,56 +416,67 @@ __device__ __forceinline__ T yee_any(const T (&exb)[V], const T (&ext)[V], const
     return yee_row<T, V, ENERGY>(exb, ext, ey, hz, hb, cs, p, gsrc, srow, src_k, hn, exo, eyo);
 }
 
-template <typename T, int V, int K, bool ENERGY, bool CHK>
+template <typename T, int V, int K, bool ENERGY, bool CHK, int T0>
 __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCtx<T, V, K>& x, int j, int je,
                                           const RowIn<T, V>& X, RowIn<T, V>& Y, const StageOut<T, V, K>& A,
-                                          StageOut<T, V, K>& B, double (&eacc)[K]) {
+                                          StageOut<T, V, K>& B, double (&eacc)[K], RowCoef<T, V> (&rc)[K]) {
+  // T0 = (j - jb) mod the loop's unroll: the coefficient set of row j - s lives in rc[(T0 - s) mod K]
+  // (registers, statically named; FDTD_REG_RING) or in the shared-memory ring
   // CHK: some stage rows may lie outside the chunk [r0, r1) (energy, probes and stores skip them)
   // and the probe table is consulted; without CHK every stage row is the chunk's own, probe-free.
   {  // ---- stage 0: step n on row j (builds the row's coefficients and parks them in the ring)
+#if FDTD_REG_RING
+    RowCoef<T, V>& cf = rc[T0 & (K - 1)];
+    row_coef<T, V>(X.ma, X.ms, Y.ma, Y.ms, p.idx, p.idy, p.wxy, p.wh, cf);
+#else
     RowCoef<T, V> cf;
     row_coef<T, V>(X.ma, X.ms, Y.ma, Y.ms, p.idx, p.idy, p.wxy, p.wh, cf);
     if (K > 1) ring_store<T, V>(x.ring, j & (K - 1), cf);
+#endif
     const T en = yee_any<T, V, ENERGY>(Y.ext, X.ext, X.ey, X.hz, A.h[0], CoefRegs<T, V>{cf}, p, x.g[0],
                                        CHK && j >= x.src_r && j < x.src_r1, x.src_k, B.h[0], B.x[0], B.y[0]);
     const bool own = !CHK || (j >= x.r0 && j < x.r1);
     if (ENERGY && own) eacc[0] += (double)en;
-    if (CHK && own && x.out) record_probes<T, V>(p, j, B.h[0], x.slot[0], x.pex - p.ex0);
+    if (CHK && own && x.out) record_probes<T, V>(p, j, B.h[0], x.slot[0], (int32_t)x.c);
   }
   if (j + 1 < je) {  // row j+1 into the buffer of row j-1 (consumed above)
-    const uint32_t o = (uint32_t)(j + 1) * (uint32_t)x.P;  // arrays hold < 2^32 elements (fdtd_create)
-    ldv(x.pex + o + x.P, Y.ext);
-    ldv(x.pey + o, Y.ey);
-    ldv(x.phz + o, Y.hz);
-    ldv(x.pma + o, Y.ma);
-    ldv(x.pms + o, Y.ms);
+    const uint32_t o = (uint32_t)(j + 1) * x.P + x.c;
+    ldv(p.ex0 + (o + x.P), Y.ext);
+    ldv(p.ey0 + o, Y.ey);
+    ldv(p.hz0 + o, Y.hz);
+    ldv(p.mea + o, Y.ma);
+    ldv(p.msb + o, Y.ms);
   }
   if (PFD > 0 && j + 1 + PFD < je) {  // pull row j+1+PFD into L2 (no registers held)
-    const uint32_t o = (uint32_t)(j + 1 + PFD) * (uint32_t)x.P;
-    prefetch_l2(x.pex + o + x.P);
-    prefetch_l2(x.pey + o);
-    prefetch_l2(x.phz + o);
-    prefetch_l2(x.pma + o);
-    prefetch_l2(x.pms + o);
+    const uint32_t o = (uint32_t)(j + 1 + PFD) * x.P + x.c;
+    prefetch_l2(p.ex0 + (o + x.P));
+    prefetch_l2(p.ey0 + o);
+    prefetch_l2(p.hz0 + o);
+    prefetch_l2(p.mea + o);
+    prefetch_l2(p.msb + o);
   }
   // ---- stage s: step n+s on row j-s, from stage s-1's outputs of rows j-s (A) and j-s+1 (B)
 #pragma unroll
   for (int s = 1; s < K; ++s) {
     const int r = j - s;
+#if FDTD_REG_RING
+    const CoefRegs<T, V> cr{rc[(T0 - s) & (K - 1)]};
+#else
     const CoefRing<T, V> cr{x.ring + (r & (K - 1)) * (NCOEF * 32 * V)};
+#endif
     const T en = yee_any<T, V, ENERGY>(A.x[s - 1], B.x[s - 1], A.y[s - 1], A.h[s - 1], A.h[s], cr, p, x.g[s],
                                        CHK && r >= x.src_r && r < x.src_r1, x.src_k, B.h[s], B.x[s], B.y[s]);
     const bool own = !CHK || (r >= x.r0 && r < x.r1);
     if (ENERGY && own) eacc[s] += (double)en;
-    if (CHK && own && x.out) record_probes<T, V>(p, r, B.h[s], x.slot[s], x.pex - p.ex0);
+    if (CHK && own && x.out) record_probes<T, V>(p, r, B.h[s], x.slot[s], (int32_t)x.c);
   }
   // stage K-1's outputs are the fields at step n+K of row j-K+1
   const int rs = j - (K - 1);
   if (x.out && (!CHK || (rs >= x.r0 && rs < x.r1))) {
-    const uint32_t o = (uint32_t)rs * (uint32_t)x.P;
-    stv(x.phz1 + o, B.h[K - 1]);
-    stv(x.pex1 + o, B.x[K - 1]);
-    stv(x.pey1 + o, B.y[K - 1]);
+    const uint32_t o = (uint32_t)rs * x.P + x.c;
+    stv(p.hz1 + o, B.h[K - 1]);
+    stv(p.ex1 + o, B.x[K - 1]);
+    stv(p.ey1 + o, B.y[K - 1]);
   }
 }
 
@@ -476,11 +492,19 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
 #ifndef FDTD_SWEEP_THREADS  // at most 8 warps per CTA (fdtd_set_tuning)
 #define FDTD_SWEEP_THREADS 256
 #endif
+#if FDTD_REG_RING && !defined(FDTD_SWEEP_MAXNREG)  // register ring: per-thread register cap
+#define FDTD_SWEEP_MAXNREG 168
+#endif
 #ifndef FDTD_SWEEP_MINB  // 2 x 256 threads: <= 128 registers, 16 resident warps per SM
-#define FDTD_SWEEP_MINB 2
+#define FDTD_SWEEP_MINB (FDTD_REG_RING ? 1 : 2)
 #endif
 template <typename T, int K, int V, bool ENERGY>
-__global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_kernel(const SweepParams<T> p) {
+#if defined(FDTD_SWEEP_MAXNREG)
+__global__ void __maxnreg__(FDTD_SWEEP_MAXNREG) sweepk_kernel(
+#else
+__global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_kernel(
+#endif
+    const SweepParams<T> p) {
   constexpr int HL = (K + V - 1) / V;  // halo lanes at each end of a warp (sweep_halo)
   constexpr int NOUT = 32 - 2 * HL;    // storing lanes per warp
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -495,10 +519,9 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   const int cy = p.chunk0 + blockIdx.y;  // row chunk
   x.r0 = p.row0 + cy * p.chunk;
   x.r1 = min(x.r0 + p.chunk, p.row0 + p.rows);
-  x.P = p.pitch;
+  x.P = (uint32_t)p.pitch;
+  x.c = (uint32_t)c;  // c >= -V: row offsets (>= one pitch) keep every element offset non-negative
   x.step = *p.step;
-  x.pex = p.ex0 + c; x.pey = p.ey0 + c; x.phz = p.hz0 + c; x.pma = p.mea + c; x.pms = p.msb + c;
-  x.pex1 = p.ex1 + c; x.pey1 = p.ey1 + c; x.phz1 = p.hz1 + c;
   const bool src_lane = p.src_row >= 0 && p.src_col >= c && p.src_col < c + V;
   x.src_k = src_lane ? (int)(p.src_col - c) : -1;
   x.src_r = src_lane ? p.src_row : INT_MIN;
@@ -515,16 +538,16 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   const int jb = x.r0 - K, je = x.r1 + K - 1;  // stage-0 rows [jb, je); jb - 1 >= 0 (ROW0 = 2 KMAX)
   RowIn<T, V> R0, R1;  // rows jb-1 (only Ex of edge row jb and the materials are used) and jb
   {
-    const int64_t o = (int64_t)(jb - 1) * x.P;
-    ldv(x.pex + o + x.P, R0.ext);
-    ldv(x.pma + o, R0.ma);
-    ldv(x.pms + o, R0.ms);
-    const int64_t o1 = o + x.P;
-    ldv(x.pex + o1 + x.P, R1.ext);
-    ldv(x.pey + o1, R1.ey);
-    ldv(x.phz + o1, R1.hz);
-    ldv(x.pma + o1, R1.ma);
-    ldv(x.pms + o1, R1.ms);
+    const uint32_t o = (uint32_t)(jb - 1) * x.P + x.c;
+    ldv(p.ex0 + (o + x.P), R0.ext);
+    ldv(p.mea + o, R0.ma);
+    ldv(p.msb + o, R0.ms);
+    const uint32_t o1 = o + x.P;
+    ldv(p.ex0 + (o1 + x.P), R1.ext);
+    ldv(p.ey0 + o1, R1.ey);
+    ldv(p.hz0 + o1, R1.hz);
+    ldv(p.mea + o1, R1.ma);
+    ldv(p.msb + o1, R1.ms);
   }
   StageOut<T, V, K> O0, O1;
 #pragma unroll
@@ -553,15 +576,33 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   // rows [jb, jm): the first stages' rows precede the chunk; [jm, jend): every stage row is the
   // chunk's own (the fast body, unless the chunk holds a probe row); [jend, je): the last rows.
   // Pairs of rows keep the ping-pong parity; the generic body checks rows at run time.
-  const int jm = min(jb + ((x.r0 + K - 1 - jb + 1) & ~1), je);
-  const int jend = (warp_probes || warp_source) ? jm : jm + (max(x.r1 - jm, 0) & ~1);
-  for (int j = jb; j < je; j += 2) {
+  // Groups of U rows keep the ping-pong parity and (register ring) the static coefficient slots.
+  constexpr int U = (FDTD_REG_RING && K > 2) ? K : 2;
+  RowCoef<T, V> rc[K];
+#if FDTD_REG_RING
+#pragma unroll
+  for (int s = 0; s < K; ++s)
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      rc[s].cax[k] = rc[s].cbx[k] = rc[s].cay[k] = rc[s].cby[k] = rc[s].wx[k] = rc[s].wy[k] = rc[s].hw[k] = T(0);
+#endif
+  const int jm = min(jb + ((x.r0 + K - jb + U - 1) / U) * U, je);
+  const int jend = (warp_probes || warp_source) ? jm : jm + (max(x.r1 - jm, 0) / U) * U;
+  for (int j = jb; j < je; j += U) {
     if (j >= jm && j < jend) {
-      sweep_row<T, V, K, ENERGY, false>(p, x, j, je, R1, R0, O0, O1, eacc);
-      sweep_row<T, V, K, ENERGY, false>(p, x, j + 1, je, R0, R1, O1, O0, eacc);
+      sweep_row<T, V, K, ENERGY, false, 0>(p, x, j, je, R1, R0, O0, O1, eacc, rc);
+      sweep_row<T, V, K, ENERGY, false, 1>(p, x, j + 1, je, R0, R1, O1, O0, eacc, rc);
+      if constexpr (U == 4) {
+        sweep_row<T, V, K, ENERGY, false, 2>(p, x, j + 2, je, R1, R0, O0, O1, eacc, rc);
+        sweep_row<T, V, K, ENERGY, false, 3>(p, x, j + 3, je, R0, R1, O1, O0, eacc, rc);
+      }
     } else {
-      sweep_row<T, V, K, ENERGY, true>(p, x, j, je, R1, R0, O0, O1, eacc);
-      if (j + 1 < je) sweep_row<T, V, K, ENERGY, true>(p, x, j + 1, je, R0, R1, O1, O0, eacc);
+      sweep_row<T, V, K, ENERGY, true, 0>(p, x, j, je, R1, R0, O0, O1, eacc, rc);
+      if (j + 1 < je) sweep_row<T, V, K, ENERGY, true, 1>(p, x, j + 1, je, R0, R1, O1, O0, eacc, rc);
+      if constexpr (U == 4) {
+        if (j + 2 < je) sweep_row<T, V, K, ENERGY, true, 2>(p, x, j + 2, je, R1, R0, O0, O1, eacc, rc);
+        if (j + 3 < je) sweep_row<T, V, K, ENERGY, true, 3>(p, x, j + 3, je, R0, R1, O1, O0, eacc, rc);
+      }
     }
   }
   if (!x.out) {
@@ -1259,7 +1300,7 @@ template void launch_min2<double>(const double*, const double*, int64_t, double*
 template <typename T, int K>
 void sweepk_launch(const SweepParams<T>& q, dim3 grid, int threads, cudaStream_t s) {
   constexpr int V = (sizeof(T) == 4 && K < 4) ? 4 : 2;  // sweep_width
-  const size_t smem = K > 1 ? (size_t)(threads / 32) * K * NCOEF * 32 * V * sizeof(T) : 0;
+  const size_t smem = (K > 1 && !FDTD_REG_RING) ? (size_t)(threads / 32) * K * NCOEF * 32 * V * sizeof(T) : 0;
   if (q.partials) {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(sweepk_kernel<T, K, V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
