@@ -228,9 +228,10 @@ fdtd_status fdtd_set_time_blocking(fdtd_ctx *c, int32_t steps_per_pass);
  * b = exp(-sigma dt / eps0), a = b - 1; psi_hz = b psi_hz + a dEy/dx (Hz -= dt/mu0 psi_hz),
  * psi_ey = b psi_ey + a dHz/dx (Ey's curl term -dHz/dx becomes -(dHz/dx + psi_ey)).  width 0
  * removes the layers.  The layer cells stay in the storage function (their standard terms).
- * FDTD_E_ARG with several ranks, when 2 (width + 4) > nx, or when a ROM instance's ring comes
- * within 3 cells of a layer (K-step passes need 2K + 1; shallower passes are used otherwise).
- * Resets the auxiliary state. */
+ * With row slabs every rank calls it with the same arguments; the psi rows of the ghost rows
+ * travel with the halo exchange (psi_ey with Ey, psi_hz with Hz).  FDTD_E_ARG when
+ * 2 (width + 4) > nx, or when a ROM instance's ring comes within 3 cells of a layer (K-step
+ * passes need 2K + 1; shallower passes are used otherwise).  Resets the auxiliary state. */
 fdtd_status fdtd_set_pml(fdtd_ctx *c, int32_t width, int32_t order, double r0);
 
 /* Tuning knobs for the fused sweep (rows per CTA, warps per CTA); 0 keeps default. */

@@ -58,6 +58,9 @@ def lib():
         L.osim_set_source_line.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, _dp, C.c_int64, C.c_int64]
         L.osim_set_pml.restype = C.c_int
         L.osim_set_pml.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double]
+        for n in ("osim_get_psi", "osim_set_psi"):
+            getattr(L, n).restype = C.c_int
+            getattr(L, n).argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.osim_set_probes.argtypes = [C.c_void_p, _ip, C.c_int]
         L.osim_step.argtypes = [C.c_void_p, C.c_int64, _dp, C.c_int64, _dp]
         L.osim_get_state.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp]
@@ -149,6 +152,19 @@ class OracleSim:
         rc = lib().osim_set_pml(self._h, int(width), int(order), float(r0))
         if rc != 0:
             raise ValueError("osim_set_pml failed with code %d" % rc)
+
+    def get_psi(self):
+        """CPML auxiliary state (psi_hz [ny, nx], psi_ey [ny, nx + 1]); state only."""
+        ph, pe = np.zeros((self.ny, self.nx)), np.zeros((self.ny, self.nx + 1))
+        if lib().osim_get_psi(self._h, _p(ph), _p(pe)) != 0:
+            raise ValueError("no CPML layers")
+        return ph, pe
+
+    def set_psi(self, psi_hz, psi_ey):
+        ph, pe = _f64(psi_hz), _f64(psi_ey)
+        assert ph.size == self.ny * self.nx and pe.size == self.ny * (self.nx + 1)
+        if lib().osim_set_psi(self._h, _p(ph), _p(pe)) != 0:
+            raise ValueError("no CPML layers")
 
     def set_probes(self, ij):
         a = np.ascontiguousarray(np.asarray(ij, dtype=np.int32).reshape(-1, 2))

@@ -210,6 +210,21 @@ int osim_set_pml(osim *s, int w, int order, double r0) {
   return 0;
 }
 
+/* CPML state accessors (row-slab tests exchange psi rows): psi_hz ny x nx, psi_ey ny x (nx + 1);
+   returns -1 without layers.  State only, no arithmetic. */
+int osim_get_psi(const osim *s, double *psi_hz, double *psi_ey) {
+  if (s->pml_w <= 0) return -1;
+  memcpy(psi_hz, s->psi_hz, sizeof(double) * (size_t)s->nx * s->ny);
+  memcpy(psi_ey, s->psi_ey, sizeof(double) * (size_t)(s->nx + 1) * s->ny);
+  return 0;
+}
+int osim_set_psi(osim *s, const double *psi_hz, const double *psi_ey) {
+  if (s->pml_w <= 0) return -1;
+  memcpy(s->psi_hz, psi_hz, sizeof(double) * (size_t)s->nx * s->ny);
+  memcpy(s->psi_ey, psi_ey, sizeof(double) * (size_t)(s->nx + 1) * s->ny);
+  return 0;
+}
+
 static int in_pml_col(const osim *s, int i) { return s->pml_w > 0 && (i < s->pml_w || i >= s->nx - s->pml_w); }
 
 void osim_destroy(osim *s) {

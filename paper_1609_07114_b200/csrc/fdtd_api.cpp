@@ -306,6 +306,15 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q, int K) {
   return p;
 }
 
+// CPML state buffer q (0/1) of psi_hz (e = 0: w columns per row) or psi_ey (e = 1: w + 1 columns),
+// both sides: [buffer][side][row][column]
+inline char* psi_base(const fdtd_ctx* c, int e, int q, int side) {
+  const int64_t rw = e ? c->pml_w + 1 : c->pml_w;
+  return (char*)(e ? c->d_psie : c->d_psih) + (size_t)((2 * q + side) * c->nrows_alloc * rw) * c->es;
+}
+template <typename T>
+T* psi_buf(const fdtd_ctx* c, int e, int q) { return (T*)psi_base(c, e, q, 0); }
+
 template <typename T>
 fdtd::PmlParams<T> pml_params(fdtd_ctx* c, int q) {
   fdtd::PmlParams<T> p{};
@@ -315,7 +324,9 @@ fdtd::PmlParams<T> pml_params(fdtd_ctx* c, int q) {
   p.pitch = c->pitch; p.nx = c->d.nx; p.rows = c->rows; p.row0 = ROW0; p.chunk = PML_CHUNK;
   p.w = c->pml_w; p.Kz = c->kz;
   p.bh = (const T*)c->d_pml_bh; p.ah = (const T*)c->d_pml_ah; p.be = (const T*)c->d_pml_be; p.ae = (const T*)c->d_pml_ae;
-  p.psih = (T*)c->d_psih; p.psie = (T*)c->d_psie; p.psi_rows = c->nrows_alloc;
+  p.psih = psi_buf<T>(c, 0, q); p.psie = psi_buf<T>(c, 1, q);
+  p.psih1 = psi_buf<T>(c, 0, 1 - q); p.psie1 = psi_buf<T>(c, 1, 1 - q);
+  p.psi_rows = c->nrows_alloc;
   p.chx = (T)(c->d.dt / (MU0 * c->d.dx));
   p.chy = (T)(c->d.dt / (MU0 * c->d.dy));
   p.idx = (T)(1.0 / c->d.dx); p.idy = (T)(1.0 / c->d.dy);
@@ -342,46 +353,60 @@ fdtd::PmlParams<T> pml_params(fdtd_ctx* c, int q) {
 // the K rows below (the top K rows of rank g-1), Ex of the K edge rows above and Ey / Hz of the
 // K-1 cell rows above (the bottom rows of rank g+1).  Rows are whole device rows (pitch
 // elements); sends and receives are listed in the order both transports pair them.
+// With CPML layers (NEXT-2) the psi rows travel with the field they belong to: psi_ey (a = 3, 4:
+// left / right side) with Ey, psi_hz (a = 5, 6) with Hz.
 struct HaloRow { int a; int64_t row; int peer; };
 void halo_plan(const fdtd_ctx* c, int depth, std::vector<HaloRow>& sends, std::vector<HaloRow>& recvs) {
   sends.clear();
   recvs.clear();
   const int up = c->d.rank + 1, dn = c->d.rank - 1;
   const int64_t top = ROW0 + c->rows;  // first row above the slab
+  const bool pml = c->pml_w > 0;
+  auto push = [&](std::vector<HaloRow>& v, int a, int64_t r, int peer) {
+    v.push_back({a, r, peer});
+    if (pml && a == 1) { v.push_back({3, r, peer}); v.push_back({4, r, peer}); }
+    if (pml && a == 2) { v.push_back({5, r, peer}); v.push_back({6, r, peer}); }
+  };
   auto down_list = [&](int64_t base, int peer, std::vector<HaloRow>& v) {  // rows the lower rank needs
     for (int64_t r = 0; r < depth; ++r) {
-      v.push_back({0, base + r, peer});
+      push(v, 0, base + r, peer);
       if (r + 1 < depth) {
-        v.push_back({1, base + r, peer});
-        v.push_back({2, base + r, peer});
+        push(v, 1, base + r, peer);
+        push(v, 2, base + r, peer);
       }
     }
   };
   if (up < c->d.nranks) {
     for (int64_t r = top - depth; r < top; ++r)
-      for (int a = 0; a < 3; ++a) sends.push_back({a, r, up});
+      for (int a = 0; a < 3; ++a) push(sends, a, r, up);
     down_list(top, up, recvs);  // rows above the slab come from rank g+1's bottom rows
   }
   if (dn >= 0) {
     for (int64_t r = ROW0 - depth; r < ROW0; ++r)
-      for (int a = 0; a < 3; ++a) recvs.push_back({a, r, dn});
+      for (int a = 0; a < 3; ++a) push(recvs, a, r, dn);
     down_list(ROW0, dn, sends);
   }
 }
 
+// device address and element count of halo row (a, r) of buffer q
 inline char* dev_row(const fdtd_ctx* c, int q, int a, int64_t r) {
-  return (char*)c->f[q][a] + (size_t)r * c->pitch * c->es;
+  if (a < 3) return (char*)c->f[q][a] + (size_t)r * c->pitch * c->es;
+  const int e = a < 5 ? 1 : 0, side = (a - 3) & 1;
+  const int64_t rw = e ? c->pml_w + 1 : c->pml_w;
+  return psi_base(c, e, q, side) + (size_t)(r * rw) * c->es;
+}
+inline size_t row_elems(const fdtd_ctx* c, int a) {
+  return a < 3 ? (size_t)c->pitch : (size_t)(a < 5 ? c->pml_w + 1 : c->pml_w);
 }
 
 fdtd_status halo_exchange(fdtd_ctx* c, int q, cudaStream_t s, int depth) {
   if (c->d.nranks <= 1 || (c->d.flags & FDTD_LOCAL_GROUP)) return FDTD_OK;
-  const size_t n = (size_t)c->pitch;
   const int dt = c->prec == 64 ? NCCL_F64 : NCCL_F32;
   std::vector<HaloRow> sends, recvs;
   halo_plan(c, depth, sends, recvs);
   NK(g_nccl.GroupStart());
-  for (auto& x : sends) NK(g_nccl.Send(dev_row(c, q, x.a, x.row), n, dt, x.peer, c->comm, s));
-  for (auto& x : recvs) NK(g_nccl.Recv(dev_row(c, q, x.a, x.row), n, dt, x.peer, c->comm, s));
+  for (auto& x : sends) NK(g_nccl.Send(dev_row(c, q, x.a, x.row), row_elems(c, x.a), dt, x.peer, c->comm, s));
+  for (auto& x : recvs) NK(g_nccl.Recv(dev_row(c, q, x.a, x.row), row_elems(c, x.a), dt, x.peer, c->comm, s));
   NK(g_nccl.GroupEnd());
   return FDTD_OK;
 }
@@ -399,9 +424,11 @@ fdtd_status halo_local(fdtd_ctx* const* g, int n, int k, int q, cudaStream_t s, 
     for (auto& x : recvs) if (x.peer == peer) in.push_back(x);
     for (auto& x : psends) if (x.peer == k) out.push_back(x);
     if (in.size() != out.size()) return fail(c, FDTD_E_STATE, "halo plans of ranks %d and %d do not pair", k, peer);
-    for (size_t i = 0; i < in.size(); ++i)
+    for (size_t i = 0; i < in.size(); ++i) {
+      if (in[i].a != out[i].a) return fail(c, FDTD_E_STATE, "halo plans of ranks %d and %d do not pair", k, peer);
       CK(cudaMemcpyAsync(dev_row(c, q, in[i].a, in[i].row), dev_row(g[peer], q, out[i].a, out[i].row),
-                         (size_t)c->pitch * c->es, cudaMemcpyDeviceToDevice, s));
+                         row_elems(c, in[i].a) * c->es, cudaMemcpyDeviceToDevice, s));
+    }
   }
   return FDTD_OK;
 }
@@ -1562,7 +1589,6 @@ fdtd_status fdtd_step_group(fdtd_ctx** g, int32_t n, int64_t nsteps) {
 fdtd_status fdtd_set_pml(fdtd_ctx* c, int32_t width, int32_t order, double r0) {
   if (!c) return FDTD_E_ARG;
   if (width < 0 || order < 0 || order > 8 || !(r0 > 0 && r0 < 1)) return fail(c, FDTD_E_ARG, "bad CPML parameters");
-  if (width > 0 && c->d.nranks > 1) return fail(c, FDTD_E_ARG, "CPML layers need a single rank (row slabs: NEXT)");
   if (2 * (width + 4) > c->d.nx) return fail(c, FDTD_E_ARG, "CPML layers of %d cells do not fit nx = %lld", width,
                                              (long long)c->d.nx);
   for (size_t r = 0; width > 0 && r < c->rects.size(); r += 4)  // rings 3 cells clear of the layers (K = 1)
@@ -1595,8 +1621,8 @@ fdtd_status fdtd_set_pml(fdtd_ctx* c, int32_t width, int32_t order, double r0) {
     if ((st = upload_T(c, &c->d_pml_ah, ah)) != FDTD_OK) return st;
     if ((st = upload_T(c, &c->d_pml_be, be)) != FDTD_OK) return st;
     if ((st = upload_T(c, &c->d_pml_ae, ae)) != FDTD_OK) return st;
-    c->d_psih = dalloc(c, (size_t)2 * c->nrows_alloc * width * c->es);
-    c->d_psie = dalloc(c, (size_t)2 * c->nrows_alloc * (width + 1) * c->es);
+    c->d_psih = dalloc(c, (size_t)4 * c->nrows_alloc * width * c->es);        // [buffer][side][row][col]
+    c->d_psie = dalloc(c, (size_t)4 * c->nrows_alloc * (width + 1) * c->es);
     if (!c->d_psih || !c->d_psie) return fail(c, FDTD_E_NOMEM, "CPML state");
   }
   c->kz_dirty = true;

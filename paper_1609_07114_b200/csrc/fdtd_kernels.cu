@@ -1029,7 +1029,7 @@ __global__ void __launch_bounds__(512) postk_kernel(const PostParams<T> p) {
 }
 
 // NEXT-2: CPML band fix-up.  Per CTA: one row chunk [r0, r1) of one side; region = columns
-// [c0, c0 + WB), WB = w + 2K + 2, rows [r0 - K, r1 + K - 1) (+ one Ex edge row).  K steps with the
+// [c0, c0 + WB), WB = w + Kz + K + 2, rows [r0 - K, r1 + K - 1) (+ one Ex edge row).  K steps with the
 // sweep's device functions plus, in the layer, psi_hz = b psi_hz + a dEy/dx (Hz -= dt/mu0 psi_hz)
 // and psi_ey = b psi_ey + a dHz/dx (the Ey curl term gains dx psi_ey).  Values go wrong from the
 // region's border inwards one cell per step, so after K steps the write-back columns (the layer
@@ -1041,7 +1041,8 @@ __global__ void __launch_bounds__(256) pml_kernel(const PmlParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[32];
   const int side = blockIdx.y;
-  const int w = p.w, WB = w + 2 * K + 2, WW = w + p.Kz + 1;
+  // region: the write-back columns plus K + 1 (Kz > K on the shorter passes ending a step count)
+  const int w = p.w, WW = w + p.Kz + 1, WB = WW + K + 1;
   const int64_t nx = p.nx, P = p.pitch;
   const int r0 = p.row0 + blockIdx.x * p.chunk, r1 = min(r0 + p.chunk, p.row0 + p.rows);
   const int R0 = r0 - K, Hr = (r1 - r0) + 2 * K - 1;  // region cell rows [R0, R0 + Hr)
@@ -1066,8 +1067,10 @@ __global__ void __launch_bounds__(256) pml_kernel(const PmlParams<T> p) {
   auto ecol = [&](int64_t gi) { return side == 0 ? (int)gi : (int)(gi - lay0); };
   const T* bh = p.bh + side * w; const T* ah = p.ah + side * w;
   const T* be = p.be + side * (w + 1); const T* ae = p.ae + side * (w + 1);
-  T* psih = p.psih + (int64_t)side * p.psi_rows * w;
-  T* psie = p.psie + (int64_t)side * p.psi_rows * (w + 1);
+  const T* psih = p.psih + (int64_t)side * p.psi_rows * w;
+  const T* psie = p.psie + (int64_t)side * p.psi_rows * (w + 1);
+  T* psih1 = p.psih1 + (int64_t)side * p.psi_rows * w;
+  T* psie1 = p.psie1 + (int64_t)side * p.psi_rows * (w + 1);
   // ---- load the region (fields at step n, materials, psi)
   for (int t = tid; t < n; t += nt) {
     const int u = t % WB, v = t / WB;
@@ -1164,11 +1167,8 @@ __global__ void __launch_bounds__(256) pml_kernel(const PmlParams<T> p) {
     p.hz1[o] = H[t];
     p.ex1[o] = EX[t];
     p.ey1[o] = EY[v * W1 + u];
-    if (in_layer_h(gi)) psih[(int64_t)lr * w + hcol(gi)] = PH[t];
-    if (in_layer_e(gi)) psie[(int64_t)lr * (w + 1) + ecol(gi)] = PE[v * W1 + u];
-  }
-  if (side == 1 && tid < Hr) {  // the right layer's outermost psi_ey column sits at the wall edge nx
-    (void)0;
+    if (in_layer_h(gi)) psih1[(int64_t)lr * w + hcol(gi)] = PH[t];
+    if (in_layer_e(gi)) psie1[(int64_t)lr * (w + 1) + ecol(gi)] = PE[v * W1 + u];
   }
   if (ENERGY) {
 #pragma unroll 1
@@ -1386,7 +1386,7 @@ void launch_zone(T* msb, const T* mea, int64_t pitch, const int32_t* rects, int6
 
 template <typename T, int K>
 void pml_launch(const PmlParams<T>& p, bool energy, cudaStream_t s) {
-  const int WB = p.w + 2 * K + 2, Hr = p.chunk + 2 * K - 1;
+  const int WB = p.w + p.Kz + K + 2, Hr = p.chunk + 2 * K - 1;
   const size_t smem = sizeof(T) * ((size_t)5 * Hr * WB + WB + (size_t)2 * Hr * (WB + 1));
   dim3 grid((p.rows + p.chunk - 1) / p.chunk, 2);
   auto kern = energy ? pml_kernel<T, K, true> : pml_kernel<T, K, false>;

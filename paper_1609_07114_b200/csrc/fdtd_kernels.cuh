@@ -90,7 +90,7 @@ struct PostParams {
 };
 
 // CPML band fix-up (NEXT-2): the sweep advances the two x-end layers with the plain Yee update; per
-// row chunk and side this kernel recomputes the K steps on the band [layer + 2K + 2 columns] x
+// row chunk and side this kernel recomputes the K steps on the band [layer + Kz + K + 2 columns] x
 // [chunk rows +- K] from the pass's input buffer with the CPML terms (Roden-Gedney, kappa 1, alpha 0)
 // and writes back the layer plus Kz + 1 interior columns (the sweep skipped their energy: msb marks).
 template <typename T>
@@ -103,8 +103,10 @@ struct PmlParams {
   int w, Kz;                   // layer width (cells); zone depth (write-back = w + Kz + 1 columns)
   const T* bh; const T* ah;    // per side [2][w]: Hz columns, index = distance into the layer
   const T* be; const T* ae;    // per side [2][w + 1]: Ey columns
-  T* psih; T* psie;            // [2][rows_alloc][w], [2][rows_alloc][w + 1]
-  int64_t psi_rows;            // rows_alloc
+  const T* psih; const T* psie;  // psi at step n: [2 sides][rows_alloc][w], [2 sides][rows_alloc][w + 1]
+  T* psih1; T* psie1;            // psi at step n + K (ping-pong like the fields: CTAs read their
+                                 // neighbours' ghost rows while they write their own)
+  int64_t psi_rows;              // rows_alloc
   T chx, chy, idx, idy, wxy, wh, cpsi, dxv;  // cpsi = dt / mu0, dxv = dx
   int src_row, src_row_end; int64_t src_col; const double* src_samples; int64_t src_n, src_t0;
   const int64_t* step;

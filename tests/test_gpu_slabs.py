@@ -44,7 +44,7 @@ def run_single(s, n, init):
     return out
 
 
-def run_group(s, n, init, nslab, spp=2):
+def run_group(s, n, init, nslab, spp=2, check_spp=True):
     import torch
 
     from paper_1609_07114_b200 import Simulation, step_group
@@ -67,7 +67,12 @@ def run_group(s, n, init, nslab, spp=2):
             if len(sel):
                 sim.add_rom(m, sel[:, 1:3])
                 mine += [(m, int(i0), int(j0)) for _, i0, j0 in sel]
-        sim.set_source(*s.source, s.samples)
+        if "pml" in s.meta:
+            sim.set_pml(*s.meta["pml"])
+        if "source_rows" in s.meta:
+            sim.set_source_line(s.source[0], *s.meta["source_rows"], s.samples)
+        else:
+            sim.set_source(*s.source, s.samples)
         sim.set_probes(s.probes)
         sim.record_energy(True)
         sim.set_time_blocking(spp)
@@ -78,7 +83,8 @@ def run_group(s, n, init, nslab, spp=2):
         sims.append(sim)
         local.append(idx)
     step_group(sims, n)
-    assert all(sim.info().steps_per_pass == min(spp, 4 if s.precision == 32 else 2) for sim in sims)
+    if check_spp:
+        assert all(sim.info().steps_per_pass == min(spp, 4 if s.precision == 32 else 2) for sim in sims)
     F = [np.zeros((s.ny + 1, s.nx)), np.zeros((s.ny, s.nx + 1)), np.zeros((s.ny, s.nx))]
     xs_out = np.zeros_like(xs)
     pr, en = 0, 0
@@ -108,6 +114,30 @@ def test_slabs_bitwise_equal_single(nslab, precision, spp):
     init = consistent_random_state(s, 3)
     (W1, x1, p1, e1) = run_single(s, 301, init)
     (W2, x2, p2, e2) = run_group(s, 301, init, nslab, spp)
+    for a, b in zip(W1, W2):
+        assert np.array_equal(a, b)
+    assert np.array_equal(x1, x2)
+    assert np.array_equal(p1, p2)
+    np.testing.assert_allclose(e2, e1, rtol=1e-12 if precision == 64 else 1e-6)
+
+
+@pytest.mark.parametrize("spp", [1, 2, 4])
+@pytest.mark.parametrize("nslab", [2, 3])
+@pytest.mark.parametrize("precision", [32, 64])
+@pytest.mark.parametrize("rom", [False, True])
+def test_cpml_slabs_bitwise_equal_single(nslab, precision, spp, rom):
+    """NEXT-2 on row slabs: CPML layers + a line source across the slab edges; the psi rows of the
+    ghost rows travel with the halo exchange.  Fields, ROM states and probes bit-identical to one
+    context."""
+    from test_gpu_pml import channel_scene
+
+    s = channel_scene(precision, ny=60, rom=rom)
+    if rom:
+        s.placements = np.array([[0, 98, 11], [0, 120, 41]], np.int32)
+        assert slabs.check_partition(s.placements, s.models, s.ny, nslab)
+    init = consistent_random_state(s, 5)
+    (W1, x1, p1, e1) = run_single(s, 301, init)
+    (W2, x2, p2, e2) = run_group(s, 301, init, nslab, spp, check_spp=not rom)  # 3 slabs: ROM regions cross a slab edge -> shallower passes
     for a, b in zip(W1, W2):
         assert np.array_equal(a, b)
     assert np.array_equal(x1, x2)
