@@ -9,14 +9,14 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfdtdrom.so")
-SOURCES = ["fdtd_kernels.cu", "fdtd_api.cpp"]
+SOURCES = ["fdtd_kernels.cu", "fdtd_api.cpp", "rom_build.cu"]
 HEADERS = ["fdtd_kernels.cuh", "dense.hpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
 def _inputs():
-    return [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "fdtdrom.h"),
+    return [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "fdtdrom.h"), os.path.join(ROOT, "include", "fdtdrom_build.h"),
                                                               os.path.abspath(__file__)]
 
 

@@ -52,6 +52,20 @@ class Info(C.Structure):
                 ("sweep_stream", C.c_void_p)]
 
 
+class RomSpec(C.Structure):  # fdtdrom_build.h
+    _fields_ = [("bx", C.c_int32), ("by", C.c_int32), ("r", C.c_int32), ("dx", C.c_double), ("dy", C.c_double),
+                ("eps_r", C.c_void_p), ("sigma", C.c_void_p), ("q", C.c_int32), ("fmax", C.c_double),
+                ("dt_target", C.c_double), ("cg_tol", C.c_double)]
+
+
+class RomBuilt(C.Structure):
+    _fields_ = [("R11", C.c_void_p), ("R22", C.c_void_p), ("F11", C.c_void_p), ("K", C.c_void_p),
+                ("L", C.c_void_p), ("q1", C.c_int32), ("q2", C.c_int32), ("nY", C.c_int32),
+                ("n_clipped", C.c_int32), ("natural_dt_limit", C.c_double), ("krylov_vectors", C.c_int32),
+                ("cg_iterations_max", C.c_int32), ("jacobi_sweeps_max", C.c_int32), ("ms_total", C.c_double),
+                ("ms_solve", C.c_double), ("ms_orth", C.c_double), ("ms_svd", C.c_double)]
+
+
 class FDTDError(RuntimeError):
     def __init__(self, status, msg):
         super().__init__("%s: %s" % (STATUS.get(status, status), msg))
@@ -97,6 +111,10 @@ def lib():
         L.fdtd_status_string.restype = C.c_char_p
         L.fdtd_destroy.argtypes = [vp]
         L.fdtd_destroy.restype = None
+        L.fdtd_rom_build.argtypes = [C.POINTER(RomSpec), C.POINTER(RomBuilt)]
+        L.fdtd_rom_build.restype = C.c_int
+        L.fdtd_rom_build_last_error.argtypes = []
+        L.fdtd_rom_build_last_error.restype = C.c_char_p
         for n in ("create", "add_rom", "set_source", "set_probes", "record_energy", "step", "probe", "energy",
                   "get_window", "set_window", "get_rom_state", "set_rom_state", "sync", "get_info", "set_tuning",
                   "nccl_unique_id", "profile", "profile_read", "step_group", "set_time_blocking",
@@ -109,8 +127,37 @@ def lib():
 def exported_symbols():
     """Names declared in include/fdtdrom.h (used by the ABI test)."""
     import re
-    hdr = open(os.path.join(os.path.dirname(_HERE), "include", "fdtdrom.h")).read()
-    return sorted(set(re.findall(r"\b(fdtd_[a-z_0-9]+)\s*\(", hdr)))
+    names = set()
+    for h in ("fdtdrom.h", "fdtdrom_build.h"):
+        hdr = open(os.path.join(os.path.dirname(_HERE), "include", h)).read()
+        names |= set(re.findall(r"\b(fdtd_[a-z_0-9]+)\s*\(", hdr))
+    return sorted(names)
+
+
+def build_rom(bx, by, r, dx, dy, eps_r, sigma, q, fmax, dt_target=None, cg_tol=0.0):
+    """GPU-side ROM construction (fdtdrom_build.h, NEXT-3): fine assembly, collapse onto coarse-edge
+    ports, SPRIM(q) with CG-solved shifts, congruence, optional CFL clip at dt_target.  Returns the
+    model dict fdtd_add_rom consumes (R11, R22, F11, K, L, q1, q2, bx, by, r, n_clipped, literal,
+    natural_dt_limit) plus the builder's diagnostics under "gpu_build"."""
+    eps = _f64(eps_r).reshape(by * r, bx * r)
+    sig = _f64(sigma).reshape(by * r, bx * r)
+    q1w, q2w, nY = (q + 1) // 2, q // 2, 2 * bx + 2 * by
+    R11, F11 = np.zeros((q1w, q1w)), np.zeros((q1w, q1w))
+    R22, K, L = np.zeros((q2w, q2w)), np.zeros((q1w, q2w)), np.zeros((q1w, nY))
+    spec = RomSpec(int(bx), int(by), int(r), float(dx), float(dy), eps.ctypes.data, sig.ctypes.data, int(q),
+                   float(fmax), float(dt_target or 0.0), float(cg_tol))
+    out = RomBuilt(R11.ctypes.data, R22.ctypes.data, F11.ctypes.data, K.ctypes.data, L.ctypes.data)
+    st = lib().fdtd_rom_build(C.byref(spec), C.byref(out))
+    if st:
+        raise FDTDError(st, lib().fdtd_rom_build_last_error().decode())
+    q1, q2 = out.q1, out.q2
+    unpack = lambda a, m, n: np.ascontiguousarray(a.ravel()[: m * n].reshape(m, n))
+    return dict(bx=int(bx), by=int(by), r=int(r), q1=q1, q2=q2, R11=unpack(R11, q1, q1), R22=unpack(R22, q2, q2),
+                F11=unpack(F11, q1, q1), K=unpack(K, q1, q2), L=unpack(L, q1, nY), n_clipped=int(out.n_clipped),
+                literal=False, natural_dt_limit=float(out.natural_dt_limit),
+                gpu_build=dict(krylov_vectors=out.krylov_vectors, cg_iterations_max=out.cg_iterations_max,
+                               jacobi_sweeps_max=out.jacobi_sweeps_max, ms_total=out.ms_total,
+                               ms_solve=out.ms_solve, ms_orth=out.ms_orth, ms_svd=out.ms_svd))
 
 
 def nccl_unique_id() -> bytes:
