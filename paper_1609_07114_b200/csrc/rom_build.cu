@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -271,6 +272,249 @@ __global__ void __launch_bounds__(CG_NT) cg_kernel(CGArgs a) {
   if (tid == 0) a.iters[c] = it < a.maxit ? it : -1;
 }
 
+// ---- H-form shifted solves: eliminate E instead of H,
+//   (s0 R22 + K^T D^-1 K) xH = bH - K^T D^-1 bE,   xE = D^-1 (bE + K xH),   D = 2 F11 + s0 R11.
+// S_H is a 5-point stencil on the fine cells (one coupling per interior edge) plus one rank-1 block
+// per port (the r cells along a coarse interface edge).  CG preconditioned by a geometric multigrid
+// V-cycle (2 x 2 aggregation, Galerkin coarse stencils, symmetric red-black Gauss-Seidel) on the
+// stencil with the port blocks' diagonal; one CTA per right-hand side for the whole iteration.
+constexpr int MG_MAXLEV = 16;
+struct MGLevel { int nx, ny; long off; };
+struct MGArgs {
+  Geo g;
+  int nlev; MGLevel lev[MG_MAXLEV];
+  const double *cc, *we, *wn;  // per level (pool offsets): diagonal, east and north couplings
+  const double* cS;            // level-0 exact stencil diagonal (no port terms)
+  const double* pw;            // per port: v^2 / D_e (v = fdx for S/N ports, fdy for W/E)
+  const double* B; int ldb;    // right-hand sides (nH x ncol)
+  double* X; int ldx;          // solutions
+  double* work; long wstride;  // per column: r, z, p, q (4 nH), then per level >= 1: x, b
+  double* psum;                // per column: nY
+  double tol; int maxit; int* iters;
+};
+
+// level-0 stencil: we(i,j) couples (i,j)-(i+1,j) through interior Ey(i+1,j); wn(i,j) couples
+// (i,j)-(i,j+1) through interior Ex(i,j+1) (entries k_a k_b / D_e = -fdy^2/D, -fdx^2/D)
+__global__ void hs_setup0_kernel(Geo g, double s0, const double* r22, const double* d, double* cS, double* cc,
+                                 double* we, double* wn, double* pw) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < g.nY) pw[t] = (t < 2 * g.bx ? g.fdx * g.fdx : g.fdy * g.fdy) / d[t];
+  if (t >= g.nH) return;
+  const int i = t % g.Nx, j = t / g.Nx;
+  we[t] = i < g.Nx - 1 ? -g.fdy * g.fdy / d[g.ey(i + 1, j)] : 0.0;
+  wn[t] = j < g.Ny - 1 ? -g.fdx * g.fdx / d[g.ex(i, j + 1)] : 0.0;
+}
+__global__ void hs_setup0b_kernel(Geo g, double s0, const double* r22, const double* pw, double* cS, double* cc,
+                                  const double* we, const double* wn) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= g.nH) return;
+  const int i = t % g.Nx, j = t / g.Nx;
+  double c = s0 * r22[t] - we[t] - wn[t];
+  if (i > 0) c -= we[t - 1];
+  if (j > 0) c -= wn[t - g.Nx];
+  cS[t] = c;
+  if (j == 0) c += pw[i / g.r];
+  if (j == g.Ny - 1) c += pw[g.bx + i / g.r];
+  if (i == 0) c += pw[2 * g.bx + j / g.r];
+  if (i == g.Nx - 1) c += pw[2 * g.bx + g.by + j / g.r];
+  cc[t] = c;
+}
+// Galerkin coarsening with piecewise-constant 2 x 2 aggregation: A_c = P^T A P
+__global__ void hs_coarsen_kernel(MGLevel f, MGLevel c, const double* cc_f, const double* we_f, const double* wn_f,
+                                  double* cc_c, double* we_c, double* wn_c) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= c.nx * c.ny) return;
+  const int I = t % c.nx, J = t / c.nx;
+  const int i0 = 2 * I, j0 = 2 * J, i1 = min(i0 + 1, f.nx - 1), j1 = min(j0 + 1, f.ny - 1);
+  double dg = 0.0, e = 0.0, n = 0.0;
+  for (int j = j0; j <= j1; ++j)
+    for (int i = i0; i <= i1; ++i) {
+      const int k = j * f.nx + i;
+      dg += cc_f[k];
+      if (i < i1) dg += 2.0 * we_f[k];  // internal horizontal coupling
+      if (j < j1) dg += 2.0 * wn_f[k];  // internal vertical coupling
+      if (i == i1 && I + 1 < c.nx) e += we_f[k];
+      if (j == j1 && J + 1 < c.ny) n += wn_f[k];
+    }
+  cc_c[t] = dg;
+  we_c[t] = e;
+  wn_c[t] = n;
+}
+
+constexpr int MG_NT = 1024;
+__device__ __forceinline__ void mg_smooth(const MGArgs& a, int l, double* x, const double* b, int color) {
+  const MGLevel L = a.lev[l];
+  const double *c = a.cc + L.off, *we = a.we + L.off, *wn = a.wn + L.off;
+  const int nx = L.nx, n = L.nx * L.ny;
+  // cells of one colour: (i + j) % 2 == color; thread t handles the t-th such cell
+  const int half = (n + 1) / 2 + 1;
+  for (int u = threadIdx.x; u < half; u += MG_NT) {
+    // row-major walk over the colour: cell index k = 2u + ((row parity) ^ color) within its row
+    const int k2 = 2 * u;
+    int j = k2 / nx, i = k2 % nx;
+    if (((i + j) & 1) != color) ++i;
+    if (i >= nx) { i -= nx; ++j; }
+    if (j >= L.ny) continue;
+    const int k = j * nx + i;
+    if (k >= n) continue;
+    double s = b[k];
+    if (i > 0) s -= we[k - 1] * x[k - 1];
+    if (i < nx - 1) s -= we[k] * x[k + 1];
+    if (j > 0) s -= wn[k - nx] * x[k - nx];
+    if (j < L.ny - 1) s -= wn[k] * x[k + nx];
+    x[k] = s / c[k];
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void mg_restrict(const MGArgs& a, int l, const double* x, const double* b, double* bc) {
+  const MGLevel f = a.lev[l], c = a.lev[l + 1];
+  const double *cc = a.cc + f.off, *we = a.we + f.off, *wn = a.wn + f.off;
+  for (int t = threadIdx.x; t < c.nx * c.ny; t += MG_NT) {
+    const int I = t % c.nx, J = t / c.nx;
+    const int i0 = 2 * I, j0 = 2 * J, i1 = min(i0 + 1, f.nx - 1), j1 = min(j0 + 1, f.ny - 1);
+    double s = 0.0;
+    for (int j = j0; j <= j1; ++j)
+      for (int i = i0; i <= i1; ++i) {
+        const int k = j * f.nx + i;
+        double r = b[k] - cc[k] * x[k];
+        if (i > 0) r -= we[k - 1] * x[k - 1];
+        if (i < f.nx - 1) r -= we[k] * x[k + 1];
+        if (j > 0) r -= wn[k - f.nx] * x[k - f.nx];
+        if (j < f.ny - 1) r -= wn[k] * x[k + f.nx];
+        s += r;
+      }
+    bc[t] = s;
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void mg_prolong(const MGArgs& a, int l, double* x, const double* xc) {
+  const MGLevel f = a.lev[l], c = a.lev[l + 1];
+  for (int k = threadIdx.x; k < f.nx * f.ny; k += MG_NT) {
+    const int i = k % f.nx, j = k / f.nx;
+    x[k] += xc[(j / 2) * c.nx + i / 2];
+  }
+  __syncthreads();
+}
+// z = V-cycle(r): symmetric (pre: red-black, post: black-red; coarsest: symmetric sweep pairs)
+__device__ void mg_vcycle(const MGArgs& a, double* wcol, double* z, double* r) {
+  constexpr int NU = 2, NCOARSE = 30;
+  auto xl = [&](int l) { return l == 0 ? z : wcol + 4L * a.g.nH + 2 * (a.lev[l].off - a.lev[1].off); };
+  auto bl = [&](int l) { return l == 0 ? r : wcol + 4L * a.g.nH + 2 * (a.lev[l].off - a.lev[1].off) + a.lev[l].nx * a.lev[l].ny; };
+  for (int l = 0; l < a.nlev; ++l) {
+    double* x = xl(l);
+    for (int k = threadIdx.x; k < a.lev[l].nx * a.lev[l].ny; k += MG_NT) x[k] = 0.0;
+    __syncthreads();
+    if (l == a.nlev - 1) {
+      for (int it = 0; it < NCOARSE; ++it) {
+        mg_smooth(a, l, x, bl(l), 0); mg_smooth(a, l, x, bl(l), 1);
+        mg_smooth(a, l, x, bl(l), 1); mg_smooth(a, l, x, bl(l), 0);
+      }
+      break;
+    }
+    for (int it = 0; it < NU; ++it) { mg_smooth(a, l, x, bl(l), 0); mg_smooth(a, l, x, bl(l), 1); }
+    mg_restrict(a, l, x, bl(l), bl(l + 1));
+  }
+  for (int l = a.nlev - 2; l >= 0; --l) {
+    mg_prolong(a, l, xl(l), xl(l + 1));
+    for (int it = 0; it < NU; ++it) { mg_smooth(a, l, xl(l), bl(l), 1); mg_smooth(a, l, xl(l), bl(l), 0); }
+  }
+}
+// q = S_H p exactly (stencil with cS + the port rank-1 blocks)
+__device__ __forceinline__ void hs_apply(const MGArgs& a, const double* p, double* q, double* ps) {
+  const Geo& g = a.g;
+  for (int e = threadIdx.x; e < g.nY; e += MG_NT) {
+    double s = 0.0;
+    for (int u = 0; u < g.r; ++u) {
+      int cell;
+      if (e < g.bx) cell = e * g.r + u;                                             // S: row 0
+      else if (e < 2 * g.bx) cell = (g.Ny - 1) * g.Nx + (e - g.bx) * g.r + u;       // N: row Ny-1
+      else if (e < 2 * g.bx + g.by) cell = ((e - 2 * g.bx) * g.r + u) * g.Nx;       // W: column 0
+      else cell = ((e - 2 * g.bx - g.by) * g.r + u) * g.Nx + g.Nx - 1;              // E: column Nx-1
+      s += p[cell];
+    }
+    ps[e] = a.pw[e] * s;
+  }
+  __syncthreads();
+  const int nx = g.Nx;
+  for (int k = threadIdx.x; k < g.nH; k += MG_NT) {
+    const int i = k % nx, j = k / nx;
+    double y = a.cS[k] * p[k];
+    if (i > 0) y += a.we[k - 1] * p[k - 1];
+    if (i < nx - 1) y += a.we[k] * p[k + 1];
+    if (j > 0) y += a.wn[k - nx] * p[k - nx];
+    if (j < g.Ny - 1) y += a.wn[k] * p[k + nx];
+    if (j == 0) y += ps[i / g.r];
+    if (j == g.Ny - 1) y += ps[g.bx + i / g.r];
+    if (i == 0) y += ps[2 * g.bx + j / g.r];
+    if (i == nx - 1) y += ps[2 * g.bx + g.by + j / g.r];
+    q[k] = y;
+  }
+  __syncthreads();
+}
+__global__ void __launch_bounds__(MG_NT) mg_pcg_kernel(MGArgs a) {
+  __shared__ double red[32];
+  const int c = blockIdx.x, n = a.g.nH, tid = threadIdx.x;
+  const double* b = a.B + (size_t)c * a.ldb;
+  double* x = a.X + (size_t)c * a.ldx;
+  double* wcol = a.work + (size_t)c * a.wstride;
+  double *r = wcol, *z = wcol + n, *p = wcol + 2L * n, *q = wcol + 3L * n;
+  double* ps = a.psum + (size_t)c * a.g.nY;
+  double bb = 0.0;
+  for (int i = tid; i < n; i += MG_NT) { x[i] = 0.0; r[i] = b[i]; bb += b[i] * b[i]; }
+  bb = block_sum<MG_NT>(bb, red);
+  if (bb == 0.0) { if (tid == 0) a.iters[c] = 0; return; }
+  const double stop = a.tol * a.tol * bb;
+  mg_vcycle(a, wcol, z, r);
+  double rz = 0.0;
+  for (int i = tid; i < n; i += MG_NT) { p[i] = z[i]; rz += r[i] * z[i]; }
+  rz = block_sum<MG_NT>(rz, red);
+  int it = 0;
+  for (; it < a.maxit; ++it) {
+    hs_apply(a, p, q, ps);
+    double pq = 0.0;
+    for (int i = tid; i < n; i += MG_NT) pq += p[i] * q[i];
+    pq = block_sum<MG_NT>(pq, red);
+    const double alpha = rz / pq;
+    double rr = 0.0;
+    for (int i = tid; i < n; i += MG_NT) {
+      x[i] += alpha * p[i];
+      r[i] -= alpha * q[i];
+      rr += r[i] * r[i];
+    }
+    rr = block_sum<MG_NT>(rr, red);
+    if (rr <= stop) { ++it; break; }
+    mg_vcycle(a, wcol, z, r);
+    double rzn = 0.0;
+    for (int i = tid; i < n; i += MG_NT) rzn += r[i] * z[i];
+    rzn = block_sum<MG_NT>(rzn, red);
+    const double beta = rzn / rz;
+    rz = rzn;
+    for (int i = tid; i < n; i += MG_NT) p[i] = z[i] + beta * p[i];
+    __syncthreads();
+  }
+  if (tid == 0) a.iters[c] = it < a.maxit ? it : -1;
+}
+// rhsH = bH - K^T D^-1 bE
+__global__ void hs_rhs_kernel(Geo g, const int* colT, const double* valT, const double* d, const double* BE, int ldbe,
+                              const double* BH, int ldbh, double* R, int ldr, int ncol) {
+  const int h = blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y;
+  if (h >= g.nH || c >= ncol) return;
+  const double* e = BE + (size_t)c * ldbe;
+  double s = 0.0;
+  for (int u = 0; u < 4; ++u) s += valT[4 * h + u] * e[colT[4 * h + u]] / d[colT[4 * h + u]];
+  R[(size_t)c * ldr + h] = (BH ? BH[(size_t)c * ldbh + h] : 0.0) - s;
+}
+// xE = D^-1 (bE + K xH)
+__global__ void hs_erec_kernel(Geo g, const int* col, const double* val, const double* d, const double* BE, int ldbe,
+                               const double* XH, int ldxh, double* XE, int ldxe, int ncol) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y;
+  if (e >= g.nEc || c >= ncol) return;
+  const double* xh = XH + (size_t)c * ldxh;
+  double s = BE[(size_t)c * ldbe + e];
+  for (int p = g.rowptr(e); p < g.rowptr(e + 1); ++p) s += val[p] * xh[col[p]];
+  XE[(size_t)c * ldxe + e] = s / d[e];
+}
+
 // ---- Gram-Schmidt in the C inner product (c = [R11; R22] diagonal)
 // out[0] = sum c v^2 (one CTA; fixed order)
 constexpr int RN_NT = 1024;
@@ -464,6 +708,80 @@ struct Builder {
 
   int n() const { return g.nEc + g.nH; }
 
+  // multigrid hierarchy of the H-form solve
+  int nlev = 0;
+  MGLevel lev[MG_MAXLEV];
+  double *mcc = nullptr, *mwe = nullptr, *mwn = nullptr, *mcS = nullptr, *mpw = nullptr;
+  double *hrhs = nullptr, *hwork = nullptr, *hpsum = nullptr;
+  int h_cols = 0;
+  long wstride = 0;
+  bool h_form = true;
+
+  fdtd_status setup_mg() {
+    long off = 0;
+    int nx = g.Nx, ny = g.Ny;
+    nlev = 0;
+    while (true) {
+      lev[nlev] = MGLevel{nx, ny, off};
+      off += (long)nx * ny;
+      ++nlev;
+      if ((long)nx * ny <= 64 || nlev == MG_MAXLEV) break;
+      nx = (nx + 1) / 2;
+      ny = (ny + 1) / 2;
+    }
+    mcc = dev.alloc<double>(off); mwe = dev.alloc<double>(off); mwn = dev.alloc<double>(off);
+    mcS = dev.alloc<double>(g.nH); mpw = dev.alloc<double>(g.nY);
+    if (!mcc || !mwe || !mwn || !mcS || !mpw) return failf(FDTD_E_NOMEM, "multigrid hierarchy");
+    hs_setup0_kernel<<<blocks(std::max(g.nH, g.nY), 256), 256, 0, s>>>(g, s0, r22, d, mcS, mcc, mwe, mwn, mpw);
+    hs_setup0b_kernel<<<blocks(g.nH, 256), 256, 0, s>>>(g, s0, r22, mpw, mcS, mcc, mwe, mwn);
+    for (int l = 0; l + 1 < nlev; ++l) {
+      const MGLevel f = lev[l], c = lev[l + 1];
+      hs_coarsen_kernel<<<blocks((long)c.nx * c.ny, 256), 256, 0, s>>>(f, c, mcc + f.off, mwe + f.off, mwn + f.off,
+                                                                      mcc + c.off, mwe + c.off, mwn + c.off);
+    }
+    wstride = 4L * g.nH + 2 * (off - lev[nlev > 1 ? 1 : 0].off);
+    CUCK(cudaGetLastError());
+    return FDTD_OK;
+  }
+
+  fdtd_status ensure_h(int ncol) {
+    if (ncol <= h_cols) return FDTD_OK;
+    h_cols = ncol;
+    hrhs = dev.alloc<double>((size_t)ncol * g.nH);
+    hwork = dev.alloc<double>((size_t)ncol * wstride);
+    hpsum = dev.alloc<double>((size_t)ncol * g.nY);
+    if (!cg_it) cg_it = dev.alloc<int>(std::max(ncol, 256));
+    if (!hrhs || !hwork || !hpsum || !cg_it) return failf(FDTD_E_NOMEM, "H-form scratch");
+    return FDTD_OK;
+  }
+
+  // H-form: rhsH = bH - K^T D^-1 bE; multigrid-PCG on S_H; xE = D^-1 (bE + K xH)
+  fdtd_status solve_h(const double* BE, int ldbe, const double* BH, int ldbh, int ncol, double* X) {
+    STCK(ensure_h(ncol));
+    if (ncol > 256) return failf(FDTD_E_ARG, "block of %d right-hand sides", ncol);
+    t_solve.start(s);
+    const dim3 ge(blocks(g.nEc, 256), ncol), gh(blocks(g.nH, 256), ncol);
+    hs_rhs_kernel<<<gh, 256, 0, s>>>(g, colT, valT, d, BE, ldbe, BH, ldbh, hrhs, g.nH, ncol);
+    MGArgs a{};
+    a.g = g; a.nlev = nlev;
+    for (int l = 0; l < nlev; ++l) a.lev[l] = lev[l];
+    a.cc = mcc; a.we = mwe; a.wn = mwn; a.cS = mcS; a.pw = mpw;
+    a.B = hrhs; a.ldb = g.nH; a.X = X + g.nEc; a.ldx = n();
+    a.work = hwork; a.wstride = wstride; a.psum = hpsum;
+    a.tol = cg_tol; a.maxit = 5000; a.iters = cg_it;
+    mg_pcg_kernel<<<ncol, MG_NT, 0, s>>>(a);
+    hs_erec_kernel<<<ge, 256, 0, s>>>(g, col, val, d, BE, ldbe, X + g.nEc, n(), X, n(), ncol);
+    CUCK(cudaGetLastError());
+    std::vector<int> it(ncol);
+    CUCK(cudaMemcpyAsync(it.data(), cg_it, sizeof(int) * ncol, cudaMemcpyDeviceToHost, s));
+    t_solve.stop(s);
+    for (int k = 0; k < ncol; ++k) {
+      if (it[k] < 0) return failf(FDTD_E_STATE, "multigrid PCG did not converge to %.1e (column %d)", cg_tol, k);
+      cg_it_max = std::max(cg_it_max, it[k]);
+    }
+    return FDTD_OK;
+  }
+
   fdtd_status ensure_cg(int ncol) {
     if (ncol <= cg_cols) return FDTD_OK;
     cg_cols = ncol;
@@ -481,6 +799,7 @@ struct Builder {
   // or nullptr: 0): eliminate H (xH = dH o (bH - K^T xE)), CG on the Schur complement for xE.
   fdtd_status solve(const double* BE, int ldbe, const double* BH, int ldbh, int ncol, double* X) {
     if (ncol == 0) return FDTD_OK;
+    if (h_form) return solve_h(BE, ldbe, BH, ldbh, ncol, X);
     STCK(ensure_cg(ncol));
     t_solve.start(s);
     const dim3 ge(blocks(g.nEc, 256), ncol), gh(blocks(g.nH, 256), ncol);
@@ -503,17 +822,14 @@ struct Builder {
 
   // one-sided Jacobi SVD of A (rows x m, ld lda, overwritten by A V); V (m x m) accumulated if
   // non-null.  sig: column norms afterwards (unsorted).
-  fdtd_status jacobi(double* A, int lda, int rows, int m, double* V, std::vector<double>& sig) {
-    sig.assign(m, 0.0);
-    if (m == 0) return FDTD_OK;
-    t_svd.start(s);
-    if (V) identity_kernel<<<blocks((long)m * m, 256), 256, 0, s>>>(V, m);
+  // Jacobi sweeps on A (rows x m, ld lda) until no pair rotates; V (m x m) accumulates the
+  // rotations (initialised to I when init is set).
+  fdtd_status jacobi_sweeps(double* A, int lda, int rows, int m, double* V, bool init) {
+    if (V && init) identity_kernel<<<blocks((long)m * m, 256), 256, 0, s>>>(V, m);
     const int mp = m + (m & 1);
     // converged when every pair is orthogonal to sqrt(m) eps relative (the dgesvj criterion)
     const double tol = std::max(1e-15, std::sqrt((double)m) * 2.220446049250313e-16);
     int* rot = (int*)scal;
-    double* nrm = dev.alloc<double>(m);
-    if (!nrm) return failf(FDTD_E_NOMEM, "jacobi");
     int sweeps = 0;
     for (; sweeps < 60; ++sweeps) {
       CUCK(cudaMemsetAsync(rot, 0, sizeof(int), s));
@@ -525,6 +841,35 @@ struct Builder {
       if (h == 0) break;
     }
     jac_sweeps_max = std::max(jac_sweeps_max, sweeps + 1);
+    CUCK(cudaGetLastError());
+    return FDTD_OK;
+  }
+
+  // one-sided Jacobi SVD of A (rows x m, ld lda, overwritten by A V = U S); V (m x m) returned if
+  // non-null.  sig: column norms afterwards (unsorted).  Tall A is first rotated by the
+  // eigenvectors of its Gram matrix A^T A (itself diagonalised by Jacobi), after which the
+  // columns are orthogonal up to the Gram matrix's rounding and few sweeps remain.
+  fdtd_status jacobi(double* A, int lda, int rows, int m, double* V, std::vector<double>& sig) {
+    sig.assign(m, 0.0);
+    if (m == 0) return FDTD_OK;
+    t_svd.start(s);
+    if (rows >= 2 * m && m >= 16) {
+      double* G = dev.alloc<double>((size_t)m * m);
+      double* Vg = dev.alloc<double>((size_t)m * m);
+      double* T = dev.alloc<double>((size_t)rows * m);
+      if (!G || !Vg || !T) return failf(FDTD_E_NOMEM, "jacobi preconditioning");
+      gemm<true, false>(m, m, rows, A, lda, nullptr, A, lda, G, m);
+      STCK(jacobi_sweeps(G, m, m, m, Vg, true));
+      gemm<false, false>(rows, m, m, A, lda, nullptr, Vg, m, T, rows);
+      CUCK(cudaMemcpy2DAsync(A, (size_t)lda * 8, T, (size_t)rows * 8, (size_t)rows * 8, m, cudaMemcpyDeviceToDevice,
+                             s));
+      if (V) CUCK(cudaMemcpyAsync(V, Vg, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, s));
+      STCK(jacobi_sweeps(A, lda, rows, m, V, false));
+    } else {
+      STCK(jacobi_sweeps(A, lda, rows, m, V, true));
+    }
+    double* nrm = dev.alloc<double>(m);
+    if (!nrm) return failf(FDTD_E_NOMEM, "jacobi");
     colnorm_kernel<<<m, JB_NT, 0, s>>>(A, lda, rows, nrm);
     CUCK(cudaMemcpyAsync(sig.data(), nrm, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
     t_svd.stop(s);
@@ -711,6 +1056,11 @@ fdtd_status build(const fdtd_rom_spec* sp, fdtd_rom_built* out) {
   assemble_h_kernel<<<blocks(g.nH, 256), 256, 0, b.s>>>(g, b.r22, b.colT, b.valT);
   schur_diag_kernel<<<blocks(std::max(g.nEc, g.nH), 256), 256, 0, b.s>>>(g, b.s0, b.r11, b.f11, b.r22, b.col, b.val,
                                                                           b.d, b.dH, b.minv);
+  {  // FDTD_ROM_SOLVER=e: the E-form (Jacobi-preconditioned CG on the E-node Schur complement)
+    const char* sv = getenv("FDTD_ROM_SOLVER");
+    b.h_form = !(sv && sv[0] == 'e');
+  }
+  if (b.h_form) STCK(b.setup_mg());
   CUCK(cudaMemcpyAsync(b.cdiag, b.r11, sizeof(double) * g.nEc, cudaMemcpyDeviceToDevice, b.s));
   CUCK(cudaMemcpyAsync(b.cdiag + g.nEc, b.r22, sizeof(double) * g.nH, cudaMemcpyDeviceToDevice, b.s));
   CUCK(cudaGetLastError());

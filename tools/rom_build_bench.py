@@ -56,6 +56,24 @@ def cases(which):
     return out
 
 
+def embedded_rods4(mg, mc, dtf3, steps=3000):
+    """Probe series (line probe at x = 19 mm) of the four-rod waveguide with the GPU-built and the
+    CPU-built model embedded (fp64 GPU runs, same scene): their relative L2 difference."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import rods4_replay as r4
+    from helpers import gpu_from_scene
+    dt = 0.99 * min(sc.cfl_limit(r4.DX, r4.DX), dtf3)
+    out = []
+    for m in (mc, mg):
+        s = r4.scene(m, dt, steps)
+        g = gpu_from_scene(s, record_capacity=steps + 16)
+        g.step(steps)
+        out.append(g.probe().mean(axis=0))
+        g.close()
+    return dict(steps=steps, dt=dt, probe_rel_l2=float(np.linalg.norm(out[1] - out[0]) / np.linalg.norm(out[0])))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", default="cfg4,cfg5,rods4")
@@ -77,11 +95,16 @@ def main():
         mc = rg.build_rom(bx, by, r, dx, dx, fe, fs, q, fmax, dt_target=dt)
         t_cpu = time.perf_counter() - t0
         errs = max_rel(mg, mc)
+        if name.startswith("rods4"):  # embedded response: both models in the Sec. VI-C waveguide
+            row_resp = embedded_rods4(mg, mc, dt)
+        else:
+            row_resp = None
         row = dict(model=name, fine_cells=bx * r * by * r, full_order=rg.full_order(sysf), q1=mg["q1"], q2=mg["q2"],
                    q1_cpu=mc["q1"], q2_cpu=mc["q2"], n_clipped=mg["n_clipped"], n_clipped_cpu=mc["n_clipped"],
                    gpu_s=t_gpu, cpu_s=t_cpu, cpu_threads=os.cpu_count(), speedup=t_cpu / t_gpu,
                    fine_dt_limit_cpu_s=t_dtf, gpu_phases_ms=mg["gpu_build"], max_rel_spectrum_diff=errs,
-                   natural_dt_limit_ratio=mg["natural_dt_limit"] / mc["natural_dt_limit"])
+                   natural_dt_limit_ratio=mg["natural_dt_limit"] / mc["natural_dt_limit"],
+                   embedded_response=row_resp)
         print(json.dumps(row), flush=True)
         res.append(row)
     with open(args.out, "w") as f:
