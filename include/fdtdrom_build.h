@@ -14,12 +14,14 @@
  *      Gram-Schmidt run twice in the C inner product, deflation 1e-10; the shifted systems are
  *      solved through the E-node Schur complement diag(2 F11 + s0 R11) + K (s0 R22)^{-1} K^T with
  *      Jacobi-preconditioned conjugate gradients (one CTA per right-hand side);
- *   3. the E and H rows of the basis orthonormalised separately by one-sided Jacobi SVD (leading
- *      directions first, relative rank tolerance 1e-12): V = blkdiag(V1, V2) (eq:V L394-400);
+ *   3. the E and H rows of the basis orthonormalised separately, column by column in Krylov order
+ *      (classical Gram-Schmidt twice, deflation 1e-10), the first q1 / q2 directions kept:
+ *      V = blkdiag(V1, V2) (eq:V L394-400);
  *   4. congruence eq:R11_tilde .. eq:K_tilde (L431-447): R~11 = V1^T R11 V1, R~22, F~11,
  *      K~ = V1^T K V2, L~ = V1^T L_c (the port rows of V1);
  *   5. optionally the CFL extension (eq:CFLgeneralized L741-745, R11/R12): the singular
- *      values of R~11^{-1/2} K~ R~22^{-1/2} are clipped at (2 / dt_target)(1 - 1e-6).
+ *      values of R~11^{-1/2} K~ R~22^{-1/2} (one-sided Jacobi SVD) are clipped at
+ *      (2 / dt_target)(1 - 1e-6).
  * The same algorithm, step for step, is inputs/romgen.py (the CPU input generator); the two share
  * no code.  Only the collapsed-port form is built here (not the literal nP-port basis of NEXT-1).
  *

@@ -15,7 +15,8 @@ Pipeline (citations are PAPER.md lines):
      under eq:equalE (L608-611); ports become the nY coarse interface edges.
   3. ``sprim``        -- SPRIM (L393): block Arnoldi on (G + s0 C)^{-1} C with
      starting block (G + s0 C)^{-1} B, basis split into E / H rows and each part
-     orthonormalised, giving V = blkdiag(V1, V2) (eq:V L394-400; R10).
+     orthonormalised in Krylov order, giving V = blkdiag(V1, V2) (eq:V L394-400;
+     DESIGN.md R10).
   4. ``reduce``       -- congruence eq:R11_tilde ... eq:K_tilde (L431-447).
   5. ``extend_cfl``   -- clip the singular values of R11~^-1/2 K~ R22~^-1/2 at
      2/dt_target (eq:CFLgeneralized L741-745; R11/R12).
@@ -232,7 +233,9 @@ def sprim_basis(csys, q, fmax, defl_tol=1e-10):
     """SPRIM basis with q1 = ceil(q/2), q2 = floor(q/2) where the Krylov space allows it.
 
     The E and H parts of an m-vector Krylov basis can have rank < m, so m grows until both parts
-    reach their share (or the space is exhausted); each part keeps its leading directions.
+    reach their share (or the space is exhausted); each part keeps its first directions in Krylov
+    order (the span of the E / H rows of the leading Krylov vectors, so the moments they match and
+    the port directions of the first block are never traded for later ones).
     """
     q1w, q2w = (q + 1) // 2, q // 2
     m = q1w
@@ -308,9 +311,32 @@ def _sprim_basis_m(csys, m, fmax, defl_tol=1e-10):
         Y = solve(r11[:, None] * Wb[:nEc], r22[:, None] * Wb[nEc:])  # M w = (G+s0C)^-1 C w
         block = [Y[:, c] for c in range(Y.shape[1])]
     Wm = Wmat[:, :len(W)]
-    V1 = _orth(Wm[:nEc])
-    V2 = _orth(Wm[nEc:])
+    V1 = _orth_ordered(Wm[:nEc])
+    V2 = _orth_ordered(Wm[nEc:])
     return V1, V2
+
+
+def _orth_ordered(A, tol=1e-10):
+    """Orthonormal basis of span(A) built column by column in Krylov order (classical Gram-Schmidt
+    run twice; a column is deflated when less than tol of its norm remains), so that the first k
+    directions span the E (or H) rows of the first Krylov vectors and keep their moments, ports
+    included (R10)."""
+    Q = np.zeros_like(A)
+    k = 0
+    for j in range(A.shape[1]):
+        v = A[:, j].copy()
+        n0 = np.linalg.norm(v)
+        if n0 == 0.0:
+            continue
+        for _ in range(2):
+            if k:
+                v = v - Q[:, :k] @ (Q[:, :k].T @ v)
+        n1 = np.linalg.norm(v)
+        if n1 <= tol * n0:
+            continue
+        Q[:, k] = v / n1
+        k += 1
+    return Q[:, :k]
 
 
 def _orth(A, tol=1e-12):

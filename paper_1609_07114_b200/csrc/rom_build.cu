@@ -13,6 +13,7 @@
 // collapsed K with r entries on port rows and 2 on interior rows; K^T with 4 entries per cell).
 // The CG runs one CTA per right-hand side for the whole iteration (vectors stay in L2), the
 // Jacobi SVD one CTA per column pair and round, the dense products in a tiled fp64 kernel.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -28,6 +29,8 @@
 #include "fdtdrom_build.h"
 
 namespace {
+
+namespace cg = cooperative_groups;
 
 constexpr double PI = 3.14159265358979323846;
 constexpr double MU0 = 4.0e-7 * PI;
@@ -521,7 +524,7 @@ constexpr int RN_NT = 1024;
 __global__ void __launch_bounds__(RN_NT) cnorm2_kernel(const double* c, const double* v, int n, double* out) {
   __shared__ double red[32];
   double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += RN_NT) s += c[i] * v[i] * v[i];
+  for (int i = threadIdx.x; i < n; i += RN_NT) s += (c ? c[i] : 1.0) * v[i] * v[i];
   s = block_sum<RN_NT>(s, red);
   if (threadIdx.x == 0) *out = s;
 }
@@ -532,7 +535,7 @@ __global__ void __launch_bounds__(GV_NT) wtcv_kernel(const double* W, int ldw, c
   __shared__ double red[32];
   const double* w = W + (size_t)blockIdx.x * ldw;
   double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += GV_NT) s += w[i] * c[i] * v[i];
+  for (int i = threadIdx.x; i < n; i += GV_NT) s += w[i] * (c ? c[i] : 1.0) * v[i];
   s = block_sum<GV_NT>(s, red);
   if (threadIdx.x == 0) h[blockIdx.x] = s;
 }
@@ -559,13 +562,12 @@ __global__ void gather_cols_kernel(const double* In, int ldi, const int* idx, co
 // ---- one-sided Jacobi SVD (Hestenes): one round of the round-robin pairing, one CTA per pair.
 // Players 0 .. mp-1 (mp even); in round t player 0 is fixed and the others rotate.
 constexpr int JB_NT = 256;
-__global__ void __launch_bounds__(JB_NT) jacobi_round_kernel(double* A, int lda, int rows, int m, double* V,
-                                                             int ldv, int vrows, int mp, int t, double tol,
-                                                             int* rotated) {
-  __shared__ double red[32];
+__device__ __forceinline__ void jacobi_pair(double* A, int lda, int rows, int m, double* V, int ldv, int vrows,
+                                            int mp, int t, int pair, double tol, double floor2, int* rotated,
+                                            double* red) {
   auto player = [&](int k) { return k == 0 ? 0 : (k - 1 + t) % (mp - 1) + 1; };
-  int a = player(blockIdx.x), b = player(mp - 1 - blockIdx.x);
-  if (a >= m || b >= m) return;
+  int a = player(pair), b = player(mp - 1 - pair);
+  if (a >= m || b >= m) return;  // uniform over the CTA
   if (a > b) { const int x = a; a = b; b = x; }
   double* ca = A + (size_t)a * lda;
   double* cb = A + (size_t)b * lda;
@@ -577,7 +579,9 @@ __global__ void __launch_bounds__(JB_NT) jacobi_round_kernel(double* A, int lda,
   al = block_sum<JB_NT>(al, red);
   be = block_sum<JB_NT>(be, red);
   ga = block_sum<JB_NT>(ga, red);
-  if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) return;
+  // converged pair, or a column at rounding level of the largest (floor2 = (1e-15 s_max)^2): such
+  // directions are below every rank tolerance used here and would rotate forever on noise
+  if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be) || al < floor2 || be < floor2) return;
   const double zeta = (be - al) / (2.0 * ga);
   const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
   const double cs = 1.0 / hypot(1.0, tt), sn = cs * tt;
@@ -596,6 +600,25 @@ __global__ void __launch_bounds__(JB_NT) jacobi_round_kernel(double* A, int lda,
     }
   }
   if (threadIdx.x == 0) atomicAdd(rotated, 1);
+  __syncthreads();
+}
+__global__ void __launch_bounds__(JB_NT) jacobi_round_kernel(double* A, int lda, int rows, int m, double* V,
+                                                             int ldv, int vrows, int mp, int t, double tol,
+                                                             double floor2, int* rotated) {
+  __shared__ double red[32];
+  jacobi_pair(A, lda, rows, m, V, ldv, vrows, mp, t, blockIdx.x, tol, floor2, rotated, red);
+}
+// a whole sweep (mp - 1 rounds) in one cooperative launch: grid-wide barrier between rounds
+__global__ void __launch_bounds__(JB_NT) jacobi_sweep_kernel(double* A, int lda, int rows, int m, double* V,
+                                                             int ldv, int vrows, int mp, double tol, double floor2,
+                                                             int* rotated) {
+  __shared__ double red[32];
+  cg::grid_group grid = cg::this_grid();
+  for (int t = 0; t < mp - 1; ++t) {
+    for (int pair = blockIdx.x; pair < mp / 2; pair += gridDim.x)
+      jacobi_pair(A, lda, rows, m, V, ldv, vrows, mp, t, pair, tol, floor2, rotated, red);
+    grid.sync();
+  }
 }
 // norms of the columns
 __global__ void __launch_bounds__(JB_NT) colnorm_kernel(const double* A, int lda, int rows, double* out) {
@@ -716,6 +739,18 @@ struct Builder {
   int h_cols = 0;
   long wstride = 0;
   bool h_form = true;
+  int coop_grid = 0;  // co-resident CTAs of the cooperative Jacobi sweep (0: one launch per round)
+
+  void setup_coop() {
+    int dev_id = 0, nsm = 0, per = 0, coop = 0;
+    cudaGetDevice(&dev_id);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev_id);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev_id);
+    if (coop && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, jacobi_sweep_kernel, JB_NT, 0) == cudaSuccess)
+      coop_grid = per * nsm;
+    const char* e = getenv("FDTD_ROM_JACOBI_ROUNDS");  // 1: one launch per round (comparison)
+    if (e && e[0] == '1') coop_grid = 0;
+  }
 
   fdtd_status setup_mg() {
     long off = 0;
@@ -824,23 +859,46 @@ struct Builder {
   // non-null.  sig: column norms afterwards (unsorted).
   // Jacobi sweeps on A (rows x m, ld lda) until no pair rotates; V (m x m) accumulates the
   // rotations (initialised to I when init is set).
-  fdtd_status jacobi_sweeps(double* A, int lda, int rows, int m, double* V, bool init) {
+  fdtd_status jacobi_sweeps(double* A, int lda, int rows, int m, double* V, bool init, double tol = 0.0,
+                             double floor_rel = 1e-15) {
     if (V && init) identity_kernel<<<blocks((long)m * m, 256), 256, 0, s>>>(V, m);
     const int mp = m + (m & 1);
     // converged when every pair is orthogonal to sqrt(m) eps relative (the dgesvj criterion)
-    const double tol = std::max(1e-15, std::sqrt((double)m) * 2.220446049250313e-16);
+    if (tol <= 0) tol = std::max(1e-15, std::sqrt((double)m) * 2.220446049250313e-16);
     int* rot = (int*)scal;
+    double floor2 = 0.0;
+    {
+      double* nrm = dev.alloc<double>(m);
+      if (!nrm) return failf(FDTD_E_NOMEM, "jacobi");
+      colnorm_kernel<<<m, JB_NT, 0, s>>>(A, lda, rows, nrm);
+      std::vector<double> h(m);
+      CUCK(cudaMemcpyAsync(h.data(), nrm, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+      CUCK(cudaStreamSynchronize(s));
+      const double mx = *std::max_element(h.begin(), h.end());
+      floor2 = (floor_rel * mx) * (floor_rel * mx);  // column norms only shrink below the largest
+    }
     int sweeps = 0;
     for (; sweeps < 60; ++sweeps) {
       CUCK(cudaMemsetAsync(rot, 0, sizeof(int), s));
-      for (int t = 0; t < mp - 1; ++t)
-        jacobi_round_kernel<<<mp / 2, JB_NT, 0, s>>>(A, lda, rows, m, V, m, m, mp, t, tol, rot);
+      if (coop_grid > 0 && mp > 2) {  // one launch per sweep
+        int ldv = m, vrows = m;
+        double* Vp = V;
+        double tl = tol;
+        int mm = m, mpp = mp, ld = lda, rw = rows;
+        void* args[] = {&A, &ld, &rw, &mm, &Vp, &ldv, &vrows, &mpp, &tl, &floor2, &rot};
+        CUCK(cudaLaunchCooperativeKernel((void*)jacobi_sweep_kernel, dim3(std::min(coop_grid, mp / 2)), dim3(JB_NT),
+                                         args, 0, s));
+      } else {
+        for (int t = 0; t < mp - 1; ++t)
+          jacobi_round_kernel<<<mp / 2, JB_NT, 0, s>>>(A, lda, rows, m, V, m, m, mp, t, tol, floor2, rot);
+      }
       int h = 0;
       CUCK(cudaMemcpyAsync(&h, rot, sizeof(int), cudaMemcpyDeviceToHost, s));
       CUCK(cudaStreamSynchronize(s));
       if (h == 0) break;
     }
     jac_sweeps_max = std::max(jac_sweeps_max, sweeps + 1);
+    if (getenv("FDTD_ROM_VERBOSE")) fprintf(stderr, "jacobi %d x %d: %d sweeps\n", rows, m, sweeps + 1);
     CUCK(cudaGetLastError());
     return FDTD_OK;
   }
@@ -849,24 +907,25 @@ struct Builder {
   // non-null.  sig: column norms afterwards (unsorted).  Tall A is first rotated by the
   // eigenvectors of its Gram matrix A^T A (itself diagonalised by Jacobi), after which the
   // columns are orthogonal up to the Gram matrix's rounding and few sweeps remain.
-  fdtd_status jacobi(double* A, int lda, int rows, int m, double* V, std::vector<double>& sig) {
+  fdtd_status jacobi(double* A, int lda, int rows, int m, double* V, std::vector<double>& sig,
+                     double floor_rel = 1e-15) {
     sig.assign(m, 0.0);
     if (m == 0) return FDTD_OK;
     t_svd.start(s);
-    if (rows >= 2 * m && m >= 16) {
+    if (rows > m && m >= 16) {
       double* G = dev.alloc<double>((size_t)m * m);
       double* Vg = dev.alloc<double>((size_t)m * m);
       double* T = dev.alloc<double>((size_t)rows * m);
       if (!G || !Vg || !T) return failf(FDTD_E_NOMEM, "jacobi preconditioning");
       gemm<true, false>(m, m, rows, A, lda, nullptr, A, lda, G, m);
-      STCK(jacobi_sweeps(G, m, m, m, Vg, true));
+      STCK(jacobi_sweeps(G, m, m, m, Vg, true, 1e-10, 1e-12));  // a preconditioner: loose
       gemm<false, false>(rows, m, m, A, lda, nullptr, Vg, m, T, rows);
       CUCK(cudaMemcpy2DAsync(A, (size_t)lda * 8, T, (size_t)rows * 8, (size_t)rows * 8, m, cudaMemcpyDeviceToDevice,
                              s));
       if (V) CUCK(cudaMemcpyAsync(V, Vg, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, s));
-      STCK(jacobi_sweeps(A, lda, rows, m, V, false));
+      STCK(jacobi_sweeps(A, lda, rows, m, V, false, 0.0, floor_rel));
     } else {
-      STCK(jacobi_sweeps(A, lda, rows, m, V, true));
+      STCK(jacobi_sweeps(A, lda, rows, m, V, true, 0.0, floor_rel));
     }
     double* nrm = dev.alloc<double>(m);
     if (!nrm) return failf(FDTD_E_NOMEM, "jacobi");
@@ -877,26 +936,33 @@ struct Builder {
     return FDTD_OK;
   }
 
-  // _orth: U (rows x k) = leading left singular vectors of A (rows x m) with s > 1e-12 s_max,
-  // in descending order of s (A is destroyed).
-  fdtd_status orth(double* A, int lda, int rows, int m, double* U, int ldu, int& k) {
-    std::vector<double> sg;
-    STCK(jacobi(A, lda, rows, m, nullptr, sg));
-    std::vector<int> perm(m);
-    std::iota(perm.begin(), perm.end(), 0);
-    std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return sg[x] > sg[y]; });
-    const double smax = m ? sg[perm[0]] : 0.0;
+  // U (rows x k): orthonormal basis of span(A) (rows x m) built column by column in Krylov order
+  // (classical Gram-Schmidt twice, Euclidean; a column is deflated when less than 1e-10 of its norm
+  // remains) -- romgen._orth_ordered, R10
+  fdtd_status orth(const double* A, int lda, int rows, int m, double* U, int ldu, int& k) {
     k = 0;
-    while (k < m && smax > 0 && sg[perm[k]] > 1e-12 * smax) ++k;
-    if (k == 0) return FDTD_OK;
-    std::vector<double> sc(k);
-    for (int t = 0; t < k; ++t) sc[t] = 1.0 / sg[perm[t]];
-    int* dperm = dev.alloc<int>(k);
-    double* dsc = dev.alloc<double>(k);
-    if (!dperm || !dsc) return failf(FDTD_E_NOMEM, "orth");
-    CUCK(cudaMemcpyAsync(dperm, perm.data(), sizeof(int) * k, cudaMemcpyHostToDevice, s));
-    CUCK(cudaMemcpyAsync(dsc, sc.data(), sizeof(double) * k, cudaMemcpyHostToDevice, s));
-    permute_scale_kernel<<<dim3(blocks(rows, 256), k), 256, 0, s>>>(A, lda, dperm, dsc, rows, U, ldu, k);
+    double* v = dev.alloc<double>(rows);
+    double* h = dev.alloc<double>(std::max(m, 1));
+    if (!v || !h) return failf(FDTD_E_NOMEM, "orth");
+    double* nrm = scal + 24;
+    t_orth.start(s);
+    for (int j = 0; j < m; ++j) {
+      CUCK(cudaMemcpyAsync(v, A + (size_t)j * lda, sizeof(double) * rows, cudaMemcpyDeviceToDevice, s));
+      cnorm2_kernel<<<1, RN_NT, 0, s>>>(nullptr, v, rows, nrm);
+      for (int pass = 0; pass < 2 && k > 0; ++pass) {
+        wtcv_kernel<<<k, GV_NT, 0, s>>>(U, ldu, nullptr, v, rows, h);
+        v_minus_wh_kernel<<<blocks(rows, 256), 256, 0, s>>>(U, ldu, h, k, v, rows);
+      }
+      cnorm2_kernel<<<1, RN_NT, 0, s>>>(nullptr, v, rows, nrm + 1);
+      double nn[2];
+      CUCK(cudaMemcpyAsync(nn, nrm, sizeof nn, cudaMemcpyDeviceToHost, s));
+      CUCK(cudaStreamSynchronize(s));
+      const double n0 = std::sqrt(nn[0]), n1 = std::sqrt(nn[1]);
+      if (n0 == 0.0 || n1 <= 1e-10 * n0) continue;
+      scale_copy_kernel<<<blocks(rows, 256), 256, 0, s>>>(v, 1.0 / n1, U + (size_t)k * ldu, rows);
+      ++k;
+    }
+    t_orth.stop(s);
     CUCK(cudaGetLastError());
     return FDTD_OK;
   }
@@ -966,15 +1032,9 @@ struct Builder {
       STCK(solve(bE, g.nEc, bH, g.nH, nb, blk));
     }
     used = k;
-    // V1 = orth(W_E), V2 = orth(W_H) (copies: the SVD overwrites its input)
-    double* WE = dev.alloc<double>((size_t)g.nEc * std::max(k, 1));
-    double* WH = dev.alloc<double>((size_t)g.nH * std::max(k, 1));
-    if (!WE || !WH) return failf(FDTD_E_NOMEM, "orth copies");
-    CUCK(cudaMemcpy2DAsync(WE, (size_t)g.nEc * 8, W, (size_t)N * 8, (size_t)g.nEc * 8, k, cudaMemcpyDeviceToDevice, s));
-    CUCK(cudaMemcpy2DAsync(WH, (size_t)g.nH * 8, W + g.nEc, (size_t)N * 8, (size_t)g.nH * 8, k,
-                           cudaMemcpyDeviceToDevice, s));
-    STCK(orth(WE, g.nEc, g.nEc, k, V1, g.nEc, k1));
-    STCK(orth(WH, g.nH, g.nH, k, V2, g.nH, k2));
+    // V1, V2: the E and H rows of W orthonormalised in Krylov order
+    STCK(orth(W, N, g.nEc, k, V1, g.nEc, k1));
+    STCK(orth(W + g.nEc, N, g.nH, k, V2, g.nH, k2));
     return FDTD_OK;
   }
 };
@@ -1061,6 +1121,7 @@ fdtd_status build(const fdtd_rom_spec* sp, fdtd_rom_built* out) {
     b.h_form = !(sv && sv[0] == 'e');
   }
   if (b.h_form) STCK(b.setup_mg());
+  b.setup_coop();
   CUCK(cudaMemcpyAsync(b.cdiag, b.r11, sizeof(double) * g.nEc, cudaMemcpyDeviceToDevice, b.s));
   CUCK(cudaMemcpyAsync(b.cdiag + g.nEc, b.r22, sizeof(double) * g.nH, cudaMemcpyDeviceToDevice, b.s));
   CUCK(cudaGetLastError());

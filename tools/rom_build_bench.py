@@ -81,6 +81,8 @@ def main():
     args = ap.parse_args()
     fe, fs = sc.uniform_fill(2, 2, 2, 1, 1, 4, 0, 0.05)
     build_rom(2, 2, 2, DX, DY, fe, fs, 8, 30e9)  # context + module load
+    fe, fs = sc.uniform_fill(4, 4, 3, 1, 1, 4, 0, 0.05)
+    build_rom(4, 4, 3, DX, DY, fe, fs, 40, 30e9)  # ... and the cooperative Jacobi path
     res = []
     for name, bx, by, r, fe, fs, q, fmax, clip, dx in cases(args.cases.split(",")):
         t0 = time.perf_counter()
