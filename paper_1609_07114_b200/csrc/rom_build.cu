@@ -159,16 +159,6 @@ __global__ void schur_diag_kernel(Geo g, double s0, const double* r11, const dou
   minv[e] = 1.0 / s;
 }
 
-// Y[:, c] = K^T X[:, c] (nH rows)
-__global__ void kt_apply_kernel(Geo g, const int* colT, const double* valT, const double* X, int ldx, double* Y,
-                                int ldy, int ncol) {
-  const int h = blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y;
-  if (h >= g.nH || c >= ncol) return;
-  const double* x = X + (size_t)c * ldx;
-  Y[(size_t)c * ldy + h] = valT[4 * h] * x[colT[4 * h]] + valT[4 * h + 1] * x[colT[4 * h + 1]] +
-                           valT[4 * h + 2] * x[colT[4 * h + 2]] + valT[4 * h + 3] * x[colT[4 * h + 3]];
-}
-
 // Y[:, c] = A[:, c] + K (w o X[:, c]) (nEc rows; w = nullptr: 1, A = nullptr: 0)
 __global__ void k_apply_kernel(Geo g, const int* col, const double* val, const double* w, const double* X, int ldx,
                                const double* A, int lda, double* Y, int ldy, int ncol) {

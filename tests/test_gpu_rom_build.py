@@ -45,11 +45,18 @@ def _compare(mg, mc, tol):
     return errs
 
 
-@pytest.mark.parametrize("case", ["uniform", "lossy_random", "inclusion"])
+@pytest.mark.parametrize("case", ["uniform", "lossy_random", "inclusion", "r1", "strip"])
 def test_gpu_build_matches_romgen_invariants(case):
     if case == "uniform":
         bx, by, r, q = 3, 2, 3, 20
         fe, fs = sc.uniform_fill(bx, by, r, 1, 1, 4, 0, 0.05)
+    elif case == "r1":  # no refinement: every port is one fine edge
+        bx, by, r, q = 5, 3, 1, 12
+        fe, fs = sc.uniform_fill(bx, by, r, 3, 1, 4, 0, 0.05)
+    elif case == "strip":  # one coarse row, odd fine sizes (ragged multigrid levels)
+        bx, by, r, q = 7, 1, 5, 24
+        rng = np.random.default_rng(2)
+        fe, fs = rng.uniform(1, 6, (by * r, bx * r)), rng.uniform(0, 0.1, (by * r, bx * r))
     elif case == "lossy_random":
         bx, by, r, q = 4, 3, 4, 32
         rng = np.random.default_rng(5)

@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(256, 2) walk(const float* a0, const float* a1,
       const uint32_t o = (uint32_t)(j + 1 + PFD) * P + c;
       pf(a0 + o); pf(a1 + o); pf(a2 + o); pf(a3 + o); pf(a4 + o);
     }
-    if (j >= r0 && lane >= 2 && lane < 30) {
+    if (j >= r0 && lane >= (V == 2 ? 2 : 1) && lane < (V == 2 ? 30 : 31)) {
       const uint32_t o = (uint32_t)(j - 3) * P + c;
       VT s;
       s.x = y0.x + y1.x * y3.x; s.y = y0.y + y1.y * y3.y;
@@ -142,6 +142,13 @@ int main() {
       if (pfd == 3) time([&] { walk<2, 3><<<g2, wpc * 32>>>(buf[0], buf[1], buf[2], buf[3], buf[4], buf[5], buf[6], buf[7], P, ny, chunk, nout); }, "walk V2 pfd3 ch256 w4", bytes);
       else time([&] { walk<2, 4><<<g2, wpc * 32>>>(buf[0], buf[1], buf[2], buf[3], buf[4], buf[5], buf[6], buf[7], P, ny, chunk, nout); }, "walk V2 pfd4 ch256 w4", bytes);
     }
+  }
+  {
+    const int nout = 30, wpc = 4, chunk = 256;  // V = 4: 16-byte vectors, one halo lane per side
+    dim3 g((nx / 4 + nout * wpc - 1) / (nout * wpc), ny / chunk);
+    time([&] { walk<4, 1><<<g, wpc * 32>>>(buf[0], buf[1], buf[2], buf[3], buf[4], buf[5], buf[6], buf[7], P, ny, chunk, nout); }, "walk V4 pfd1 ch256 w4", bytes);
+    time([&] { walk<4, 0><<<g, wpc * 32>>>(buf[0], buf[1], buf[2], buf[3], buf[4], buf[5], buf[6], buf[7], P, ny, chunk, nout); }, "walk V4 pfd0 ch256 w4", bytes);
+    time([&] { walk<4, 2><<<g, wpc * 32>>>(buf[0], buf[1], buf[2], buf[3], buf[4], buf[5], buf[6], buf[7], P, ny, chunk, nout); }, "walk V4 pfd2 ch256 w4", bytes);
   }
   time([&] { copyk<<<148 * 8, 512>>>((const float4*)buf[0], (float4*)buf[5], n / 4); }, "copy (1 in 1 out)", 8.0 * n);
   return 0;
