@@ -170,14 +170,20 @@ __device__ __forceinline__ T cell_energy(T acc, T ex, T ey, T h0, T h1, T wx, T 
 }
 
 // Per-cell coefficient set of one row of a warp strip (K1): the cell's bottom Ex edge
-// (cax, cbx), left Ey edge (cay, cby), the energy weights of those edges (wx, wy; 0 if dead or a
-// zone cell) and hw = mu0 dx dy/dt (+0 on zone cells: the fix-up adds their energy; -0 on dead
-// cells, whose Hz is kept).  Built once per pass at stage 0 and reused by stages 1..K-1.
+// (cax, cbx), left Ey edge (cay, cby) and the energy weights of those edges (wx, wy; 0 if dead or a
+// zone cell).  The cell's own flags ride in the sign bits of the weights, which are otherwise
+// non-negative: wx = -0 on a dead cell (hole, wall, padding: its Hz is kept), wy = -0 on a fix-up
+// zone cell (the fix-up adds its energy); the Hz weight mu0 dx dy/dt applies when neither is set
+// (cell_hw).  Six vectors per row: built once per pass at stage 0, reused by stages 1..K-1.
 template <typename T, int V>
 struct RowCoef {
-  T cax[V], cbx[V], cay[V], cby[V], wx[V], wy[V], hw[V];
+  T cax[V], cbx[V], cay[V], cby[V], wx[V], wy[V];
 };
-constexpr int NCOEF = 7;
+constexpr int NCOEF = 6;
+template <typename T>
+__device__ __forceinline__ bool cell_dead(T wx) { return signbit(wx); }
+template <typename T>
+__device__ __forceinline__ T cell_hw(T wx, T wy, T wh) { return (signbit(wx) | signbit(wy)) ? T(0) : wh; }
 
 template <typename T, int V>
 __device__ __forceinline__ void row_coef(const T (&ma)[V], const T (&ms)[V], const T (&mb)[V], const T (&sb)[V],
@@ -191,9 +197,9 @@ __device__ __forceinline__ void row_coef(const T (&ma)[V], const T (&ms)[V], con
     edge_coef(mb[k], sb[k], ma[k], ms[k], idy, cf.cax[k], cf.cbx[k], ax, lx);
     edge_coef(k ? ma[k - 1] : la, k ? ms[k - 1] : ls, ma[k], ms[k], -idx, cf.cay[k], cf.cby[k], ay, ly);
     const bool z = signbit(ms[k]);
-    cf.wx[k] = (lx && !z) ? mul_rn(wxy, ax) : T(0);
-    cf.wy[k] = (ly && !z) ? mul_rn(wxy, ay) : T(0);
-    cf.hw[k] = ma[k] < T(0) ? T(-0.0) : (z ? T(0) : wh);
+    cf.wx[k] = (lx && !z) ? mul_rn(wxy, ax) : (ma[k] < T(0) ? T(-0.0) : T(0));  // a dead cell has no live edge
+    cf.wy[k] = (ly && !z) ? mul_rn(wxy, ay) : (z ? T(-0.0) : T(0));
+    (void)wh;
   }
 }
 
@@ -202,7 +208,6 @@ __device__ __forceinline__ void row_coef(const T (&ma)[V], const T (&ms)[V], con
 template <typename T, int V>
 struct CoefRegs {
   const RowCoef<T, V>& c;
-  __device__ __forceinline__ void hw(T (&o)[V]) const { for (int k = 0; k < V; ++k) o[k] = c.hw[k]; }
   __device__ __forceinline__ void ex(T (&a)[V], T (&b)[V]) const {
     for (int k = 0; k < V; ++k) { a[k] = c.cax[k]; b[k] = c.cbx[k]; }
   }
@@ -216,7 +221,6 @@ struct CoefRegs {
 template <typename T, int V>
 struct CoefRing {
   const T* b;  // this lane's slot: component i at b + i * 32 * V
-  __device__ __forceinline__ void hw(T (&o)[V]) const { ldv_s(b + 6 * 32 * V, o); }
   __device__ __forceinline__ void ex(T (&a)[V], T (&c)[V]) const { ldv_s(b, a); ldv_s(b + 32 * V, c); }
   __device__ __forceinline__ void ey(T (&a)[V], T (&c)[V]) const { ldv_s(b + 2 * 32 * V, a); ldv_s(b + 3 * 32 * V, c); }
   __device__ __forceinline__ void w(T (&a)[V], T (&c)[V]) const { ldv_s(b + 4 * 32 * V, a); ldv_s(b + 5 * 32 * V, c); }
@@ -233,12 +237,12 @@ __device__ __forceinline__ T yee_row(const T (&exb)[V], const T (&ext)[V], const
                                      const T (&hb)[V], const CS& cs, const SweepParams<T>& p, T gsrc,
                                      bool srow, int src_k, T (&hn)[V], T (&exo)[V], T (&eyo)[V]) {
   const T eyr = __shfl_down_sync(FULL, ey[0], 1);
-  T hw[V];
-  cs.hw(hw);
+  T wx[V], wy[V];  // energy weights, with the dead / zone flags in their sign bits
+  cs.w(wx, wy);
 #pragma unroll
   for (int k = 0; k < V; ++k) {
     const T hu = hupd(hz[k], ext[k], exb[k], k + 1 < V ? ey[k + 1] : eyr, ey[k], p.chy, p.chx);
-    hn[k] = signbit(hw[k]) ? hz[k] : hu;  // dead cells keep their Hz
+    hn[k] = cell_dead(wx[k]) ? hz[k] : hu;  // dead cells keep their Hz
   }
   if (srow) {  // S2: soft source after the H half-step (this lane holds the source column)
 #pragma unroll
@@ -260,10 +264,9 @@ __device__ __forceinline__ T yee_row(const T (&exb)[V], const T (&ext)[V], const
   }
   T en = T(0);
   if (ENERGY) {
-    T wx[V], wy[V];
-    cs.w(wx, wy);
 #pragma unroll
-    for (int k = 0; k < V; ++k) en = cell_energy(en, exb[k], ey[k], hz[k], hn[k], wx[k], wy[k], hw[k]);
+    for (int k = 0; k < V; ++k)
+      en = cell_energy(en, exb[k], ey[k], hz[k], hn[k], wx[k], wy[k], cell_hw(wx[k], wy[k], p.wh));
   }
   return en;
 }
@@ -277,16 +280,16 @@ __device__ __forceinline__ float yee_row_f2(const float (&exb)[V], const float (
                                             float (&hn)[V], float (&exo)[V], float (&eyo)[V]) {
   static_assert(V % 2 == 0, "pairs");
   const float eyr = __shfl_down_sync(FULL, ey[0], 1);
-  float hw[V];
-  cs.hw(hw);
+  float wx[V], wy[V];  // energy weights, with the dead / zone flags in their sign bits
+  cs.w(wx, wy);
   const F2 chy{p.chy, p.chy}, mchx{-p.chx, -p.chx};
 #pragma unroll
   for (int k = 0; k < V; k += 2) {
     const F2 dex = sub2(F2{ext[k], ext[k + 1]}, F2{exb[k], exb[k + 1]});
     const F2 dey = sub2(F2{ey[k + 1], k + 2 < V ? ey[k + 2] : eyr}, F2{ey[k], ey[k + 1]});
     const F2 hu = fma2(mchx, dey, fma2(chy, dex, F2{hz[k], hz[k + 1]}));
-    hn[k] = signbit(hw[k]) ? hz[k] : hu.x;  // dead cells keep their Hz
-    hn[k + 1] = signbit(hw[k + 1]) ? hz[k + 1] : hu.y;
+    hn[k] = cell_dead(wx[k]) ? hz[k] : hu.x;  // dead cells keep their Hz
+    hn[k + 1] = cell_dead(wx[k + 1]) ? hz[k + 1] : hu.y;
   }
   if (srow) {  // S2: soft source after the H half-step (this lane holds the source column)
 #pragma unroll
@@ -316,15 +319,14 @@ __device__ __forceinline__ float yee_row_f2(const float (&exb)[V], const float (
   }
   float en = 0.f;
   if (ENERGY) {
-    float wx[V], wy[V];
-    cs.w(wx, wy);
     F2 acc{0.f, 0.f};
 #pragma unroll
     for (int k = 0; k < V; k += 2) {
       const F2 ex2{exb[k], exb[k + 1]}, ey2{ey[k], ey[k + 1]};
+      const F2 hw{cell_hw(wx[k], wy[k], p.wh), cell_hw(wx[k + 1], wy[k + 1], p.wh)};
       acc = fma2(mul2(F2{wx[k], wx[k + 1]}, ex2), ex2, acc);
       acc = fma2(mul2(F2{wy[k], wy[k + 1]}, ey2), ey2, acc);
-      acc = fma2(mul2(F2{hw[k], hw[k + 1]}, F2{hz[k], hz[k + 1]}), F2{hn[k], hn[k + 1]}, acc);
+      acc = fma2(mul2(hw, F2{hz[k], hz[k + 1]}), F2{hn[k], hn[k + 1]}, acc);
     }
     en = acc.x + acc.y;
   }
@@ -367,14 +369,12 @@ __device__ __forceinline__ void ring_store(T* ring, int slot, const RowCoef<T, V
   T* b = ring + slot * (NCOEF * 32 * V);
   stv_s(b + 0 * 32 * V, cf.cax); stv_s(b + 1 * 32 * V, cf.cbx); stv_s(b + 2 * 32 * V, cf.cay);
   stv_s(b + 3 * 32 * V, cf.cby); stv_s(b + 4 * 32 * V, cf.wx); stv_s(b + 5 * 32 * V, cf.wy);
-  stv_s(b + 6 * 32 * V, cf.hw);
 }
 template <typename T, int V>
 __device__ __forceinline__ void ring_load(const T* ring, int slot, RowCoef<T, V>& cf) {
   const T* b = ring + slot * (NCOEF * 32 * V);
   ldv_s(b + 0 * 32 * V, cf.cax); ldv_s(b + 1 * 32 * V, cf.cbx); ldv_s(b + 2 * 32 * V, cf.cay);
   ldv_s(b + 3 * 32 * V, cf.cby); ldv_s(b + 4 * 32 * V, cf.wx); ldv_s(b + 5 * 32 * V, cf.wy);
-  ldv_s(b + 6 * 32 * V, cf.hw);
 }
 
 // Row data of one stage-0 row j (loaded from HBM): Ex of edge row j+1, Ey / Hz / materials of row j
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   for (int s = 0; s < K; ++s)
 #pragma unroll
     for (int k = 0; k < V; ++k)
-      rc[s].cax[k] = rc[s].cbx[k] = rc[s].cay[k] = rc[s].cby[k] = rc[s].wx[k] = rc[s].wy[k] = rc[s].hw[k] = T(0);
+      rc[s].cax[k] = rc[s].cbx[k] = rc[s].cay[k] = rc[s].cby[k] = rc[s].wx[k] = rc[s].wy[k] = T(0);
 #endif
   const int jm = min(jb + ((x.r0 + K - jb + U - 1) / U) * U, je);
   const int jend = (warp_probes || warp_source) ? jm : jm + (max(x.r1 - jm, 0) / U) * U;
