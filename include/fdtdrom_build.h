@@ -23,7 +23,7 @@
  *      values of R~11^{-1/2} K~ R~22^{-1/2} (one-sided Jacobi SVD) are clipped at
  *      (2 / dt_target)(1 - 1e-6).
  * The same algorithm, step for step, is inputs/romgen.py (the CPU input generator); the two share
- * no code.  Only the collapsed-port form is built here (not the literal nP-port basis of NEXT-1).
+ * no code.  Both port forms: collapsed (R9) and the paper-literal nP-port set (NEXT-1).
  *
  * Ownership: host inputs are read before the call returns; outputs are written into caller
  * buffers sized for the requested order.  Device memory is allocated and freed inside the call
@@ -51,11 +51,16 @@ typedef struct {
   double fmax;           /* expansion point s0 = pi fmax (Hz)                                  */
   double dt_target;      /* > 0: clip at (2 / dt_target)(1 - 1e-6); <= 0: no clip             */
   double cg_tol;         /* relative residual of the shifted solves (<= 0: 1e-13)              */
+  int32_t literal;       /* 1: the paper-literal nP-port form (NEXT-1): ports are the nP =
+                          * 2 (bx + by) r fine boundary nodes (no collapse), the E basis is
+                          * [port unit vectors | SPRIM directions] orthonormalised in order
+                          * (q1 = nP + ceil(q/2)); output L is q1 x nP                        */
 } fdtd_rom_spec;
 
 typedef struct {
-  /* outputs (row-major, host, caller-allocated for q1 = ceil(q/2), q2 = floor(q/2) and
-   * nY = 2 bx + 2 by): R11 q1 x q1, R22 q2 x q2, F11 q1 x q1, K q1 x q2, L q1 x nY.  The built
+  /* outputs (row-major, host, caller-allocated for q1 = ceil(q/2) (literal: nP + ceil(q/2)),
+   * q2 = floor(q/2) and nY = 2 bx + 2 by (literal: nP = r nY)): R11 q1 x q1, R22 q2 x q2,
+   * F11 q1 x q1, K q1 x q2, L q1 x nY.  The built
    * orders are returned in q1 / q2 (smaller when the Krylov space is exhausted) and the arrays
    * are packed for those orders. */
   double *R11, *R22, *F11, *K, *L;

@@ -218,12 +218,12 @@ def literal_system(sysf):
 
 def with_port_directions(V1, nP):
     """Make the E basis contain the nP port-node unit vectors (ports are the first nP rows):
-    the literal coupling needs L~^T = V1[:nP] of full row rank (A1 regular, R9)."""
+    the literal coupling needs L~^T = V1[:nP] of full row rank (A1 regular, R9).
+    The port directions come first, then V1's columns in order with the port rows projected out
+    (ordered Gram-Schmidt, R10), so truncating keeps V1's leading directions."""
     P = np.zeros((V1.shape[0], nP))
     P[np.arange(nP), np.arange(nP)] = 1.0
-    rest = V1 - P @ (P.T @ V1)
-    U = _orth(rest)
-    return np.hstack([P, U])
+    return _orth_ordered(np.hstack([P, V1]))
 
 
 # --------------------------------------------------------------------------

@@ -1075,6 +1075,10 @@ fdtd_status build(const fdtd_rom_spec* sp, fdtd_rom_built* out) {
   g.bx = sp->bx; g.by = sp->by; g.r = sp->r;
   g.Nx = g.bx * g.r; g.Ny = g.by * g.r;
   g.fdx = sp->dx / g.r; g.fdy = sp->dy / g.r;
+  if (sp->literal) {  // NEXT-1 port set: every fine boundary node is a port (Geo's port math with
+                      // Nx x Ny "coarse edges" of one fine node each)
+    g.bx = g.Nx; g.by = g.Ny; g.r = 1;
+  }
   g.nY = 2 * g.bx + 2 * g.by;
   g.nEc = g.nY + (g.Ny - 1) * g.Nx + g.Ny * (g.Nx - 1);
   g.nH = g.Nx * g.Ny;
@@ -1130,8 +1134,25 @@ fdtd_status build(const fdtd_rom_spec* sp, fdtd_rom_built* out) {
     if ((k1 >= q1w && k2 >= q2w) || m >= g.nEc + g.nH) break;
     m = (int)(m + std::max({q1w - k1, q2w - k2, 1}) * 1.5);
   }
-  const int q1 = std::min(k1, q1w), q2 = std::min(k2, q2w);
+  int q1 = std::min(k1, q1w);
+  const int q2 = std::min(k2, q2w);
   if (q1 < 1 || q2 < 1) return failf(FDTD_E_STATE, "empty basis (q1 %d, q2 %d)", q1, q2);
+  if (sp->literal) {  // the E basis must span the nP port directions (A1 regular, R9):
+                      // [P | V1] orthonormalised in order, the first nP + ceil(q/2) kept
+    const int nP = g.nY, mc = nP + q1;
+    double* PV = b.dev.alloc<double>((size_t)g.nEc * mc);
+    double* VL = b.dev.alloc<double>((size_t)g.nEc * mc);
+    if (!PV || !VL) return failf(FDTD_E_NOMEM, "literal basis");
+    std::vector<double> one(1, 1.0);
+    for (int k = 0; k < nP; ++k)
+      CUCK(cudaMemcpyAsync(PV + (size_t)k * g.nEc + k, one.data(), sizeof(double), cudaMemcpyHostToDevice, b.s));
+    CUCK(cudaMemcpy2DAsync(PV + (size_t)nP * g.nEc, (size_t)g.nEc * 8, V1, (size_t)g.nEc * 8, (size_t)g.nEc * 8, q1,
+                           cudaMemcpyDeviceToDevice, b.s));
+    int kl = 0;
+    STCK(b.orth(PV, g.nEc, g.nEc, mc, VL, g.nEc, kl));
+    V1 = VL;
+    q1 = std::min(kl, nP + q1w);
+  }
 
   // congruence (eq:R11_tilde .. eq:K_tilde)
   double* R11 = b.dev.alloc<double>((size_t)q1 * q1);

@@ -55,7 +55,7 @@ class Info(C.Structure):
 class RomSpec(C.Structure):  # fdtdrom_build.h
     _fields_ = [("bx", C.c_int32), ("by", C.c_int32), ("r", C.c_int32), ("dx", C.c_double), ("dy", C.c_double),
                 ("eps_r", C.c_void_p), ("sigma", C.c_void_p), ("q", C.c_int32), ("fmax", C.c_double),
-                ("dt_target", C.c_double), ("cg_tol", C.c_double)]
+                ("dt_target", C.c_double), ("cg_tol", C.c_double), ("literal", C.c_int32)]
 
 
 class RomBuilt(C.Structure):
@@ -134,18 +134,19 @@ def exported_symbols():
     return sorted(names)
 
 
-def build_rom(bx, by, r, dx, dy, eps_r, sigma, q, fmax, dt_target=None, cg_tol=0.0):
+def build_rom(bx, by, r, dx, dy, eps_r, sigma, q, fmax, dt_target=None, cg_tol=0.0, literal=False):
     """GPU-side ROM construction (fdtdrom_build.h, NEXT-3): fine assembly, collapse onto coarse-edge
     ports, SPRIM(q) with CG-solved shifts, congruence, optional CFL clip at dt_target.  Returns the
     model dict fdtd_add_rom consumes (R11, R22, F11, K, L, q1, q2, bx, by, r, n_clipped, literal,
     natural_dt_limit) plus the builder's diagnostics under "gpu_build"."""
     eps = _f64(eps_r).reshape(by * r, bx * r)
     sig = _f64(sigma).reshape(by * r, bx * r)
-    q1w, q2w, nY = (q + 1) // 2, q // 2, 2 * bx + 2 * by
+    nY = (2 * bx + 2 * by) * (r if literal else 1)
+    q1w, q2w = (q + 1) // 2 + (nY if literal else 0), q // 2
     R11, F11 = np.zeros((q1w, q1w)), np.zeros((q1w, q1w))
     R22, K, L = np.zeros((q2w, q2w)), np.zeros((q1w, q2w)), np.zeros((q1w, nY))
     spec = RomSpec(int(bx), int(by), int(r), float(dx), float(dy), eps.ctypes.data, sig.ctypes.data, int(q),
-                   float(fmax), float(dt_target or 0.0), float(cg_tol))
+                   float(fmax), float(dt_target or 0.0), float(cg_tol), int(bool(literal)))
     out = RomBuilt(R11.ctypes.data, R22.ctypes.data, F11.ctypes.data, K.ctypes.data, L.ctypes.data)
     st = lib().fdtd_rom_build(C.byref(spec), C.byref(out))
     if st:
@@ -154,7 +155,7 @@ def build_rom(bx, by, r, dx, dy, eps_r, sigma, q, fmax, dt_target=None, cg_tol=0
     unpack = lambda a, m, n: np.ascontiguousarray(a.ravel()[: m * n].reshape(m, n))
     return dict(bx=int(bx), by=int(by), r=int(r), q1=q1, q2=q2, R11=unpack(R11, q1, q1), R22=unpack(R22, q2, q2),
                 F11=unpack(F11, q1, q1), K=unpack(K, q1, q2), L=unpack(L, q1, nY), n_clipped=int(out.n_clipped),
-                literal=False, natural_dt_limit=float(out.natural_dt_limit),
+                literal=bool(literal), natural_dt_limit=float(out.natural_dt_limit),
                 gpu_build=dict(krylov_vectors=out.krylov_vectors, cg_iterations_max=out.cg_iterations_max,
                                jacobi_sweeps_max=out.jacobi_sweeps_max, ms_total=out.ms_total,
                                ms_solve=out.ms_solve, ms_orth=out.ms_orth, ms_svd=out.ms_svd))

@@ -123,3 +123,29 @@ def test_gpu_build_errors():
         build_rom(2, 2, 2, DX, DY, -fe, fs, 8, 30e9)
     with pytest.raises(FDTDError):
         build_rom(2, 2, 2, DX, DY, fe, fs, 1, 30e9)
+
+
+def test_gpu_build_literal_ports_matches_romgen():
+    """NEXT-1 models built on the GPU: the paper-literal nP-port basis ([port directions | SPRIM
+    directions] in order).  Same invariants as the collapsed form, L~ of size q1 x nP, and the
+    embedded response (oracle, literal coupling) to 1e-9."""
+    import oracle as O
+    bx, by, r, q = 3, 3, 3, 16
+    fe, fs = sc.uniform_fill(bx, by, r, 6, 1, 4, 0, 0.05)
+    mc = rg.build_rom(bx, by, r, DX, DY, fe, fs, q, 30e9, literal=True)
+    mg = build_rom(bx, by, r, DX, DY, fe, fs, q, 30e9, literal=True)
+    nP = 2 * (bx + by) * r
+    assert mg["literal"] and mg["L"].shape == (mg["q1"], nP) and mg["q1"] == nP + q // 2
+    _compare(mg, mc, 1e-8)
+    nx = ny = 30
+    rng = np.random.default_rng(3)
+    eps, sig = rng.uniform(1, 3, (ny, nx)), rng.uniform(0, 0.02, (ny, nx))
+    dt = 0.95 * min(rg.fine_cfl_limit(rg.fine_system(bx, by, r, DX, DY, fe, fs)), sc.cfl_limit(DX, DY))
+    out = []
+    for m in (mc, mg):
+        o = O.OracleSim(nx, ny, DX, DY, dt, eps, sig)
+        o.add_rom(m, 13, 13)
+        o.set_source(6, 6, sc.gaussian_samples(250, dt, 30e9, True))
+        o.set_probes(np.array([[22, 22], [16, 10]], np.int32))
+        out.append(o.step(250)[0])
+    assert rel(out[1], out[0]) <= 1e-9
