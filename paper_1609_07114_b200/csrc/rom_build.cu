@@ -1,18 +1,19 @@
 // GPU-side ROM construction, declared in include/fdtdrom_build.h.
 //
 // Steps (PAPER.md lines): fine assembly of the refined block with the exact collapse onto
-// coarse-edge ports (Sec. II, eq:equalE, R9) -> SPRIM block Arnoldi
-// (L393-400, R10) with the shifted systems solved by Jacobi-preconditioned CG on the
-// E-node Schur complement -> one-sided Jacobi SVD of the E and H rows -> congruence (eq:R11_tilde
-// .. eq:K_tilde, L431-447) -> optional CFL extension (eq:CFLgeneralized L741-745, R11).
+// coarse-edge ports (Sec. II, eq:equalE, R9; or the literal nP-port
+// set of NEXT-1) -> SPRIM block Arnoldi (L393-400, R10) with the shifted systems solved
+// in H form (multigrid-preconditioned CG on the cell stencil) -> the E and H rows orthonormalised
+// in Krylov order -> congruence (eq:R11_tilde .. eq:K_tilde, L431-447) -> optional CFL extension
+// (eq:CFLgeneralized L741-745, R11) through one-sided Jacobi SVDs.
 //
-// Design: every O(n) or larger step runs in kernels of this file; the host
-// only sequences them and takes the scalar decisions of the Gram-Schmidt deflation and the Jacobi
-// convergence test.  The fine operator is never formed as a matrix product: the Schur complement
-// S = diag(2 F11 + s0 R11) + K (s0 R22)^{-1} K^T is applied as K^T, a diagonal and K (CSR of the
-// collapsed K with r entries on port rows and 2 on interior rows; K^T with 4 entries per cell).
-// The CG runs one CTA per right-hand side for the whole iteration (vectors stay in L2), the
-// Jacobi SVD one CTA per column pair and round, the dense products in a tiled fp64 kernel.
+// Design: every O(n) or larger step runs in kernels of this file; the host only
+// sequences them and takes the scalar decisions (Gram-Schmidt deflation, Jacobi convergence).  The
+// fine operator is never formed as a matrix product: K is a CSR of the collapsed curl (r entries
+// on port rows, 2 on interior rows; K^T 4 per cell), and the H-form Schur complement
+// s0 R22 + K^T D^-1 K is a 5-point cell stencil plus one rank-1 block per port.  The CG runs one
+// CTA per right-hand side for the whole iteration, the Jacobi SVD one CTA per column pair (a whole
+// sweep per cooperative launch), the dense products in a tiled fp64 kernel.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
