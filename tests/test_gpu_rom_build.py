@@ -45,9 +45,14 @@ def _compare(mg, mc, tol):
     return errs
 
 
-@pytest.mark.parametrize("case", ["uniform", "lossy_random", "inclusion", "r1", "strip"])
+@pytest.mark.parametrize("case", ["uniform", "lossy_random", "inclusion", "r1", "strip", "aniso_odd_q"])
 def test_gpu_build_matches_romgen_invariants(case):
-    if case == "uniform":
+    dx, dy = DX, DY
+    if case == "aniso_odd_q":  # dx != dy (a swapped fdx / fdy shows) and an odd order
+        bx, by, r, q = 4, 3, 3, 23
+        dx, dy = 1e-3, 0.6e-3
+        fe, fs = sc.uniform_fill(bx, by, r, 9, 1, 5, 0, 0.1)
+    elif case == "uniform":
         bx, by, r, q = 3, 2, 3, 20
         fe, fs = sc.uniform_fill(bx, by, r, 1, 1, 4, 0, 0.05)
     elif case == "r1":  # no refinement: every port is one fine edge
@@ -65,8 +70,8 @@ def test_gpu_build_matches_romgen_invariants(case):
         bx = by = 6
         r, q = 4, 48
         fe, fs = sc.inclusion_fill(6, 4, 3)
-    mc = rg.build_rom(bx, by, r, DX, DY, fe, fs, q, 30e9)
-    mg = build_rom(bx, by, r, DX, DY, fe, fs, q, 30e9)
+    mc = rg.build_rom(bx, by, r, dx, dy, fe, fs, q, 30e9)
+    mg = build_rom(bx, by, r, dx, dy, fe, fs, q, 30e9)
     _compare(mg, mc, 1e-8)
     assert abs(mg["natural_dt_limit"] / mc["natural_dt_limit"] - 1) < 1e-8
     ok, _, _ = rg.check_passivity(mg, 0.95 * mc["fine_dt_limit"])
