@@ -8,9 +8,9 @@ import sys
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "tools"))
+sys.path.insert(0, os.path.join(ROOT, "tests", "replays"))
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 import oracle as O  # noqa: E402
 import rods4_replay as r4  # noqa: E402

@@ -21,7 +21,7 @@ import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
@@ -29,29 +29,8 @@ import numpy as np  # noqa: E402
 from inputs import romgen as rg  # noqa: E402
 from inputs import scene as sc  # noqa: E402
 
-NX, NY, DX = 66, 40, 1e-3
-BOX = (39, 16, 8, 8)   # i0, j0, bx, by (coarse cells)
-R = 6
-RODS = [(41e-3, 22e-3), (41e-3, 18e-3), (45e-3, 22e-3), (45e-3, 18e-3)]
-ROD_R = 1e-3
-PML = 15
-SRC_X, PROBE_X = 17, 19
-FMAX = 30e9
-
-
-def fine_fill(rods):
-    i0, j0, bx, by = BOX
-    N = bx * R
-    fdx = DX / R
-    eps = np.ones((N, N))
-    sig = np.zeros((N, N))
-    if rods:
-        jj, ii = np.mgrid[0:N, 0:N]
-        x = (i0 + (ii + 0.5) / R) * DX
-        y = (j0 + (jj + 0.5) / R) * DX
-        for cx, cy in RODS:
-            sig[(x - cx) ** 2 + (y - cy) ** 2 <= ROD_R ** 2] = 5.8e7
-    return eps, sig, fdx
+from inputs.rods4 import (BOX, DX, FMAX, NX, NY, PML, PROBE_X, R, ROD_R, RODS, SRC_X,  # noqa: E402,F401
+                          fine_fill, scene)
 
 
 def build_model(rods, reduced, q):
@@ -70,16 +49,6 @@ def build_model(rods, reduced, q):
     if reduced:
         m = rg.extend_cfl(m, 3.0 * dtf)  # "extended by 3 times" (L945)
     return m, dtf
-
-
-def scene(model, dt, steps):
-    eps = np.ones((NY, NX))
-    sig = np.zeros((NY, NX))
-    probes = np.array([[PROBE_X, j] for j in range(NY)], dtype=np.int32)
-    return sc.Scene(name="rods4", nx=NX, ny=NY, dx=DX, dy=DX, dt=dt, eps_r=eps, sigma=sig, precision=64,
-                    steps=steps, source=(SRC_X, 0), samples=sc.gaussian_samples(steps, dt, FMAX, derivative=False),
-                    probes=probes, models=[model], placements=np.array([[0, BOX[0], BOX[1]]], dtype=np.int32),
-                    meta=dict(pml=(PML, 3, 1e-8), source_rows=(0, NY)))
 
 
 def main():

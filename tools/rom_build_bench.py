@@ -48,8 +48,7 @@ def cases(which):
         out.append(("cfg5 largest model (31x31, r 10, q 256, clip 1 dt_f)", 31, 31, 10, fe, fs, 256, 10e9, None,
                     DX))
     if "rods4" in which:  # Sec. VI-C: 8 x 8 box, r = 6, copper rods, q 1920, 3x CFL extension
-        sys.path.insert(0, os.path.join(ROOT, "tools"))
-        import rods4_replay as r4
+        from inputs import rods4 as r4
         fe, fs, _ = r4.fine_fill(True)
         out.append(("rods4 box (8x8, r 6, four copper rods, q 1920, clip 3 dt_f)", r4.BOX[2], r4.BOX[3], r4.R, fe, fs,
                     1920, r4.FMAX, 3.0, r4.DX))
@@ -59,10 +58,9 @@ def cases(which):
 def embedded_rods4(mg, mc, dtf3, steps=3000):
     """Probe series (line probe at x = 19 mm) of the four-rod waveguide with the GPU-built and the
     CPU-built model embedded (fp64 GPU runs, same scene): their relative L2 difference."""
-    sys.path.insert(0, os.path.join(ROOT, "tools"))
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import rods4_replay as r4
     from helpers import gpu_from_scene
+    from inputs import rods4 as r4
     dt = 0.99 * min(sc.cfl_limit(r4.DX, r4.DX), dtf3)
     out = []
     for m in (mc, mg):
