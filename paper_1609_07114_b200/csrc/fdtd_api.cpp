@@ -158,6 +158,9 @@ struct fdtd_ctx {
   nccl_comm comm = nullptr;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+  // row slabs: the slab-edge row chunks run on a side stream beside the interior chunks
+  cudaStream_t edge_stream = nullptr;
+  cudaEvent_t ev_edge_go = nullptr, ev_edge = nullptr;
   std::vector<void*> owned;  // every device allocation
 };
 
@@ -455,11 +458,22 @@ fdtd_status enqueue_pass(fdtd_ctx* c, int q, cudaStream_t s, int K) {
   while (hi > lo && std::min((hi) * c->chunk, c->rows) + K > c->rows) --hi;
   const bool split = c->d.nranks > 1 && hi > lo;
   const bool nccl_overlap = split && c->comm && c->comm_stream;
-  auto sweep = [&](int b, int n) {
+  auto sweep_on = [&](int b, int n, cudaStream_t st) {
     if (n <= 0) return;
-    if (c->prec == 64) fdtd::launch_sweep<double>(sweep_params<double>(c, q), K, c->warps, s, b, n);
-    else fdtd::launch_sweep<float>(sweep_params<float>(c, q), K, c->warps, s, b, n);
+    if (c->prec == 64) fdtd::launch_sweep<double>(sweep_params<double>(c, q), K, c->warps, st, b, n);
+    else fdtd::launch_sweep<float>(sweep_params<float>(c, q), K, c->warps, st, b, n);
     c->launches += 1;
+  };
+  auto sweep = [&](int b, int n) { sweep_on(b, n, s); };
+  // the chunk rows next to the slab edges (one or two chunk rows: a fraction of a wave) run on a
+  // side stream once their ghost rows are in, beside the interior launch, whose tail they fill
+  // instead of idling the GPU after it
+  auto edges_beside = [&](cudaEvent_t ready) -> fdtd_status {
+    CK(cudaStreamWaitEvent(c->edge_stream, ready, 0));
+    sweep_on(0, lo, c->edge_stream);
+    sweep_on(hi, nch - hi, c->edge_stream);
+    CK(cudaEventRecord(c->ev_edge, c->edge_stream));
+    return FDTD_OK;
   };
   cudaEvent_t e[3];
   if (prof) {
@@ -473,16 +487,30 @@ fdtd_status enqueue_pass(fdtd_ctx* c, int q, cudaStream_t s, int K) {
     if (st != FDTD_OK) return st;
     CK(cudaEventRecord(c->ev_halo, c->comm_stream));
     sweep(lo, hi - lo);  // interior chunks: no ghost rows needed
-    CK(cudaStreamWaitEvent(s, c->ev_halo, 0));
-    sweep(0, lo);
-    sweep(hi, nch - hi);
+    if (c->edge_stream) {
+      fdtd_status st2 = edges_beside(c->ev_halo);
+      if (st2 != FDTD_OK) return st2;
+      CK(cudaStreamWaitEvent(s, c->ev_edge, 0));
+    } else {
+      CK(cudaStreamWaitEvent(s, c->ev_halo, 0));
+      sweep(0, lo);
+      sweep(hi, nch - hi);
+    }
   } else {
     fdtd_status st = halo_exchange(c, q, s, K);
     if (st != FDTD_OK) return st;
     if (split) {  // local groups: same split launches (their halo copies precede on this stream)
-      sweep(lo, hi - lo);
-      sweep(0, lo);
-      sweep(hi, nch - hi);
+      if (c->edge_stream) {
+        CK(cudaEventRecord(c->ev_edge_go, s));
+        sweep(lo, hi - lo);
+        fdtd_status st2 = edges_beside(c->ev_edge_go);
+        if (st2 != FDTD_OK) return st2;
+        CK(cudaStreamWaitEvent(s, c->ev_edge, 0));
+      } else {
+        sweep(lo, hi - lo);
+        sweep(0, lo);
+        sweep(hi, nch - hi);
+      }
     } else {
       sweep(0, nch);
     }
@@ -937,6 +965,12 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
       return FDTD_E_CUDA;
     }
   }
+  if (nranks > 1 && (cudaStreamCreateWithFlags(&c->edge_stream, cudaStreamNonBlocking) != cudaSuccess ||
+                     cudaEventCreateWithFlags(&c->ev_edge_go, cudaEventDisableTiming) != cudaSuccess ||
+                     cudaEventCreateWithFlags(&c->ev_edge, cudaEventDisableTiming) != cudaSuccess)) {
+    fdtd_destroy(c);
+    return FDTD_E_CUDA;
+  }
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) { fdtd_destroy(c); return FDTD_E_CUDA; }
   *out = c;
   return FDTD_OK;
@@ -946,6 +980,8 @@ fdtd_status fdtd_set_tuning(fdtd_ctx* c, int32_t rows_per_cta, int32_t warps_per
   if (!c) return FDTD_E_ARG;
   if (rows_per_cta < 0 || warps_per_cta < 0 || warps_per_cta > 8) return fail(c, FDTD_E_ARG, "bad tuning");
   // rows per CTA: long chunks amortise the K-row prologue, short ones keep enough CTAs for ~8 waves
+  // rows per CTA: long enough that the 2K - 1 recomputed stage rows at a chunk start stay a few per
+  // cent, short enough for several waves of CTAs (the last wave's tail is paid once per slab)
   c->chunk = rows_per_cta ? rows_per_cta : (c->rows >= 16384 ? 256 : c->rows >= 2048 ? 64 : 32);
   c->warps = warps_per_cta ? warps_per_cta : 4;
   if (!rows_per_cta)
@@ -1702,6 +1738,9 @@ void fdtd_destroy(fdtd_ctx* c) {
   for (auto e : c->ev) cudaEventDestroy(e);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  if (c->edge_stream) cudaStreamDestroy(c->edge_stream);
+  if (c->ev_edge_go) cudaEventDestroy(c->ev_edge_go);
+  if (c->ev_edge) cudaEventDestroy(c->ev_edge);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->ev_halo) cudaEventDestroy(c->ev_halo);
