@@ -158,6 +158,7 @@ struct fdtd_ctx {
   nccl_comm comm = nullptr;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+  double* d_level2 = nullptr;  // [KMAX][FIN_GRID]
   // row slabs: the slab-edge row chunks run on a side stream beside the interior chunks
   cudaStream_t edge_stream = nullptr;
   cudaEvent_t ev_edge_go = nullptr, ev_edge = nullptr;
@@ -294,14 +295,9 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q, int K) {
   p.src_row_end = src_here ? (int)lrow(c, sj1) : -1;
   p.src_col = src_here ? c->src_i : -1;
   p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
-  p.sweep_partials = c->d_partials;  // exactly the partials the matching sweep launches wrote
-  p.n_sweep_partials = (int64_t)sweep_gx(c, K) * ((c->rows + c->chunk - 1) / c->chunk) +
-                       (c->pml_w > 0 ? fdtd::pml_ctas(c->rows, PML_CHUNK) : 0);  // + the CPML band CTAs
-  p.pstride = c->n_partials;
   p.rom_partials = c->d_rom_partials;
   p.level1 = c->d_level1;
-  p.energy_ring = c->d_energy_ring;
-  p.step = c->d_step; p.done = c->d_done;
+  p.step = c->d_step;
   p.n_batch = c->inst_model.empty() ? 0 : (int)(c->batch_tab.size() / 5);
   p.batch_tab = c->d_batch_tab;
   p.block = c->post_threads;
@@ -317,6 +313,21 @@ inline char* psi_base(const fdtd_ctx* c, int e, int q, int side) {
 }
 template <typename T>
 T* psi_buf(const fdtd_ctx* c, int e, int q) { return (T*)psi_base(c, e, q, 0); }
+
+fdtd::FinParams fin_params(fdtd_ctx* c, int K) {
+  fdtd::FinParams f{};
+  f.sweep_partials = c->d_partials;  // exactly the partials the matching sweep / band launches wrote
+  f.n_sweep_partials = (int64_t)sweep_gx(c, K) * ((c->rows + c->chunk - 1) / c->chunk) +
+                       (c->pml_w > 0 ? fdtd::pml_ctas(c->rows, PML_CHUNK) : 0);  // + the CPML band CTAs
+  f.pstride = c->n_partials;
+  f.rom_level1 = c->d_level1;
+  f.n_rom = c->inst_model.empty() ? 0 : (int)(c->batch_tab.size() / 5);
+  f.level2 = c->d_level2;
+  f.energy_ring = c->d_energy_ring; f.cap = c->cap;
+  f.step = c->d_step; f.done = c->d_done;
+  f.K = K; f.energy = c->energy_on;
+  return f;
+}
 
 template <typename T>
 fdtd::PmlParams<T> pml_params(fdtd_ctx* c, int q) {
@@ -475,6 +486,12 @@ fdtd_status enqueue_pass(fdtd_ctx* c, int q, cudaStream_t s, int K) {
     CK(cudaEventRecord(c->ev_edge, c->edge_stream));
     return FDTD_OK;
   };
+  const bool has_fix = !c->inst_model.empty();
+  auto post = [&](cudaStream_t st) {
+    if (c->prec == 64) fdtd::launch_post<double>(post_params<double>(c, q, K), K, c->energy_on, st);
+    else fdtd::launch_post<float>(post_params<float>(c, q, K), K, c->energy_on, st);
+    c->launches += 1;
+  };
   cudaEvent_t e[3];
   if (prof) {
     for (auto& x : e) x = next_event(c);
@@ -529,10 +546,10 @@ fdtd_status enqueue_pass(fdtd_ctx* c, int q, cudaStream_t s, int K) {
     c->launches += 1;
   }
   if (prof) CK(cudaEventRecord(e[1], s));
-  if (c->prec == 64) fdtd::launch_post<double>(post_params<double>(c, q, K), K, c->energy_on, s);
-  else fdtd::launch_post<float>(post_params<float>(c, q, K), K, c->energy_on, s);
-  if (prof) CK(cudaEventRecord(e[2], s));
+  if (has_fix) post(s);
+  fdtd::launch_finalize(fin_params(c, K), s);  // energy of the K steps, step counter
   c->launches += 1;
+  if (prof) CK(cudaEventRecord(e[2], s));
   return FDTD_OK;
 }
 
@@ -947,6 +964,7 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
   c->d_done = (unsigned*)dalloc(c, sizeof(unsigned) * 4);
   c->d_energy_ring = (double*)dalloc(c, c->cap * sizeof(double));
   c->d_level1 = (double*)dalloc(c, KMAX * sizeof(double));
+  c->d_level2 = (double*)dalloc(c, (size_t)KMAX * fdtd::FIN_GRID * sizeof(double));
   c->k_want = c->V;  // deepest pass the vector width allows (4 in fp32, 2 in fp64)
   if (const char* e = getenv("FDTD_K")) c->k_want = std::max(1, atoi(e));
   if (!c->d_step || !c->d_done || !c->d_energy_ring) { fdtd_destroy(c); return FDTD_E_NOMEM; }

@@ -973,7 +973,6 @@ __global__ void __launch_bounds__(512) postk_kernel(const PostParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[32];
   __shared__ double zsum[64];
-  __shared__ bool last;
   T* sv = reinterpret_cast<T*>(smem_raw);
   const int b = blockIdx.x;
   const int64_t step = *p.step;
@@ -987,21 +986,38 @@ __global__ void __launch_bounds__(512) postk_kernel(const PostParams<T> p) {
     }
   }
   if (b < p.n_batch) fixup_batch<T, K, ENERGY>(p, b, sv, g, step, zsum);
-  if (ENERGY) {
-    // level 1 (every CTA, fixed slice): sweep partials [b*per, (b+1)*per) + this batch's ROM energies
-    const int64_t per = (p.n_sweep_partials + gridDim.x - 1) / gridDim.x;
-    const int64_t k0 = b * per, k1 = min(p.n_sweep_partials, k0 + per);
-    __syncthreads();  // rom_partials of this batch written (fixup_batch ends with barriers)
+  if (ENERGY && b < p.n_batch) {  // this batch's ROM + zone energies, one value per step (level 1)
+    __syncthreads();              // rom_partials of this batch written (fixup_batch ends with barriers)
+    const int first = p.batch_tab[5 * b + 1], nb = p.batch_tab[5 * b + 2];
 #pragma unroll 1
     for (int s = 0; s < K; ++s) {
       double v = 0.0;
-      for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) v += __ldcg(p.sweep_partials + s * p.pstride + k);
-      if (b < p.n_batch) {
-        const int first = p.batch_tab[5 * b + 1], nb = p.batch_tab[5 * b + 2];
-        for (int k = threadIdx.x; k < nb; k += blockDim.x) v += p.rom_partials[(int64_t)s * p.n_inst + first + k];
-      }
+      for (int k = threadIdx.x; k < nb; k += blockDim.x) v += p.rom_partials[(int64_t)s * p.n_inst + first + k];
       const double tot = block_sum(v, red);
-      if (threadIdx.x == 0) p.level1[(int64_t)s * gridDim.x + b] = tot;
+      if (threadIdx.x == 0) p.level1[(int64_t)s * p.n_batch + b] = tot;
+    }
+  }
+}
+
+// End of a pass: W^{n+s} = fixed-order two-level sum of the sweep / band partials and the fix-up
+// batches' values (deterministic), and the device step counter.
+__global__ void __launch_bounds__(256) finalize_kernel(const FinParams p) {
+  __shared__ double red[32];
+  __shared__ bool last;
+  const int b = blockIdx.x;
+  const int64_t step = *p.step;
+  if (p.energy) {
+    const int64_t per = (p.n_sweep_partials + gridDim.x - 1) / gridDim.x;
+    const int64_t k0 = b * per, k1 = min(p.n_sweep_partials, k0 + per);
+    const int perr = (p.n_rom + gridDim.x - 1) / gridDim.x;
+    const int r0 = b * perr, r1 = min(p.n_rom, r0 + perr);
+#pragma unroll 1
+    for (int s = 0; s < p.K; ++s) {
+      double v = 0.0;
+      for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) v += __ldcg(p.sweep_partials + s * p.pstride + k);
+      for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) v += __ldcg(p.rom_level1 + (int64_t)s * p.n_rom + k);
+      const double tot = block_sum(v, red);
+      if (threadIdx.x == 0) p.level2[(int64_t)s * gridDim.x + b] = tot;
     }
   }
   __syncthreads();
@@ -1013,18 +1029,18 @@ __global__ void __launch_bounds__(512) postk_kernel(const PostParams<T> p) {
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (ENERGY) {  // level 2: fixed-order sum of the per-CTA values (deterministic)
+  if (p.energy) {
 #pragma unroll 1
-    for (int s = 0; s < K; ++s) {
+    for (int s = 0; s < p.K; ++s) {
       double v = 0.0;
-      for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) v += __ldcg(p.level1 + (int64_t)s * gridDim.x + k);
+      for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) v += __ldcg(p.level2 + (int64_t)s * gridDim.x + k);
       const double tot = block_sum(v, red);
       if (threadIdx.x == 0) p.energy_ring[(step + s) % p.cap] = tot;
     }
   }
   if (threadIdx.x == 0) {
     *p.done = 0u;
-    *p.step = step + K;
+    *p.step = step + p.K;
   }
 }
 
@@ -1334,7 +1350,7 @@ size_t post_smem_bytes(size_t es, int nvec, int batch, int region_stride) {
 template <typename T, int K>
 void postk_launch(const PostParams<T>& p, bool energy, cudaStream_t s) {
   const size_t smem = p.smem_bytes;
-  const int grid = p.n_batch > 0 ? p.n_batch : 1;
+  const int grid = p.n_batch;
   if (energy) {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(postk_kernel<T, K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1346,8 +1362,11 @@ void postk_launch(const PostParams<T>& p, bool energy, cudaStream_t s) {
   }
 }
 
+void launch_finalize(const FinParams& p, cudaStream_t s) { finalize_kernel<<<p.energy ? FIN_GRID : 1, 256, 0, s>>>(p); }
+
 template <typename T>
 void launch_post(const PostParams<T>& p, int K, bool energy, cudaStream_t s) {
+  if (p.n_batch <= 0) return;  // no ROM instances: nothing to fix up
   if (K == 1) postk_launch<T, 1>(p, energy, s);
   else if (K == 2) postk_launch<T, 2>(p, energy, s);
   else if constexpr (sizeof(T) == 4) postk_launch<T, 4>(p, energy, s);

@@ -80,14 +80,26 @@ struct PostParams {
   T* probe_ring; int64_t cap;
   T chx, chy, idx, idy, wxy, wh;
   int src_row, src_row_end; int64_t src_col; const double* src_samples; int64_t src_n, src_t0;
-  const double* sweep_partials; int64_t n_sweep_partials, pstride;  // [s * pstride + cta]
   double* rom_partials;            // [s * n_inst + instance]: ROM + zone energy of step n+s
-  double* level1;                  // [s * gridDim.x + cta]
-  double* energy_ring;             // W^n per step (fp64 ring of cap entries)
-  int64_t* step; unsigned int* done;
+  double* level1;                  // [s * n_batch + batch]: the batch's sum of rom_partials
+  const int64_t* step;             // step counter (value n during the pass; finalize advances it)
   int block;         // threads per CTA
   size_t smem_bytes; // dynamic shared memory of the launch (max over batches)
 };
+
+// End of a pass (finalize_kernel, after the sweep, the CPML bands and the fix-up): W^{n+s} as a
+// fixed-order two-level sum of the sweep / band partials and the fix-up batches' values
+// (deterministic), and the device step counter.  FIN_GRID CTAs (one when energy is off).
+constexpr int FIN_GRID = 64;
+struct FinParams {
+  const double* sweep_partials; int64_t n_sweep_partials, pstride;  // [s * pstride + cta]
+  const double* rom_level1; int n_rom;                              // [s * n_rom + batch]
+  double* level2;                  // [s * FIN_GRID + cta]
+  double* energy_ring; int64_t cap;
+  int64_t* step; unsigned int* done;
+  int K; bool energy;
+};
+void launch_finalize(const FinParams& p, cudaStream_t s);
 
 // CPML band fix-up (NEXT-2): the sweep advances the two x-end layers with the plain Yee update; per
 // row chunk and side this kernel recomputes the K steps on the band [layer + Kz + K + 2 columns] x
