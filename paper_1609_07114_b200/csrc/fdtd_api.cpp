@@ -771,8 +771,17 @@ fdtd_status apply_passes(fdtd_ctx* c, int k) {
   // (~110 KB: two fix-up CTAs per SM), so small models are batched 8 at a time and the largest
   // still fits; the launch uses the largest batch footprint.
   {
+    // up to 8 instances per CTA; a row slab with few instances uses smaller batches so that the
+    // fix-up's CTAs still fill one wave (it is latency-bound)
     const char* env = getenv("FDTD_ROM_BATCH");
-    const int Bmax = env ? std::max(1, std::min(64, atoi(env))) : 8;
+    int Bauto = 8;
+    if (c->d.nranks > 1) {
+      int nsm = 148, dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      while (Bauto > 1 && (int64_t)c->inst_model.size() <= (int64_t)(Bauto / 2) * 2 * nsm) Bauto /= 2;
+    }
+    const int Bmax = env ? std::max(1, std::min(64, atoi(env))) : Bauto;
     const size_t budget = 110 * 1024;
     struct Shape { int B, stride; size_t per; };
     std::vector<Shape> shp;
@@ -1000,7 +1009,11 @@ fdtd_status fdtd_set_tuning(fdtd_ctx* c, int32_t rows_per_cta, int32_t warps_per
   // rows per CTA: long chunks amortise the K-row prologue, short ones keep enough CTAs for ~8 waves
   // rows per CTA: long enough that the 2K - 1 recomputed stage rows at a chunk start stay a few per
   // cent, short enough for several waves of CTAs (the last wave's tail is paid once per slab)
-  c->chunk = rows_per_cta ? rows_per_cta : (c->rows >= 16384 ? 256 : c->rows >= 2048 ? 64 : 32);
+  // rows per CTA: the 2K - 1 stage rows recomputed at a chunk start against the tail of the last
+  // wave; a row slab of a multi-GPU run (a few thousand rows) does better with 128 than 64
+  const bool slab = c->d.nranks > 1;
+  c->chunk = rows_per_cta ? rows_per_cta
+                          : (c->rows >= 16384 ? 256 : c->rows >= 2048 ? (slab && c->rows < 8192 ? 128 : 64) : 32);
   c->warps = warps_per_cta ? warps_per_cta : 4;
   if (!rows_per_cta)
     if (const char* e = getenv("FDTD_CHUNK")) c->chunk = std::max(1, atoi(e));  // tuning experiments
