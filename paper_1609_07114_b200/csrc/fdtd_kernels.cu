@@ -1,18 +1,16 @@
-// CUDA kernels of the hot path (sm_100a).  See DESIGN.md for the derivations.
-//
-//  K1 sweep_kernel : one pass over the grid per time step.  For every owned cell row it
-//                    computes Hz^{n+1/2} (eq:updateH), adds the soft
-//                    source, then the E^{n+1} of that row's x- and y-directed edges
-//                    (eq:updateEx L209-214 and its Ey analogue L223) from the new Hz of
-//                    this row and the row below (kept in registers).  16-byte vector
-//                    loads, one warp per 32x16-byte column strip, rows walked upward by
-//                    each CTA over a chunk; ping-pong buffers so no CTA ever reads a value
-//                    another CTA writes in the same launch.  Edge masks (PEC, ROM holes,
-//                    ROM interfaces) are encoded in the coefficients (ca = 1, cb = 0).
-//  K3 post_kernel  : per ROM instance (one CTA each) the factored eq:connExplicit update
-//                    (gather h, y; reduced matvecs; Schur solve; scatter y^{n+1});
-//                    one CTA records the probes; the last CTA to finish reduces the
-//                    energy partials in a fixed order and advances the step counter.
+// Kernels of the hot path.  One pass advances K time steps:
+//  K1 sweepk_kernel  : the fused Yee sweep -- per stage-0 row, the K steps of the wavefront in
+//                      registers (H half-step eq:updateH L267-273, soft source, probes, storage-
+//                      function partials, E half-step eq:updateEx L209-214 and its Ey analogue
+//                      L223), packed fp32x2 arithmetic, a per-warp shared-memory ring of the rows'
+//                      edge coefficients, ping-pong buffers (no CTA reads a value another CTA
+//                      writes in the same launch).  Edge masks (PEC, ROM holes, interfaces) are
+//                      encoded in the coefficients (ca = 1, cb = 0).
+//  K3 postk_kernel   : per batch of ROM instances, the K steps recomputed on each instance's
+//                      region with the factored eq:connExplicit update between H and E (gather,
+//                      batched reduced GEMMs, Schur solve, scatter), written back on the zone.
+//  pml_kernel        : the CPML band fix-up on both x-ends (NEXT-2).
+//  finalize_kernel   : fixed-order energy sum of the pass and the device step counter.
 #include "fdtd_kernels.cuh"
 
 #include <climits>

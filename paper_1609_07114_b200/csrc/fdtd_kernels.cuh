@@ -54,8 +54,8 @@ struct RomModelDev {
 // Fix-up kernel: per ROM instance, the K steps of the pass are recomputed on
 // the region [i0-M, i0+bx+M) x [j0-M, j0+by+M) (M = Kz + K - 1) from the pass's input buffer,
 // with the ROM update (S4-S6, eq:connExplicit) between them; the zone cells (the ones the sweep
-// may have got wrong and whose energy it skipped) are written back.  Also: zone probes, the
-// deterministic energy finalisation and the device step counter.
+// may have got wrong and whose energy it skipped) are written back.  Also: zone probes and the
+// per-batch ROM + zone energies (finalize_kernel sums them with the sweep's).
 template <typename T>
 struct PostParams {
   int n_inst;
