@@ -846,14 +846,19 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   load_rom_state(p, m, first, nb, B, sv);
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  // Values go wrong from the region's border inwards one cell per step, so step s only updates the
+  // cone that is still exact: cells [s, Wr - s) x [s, Hr - s) (edges one further in across their
+  // normal); the zone, the ROM's gather cells and the write-back all lie inside the last cone.
 #pragma unroll 1
   for (int s = 0; s < K; ++s) {
     // ---- H half-step (+ source, + zone-cell energy of W^{n+s})
     for (int b = 0; b < nb; ++b) {
       const Geo q = geo(b);
       const int W1 = q.Wr + 1;
-      for (int t = tid; t < q.Hr * q.Wr; t += nt) {
-        const int u = t % q.Wr, v = t / q.Wr;
+      const int cw = q.Wr - 2 * s, ch = q.Hr - 2 * s;
+      for (int i = tid; i < cw * ch; i += nt) {
+        const int u = s + i % cw, v = s + i / cw;
+        const int t = v * q.Wr + u;
         const T h0 = q.H[t];
         const T hu = hupd(h0, q.EX[t + q.Wr], q.EX[t], q.EY[v * W1 + u + 1], q.EY[v * W1 + u], p.chy, p.chx);
         T h = q.MA[t] < T(0) ? h0 : hu;  // dead cells keep their Hz (as in yee_row)
@@ -919,14 +924,16 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     for (int b = 0; b < nb; ++b) {
       const Geo q = geo(b);
       const int W1 = q.Wr + 1;
-      for (int t = q.Wr + tid; t < q.Hr * q.Wr; t += nt) {  // Ex edge rows 1 .. Hr-1
+      const int cw = q.Wr - 2 * s, ch = q.Hr - 2 * s;
+      for (int i = tid; i < cw * (ch - 1); i += nt) {  // Ex edge rows s+1 .. Hr-s-1, columns s .. Wr-s-1
+        const int t = (s + 1 + i / cw) * q.Wr + s + i % cw;
         bool l;
         T a, ca, cb;
         edge_coef(q.MA[t - q.Wr], q.MS[t - q.Wr], q.MA[t], q.MS[t], p.idy, ca, cb, a, l);
         q.EX[t] = eupd(q.EX[t], ca, cb, q.H[t] - q.H[t - q.Wr]);
       }
-      for (int t = tid; t < q.Hr * (q.Wr - 1); t += nt) {  // Ey edge columns 1 .. Wr-1
-        const int u = t % (q.Wr - 1) + 1, v = t / (q.Wr - 1);
+      for (int i = tid; i < (cw - 1) * ch; i += nt) {  // Ey edge columns s+1 .. Wr-s-1, rows s .. Hr-s-1
+        const int u = s + 1 + i % (cw - 1), v = s + i / (cw - 1);
         const int c = v * q.Wr + u;
         bool l;
         T a, ca, cb;
