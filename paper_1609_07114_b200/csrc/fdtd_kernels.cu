@@ -648,11 +648,22 @@ __device__ __forceinline__ void bgemm_ipi(const T* __restrict__ A, int m, int ld
   const int G = B / IPI;
   for (int it = threadIdx.x; it < m * G; it += blockDim.x) {
     const int i = it % m, g = (it / m) * IPI;
-    T acc[IPI];
+    // two interleaved partial sums per output (even / odd c): half the dependent FMA chain
+    T acc[IPI], acc2[IPI];
 #pragma unroll
-    for (int u = 0; u < IPI; ++u) acc[u] = T(0);
-#pragma unroll 16
-    for (int c = 0; c < k; ++c) {
+    for (int u = 0; u < IPI; ++u) acc[u] = acc2[u] = T(0);
+    int c = 0;
+#pragma unroll 8
+    for (; c + 1 < k; c += 2) {
+      const T a = __ldg(A + (int64_t)c * lda + i), a2 = __ldg(A + (int64_t)(c + 1) * lda + i);
+      const T* x = X + c * B + g;
+#pragma unroll
+      for (int u = 0; u < IPI; ++u) {
+        acc[u] = fma_rn(a, x[u], acc[u]);
+        acc2[u] = fma_rn(a2, x[B + u], acc2[u]);
+      }
+    }
+    if (c < k) {
       const T a = __ldg(A + (int64_t)c * lda + i);
       const T* x = X + c * B + g;
 #pragma unroll
@@ -660,7 +671,7 @@ __device__ __forceinline__ void bgemm_ipi(const T* __restrict__ A, int m, int ld
     }
     T* y = Y + i * B + g;
 #pragma unroll
-    for (int u = 0; u < IPI; ++u) y[u] = fma_rn(alpha, acc[u], y[u]);
+    for (int u = 0; u < IPI; ++u) y[u] = fma_rn(alpha, acc[u] + acc2[u], y[u]);
   }
 }
 
@@ -725,10 +736,14 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first
   for (int it = tid; it < nY * nb; it += nt) {
     const int i = it % nY, b = it / nY;
     const T* Sk = p.Sk + p.Sk_off[first + b] + i;
-    T a = T(0);
-#pragma unroll 16
-    for (int c = 0; c < nY; ++c) a = fma_rn(__ldg(Sk + (int64_t)c * nY), v.st[c * B + b], a);
-    v.sU[i * B + b] = a;
+    T a[4] = {T(0), T(0), T(0), T(0)};  // four interleaved partial sums: a quarter of the FMA chain
+    int c = 0;
+#pragma unroll 4
+    for (; c + 3 < nY; c += 4)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = fma_rn(__ldg(Sk + (int64_t)(c + u) * nY), v.st[(c + u) * B + b], a[u]);
+    for (; c < nY; ++c) a[0] = fma_rn(__ldg(Sk + (int64_t)c * nY), v.st[c * B + b], a[0]);
+    v.sU[i * B + b] = (a[0] + a[1]) + (a[2] + a[3]);
   }
   for (int64_t k = tid; k < (int64_t)m2 * B; k += nt) {
     const int64_t r = k / B;
