@@ -871,8 +871,10 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       const Geo q = geo(b);
       const int W1 = q.Wr + 1;
       const int cw = q.Wr - 2 * s, ch = q.Hr - 2 * s;
-      for (int i = tid; i < cw * ch; i += nt) {
-        const int u = s + i % cw, v = s + i / cw;
+      const int du = nt % cw, dv = nt / cw;  // (u, v) advanced incrementally: no division per cell
+      int u = s + tid % cw, v = s + tid / cw;
+      for (int i = tid; i < cw * ch; i += nt, u += du, v += dv) {
+        if (u >= s + cw) { u -= cw; ++v; }
         const int t = v * q.Wr + u;
         const T h0 = q.H[t];
         const T hu = hupd(h0, q.EX[t + q.Wr], q.EX[t], q.EY[v * W1 + u + 1], q.EY[v * W1 + u], p.chy, p.chx);
@@ -940,15 +942,21 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       const Geo q = geo(b);
       const int W1 = q.Wr + 1;
       const int cw = q.Wr - 2 * s, ch = q.Hr - 2 * s;
-      for (int i = tid; i < cw * (ch - 1); i += nt) {  // Ex edge rows s+1 .. Hr-s-1, columns s .. Wr-s-1
-        const int t = (s + 1 + i / cw) * q.Wr + s + i % cw;
+      const int du = nt % cw, dv = nt / cw;
+      int eu = s + tid % cw, ev = s + 1 + tid / cw;
+      for (int i = tid; i < cw * (ch - 1); i += nt, eu += du, ev += dv) {  // Ex edge rows s+1 .. Hr-s-1,
+        if (eu >= s + cw) { eu -= cw; ++ev; }                              // columns s .. Wr-s-1
+        const int t = ev * q.Wr + eu;
         bool l;
         T a, ca, cb;
         edge_coef(q.MA[t - q.Wr], q.MS[t - q.Wr], q.MA[t], q.MS[t], p.idy, ca, cb, a, l);
         q.EX[t] = eupd(q.EX[t], ca, cb, q.H[t] - q.H[t - q.Wr]);
       }
-      for (int i = tid; i < (cw - 1) * ch; i += nt) {  // Ey edge columns s+1 .. Wr-s-1, rows s .. Hr-s-1
-        const int u = s + 1 + i % (cw - 1), v = s + i / (cw - 1);
+      const int dy_u = nt % (cw - 1), dy_v = nt / (cw - 1);
+      int yu = s + 1 + tid % (cw - 1), yv = s + tid / (cw - 1);
+      for (int i = tid; i < (cw - 1) * ch; i += nt, yu += dy_u, yv += dy_v) {  // Ey edge columns s+1 ..
+        if (yu >= s + cw) { yu -= cw - 1; ++yv; }                               // Wr-s-1, rows s .. Hr-s-1
+        const int u = yu, v = yv;
         const int c = v * q.Wr + u;
         bool l;
         T a, ca, cb;
