@@ -154,3 +154,13 @@ def test_gpu_build_literal_ports_matches_romgen():
         o.set_probes(np.array([[22, 22], [16, 10]], np.int32))
         out.append(o.step(250)[0])
     assert rel(out[1], out[0]) <= 1e-9
+
+
+def test_gpu_build_order_beyond_full_order():
+    """q larger than the full order: the Krylov space is exhausted and both builders return the
+    full order (q1 = nEc, q2 = nH), i.e. an exact model."""
+    fe, fs = sc.uniform_fill(2, 2, 2, 1, 1, 4, 0, 0.05)
+    mc = rg.build_rom(2, 2, 2, DX, DY, fe, fs, 200, 30e9)
+    mg = build_rom(2, 2, 2, DX, DY, fe, fs, 200, 30e9)
+    assert (mg["q1"], mg["q2"]) == (mc["q1"], mc["q2"]) == (32, 16)
+    _compare(mg, mc, 1e-8)
