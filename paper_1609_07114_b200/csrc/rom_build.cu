@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -538,6 +539,36 @@ __global__ void v_minus_wh_kernel(const double* W, int ldw, const double* h, int
   for (int j = 0; j < k; ++j) s += W[(size_t)j * ldw + i] * h[j];
   v[i] -= s;
 }
+// Two-level fixed-order versions for long vectors: slice partials, then one ordered sum.
+constexpr int RED_SLICE = 8192;  // rows per partial
+__global__ void __launch_bounds__(GV_NT) cnorm2_part_kernel(const double* c, const double* v, int n, double* part) {
+  __shared__ double red[32];
+  const int i0 = blockIdx.x * RED_SLICE, i1 = min(n, i0 + RED_SLICE);
+  double s = 0.0;
+  for (int i = i0 + threadIdx.x; i < i1; i += GV_NT) s += (c ? c[i] : 1.0) * v[i] * v[i];
+  s = block_sum<GV_NT>(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+// h_part[g * k + col] = slice g of W[:, col]^T (c o v)
+__global__ void __launch_bounds__(GV_NT) wtcv_part_kernel(const double* W, int ldw, const double* c, const double* v,
+                                                          int n, int k, double* part) {
+  __shared__ double red[32];
+  const int col = blockIdx.x, g = blockIdx.y;
+  const int i0 = g * RED_SLICE, i1 = min(n, i0 + RED_SLICE);
+  const double* w = W + (size_t)col * ldw;
+  double s = 0.0;
+  for (int i = i0 + threadIdx.x; i < i1; i += GV_NT) s += w[i] * (c ? c[i] : 1.0) * v[i];
+  s = block_sum<GV_NT>(s, red);
+  if (threadIdx.x == 0) part[(size_t)g * k + col] = s;
+}
+// out[j] = sum over g of part[g * m + j], in order (m outputs, ng slices)
+__global__ void sum_parts_kernel(const double* part, int ng, int m, double* out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double s = 0.0;
+  for (int g = 0; g < ng; ++g) s += part[(size_t)g * m + j];
+  out[j] = s;
+}
 __global__ void scale_copy_kernel(const double* v, double a, double* out, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = a * v[i];
@@ -636,23 +667,27 @@ __global__ void identity_kernel(double* V, int n) {
 constexpr int GT = 32;
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, const double* A, int lda, const double* w,
-                                                   const double* B, int ldb, double* C, int ldc) {
+                                                   const double* B, int ldb, double* C, int ldc, int kchunk) {
+  // blockIdx.z: a K range of kchunk (split-K); C then points at this split's partial matrix
   __shared__ double As[GT][GT + 1], Bs[GT][GT + 1];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // 16 x 16 threads, 2 x 2 outputs each
   const int i0 = blockIdx.x * GT, j0 = blockIdx.y * GT;
+  const int kb0 = blockIdx.z * kchunk, kb1 = min(K, kb0 + kchunk);
+  C += (size_t)blockIdx.z * ldc * N;
   double acc[2][2] = {{0, 0}, {0, 0}};
-  for (int k0 = 0; k0 < K; k0 += GT) {
+  for (int k0 = kb0; k0 < kb1; k0 += GT) {
     for (int t = threadIdx.x; t < GT * GT; t += 256) {
-      const int ii = t % GT, kk = t / GT;  // As[kk][ii] = op(A)(i0 + ii, k0 + kk) * w
+      // the index that is contiguous in memory runs fastest across threads (coalesced tiles)
+      const int ii = TA ? t / GT : t % GT, kk = TA ? t % GT : t / GT;  // As[kk][ii] = op(A)(i0+ii, k0+kk) w
       const int gi = i0 + ii, gk = k0 + kk;
       double av = 0.0;
-      if (gi < M && gk < K) av = TA ? A[(size_t)gi * lda + gk] : A[(size_t)gk * lda + gi];
-      if (w && gk < K) av *= w[gk];
+      if (gi < M && gk < kb1) av = TA ? A[(size_t)gi * lda + gk] : A[(size_t)gk * lda + gi];
+      if (w && gk < kb1) av *= w[gk];
       As[kk][ii] = av;
-      const int jj = t % GT, kb = t / GT;  // Bs[kb][jj] = op(B)(k0 + kb, j0 + jj)
+      const int jj = TB ? t % GT : t / GT, kb = TB ? t / GT : t % GT;  // Bs[kb][jj] = op(B)(k0+kb, j0+jj)
       const int gj = j0 + jj, gkb = k0 + kb;
       double bv = 0.0;
-      if (gj < N && gkb < K) bv = TB ? B[(size_t)gkb * ldb + gj] : B[(size_t)gj * ldb + gkb];
+      if (gj < N && gkb < kb1) bv = TB ? B[(size_t)gkb * ldb + gj] : B[(size_t)gj * ldb + gkb];
       Bs[kb][jj] = bv;
     }
     __syncthreads();
@@ -670,21 +705,46 @@ __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, const do
       if (gi < M && gj < N) C[(size_t)gj * ldc + gi] = acc[u][v];
     }
 }
+// C = sum over the splits of the partials, in split order (deterministic)
+__global__ void sum_splits_kernel(const double* P, int splits, int M, int N, double* C, int ldc) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)M * N) return;
+  const int i = (int)(t % M), j = (int)(t / M);
+  double s = 0.0;
+  for (int z = 0; z < splits; ++z) s += P[((size_t)z * N + j) * M + i];
+  C[(size_t)j * ldc + i] = s;
+}
 
 // ------------------------------------------------------------------------------------------
 // host side
+// Stream-ordered device memory of one build (zeroed), from the device's default memory pool, which
+// keeps freed blocks for the next build (no cudaMalloc / cudaFree round trips per buffer).
 struct Dev {
+  cudaStream_t s = nullptr;
   std::vector<void*> owned;
-  ~Dev() { for (void* p : owned) cudaFree(p); }
+  ~Dev() { for (void* p : owned) cudaFreeAsync(p, s); }
   template <typename T>
   T* alloc(size_t n) {
     void* p = nullptr;
-    if (cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) return nullptr;
+    const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+    if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) return nullptr;
     owned.push_back(p);
-    cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T));
+    cudaMemsetAsync(p, 0, bytes, s);
     return (T*)p;
   }
 };
+void keep_pool_memory() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  int dev = 0;
+  cudaMemPool_t pool;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+}
 
 struct Timer {
   cudaEvent_t a = nullptr, b = nullptr;
@@ -698,6 +758,18 @@ struct Timer {
     float t = 0.f;
     cudaEventElapsedTime(&t, a, b);
     ms += t;
+  }
+};
+
+struct PhaseLog {  // FDTD_ROM_VERBOSE: device-synchronised wall time of each construction phase
+  bool on = getenv("FDTD_ROM_VERBOSE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(cudaStream_t s, const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "rom_build %-12s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
   }
 };
 
@@ -939,12 +1011,12 @@ struct Builder {
     t_orth.start(s);
     for (int j = 0; j < m; ++j) {
       CUCK(cudaMemcpyAsync(v, A + (size_t)j * lda, sizeof(double) * rows, cudaMemcpyDeviceToDevice, s));
-      cnorm2_kernel<<<1, RN_NT, 0, s>>>(nullptr, v, rows, nrm);
+      STCK(cnorm2(nullptr, v, rows, nrm));
       for (int pass = 0; pass < 2 && k > 0; ++pass) {
-        wtcv_kernel<<<k, GV_NT, 0, s>>>(U, ldu, nullptr, v, rows, h);
+        STCK(wtcv(U, ldu, nullptr, v, rows, k, h));
         v_minus_wh_kernel<<<blocks(rows, 256), 256, 0, s>>>(U, ldu, h, k, v, rows);
       }
-      cnorm2_kernel<<<1, RN_NT, 0, s>>>(nullptr, v, rows, nrm + 1);
+      STCK(cnorm2(nullptr, v, rows, nrm + 1));
       double nn[2];
       CUCK(cudaMemcpyAsync(nn, nrm, sizeof nn, cudaMemcpyDeviceToHost, s));
       CUCK(cudaStreamSynchronize(s));
@@ -958,10 +1030,62 @@ struct Builder {
     return FDTD_OK;
   }
 
+  // C (M x N) = op(A) diag(w) op(B); a long K is split over enough CTAs to fill the GPU, the
+  // partials summed in a fixed order
+  double* gemm_part = nullptr;
+  size_t gemm_cap = 0;
   template <bool TA, bool TB>
   void gemm(int M, int N, int K, const double* A, int lda, const double* w, const double* B, int ldb, double* C,
             int ldc) {
-    gemm_kernel<TA, TB><<<dim3(blocks(M, GT), blocks(N, GT)), 256, 0, s>>>(M, N, K, A, lda, w, B, ldb, C, ldc);
+    const int tiles = (int)(blocks(M, GT) * blocks(N, GT));
+    int splits = std::max(1, std::min((K + 4095) / 4096, 296 / std::max(tiles, 1)));
+    if (splits > 1 && (size_t)splits * M * N > gemm_cap) {
+      gemm_cap = (size_t)splits * M * N;
+      gemm_part = dev.alloc<double>(gemm_cap);
+      if (!gemm_part) splits = 1;
+    }
+    if (splits == 1) {
+      gemm_kernel<TA, TB><<<dim3(blocks(M, GT), blocks(N, GT), 1), 256, 0, s>>>(M, N, K, A, lda, w, B, ldb, C, ldc, K);
+      return;
+    }
+    const int kchunk = ((K + splits - 1) / splits + GT - 1) / GT * GT;
+    splits = (K + kchunk - 1) / kchunk;
+    gemm_kernel<TA, TB><<<dim3(blocks(M, GT), blocks(N, GT), splits), 256, 0, s>>>(M, N, K, A, lda, w, B, ldb,
+                                                                                 gemm_part, M, kchunk);
+    sum_splits_kernel<<<blocks((long)M * N, 256), 256, 0, s>>>(gemm_part, splits, M, N, C, ldc);
+  }
+
+  // ||v||_c^2 into out[0] and W[:, :k]^T (c o v) into h, single-CTA for short vectors, two-level
+  // (slices of RED_SLICE rows, ordered sum) for long ones; deterministic either way
+  double* red_part = nullptr;
+  size_t red_cap = 0;
+  fdtd_status red_buf(size_t n) {
+    if (n <= red_cap) return FDTD_OK;
+    red_cap = n;
+    red_part = dev.alloc<double>(n);
+    return red_part ? FDTD_OK : failf(FDTD_E_NOMEM, "reduction scratch");
+  }
+  fdtd_status cnorm2(const double* c, const double* v, int n, double* out) {
+    const int ng = (n + RED_SLICE - 1) / RED_SLICE;
+    if (ng <= 2) {
+      cnorm2_kernel<<<1, RN_NT, 0, s>>>(c, v, n, out);
+      return FDTD_OK;
+    }
+    STCK(red_buf(ng));
+    cnorm2_part_kernel<<<ng, GV_NT, 0, s>>>(c, v, n, red_part);
+    sum_parts_kernel<<<1, 32, 0, s>>>(red_part, ng, 1, out);
+    return FDTD_OK;
+  }
+  fdtd_status wtcv(const double* W, int ldw, const double* c, const double* v, int n, int k, double* h) {
+    const int ng = (n + RED_SLICE - 1) / RED_SLICE;
+    if (ng <= 2) {
+      wtcv_kernel<<<k, GV_NT, 0, s>>>(W, ldw, c, v, n, h);
+      return FDTD_OK;
+    }
+    STCK(red_buf((size_t)ng * k));
+    wtcv_part_kernel<<<dim3(k, ng), GV_NT, 0, s>>>(W, ldw, c, v, n, k, red_part);
+    sum_parts_kernel<<<blocks(k, 128), 128, 0, s>>>(red_part, ng, k, h);
+    return FDTD_OK;
   }
 
   // SPRIM basis from m Krylov vectors (romgen._sprim_basis_m): V1 (nEc x k1), V2 (nH x k2)
@@ -983,7 +1107,10 @@ struct Builder {
         CUCK(cudaMemcpyAsync(B0 + (size_t)k * g.nEc + k, &sc[k], sizeof(double), cudaMemcpyHostToDevice, s));
       CUCK(cudaStreamSynchronize(s));
     }
+    PhaseLog lg;
+    lg.mark(s, " B0");
     STCK(solve(B0, g.nEc, nullptr, 0, nY, blk));
+    lg.mark(s, " X0 solve");
     int nb = nY, k = 0;
     double* nrm = scal + 16;
     std::vector<int> acc;
@@ -993,13 +1120,13 @@ struct Builder {
         // add(v): CGS2 in the C inner product with deflation 1e-10 (romgen.add)
         t_orth.start(s);
         const double* src = blk + (size_t)c * N;
-        cnorm2_kernel<<<1, RN_NT, 0, s>>>(cdiag, src, N, nrm);
+        STCK(cnorm2(cdiag, src, N, nrm));
         CUCK(cudaMemcpyAsync(v, src, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
         for (int pass = 0; pass < 2 && k > 0; ++pass) {
-          wtcv_kernel<<<k, GV_NT, 0, s>>>(W, N, cdiag, v, N, h);
+          STCK(wtcv(W, N, cdiag, v, N, k, h));
           v_minus_wh_kernel<<<blocks(N, 256), 256, 0, s>>>(W, N, h, k, v, N);
         }
-        cnorm2_kernel<<<1, RN_NT, 0, s>>>(cdiag, v, N, nrm + 1);
+        STCK(cnorm2(cdiag, v, N, nrm + 1));
         double nn[2];
         CUCK(cudaMemcpyAsync(nn, nrm, sizeof nn, cudaMemcpyDeviceToHost, s));
         t_orth.stop(s);
@@ -1009,6 +1136,7 @@ struct Builder {
         acc.push_back(k);
         ++k;
       }
+      lg.mark(s, " block GS");
       if (k >= m || acc.empty()) break;
       // next block: solve(R11 o W_E[:, acc], R22 o W_H[:, acc])
       nb = (int)acc.size();
@@ -1021,11 +1149,13 @@ struct Builder {
       gather_cols_kernel<<<dim3(blocks(g.nEc, 256), nb), 256, 0, s>>>(W, N, didx, r11, g.nEc, bE, g.nEc, nb);
       gather_cols_kernel<<<dim3(blocks(g.nH, 256), nb), 256, 0, s>>>(W + g.nEc, N, didx, r22, g.nH, bH, g.nH, nb);
       STCK(solve(bE, g.nEc, bH, g.nH, nb, blk));
+      lg.mark(s, " block solve");
     }
     used = k;
     // V1, V2: the E and H rows of W orthonormalised in Krylov order
     STCK(orth(W, N, g.nEc, k, V1, g.nEc, k1));
     STCK(orth(W + g.nEc, N, g.nH, k, V2, g.nH, k2));
+    lg.mark(s, " orth");
     return FDTD_OK;
   }
 };
@@ -1071,7 +1201,16 @@ fdtd_status build(const fdtd_rom_spec* sp, fdtd_rom_built* out) {
   if (!sp || !out || !sp->eps_r || !sp->sigma || sp->bx < 1 || sp->by < 1 || sp->r < 1 || sp->q < 2 ||
       !(sp->dx > 0) || !(sp->dy > 0) || !(sp->fmax > 0))
     return failf(FDTD_E_ARG, "invalid ROM spec");
+  // the stream outlives the builder (its buffers are freed on it, then it is synchronised)
+  struct StreamGuard {
+    cudaStream_t s = nullptr;
+    ~StreamGuard() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } }
+  } sg;
+  CUCK(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  keep_pool_memory();
   Builder b;
+  b.s = sg.s;
+  b.dev.s = sg.s;
   Geo& g = b.g;
   g.bx = sp->bx; g.by = sp->by; g.r = sp->r;
   g.Nx = g.bx * g.r; g.Ny = g.by * g.r;
@@ -1089,8 +1228,6 @@ fdtd_status build(const fdtd_rom_spec* sp, fdtd_rom_built* out) {
       return failf(FDTD_E_ARG, "fine cell %zu: eps_r must be positive and finite, sigma finite and >= 0", i);
   b.s0 = PI * sp->fmax;
   b.cg_tol = sp->cg_tol > 0 ? sp->cg_tol : 1e-13;
-  CUCK(cudaStreamCreateWithFlags(&b.s, cudaStreamNonBlocking));
-  struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } sg{b.s};
   Timer t_all;
   t_all.start(b.s);
   const int nnz = g.nY * g.r + 2 * (g.nEc - g.nY);
@@ -1115,7 +1252,10 @@ fdtd_status build(const fdtd_rom_spec* sp, fdtd_rom_built* out) {
     const char* sv = getenv("FDTD_ROM_SOLVER");
     b.h_form = !(sv && sv[0] == 'e');
   }
+  PhaseLog plog;
+  plog.mark(b.s, "assembly");
   if (b.h_form) STCK(b.setup_mg());
+  plog.mark(b.s, "multigrid");
   b.setup_coop();
   CUCK(cudaMemcpyAsync(b.cdiag, b.r11, sizeof(double) * g.nEc, cudaMemcpyDeviceToDevice, b.s));
   CUCK(cudaMemcpyAsync(b.cdiag + g.nEc, b.r22, sizeof(double) * g.nH, cudaMemcpyDeviceToDevice, b.s));
@@ -1155,6 +1295,7 @@ fdtd_status build(const fdtd_rom_spec* sp, fdtd_rom_built* out) {
     q1 = std::min(kl, nP + q1w);
   }
 
+  plog.mark(b.s, "sprim");
   // congruence (eq:R11_tilde .. eq:K_tilde)
   double* R11 = b.dev.alloc<double>((size_t)q1 * q1);
   double* F11 = b.dev.alloc<double>((size_t)q1 * q1);
@@ -1170,6 +1311,7 @@ fdtd_status build(const fdtd_rom_spec* sp, fdtd_rom_built* out) {
   b.gemm<true, false>(q1, q2, g.nEc, V1, g.nEc, nullptr, KV2, g.nEc, Kt, q1);
   CUCK(cudaGetLastError());
 
+  plog.mark(b.s, "congruence");
   // CFL: singular values of R11^-1/2 K R22^-1/2 (eq:CFLgeneralized), optional clip
   double *h1 = b.dev.alloc<double>((size_t)q1 * q1), *i1 = b.dev.alloc<double>((size_t)q1 * q1);
   double *h2 = b.dev.alloc<double>((size_t)q2 * q2), *i2 = b.dev.alloc<double>((size_t)q2 * q2);
@@ -1231,6 +1373,7 @@ fdtd_status build(const fdtd_rom_spec* sp, fdtd_rom_built* out) {
     }
   }
 
+  plog.mark(b.s, "cfl");
   // outputs (row-major)
   std::vector<double> hK((size_t)q1 * q2), hV1p((size_t)g.nY * q1);
   CUCK(cudaMemcpyAsync(hK.data(), Kt, sizeof(double) * q1 * q2, cudaMemcpyDeviceToHost, b.s));
