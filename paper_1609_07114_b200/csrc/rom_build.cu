@@ -279,11 +279,13 @@ struct MGArgs {
   Geo g;
   int nlev; MGLevel lev[MG_MAXLEV];
   const double *cc, *we, *wn;  // per level (pool offsets): diagonal, east and north couplings
+  const float *fcc, *fwe, *fwn;  // the same in fp32: the V-cycle is a preconditioner, run in fp32
   const double* cS;            // level-0 exact stencil diagonal (no port terms)
   const double* pw;            // per port: v^2 / D_e (v = fdx for S/N ports, fdy for W/E)
   const double* B; int ldb;    // right-hand sides (nH x ncol)
   double* X; int ldx;          // solutions
-  double* work; long wstride;  // per column: r, z, p, q (4 nH), then per level >= 1: x, b
+  double* work; long wstride;  // per column: r, z, p, q (4 nH doubles), then the V-cycle's fp32
+                               // x, b of every level (level 0 first)
   double* psum;                // per column: nY
   double tol; int maxit; int* iters;
 };
@@ -337,9 +339,9 @@ __global__ void hs_coarsen_kernel(MGLevel f, MGLevel c, const double* cc_f, cons
 }
 
 constexpr int MG_NT = 1024;
-__device__ __forceinline__ void mg_smooth(const MGArgs& a, int l, double* x, const double* b, int color) {
+__device__ __forceinline__ void mg_smooth(const MGArgs& a, int l, float* x, const float* b, int color) {
   const MGLevel L = a.lev[l];
-  const double *c = a.cc + L.off, *we = a.we + L.off, *wn = a.wn + L.off;
+  const float *c = a.fcc + L.off, *we = a.fwe + L.off, *wn = a.fwn + L.off;
   const int nx = L.nx, n = L.nx * L.ny;
   // cells of one colour: (i + j) % 2 == color; thread t handles the t-th such cell
   const int half = (n + 1) / 2 + 1;
@@ -352,7 +354,7 @@ __device__ __forceinline__ void mg_smooth(const MGArgs& a, int l, double* x, con
     if (j >= L.ny) continue;
     const int k = j * nx + i;
     if (k >= n) continue;
-    double s = b[k];
+    float s = b[k];
     if (i > 0) s -= we[k - 1] * x[k - 1];
     if (i < nx - 1) s -= we[k] * x[k + 1];
     if (j > 0) s -= wn[k - nx] * x[k - nx];
@@ -361,17 +363,17 @@ __device__ __forceinline__ void mg_smooth(const MGArgs& a, int l, double* x, con
   }
   __syncthreads();
 }
-__device__ __forceinline__ void mg_restrict(const MGArgs& a, int l, const double* x, const double* b, double* bc) {
+__device__ __forceinline__ void mg_restrict(const MGArgs& a, int l, const float* x, const float* b, float* bc) {
   const MGLevel f = a.lev[l], c = a.lev[l + 1];
-  const double *cc = a.cc + f.off, *we = a.we + f.off, *wn = a.wn + f.off;
+  const float *cc = a.fcc + f.off, *we = a.fwe + f.off, *wn = a.fwn + f.off;
   for (int t = threadIdx.x; t < c.nx * c.ny; t += MG_NT) {
     const int I = t % c.nx, J = t / c.nx;
     const int i0 = 2 * I, j0 = 2 * J, i1 = min(i0 + 1, f.nx - 1), j1 = min(j0 + 1, f.ny - 1);
-    double s = 0.0;
+    float s = 0.f;
     for (int j = j0; j <= j1; ++j)
       for (int i = i0; i <= i1; ++i) {
         const int k = j * f.nx + i;
-        double r = b[k] - cc[k] * x[k];
+        float r = b[k] - cc[k] * x[k];
         if (i > 0) r -= we[k - 1] * x[k - 1];
         if (i < f.nx - 1) r -= we[k] * x[k + 1];
         if (j > 0) r -= wn[k - f.nx] * x[k - f.nx];
@@ -382,7 +384,7 @@ __device__ __forceinline__ void mg_restrict(const MGArgs& a, int l, const double
   }
   __syncthreads();
 }
-__device__ __forceinline__ void mg_prolong(const MGArgs& a, int l, double* x, const double* xc) {
+__device__ __forceinline__ void mg_prolong(const MGArgs& a, int l, float* x, const float* xc) {
   const MGLevel f = a.lev[l], c = a.lev[l + 1];
   for (int k = threadIdx.x; k < f.nx * f.ny; k += MG_NT) {
     const int i = k % f.nx, j = k / f.nx;
@@ -390,14 +392,17 @@ __device__ __forceinline__ void mg_prolong(const MGArgs& a, int l, double* x, co
   }
   __syncthreads();
 }
-// z = V-cycle(r): symmetric (pre: red-black, post: black-red; coarsest: symmetric sweep pairs)
-__device__ void mg_vcycle(const MGArgs& a, double* wcol, double* z, double* r) {
+// z = V-cycle(r) (fp32 inside, fp64 in and out): symmetric (pre: red-black, post: black-red;
+// coarsest: symmetric sweep pairs)
+__device__ void mg_vcycle(const MGArgs& a, double* wcol, double* z, const double* r) {
   constexpr int NU = 2, NCOARSE = 30;
-  auto xl = [&](int l) { return l == 0 ? z : wcol + 4L * a.g.nH + 2 * (a.lev[l].off - a.lev[1].off); };
-  auto bl = [&](int l) { return l == 0 ? r : wcol + 4L * a.g.nH + 2 * (a.lev[l].off - a.lev[1].off) + a.lev[l].nx * a.lev[l].ny; };
+  float* fb = reinterpret_cast<float*>(wcol + 4L * a.g.nH);
+  auto xl = [&](int l) { return fb + 2 * a.lev[l].off; };
+  auto bl = [&](int l) { return fb + 2 * a.lev[l].off + a.lev[l].nx * a.lev[l].ny; };
+  for (int k = threadIdx.x; k < a.g.nH; k += MG_NT) bl(0)[k] = (float)r[k];
   for (int l = 0; l < a.nlev; ++l) {
-    double* x = xl(l);
-    for (int k = threadIdx.x; k < a.lev[l].nx * a.lev[l].ny; k += MG_NT) x[k] = 0.0;
+    float* x = xl(l);
+    for (int k = threadIdx.x; k < a.lev[l].nx * a.lev[l].ny; k += MG_NT) x[k] = 0.f;
     __syncthreads();
     if (l == a.nlev - 1) {
       for (int it = 0; it < NCOARSE; ++it) {
@@ -413,6 +418,12 @@ __device__ void mg_vcycle(const MGArgs& a, double* wcol, double* z, double* r) {
     mg_prolong(a, l, xl(l), xl(l + 1));
     for (int it = 0; it < NU; ++it) { mg_smooth(a, l, xl(l), bl(l), 1); mg_smooth(a, l, xl(l), bl(l), 0); }
   }
+  for (int k = threadIdx.x; k < a.g.nH; k += MG_NT) z[k] = (double)xl(0)[k];
+  __syncthreads();
+}
+__global__ void to_f32_kernel(const double* a, float* b, long n) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = (float)a[i];
 }
 // q = S_H p exactly (stencil with cS + the port rank-1 blocks)
 __device__ __forceinline__ void hs_apply(const MGArgs& a, const double* p, double* q, double* ps) {
@@ -798,6 +809,7 @@ struct Builder {
   int nlev = 0;
   MGLevel lev[MG_MAXLEV];
   double *mcc = nullptr, *mwe = nullptr, *mwn = nullptr, *mcS = nullptr, *mpw = nullptr;
+  float *fcc = nullptr, *fwe = nullptr, *fwn = nullptr;
   double *hrhs = nullptr, *hwork = nullptr, *hpsum = nullptr;
   int h_cols = 0;
   long wstride = 0;
@@ -837,7 +849,12 @@ struct Builder {
       hs_coarsen_kernel<<<blocks((long)c.nx * c.ny, 256), 256, 0, s>>>(f, c, mcc + f.off, mwe + f.off, mwn + f.off,
                                                                       mcc + c.off, mwe + c.off, mwn + c.off);
     }
-    wstride = 4L * g.nH + 2 * (off - lev[nlev > 1 ? 1 : 0].off);
+    fcc = dev.alloc<float>(off); fwe = dev.alloc<float>(off); fwn = dev.alloc<float>(off);
+    if (!fcc || !fwe || !fwn) return failf(FDTD_E_NOMEM, "multigrid hierarchy");
+    to_f32_kernel<<<blocks(off, 256), 256, 0, s>>>(mcc, fcc, off);
+    to_f32_kernel<<<blocks(off, 256), 256, 0, s>>>(mwe, fwe, off);
+    to_f32_kernel<<<blocks(off, 256), 256, 0, s>>>(mwn, fwn, off);
+    wstride = 4L * g.nH + (2 * off + 1) / 2;  // + the fp32 x, b of every level (in doubles)
     CUCK(cudaGetLastError());
     return FDTD_OK;
   }
@@ -864,6 +881,7 @@ struct Builder {
     a.g = g; a.nlev = nlev;
     for (int l = 0; l < nlev; ++l) a.lev[l] = lev[l];
     a.cc = mcc; a.we = mwe; a.wn = mwn; a.cS = mcS; a.pw = mpw;
+    a.fcc = fcc; a.fwe = fwe; a.fwn = fwn;
     a.B = hrhs; a.ldb = g.nH; a.X = X + g.nEc; a.ldx = n();
     a.work = hwork; a.wstride = wstride; a.psum = hpsum;
     a.tol = cg_tol; a.maxit = 5000; a.iters = cg_it;
