@@ -12,12 +12,12 @@ from helpers import consistent_random_state, gpu_from_scene, ordered_instances
 pytestmark = pytest.mark.gpu
 
 
-def slab_scene(precision=32):
+def slab_scene(precision=32, literal=False):
     nx, ny = 203, 240
     rng = np.random.default_rng(12)
     dx = dy = 1e-3
     fe, fs = sc.uniform_fill(3, 2, 3, 1, 1, 4, 0, 0.05)
-    m1 = rg.build_rom(3, 2, 3, dx, dy, fe, fs, 20, 30e9)
+    m1 = rg.build_rom(3, 2, 3, dx, dy, fe, fs, 20, 30e9, literal=literal)
     fe, fs = sc.uniform_fill(2, 2, 4, 2, 1, 4, 0, 0.05)
     m2 = rg.build_rom(2, 2, 4, dx, dy, fe, fs, 16, 30e9)
     dt = 0.95 * min(m1["fine_dt_limit"], m2["fine_dt_limit"])
@@ -143,3 +143,18 @@ def test_cpml_slabs_bitwise_equal_single(nslab, precision, spp, rom):
     assert np.array_equal(x1, x2)
     assert np.array_equal(p1, p2)
     np.testing.assert_allclose(e2, e1, rtol=1e-12 if precision == 64 else 1e-6)
+
+
+@pytest.mark.parametrize("nslab", [2, 3])
+def test_literal_models_on_slabs_bitwise(nslab):
+    """NEXT-1 (paper-literal nP-port) models on row slabs: bit-identical to one context."""
+    s = slab_scene(64, literal=True)
+    assert slabs.check_partition(s.placements, s.models, s.ny, nslab)
+    init = consistent_random_state(s, 4)
+    (W1, x1, p1, e1) = run_single(s, 201, init)
+    (W2, x2, p2, e2) = run_group(s, 201, init, nslab, 2)
+    for a, b in zip(W1, W2):
+        assert np.array_equal(a, b)
+    assert np.array_equal(x1, x2)
+    assert np.array_equal(p1, p2)
+    np.testing.assert_allclose(e2, e1, rtol=1e-12)
