@@ -304,6 +304,9 @@ def run_ours(args):
             "sweep_ms_per_launch": sweep_avg_s * 1e3,
             "post_ms_per_launch": post_ms / max(nl, 1), "sweep_share_of_step": sweep_ms / max(ms, 1e-9),
             "frac_of_8TBs_nominal": achieved / 8000.0}
+    if traffic:  # the DRAM bytes the kernel actually moves (ncu) over the same launch time
+        roof["dram_gbs"] = traffic / sweep_avg_s / 1e9
+        roof["dram_frac"] = roof["dram_gbs"] / peak
     cpu = None
     if ws == 1 and not args.no_cpu:
         v, dt, done, sample, cores = oracle_rate(wl, 10 ** 6, max_seconds=args.cpu_seconds)
