@@ -266,7 +266,7 @@ int sweep_gx_max(const fdtd_ctx* c) {
 }
 
 template <typename T>
-fdtd::PostParams<T> post_params(fdtd_ctx* c, int q, int K) {
+fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
   fdtd::PostParams<T> p{};
   p.n_inst = (int)c->inst_model.size();
   p.models = c->d_models; p.mpool = (const T*)c->d_mpool;
@@ -488,8 +488,8 @@ fdtd_status enqueue_pass(fdtd_ctx* c, int q, cudaStream_t s, int K) {
   };
   const bool has_fix = !c->inst_model.empty();
   auto post = [&](cudaStream_t st) {
-    if (c->prec == 64) fdtd::launch_post<double>(post_params<double>(c, q, K), K, c->energy_on, st);
-    else fdtd::launch_post<float>(post_params<float>(c, q, K), K, c->energy_on, st);
+    if (c->prec == 64) fdtd::launch_post<double>(post_params<double>(c, q), K, c->energy_on, st);
+    else fdtd::launch_post<float>(post_params<float>(c, q), K, c->energy_on, st);
     c->launches += 1;
   };
   cudaEvent_t e[3];
@@ -700,7 +700,6 @@ fdtd_status apply_passes(fdtd_ctx* c, int k);
 // on kz: one NCCL min-reduction).  Runs at the first fdtd_step after a configuration change.
 fdtd_status configure_passes(fdtd_ctx* c) {
   if (!c->kz_dirty) return FDTD_OK;
-  fdtd_status st;
   int want = std::max(1, std::min(c->k_want, c->V));
   int k = want >= 4 ? 4 : want >= 2 ? 2 : 1;
   while (k > 1 && !passes_valid(c, k)) k /= 2;

@@ -74,12 +74,6 @@ __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(
 struct F2 {
   float x, y;
 };
-__device__ __forceinline__ F2 add2(F2 a, F2 b) {
-  F2 r;
-  asm("{.reg .b64 ra, rb, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n add.rn.f32x2 rd, ra, rb;\n"
-      " mov.b64 {%0,%1}, rd;}" : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return r;
-}
 __device__ __forceinline__ F2 sub2(F2 a, F2 b) {
   F2 r;
   asm("{.reg .b64 ra, rb, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n sub.rn.f32x2 rd, ra, rb;\n"

@@ -1186,7 +1186,6 @@ fdtd_status spd_sqrt(Builder& b, const double* A, int m, double* H, double* I, c
   double* w = b.dev.alloc<double>(m);
   if (!W || !U || !w) return failf(FDTD_E_NOMEM, "spd_sqrt");
   CUCK(cudaMemcpyAsync(W, A, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, b.s));
-  int k = 0;
   std::vector<double> sg;
   STCK(b.jacobi(W, m, m, m, nullptr, sg));
   std::vector<int> perm(m);
@@ -1202,7 +1201,6 @@ fdtd_status spd_sqrt(Builder& b, const double* A, int m, double* H, double* I, c
   CUCK(cudaMemcpyAsync(dperm, perm.data(), sizeof(int) * m, cudaMemcpyHostToDevice, b.s));
   CUCK(cudaMemcpyAsync(dsc, sc.data(), sizeof(double) * m, cudaMemcpyHostToDevice, b.s));
   permute_scale_kernel<<<dim3(blocks(m, 256), m), 256, 0, b.s>>>(W, m, dperm, dsc, m, U, m, m);
-  (void)k;
   for (int t = 0; t < m; ++t) ws[t] = std::sqrt(sg[perm[t]]);
   CUCK(cudaMemcpyAsync(w, ws.data(), sizeof(double) * m, cudaMemcpyHostToDevice, b.s));
   b.gemm<false, true>(m, m, m, U, m, w, U, m, H, m);  // U diag(sqrt s) U^T
