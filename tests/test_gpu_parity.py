@@ -341,3 +341,23 @@ def test_source_and_probes_on_warp_and_chunk_seams(src):
         assert np.array_equal(a, b)
     assert np.array_equal(outs[0][1], outs[1][1])
     _compare(s, 300, 1e-4)
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_degenerate_roms(precision):
+    """The method's smallest cases: a one-cell block (bx = by = 1, r = 2) and order q = 2
+    (q1 = q2 = 1), next to full-order 1x1 blocks, in one lossy grid with a random start:
+    fp64 <= 1e-10 / fp32 <= 1e-4 against the oracle."""
+    rng = np.random.default_rng(21)
+    nx, ny, dx = 40, 36, 1e-3
+    eps, sig = rng.uniform(1, 3, (ny, nx)), rng.uniform(0, 0.03, (ny, nx))
+    fe, fs = sc.uniform_fill(1, 1, 2, 5, 1, 4, 0, 0.05)
+    m_q2 = rg.build_rom(1, 1, 2, dx, dx, fe, fs, 2, 30e9)
+    m_full = rg.build_rom(1, 1, 3, dx, dx, *sc.uniform_fill(1, 1, 3, 6, 1, 4, 0, 0.05), 4, 30e9, full=True)
+    assert (m_q2["q1"], m_q2["q2"]) == (1, 1)
+    dt = 0.95 * min(m_q2["fine_dt_limit"], m_full["fine_dt_limit"], sc.cfl_limit(dx, dx))
+    s = sc.Scene(name="degenerate", nx=nx, ny=ny, dx=dx, dy=dx, dt=dt, eps_r=eps, sigma=sig, precision=precision,
+                 steps=500, source=(8, 9), samples=sc.gaussian_samples(500, dt, 30e9, True),
+                 probes=np.array([[30, 30], [20, 18], [11, 25]], np.int32), models=[m_q2, m_full],
+                 placements=np.array([[0, 18, 18], [0, 26, 12], [1, 12, 24]], np.int32))
+    _compare(s, 500, 1e-10 if precision == 64 else 1e-4, random_init=7)
