@@ -636,7 +636,7 @@ __device__ double block_sum(double v, double* red) {
 // Y[i][b] += alpha * sum_c A[c*m + i] X[c][b] for i < m, b < B.  A is a shared model operator
 // (column-major, L2-resident: one coalesced 128-byte row of A per warp and column, reused for the
 // IPI instances of a thread's item); X, Y in shared memory with row stride B.
-template <typename T, int IPI>
+template <typename T, int IPI, bool ACC>
 __device__ __forceinline__ void bgemm_ipi(const T* __restrict__ A, int m, int lda, int k, const T* X, T* Y, int B,
                                           T alpha) {
   const int G = B / IPI;
@@ -665,16 +665,17 @@ __device__ __forceinline__ void bgemm_ipi(const T* __restrict__ A, int m, int ld
     }
     T* y = Y + i * B + g;
 #pragma unroll
-    for (int u = 0; u < IPI; ++u) y[u] = fma_rn(alpha, acc[u] + acc2[u], y[u]);
+    for (int u = 0; u < IPI; ++u) y[u] = ACC ? fma_rn(alpha, acc[u] + acc2[u], y[u]) : mul_rn(alpha, acc[u] + acc2[u]);
   }
 }
 
-// B (the batch's slot count) is a power of two (fdtd_api.cpp apply_passes), so B / IPI covers it
-template <typename T>
+// B (the batch's slot count) is a power of two (fdtd_api.cpp apply_passes), so B / IPI covers it.
+// ACC: Y += alpha A X; else Y = alpha A X (no zeroing pass; identical to accumulating onto zeros)
+template <typename T, bool ACC>
 __device__ __forceinline__ void bgemm(const T* A, int m, int lda, int k, const T* X, T* Y, int B, T alpha) {
-  if (m * (B / 4) >= (int)blockDim.x) bgemm_ipi<T, 4>(A, m, lda, k, X, Y, B, alpha);
-  else if (m * (B / 2) >= (int)blockDim.x) bgemm_ipi<T, 2>(A, m, lda, k, X, Y, B, alpha);
-  else bgemm_ipi<T, 1>(A, m, lda, k, X, Y, B, alpha);
+  if (m * (B / 4) >= (int)blockDim.x) bgemm_ipi<T, 4, ACC>(A, m, lda, k, X, Y, B, alpha);
+  else if (m * (B / 2) >= (int)blockDim.x) bgemm_ipi<T, 2, ACC>(A, m, lda, k, X, Y, B, alpha);
+  else bgemm_ipi<T, 1, ACC>(A, m, lda, k, X, Y, B, alpha);
 }
 
 // Shared-memory vectors of a batch (row stride B, NV rows each):
@@ -699,12 +700,9 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first
   const int tid = threadIdx.x, nt = blockDim.x;
   RomVec<T> v(sv, S);
   const T* mp = p.mpool;
-  for (int64_t k = tid; k < 2 * S; k += nt) v.so[k] = T(0);
-  for (int64_t k = tid; k < S; k += nt) v.so2[k] = T(0);
-  __syncthreads();
   // [H~^{n+1}; E*; -L~^T E*] = M1 x~^n, and with ENERGY also R~ x~^n (R~ is stored after M1 as
-  // q1 + q2 further rows of the same column-major operator: one GEMM phase)
-  bgemm<T>(mp + m.off_M1, ENERGY ? m1 + nx : m1, m1 + nx, nx, v.sx, v.so, B, T(1));
+  // q1 + q2 further rows of the same column-major operator: one GEMM phase); so is overwritten
+  bgemm<T, false>(mp + m.off_M1, ENERGY ? m1 + nx : m1, m1 + nx, nx, v.sx, v.so, B, T(1));
   __syncthreads();
   if (ENERGY) {  // x~^T R~ x~ + sum D_l D_l' eps/dt y^2 (storage function, R17)
     const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
@@ -745,7 +743,7 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first
   }
   __syncthreads();
   // [E~^{n+1}; y^{n+1}] = [E*; L~^T E*] + M2 U
-  bgemm<T>(mp + m.off_M2, m2, m2, nY, v.sU, v.so2, B, T(1));
+  bgemm<T, true>(mp + m.off_M2, m2, m2, nY, v.sU, v.so2, B, T(1));
   __syncthreads();
   for (int64_t k = tid; k < (int64_t)nx * B; k += nt) {
     const int64_t r = k / B;
@@ -931,7 +929,20 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     double* eout = p.rom_partials + (int64_t)s * p.n_inst + first;
     rom_step<T, ENERGY>(p, m, first, nb, B, S, sv, eout);
     if (ENERGY && tid < nb) eout[tid] += zsum[tid];
-    // ---- E half-step on the region's interior edges (frozen edges keep their value)
+    // ---- S6: y^{n+s+1} into the region's interface edges, and in the same phase the E half-step
+    // on the region's live edges (dead edges -- interface, PEC, hole -- keep their value: they are
+    // skipped, so the scatter and the update never touch the same edge)
+    for (int b = 0; b < nb; ++b) {
+      const Geo q = geo(b);
+      const int W1 = q.Wr + 1;
+      for (int i = tid; i < nY; i += nt) {
+        const T y = sy[i * B + b];
+        if (i < q.bx) q.EX[M * q.Wr + M + i] = y;
+        else if (i < 2 * q.bx) q.EX[(M + q.by) * q.Wr + M + i - q.bx] = y;
+        else if (i < 2 * q.bx + q.by) q.EY[(M + i - 2 * q.bx) * W1 + M] = y;
+        else q.EY[(M + i - 2 * q.bx - q.by) * W1 + M + q.bx] = y;
+      }
+    }
     for (int b = 0; b < nb; ++b) {
       const Geo q = geo(b);
       const int W1 = q.Wr + 1;
@@ -944,7 +955,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
         bool l;
         T a, ca, cb;
         edge_coef(q.MA[t - q.Wr], q.MS[t - q.Wr], q.MA[t], q.MS[t], p.idy, ca, cb, a, l);
-        q.EX[t] = eupd(q.EX[t], ca, cb, q.H[t] - q.H[t - q.Wr]);
+        if (l) q.EX[t] = eupd(q.EX[t], ca, cb, q.H[t] - q.H[t - q.Wr]);
       }
       const int dy_u = nt % (cw - 1), dy_v = nt / (cw - 1);
       int yu = s + 1 + tid % (cw - 1), yv = s + tid / (cw - 1);
@@ -955,20 +966,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
         bool l;
         T a, ca, cb;
         edge_coef(q.MA[c - 1], q.MS[c - 1], q.MA[c], q.MS[c], -p.idx, ca, cb, a, l);
-        q.EY[v * W1 + u] = eupd(q.EY[v * W1 + u], ca, cb, q.H[c] - q.H[c - 1]);
-      }
-    }
-    __syncthreads();
-    // ---- S6: y^{n+s+1} into the region's interface edges
-    for (int b = 0; b < nb; ++b) {
-      const Geo q = geo(b);
-      const int W1 = q.Wr + 1;
-      for (int i = tid; i < nY; i += nt) {
-        const T y = sy[i * B + b];
-        if (i < q.bx) q.EX[M * q.Wr + M + i] = y;
-        else if (i < 2 * q.bx) q.EX[(M + q.by) * q.Wr + M + i - q.bx] = y;
-        else if (i < 2 * q.bx + q.by) q.EY[(M + i - 2 * q.bx) * W1 + M] = y;
-        else q.EY[(M + i - 2 * q.bx - q.by) * W1 + M + q.bx] = y;
+        if (l) q.EY[v * W1 + u] = eupd(q.EY[v * W1 + u], ca, cb, q.H[c] - q.H[c - 1]);
       }
     }
     __syncthreads();
