@@ -60,9 +60,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=96)
     ap.add_argument("--slabs", default="1,2,4,8")
+    ap.add_argument("--workload", default="cfg4")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_slab_overhead.json"))
     a = ap.parse_args()
-    scene = configs.make("cfg4", device="cuda")
+    scene = configs.make(a.workload, device="cuda")
     stream = torch.cuda.Stream()
     rows = []
     base = None
@@ -86,7 +87,7 @@ def main():
                          cell_updates_per_s=scene.nx * scene.ny / ms * 1e3,
                          per_pass_sum_over_slabs_ms=dict(sweep=sweep_ms, fixup=post_ms)))
         print(json.dumps(rows[-1]), flush=True)
-    out = dict(what="config 4 as N in-process row slabs on one B200 (sequential on one stream) vs one context",
+    out = dict(what="%s as N in-process row slabs on one B200 (sequential on one stream) vs one context" % a.workload,
                steps=a.steps, rows=rows)
     with open(a.out, "w") as f:
         json.dump(out, f, indent=1)
