@@ -7,8 +7,10 @@ A "step" is one time step of the whole hot path (S1..S8 of DESIGN.md) over the
 workload.  Default workload: BASELINE config 4 (the metric's 1/2/4/8-GPU
 config): 32768^2 fp32 coarse grid, smooth random lossy medium, 4096 instances of
 one ROM (16x16 block, r = 4, q = 128), source, 64 probes and the energy trace
-recorded every step.  N > 1: launched by torchrun, one rank per GPU, row slabs
-of 32768/N rows with the per-step NCCL halo exchange (strong scaling).
+recorded every step.  N > 1: one rank per GPU (bench.py re-launches itself under
+torch.distributed.run when it is not already a torchrun rank, and fails when fewer than N GPUs
+are visible), row slabs of 32768/N rows with the K-row NCCL halo exchange per K-step pass
+(strong scaling).
 ``--impl reference`` times the fp64 CPU oracle (the base contract's reference
 arm for this tier) on a bounded sample of the same workload.
 """
@@ -54,6 +56,42 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     lrank = int(os.environ.get("LOCAL_RANK", str(rank)))
     return ws, rank, lrank
+
+
+def kernel_source_sha():
+    """Hash of the sources that define the kernels and their build flags: the ncu traffic recorded
+    in profiles/sweep_traffic.json is only valid for the build it was measured on."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in ("paper_1609_07114_b200/csrc/fdtd_kernels.cu", "paper_1609_07114_b200/csrc/fdtd_kernels.cuh",
+              "paper_1609_07114_b200/build.py"):
+        h.update(open(os.path.join(ROOT, f), "rb").read())
+    return h.hexdigest()[:16]
+
+
+def ensure_ranks(args):
+    """--gpus N > 1 outside torchrun: re-launch this command as N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1; fail loudly when fewer than N GPUs are visible."""
+    ws, _, _ = dist_env()
+    if "WORLD_SIZE" in os.environ:
+        if ws != args.gpus:
+            sys.exit("bench.py: --gpus %d but WORLD_SIZE=%d" % (args.gpus, ws))
+        return
+    if args.gpus <= 1:
+        return
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.exit("bench.py: --gpus %d but only %d CUDA device(s) visible" % (args.gpus, have))
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 # ------------------------------------------------------------------ CPU oracle timing
@@ -159,9 +197,16 @@ def run_ours(args):
     from paper_1609_07114_b200 import Simulation, nccl_unique_id, slabs
 
     ws, rank, lrank = dist_env()
+    if torch.cuda.device_count() < max(ws, lrank + 1):
+        sys.exit("bench.py: rank %d needs CUDA device %d, %d visible" % (rank, lrank, torch.cuda.device_count()))
     torch.cuda.set_device(lrank)
+    dev = torch.device("cuda", lrank)
     if ws > 1:
-        dist.init_process_group("gloo")
+        # NCCL init lines (one per rank: "nranks N") go to stderr, keeping stdout to the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        dist.init_process_group("nccl", device_id=dev)
     wl = args.workload
     t_setup = time.perf_counter()
     scene = configs.make(wl, device="cuda")
@@ -169,11 +214,11 @@ def run_ours(args):
     rb, re = slabs.slab_rows(ny, ws, rank)
     nid = None
     if ws > 1:
-        t = torch.zeros(128, dtype=torch.uint8)
+        t = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
-            t = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8).clone()
+            t = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8).clone().to(dev)
         dist.broadcast(t, 0)
-        nid = bytes(t.numpy().tobytes())
+        nid = bytes(t.cpu().numpy().tobytes())
     m0, m1 = max(rb - 4, 0), min(re + 4, ny)  # materials of rows [rb-4, re+4): the 4-step halo
     eps = scene.eps_r[m0:m1].contiguous()
     sig = scene.sigma[m0:m1].contiguous()
@@ -183,12 +228,13 @@ def run_ours(args):
     del eps, sig
     ninst = 0
     if scene.placements is not None:
+        # fdtd_add_rom is collective with several ranks: every rank adds every model (count 0
+        # where it owns none of its instances)
         P = slabs.owned_placements(scene.placements, scene.models, rb, re)
         for k, m in enumerate(scene.models):
             sel = P[P[:, 0] == k]
-            if len(sel):
-                sim.add_rom(m, sel[:, 1:3])
-                ninst += len(sel)
+            sim.add_rom(m, sel[:, 1:3])
+            ninst += len(sel)
     sim.set_source(*scene.source, scene.samples)
     sim.set_probes(scene.probes)
     sim.record_energy(not args.no_energy)
@@ -228,7 +274,7 @@ def run_ours(args):
     launches = sim.info().kernel_launches - l0
     ms_all = ms
     if ws > 1:
-        t = torch.tensor([ms, sweep_ms, post_ms], dtype=torch.float64)
+        t = torch.tensor([ms, sweep_ms, post_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_all, sweep_ms_max, post_ms_max = t.tolist()
     value = cells_total * args.steps / (ms_all / 1e3)
@@ -258,7 +304,7 @@ def run_ours(args):
         barrier()
         dt_e2e = time.perf_counter() - t0
         if ws > 1:
-            t = torch.tensor([dt_e2e], dtype=torch.float64)
+            t = torch.tensor([dt_e2e], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt_e2e = t.item()
         es = 8 if scene.precision == 64 else 4
@@ -279,34 +325,47 @@ def run_ours(args):
     es = 8 if scene.precision == 64 else 4
     info = sim.info()
     spp = info.steps_per_pass              # time steps advanced by one sweep pass (1, 2 or 4)
-    # algorithmic bytes: 40 B per cell-step fp32 -- read Ex, Ey, Hz and the per-edge
-    # (ca, cb) pairs, write Ex, Ey, Hz -- times the cell-steps one launch advances
-    alg_bytes = 10 * es * cells_rank * spp
     sweep_avg_s = (sweep_ms / max(nl, 1)) / 1e3
-    achieved = alg_bytes / sweep_avg_s / 1e9
     peak = pk.get("hbm_gbs", 6650.0)
-    traffic = None
+    # Bytes one launch must move as implemented: Ex, Ey, Hz and the two per-cell material terms read
+    # once, Ex, Ey, Hz written once per K-step pass (8 arrays x es per cell).  The DRAM traffic
+    # ncu measured on this build (profiles/sweep_traffic.json, valid only while the kernel sources'
+    # hash matches) replaces it when present: `frac` is then the fraction of the measured copy
+    # bandwidth the kernel's actual DRAM traffic reaches.
+    compulsory = 8 * es * cells_rank
+    traffic, tsrc = None, None
     tpath = os.path.join(ROOT, "profiles", "sweep_traffic.json")
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))
-            if tj.get("workload") == wl and int(tj.get("steps_per_pass", 1)) == spp:
+            if (tj.get("workload") == wl and int(tj.get("steps_per_pass", 1)) == spp and ws == 1
+                    and tj.get("kernel_src_sha") == kernel_source_sha()):
                 traffic = tj.get("bytes_per_launch_per_cell") * cells_rank
+                tsrc = tj.get("source")
         except Exception:
             traffic = None
+    moved = traffic if traffic else compulsory
+    achieved = moved / sweep_avg_s / 1e9
+    # SURVEY 8(d)'s algorithmic count (40 B per cell-step fp32 -- Ex, Ey, Hz read and written plus
+    # the per-edge (ca, cb) pairs -- times the cell-steps of one launch): with K steps per HBM pass
+    # this is an *effective* bandwidth, above the roof by up to K x 40/32
+    alg_bytes = 10 * es * cells_rank * spp
     kname = "sweepk_kernel<%s, K=%d> (fused H+E, %d time step%s per HBM pass)" % (
         "float" if es == 4 else "double", spp, spp, "s" if spp > 1 else "")
     roof = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": peak,
             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "bytes_per_launch": moved,
+            "bytes_source": ("ncu dram__bytes_read.sum + dram__bytes_write.sum of this build (%s)" % tsrc) if traffic
+            else "compulsory bytes as implemented (8 arrays x %d B per cell per pass; no ncu capture of this build)"
+            % es,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in pk else "fallback",
+            "kernel_src_sha": kernel_source_sha(),
             "algorithmic_bytes_per_launch": alg_bytes, "steps_per_launch": spp,
+            "achieved_algorithmic_gbs": alg_bytes / sweep_avg_s / 1e9,
+            "frac_algorithmic": alg_bytes / sweep_avg_s / 1e9 / peak,
             "implemented_bytes_per_cell_step": info.bytes_per_cell_step,
             "sweep_ms_per_launch": sweep_avg_s * 1e3,
-            "post_ms_per_launch": post_ms / max(nl, 1), "sweep_share_of_step": sweep_ms / max(ms, 1e-9),
-            "frac_of_8TBs_nominal": achieved / 8000.0}
-    if traffic:  # the DRAM bytes the kernel actually moves (ncu) over the same launch time
-        roof["dram_gbs"] = traffic / sweep_avg_s / 1e9
-        roof["dram_frac"] = roof["dram_gbs"] / peak
+            "post_ms_per_launch": post_ms / max(nl, 1), "sweep_share_of_step": sweep_ms / max(ms, 1e-9)}
     cpu = None
     if ws == 1 and not args.no_cpu:
         v, dt, done, sample, cores = oracle_rate(wl, 10 ** 6, max_seconds=args.cpu_seconds)
@@ -348,6 +407,7 @@ def main():
         args.warmup = 3  # timing rule: at least 3 warm-up steps
     if args.impl == "reference":
         return run_reference(args)
+    ensure_ranks(args)
     return run_ours(args)
 
 

@@ -25,9 +25,22 @@
  * fdtd_last_error() gives the text of the last failure of that context.
  * fdtd_step only enqueues work; asynchronous faults (CUDA errors, the
  * non-finite sentinel) surface at the next synchronous call (fdtd_probe,
- * fdtd_energy, fdtd_get_window, fdtd_sync).
+ * fdtd_energy, fdtd_get_window, fdtd_get_rom_state, fdtd_sync).  The
+ * non-finite sentinel ("instability detected") is a device
+ * flag set at the end of every pass when a recorded energy value W^n (which
+ * sums the square of every field value and ROM state), one of 256 Hz cells
+ * sampled on a fixed stride pattern of the pass's output, or a stored ROM state
+ * is not finite; it is sticky and turns every later synchronous call into
+ * FDTD_E_UNSTABLE.
  *
  * Threading: a context is single-threaded; several contexts may coexist.
+ *
+ * Several ranks (nranks > 1, one process per GPU over NCCL): fdtd_create,
+ * fdtd_add_rom, fdtd_set_probes, fdtd_set_pml, fdtd_set_time_blocking,
+ * fdtd_step, fdtd_probe, fdtd_energy and fdtd_sync are collective -- every rank
+ * calls them, in the same order (fdtd_add_rom with count 0 on a rank that owns
+ * none of a model's instances); their validity checks are agreed over the ranks
+ * so that all ranks fail together.  The other calls are rank-local.
  */
 #ifndef FDTDROM_H
 #define FDTDROM_H
@@ -92,7 +105,12 @@ typedef struct {
 /* Create a context: validates the descriptor, builds the per-edge update
  * coefficients of eq:updateEx (L209-214) on the device, allocates the fields
  * (zero) and checks dt against eq.(1) (L36-38) with c_max = c0/sqrt(min eps_r).
- * FDTD_E_UNSTABLE if dt exceeds eq.(1) and FDTD_ALLOW_DT_ABOVE_EQ1 is not set. */
+ * FDTD_E_UNSTABLE if dt exceeds eq.(1) and FDTD_ALLOW_DT_ABOVE_EQ1 is not set.
+ * Device materials (FDTD_MATERIALS_ON_DEVICE) must be ready on desc->stream (the copy is
+ * ordered on that stream only).  With NCCL ranks the communicator is created first and the
+ * global minimum eps_r / sigma (over all ranks' rows) decides the eq.(1) check on every rank;
+ * FDTD_E_ARG (on every rank) if a slab holds fewer than 4 rows (the deepest pass sends 4 owned
+ * rows to each neighbour). */
 fdtd_status fdtd_create(const fdtd_grid_desc *desc, fdtd_ctx **out);
 
 /* One reduced model, as emitted by the ROM generator (fp64, row-major, host):
@@ -200,6 +218,8 @@ typedef struct {
   double bytes_per_cell_step;  /* HBM bytes of the sweep per cell-step as implemented       */
   int32_t steps_per_pass;      /* time steps per sweep pass in use (1, 2 or 4)              */
   void *sweep_stream;          /* cudaStream_t the kernels are launched on                 */
+  int64_t graph_builds;        /* CUDA graphs captured so far (a new source window on the same
+                                  cells, or a new probe/energy read, keeps the graph)          */
 } fdtd_info;
 fdtd_status fdtd_get_info(const fdtd_ctx *c, fdtd_info *out);
 
@@ -236,6 +256,18 @@ fdtd_status fdtd_set_pml(fdtd_ctx *c, int32_t width, int32_t order, double r0);
 
 /* Tuning knobs for the fused sweep (rows per CTA, warps per CTA); 0 keeps default. */
 fdtd_status fdtd_set_tuning(fdtd_ctx *c, int32_t rows_per_cta, int32_t warps_per_cta);
+
+/* Halo plan of one K-step pass (no paper counterpart -- the row-slab
+ * decomposition of north_star (4)): the rows rank `rank` of `nranks` (owning global cell rows
+ * and Ex edge rows [row_begin, row_end)) sends to and receives from its neighbours before a pass
+ * of `depth` (1..4) steps, in the order both transports pair them.  Host-only (no context, no
+ * device).  out[4k .. 4k+3] = {direction (0 send, 1 receive), array (0 Ex edge row, 1 Ey cell
+ * row, 2 Hz cell row; with pml != 0 also 3 / 4 psi_ey of the left / right CPML layer and 5 / 6
+ * psi_hz), global row, peer rank}; sends first, then receives; *n = number of entries.
+ * FDTD_E_ARG on bad sizes, a slab shorter than 4 rows with nranks > 1, or cap < *n (then *n
+ * still holds the count). */
+fdtd_status fdtd_halo_plan(int32_t nranks, int32_t rank, int64_t row_begin, int64_t row_end, int32_t depth,
+                           int32_t pml, int64_t *out, int32_t cap, int32_t *n);
 
 /* Fill out[128] with a fresh ncclUniqueId (rank 0 calls it and broadcasts the bytes, e.g. with
  * torch.distributed.broadcast).  FDTD_E_NCCL if libnccl.so.2 cannot be loaded. */

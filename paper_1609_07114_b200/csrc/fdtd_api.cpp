@@ -61,7 +61,7 @@ struct Nccl {
   }
 };
 Nccl g_nccl;
-constexpr int NCCL_I32 = 2, NCCL_F32 = 7, NCCL_F64 = 8, NCCL_SUM = 0, NCCL_MIN = 3;
+constexpr int NCCL_I32 = 2, NCCL_F32 = 7, NCCL_F64 = 8, NCCL_SUM = 0, NCCL_MAX = 2, NCCL_MIN = 3;
 
 struct ModelHost {
   int bx, by, nY, q1, q2;
@@ -99,7 +99,10 @@ struct fdtd_ctx {
   int chunk = 64, warps = 4;
   // source
   double* d_src = nullptr;
-  int64_t src_n = 0, src_t0 = 0, src_i = -1, src_j = -1, src_j1 = -1, src_cap = 0;  // cells (i, j .. j1-1)
+  int64_t* d_src_meta = nullptr;  // {t0, n} of the sample window (device: graphs survive a new window)
+  int64_t h_src_meta[2] = {0, 0};
+  int64_t src_i = -1, src_j = -1, src_j1 = -1, src_cap = 0;  // cells (i, j .. j1-1)
+  int* d_flag = nullptr;          // non-finite sentinel (sticky; read at the synchronous calls)
   // probes & energy rings
   int64_t cap = 65536;
   int n_probe = 0;
@@ -149,6 +152,7 @@ struct fdtd_ctx {
   bool graph_dirty = true;
   int graph_steps = 0;
   int64_t graph_launches = 0;
+  int64_t graph_builds = 0;
   int64_t launches = 0;
   // profiling (event pairs around each launch)
   bool profiling = false;
@@ -246,7 +250,7 @@ fdtd::SweepParams<T> sweep_params(fdtd_ctx* c, int q) {
   p.src_row = src_here ? (int)lrow(c, sj0) : -1;
   p.src_row_end = src_here ? (int)lrow(c, sj1) : -1;
   p.src_col = src_here ? c->src_i : -1;
-  p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
+  p.src_samples = c->d_src; p.src_meta = c->d_src_meta;
   p.step = c->d_step;
   p.partials = c->energy_on ? c->d_partials : nullptr;
   p.pstride = c->n_partials;
@@ -294,7 +298,7 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
   p.src_row = src_here ? (int)lrow(c, sj0) : -1;
   p.src_row_end = src_here ? (int)lrow(c, sj1) : -1;
   p.src_col = src_here ? c->src_i : -1;
-  p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
+  p.src_samples = c->d_src; p.src_meta = c->d_src_meta;
   p.rom_partials = c->d_rom_partials;
   p.level1 = c->d_level1;
   p.step = c->d_step;
@@ -302,6 +306,7 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
   p.batch_tab = c->d_batch_tab;
   p.block = c->post_threads;
   p.smem_bytes = c->post_smem;
+  p.flag = c->d_flag;
   return p;
 }
 
@@ -314,7 +319,7 @@ inline char* psi_base(const fdtd_ctx* c, int e, int q, int side) {
 template <typename T>
 T* psi_buf(const fdtd_ctx* c, int e, int q) { return (T*)psi_base(c, e, q, 0); }
 
-fdtd::FinParams fin_params(fdtd_ctx* c, int K) {
+fdtd::FinParams fin_params(fdtd_ctx* c, int K, int q) {
   fdtd::FinParams f{};
   f.sweep_partials = c->d_partials;  // exactly the partials the matching sweep / band launches wrote
   f.n_sweep_partials = (int64_t)sweep_gx(c, K) * ((c->rows + c->chunk - 1) / c->chunk) +
@@ -326,6 +331,8 @@ fdtd::FinParams fin_params(fdtd_ctx* c, int K) {
   f.energy_ring = c->d_energy_ring; f.cap = c->cap;
   f.step = c->d_step; f.done = c->d_done;
   f.K = K; f.energy = c->energy_on;
+  f.hz = c->f[1 - q][2]; f.pitch = c->pitch; f.nx = c->d.nx; f.row0 = ROW0; f.rows = c->rows; f.es = (int)c->es;
+  f.flag = c->d_flag;
   return f;
 }
 
@@ -353,7 +360,7 @@ fdtd::PmlParams<T> pml_params(fdtd_ctx* c, int q) {
   p.src_row = src_here ? (int)lrow(c, sj0) : -1;
   p.src_row_end = src_here ? (int)lrow(c, sj1) : -1;
   p.src_col = src_here ? c->src_i : -1;
-  p.src_samples = c->d_src; p.src_n = c->src_n; p.src_t0 = c->src_t0;
+  p.src_samples = c->d_src; p.src_meta = c->d_src_meta;
   p.step = c->d_step;
   p.n_probe = c->d_probe_gi ? c->n_probe : 0;
   p.probe_gi = c->d_probe_gi; p.probe_lr = c->d_probe_lr; p.probe_ring = (T*)c->d_probe_ring; p.cap = c->cap;
@@ -370,12 +377,12 @@ fdtd::PmlParams<T> pml_params(fdtd_ctx* c, int q) {
 // With CPML layers (NEXT-2) the psi rows travel with the field they belong to: psi_ey (a = 3, 4:
 // left / right side) with Ey, psi_hz (a = 5, 6) with Hz.
 struct HaloRow { int a; int64_t row; int peer; };
-void halo_plan(const fdtd_ctx* c, int depth, std::vector<HaloRow>& sends, std::vector<HaloRow>& recvs) {
+void halo_plan_rows(int nranks, int rank, int64_t rows, int depth, bool pml, std::vector<HaloRow>& sends,
+                    std::vector<HaloRow>& recvs) {
   sends.clear();
   recvs.clear();
-  const int up = c->d.rank + 1, dn = c->d.rank - 1;
-  const int64_t top = ROW0 + c->rows;  // first row above the slab
-  const bool pml = c->pml_w > 0;
+  const int up = rank + 1, dn = rank - 1;
+  const int64_t top = ROW0 + rows;  // first row above the slab
   auto push = [&](std::vector<HaloRow>& v, int a, int64_t r, int peer) {
     v.push_back({a, r, peer});
     if (pml && a == 1) { v.push_back({3, r, peer}); v.push_back({4, r, peer}); }
@@ -390,7 +397,7 @@ void halo_plan(const fdtd_ctx* c, int depth, std::vector<HaloRow>& sends, std::v
       }
     }
   };
-  if (up < c->d.nranks) {
+  if (up < nranks) {
     for (int64_t r = top - depth; r < top; ++r)
       for (int a = 0; a < 3; ++a) push(sends, a, r, up);
     down_list(top, up, recvs);  // rows above the slab come from rank g+1's bottom rows
@@ -400,6 +407,9 @@ void halo_plan(const fdtd_ctx* c, int depth, std::vector<HaloRow>& sends, std::v
       for (int a = 0; a < 3; ++a) push(recvs, a, r, dn);
     down_list(ROW0, dn, sends);
   }
+}
+void halo_plan(const fdtd_ctx* c, int depth, std::vector<HaloRow>& sends, std::vector<HaloRow>& recvs) {
+  halo_plan_rows(c->d.nranks, c->d.rank, c->rows, depth, c->pml_w > 0, sends, recvs);
 }
 
 // device address and element count of halo row (a, r) of buffer q
@@ -547,7 +557,7 @@ fdtd_status enqueue_pass(fdtd_ctx* c, int q, cudaStream_t s, int K) {
   }
   if (prof) CK(cudaEventRecord(e[1], s));
   if (has_fix) post(s);
-  fdtd::launch_finalize(fin_params(c, K), s);  // energy of the K steps, step counter
+  fdtd::launch_finalize(fin_params(c, K, q), s);  // energy of the K steps, step counter
   c->launches += 1;
   if (prof) CK(cudaEventRecord(e[2], s));
   return FDTD_OK;
@@ -578,12 +588,24 @@ fdtd_status build_graph(fdtd_ctx* c) {
   if (e != cudaSuccess) return fail(c, FDTD_E_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
   c->graph_steps = 2 * c->kz;
   c->graph_dirty = false;
+  c->graph_builds += 1;
   return FDTD_OK;
 }
 
-fdtd_status check_async(fdtd_ctx* c) {
+// Synchronous point: CUDA faults, then the non-finite sentinel (include/fdtdrom.h "Errors").
+// collective: with NCCL ranks the sentinel is first max-reduced over ranks, so that every rank
+// of a collective read (fdtd_probe, fdtd_energy) fails together instead of one rank leaving the
+// records' all-reduce.
+fdtd_status check_async(fdtd_ctx* c, bool collective = false) {
+  if (collective && c->d.nranks > 1 && c->comm)
+    NK(g_nccl.AllReduce(c->d_flag, c->d_flag, 1, NCCL_I32, NCCL_MAX, c->comm, c->stream));
+  int flag = 0;
+  CK(cudaMemcpyAsync(&flag, c->d_flag, sizeof flag, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaGetLastError());
+  if (flag)
+    return fail(c, FDTD_E_UNSTABLE, "non-finite field or ROM state detected (by step %lld): the scheme is unstable at "
+                "dt = %g", (long long)c->steps, c->d.dt);
   return FDTD_OK;
 }
 
@@ -942,6 +964,35 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
     for (int k = 0; k < nb; ++k) { emin = std::min(emin, hm[2 * k]); smin = std::min(smin, hm[2 * k + 1]); }
     dfree(c, dm);
   }
+  // a row slab must hold the K rows a K-step pass sends to each neighbour (the halo plan sends
+  // owned rows only)
+  double short_slab = (nranks > 1 && c->rows < KMAX) ? 1.0 : 0.0;
+  if (nranks > 1 && !(d.flags & FDTD_LOCAL_GROUP)) {
+    // The checks below are collective (every rank takes the same decision): the communicator is
+    // created first and the global min eps_r / sigma and the slab check are agreed over the ranks,
+    // so no rank can return while its peers block in ncclCommInitRank or a later collective.
+    if (!g_nccl.load(c->err)) { fdtd_destroy(c); return FDTD_E_NCCL; }
+    nccl_uid id;
+    memcpy(&id, d.nccl_id, sizeof id);
+    if (g_nccl.CommInitRank(&c->comm, nranks, id, d.rank) != 0) { fdtd_destroy(c); return FDTD_E_NCCL; }
+    double hv[3] = {emin, smin, -short_slab};
+    double* dv = (double*)dalloc(c, sizeof hv);
+    if (!dv || cudaMemcpyAsync(dv, hv, sizeof hv, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+        g_nccl.AllReduce(dv, dv, 3, NCCL_F64, NCCL_MIN, c->comm, c->stream) != 0 ||
+        cudaMemcpyAsync(hv, dv, sizeof hv, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess) {
+      fdtd_destroy(c);
+      return FDTD_E_NCCL;
+    }
+    dfree(c, dv);
+    emin = hv[0];
+    smin = hv[1];
+    short_slab = -hv[2];
+  }
+  if (short_slab > 0) {
+    fdtd_destroy(c);
+    return FDTD_E_ARG;
+  }
   if (!(emin > 0) || smin < 0) {
     fail(c, FDTD_E_ARG, "materials must have eps_r > 0 and sigma >= 0");
     fdtd_destroy(c);
@@ -969,21 +1020,22 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
   for (int a = 0; a < 2; ++a)
     if (!(c->coef[a] = dalloc(c, fbytes))) { fdtd_destroy(c); return FDTD_E_NOMEM; }
   c->d_step = (int64_t*)dalloc(c, sizeof(int64_t));
+  c->d_flag = (int*)dalloc(c, sizeof(int));
+  c->d_src_meta = (int64_t*)dalloc(c, 2 * sizeof(int64_t));
   c->d_done = (unsigned*)dalloc(c, sizeof(unsigned) * 4);
   c->d_energy_ring = (double*)dalloc(c, c->cap * sizeof(double));
   c->d_level1 = (double*)dalloc(c, KMAX * sizeof(double));
   c->d_level2 = (double*)dalloc(c, (size_t)KMAX * fdtd::FIN_GRID * sizeof(double));
   c->k_want = c->V;  // deepest pass the vector width allows (4 in fp32, 2 in fp64)
   if (const char* e = getenv("FDTD_K")) c->k_want = std::max(1, atoi(e));
-  if (!c->d_step || !c->d_done || !c->d_energy_ring) { fdtd_destroy(c); return FDTD_E_NOMEM; }
+  if (!c->d_step || !c->d_done || !c->d_energy_ring || !c->d_flag || !c->d_src_meta) {
+    fdtd_destroy(c);
+    return FDTD_E_NOMEM;
+  }
   fdtd_status st = f32 ? build_coefficients<float>(c) : build_coefficients<double>(c);
   if (st != FDTD_OK) { fdtd_destroy(c); return st; }
   fdtd_set_tuning(c, 0, 0);
   if (nranks > 1 && !(d.flags & FDTD_LOCAL_GROUP)) {
-    if (!g_nccl.load(c->err)) { fdtd_destroy(c); return FDTD_E_NCCL; }
-    nccl_uid id;
-    memcpy(&id, d.nccl_id, sizeof id);
-    if (g_nccl.CommInitRank(&c->comm, nranks, id, d.rank) != 0) { fdtd_destroy(c); return FDTD_E_NCCL; }
     if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming) != cudaSuccess) {
@@ -1327,19 +1379,25 @@ fdtd_status fdtd_set_source_line(fdtd_ctx* c, int64_t i, int64_t j0, int64_t j1,
   if (!c) return FDTD_E_ARG;
   if (i < 0 || i >= c->d.nx || j0 < 0 || j1 > c->d.ny || j1 <= j0 || n < 0 || (n > 0 && !samples))
     return fail(c, FDTD_E_ARG, "bad source");
+  // The captured graph bakes the sample pointer and the source cells into its kernels, not the
+  // window {t0, n}: a new window of at most src_cap samples on the same cells (the per-call
+  // pattern of an end-to-end run) keeps the graph.
+  bool regraph = !c->d_src || i != c->src_i || j0 != c->src_j || j1 != c->src_j1;
   if (!c->d_src || n > c->src_cap) {
     if (c->d_src) dfree(c, c->d_src);
     c->src_cap = std::max<int64_t>(n, 1);
     c->d_src = (double*)dalloc(c, c->src_cap * sizeof(double));
     if (!c->d_src) return fail(c, FDTD_E_NOMEM, "source");
+    regraph = true;
   }
   if (n) CK(cudaMemcpyAsync(c->d_src, samples, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  c->src_n = n;
-  c->src_t0 = step0;
+  c->h_src_meta[0] = step0;
+  c->h_src_meta[1] = n;
+  CK(cudaMemcpyAsync(c->d_src_meta, c->h_src_meta, sizeof c->h_src_meta, cudaMemcpyHostToDevice, c->stream));
   c->src_i = i;
   c->src_j = j0;
   c->src_j1 = j1;
-  drop_graph(c);
+  if (regraph) drop_graph(c);
   return FDTD_OK;
 }
 
@@ -1458,7 +1516,7 @@ static fdtd_status read_ring(fdtd_ctx* c, const void* ring, int rows_, size_t es
 
 fdtd_status fdtd_probe(fdtd_ctx* c, double* out, int64_t cap_steps, int64_t* n_steps) {
   if (!c || !n_steps) return FDTD_E_ARG;
-  fdtd_status st = check_async(c);
+  fdtd_status st = check_async(c, true);
   if (st != FDTD_OK) return st;
   const int64_t n = c->steps - c->rd_probe;
   if (n > cap_steps) return fail(c, FDTD_E_ARG, "output holds %lld steps, %lld pending", (long long)cap_steps, (long long)n);
@@ -1479,7 +1537,7 @@ fdtd_status fdtd_probe(fdtd_ctx* c, double* out, int64_t cap_steps, int64_t* n_s
 
 fdtd_status fdtd_energy(fdtd_ctx* c, double* out, int64_t cap, int64_t* n_out) {
   if (!c || !n_out) return FDTD_E_ARG;
-  fdtd_status st = check_async(c);
+  fdtd_status st = check_async(c, true);
   if (st != FDTD_OK) return st;
   const int64_t n = c->energy_on ? c->steps - c->rd_energy : 0;
   if (n > cap) return fail(c, FDTD_E_ARG, "output holds %lld steps, %lld pending", (long long)cap, (long long)n);
@@ -1732,7 +1790,7 @@ fdtd_status fdtd_profile_read(fdtd_ctx* c, double* sweep_ms, double* post_ms, in
 
 fdtd_status fdtd_sync(fdtd_ctx* c) {
   if (!c) return FDTD_E_ARG;
-  return check_async(c);
+  return check_async(c, true);
 }
 
 fdtd_status fdtd_get_info(const fdtd_ctx* c, fdtd_info* o) {
@@ -1748,6 +1806,7 @@ fdtd_status fdtd_get_info(const fdtd_ctx* c, fdtd_info* o) {
   // read Ex, Ey, Hz, mea, msb and write Ex, Ey, Hz once per pass
   o->bytes_per_cell_step = 8.0 * (double)c->es / o->steps_per_pass;
   o->sweep_stream = (void*)c->stream;
+  o->graph_builds = c->graph_builds;
   return FDTD_OK;
 }
 
@@ -1758,6 +1817,27 @@ fdtd_status fdtd_nccl_unique_id(void* out128) {
   nccl_uid id;
   if (g_nccl.GetUniqueId(&id) != 0) return FDTD_E_NCCL;
   memcpy(out128, &id, sizeof id);
+  return FDTD_OK;
+}
+
+fdtd_status fdtd_halo_plan(int32_t nranks, int32_t rank, int64_t row_begin, int64_t row_end, int32_t depth,
+                           int32_t pml, int64_t* out, int32_t cap, int32_t* n) {
+  if (!n || nranks < 1 || rank < 0 || rank >= nranks || row_end - row_begin < 1 || depth < 1 || depth > KMAX ||
+      (nranks > 1 && row_end - row_begin < KMAX) || cap < 0 || (cap > 0 && !out))
+    return FDTD_E_ARG;
+  std::vector<HaloRow> sends, recvs;
+  halo_plan_rows(nranks, rank, row_end - row_begin, depth, pml != 0, sends, recvs);
+  *n = (int32_t)(sends.size() + recvs.size());
+  if (*n > cap) return FDTD_E_ARG;
+  int k = 0;
+  for (int dir = 0; dir < 2; ++dir)
+    for (const HaloRow& x : dir ? recvs : sends) {
+      out[4 * k + 0] = dir;
+      out[4 * k + 1] = x.a;
+      out[4 * k + 2] = row_begin + x.row - ROW0;  // global row (cell row for Ey / Hz / psi, edge row for Ex)
+      out[4 * k + 3] = x.peer;
+      ++k;
+    }
   return FDTD_OK;
 }
 

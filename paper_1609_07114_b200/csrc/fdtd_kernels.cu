@@ -522,8 +522,8 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   for (int s = 0; s < K; ++s) {
     x.g[s] = T(0);
     if (p.src_row >= 0) {
-      const int64_t k = x.step + s - p.src_t0;
-      if (k >= 0 && k < p.src_n) x.g[s] = (T)p.src_samples[k];
+      const int64_t k = x.step + s - p.src_meta[0];
+      if (k >= 0 && k < p.src_meta[1]) x.g[s] = (T)p.src_samples[k];
     }
     x.slot[s] = (x.step + s) % p.cap;
   }
@@ -780,10 +780,14 @@ __device__ void store_rom(const PostParams<T>& p, const RomModelDev& m, int firs
     else ex[e & IDX_MASK] = sy[i * B + b];
   }
   const int nx = m.q1 + m.q2;
+  bool bad = false;
   for (int it = threadIdx.x; it < nx * nb; it += blockDim.x) {
     const int i = it % nx, b = it / nx;
-    p.state[p.state_off[first + b] + i] = sx[i * B + b];
+    const T v = sx[i * B + b];
+    bad |= !isfinite(v);
+    p.state[p.state_off[first + b] + i] = v;
   }
+  if (bad) *p.flag = 1;  // non-finite sentinel (a ROM blow-up reaches the state first)
 }
 
 // K3: the K-step fix-up of one batch (instances of one model).  The sweep advanced every cell K
@@ -1001,8 +1005,8 @@ __global__ void __launch_bounds__(512) postk_kernel(const PostParams<T> p) {
   for (int s = 0; s < K; ++s) {
     g[s] = T(0);
     if (p.src_row >= 0) {
-      const int64_t k = step + s - p.src_t0;
-      if (k >= 0 && k < p.src_n) g[s] = (T)p.src_samples[k];
+      const int64_t k = step + s - p.src_meta[0];
+      if (k >= 0 && k < p.src_meta[1]) g[s] = (T)p.src_samples[k];
     }
   }
   if (b < p.n_batch) fixup_batch<T, K, ENERGY>(p, b, sv, g, step, zsum);
@@ -1049,15 +1053,29 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinParams p) {
   __syncthreads();
   if (!last) return;
   __threadfence();
+  bool bad = false;
   if (p.energy) {
 #pragma unroll 1
     for (int s = 0; s < p.K; ++s) {
       double v = 0.0;
       for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) v += __ldcg(p.level2 + (int64_t)s * gridDim.x + k);
       const double tot = block_sum(v, red);
-      if (threadIdx.x == 0) p.energy_ring[(step + s) % p.cap] = tot;
+      if (threadIdx.x == 0) {
+        p.energy_ring[(step + s) % p.cap] = tot;
+        bad |= !isfinite(tot);  // the storage function sums the square of every field value
+      }
     }
   }
+  // non-finite sentinel: NSAMPLE Hz cells of the pass's output on a fixed stride pattern (a blow-up
+  // is a growing global mode; with the energy recorded every cell is covered above)
+  for (int k = threadIdx.x; k < NSAMPLE && p.rows > 0; k += blockDim.x) {
+    const int64_t r = p.row0 + (int64_t)(((uint64_t)k * 2654435761u + (uint64_t)step) % (uint64_t)p.rows);
+    const int64_t col = (int64_t)(((uint64_t)k * 40503u + (uint64_t)step * 7u) % (uint64_t)p.nx);
+    const int64_t o = r * p.pitch + col;
+    const double v = p.es == 8 ? __ldcg((const double*)p.hz + o) : (double)__ldcg((const float*)p.hz + o);
+    bad |= !isfinite(v);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *p.flag = 1;
   if (threadIdx.x == 0) {
     *p.done = 0u;
     *p.step = step + p.K;
@@ -1129,8 +1147,8 @@ __global__ void __launch_bounds__(256) pml_kernel(const PmlParams<T> p) {
   for (int s = 0; s < K; ++s) {
     T gsrc = T(0);
     if (p.src_row >= 0) {
-      const int64_t k = step + s - p.src_t0;
-      if (k >= 0 && k < p.src_n) gsrc = (T)p.src_samples[k];
+      const int64_t k = step + s - p.src_meta[0];
+      if (k >= 0 && k < p.src_meta[1]) gsrc = (T)p.src_samples[k];
     }
     // ---- H half-step (+ CPML psi_hz, + source, + storage terms of the write-back cells)
     T ea = T(0);

@@ -29,7 +29,9 @@ struct SweepParams {
   int src_row;     // local rows [src_row, src_row_end) of the soft (line) source at column src_col (-1: none)
   int src_row_end;
   int64_t src_col;
-  const double* src_samples; int64_t src_n, src_t0;
+  // src_meta = {t0, n}: the samples cover steps [t0, t0 + n) (device memory, so a new sample
+  // window does not invalidate a captured graph)
+  const double* src_samples; const int64_t* src_meta;
   const int64_t* step;  // device step counter (value n during the pass starting at step n)
   double* partials;     // energy partial per CTA and step: partials[s * pstride + cta] (nullptr: off)
   int64_t pstride;
@@ -79,12 +81,13 @@ struct PostParams {
   const int32_t* zp_off; const int32_t* zp;  // zone probes per instance: (gi, gj, probe index)
   T* probe_ring; int64_t cap;
   T chx, chy, idx, idy, wxy, wh;
-  int src_row, src_row_end; int64_t src_col; const double* src_samples; int64_t src_n, src_t0;
+  int src_row, src_row_end; int64_t src_col; const double* src_samples; const int64_t* src_meta;
   double* rom_partials;            // [s * n_inst + instance]: ROM + zone energy of step n+s
   double* level1;                  // [s * n_batch + batch]: the batch's sum of rom_partials
   const int64_t* step;             // step counter (value n during the pass; finalize advances it)
   int block;         // threads per CTA
   size_t smem_bytes; // dynamic shared memory of the launch (max over batches)
+  int* flag;         // non-finite sentinel: set to 1 when a stored ROM state is not finite
 };
 
 // End of a pass (finalize_kernel, after the sweep, the CPML bands and the fix-up): W^{n+s} as a
@@ -98,7 +101,12 @@ struct FinParams {
   double* energy_ring; int64_t cap;
   int64_t* step; unsigned int* done;
   int K; bool energy;
+  // non-finite sentinel (include/fdtdrom.h "Errors"): the last CTA sets *flag = 1 when an energy
+  // value of the pass or one of NSAMPLE strided Hz cells of the pass's output is not finite
+  const void* hz; int64_t pitch, nx; int row0, rows, es;
+  int* flag;
 };
+constexpr int NSAMPLE = 256;
 void launch_finalize(const FinParams& p, cudaStream_t s);
 
 // CPML band fix-up (NEXT-2): the sweep advances the two x-end layers with the plain Yee update; per
@@ -120,7 +128,7 @@ struct PmlParams {
                                  // neighbours' ghost rows while they write their own)
   int64_t psi_rows;              // rows_alloc
   T chx, chy, idx, idy, wxy, wh, cpsi, dxv;  // cpsi = dt / mu0, dxv = dx
-  int src_row, src_row_end; int64_t src_col; const double* src_samples; int64_t src_n, src_t0;
+  int src_row, src_row_end; int64_t src_col; const double* src_samples; const int64_t* src_meta;
   const int64_t* step;
   int n_probe; const int64_t* probe_gi; const int32_t* probe_lr; T* probe_ring; int64_t cap;
   double* partials; int64_t pstride, poff;  // energy: partials[s * pstride + poff + cta]

@@ -49,7 +49,7 @@ class Info(C.Structure):
     _fields_ = [("steps_taken", C.c_int64), ("n_instances", C.c_int64), ("kernel_launches", C.c_int64),
                 ("pitch", C.c_int64), ("sweep_ctas", C.c_int64), ("graphs", C.c_int32),
                 ("precision", C.c_int32), ("bytes_per_cell_step", C.c_double), ("steps_per_pass", C.c_int32),
-                ("sweep_stream", C.c_void_p)]
+                ("sweep_stream", C.c_void_p), ("graph_builds", C.c_int64)]
 
 
 class RomSpec(C.Structure):  # fdtdrom_build.h
@@ -106,6 +106,7 @@ def lib():
         L.fdtd_set_time_blocking.argtypes = [vp, i32]
         L.fdtd_profile_read.argtypes = [vp, dp, dp, C.POINTER(i64)]
         L.fdtd_nccl_unique_id.argtypes = [vp]
+        L.fdtd_halo_plan.argtypes = [i32, i32, i64, i64, i32, i32, vp, i32, C.POINTER(i32)]
         L.fdtd_last_error.argtypes = [vp]
         L.fdtd_last_error.restype = C.c_char_p
         L.fdtd_status_string.restype = C.c_char_p
@@ -118,7 +119,7 @@ def lib():
         for n in ("create", "add_rom", "set_source", "set_probes", "record_energy", "step", "probe", "energy",
                   "get_window", "set_window", "get_rom_state", "set_rom_state", "sync", "get_info", "set_tuning",
                   "nccl_unique_id", "profile", "profile_read", "step_group", "set_time_blocking",
-                  "set_source_line", "set_pml"):
+                  "set_source_line", "set_pml", "halo_plan"):
             getattr(L, "fdtd_" + n).restype = C.c_int
         _lib = L
     return _lib
@@ -161,6 +162,20 @@ def build_rom(bx, by, r, dx, dy, eps_r, sigma, q, fmax, dt_target=None, cg_tol=0
                                ms_solve=out.ms_solve, ms_orth=out.ms_orth, ms_svd=out.ms_svd))
 
 
+def halo_plan(nranks, rank, row_begin, row_end, depth, pml=False):
+    """fdtd_halo_plan: the rows exchanged before a `depth`-step pass, as an int64 array of
+    (direction 0 send / 1 receive, array, global row, peer) rows, sends first (host only)."""
+    n = C.c_int32(0)
+    lib().fdtd_halo_plan(int(nranks), int(rank), int(row_begin), int(row_end), int(depth), int(bool(pml)), None, 0,
+                         C.byref(n))
+    out = np.zeros((max(n.value, 1), 4), dtype=np.int64)
+    st = lib().fdtd_halo_plan(int(nranks), int(rank), int(row_begin), int(row_end), int(depth), int(bool(pml)),
+                              _ptr(out), n.value, C.byref(n))
+    if st:
+        raise FDTDError(st, "fdtd_halo_plan rejected its arguments")
+    return out[: n.value]
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     st = lib().fdtd_nccl_unique_id(buf)
@@ -198,6 +213,8 @@ class Simulation:
         flags = 0
         if isinstance(eps_r, torch.Tensor):
             assert eps_r.is_cuda and sigma.is_cuda and eps_r.dtype == sigma.dtype
+            # fdtd_create copies them on self.stream: order it after their producer (the current stream)
+            self.stream.wait_stream(torch.cuda.current_stream(self.device))
             self._mat = (eps_r.contiguous(), sigma.contiguous())
             flags |= FDTD_MATERIALS_ON_DEVICE
             if eps_r.dtype == torch.float32:

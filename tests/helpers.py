@@ -141,3 +141,49 @@ def cone_window(scene, box, nsteps, margin=3):
                 W = _union(W, r)
                 changed = True
     return (max(W[0], 0), max(W[1], 0), min(W[2], scene.nx), min(W[3], scene.ny))
+
+
+# ------------------------------------------------------------------ per-instance checks
+def instance_y(m, i0, j0, Ex, Ey, a0=0, b0=0):
+    """The nY interface values y (ports S, N, W, E) of an instance at (i0, j0), read from window
+    arrays whose lower-left cell is (a0, b0)."""
+    bx, by = m["bx"], m["by"]
+    u, v = i0 - a0, j0 - b0
+    return np.concatenate([Ex[v, u:u + bx], Ex[v + by, u:u + bx], Ey[v:v + by, u], Ey[v:v + by, u + bx]])
+
+
+def per_instance_errors(pairs, floor_frac=1e-3):
+    """pairs: list of (got, ref) vectors, one per instance.  Returns (max per-instance relative L2,
+    max per-instance relative max-abs).  Each instance is normalised by its own reference norm,
+    floored at floor_frac of the largest instance's (so that an instance still at rest is not
+    divided by dust): one bad instance among thousands cannot hide in a global norm."""
+    if not pairs:
+        return 0.0, 0.0
+    gl2 = max(np.linalg.norm(r) for _, r in pairs)
+    gmx = max(np.abs(r).max() if r.size else 0.0 for _, r in pairs)
+    l2 = mx = 0.0
+    for g, r in pairs:
+        if r.size == 0:
+            continue
+        d = np.asarray(g, np.float64) - np.asarray(r, np.float64)
+        l2 = max(l2, np.linalg.norm(d) / max(np.linalg.norm(r), floor_frac * gl2, 1e-300))
+        mx = max(mx, np.abs(d).max() / max(np.abs(r).max(), floor_frac * gmx, 1e-300))
+    return float(l2), float(mx)
+
+
+def split_states(scene, xs):
+    """Split a concatenated ROM state vector into per-instance vectors (ordered_instances order)."""
+    out, o = [], 0
+    for m, _, _ in ordered_instances(scene):
+        q = m["q1"] + m["q2"]
+        out.append(np.asarray(xs[o:o + q]))
+        o += q
+    return out
+
+
+def instance_pairs(scene, Wg, Wo, xg, xo):
+    """Per-instance (got, ref) pairs of x~ and of y for whole-grid windows Wg, Wo = (Ex, Ey, Hz)."""
+    px = list(zip(split_states(scene, xg), split_states(scene, xo)))
+    py = [(instance_y(m, i0, j0, Wg[0], Wg[1]), instance_y(m, i0, j0, Wo[0], Wo[1]))
+          for m, i0, j0 in ordered_instances(scene)]
+    return px, py

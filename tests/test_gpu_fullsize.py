@@ -168,3 +168,114 @@ def test_full_grid_first_200_steps(name):
     g.close()
     o.close()
     torch.cuda.empty_cache()
+
+
+def _clusters(scene, k=3, count=2):
+    """Boxes (footprint + ring + 2) around clusters of k ROM instances: an instance and its k-1
+    nearest neighbours, one cluster near the grid's centre and one near its south-west quarter."""
+    P = np.asarray(scene.placements)
+    byx = np.array([[scene.models[m]["bx"], scene.models[m]["by"]] for m in P[:, 0]])
+    c = P[:, 1:3] + byx / 2.0
+    out = []
+    for tx, ty in [(0.5, 0.5), (0.25, 0.3)][:count]:
+        a = int(np.argmin(np.hypot(c[:, 0] - tx * scene.nx, c[:, 1] - ty * scene.ny)))
+        near = np.argsort(np.hypot(c[:, 0] - c[a, 0], c[:, 1] - c[a, 1]))[:k]
+        x0 = min(P[t, 1] for t in near) - 3
+        y0 = min(P[t, 2] for t in near) - 3
+        x1 = max(P[t, 1] + byx[t, 0] for t in near) + 3
+        y1 = max(P[t, 2] + byx[t, 1] for t in near) + 3
+        out.append(((int(x0), int(y0), int(x1), int(y1)), [int(t) for t in near]))
+    return out
+
+
+@pytest.mark.parametrize("name", ["cfg4", "cfg5"])
+def test_full_size_first_200_steps_rom_clusters(name):
+    """BASELINE configs 4 (32768^2, 4096 instances) and 5 (49152^2, 8192 instances of 32 models) at
+    full size, in bench.py's launch configuration (K = 4 passes, CUDA graphs): the first 200 steps
+    of two clusters of >= 3 ROM instances each, from random fields and random consistent ROM states
+    (R26), against the fp64 oracle run on each cluster's 200-step dependency cone.  Fields in the
+    clusters <= 1e-4; every instance's x~ and y <= 1e-4 (relative L2, own norm) and <= 1e-3
+    (relative max-abs)."""
+    import torch
+
+    from helpers import instance_y, ordered_instances, per_instance_errors
+    from paper_1609_07114_b200 import Simulation
+
+    n_steps = 200
+    scene = configs.make(name, device="cuda")
+    sim = Simulation(scene.nx, scene.ny, scene.dx, scene.dy, scene.dt, scene.eps_r, scene.sigma,
+                     precision=scene.precision)
+    for k, m in enumerate(scene.models):
+        sel = scene.placements[scene.placements[:, 0] == k]
+        if len(sel):
+            sim.add_rom(m, sel[:, 1:3])
+    sim.set_source(*scene.source, scene.samples)
+    inst = ordered_instances(scene)  # the order of get_rom_state
+    where = {(i0, j0): t for t, (_, i0, j0) in enumerate(inst)}
+    qs = [m["q1"] + m["q2"] for m, _, _ in inst]
+    offs = np.cumsum([0] + qs)
+    xs_all = np.zeros(offs[-1])
+    rng = np.random.default_rng(5)
+    cl = _clusters(scene)
+    wins = [cone_window(scene, box, n_steps) for box, _ in cl]
+    a, b = wins
+    assert not (a[0] < b[2] and b[0] < a[2] and a[1] < b[3] and b[1] < a[3]), "windows overlap"
+    runs = []
+    for (box, near), W in zip(cl, wins):
+        a0, b0, a1, b1 = W
+        Ex, Ey, Hz = _random_window(rng, W, None)
+        _zero_rom_parts(scene, W, Ex, Ey, Hz, scene.nx, scene.ny)
+        inside = []  # instances whose footprint + ring lies in the window (the oracle embeds them)
+        for m, i0, j0 in inst:
+            if a0 <= i0 - 1 and i0 + m["bx"] + 1 <= a1 and b0 <= j0 - 1 and j0 + m["by"] + 1 <= b1:
+                t = where[(i0, j0)]
+                xt = rng.standard_normal(qs[t])
+                xt[m["q1"]:] /= 377.0
+                y = m["L"].T @ xt[:m["q1"]]
+                bx, by = m["bx"], m["by"]
+                u, v = i0 - a0, j0 - b0
+                Ex[v, u:u + bx], Ex[v + by, u:u + bx] = y[:bx], y[bx:2 * bx]
+                Ey[v:v + by, u], Ey[v:v + by, u + bx] = y[2 * bx:2 * bx + by], y[2 * bx + by:]
+                xs_all[offs[t]:offs[t + 1]] = xt
+                inside.append((m, i0, j0, t))
+        assert all(any(t == x[3] for x in inside) for t in near)
+        sim.set_window(a0, b0, Ex, Ey, Hz)
+        runs.append((Ex, Ey, Hz, inside))
+    sim.set_rom_state(xs_all)
+    sim.step(n_steps)
+    xg_all = sim.get_rom_state()
+    for (box, near), W, (Ex, Ey, Hz, inside) in zip(cl, wins, runs):
+        a0, b0, a1, b1 = W
+        eps = scene.eps_r[b0:b1, a0:a1].double().cpu().numpy()
+        sig = scene.sigma[b0:b1, a0:a1].double().cpu().numpy()
+        o = O.OracleSim(a1 - a0, b1 - b0, scene.dx, scene.dy, scene.dt, eps, sig)
+        for m, i0, j0, t in inside:
+            o.add_rom(m, i0 - a0, j0 - b0)
+        sx, sy = scene.source
+        if a0 <= sx < a1 and b0 <= sy < b1:
+            o.set_source(sx - a0, sy - b0, scene.samples)
+        o.set_state(Ex, Ey, Hz, np.concatenate([xs_all[offs[t]:offs[t + 1]] for *_, t in inside]))
+        o.step(n_steps, probes=False, energy=False)
+        Exo, Eyo, Hzo, xo = o.get_state()
+        i0, j0, i1, j1 = box
+        gEx, gEy, gHz = sim.get_window(i0, j0, i1 - i0, j1 - j0)
+        e = [rel(gHz, Hzo[j0 - b0:j1 - b0, i0 - a0:i1 - a0]),
+             rel(gEx, Exo[j0 - b0:j1 - b0 + 1, i0 - a0:i1 - a0]),
+             rel(gEy, Eyo[j0 - b0:j1 - b0, i0 - a0:i1 - a0 + 1])]
+        xo_split, o_off = {}, 0
+        for m, ii, jj, t in inside:
+            xo_split[t] = xo[o_off:o_off + qs[t]]
+            o_off += qs[t]
+        px, py = [], []
+        for t in near:
+            m, ii, jj = inst[t]
+            px.append((xg_all[offs[t]:offs[t + 1]], xo_split[t]))
+            py.append((instance_y(m, ii, jj, gEx, gEy, i0, j0), instance_y(m, ii, jj, Exo, Eyo, a0, b0)))
+        ex = per_instance_errors(px, floor_frac=0.0)
+        ey = per_instance_errors(py, floor_frac=0.0)
+        print("%s cluster %s window %s instances %d fields %s x~ %s y %s" % (name, box, W, len(inside), e, ex, ey))
+        assert len(near) >= 3 and max(e) <= 1e-4, (name, box, e)
+        assert ex[0] <= 1e-4 and ey[0] <= 1e-4 and ex[1] <= 1e-3 and ey[1] <= 1e-3, (name, box, ex, ey)
+    sim.close()
+    del scene
+    torch.cuda.empty_cache()

@@ -11,7 +11,7 @@ from inputs import configs
 from inputs import romgen as rg
 from inputs import scene as sc
 
-from helpers import consistent_random_state, gpu_from_scene, oracle_from_scene, rel
+from helpers import consistent_random_state, gpu_from_scene, instance_pairs, oracle_from_scene, per_instance_errors, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -35,13 +35,21 @@ def _compare(scene, n, tol, energy=True, random_init=None, tuning=None, **kw):
     po, eo = o.step(n, energy=energy)
     Exo, Eyo, Hzo, xo = o.get_state()
     errs = dict(probe=rel(pg, po), Ex=rel(Exg, Exo), Ey=rel(Eyg, Eyo), Hz=rel(Hzg, Hzo))
+    maxabs = {}
     if xo.size:
         errs["rom"] = rel(xg, xo)
+        # per instance: x~ and the interface values y, each against its own norm (a global norm
+        # would hide one bad instance among many); max-abs within 10x the L2 bar
+        px, py = instance_pairs(scene, (Exg, Eyg, Hzg), (Exo, Eyo, Hzo), xg, xo)
+        errs["rom_inst"], maxabs["rom_inst"] = per_instance_errors(px)
+        errs["y_inst"], maxabs["y_inst"] = per_instance_errors(py)
     if energy:
         errs["energy"] = rel(eg, eo)
     g.close()
+    print("errs", errs, "per-instance max-abs", maxabs)
     bad = {k: v for k, v in errs.items() if not v <= tol}
-    assert not bad, errs
+    bad.update({k: v for k, v in maxabs.items() if not v <= 10 * tol})
+    assert not bad, (errs, maxabs)
     return errs, (eg if energy else None)
 
 
@@ -122,16 +130,20 @@ def test_graph_and_eager_paths_agree():
     assert np.array_equal(a.energy(), b.energy())
 
 
-@pytest.mark.parametrize("name,n", [("cfg2", 256), ("cfg3", 512)])
+@pytest.mark.parametrize("name,n", [("cfg2", 256), ("cfg3", 512), ("cfg4", 1024)])
 def test_fp32_crops_2000_steps(name, n):
-    """Seeded cropped sub-instances of configs 2 and 3, fp32, first 2000 steps: <= 1e-4."""
+    """Seeded cropped sub-instances of configs 2, 3 and 4 (the headline config: 1024^2 with 4
+    instances of its q = 128 model), fp32, first 2000 steps: <= 1e-4, per instance too."""
     s = configs.make(name, n=n)
-    _compare(s, 2000, 1e-4, random_init=7 if name == "cfg3" else None)
+    if name == "cfg4":
+        assert len(s.placements) >= 4 and s.models[0]["q1"] + s.models[0]["q2"] == 128
+    _compare(s, 2000, 1e-4, random_init=None if name == "cfg2" else 7)
 
 
-def test_fp32_energy_non_increasing_source_free():
+@pytest.mark.parametrize("name,n", [("cfg3", 256), ("cfg4", 1024)])
+def test_fp32_energy_non_increasing_source_free(name, n):
     """Q24: source-free, the fp32 GPU trace never rises by more than 1e-6 relative per step."""
-    s = configs.make("cfg3", n=256)
+    s = configs.make(name, n=n)
     g = gpu_from_scene(s, source=False)
     Ex, Ey, Hz, xs = consistent_random_state(s, 21)
     g.set_window(0, 0, Ex, Ey, Hz)
