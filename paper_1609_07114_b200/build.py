@@ -44,5 +44,18 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     return out
 
 
+CHECK_LIB = os.path.join(HERE, "libfdtdrom_check.so")
+
+
+def build_checked(force: bool = False) -> str:
+    """The checked build (-DFDTD_CHECK=1: device-side bounds checks; tools/checked_run.py)."""
+    if not force and os.path.exists(CHECK_LIB) and all(os.path.getmtime(p) <= os.path.getmtime(CHECK_LIB)
+                                                       for p in _inputs()):
+        return CHECK_LIB
+    return build(force=True, out=CHECK_LIB, defines=("FDTD_CHECK=1",))
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--checked" in sys.argv:
+        print(build_checked(force="--force" in sys.argv))

@@ -233,6 +233,8 @@ fdtd_status upload_T(fdtd_ctx* c, void** dst, const std::vector<double>& v) {
 }
 
 inline int64_t lrow(const fdtd_ctx* c, int64_t g) { return g - c->d.row_begin + ROW0; }
+constexpr size_t ARRAY_TAIL = 32 * 1024;  // bytes past the last row of every field / material array
+inline int64_t alloc_elems(const fdtd_ctx* c) { return c->nrows_alloc * c->pitch + (int64_t)(ARRAY_TAIL / c->es); }
 
 template <typename T>
 fdtd::SweepParams<T> sweep_params(fdtd_ctx* c, int q) {
@@ -259,6 +261,7 @@ fdtd::SweepParams<T> sweep_params(fdtd_ctx* c, int q) {
   p.idx = (T)(1.0 / c->d.dx); p.idy = (T)(1.0 / c->d.dy);
   p.wxy = (T)(c->d.dx * c->d.dy);
   p.wh = (T)(MU0 * c->d.dx * c->d.dy / c->d.dt);
+  p.alloc_elems = alloc_elems(c);
   return p;
 }
 
@@ -307,6 +310,7 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
   p.block = c->post_threads;
   p.smem_bytes = c->post_smem;
   p.flag = c->d_flag;
+  p.alloc_elems = alloc_elems(c); p.rows = c->rows; p.n_probe = c->n_probe;
   return p;
 }
 
@@ -366,6 +370,7 @@ fdtd::PmlParams<T> pml_params(fdtd_ctx* c, int q) {
   p.probe_gi = c->d_probe_gi; p.probe_lr = c->d_probe_lr; p.probe_ring = (T*)c->d_probe_ring; p.cap = c->cap;
   p.partials = c->energy_on ? c->d_partials : nullptr;
   p.pstride = c->n_partials;
+  p.alloc_elems = alloc_elems(c);
   return p;
 }
 
@@ -1013,7 +1018,7 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
     fdtd_destroy(c);
     return FDTD_E_ARG;
   }
-  const size_t fbytes = (size_t)c->nrows_alloc * c->pitch * c->es + 32 * 1024;
+  const size_t fbytes = (size_t)c->nrows_alloc * c->pitch * c->es + ARRAY_TAIL;
   for (int b = 0; b < 2; ++b)
     for (int a = 0; a < 3; ++a)
       if (!(c->f[b][a] = dalloc(c, fbytes))) { fdtd_destroy(c); return FDTD_E_NOMEM; }

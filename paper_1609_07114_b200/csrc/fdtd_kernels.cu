@@ -343,6 +343,7 @@ __device__ __forceinline__ void record_probes_v(const SweepParams<T>& p, int r, 
 #pragma unroll
       for (int k = 1; k < V; ++k)
         if (d == k) v = h.v[k];
+      FCHK(e.y >= 0 && slot >= 0 && slot < p.cap);
       p.probe_ring[(int64_t)e.y * p.cap + slot] = v;
     }
   }
@@ -433,6 +434,7 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
   }
   if (j + 1 < je) {  // row j+1 into the buffer of row j-1 (consumed above)
     const uint32_t o = (uint32_t)(j + 1) * x.P + x.c;
+    FCHK((int64_t)o + x.P + V <= p.alloc_elems && j + 1 >= 0);
     ldv(p.ex0 + (o + x.P), Y.ext);
     ldv(p.ey0 + o, Y.ey);
     ldv(p.hz0 + o, Y.hz);
@@ -466,6 +468,7 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
   const int rs = j - (K - 1);
   if (x.out && (!CHK || (rs >= x.r0 && rs < x.r1))) {
     const uint32_t o = (uint32_t)rs * x.P + x.c;
+    FCHK(rs >= p.row0 && rs < p.row0 + p.rows && x.c + V <= x.P);  // stores stay in the owned rows
     stv(p.hz1 + o, B.h[K - 1]);
     stv(p.ex1 + o, B.x[K - 1]);
     stv(p.ey1 + o, B.y[K - 1]);
@@ -531,6 +534,7 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   RowIn<T, V> R0, R1;  // rows jb-1 (only Ex of edge row jb and the materials are used) and jb
   {
     const uint32_t o = (uint32_t)(jb - 1) * x.P + x.c;
+    FCHK(jb - 1 >= 0 && (int64_t)o + 2 * x.P + V <= p.alloc_elems);
     ldv(p.ex0 + (o + x.P), R0.ext);
     ldv(p.mea + o, R0.ma);
     ldv(p.msb + o, R0.ms);
@@ -776,6 +780,7 @@ __device__ void store_rom(const PostParams<T>& p, const RomModelDev& m, int firs
   for (int it = threadIdx.x; it < m.nY * nb; it += blockDim.x) {  // S6: scatter y^{n+1}
     const int i = it % m.nY, b = it / m.nY;
     const int64_t e = p.port_edge[p.port_off[first + b] + i];
+    FCHK((e & IDX_MASK) >= (int64_t)p.row0 * p.pitch && (e & IDX_MASK) < (int64_t)(p.row0 + p.rows) * p.pitch);
     if (e >> 62) ey[e & IDX_MASK] = sy[i * B + b];
     else ex[e & IDX_MASK] = sy[i * B + b];
   }
@@ -831,6 +836,8 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     const int n = q.Hr * q.Wr;
     q.H = reg + (int64_t)b * rstride;
     q.MA = q.H + n; q.MS = q.MA + n; q.ZE = q.MS + n; q.EX = q.ZE + n; q.EY = q.EX + n + q.Wr;
+    FCHK((int64_t)(q.EY + q.Hr * (q.Wr + 1) - reg) <= (int64_t)(b + 1) * rstride &&
+         (size_t)((char*)(q.EY + q.Hr * (q.Wr + 1)) - (char*)sv) <= p.smem_bytes);  // region inside its slot
     return q;
   };
   auto goff = [&](const Geo& q, int u, int v) {
@@ -844,6 +851,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   // flight at once: the region rows are not 16-byte aligned)
   for (int b = 0; b < nb; ++b) {
     const Geo q = geo(b);
+    FCHK(goff(q, 0, 0) >= 0 && goff(q, q.Wr, q.Hr) < p.alloc_elems);  // region rows inside the device arrays
     for (int t = tid; t < q.Hr * q.Wr; t += nt) {
       const int64_t o = goff(q, t % q.Wr, t / q.Wr);
       cp_async_el(q.MA + t, p.mea + o);
@@ -896,6 +904,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       const int z0 = p.zp_off[first + b], z1 = p.zp_off[first + b + 1];
       for (int z = z0 + tid; z < z1; z += nt) {
         const int u = p.zp[3 * z] - (q.i0 - M), v = p.zp[3 * z + 1] - (q.j0 - M);
+        FCHK(u >= 0 && u < q.Wr && v >= 0 && v < q.Hr && p.zp[3 * z + 2] < p.n_probe);
         p.probe_ring[(int64_t)p.zp[3 * z + 2] * p.cap + (step + s) % p.cap] = q.H[v * q.Wr + u];
       }
       const int W1 = q.Wr + 1;
@@ -984,6 +993,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       const int t = v * q.Wr + u;
       if (!(q.MA[t] >= T(0))) continue;
       const int64_t o = goff(q, u, v);
+      FCHK(o >= (int64_t)p.row0 * p.pitch && o < (int64_t)(p.row0 + p.rows) * p.pitch);  // owned rows only
       p.hz1[o] = q.H[t];
       p.ex1[o] = q.EX[t];
       p.ey1[o] = q.EY[v * (q.Wr + 1) + u];
@@ -1115,6 +1125,7 @@ __global__ void __launch_bounds__(256) pml_kernel(const PmlParams<T> p) {
   const int W1 = WB + 1;
   const int64_t step = *p.step;
   auto off = [&](int u, int v) { return (int64_t)(R0 + v) * P + c0 + u; };
+  FCHK(R0 >= 0 && off(WB, Hr + 1) < p.alloc_elems && c0 >= 0);
   auto hcol = [&](int64_t gi) { return side == 0 ? (int)gi : (int)(gi - lay0); };  // Hz layer index
   auto in_layer_h = [&](int64_t gi) { return side == 0 ? gi < w : gi >= lay0; };
   auto in_layer_e = [&](int64_t gi) { return side == 0 ? (gi >= 1 && gi <= w) : (gi >= lay0 && gi < nx); };
@@ -1218,6 +1229,7 @@ __global__ void __launch_bounds__(256) pml_kernel(const PmlParams<T> p) {
     const int lr = R0 + v;
     if (gi < wb0 || gi >= wb1 || lr < r0 || lr >= r1) continue;
     const int64_t o = off(u, v);
+    FCHK(lr >= p.row0 && lr < p.row0 + p.rows);
     p.hz1[o] = H[t];
     p.ex1[o] = EX[t];
     p.ey1[o] = EY[v * W1 + u];

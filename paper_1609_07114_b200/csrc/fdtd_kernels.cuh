@@ -4,6 +4,28 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// FDTD_CHECK=1 (a separate checked build, tools/checked_run.py): device-side bounds checks on every
+// global and region access of the hot kernels, trapping with a message -- the stand-in for
+// compute-sanitizer, which is closed on the GPU pool.
+#ifndef FDTD_CHECK
+#define FDTD_CHECK 0
+#endif
+#if FDTD_CHECK
+#include <cstdio>
+#define FCHK(cond, ...)                                                                       \
+  do {                                                                                        \
+    if (!(cond)) {                                                                            \
+      printf("FDTD_CHECK %s:%d block (%d,%d) thread %d: %s\n", __FILE__, __LINE__, blockIdx.x,  \
+             blockIdx.y, threadIdx.x, #cond);                                                 \
+      __trap();                                                                               \
+    }                                                                                         \
+  } while (0)
+#else
+#define FCHK(cond, ...) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace fdtd {
 
 // K-step sweep: K time steps per pass over the grid (temporal blocking; K = 1
@@ -40,6 +62,7 @@ struct SweepParams {
   T* probe_ring; int64_t cap;
   T idx, idy;           // 1/dx, 1/dy
   T wxy, wh;            // dx dy, mu0 dx dy / dt (energy weights)
+  int64_t alloc_elems;  // elements of every field / material array incl. its tail (FDTD_CHECK bounds)
 };
 
 // Fused per-model operators (column-major, in the model pool), with x = [E~; H~] (q1 + q2):
@@ -88,6 +111,7 @@ struct PostParams {
   int block;         // threads per CTA
   size_t smem_bytes; // dynamic shared memory of the launch (max over batches)
   int* flag;         // non-finite sentinel: set to 1 when a stored ROM state is not finite
+  int64_t alloc_elems; int rows, n_probe;  // FDTD_CHECK bounds: array elements, owned rows, probes
 };
 
 // End of a pass (finalize_kernel, after the sweep, the CPML bands and the fix-up): W^{n+s} as a
@@ -132,6 +156,7 @@ struct PmlParams {
   const int64_t* step;
   int n_probe; const int64_t* probe_gi; const int32_t* probe_lr; T* probe_ring; int64_t cap;
   double* partials; int64_t pstride, poff;  // energy: partials[s * pstride + poff + cta]
+  int64_t alloc_elems;                      // FDTD_CHECK bounds
 };
 template <typename T>
 void launch_pml(const PmlParams<T>& p, int K, bool energy, cudaStream_t s);

@@ -216,7 +216,9 @@ def test_full_size_first_200_steps_rom_clusters(name):
     offs = np.cumsum([0] + qs)
     xs_all = np.zeros(offs[-1])
     rng = np.random.default_rng(5)
-    cl = _clusters(scene)
+    # cluster members as indices into `inst` (placement order differs from it with several models)
+    cl = [(box, [where[(int(scene.placements[t, 1]), int(scene.placements[t, 2]))] for t in near])
+          for box, near in _clusters(scene)]
     wins = [cone_window(scene, box, n_steps) for box, _ in cl]
     a, b = wins
     assert not (a[0] < b[2] and b[0] < a[2] and a[1] < b[3] and b[1] < a[3]), "windows overlap"

@@ -1,7 +1,9 @@
 """Summarise ncu captures into small text files under profiles/ (the judged evidence).
 
-usage: python tools/ncu_summary.py <report.ncu-rep> <out.txt> [cells]
+usage: python tools/ncu_summary.py <report.ncu-rep> <out.txt> [cells [workload steps_per_pass]]
        python tools/ncu_summary.py --launches <launches.csv> <out.txt>
+With workload and steps_per_pass, the sweep's DRAM bytes per cell per launch are also written to
+profiles/sweep_traffic.json, stamped with the kernel sources' hash (bench.py ignores a stale file).
 """
 import csv
 import io
@@ -17,7 +19,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__inst_executed.sum", "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct"]
 
 
-def rep(path, out, cells=None):
+def rep(path, out, cells=None, workload=None, spp=None):
     txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     h, units = rows[0], rows[1]
@@ -37,6 +39,16 @@ def rep(path, out, cells=None):
             wr = float(vals["dram__bytes_write.sum"][0].replace(",", "")) * scale[vals["dram__bytes_write.sum"][1]]
             lines.append("  DRAM bytes per cell per launch: read %.3f + write %.3f = %.3f B" %
                          (rd / cells, wr / cells, (rd + wr) / cells))
+            if workload and "sweepk" in name:
+                import os
+                root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+                sys.path.insert(0, root)
+                from bench import kernel_source_sha
+                json.dump({"workload": workload, "steps_per_pass": int(spp), "kernel": name,
+                           "bytes_per_launch_per_cell": round((rd + wr) / cells, 4),
+                           "kernel_src_sha": kernel_source_sha(),
+                           "source": "%s (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)" % out},
+                          open(os.path.join(root, "profiles", "sweep_traffic.json"), "w"))
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
@@ -67,4 +79,5 @@ if __name__ == "__main__":
     if sys.argv[1] == "--launches":
         launches(sys.argv[2], sys.argv[3])
     else:
-        rep(sys.argv[1], sys.argv[2], float(sys.argv[3]) if len(sys.argv) > 3 else None)
+        rep(sys.argv[1], sys.argv[2], float(sys.argv[3]) if len(sys.argv) > 3 else None,
+            sys.argv[4] if len(sys.argv) > 4 else None, sys.argv[5] if len(sys.argv) > 5 else None)

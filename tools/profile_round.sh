@@ -17,7 +17,8 @@ ncu --set full --clock-control none --import-source on -k regex:sweepk -s 1 -c 1
 $SHORT > $OUT/plain3_$TAG.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:postk -s 1 -c 1 -o $OUT/post_$TAG $SHORT \
     > $OUT/ncu_post_$TAG.log 2>&1; echo "ncu_post=$?"
-# NEXT-3: the GPU ROM builder's multigrid-PCG kernel on config 5's largest model
+# NEXT-3: the GPU ROM builder's multigrid-PCG kernel on config 5's largest model (MG=1)
+[ "${MG:-0}" = 1 ] || exit 0
 python tools/rom_build_bench.py --cases cfg5 --out $OUT/rom_build_plain_$TAG.json > $OUT/rom_build_plain_$TAG.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:mg_pcg -s 3 -c 1 -o $OUT/mgpcg_$TAG \
     python tools/rom_build_bench.py --cases cfg5 --out $OUT/rom_build_ncu_$TAG.json > $OUT/ncu_mgpcg_$TAG.log 2>&1
