@@ -119,7 +119,7 @@ struct fdtd_ctx {
   int k_want = 4, k_ok = 1, kz = 1, kz_marked = 1;
   bool kz_dirty = true;
   size_t post_smem = 0;  // dynamic shared memory of the fix-up launch
-  int post_threads = 256;
+  int post_threads = 512;
   int32_t* d_rects = nullptr;
   std::vector<int32_t> zp_off, zp;  // zone probes per instance (gi, gj, probe index)
   // CPML on the two x-ends (NEXT-2): width, per-column coefficients, psi state, marked columns
@@ -135,7 +135,7 @@ struct fdtd_ctx {
   std::vector<int32_t> inst_model, rects;  // rects: (i0, j0, bx, by) global
   std::vector<int64_t> port_off, port_edge, state_off, Sk_off;
   std::vector<double> cya, cyg, ehalf, Sk;  // fp64 host copies (converted on upload)
-  std::vector<double> mpool;                // shared model matrices (col-major, fp64)
+  std::vector<double> mpool;                // shared model operators, fp64, tiled for the DMMA GEMMs
   int nvec = 1;
   std::vector<int32_t> batch_tab;  // (model, first instance, count, slots B, region stride)
   int32_t* d_batch_tab = nullptr;
@@ -276,7 +276,7 @@ template <typename T>
 fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
   fdtd::PostParams<T> p{};
   p.n_inst = (int)c->inst_model.size();
-  p.models = c->d_models; p.mpool = (const T*)c->d_mpool;
+  p.models = c->d_models; p.mpool64 = (const double*)c->d_mpool;
   p.Sk = (const T*)c->d_Sk; p.Sk_off = c->d_Sk_off; p.port_off = c->d_port_off;
   p.cya = (const T*)c->d_cya; p.cyg = (const T*)c->d_cyg; p.ehalf = c->d_ehalf;
   p.port_edge = c->d_port_edge;
@@ -660,7 +660,7 @@ fdtd_status upload_roms(fdtd_ctx* c) {
   fdtd_status st;
   std::vector<fdtd::RomModelDev> md;
   for (auto& m : c->models) md.push_back(m.dev);
-  if ((st = upload_T(c, &c->d_mpool, c->mpool)) != FDTD_OK) return st;
+  if ((st = upload(c, reinterpret_cast<double**>(&c->d_mpool), c->mpool)) != FDTD_OK) return st;
   if ((st = upload(c, &c->d_models, md)) != FDTD_OK) return st;
   if ((st = upload(c, &c->d_rects, c->rects)) != FDTD_OK) return st;
   if ((st = upload_T(c, &c->d_Sk, c->Sk)) != FDTD_OK) return st;
@@ -723,6 +723,23 @@ bool passes_valid(const fdtd_ctx* c, int K) {
 
 fdtd_status apply_passes(fdtd_ctx* c, int k);
 
+// Append a row-major (rows x cols) operator to the fp64 pool in the A-fragment order of
+// mma.sync.m8n8k4.f64 (fdtd_kernels.cu dmma_gemm): per 8 x 4 tile (row tile mt, column tile kt, kt
+// fastest) lane l holds A[8 mt + l / 4][4 kt + l % 4]; zero padding outside rows x cols.
+int64_t push_tiles(std::vector<double>& pool, const std::vector<double>& A, int rows, int cols, int& mt, int& kt) {
+  while (pool.size() % 32) pool.push_back(0.0);  // 256-byte aligned tiles
+  const int64_t off = (int64_t)pool.size();
+  mt = (rows + 7) / 8;
+  kt = (cols + 3) / 4;
+  for (int a = 0; a < mt; ++a)
+    for (int b = 0; b < kt; ++b)
+      for (int l = 0; l < 32; ++l) {
+        const int r = 8 * a + l / 4, cc = 4 * b + l % 4;
+        pool.push_back(r < rows && cc < cols ? A[(size_t)r * cols + cc] : 0.0);
+      }
+  return off;
+}
+
 // Zone depth, zone marks, fix-up batches and zone probes for passes of depth kz (all ranks agree
 // on kz: one NCCL min-reduction).  Runs at the first fdtd_step after a configuration change.
 fdtd_status configure_passes(fdtd_ctx* c) {
@@ -736,7 +753,7 @@ fdtd_status configure_passes(fdtd_ctx* c) {
     for (auto& m : c->models) rs = std::max(rs, fdtd::region_elems(m.bx, m.by, 2 * kk - 1));
     return (rs + 3) / 4 * 4;
   };
-  auto fits = [&](int b, int rs, size_t lim) { return fdtd::post_smem_bytes(c->es, c->nvec, b, rs) <= lim; };
+  auto fits = [&](int b, int rs, size_t lim) { return fdtd::post_smem_bytes(c->es, c->nvec, c->nvec, b, rs) <= lim; };
   while (k > 1 && !fits(1, stride_for(k), 220 * 1024)) k /= 2;
   c->k_ok = k;
   if (c->d.nranks > 1 && c->comm) {  // collective min over ranks (all ranks reach this call together)
@@ -794,8 +811,9 @@ fdtd_status apply_passes(fdtd_ctx* c, int k) {
   }
   // batches of consecutive instances of one model (instances are stored grouped by model).  Every
   // model gets its own region stride and batch size under one shared-memory budget per CTA
-  // (~110 KB: two fix-up CTAs per SM), so small models are batched 8 at a time and the largest
-  // still fits; the launch uses the largest batch footprint.
+  // (~220 KB: one 512-thread fix-up CTA per SM; 8 instances fill the DMMA's N = 8), so small
+  // models are batched 8 at a time and the largest still fits; the launch uses the largest batch
+  // footprint.
   {
     // up to 8 instances per CTA; a row slab with few instances uses smaller batches so that the
     // fix-up's CTAs still fill one wave (it is latency-bound)
@@ -808,13 +826,13 @@ fdtd_status apply_passes(fdtd_ctx* c, int k) {
       while (Bauto > 1 && (int64_t)c->inst_model.size() <= (int64_t)(Bauto / 2) * 2 * nsm) Bauto /= 2;
     }
     const int Bmax = env ? std::max(1, std::min(64, atoi(env))) : Bauto;
-    const size_t budget = 110 * 1024;
+    const size_t budget = 220 * 1024;
     struct Shape { int B, stride; size_t per; };
     std::vector<Shape> shp;
     size_t need1 = 0;
     for (auto& m : c->models) {
       const int rs = (fdtd::region_elems(m.bx, m.by, 2 * k - 1) + 3) / 4 * 4;
-      const size_t per = fdtd::post_smem_bytes(c->es, m.q1 + m.q2 + m.nY, 1, rs);
+      const size_t per = fdtd::post_smem_bytes(c->es, m.q1 + m.q2 + m.nY, m.nY, 1, rs);
       shp.push_back({1, rs, per});
       need1 = std::max(need1, per);
     }
@@ -1221,13 +1239,6 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
   } else {
     mh.P = P;
   }
-  auto push = [&](const Mat& A, int rows_, int cols_) {  // row-major host -> column-major pool
-    while (c->mpool.size() % 4) c->mpool.push_back(0.0);   // 16-byte aligned operators (cp.async)
-    const int64_t off = (int64_t)c->mpool.size();
-    for (int j = 0; j < cols_; ++j)
-      for (int i = 0; i < rows_; ++i) c->mpool.push_back(A[(size_t)i * cols_ + j]);
-    return off;
-  };
   Mat R11dt(R11), R22dt(R22);
   for (auto& v : R11dt) v /= dt;
   for (auto& v : R22dt) v /= dt;
@@ -1287,16 +1298,15 @@ fdtd_status fdtd_add_rom(fdtd_ctx* c, const fdtd_rom_model* m, const int32_t* an
       Rt[(size_t)(q1 + j) * nxs + i] = -0.5 * K[(size_t)i * q2 + j];
     }
   mh.dev.nY = nY; mh.dev.q1 = q1; mh.dev.q2 = q2; mh.dev.literal = literal ? 1 : 0;
-  {  // [M1; R~] as one column-major operator (the kernel's first GEMM phase also yields R~ x~)
+  {  // [M1; R~] as one operator (the fix-up's first GEMM phase also yields R~ x~), and M2
     Mat M1R = dense::zeros(m1 + nxs, nxs);
     for (int i = 0; i < m1; ++i)
       for (int j = 0; j < nxs; ++j) M1R[(size_t)i * nxs + j] = M1[(size_t)i * nxs + j];
     for (int i = 0; i < nxs; ++i)
       for (int j = 0; j < nxs; ++j) M1R[(size_t)(m1 + i) * nxs + j] = Rt[(size_t)i * nxs + j];
-    mh.dev.off_M1 = push(M1R, m1 + nxs, nxs);
+    mh.dev.off_M1t = push_tiles(c->mpool, M1R, m1 + nxs, nxs, mh.dev.mt1, mh.dev.kt1);
+    mh.dev.off_M2t = push_tiles(c->mpool, M2, m2, nY, mh.dev.mt2, mh.dev.kt2);
   }
-  mh.dev.off_M2 = push(M2, m2, nY);
-  mh.dev.off_Rt = mh.dev.off_M1 + m1;
   const int mid = (int)c->models.size();
   c->models.push_back(mh);
   c->nvec = std::max(c->nvec, q1 + q2 + nY);

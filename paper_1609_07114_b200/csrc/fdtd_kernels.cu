@@ -637,83 +637,119 @@ __device__ double block_sum(double v, double* red) {
   return s;  // valid in thread 0
 }
 
-// Y[i][b] += alpha * sum_c A[c*m + i] X[c][b] for i < m, b < B.  A is a shared model operator
-// (column-major, L2-resident: one coalesced 128-byte row of A per warp and column, reused for the
-// IPI instances of a thread's item); X, Y in shared memory with row stride B.
-template <typename T, int IPI, bool ACC>
-__device__ __forceinline__ void bgemm_ipi(const T* __restrict__ A, int m, int lda, int k, const T* X, T* Y, int B,
-                                          T alpha) {
-  const int G = B / IPI;
-  for (int it = threadIdx.x; it < m * G; it += blockDim.x) {
-    const int i = it % m, g = (it / m) * IPI;
-    // two interleaved partial sums per output (even / odd c): half the dependent FMA chain
-    T acc[IPI], acc2[IPI];
-#pragma unroll
-    for (int u = 0; u < IPI; ++u) acc[u] = acc2[u] = T(0);
-    int c = 0;
-#pragma unroll 8
-    for (; c + 1 < k; c += 2) {
-      const T a = __ldg(A + (int64_t)c * lda + i), a2 = __ldg(A + (int64_t)(c + 1) * lda + i);
-      const T* x = X + c * B + g;
-#pragma unroll
-      for (int u = 0; u < IPI; ++u) {
-        acc[u] = fma_rn(a, x[u], acc[u]);
-        acc2[u] = fma_rn(a2, x[B + u], acc2[u]);
-      }
-    }
-    if (c < k) {
-      const T a = __ldg(A + (int64_t)c * lda + i);
-      const T* x = X + c * B + g;
-#pragma unroll
-      for (int u = 0; u < IPI; ++u) acc[u] = fma_rn(a, x[u], acc[u]);
-    }
-    T* y = Y + i * B + g;
-#pragma unroll
-    for (int u = 0; u < IPI; ++u) y[u] = ACC ? fma_rn(alpha, acc[u] + acc2[u], y[u]) : mul_rn(alpha, acc[u] + acc2[u]);
-  }
+// ---- tensor-core path of the batched reduced GEMMs: FP64 DMMA (mma.sync.m8n8k4.f64), for fp32
+// and fp64 states alike.  A (a shared model operator) is kept in fp64 in a second pool, pre-tiled
+// in the A-fragment order of the m8n8k4 MMA (fdtd_api.cpp push_tiles): per 8 x 4 tile lane l holds
+// A[l / 4][l % 4] -- one coalesced 8-byte load per lane and tile.  The batch's vectors X (k x B,
+// row stride B; the B instances are the MMA's N = 8 columns) are widened to fp64; products and
+// sums are fp64 and only the result is rounded to the state precision (fp32 states get a more
+// accurate ROM update than fp32 FMAs would give).  Each output column depends on that column only,
+// so a batch's composition never changes an instance's values.
+__device__ __forceinline__ void mma_f64(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
 }
 
-// B (the batch's slot count) is a power of two (fdtd_api.cpp apply_passes), so B / IPI covers it.
-// ACC: Y += alpha A X; else Y = alpha A X (no zeroing pass; identical to accumulating onto zeros)
-template <typename T, bool ACC>
-__device__ __forceinline__ void bgemm(const T* A, int m, int lda, int k, const T* X, T* Y, int B, T alpha) {
-  if (m * (B / 4) >= (int)blockDim.x) bgemm_ipi<T, 4, ACC>(A, m, lda, k, X, Y, B, alpha);
-  else if (m * (B / 2) >= (int)blockDim.x) bgemm_ipi<T, 2, ACC>(A, m, lda, k, X, Y, B, alpha);
-  else bgemm_ipi<T, 1, ACC>(A, m, lda, k, X, Y, B, alpha);
+// Y = A X for rows [0, m): epi(r, c, v) receives element (r, c) in fp64.  A tiled as above with
+// mtiles x ktiles tiles of 8 x 4 (m <= 8 mtiles, k <= 4 ktiles, zero-padded); X in shared memory.
+// One warp per (8-row tile, 8-column tile) job; the k loop keeps UNR tile loads in flight.
+template <typename T, typename Epi>
+__device__ __forceinline__ void dmma_gemm(const double* __restrict__ At, int mtiles, int ktiles, int m, int k,
+                                          const T* X, int B, Epi epi) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int ntiles = (B + 7) >> 3;
+  for (int job = warp; job < mtiles * ntiles; job += nw) {
+    const int mt = job % mtiles, nt = job / mtiles;
+    const int col = nt * 8 + g;  // this lane's B-fragment column (instance slot)
+    const bool cl = col < B;
+    double d[2] = {0.0, 0.0};
+    const double* ap = At + (int64_t)mt * ktiles * 32 + lane;
+    constexpr int UNR = 8;
+    int kt = 0;
+    for (; kt + UNR <= ktiles; kt += UNR) {
+      double a[UNR], b[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) a[u] = __ldg(ap + (kt + u) * 32);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int kk = (kt + u) * 4 + t;
+        b[u] = (cl && kk < k) ? (double)X[kk * B + col] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) mma_f64(d, a[u], b[u]);
+    }
+    for (; kt < ktiles; ++kt) {
+      const int kk = kt * 4 + t;
+      mma_f64(d, __ldg(ap + kt * 32), (cl && kk < k) ? (double)X[kk * B + col] : 0.0);
+    }
+    const int r = mt * 8 + g, c0 = nt * 8 + 2 * t;
+    if (r < m) {
+      if (c0 < B) epi(r, c0, d[0]);
+      if (c0 + 1 < B) epi(r, c0 + 1, d[1]);
+    }
+  }
 }
 
 // Shared-memory vectors of a batch (row stride B, NV rows each):
 //   sx = [E~; H~] (q1 + q2), sy = y (nY), sh = h (nY), so = [M1; R~] x (q2 + q1 + nY + q1 + q2, two
-//   slots), st = t (nY), sU = U (nY), so2 = [E~; y] (q1 + nY)
-constexpr int NROMVEC = 8;  // vector slots of one batch (stride S = (q1 + q2 + nY) x B each)
+//   slots), st = t (nY), sU = U (nY)
+constexpr int NROMVEC = 7;  // vector slots of one batch (stride S = (q1 + q2 + nY) x B each)
 template <typename T>
 struct RomVec {
-  T *sx, *sy, *sh, *so, *st, *sU, *so2;
+  T *sx, *sy, *sh, *so, *st, *sU;
   __device__ RomVec(T* sv, int64_t S) : sx(sv), sy(sv + S), sh(sv + 2 * S), so(sv + 3 * S), st(sv + 5 * S),
-                                         sU(sv + 6 * S), so2(sv + 7 * S) {}
+                                         sU(sv + 6 * S) {}
 };
+// Per-pass constants of a batch, staged in shared memory once per pass (after the vectors):
+// eh = D_l D_l' eps / dt (fp64, storage function), cya, cyg = the t coefficients, per (port, slot)
+// (nYB = nY x B entries each); then zw, the per-warp zone-energy partials ([slot][ZWARPS] fp64).
+constexpr int ZWARPS = 32;
+template <typename T>
+struct RomConst {
+  double* eh; T* cya; T* cyg; double* zw;
+  __device__ RomConst(T* sv, int64_t S, int64_t nYB)
+      : eh(reinterpret_cast<double*>(sv + NROMVEC * S)),
+        cya(sv + NROMVEC * S + nYB * (int64_t)(sizeof(double) / sizeof(T))),
+        cyg(sv + NROMVEC * S + nYB * (int64_t)(sizeof(double) / sizeof(T)) + nYB),
+        zw(reinterpret_cast<double*>(sv + NROMVEC * S + nYB * (int64_t)(sizeof(double) / sizeof(T)) + 2 * nYB)) {}
+};
+template <typename T>
+__device__ __forceinline__ T* rom_end(T* sv, int64_t S, int64_t nYB, int B) {
+  // first free element after the ROM vectors, the per-pass constants and the zone partials
+  return sv + NROMVEC * S + nYB * (int64_t)(sizeof(double) / sizeof(T)) + 2 * nYB +
+         (int64_t)B * ZWARPS * (int64_t)(sizeof(double) / sizeof(T));
+}
 
 // One ROM step for a batch of nb (<= B) instances of one model (eq:connExplicit, K3).
 // On entry sx (x~^n), sy (y^n), sh (h = Hz^{n+1/2} of the outside cells) hold the batch's vectors
 // (zero padding for b >= nb).  On exit sx holds x~^{n+1} and sy holds y^{n+1}; with ENERGY the ROM
-// part of W^n (coarse half cells + x~^T R~ x~) of instance b is in eout[b].
+// part of W^n (coarse half cells + x~^T R~ x~) of instance b is in eout[b].  Four phases: M1 GEMM |
+// energy + t | Schur solve | M2 GEMM with the base added in its epilogue (fp32: tensor cores).
 template <typename T, bool ENERGY>
 __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first, int nb, int B, int64_t S, T* sv,
                          double* eout) {
   const int nY = m.nY, q1 = m.q1, q2 = m.q2, nx = q1 + q2, m1 = q2 + q1 + nY, m2 = q1 + nY;
   const int tid = threadIdx.x, nt = blockDim.x;
   RomVec<T> v(sv, S);
-  const T* mp = p.mpool;
+  const RomConst<T> rc(sv, S, (int64_t)nY * B);
   // [H~^{n+1}; E*; -L~^T E*] = M1 x~^n, and with ENERGY also R~ x~^n (R~ is stored after M1 as
-  // q1 + q2 further rows of the same column-major operator: one GEMM phase); so is overwritten
-  bgemm<T, false>(mp + m.off_M1, ENERGY ? m1 + nx : m1, m1 + nx, nx, v.sx, v.so, B, T(1));
+  // q1 + q2 further rows of the same operator: one GEMM phase); so is overwritten
+  {
+    T* so = v.so;
+    dmma_gemm(p.mpool64 + m.off_M1t, ENERGY ? m.mt1 : (m1 + 7) / 8, m.kt1, ENERGY ? m1 + nx : m1, nx, v.sx, B,
+              [&](int r, int c, double x) { so[r * B + c] = (T)x; });
+  }
   __syncthreads();
-  if (ENERGY) {  // x~^T R~ x~ + sum D_l D_l' eps/dt y^2 (storage function, R17)
+  if (ENERGY) {  // x~^T R~ x~ + sum D_l D_l' eps/dt y^2 (storage function, R17); one warp per instance
     const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
     for (int b = w; b < nb; b += nw) {
-      const int64_t po = p.port_off[first + b];
       double acc = 0.0;
-      for (int i = lane; i < nY; i += 32) acc += p.ehalf[po + i] * (double)v.sy[i * B + b] * (double)v.sy[i * B + b];
+      for (int i = lane; i < nY; i += 32) {
+        const double y = (double)v.sy[i * B + b];
+        acc += rc.eh[i * B + b] * y * y;
+      }
       for (int i = lane; i < nx; i += 32) acc += (double)v.sx[i * B + b] * (double)v.so[(m1 + i) * B + b];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
@@ -723,12 +759,11 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first
   // t = (a_y/c_y) y + (D_l G/c_y) h - L~^T E*
   for (int it = tid; it < nY * nb; it += nt) {
     const int i = it % nY, b = it / nY;
-    const int64_t po = p.port_off[first + b];
-    v.st[i * B + b] = v.so[(q2 + q1 + i) * B + b] +
-                      fma_rn(p.cyg[po + i], v.sh[i * B + b], mul_rn(p.cya[po + i], v.sy[i * B + b]));
+    const int k = i * B + b;
+    v.st[k] = v.so[(q2 + q1 + i) * B + b] + fma_rn(rc.cyg[k], v.sh[k], mul_rn(rc.cya[k], v.sy[k]));
   }
   __syncthreads();
-  // U = S_k t (per-instance Schur inverse, streamed from HBM); [E*; -L~^T E*] as the base of M2 U
+  // U = S_k t (per-instance Schur inverse, streamed from HBM)
   for (int it = tid; it < nY * nb; it += nt) {
     const int i = it % nY, b = it / nY;
     const T* Sk = p.Sk + p.Sk_off[first + b] + i;
@@ -741,25 +776,21 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first
     for (; c < nY; ++c) a[0] = fma_rn(__ldg(Sk + (int64_t)c * nY), v.st[c * B + b], a[0]);
     v.sU[i * B + b] = (a[0] + a[1]) + (a[2] + a[3]);
   }
-  for (int64_t k = tid; k < (int64_t)m2 * B; k += nt) {
-    const int64_t r = k / B;
-    v.so2[k] = r < q1 ? v.so[(q2 + r) * B + k % B] : (m.literal ? T(0) : -v.so[(q2 + r) * B + k % B]);
+  __syncthreads();
+  // [E~^{n+1}; y^{n+1}] = [E*; L~^T E*] + M2 U (the base added in fp64 in the epilogue; literal:
+  // y' = the U rows themselves), and H~^{n+1} = so rows 0 .. q2 copied beside it
+  {
+    T* sx = v.sx;
+    T* sy = v.sy;
+    const T* so = v.so;
+    const bool lit = m.literal != 0;
+    dmma_gemm(p.mpool64 + m.off_M2t, m.mt2, m.kt2, m2, nY, v.sU, B, [&](int r, int c, double x) {
+      if (r < q1) sx[r * B + c] = (T)((double)so[(q2 + r) * B + c] + x);
+      else sy[(r - q1) * B + c] = (T)((lit ? 0.0 : -(double)so[(q2 + r) * B + c]) + x);
+    });
+    for (int64_t k = tid; k < (int64_t)q2 * B; k += nt) sx[(int64_t)q1 * B + k] = so[k];
   }
   __syncthreads();
-  // [E~^{n+1}; y^{n+1}] = [E*; L~^T E*] + M2 U
-  bgemm<T, true>(mp + m.off_M2, m2, m2, nY, v.sU, v.so2, B, T(1));
-  __syncthreads();
-  for (int64_t k = tid; k < (int64_t)nx * B; k += nt) {
-    const int64_t r = k / B;
-    v.sx[k] = r < q1 ? v.so2[k] : v.so[(r - q1) * B + k % B];  // E~ from so2, H~ from so rows 0..q2
-  }
-  for (int64_t k = tid; k < (int64_t)nY * B; k += nt) v.sy[k] = v.so2[(int64_t)q1 * B + k];
-  __syncthreads();
-}
-
-template <typename T>
-__device__ __forceinline__ T* rom_end(T* sv, int64_t S) {
-  return sv + NROMVEC * S;  // first free element after the ROM vectors
 }
 
 template <typename T>
@@ -805,64 +836,115 @@ __device__ void store_rom(const PostParams<T>& p, const RomModelDev& m, int firs
 // more column / row on the right / top, holes excluded) with their bottom Ex and left Ey edges;
 // y^{n+K}; the ROM state.  Their energy (which the sweep skipped) and the zone probes are
 // recorded here for every step of the pass.
+// (b, v, u) walked over nb instances x a ch x cw cell window [v0, v0 + ch) x [u0, u0 + cw), thread
+// tid first, nt apart, advanced incrementally (no division per cell).  All instances of a batch
+// share one model, hence one region shape: the batch's regions are one flat index space.
+struct Flat {
+  int u, v, b, du, dv, db, u0, cw, v0, ch;
+  __device__ __forceinline__ Flat(int tid, int nt, int u0_, int cw_, int v0_, int ch_)
+      : u0(u0_), cw(cw_), v0(v0_), ch(ch_) {
+    const int per = cw * ch;
+    b = tid / per;
+    const int r = tid % per;
+    v = v0 + r / cw;
+    u = u0 + r % cw;
+    db = nt / per;
+    const int rr = nt % per;
+    dv = rr / cw;
+    du = rr % cw;
+  }
+  __device__ __forceinline__ void next() {
+    u += du;
+    v += dv;
+    b += db;
+    if (u >= u0 + cw) { u -= cw; ++v; }
+    if (v >= v0 + ch) { v -= ch; ++b; }
+  }
+};
+
+// per-instance constants of a batch (static shared memory of the fix-up kernel)
+constexpr int MAXB = 64;  // largest batch (FDTD_ROM_BATCH)
+struct BatchShared {
+  int64_t gbase[MAXB];     // device element offset of region cell (0, 0)
+  int su[MAXB], sv0[MAXB], sv1[MAXB];  // the source cells in region coordinates (su = -1: none)
+  double zsum[MAXB];
+};
+
+// K3: the K-step fix-up of one batch (instances of one model).  The sweep advanced every cell K
+// steps with the interface edges frozen at y^n; here, per instance, the K steps are recomputed
+// on the region [i0-M, i0+bx+M) x [j0-M, j0+by+M), M = Kz + K - 1, from the pass's input buffer
+// with the sweep's own arithmetic (yee_row's device functions), and between the H and E half
+// steps the ROM takes its step (S4 gather, S5 eq:connExplicit, S6 scatter).  Values in the
+// region go wrong from its border inwards by one cell per step, so after K steps every cell
+// within Kz of the block is exact.  Written back: the zone cells (block + Kz - 1 rings, + one
+// more column / row on the right / top, holes excluded) with their bottom Ex and left Ey edges;
+// y^{n+K}; the ROM state.  Their energy (which the sweep skipped) and the zone probes are
+// recorded here for every step of the pass.  Every region phase runs over the whole batch at once.
 template <typename T, int K, bool ENERGY>
-__device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[K], int64_t step, double* zsum) {
+__device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[K], int64_t step, BatchShared& bs) {
   const int* bt = p.batch_tab + 5 * bi;  // (model, first instance, count, slots B, region stride)
   const int model = bt[0], first = bt[1], nb = bt[2], B = bt[3], rstride = bt[4];
   const RomModelDev m = p.models[model];
   const int nY = m.nY;
   const int64_t S = (int64_t)(m.q1 + m.q2 + nY) * B;  // vector stride of this batch's layout
   const int tid = threadIdx.x, nt = blockDim.x;
-  T* reg = rom_end(sv, S);
+  const int64_t nYB = (int64_t)nY * B;
+  T* reg = rom_end(sv, S, nYB, B);
+  const RomConst<T> rc(sv, S, nYB);
   const int Kz = p.Kz, M = Kz + K - 1;
   const int64_t P = p.pitch;
-  for (int64_t k = tid; k < 7 * S; k += nt) sv[k] = T(0);
+  // the batch's common region shape (one model)
+  const int bx = p.rects[4 * (int64_t)first + 2], by = p.rects[4 * (int64_t)first + 3];
+  const int Wr = bx + 2 * M, Hr = by + 2 * M, W1 = Wr + 1, n = Hr * Wr;
+  int zu0 = 0, zu1 = 0, zv0 = 0, zv1 = 0;
+  if (Kz >= 2) {  // zone rectangle in region coordinates
+    zu0 = M - (Kz - 1); zu1 = M + bx + Kz; zv0 = M - (Kz - 1); zv1 = M + by + Kz;
+  }
+  const int zw = zu1 - zu0, nz = zw * (zv1 - zv0);
+  auto H = [&](int b) { return reg + (int64_t)b * rstride; };
+  auto MA = [&](int b) { return reg + (int64_t)b * rstride + n; };
+  auto MS = [&](int b) { return reg + (int64_t)b * rstride + 2 * n; };
+  auto EX = [&](int b) { return reg + (int64_t)b * rstride + 3 * n; };
+  auto EY = [&](int b) { return reg + (int64_t)b * rstride + 4 * n + Wr; };
+  auto ZE = [&](int b) { return reg + (int64_t)b * rstride + 4 * n + Wr + Hr * W1; };
+  FCHK(4 * n + Wr + Hr * W1 + nz <= rstride &&
+       (size_t)((char*)(reg + (int64_t)B * rstride) - (char*)sv) <= p.smem_bytes);  // regions inside the launch
+  for (int64_t k = tid; k < NROMVEC * S; k += nt) sv[k] = T(0);
+  for (int b = tid; b < nb; b += nt) {
+    const int32_t* r = p.rects + 4 * (int64_t)(first + b);
+    const int64_t lr0 = (int64_t)r[1] - M - p.row_begin + p.row0;  // local row of region row 0
+    bs.gbase[b] = lr0 * P + r[0] - M;
+    FCHK(bs.gbase[b] >= 0 && bs.gbase[b] + (int64_t)Hr * P + Wr < p.alloc_elems);  // region rows inside the arrays
+    const int64_t cu = p.src_col - (r[0] - M);
+    const bool hit = p.src_row >= 0 && cu >= 0 && cu < Wr;
+    bs.su[b] = hit ? (int)cu : -1;
+    bs.sv0[b] = hit ? (int)max(p.src_row - lr0, (int64_t)0) : 0;
+    bs.sv1[b] = hit ? (int)min(p.src_row_end - lr0, (int64_t)Hr) : 0;
+  }
+  __syncthreads();  // the zero padding lands before load_rom_state fills the live slots
   T* sy = sv + S;
   T* sh = sv + 2 * S;
-  struct Geo {
-    int i0, j0, bx, by, Wr, Hr, zu0, zu1, zv0, zv1;
-    T *H, *MA, *MS, *ZE, *EX, *EY;
-  };
-  auto geo = [&](int b) {
-    Geo q;
-    const int32_t* r = p.rects + 4 * (int64_t)(first + b);
-    q.i0 = r[0]; q.j0 = r[1]; q.bx = r[2]; q.by = r[3];
-    q.Wr = q.bx + 2 * M; q.Hr = q.by + 2 * M;
-    if (Kz >= 2) {  // zone rectangle in region coordinates
-      q.zu0 = M - (Kz - 1); q.zu1 = M + q.bx + Kz; q.zv0 = M - (Kz - 1); q.zv1 = M + q.by + Kz;
-    } else {
-      q.zu0 = q.zu1 = q.zv0 = q.zv1 = 0;
-    }
-    const int n = q.Hr * q.Wr;
-    q.H = reg + (int64_t)b * rstride;
-    q.MA = q.H + n; q.MS = q.MA + n; q.ZE = q.MS + n; q.EX = q.ZE + n; q.EY = q.EX + n + q.Wr;
-    FCHK((int64_t)(q.EY + q.Hr * (q.Wr + 1) - reg) <= (int64_t)(b + 1) * rstride &&
-         (size_t)((char*)(q.EY + q.Hr * (q.Wr + 1)) - (char*)sv) <= p.smem_bytes);  // region inside its slot
-    return q;
-  };
-  auto goff = [&](const Geo& q, int u, int v) {
-    return ((int64_t)q.j0 - M + v - p.row_begin + p.row0) * P + q.i0 - M + u;
-  };
-  auto is_src = [&](const Geo& q, int u, int v) {  // soft (line) source cell?
-    const int lr = q.j0 - M + v - (int)p.row_begin + p.row0;
-    return p.src_row >= 0 && q.i0 - M + u == p.src_col && lr >= p.src_row && lr < p.src_row_end;
-  };
-  // ---- load the region: materials and the fields at step n (asynchronous element copies, all in
+  // ---- load the regions: materials and the fields at step n (asynchronous element copies, all in
   // flight at once: the region rows are not 16-byte aligned)
-  for (int b = 0; b < nb; ++b) {
-    const Geo q = geo(b);
-    FCHK(goff(q, 0, 0) >= 0 && goff(q, q.Wr, q.Hr) < p.alloc_elems);  // region rows inside the device arrays
-    for (int t = tid; t < q.Hr * q.Wr; t += nt) {
-      const int64_t o = goff(q, t % q.Wr, t / q.Wr);
-      cp_async_el(q.MA + t, p.mea + o);
-      cp_async_el(q.MS + t, p.msb + o);
-      cp_async_el(q.H + t, p.hz0 + o);
-    }
-    for (int t = tid; t < (q.Hr + 1) * q.Wr; t += nt) cp_async_el(q.EX + t, p.ex0 + goff(q, t % q.Wr, t / q.Wr));
-    for (int t = tid; t < q.Hr * (q.Wr + 1); t += nt)
-      cp_async_el(q.EY + t, p.ey0 + goff(q, t % (q.Wr + 1), t / (q.Wr + 1)));
+  for (Flat f(tid, nt, 0, Wr, 0, Hr); f.b < nb; f.next()) {
+    const int64_t o = bs.gbase[f.b] + (int64_t)f.v * P + f.u;
+    const int t = f.v * Wr + f.u;
+    cp_async_el(MA(f.b) + t, p.mea + o);
+    cp_async_el(MS(f.b) + t, p.msb + o);
+    cp_async_el(H(f.b) + t, p.hz0 + o);
   }
+  for (Flat f(tid, nt, 0, Wr, 0, Hr + 1); f.b < nb; f.next())
+    cp_async_el(EX(f.b) + f.v * Wr + f.u, p.ex0 + bs.gbase[f.b] + (int64_t)f.v * P + f.u);
+  for (Flat f(tid, nt, 0, W1, 0, Hr); f.b < nb; f.next())
+    cp_async_el(EY(f.b) + f.v * W1 + f.u, p.ey0 + bs.gbase[f.b] + (int64_t)f.v * P + f.u);
   load_rom_state(p, m, first, nb, B, sv);
+  for (int it = tid; it < nY * nb; it += nt) {  // per-pass constants of the batch's ports (RomConst)
+    const int i = it % nY, b = it / nY;
+    const int64_t po = p.port_off[first + b] + i;
+    rc.eh[i * B + b] = p.ehalf[po];
+    rc.cya[i * B + b] = p.cya[po];
+    rc.cyg[i * B + b] = p.cyg[po];
+  }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   // Values go wrong from the region's border inwards one cell per step, so step s only updates the
@@ -870,143 +952,136 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   // normal); the zone, the ROM's gather cells and the write-back all lie inside the last cone.
 #pragma unroll 1
   for (int s = 0; s < K; ++s) {
-    // ---- H half-step (+ source, + zone-cell energy of W^{n+s})
-    for (int b = 0; b < nb; ++b) {
-      const Geo q = geo(b);
-      const int W1 = q.Wr + 1;
-      const int cw = q.Wr - 2 * s, ch = q.Hr - 2 * s;
-      const int du = nt % cw, dv = nt / cw;  // (u, v) advanced incrementally: no division per cell
-      int u = s + tid % cw, v = s + tid / cw;
-      for (int i = tid; i < cw * ch; i += nt, u += du, v += dv) {
-        if (u >= s + cw) { u -= cw; ++v; }
-        const int t = v * q.Wr + u;
-        const T h0 = q.H[t];
-        const T hu = hupd(h0, q.EX[t + q.Wr], q.EX[t], q.EY[v * W1 + u + 1], q.EY[v * W1 + u], p.chy, p.chx);
-        T h = q.MA[t] < T(0) ? h0 : hu;  // dead cells keep their Hz (as in yee_row)
-        if (is_src(q, u, v)) h += g[s];
-        if (ENERGY && u >= q.zu0 && u < q.zu1 && v >= q.zv0 && v < q.zv1) {
-          // the zone cell's full storage-function term (row_coef's weights without the zone mask)
-          bool lx, ly;
-          T ax, ay, ca, cb;
-          edge_coef(q.MA[t - q.Wr], q.MS[t - q.Wr], q.MA[t], q.MS[t], p.idy, ca, cb, ax, lx);
-          edge_coef(q.MA[t - 1], q.MS[t - 1], q.MA[t], q.MS[t], -p.idx, ca, cb, ay, ly);
-          const T wx = lx ? mul_rn(p.wxy, ax) : T(0), wy = ly ? mul_rn(p.wxy, ay) : T(0);
-          const T hw = q.MA[t] < T(0) ? T(0) : p.wh;
-          q.ZE[(v - q.zv0) * (q.zu1 - q.zu0) + u - q.zu0] = cell_energy(T(0), q.EX[t], q.EY[v * W1 + u], h0, h, wx, wy, hw);
-        }
-        q.H[t] = h;
+    const int cw = Wr - 2 * s, ch = Hr - 2 * s;
+    // ---- H half-step (+ source, + the zone cells' storage-function terms of W^{n+s})
+    for (Flat f(tid, nt, s, cw, s, ch); f.b < nb; f.next()) {
+      const int u = f.u, v = f.v, b = f.b;
+      const T* ex = EX(b);
+      const T* ey = EY(b);
+      const T* ma = MA(b);
+      T* hz = H(b);
+      const int t = v * Wr + u;
+      const T h0 = hz[t];
+      const T hu = hupd(h0, ex[t + Wr], ex[t], ey[v * W1 + u + 1], ey[v * W1 + u], p.chy, p.chx);
+      T h = ma[t] < T(0) ? h0 : hu;  // dead cells keep their Hz (as in yee_row)
+      if (u == bs.su[b] && v >= bs.sv0[b] && v < bs.sv1[b]) h += g[s];
+      if (ENERGY && u >= zu0 && u < zu1 && v >= zv0 && v < zv1) {
+        // the zone cell's full storage-function term (row_coef's weights without the zone mask)
+        const T* ms = MS(b);
+        bool lx, ly;
+        T ax, ay, ca, cb;
+        edge_coef(ma[t - Wr], ms[t - Wr], ma[t], ms[t], p.idy, ca, cb, ax, lx);
+        edge_coef(ma[t - 1], ms[t - 1], ma[t], ms[t], -p.idx, ca, cb, ay, ly);
+        const T wx = lx ? mul_rn(p.wxy, ax) : T(0), wy = ly ? mul_rn(p.wxy, ay) : T(0);
+        const T hw = ma[t] < T(0) ? T(0) : p.wh;
+        ZE(b)[(v - zv0) * zw + u - zu0] = cell_energy(T(0), ex[t], ey[v * W1 + u], h0, h, wx, wy, hw);
       }
+      hz[t] = h;
     }
     __syncthreads();
     // ---- zone probes; S4 gather of y^{n+s} (interface edges) and h = Hz^{n+s+1/2} (outside cells)
     for (int b = 0; b < nb; ++b) {
-      const Geo q = geo(b);
       const int z0 = p.zp_off[first + b], z1 = p.zp_off[first + b + 1];
+      if (z0 == z1) continue;
+      const int32_t* r = p.rects + 4 * (int64_t)(first + b);
       for (int z = z0 + tid; z < z1; z += nt) {
-        const int u = p.zp[3 * z] - (q.i0 - M), v = p.zp[3 * z + 1] - (q.j0 - M);
-        FCHK(u >= 0 && u < q.Wr && v >= 0 && v < q.Hr && p.zp[3 * z + 2] < p.n_probe);
-        p.probe_ring[(int64_t)p.zp[3 * z + 2] * p.cap + (step + s) % p.cap] = q.H[v * q.Wr + u];
+        const int u = p.zp[3 * z] - (r[0] - M), v = p.zp[3 * z + 1] - (r[1] - M);
+        FCHK(u >= 0 && u < Wr && v >= 0 && v < Hr && p.zp[3 * z + 2] < p.n_probe);
+        p.probe_ring[(int64_t)p.zp[3 * z + 2] * p.cap + (step + s) % p.cap] = H(b)[v * Wr + u];
       }
-      const int W1 = q.Wr + 1;
-      for (int i = tid; i < nY; i += nt) {
-        T y, h;
-        if (i < q.bx) {  // S side: Ex edge row M, outside cell row M-1
-          y = q.EX[M * q.Wr + M + i]; h = q.H[(M - 1) * q.Wr + M + i];
-        } else if (i < 2 * q.bx) {  // N side: Ex edge row M+by, outside cell row M+by
-          y = q.EX[(M + q.by) * q.Wr + M + i - q.bx]; h = q.H[(M + q.by) * q.Wr + M + i - q.bx];
-        } else if (i < 2 * q.bx + q.by) {  // W side: Ey edge column M, outside cell column M-1
-          const int v = M + i - 2 * q.bx;
-          y = q.EY[v * W1 + M]; h = q.H[v * q.Wr + M - 1];
-        } else {  // E side: Ey edge column M+bx, outside cell column M+bx
-          const int v = M + i - 2 * q.bx - q.by;
-          y = q.EY[v * W1 + M + q.bx]; h = q.H[v * q.Wr + M + q.bx];
-        }
-        sy[i * B + b] = y;
-        sh[i * B + b] = h;
+    }
+    for (int it = tid; it < nY * nb; it += nt) {
+      const int i = it % nY, b = it / nY;
+      const T* ex = EX(b);
+      const T* ey = EY(b);
+      const T* hz = H(b);
+      T y, h;
+      if (i < bx) {  // S side: Ex edge row M, outside cell row M-1
+        y = ex[M * Wr + M + i]; h = hz[(M - 1) * Wr + M + i];
+      } else if (i < 2 * bx) {  // N side: Ex edge row M+by, outside cell row M+by
+        y = ex[(M + by) * Wr + M + i - bx]; h = hz[(M + by) * Wr + M + i - bx];
+      } else if (i < 2 * bx + by) {  // W side: Ey edge column M, outside cell column M-1
+        const int v = M + i - 2 * bx;
+        y = ey[v * W1 + M]; h = hz[v * Wr + M - 1];
+      } else {  // E side: Ey edge column M+bx, outside cell column M+bx
+        const int v = M + i - 2 * bx - by;
+        y = ey[v * W1 + M + bx]; h = hz[v * Wr + M + bx];
       }
+      sy[i * B + b] = y;
+      sh[i * B + b] = h;
     }
     if (ENERGY) {  // zone energy per instance, fixed order (one warp per instance)
       const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
       for (int b = w; b < nb; b += nw) {
-        const Geo q = geo(b);
-        const int nz = (q.zu1 - q.zu0) * (q.zv1 - q.zv0);
+        const T* ze = ZE(b);
         double acc = 0.0;
-        for (int i = lane; i < nz; i += 32) acc += (double)q.ZE[i];
+        for (int i = lane; i < nz; i += 32) acc += (double)ze[i];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
-        if (lane == 0) zsum[b] = acc;
+        if (lane == 0) bs.zsum[b] = acc;
       }
     }
     __syncthreads();
     // ---- S5: ROM step n+s -> y^{n+s+1}, x~^{n+s+1}; ROM energy of W^{n+s}
     double* eout = p.rom_partials + (int64_t)s * p.n_inst + first;
     rom_step<T, ENERGY>(p, m, first, nb, B, S, sv, eout);
-    if (ENERGY && tid < nb) eout[tid] += zsum[tid];
-    // ---- S6: y^{n+s+1} into the region's interface edges, and in the same phase the E half-step
-    // on the region's live edges (dead edges -- interface, PEC, hole -- keep their value: they are
+    if (ENERGY && tid < nb) eout[tid] += bs.zsum[tid];
+    // ---- S6: y^{n+s+1} into the regions' interface edges, and in the same phase the E half-step
+    // on the regions' live edges (dead edges -- interface, PEC, hole -- keep their value: they are
     // skipped, so the scatter and the update never touch the same edge)
-    for (int b = 0; b < nb; ++b) {
-      const Geo q = geo(b);
-      const int W1 = q.Wr + 1;
-      for (int i = tid; i < nY; i += nt) {
-        const T y = sy[i * B + b];
-        if (i < q.bx) q.EX[M * q.Wr + M + i] = y;
-        else if (i < 2 * q.bx) q.EX[(M + q.by) * q.Wr + M + i - q.bx] = y;
-        else if (i < 2 * q.bx + q.by) q.EY[(M + i - 2 * q.bx) * W1 + M] = y;
-        else q.EY[(M + i - 2 * q.bx - q.by) * W1 + M + q.bx] = y;
-      }
+    for (int it = tid; it < nY * nb; it += nt) {
+      const int i = it % nY, b = it / nY;
+      const T y = sy[i * B + b];
+      T* ex = EX(b);
+      T* ey = EY(b);
+      if (i < bx) ex[M * Wr + M + i] = y;
+      else if (i < 2 * bx) ex[(M + by) * Wr + M + i - bx] = y;
+      else if (i < 2 * bx + by) ey[(M + i - 2 * bx) * W1 + M] = y;
+      else ey[(M + i - 2 * bx - by) * W1 + M + bx] = y;
     }
-    for (int b = 0; b < nb; ++b) {
-      const Geo q = geo(b);
-      const int W1 = q.Wr + 1;
-      const int cw = q.Wr - 2 * s, ch = q.Hr - 2 * s;
-      const int du = nt % cw, dv = nt / cw;
-      int eu = s + tid % cw, ev = s + 1 + tid / cw;
-      for (int i = tid; i < cw * (ch - 1); i += nt, eu += du, ev += dv) {  // Ex edge rows s+1 .. Hr-s-1,
-        if (eu >= s + cw) { eu -= cw; ++ev; }                              // columns s .. Wr-s-1
-        const int t = ev * q.Wr + eu;
-        bool l;
-        T a, ca, cb;
-        edge_coef(q.MA[t - q.Wr], q.MS[t - q.Wr], q.MA[t], q.MS[t], p.idy, ca, cb, a, l);
-        if (l) q.EX[t] = eupd(q.EX[t], ca, cb, q.H[t] - q.H[t - q.Wr]);
-      }
-      const int dy_u = nt % (cw - 1), dy_v = nt / (cw - 1);
-      int yu = s + 1 + tid % (cw - 1), yv = s + tid / (cw - 1);
-      for (int i = tid; i < (cw - 1) * ch; i += nt, yu += dy_u, yv += dy_v) {  // Ey edge columns s+1 ..
-        if (yu >= s + cw) { yu -= cw - 1; ++yv; }                               // Wr-s-1, rows s .. Hr-s-1
-        const int u = yu, v = yv;
-        const int c = v * q.Wr + u;
-        bool l;
-        T a, ca, cb;
-        edge_coef(q.MA[c - 1], q.MS[c - 1], q.MA[c], q.MS[c], -p.idx, ca, cb, a, l);
-        if (l) q.EY[v * W1 + u] = eupd(q.EY[v * W1 + u], ca, cb, q.H[c] - q.H[c - 1]);
-      }
+    for (Flat f(tid, nt, s, cw, s + 1, ch - 1); f.b < nb; f.next()) {  // Ex edge rows s+1 .. Hr-s-1,
+      const int t = f.v * Wr + f.u;                                       // columns s .. Wr-s-1
+      const T* ma = MA(f.b);
+      const T* ms = MS(f.b);
+      const T* hz = H(f.b);
+      T* ex = EX(f.b);
+      bool l;
+      T a, ca, cb;
+      edge_coef(ma[t - Wr], ms[t - Wr], ma[t], ms[t], p.idy, ca, cb, a, l);
+      if (l) ex[t] = eupd(ex[t], ca, cb, hz[t] - hz[t - Wr]);
+    }
+    for (Flat f(tid, nt, s + 1, cw - 1, s, ch); f.b < nb; f.next()) {  // Ey edge columns s+1 .. Wr-s-1,
+      const int c = f.v * Wr + f.u;                                       // rows s .. Hr-s-1
+      const T* ma = MA(f.b);
+      const T* ms = MS(f.b);
+      const T* hz = H(f.b);
+      T* ey = EY(f.b);
+      bool l;
+      T a, ca, cb;
+      edge_coef(ma[c - 1], ms[c - 1], ma[c], ms[c], -p.idx, ca, cb, a, l);
+      if (l) ey[f.v * W1 + f.u] = eupd(ey[f.v * W1 + f.u], ca, cb, hz[c] - hz[c - 1]);
     }
     __syncthreads();
   }
-  // ---- write back the zone: Hz of the live zone cells, their bottom Ex and left Ey edges
-  for (int b = 0; b < nb; ++b) {
-    const Geo q = geo(b);
-    const int zw = q.zu1 - q.zu0, nz = zw * (q.zv1 - q.zv0);
-    for (int i = tid; i < nz; i += nt) {
-      const int u = q.zu0 + i % zw, v = q.zv0 + i / zw;
-      const int t = v * q.Wr + u;
-      if (!(q.MA[t] >= T(0))) continue;
-      const int64_t o = goff(q, u, v);
+  // ---- write back the zones: Hz of the live zone cells, their bottom Ex and left Ey edges
+  if (nz > 0)
+    for (Flat f(tid, nt, zu0, zw, zv0, zv1 - zv0); f.b < nb; f.next()) {
+      const int t = f.v * Wr + f.u;
+      if (!(MA(f.b)[t] >= T(0))) continue;
+      const int64_t o = bs.gbase[f.b] + (int64_t)f.v * P + f.u;
       FCHK(o >= (int64_t)p.row0 * p.pitch && o < (int64_t)(p.row0 + p.rows) * p.pitch);  // owned rows only
-      p.hz1[o] = q.H[t];
-      p.ex1[o] = q.EX[t];
-      p.ey1[o] = q.EY[v * (q.Wr + 1) + u];
+      p.hz1[o] = H(f.b)[t];
+      p.ex1[o] = EX(f.b)[t];
+      p.ey1[o] = EY(f.b)[f.v * W1 + f.u];
     }
-  }
   store_rom(p, m, first, nb, B, S, sv, p.ex1, p.ey1);
 }
 
 template <typename T, int K, bool ENERGY>
-__global__ void __launch_bounds__(512) postk_kernel(const PostParams<T> p) {
+__global__ void __launch_bounds__(512, 1) postk_kernel(const PostParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[32];
-  __shared__ double zsum[64];
+  __shared__ BatchShared bs;
   T* sv = reinterpret_cast<T*>(smem_raw);
   const int b = blockIdx.x;
   const int64_t step = *p.step;
@@ -1019,7 +1094,7 @@ __global__ void __launch_bounds__(512) postk_kernel(const PostParams<T> p) {
       if (k >= 0 && k < p.src_meta[1]) g[s] = (T)p.src_samples[k];
     }
   }
-  if (b < p.n_batch) fixup_batch<T, K, ENERGY>(p, b, sv, g, step, zsum);
+  if (b < p.n_batch) fixup_batch<T, K, ENERGY>(p, b, sv, g, step, bs);
   if (ENERGY && b < p.n_batch) {  // this batch's ROM + zone energies, one value per step (level 1)
     __syncthreads();              // rom_partials of this batch written (fixup_batch ends with barriers)
     const int first = p.batch_tab[5 * b + 1], nb = p.batch_tab[5 * b + 2];
@@ -1393,8 +1468,10 @@ void launch_sweep(const SweepParams<T>& p, int K, int warps_per_cta, cudaStream_
   else if constexpr (sizeof(T) == 4) sweepk_launch<T, 4>(q, grid, nt, s);
 }
 
-size_t post_smem_bytes(size_t es, int nvec, int batch, int region_stride) {
-  return es * ((size_t)NROMVEC * nvec * batch + (size_t)batch * region_stride);
+size_t post_smem_bytes(size_t es, int nvec, int nY, int batch, int region_stride) {
+  // ROM vectors, the per-pass port constants (fp64 eh + two T arrays), the zone partials, the regions
+  return es * ((size_t)NROMVEC * nvec * batch + (size_t)(8 / es + 2) * nY * batch + (size_t)batch * ZWARPS * (8 / es) +
+               (size_t)batch * region_stride);
 }
 
 template <typename T, int K>

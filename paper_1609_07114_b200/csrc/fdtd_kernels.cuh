@@ -70,10 +70,14 @@ struct SweepParams {
 //      -> [H~^{n+1}; E*; -L~^T E*] in one product (K3)
 //   M2 ((q1 + nY) x nY) = [Bq; L~^T Bq]  -> [E~ - E*; y - L~^T E*] from U
 //   Rt ((q1 + q2) x (q1 + q2)) = [[R~11/dt, -K~/2], [-K~^T/2, R~22/dt]]  (storage function)
+// The fix-up's GEMMs run on the FP64 tensor cores (mma.sync.m8n8k4.f64, fdtd_kernels.cu
+// dmma_gemm): [M1; R~] and M2 are kept in an fp64 pool pre-tiled in the MMA's A-fragment order
+// (mt x kt tiles of 8 x 4, one double per lane and tile).
 struct RomModelDev {
   int nY, q1, q2;
   int literal;  // paper-literal coupling: U is y^{n+1} itself and M2 = [Z T; I] (K3)
-  int64_t off_M1, off_M2, off_Rt;
+  int64_t off_M1t, off_M2t;     // tiled operators in the fp64 pool
+  int mt1, kt1, mt2, kt2;       // their tile counts: [M1; R~] (m1 + q1 + q2 rows), M2 (q1 + nY rows)
 };
 
 // Fix-up kernel: per ROM instance, the K steps of the pass are recomputed on
@@ -87,7 +91,7 @@ struct PostParams {
   int n_batch;                     // CTAs doing ROM work; batches of <= batch instances of one model
   const int32_t* batch_tab;        // per batch: (model, first instance, count, slots B, region stride)
   const RomModelDev* models;
-  const T* mpool;                  // shared model matrices (column-major)
+  const double* mpool64;           // shared model operators, fp64, tiled for the DMMA GEMMs
   const T* Sk; const int64_t* Sk_off;        // per-instance Schur inverses (col-major nY x nY)
   const int64_t* port_off;                    // per-instance offset into port arrays
   const T* cya; const T* cyg;                 // a_y / c_y, D_l G / c_y per port
@@ -178,11 +182,13 @@ inline int sweep_ctas_x(int64_t nx, int elem_bytes, int K, int warps_per_cta) {
 template <typename T>
 void launch_post(const PostParams<T>& p, int K, bool energy, cudaStream_t s);
 // shared-memory bytes of the fix-up kernel for a given batch (host-side sizing)
-size_t post_smem_bytes(size_t es, int nvec, int batch, int region_stride);
+size_t post_smem_bytes(size_t es, int nvec, int nY, int batch, int region_stride);
 // elements of one instance region for zone depth Kz and pass depth K (<= Kz)
+// H, MA, MS (Hr x Wr), EX ((Hr + 1) x Wr), EY (Hr x (Wr + 1)) and the zone energies (at most
+// (bx + M) x (by + M): the zone of depth Kz spans bx + 2 Kz - 1 <= bx + M columns)
 inline int region_elems(int bx, int by, int M) {
   const int Wr = bx + 2 * M, Hr = by + 2 * M;
-  return 3 * Hr * Wr + (Hr + 1) * Wr + Hr * (Wr + 1) + (bx + 2 * M) * (by + 2 * M);
+  return 3 * Hr * Wr + (Hr + 1) * Wr + Hr * (Wr + 1) + (bx + M) * (by + M);
 }
 
 // setup kernels
