@@ -135,11 +135,15 @@ struct fdtd_ctx {
   std::vector<int32_t> inst_model, rects;  // rects: (i0, j0, bx, by) global
   std::vector<int64_t> port_off, port_edge, state_off, Sk_off;
   std::vector<double> cya, cyg, ehalf, Sk;  // fp64 host copies (converted on upload)
-  std::vector<double> mpool;                // shared model operators, fp64, tiled for the DMMA GEMMs
+  std::vector<double> mpool;                // shared model operators tiled for the DMMA GEMMs (fp64)
   int nvec = 1;
   std::vector<int32_t> batch_tab;  // (model, first instance, count, slots B, region stride)
   int32_t* d_batch_tab = nullptr;
   int post_grid = 1;
+  int n_batch_reg = 0;           // regular fix-up batches; the rest are large-model instances
+  void* d_big = nullptr;         // bigrom_kernel scratch
+  size_t big_smem = 0;
+  int big_grid = 0;
   // device ROM arrays
   void* d_mpool = nullptr; void* d_Sk = nullptr; void* d_cya = nullptr; void* d_cyg = nullptr;
   void* d_state = nullptr; double* d_ehalf = nullptr; double* d_rom_partials = nullptr;
@@ -276,7 +280,7 @@ template <typename T>
 fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
   fdtd::PostParams<T> p{};
   p.n_inst = (int)c->inst_model.size();
-  p.models = c->d_models; p.mpool64 = (const double*)c->d_mpool;
+  p.models = c->d_models; p.mpool = (const double*)c->d_mpool;
   p.Sk = (const T*)c->d_Sk; p.Sk_off = c->d_Sk_off; p.port_off = c->d_port_off;
   p.cya = (const T*)c->d_cya; p.cyg = (const T*)c->d_cyg; p.ehalf = c->d_ehalf;
   p.port_edge = c->d_port_edge;
@@ -306,6 +310,8 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
   p.level1 = c->d_level1;
   p.step = c->d_step;
   p.n_batch = c->inst_model.empty() ? 0 : (int)(c->batch_tab.size() / 5);
+  p.n_batch_reg = c->inst_model.empty() ? 0 : c->n_batch_reg;
+  p.big = (T*)c->d_big; p.big_smem_bytes = c->big_smem; p.big_grid = c->big_grid;
   p.batch_tab = c->d_batch_tab;
   p.block = c->post_threads;
   p.smem_bytes = c->post_smem;
@@ -505,7 +511,12 @@ fdtd_status enqueue_pass(fdtd_ctx* c, int q, cudaStream_t s, int K) {
   auto post = [&](cudaStream_t st) {
     if (c->prec == 64) fdtd::launch_post<double>(post_params<double>(c, q), K, c->energy_on, st);
     else fdtd::launch_post<float>(post_params<float>(c, q), K, c->energy_on, st);
-    c->launches += 1;
+    c->launches += c->n_batch_reg > 0;
+    if ((int)(c->batch_tab.size() / 5) > c->n_batch_reg) {  // large models: the cooperative fix-up
+      if (c->prec == 64) fdtd::launch_post_big<double>(post_params<double>(c, q), K, c->energy_on, st);
+      else fdtd::launch_post_big<float>(post_params<float>(c, q), K, c->energy_on, st);
+      c->launches += 1;
+    }
   };
   cudaEvent_t e[3];
   if (prof) {
@@ -837,23 +848,51 @@ fdtd_status apply_passes(fdtd_ctx* c, int k) {
       need1 = std::max(need1, per);
     }
     const size_t cap = std::max(budget, need1);
+    // Large models (order >= FDTD_BIG_Q, default 512) take the cooperative one-instance-at-a-time
+    // path (bigrom_kernel: the whole GPU on one ROM step), decided by the model alone so that every
+    // slab decomposition runs the same arithmetic; their batches follow the regular ones.
+    const char* benv = getenv("FDTD_BIG_Q");
+    const int big_q = benv ? atoi(benv) : 512;
+    std::vector<char> big(c->models.size(), 0);
+    size_t big_smem = 0;
+    int64_t big_elems = 0;
+    for (size_t mi = 0; mi < c->models.size(); ++mi) {
+      const ModelHost& m = c->models[mi];
+      if (big_q > 0 && m.q1 + m.q2 >= big_q) {
+        big[mi] = 1;
+        big_smem = std::max(big_smem, shp[mi].per);
+        big_elems = std::max<int64_t>(big_elems, 3 * (m.q1 + m.q2) + (m.q2 + m.q1 + m.nY) + 2 * m.nY);
+      }
+    }
+    c->big_grid = 0;
+    if (big_elems > 0) {
+      c->big_grid = c->prec == 64 ? fdtd::big_grid_size<double>(big_smem, k) : fdtd::big_grid_size<float>(big_smem, k);
+      if (c->big_grid <= 0) std::fill(big.begin(), big.end(), 0);  // cannot launch cooperatively: batch path
+    }
+    c->big_smem = big_smem;
     c->post_smem = 16;
-    for (auto& x : shp) {  // a power of two: the batched GEMM splits B into groups of 4, 2 or 1
-      const int fit = (int)std::max<size_t>(1, std::min<size_t>(Bmax, cap / x.per));
-      x.B = 1;
-      while (x.B * 2 <= fit) x.B *= 2;
-      c->post_smem = std::max(c->post_smem, x.B * x.per);
+    for (size_t mi = 0; mi < shp.size(); ++mi) {  // any B <= 8: the DMMA's N = 8 columns (zero-padded)
+      Shape& x = shp[mi];
+      x.B = big[mi] ? 1 : (int)std::max<size_t>(1, std::min<size_t>(Bmax, cap / x.per));
+      if (!big[mi]) c->post_smem = std::max(c->post_smem, x.B * x.per);
     }
     c->batch_tab.clear();
     const int n = (int)c->inst_model.size();
-    for (int i = 0; i < n;) {
-      const Shape& x = shp[c->inst_model[i]];
-      int e = i;
-      while (e < n && e - i < x.B && c->inst_model[e] == c->inst_model[i]) ++e;
-      c->batch_tab.insert(c->batch_tab.end(), {c->inst_model[i], i, e - i, x.B, x.stride});
-      i = e;
+    for (int pass = 0; pass < 2; ++pass) {  // regular batches, then the large models' instances
+      for (int i = 0; i < n;) {
+        const Shape& x = shp[c->inst_model[i]];
+        int e = i;
+        while (e < n && e - i < x.B && c->inst_model[e] == c->inst_model[i]) ++e;
+        if (big[c->inst_model[i]] == pass) c->batch_tab.insert(c->batch_tab.end(), {c->inst_model[i], i, e - i, x.B, x.stride});
+        i = e;
+      }
+      if (pass == 0) c->n_batch_reg = (int)(c->batch_tab.size() / 5);
     }
     if (c->batch_tab.empty()) c->batch_tab.assign(5, 0);
+    if (big_elems > 0 && c->big_grid > 0) {
+      std::vector<double> z((size_t)big_elems, 0.0);
+      if ((st = upload_T(c, &c->d_big, z)) != FDTD_OK) return st;
+    }
     if ((st = upload(c, &c->d_batch_tab, c->batch_tab)) != FDTD_OK) return st;
     c->post_grid = n > 0 ? (int)(c->batch_tab.size() / 5) : 1;
     std::vector<double> l1((size_t)KMAX * c->post_grid, 0.0);

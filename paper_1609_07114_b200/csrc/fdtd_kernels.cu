@@ -16,6 +16,8 @@
 #include <climits>
 #include <cstdio>
 
+#include <cooperative_groups.h>
+
 namespace fdtd {
 
 namespace {
@@ -638,13 +640,26 @@ __device__ double block_sum(double v, double* red) {
 }
 
 // ---- tensor-core path of the batched reduced GEMMs: FP64 DMMA (mma.sync.m8n8k4.f64), for fp32
-// and fp64 states alike.  A (a shared model operator) is kept in fp64 in a second pool, pre-tiled
-// in the A-fragment order of the m8n8k4 MMA (fdtd_api.cpp push_tiles): per 8 x 4 tile lane l holds
-// A[l / 4][l % 4] -- one coalesced 8-byte load per lane and tile.  The batch's vectors X (k x B,
-// row stride B; the B instances are the MMA's N = 8 columns) are widened to fp64; products and
-// sums are fp64 and only the result is rounded to the state precision (fp32 states get a more
-// accurate ROM update than fp32 FMAs would give).  Each output column depends on that column only,
-// so a batch's composition never changes an instance's values.
+// and fp64 states alike.  A (a shared model operator) is kept in fp64 in the pool, pre-tiled in
+// the A-fragment order of the m8n8k4 MMA (fdtd_api.cpp push_tiles): per 8 x 4 tile lane l holds
+// A[l / 4][l % 4] -- one coalesced 8-byte load per lane and tile (an fp32 copy would halve the L2
+// bytes but its per-element widening cost more than it saved: measured).  The batch's vectors X
+// (k x B, row stride B; the B instances are the MMA's N = 8 columns) are widened to fp64:
+// products and sums are fp64 and only the result is rounded to the state precision (fp32 states
+// get a more accurate ROM update than fp32 FMAs would give).  Each output column depends on that
+// column only, so a batch's composition never changes an instance's values.
+#ifndef FDTD_TPW  // dmma_gemm: row tiles per warp sharing a B fragment; A tiles in flight
+#define FDTD_TPW 3
+#endif
+#ifndef FDTD_UNR
+#define FDTD_UNR 4
+#endif
+#ifndef FDTD_SCHUR16  // Schur solve: 16 loads in flight per thread
+#define FDTD_SCHUR16 1
+#endif
+#ifndef FDTD_SKPF  // prefetch the batch's Schur inverses into L2 at the batch start
+#define FDTD_SKPF 1
+#endif
 __device__ __forceinline__ void mma_f64(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d[0]), "+d"(d[1])
@@ -653,41 +668,65 @@ __device__ __forceinline__ void mma_f64(double (&d)[2], double a, double b) {
 
 // Y = A X for rows [0, m): epi(r, c, v) receives element (r, c) in fp64.  A tiled as above with
 // mtiles x ktiles tiles of 8 x 4 (m <= 8 mtiles, k <= 4 ktiles, zero-padded); X in shared memory.
-// One warp per (8-row tile, 8-column tile) job; the k loop keeps UNR tile loads in flight.
-template <typename T, typename Epi>
-__device__ __forceinline__ void dmma_gemm(const double* __restrict__ At, int mtiles, int ktiles, int m, int k,
+// A warp owns up to TPW row tiles (w, w + nw, ...) of one 8-column tile and walks k once: each
+// B fragment is loaded and widened once for all of them, and the next UNR A tiles are in flight
+// while the current ones multiply.
+template <typename TA, typename T, typename Epi>
+__device__ __forceinline__ void dmma_gemm(const TA* __restrict__ At, int mtiles, int ktiles, int m, int k,
                                           const T* X, int B, Epi epi) {
+  constexpr int TPW = FDTD_TPW, UNR = FDTD_UNR;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int ntiles = (B + 7) >> 3;
-  for (int job = warp; job < mtiles * ntiles; job += nw) {
-    const int mt = job % mtiles, nt = job / mtiles;
-    const int col = nt * 8 + g;  // this lane's B-fragment column (instance slot)
+  const int groups = (mtiles + nw * TPW - 1) / (nw * TPW);  // passes over the row tiles
+  for (int job = warp; job < groups * nw * ntiles; job += nw) {
+    const int grp = job / (nw * ntiles), rem = job % (nw * ntiles);
+    const int nt = rem / nw, w = rem % nw;
+    const int mt0 = grp * nw * TPW + w;  // this warp's tiles: mt0 + j nw, j < TPW
+    const int col = nt * 8 + g;          // this lane's B-fragment column (instance slot)
     const bool cl = col < B;
-    double d[2] = {0.0, 0.0};
-    const double* ap = At + (int64_t)mt * ktiles * 32 + lane;
-    constexpr int UNR = 8;
-    int kt = 0;
-    for (; kt + UNR <= ktiles; kt += UNR) {
-      double a[UNR], b[UNR];
+    double d[TPW][2];
+    const TA* ap[TPW];
+    bool on[TPW];
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) a[u] = __ldg(ap + (kt + u) * 32);
+    for (int j = 0; j < TPW; ++j) {
+      d[j][0] = d[j][1] = 0.0;
+      on[j] = mt0 + j * nw < mtiles;
+      ap[j] = At + (int64_t)(on[j] ? mt0 + j * nw : 0) * ktiles * 32 + lane;
+    }
+    if (!on[0]) continue;
+    double a[2][TPW][UNR];
+    auto load = [&](int buf, int kt0) {
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const int kk = (kt + u) * 4 + t;
-        b[u] = (cl && kk < k) ? (double)X[kk * B + col] : 0.0;
+      for (int u = 0; u < UNR; ++u)
+#pragma unroll
+        for (int j = 0; j < TPW; ++j)
+          a[buf][j][u] = (on[j] && kt0 + u < ktiles) ? __ldg(ap[j] + (kt0 + u) * 32) : 0.0;
+    };
+    load(0, 0);
+    for (int kt0 = 0; kt0 < ktiles; kt0 += 2 * UNR) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kb = kt0 + h * UNR;
+        if (kb >= ktiles) break;
+        load(h ^ 1, kb + UNR);  // the next UNR tiles in flight
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const int kk = (kb + u) * 4 + t;
+          const double b = (cl && kk < k) ? (double)X[kk * B + col] : 0.0;
+#pragma unroll
+          for (int j = 0; j < TPW; ++j) mma_f64(d[j], a[h][j][u], b);
+        }
       }
+    }
+    const int c0 = nt * 8 + 2 * t;
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) mma_f64(d, a[u], b[u]);
-    }
-    for (; kt < ktiles; ++kt) {
-      const int kk = kt * 4 + t;
-      mma_f64(d, __ldg(ap + kt * 32), (cl && kk < k) ? (double)X[kk * B + col] : 0.0);
-    }
-    const int r = mt * 8 + g, c0 = nt * 8 + 2 * t;
-    if (r < m) {
-      if (c0 < B) epi(r, c0, d[0]);
-      if (c0 + 1 < B) epi(r, c0 + 1, d[1]);
+    for (int j = 0; j < TPW; ++j) {
+      const int r = (mt0 + j * nw) * 8 + g;
+      if (on[j] && r < m) {
+        if (c0 < B) epi(r, c0, d[j][0]);
+        if (c0 + 1 < B) epi(r, c0 + 1, d[j][1]);
+      }
     }
   }
 }
@@ -738,7 +777,7 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first
   // q1 + q2 further rows of the same operator: one GEMM phase); so is overwritten
   {
     T* so = v.so;
-    dmma_gemm(p.mpool64 + m.off_M1t, ENERGY ? m.mt1 : (m1 + 7) / 8, m.kt1, ENERGY ? m1 + nx : m1, nx, v.sx, B,
+    dmma_gemm(p.mpool + m.off_M1t, ENERGY ? m.mt1 : (m1 + 7) / 8, m.kt1, ENERGY ? m1 + nx : m1, nx, v.sx, B,
               [&](int r, int c, double x) { so[r * B + c] = (T)x; });
   }
   __syncthreads();
@@ -763,13 +802,19 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first
     v.st[k] = v.so[(q2 + q1 + i) * B + b] + fma_rn(rc.cyg[k], v.sh[k], mul_rn(rc.cya[k], v.sy[k]));
   }
   __syncthreads();
-  // U = S_k t (per-instance Schur inverse, streamed from HBM)
+  // U = S_k t (per-instance Schur inverse, L2-resident after the prefetch at the batch start)
   for (int it = tid; it < nY * nb; it += nt) {
     const int i = it % nY, b = it / nY;
     const T* Sk = p.Sk + p.Sk_off[first + b] + i;
     T a[4] = {T(0), T(0), T(0), T(0)};  // four interleaved partial sums: a quarter of the FMA chain
     int c = 0;
-#pragma unroll 4
+    for (; FDTD_SCHUR16 && c + 15 < nY; c += 16) {  // 16 loads in flight, then their FMAs
+      T sk[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) sk[u] = __ldg(Sk + (int64_t)(c + u) * nY);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) a[u & 3] = fma_rn(sk[u], v.st[(c + u) * B + b], a[u & 3]);
+    }
     for (; c + 3 < nY; c += 4)
 #pragma unroll
       for (int u = 0; u < 4; ++u) a[u] = fma_rn(__ldg(Sk + (int64_t)(c + u) * nY), v.st[(c + u) * B + b], a[u]);
@@ -784,13 +829,149 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first
     T* sy = v.sy;
     const T* so = v.so;
     const bool lit = m.literal != 0;
-    dmma_gemm(p.mpool64 + m.off_M2t, m.mt2, m.kt2, m2, nY, v.sU, B, [&](int r, int c, double x) {
+    dmma_gemm(p.mpool + m.off_M2t, m.mt2, m.kt2, m2, nY, v.sU, B, [&](int r, int c, double x) {
       if (r < q1) sx[r * B + c] = (T)((double)so[(q2 + r) * B + c] + x);
       else sy[(r - q1) * B + c] = (T)((lit ? 0.0 : -(double)so[(q2 + r) * B + c]) + x);
     });
     for (int64_t k = tid; k < (int64_t)q2 * B; k += nt) sx[(int64_t)q1 * B + k] = so[k];
   }
   __syncthreads();
+}
+
+// ---- the large-model path (one instance at a time on the whole GPU; fdtd_api.cpp "big" models):
+// a cooperative grid of one CTA per SM evaluates the ROM step of one instance, CTA 0 doing the
+// region work of fixup_batch.  Scratch in global memory (p.big): x~ in two buffers X0 / X1 (the
+// pass input stays in p.state until the pass ends), SO = [M1; R~] x~ (m1 + q1 + q2 rows), YH = the
+// gathered y and h (nY each).  Two grid barriers per step:
+//   phase 1: SO = [M1; R~] x~ -- every 8-row tile on one CTA (CTAs 1.. when there are several),
+//            split over its warps along k (fixed-order sum of the warps' partials); CTA 0 publishes y, h;
+//   phase 2: t and U = S_k t (every CTA, redundantly), E~' = E* + (M2 U) rows on CTAs 1..,
+//            y' rows and the storage-function term on CTA 0, H~' copied;
+// CTA 0 then scatters y' and takes the E half-step while the others start the next step's M1.
+template <typename T>
+struct BigScratch {
+  T *X0, *X1, *SO, *YH;
+  __device__ BigScratch(T* big, const RomModelDev& m) {
+    const int nx = m.q1 + m.q2, m1 = m.q2 + m.q1 + m.nY;
+    X0 = big; X1 = big + nx; SO = big + 2 * nx; YH = SO + m1 + nx;
+  }
+};
+
+template <typename T, bool ENERGY>
+__device__ void rom_step_big(const PostParams<T>& p, const RomModelDev& m, int first, int s, T* sv, int64_t S,
+                             double* eout, double* part) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int nY = m.nY, q1 = m.q1, q2 = m.q2, nx = q1 + q2, m1 = q2 + q1 + nY, m2 = q1 + nY;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const bool rg = cta == 0;
+  const int G1 = G > 1 ? G - 1 : 1, c1 = G > 1 ? cta - 1 : 0;  // CTA 0 keeps to its region when G > 1
+  const bool worker = G == 1 || cta > 0;
+  const BigScratch<T> bsc(p.big, m);
+  const T* xin = s == 0 ? p.state + p.state_off[first] : ((s - 1) & 1 ? bsc.X1 : bsc.X0);
+  T* xout = (s & 1) ? bsc.X1 : bsc.X0;
+  RomVec<T> v(sv, S);
+  const double* mp = p.mpool;
+  // ---- phase 1: SO = [M1; R~] x~ (with ENERGY all m1 + nx rows)
+  const int rows1 = ENERGY ? m1 + nx : m1, mt1 = (rows1 + 7) / 8, kt1 = m.kt1;
+  if (worker) {
+    const int kpw = (kt1 + nw - 1) / nw;
+    for (int tile = c1; tile < mt1; tile += G1) {
+      const int ka = warp * kpw, kb = min(ka + kpw, kt1);
+      const double* ap = mp + m.off_M1t + (int64_t)tile * kt1 * 32 + lane;
+      double d[2] = {0.0, 0.0};
+      int kt = ka;
+      for (; kt + 8 <= kb; kt += 8) {
+        double a[8], b[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = (double)__ldg(ap + (kt + u) * 32);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int kk = (kt + u) * 4 + t4;
+          b[u] = (g == 0 && kk < nx) ? (double)xin[kk] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mma_f64(d, a[u], b[u]);
+      }
+      for (; kt < kb; ++kt) {
+        const int kk = kt * 4 + t4;
+        mma_f64(d, (double)__ldg(ap + kt * 32), (g == 0 && kk < nx) ? (double)xin[kk] : 0.0);
+      }
+      if (t4 == 0) part[warp * 8 + g] = d[0];  // column 0 (the instance) of rows tile*8 + g
+      __syncthreads();
+      if (tid < 8) {
+        double acc = 0.0;
+        for (int w = 0; w < nw; ++w) acc += part[w * 8 + tid];
+        const int r = tile * 8 + tid;
+        if (r < rows1) bsc.SO[r] = (T)acc;
+      }
+      __syncthreads();
+    }
+  }
+  if (rg)
+    for (int i = tid; i < nY; i += nt) {
+      bsc.YH[i] = v.sy[i];
+      bsc.YH[nY + i] = v.sh[i];
+    }
+  grid.sync();
+  // ---- phase 2
+  const RomConst<T> rc(sv, S, (int64_t)nY);
+  if (ENERGY && rg && warp == 0) {  // storage function of the instance (the batch path's order)
+    double acc = 0.0;
+    for (int i = lane; i < nY; i += 32) {
+      const double y = (double)v.sy[i];
+      acc += rc.eh[i] * y * y;
+    }
+    for (int i = lane; i < nx; i += 32) acc += (double)xin[i] * (double)bsc.SO[m1 + i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
+    if (lane == 0) eout[0] = acc;
+  }
+  {  // t and U = S_k t, in every CTA
+    const int64_t po = p.port_off[first];
+    for (int i = tid; i < nY; i += nt)
+      v.st[i] = bsc.SO[q2 + q1 + i] + fma_rn(p.cyg[po + i], bsc.YH[nY + i], mul_rn(p.cya[po + i], bsc.YH[i]));
+    __syncthreads();
+    for (int i = tid; i < nY; i += nt) {
+      const T* Sk = p.Sk + p.Sk_off[first] + i;
+      T a[4] = {T(0), T(0), T(0), T(0)};
+      int c = 0;
+      for (; c + 3 < nY; c += 4)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] = fma_rn(__ldg(Sk + (int64_t)(c + u) * nY), v.st[c + u], a[u]);
+      for (; c < nY; ++c) a[0] = fma_rn(__ldg(Sk + (int64_t)c * nY), v.st[c], a[0]);
+      v.sU[i] = (a[0] + a[1]) + (a[2] + a[3]);
+    }
+    __syncthreads();
+  }
+  // [E~'; y'] = [E*; L~^T E*] + M2 U: the tiles holding y rows on CTA 0 (it scatters y'), the others
+  // one warp each on CTAs 1..
+  const int mt2 = m.mt2, kt2 = m.kt2, ty = q1 / 8;  // tiles >= ty hold y rows
+  const bool lit = m.literal != 0;
+  auto m2_tile = [&](int tile) {
+    const double* ap = mp + m.off_M2t + (int64_t)tile * kt2 * 32 + lane;
+    double d[2] = {0.0, 0.0};
+    for (int kt = 0; kt < kt2; ++kt) {
+      const int kk = kt * 4 + t4;
+      mma_f64(d, (double)__ldg(ap + kt * 32), (g == 0 && kk < nY) ? (double)v.sU[kk] : 0.0);
+    }
+    const int r = tile * 8 + g;
+    if (t4 == 0 && r < m2) {
+      if (r < q1) xout[r] = (T)((double)bsc.SO[q2 + r] + d[0]);
+      else v.sy[r - q1] = (T)((lit ? 0.0 : -(double)bsc.SO[q2 + r]) + d[0]);
+    }
+  };
+  if (rg) {
+    __syncthreads();  // the energy above read sy
+    for (int tile = ty + warp; tile < mt2; tile += nw) m2_tile(tile);
+  }
+  if (worker)
+    for (int tile = c1 * nw + warp; tile < ty; tile += G1 * nw) m2_tile(tile);
+  if (worker)
+    for (int r = c1 * nt + tid; r < q2; r += G1 * nt) xout[q1 + r] = bsc.SO[r];
+  grid.sync();
 }
 
 template <typename T>
@@ -880,14 +1061,19 @@ struct BatchShared {
 // more column / row on the right / top, holes excluded) with their bottom Ex and left Ey edges;
 // y^{n+K}; the ROM state.  Their energy (which the sweep skipped) and the zone probes are
 // recorded here for every step of the pass.  Every region phase runs over the whole batch at once.
-template <typename T, int K, bool ENERGY>
-__device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[K], int64_t step, BatchShared& bs) {
+template <typename T, int K, bool ENERGY, bool BIG = false>
+__device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[K], int64_t step, BatchShared& bs,
+                            double* part = nullptr) {
   const int* bt = p.batch_tab + 5 * bi;  // (model, first instance, count, slots B, region stride)
   const int model = bt[0], first = bt[1], nb = bt[2], B = bt[3], rstride = bt[4];
   const RomModelDev m = p.models[model];
   const int nY = m.nY;
   const int64_t S = (int64_t)(m.q1 + m.q2 + nY) * B;  // vector stride of this batch's layout
   const int tid = threadIdx.x, nt = blockDim.x;
+  // BIG (one instance on the whole cooperative grid): only CTA 0 holds the region; the others take
+  // part in the ROM step only (nr = 0 empties every region loop of theirs)
+  const bool rg = !BIG || blockIdx.x == 0;
+  const int nr = rg ? nb : 0;
   const int64_t nYB = (int64_t)nY * B;
   T* reg = rom_end(sv, S, nYB, B);
   const RomConst<T> rc(sv, S, nYB);
@@ -909,8 +1095,8 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   auto ZE = [&](int b) { return reg + (int64_t)b * rstride + 4 * n + Wr + Hr * W1; };
   FCHK(4 * n + Wr + Hr * W1 + nz <= rstride &&
        (size_t)((char*)(reg + (int64_t)B * rstride) - (char*)sv) <= p.smem_bytes);  // regions inside the launch
-  for (int64_t k = tid; k < NROMVEC * S; k += nt) sv[k] = T(0);
-  for (int b = tid; b < nb; b += nt) {
+  for (int64_t k = tid; rg && k < NROMVEC * S; k += nt) sv[k] = T(0);
+  for (int b = tid; b < nr; b += nt) {
     const int32_t* r = p.rects + 4 * (int64_t)(first + b);
     const int64_t lr0 = (int64_t)r[1] - M - p.row_begin + p.row0;  // local row of region row 0
     bs.gbase[b] = lr0 * P + r[0] - M;
@@ -926,19 +1112,23 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   T* sh = sv + 2 * S;
   // ---- load the regions: materials and the fields at step n (asynchronous element copies, all in
   // flight at once: the region rows are not 16-byte aligned)
-  for (Flat f(tid, nt, 0, Wr, 0, Hr); f.b < nb; f.next()) {
+  for (Flat f(tid, nt, 0, Wr, 0, Hr); f.b < nr; f.next()) {
     const int64_t o = bs.gbase[f.b] + (int64_t)f.v * P + f.u;
     const int t = f.v * Wr + f.u;
     cp_async_el(MA(f.b) + t, p.mea + o);
     cp_async_el(MS(f.b) + t, p.msb + o);
     cp_async_el(H(f.b) + t, p.hz0 + o);
   }
-  for (Flat f(tid, nt, 0, Wr, 0, Hr + 1); f.b < nb; f.next())
+  for (Flat f(tid, nt, 0, Wr, 0, Hr + 1); f.b < nr; f.next())
     cp_async_el(EX(f.b) + f.v * Wr + f.u, p.ex0 + bs.gbase[f.b] + (int64_t)f.v * P + f.u);
-  for (Flat f(tid, nt, 0, W1, 0, Hr); f.b < nb; f.next())
+  for (Flat f(tid, nt, 0, W1, 0, Hr); f.b < nr; f.next())
     cp_async_el(EY(f.b) + f.v * W1 + f.u, p.ey0 + bs.gbase[f.b] + (int64_t)f.v * P + f.u);
-  load_rom_state(p, m, first, nb, B, sv);
-  for (int it = tid; it < nY * nb; it += nt) {  // per-pass constants of the batch's ports (RomConst)
+  if (!BIG) load_rom_state(p, m, first, nb, B, sv);  // (BIG: the ROM step reads x~ from global memory)
+  for (int it = tid; FDTD_SKPF && it < nr * ((nY * nY + 31) / 32); it += nt) {  // the batch's Schur inverses into L2
+    const int b = it % nb, l = it / nb;
+    prefetch_l2(p.Sk + p.Sk_off[first + b] + l * 32);
+  }
+  for (int it = tid; it < nY * nr; it += nt) {  // per-pass constants of the batch's ports (RomConst)
     const int i = it % nY, b = it / nY;
     const int64_t po = p.port_off[first + b] + i;
     rc.eh[i * B + b] = p.ehalf[po];
@@ -954,7 +1144,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   for (int s = 0; s < K; ++s) {
     const int cw = Wr - 2 * s, ch = Hr - 2 * s;
     // ---- H half-step (+ source, + the zone cells' storage-function terms of W^{n+s})
-    for (Flat f(tid, nt, s, cw, s, ch); f.b < nb; f.next()) {
+    for (Flat f(tid, nt, s, cw, s, ch); f.b < nr; f.next()) {
       const int u = f.u, v = f.v, b = f.b;
       const T* ex = EX(b);
       const T* ey = EY(b);
@@ -980,7 +1170,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     }
     __syncthreads();
     // ---- zone probes; S4 gather of y^{n+s} (interface edges) and h = Hz^{n+s+1/2} (outside cells)
-    for (int b = 0; b < nb; ++b) {
+    for (int b = 0; b < nr; ++b) {
       const int z0 = p.zp_off[first + b], z1 = p.zp_off[first + b + 1];
       if (z0 == z1) continue;
       const int32_t* r = p.rects + 4 * (int64_t)(first + b);
@@ -990,7 +1180,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
         p.probe_ring[(int64_t)p.zp[3 * z + 2] * p.cap + (step + s) % p.cap] = H(b)[v * Wr + u];
       }
     }
-    for (int it = tid; it < nY * nb; it += nt) {
+    for (int it = tid; it < nY * nr; it += nt) {
       const int i = it % nY, b = it / nY;
       const T* ex = EX(b);
       const T* ey = EY(b);
@@ -1012,7 +1202,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     }
     if (ENERGY) {  // zone energy per instance, fixed order (one warp per instance)
       const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
-      for (int b = w; b < nb; b += nw) {
+      for (int b = w; b < nr; b += nw) {
         const T* ze = ZE(b);
         double acc = 0.0;
         for (int i = lane; i < nz; i += 32) acc += (double)ze[i];
@@ -1024,12 +1214,13 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     __syncthreads();
     // ---- S5: ROM step n+s -> y^{n+s+1}, x~^{n+s+1}; ROM energy of W^{n+s}
     double* eout = p.rom_partials + (int64_t)s * p.n_inst + first;
-    rom_step<T, ENERGY>(p, m, first, nb, B, S, sv, eout);
-    if (ENERGY && tid < nb) eout[tid] += bs.zsum[tid];
+    if constexpr (BIG) rom_step_big<T, ENERGY>(p, m, first, s, sv, S, eout, part);
+    else rom_step<T, ENERGY>(p, m, first, nb, B, S, sv, eout);
+    if (ENERGY && tid < nr) eout[tid] += bs.zsum[tid];
     // ---- S6: y^{n+s+1} into the regions' interface edges, and in the same phase the E half-step
     // on the regions' live edges (dead edges -- interface, PEC, hole -- keep their value: they are
     // skipped, so the scatter and the update never touch the same edge)
-    for (int it = tid; it < nY * nb; it += nt) {
+    for (int it = tid; it < nY * nr; it += nt) {
       const int i = it % nY, b = it / nY;
       const T y = sy[i * B + b];
       T* ex = EX(b);
@@ -1039,7 +1230,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       else if (i < 2 * bx + by) ey[(M + i - 2 * bx) * W1 + M] = y;
       else ey[(M + i - 2 * bx - by) * W1 + M + bx] = y;
     }
-    for (Flat f(tid, nt, s, cw, s + 1, ch - 1); f.b < nb; f.next()) {  // Ex edge rows s+1 .. Hr-s-1,
+    for (Flat f(tid, nt, s, cw, s + 1, ch - 1); f.b < nr; f.next()) {  // Ex edge rows s+1 .. Hr-s-1,
       const int t = f.v * Wr + f.u;                                       // columns s .. Wr-s-1
       const T* ma = MA(f.b);
       const T* ms = MS(f.b);
@@ -1050,7 +1241,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       edge_coef(ma[t - Wr], ms[t - Wr], ma[t], ms[t], p.idy, ca, cb, a, l);
       if (l) ex[t] = eupd(ex[t], ca, cb, hz[t] - hz[t - Wr]);
     }
-    for (Flat f(tid, nt, s + 1, cw - 1, s, ch); f.b < nb; f.next()) {  // Ey edge columns s+1 .. Wr-s-1,
+    for (Flat f(tid, nt, s + 1, cw - 1, s, ch); f.b < nr; f.next()) {  // Ey edge columns s+1 .. Wr-s-1,
       const int c = f.v * Wr + f.u;                                       // rows s .. Hr-s-1
       const T* ma = MA(f.b);
       const T* ms = MS(f.b);
@@ -1065,7 +1256,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   }
   // ---- write back the zones: Hz of the live zone cells, their bottom Ex and left Ey edges
   if (nz > 0)
-    for (Flat f(tid, nt, zu0, zw, zv0, zv1 - zv0); f.b < nb; f.next()) {
+    for (Flat f(tid, nt, zu0, zw, zv0, zv1 - zv0); f.b < nr; f.next()) {
       const int t = f.v * Wr + f.u;
       if (!(MA(f.b)[t] >= T(0))) continue;
       const int64_t o = bs.gbase[f.b] + (int64_t)f.v * P + f.u;
@@ -1074,6 +1265,13 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       p.ex1[o] = EX(f.b)[t];
       p.ey1[o] = EY(f.b)[f.v * W1 + f.u];
     }
+  if constexpr (BIG) {  // the final x~ from the scratch into the slot store_rom reads
+    if (!rg) return;
+    const BigScratch<T> bsc(p.big, m);
+    const T* xf = ((K - 1) & 1) ? bsc.X1 : bsc.X0;
+    for (int i = tid; i < m.q1 + m.q2; i += nt) sv[i] = xf[i];
+    __syncthreads();
+  }
   store_rom(p, m, first, nb, B, S, sv, p.ex1, p.ey1);
 }
 
@@ -1094,8 +1292,8 @@ __global__ void __launch_bounds__(512, 1) postk_kernel(const PostParams<T> p) {
       if (k >= 0 && k < p.src_meta[1]) g[s] = (T)p.src_samples[k];
     }
   }
-  if (b < p.n_batch) fixup_batch<T, K, ENERGY>(p, b, sv, g, step, bs);
-  if (ENERGY && b < p.n_batch) {  // this batch's ROM + zone energies, one value per step (level 1)
+  if (b < p.n_batch_reg) fixup_batch<T, K, ENERGY>(p, b, sv, g, step, bs);
+  if (ENERGY && b < p.n_batch_reg) {  // this batch's ROM + zone energies, one value per step (level 1)
     __syncthreads();              // rom_partials of this batch written (fixup_batch ends with barriers)
     const int first = p.batch_tab[5 * b + 1], nb = p.batch_tab[5 * b + 2];
 #pragma unroll 1
@@ -1105,6 +1303,40 @@ __global__ void __launch_bounds__(512, 1) postk_kernel(const PostParams<T> p) {
       const double tot = block_sum(v, red);
       if (threadIdx.x == 0) p.level1[(int64_t)s * p.n_batch + b] = tot;
     }
+  }
+}
+
+// The large-model fix-up (one instance at a time on a cooperative grid of one CTA per SM): the
+// batches [n_batch_reg, n_batch), each a single instance of a model of order >= the big threshold.
+template <typename T, int K, bool ENERGY>
+__global__ void __launch_bounds__(512, 1) bigrom_kernel(const PostParams<T> p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[32];
+  __shared__ BatchShared bs;
+  __shared__ double part[16 * 8];  // phase-1 partials: [warp][row]
+  T* sv = reinterpret_cast<T*>(smem_raw);
+  const int64_t step = *p.step;
+  T g[K];
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    g[s] = T(0);
+    if (p.src_row >= 0) {
+      const int64_t k = step + s - p.src_meta[0];
+      if (k >= 0 && k < p.src_meta[1]) g[s] = (T)p.src_samples[k];
+    }
+  }
+  for (int b = p.n_batch_reg; b < p.n_batch; ++b) {
+    fixup_batch<T, K, ENERGY, true>(p, b, sv, g, step, bs, part);
+    if (ENERGY && blockIdx.x == 0) {
+      __syncthreads();
+      const int first = p.batch_tab[5 * b + 1];
+#pragma unroll 1
+      for (int s = 0; s < K; ++s) {
+        const double tot = block_sum(threadIdx.x == 0 ? p.rom_partials[(int64_t)s * p.n_inst + first] : 0.0, red);
+        if (threadIdx.x == 0) p.level1[(int64_t)s * p.n_batch + b] = tot;
+      }
+    }
+    cooperative_groups::this_grid().sync();  // the scratch is reused by the next instance
   }
 }
 
@@ -1477,7 +1709,8 @@ size_t post_smem_bytes(size_t es, int nvec, int nY, int batch, int region_stride
 template <typename T, int K>
 void postk_launch(const PostParams<T>& p, bool energy, cudaStream_t s) {
   const size_t smem = p.smem_bytes;
-  const int grid = p.n_batch;
+  const int grid = p.n_batch_reg;
+  if (grid <= 0) return;
   if (energy) {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(postk_kernel<T, K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1490,6 +1723,45 @@ void postk_launch(const PostParams<T>& p, bool energy, cudaStream_t s) {
 }
 
 void launch_finalize(const FinParams& p, cudaStream_t s) { finalize_kernel<<<p.energy ? FIN_GRID : 1, 256, 0, s>>>(p); }
+
+template <typename T, int K, bool ENERGY>
+void bigrom_launch(const PostParams<T>& p, cudaStream_t s) {
+  auto kern = bigrom_kernel<T, K, ENERGY>;
+  const size_t smem = p.big_smem_bytes;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.big_grid);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+template <typename T>
+void launch_post_big(const PostParams<T>& p, int K, bool energy, cudaStream_t s) {
+  if (p.n_batch <= p.n_batch_reg) return;
+  if (K == 1) energy ? bigrom_launch<T, 1, true>(p, s) : bigrom_launch<T, 1, false>(p, s);
+  else if (K == 2) energy ? bigrom_launch<T, 2, true>(p, s) : bigrom_launch<T, 2, false>(p, s);
+  else if constexpr (sizeof(T) == 4) energy ? bigrom_launch<T, 4, true>(p, s) : bigrom_launch<T, 4, false>(p, s);
+}
+
+// co-resident CTAs of the large-model kernel (one per SM), 0 if it cannot be launched cooperatively
+template <typename T>
+int big_grid_size(size_t smem, int K) {
+  int dev = 0, nsm = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  auto kern = K == 1 ? bigrom_kernel<T, 1, true> : bigrom_kernel<T, 2, true>;
+  if constexpr (sizeof(T) == 4) if (K == 4) kern = bigrom_kernel<T, 4, true>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 512, smem) != cudaSuccess || per < 1) return 0;
+  return nsm;
+}
 
 template <typename T>
 void launch_post(const PostParams<T>& p, int K, bool energy, cudaStream_t s) {
@@ -1558,6 +1830,8 @@ void launch_band_marks(T* msb, const T* mea, int64_t pitch, int64_t nx, int row0
 #define INST(T)                                                                                     \
   template void launch_sweep<T>(const SweepParams<T>&, int, int, cudaStream_t, int, int);         \
   template void launch_post<T>(const PostParams<T>&, int, bool, cudaStream_t);                   \
+  template void launch_post_big<T>(const PostParams<T>&, int, bool, cudaStream_t);               \
+  template int big_grid_size<T>(size_t, int);                                                     \
   template void launch_materials<T, float>(const float*, const float*, int64_t, int64_t, int64_t, int64_t, \
                                            int64_t, int, int, int64_t, double, T*, T*, cudaStream_t);     \
   template void launch_materials<T, double>(const double*, const double*, int64_t, int64_t, int64_t,      \

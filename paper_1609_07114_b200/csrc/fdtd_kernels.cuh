@@ -71,12 +71,12 @@ struct SweepParams {
 //   M2 ((q1 + nY) x nY) = [Bq; L~^T Bq]  -> [E~ - E*; y - L~^T E*] from U
 //   Rt ((q1 + q2) x (q1 + q2)) = [[R~11/dt, -K~/2], [-K~^T/2, R~22/dt]]  (storage function)
 // The fix-up's GEMMs run on the FP64 tensor cores (mma.sync.m8n8k4.f64, fdtd_kernels.cu
-// dmma_gemm): [M1; R~] and M2 are kept in an fp64 pool pre-tiled in the MMA's A-fragment order
+// dmma_gemm): [M1; R~] and M2 are kept in an fp64 pool, pre-tiled in the MMA's A-fragment order
 // (mt x kt tiles of 8 x 4, one double per lane and tile).
 struct RomModelDev {
   int nY, q1, q2;
   int literal;  // paper-literal coupling: U is y^{n+1} itself and M2 = [Z T; I] (K3)
-  int64_t off_M1t, off_M2t;     // tiled operators in the fp64 pool
+  int64_t off_M1t, off_M2t;     // tiled operators in the pool
   int mt1, kt1, mt2, kt2;       // their tile counts: [M1; R~] (m1 + q1 + q2 rows), M2 (q1 + nY rows)
 };
 
@@ -88,10 +88,12 @@ struct RomModelDev {
 template <typename T>
 struct PostParams {
   int n_inst;
-  int n_batch;                     // CTAs doing ROM work; batches of <= batch instances of one model
+  int n_batch;                     // batches of <= batch instances of one model (level-1 energy slots)
+  int n_batch_reg;                 // batches [0, n_batch_reg): postk_kernel; the rest are single
+                                   // instances of large models (bigrom_kernel, cooperative)
   const int32_t* batch_tab;        // per batch: (model, first instance, count, slots B, region stride)
   const RomModelDev* models;
-  const double* mpool64;           // shared model operators, fp64, tiled for the DMMA GEMMs
+  const double* mpool;             // shared model operators (fp64), tiled for the DMMA GEMMs
   const T* Sk; const int64_t* Sk_off;        // per-instance Schur inverses (col-major nY x nY)
   const int64_t* port_off;                    // per-instance offset into port arrays
   const T* cya; const T* cyg;                 // a_y / c_y, D_l G / c_y per port
@@ -115,6 +117,8 @@ struct PostParams {
   int block;         // threads per CTA
   size_t smem_bytes; // dynamic shared memory of the launch (max over batches)
   int* flag;         // non-finite sentinel: set to 1 when a stored ROM state is not finite
+  T* big;            // bigrom_kernel scratch (x~ twice, [M1; R~] x~, y and h of the largest model)
+  size_t big_smem_bytes; int big_grid;
   int64_t alloc_elems; int rows, n_probe;  // FDTD_CHECK bounds: array elements, owned rows, probes
 };
 
@@ -181,6 +185,10 @@ inline int sweep_ctas_x(int64_t nx, int elem_bytes, int K, int warps_per_cta) {
 }
 template <typename T>
 void launch_post(const PostParams<T>& p, int K, bool energy, cudaStream_t s);
+template <typename T>
+void launch_post_big(const PostParams<T>& p, int K, bool energy, cudaStream_t s);
+template <typename T>
+int big_grid_size(size_t smem, int K);
 // shared-memory bytes of the fix-up kernel for a given batch (host-side sizing)
 size_t post_smem_bytes(size_t es, int nvec, int nY, int batch, int region_stride);
 // elements of one instance region for zone depth Kz and pass depth K (<= Kz)

@@ -373,3 +373,47 @@ def test_degenerate_roms(precision):
                  probes=np.array([[30, 30], [20, 18], [11, 25]], np.int32), models=[m_q2, m_full],
                  placements=np.array([[0, 18, 18], [0, 26, 12], [1, 12, 24]], np.int32))
     _compare(s, 500, 1e-10 if precision == 64 else 1e-4, random_init=7)
+
+
+# ----------------------------------------------------------------- the large-model cooperative path
+@pytest.fixture
+def big_path(monkeypatch):
+    """Route every model through bigrom_kernel (FDTD_BIG_Q = 1: the whole-GPU one-instance path)."""
+    monkeypatch.setenv("FDTD_BIG_Q", "1")
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_big_rom_path_parity(big_path, precision):
+    """Several instances of two models (a lossy inclusion and the literal coupling) on the cooperative
+    large-model path: the oracle's LU route to 1e-10 (fp64) / 1e-4 (fp32), per instance too."""
+    s = _ragged_scene(130, 61, precision)
+    _compare(s, 600, 1e-10 if precision == 64 else 1e-4, random_init=5)
+
+
+def test_big_rom_path_literal_fp64(big_path):
+    s = _literal_scene(64)
+    _compare(s, 400, 1e-10, random_init=5)
+
+
+def test_big_rom_path_k_bitwise(big_path):
+    """K = 1, 2, 4 steps per pass agree bit for bit on the large-model path too."""
+    s = configs.make("cfg3", n=256)
+    outs = []
+    for spp in (1, 2, 4):
+        g = gpu_from_scene(s)
+        g.set_time_blocking(spp)
+        Ex, Ey, Hz, xs = consistent_random_state(s, 13)
+        g.set_window(0, 0, Ex, Ey, Hz)
+        g.set_rom_state(xs)
+        g.record_energy(True)
+        for n in (1, 2, 3, 5, 8, 40, 1, 7):
+            g.step(n)
+        assert g.info().steps_per_pass == spp
+        outs.append((g.get_window(), g.get_rom_state(), g.probe(), g.energy()))
+        g.close()
+    for (w, x, p, e) in outs[1:]:
+        for a, b in zip(outs[0][0], w):
+            assert np.array_equal(a, b)
+        assert np.array_equal(outs[0][1], x)
+        assert np.array_equal(outs[0][2], p)
+        np.testing.assert_allclose(e, outs[0][3], rtol=2e-6)
