@@ -157,6 +157,7 @@ struct fdtd_ctx {
   int graph_steps = 0;
   int64_t graph_launches = 0;
   int64_t graph_builds = 0;
+  bool graph_broken = false;
   int64_t launches = 0;
   // profiling (event pairs around each launch)
   bool profiling = false;
@@ -534,6 +535,7 @@ fdtd_status enqueue_pass(fdtd_ctx* c, int q, cudaStream_t s, int K) {
       fdtd_status st2 = edges_beside(c->ev_halo);
       if (st2 != FDTD_OK) return st2;
       CK(cudaStreamWaitEvent(s, c->ev_edge, 0));
+      CK(cudaStreamWaitEvent(s, c->ev_halo, 0));  // join the comm stream too (graph capture)
     } else {
       CK(cudaStreamWaitEvent(s, c->ev_halo, 0));
       sweep(0, lo);
@@ -1520,15 +1522,25 @@ fdtd_status fdtd_step(fdtd_ctx* c, int64_t nsteps) {
   if (c->steps + nsteps - oldest > c->cap)
     return fail(c, FDTD_E_STATE, "unread records would exceed record_capacity (%lld)", (long long)c->cap);
   if (c->d.flags & FDTD_LOCAL_GROUP) return fail(c, FDTD_E_STATE, "members of a local group step with fdtd_step_group");
-  const bool use_graph = !(c->d.flags & FDTD_NO_GRAPH) && c->d.nranks == 1 && !c->profiling;
+  // graphs also with NCCL ranks (the halo send/recv group and the split sweeps are captured with
+  // the side streams forked and joined by events); a capture that fails falls back to eager passes
+  const bool use_graph = !(c->d.flags & FDTD_NO_GRAPH) && !(c->d.flags & FDTD_LOCAL_GROUP) && !c->profiling &&
+                         !c->graph_broken;
   fdtd_status st = configure_passes(c);
   if (st != FDTD_OK) return st;
   int64_t left = nsteps;
   while (left > 0) {
     const int per = 2 * c->kz;
     if (use_graph && c->cur == 0 && left >= per) {
-      if (c->graph_dirty || !c->gexec || c->graph_steps != per)
-        if ((st = build_graph(c)) != FDTD_OK) return st;
+      if (c->graph_dirty || !c->gexec || c->graph_steps != per) {
+        if ((st = build_graph(c)) != FDTD_OK) {
+          if (st != FDTD_E_CUDA) return st;
+          c->graph_broken = true;  // e.g. a launch the runtime cannot capture: stay eager
+          cudaGetLastError();
+          drop_graph(c);
+          continue;
+        }
+      }
       CK(cudaGraphLaunch(c->gexec, c->stream));
       c->launches += c->graph_launches;
       c->steps += per;
@@ -1854,7 +1866,7 @@ fdtd_status fdtd_get_info(const fdtd_ctx* c, fdtd_info* o) {
   o->kernel_launches = c->launches;
   o->pitch = c->pitch;
   o->sweep_ctas = c->n_partials;
-  o->graphs = !(c->d.flags & FDTD_NO_GRAPH) && c->d.nranks == 1;
+  o->graphs = !(c->d.flags & FDTD_NO_GRAPH) && !(c->d.flags & FDTD_LOCAL_GROUP) && !c->graph_broken;
   o->precision = c->prec;
   o->steps_per_pass = c->kz;
   // read Ex, Ey, Hz, mea, msb and write Ex, Ey, Hz once per pass
