@@ -35,6 +35,8 @@ WORKLOADS = {
     "cfg4": "BASELINE config 4: 32768^2 fp32 coarse TEz grid, copula medium eps_r U[1,10] sigma U[0,0.1] l=32, "
             "4096 instances of one ROM (16x16 coarse block, r=4, disc inclusion, q=128, clipped at 2 dt_f), "
             "dt = 1.9 dt_f, Gaussian source, 64 probes, energy every step",
+    "cfg4dense": "BASELINE config 4 with SURVEY Q19's placement rule (footprint + one-cell ring disjoint, 1 cell "
+                 "from the walls and slab rows): close instances are fixed up as clusters",
     "cfg3": "BASELINE config 3: 8192^2 fp32, 1024 instances of one ROM (8x8 block, r=8, q=64), dt = 1.9 dt_f",
     "cfg2": "BASELINE config 2: 8192^2 fp32 plain grid, no ROMs, dt = 0.99 eq.(1)",
     "cfg5": "BASELINE config 5: 49152^2 fp32, copula medium, 32 distinct ROM models (b 4..32, r 4..10, "

@@ -220,6 +220,9 @@ typedef struct {
   void *sweep_stream;          /* cudaStream_t the kernels are launched on                 */
   int64_t graph_builds;        /* CUDA graphs captured so far (a new source window on the same
                                   cells, or a new probe/energy read, keeps the graph)          */
+  int32_t fixup_clusters;      /* fix-up regions shared by several instances closer than the pass
+                                  depth allows                        */
+  int32_t big_instances;       /* instances on the cooperative large-model path                */
 } fdtd_info;
 fdtd_status fdtd_get_info(const fdtd_ctx *c, fdtd_info *out);
 

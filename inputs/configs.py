@@ -16,6 +16,7 @@ sub-instances are the "seeded cropped sub-instances" the oracle can finish.
          q=64; clip at 2 dt_f; dt = 1.9 dt_f; 10000 steps.
   cfg4   32768^2 fp32 medium as cfg2 + 4096 placements: 16x16 block, r=4, inclusion,
          q=128; clip at 2 dt_f; dt = 1.9 dt_f; 5000 steps.
+  cfg4dense  cfg4 with SURVEY Q19's placement rule (one-cell rings disjoint, 1 cell from the walls).
   cfg5   49152^2 fp32, 32 models (b U{4..32}, r U{4..10}, q U{32,64,128,256}, fill
          eps_r U[1,12], sigma U[0,0.2]), 8192 placements; dt = 1.9 min dt_f; 2000 steps.
 """
@@ -91,7 +92,7 @@ def _medium(n, seed, device, lo_e=1.0, hi_e=10.0, hi_s=0.1):
     return eps, sig
 
 
-def _grid_scene(name, N, n, device, steps, rom=None, count=0, seed=100):
+def _grid_scene(name, N, n, device, steps, rom=None, count=0, seed=100, dense=False):
     n = N if n is None else int(n)
     eps, sig = _medium(n, seed, device)
     dtc = sc.cfl_limit(DX, DY, eps_r_min=1.0)  # c_max: eps_r >= 1 everywhere
@@ -106,8 +107,12 @@ def _grid_scene(name, N, n, device, steps, rom=None, count=0, seed=100):
         m = rg.extend_cfl(m0, 2.0 * dtf)
         dt = min(1.9 * dtf, 0.99 * dtc)
         cnt = max(1, int(round(count * (n / N) ** 2)))
+        # dense: SURVEY Q19's own rule -- footprint + one-cell ring inside the grid and the slab, rings
+        # pairwise disjoint (instances may sit 2 cells apart and next to the walls: the fix-up then
+        # merges close instances into clusters); default: 7 / 4 cells
         placements = sc.place_blocks(n, n, [(b, b)], cnt, seed + 5, nslabs=8 if n % 8 == 0 else 1,
-                                     forbid=[src] + [tuple(p) for p in probes])
+                                     forbid=[src] + [tuple(p) for p in probes],
+                                     **(dict(margin=1, clear=1) if dense else {}))
         models = [m]
     samples = sc.gaussian_samples(steps, dt, fmax, derivative=False)
     return sc.Scene(name=name, nx=n, ny=n, dx=DX, dy=DY, dt=dt, eps_r=eps, sigma=sig, precision=32,
@@ -165,6 +170,8 @@ def make(name, n=None, device="cpu", **kw):
         return _grid_scene("cfg3", 8192, n, device, 10000, rom=(8, 8, 64), count=1024, seed=300)
     if name == "cfg4":
         return _grid_scene("cfg4", 32768, n, device, 5000, rom=(16, 4, 128), count=4096, seed=400)
+    if name == "cfg4dense":  # cfg4 with SURVEY Q19's one-cell-ring placement rule
+        return _grid_scene("cfg4dense", 32768, n, device, 5000, rom=(16, 4, 128), count=4096, seed=400, dense=True)
     if name == "cfg5":
         return _cfg5(n, device, **kw)
     raise KeyError(name)

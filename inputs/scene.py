@@ -82,7 +82,7 @@ def place_blocks(nx, ny, sizes, count, seed, nslabs=8, forbid=(), max_tries=2_00
     outside every footprint plus ring (source, probes).
     Returns int32 array (count, 3): (model, i0, j0).
     """
-    assert margin >= 2 and clear >= 1
+    assert margin >= 1 and clear >= 1
     rng = np.random.default_rng(seed)
     slab = ny // nslabs if nslabs > 1 and ny % nslabs == 0 else ny
     forbid = [(int(i), int(j)) for i, j in forbid]

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <array>
+#include <functional>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -137,8 +138,14 @@ struct fdtd_ctx {
   std::vector<double> cya, cyg, ehalf, Sk;  // fp64 host copies (converted on upload)
   std::vector<double> mpool;                // shared model operators tiled for the DMMA GEMMs (fp64)
   int nvec = 1;
-  std::vector<int32_t> batch_tab;  // (model, first instance, count, slots B, region stride)
+  std::vector<int32_t> batch_tab;  // (model, member offset, count, slots B, region stride, kind)
+  std::vector<int32_t> batch_inst, batch_rect;  // batch members; cluster boxes (kind 1)
   int32_t* d_batch_tab = nullptr;
+  int32_t* d_batch_inst = nullptr;
+  int32_t* d_batch_rect = nullptr;
+  std::vector<int32_t> zone_marked;  // the zone boxes whose cells carry the msb marks (kz_marked deep)
+  int32_t* d_zone_marked = nullptr;
+  int n_clusters = 0;
   int post_grid = 1;
   int n_batch_reg = 0;           // regular fix-up batches; the rest are large-model instances
   void* d_big = nullptr;         // bigrom_kernel scratch
@@ -310,10 +317,14 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
   p.rom_partials = c->d_rom_partials;
   p.level1 = c->d_level1;
   p.step = c->d_step;
-  p.n_batch = c->inst_model.empty() ? 0 : (int)(c->batch_tab.size() / 5);
+  p.n_batch = c->inst_model.empty() ? 0 : (int)(c->batch_tab.size() / fdtd::BATCH_FIELDS);
   p.n_batch_reg = c->inst_model.empty() ? 0 : c->n_batch_reg;
   p.big = (T*)c->d_big; p.big_smem_bytes = c->big_smem; p.big_grid = c->big_grid;
   p.batch_tab = c->d_batch_tab;
+  p.batch_inst = c->d_batch_inst;
+  p.batch_rect = c->d_batch_rect;
+  p.nx = c->d.nx;
+  p.ny = c->d.ny;
   p.block = c->post_threads;
   p.smem_bytes = c->post_smem;
   p.flag = c->d_flag;
@@ -337,7 +348,7 @@ fdtd::FinParams fin_params(fdtd_ctx* c, int K, int q) {
                        (c->pml_w > 0 ? fdtd::pml_ctas(c->rows, PML_CHUNK) : 0);  // + the CPML band CTAs
   f.pstride = c->n_partials;
   f.rom_level1 = c->d_level1;
-  f.n_rom = c->inst_model.empty() ? 0 : (int)(c->batch_tab.size() / 5);
+  f.n_rom = c->inst_model.empty() ? 0 : (int)(c->batch_tab.size() / fdtd::BATCH_FIELDS);
   f.level2 = c->d_level2;
   f.energy_ring = c->d_energy_ring; f.cap = c->cap;
   f.step = c->d_step; f.done = c->d_done;
@@ -513,7 +524,7 @@ fdtd_status enqueue_pass(fdtd_ctx* c, int q, cudaStream_t s, int K) {
     if (c->prec == 64) fdtd::launch_post<double>(post_params<double>(c, q), K, c->energy_on, st);
     else fdtd::launch_post<float>(post_params<float>(c, q), K, c->energy_on, st);
     c->launches += c->n_batch_reg > 0;
-    if ((int)(c->batch_tab.size() / 5) > c->n_batch_reg) {  // large models: the cooperative fix-up
+    if ((int)(c->batch_tab.size() / fdtd::BATCH_FIELDS) > c->n_batch_reg) {  // large models: the cooperative fix-up
       if (c->prec == 64) fdtd::launch_post_big<double>(post_params<double>(c, q), K, c->energy_on, st);
       else fdtd::launch_post_big<float>(post_params<float>(c, q), K, c->energy_on, st);
       c->launches += 1;
@@ -696,10 +707,84 @@ fdtd_status upload_roms(fdtd_ctx* c) {
   return FDTD_OK;
 }
 
-// Can this rank run K-step passes (K3)?  Every instance's fix-up region (block + 2K-1
-// cells) must lie inside the grid columns and inside this slab's rows, and the (block + K)
-// rectangles of two instances must not meet (so the fix-up of one never needs the other's ROM and
-// the zones are disjoint).
+// The fix-up regions of a K-step pass: instances whose (block + K)
+// rectangles meet, directly or through others, share one region -- their bounding box plus the
+// margin -- and are fixed up together by one CTA (a "cluster"); every other instance has its own.
+// Two regions' (block + K) boxes never meet, so no fix-up needs another's ROM within the K steps.
+struct PassRegion {
+  int model = -1;
+  bool mixed = false;            // members of different models (not supported: a shallower pass)
+  std::vector<int> members;      // instance indices, ascending
+  int64_t i0 = 0, j0 = 0, i1 = 0, j1 = 0;  // bounding box of the blocks [i0, i1) x [j0, j1)
+};
+
+std::vector<PassRegion> pass_regions(const fdtd_ctx* c, int K) {
+  // Start from one region per instance and merge any two regions whose boxes, grown by K, meet --
+  // with the merged (bounding) boxes, until no pair meets: then no region's box + 2K - 1 reaches
+  // into another region, whatever the shape of a cluster.
+  const int n = (int)c->inst_model.size();
+  std::vector<PassRegion> cur(n);
+  for (int i = 0; i < n; ++i) {
+    PassRegion& g = cur[i];
+    g.model = c->inst_model[i];
+    g.members = {i};
+    g.i0 = c->rects[4 * i]; g.j0 = c->rects[4 * i + 1];
+    g.i1 = g.i0 + c->rects[4 * i + 2]; g.j1 = g.j0 + c->rects[4 * i + 3];
+  }
+  if (K < 2) return cur;
+  for (bool merged = true; merged;) {
+    merged = false;
+    const int m = (int)cur.size();
+    std::vector<int> ord(m), par(m);
+    for (int i = 0; i < m; ++i) ord[i] = par[i] = i;
+    std::function<int(int)> find = [&](int x) { return par[x] == x ? x : par[x] = find(par[x]); };
+    std::sort(ord.begin(), ord.end(), [&](int a, int b) { return cur[a].i0 < cur[b].i0; });
+    int64_t wmax = 0;
+    for (const PassRegion& g : cur) wmax = std::max(wmax, g.i1 - g.i0);
+    for (int a = 0; a < m; ++a)
+      for (int b = a + 1; b < m && cur[ord[b]].i0 <= cur[ord[a]].i1 + wmax + 2 * K; ++b) {
+        const PassRegion &A = cur[ord[a]], &Bq = cur[ord[b]];
+        const bool ox = A.i0 - K < Bq.i1 + K && Bq.i0 - K < A.i1 + K;
+        const bool oy = A.j0 - K < Bq.j1 + K && Bq.j0 - K < A.j1 + K;
+        if (ox && oy && find(ord[a]) != find(ord[b])) {
+          par[find(ord[a])] = find(ord[b]);
+          merged = true;
+        }
+      }
+    if (!merged) break;
+    std::vector<PassRegion> next;
+    std::vector<int> slot(m, -1);
+    for (int i = 0; i < m; ++i) {  // in instance order of the first members
+      const int r = find(i);
+      if (slot[r] < 0) {
+        slot[r] = (int)next.size();
+        next.push_back(cur[i]);
+        continue;
+      }
+      PassRegion& g = next[slot[r]];
+      g.mixed |= cur[i].mixed || g.model != cur[i].model;
+      g.i0 = std::min(g.i0, cur[i].i0); g.j0 = std::min(g.j0, cur[i].j0);
+      g.i1 = std::max(g.i1, cur[i].i1); g.j1 = std::max(g.j1, cur[i].j1);
+      g.members.insert(g.members.end(), cur[i].members.begin(), cur[i].members.end());
+    }
+    for (PassRegion& g : next) std::sort(g.members.begin(), g.members.end());
+    cur.swap(next);
+  }
+  return cur;
+}
+
+// shared memory of one fix-up batch: B member slots of model m's vectors plus nreg regions of
+// stride rs
+size_t batch_smem(const fdtd_ctx* c, const ModelHost& m, int B, int nreg, int rs) {
+  return fdtd::post_smem_bytes(c->es, m.q1 + m.q2 + m.nY, m.nY, B, 0) + (size_t)nreg * rs * c->es;
+}
+constexpr size_t FIX_BUDGET = 220 * 1024;  // one 512-thread fix-up CTA per SM
+constexpr int MAX_CLUSTER = 64;            // fdtd_kernels.cu MAXB
+
+// Can this rank run K-step passes (K3)?  Every fix-up region (block or cluster box +
+// 2K-1 cells) must lie inside this slab's rows wherever a neighbouring slab continues the grid
+// (beyond the PEC walls the region holds dead cells), a cluster must hold instances of one model
+// only, and its batch must fit the fix-up's shared memory.
 bool passes_valid(const fdtd_ctx* c, int K) {
   if (K > c->V) return false;  // a halo lane of V columns covers at most V steps of error spread
   const int64_t M = 2 * K - 1;
@@ -713,24 +798,16 @@ bool passes_valid(const fdtd_ctx* c, int K) {
         return false;
   }
   if (K == 1) return true;
-  struct Rc { int64_t i0, j0, bx, by; };
-  std::vector<Rc> all;
-  for (size_t r = 0; r < c->rects.size(); r += 4) {
-    Rc x{c->rects[r], c->rects[r + 1], c->rects[r + 2], c->rects[r + 3]};
-    if (x.i0 - M < 0 || x.i0 + x.bx + M > c->d.nx || x.j0 - M < c->d.row_begin || x.j0 + x.by + M > c->d.row_end)
+  for (const PassRegion& g : pass_regions(c, K)) {
+    if (g.mixed || (int)g.members.size() > MAX_CLUSTER) return false;
+    if ((g.j0 - M < c->d.row_begin && c->d.row_begin > 0) || (g.j1 + M > c->d.row_end && c->d.row_end < c->d.ny))
       return false;
-    all.push_back(x);
-  }
-  std::sort(all.begin(), all.end(), [](const Rc& a, const Rc& b) { return a.i0 < b.i0; });
-  int64_t wmax = 0;
-  for (auto& r : all) wmax = std::max(wmax, r.bx);
-  for (size_t a = 0; a < all.size(); ++a)
-    for (size_t b = a + 1; b < all.size() && all[b].i0 <= all[a].i0 + all[a].bx + wmax + 2 * K; ++b) {
-      const Rc &A = all[a], &B = all[b];
-      const bool ox = A.i0 - K < B.i0 + B.bx + K && B.i0 - K < A.i0 + A.bx + K;
-      const bool oy = A.j0 - K < B.j0 + B.by + K && B.j0 - K < A.j0 + A.by + K;
-      if (ox && oy) return false;
+    if (g.members.size() > 1) {
+      const ModelHost& m = c->models[g.model];
+      const int rs = (fdtd::region_elems((int)(g.i1 - g.i0), (int)(g.j1 - g.j0), (int)M) + 3) / 4 * 4;
+      if (batch_smem(c, m, (int)g.members.size(), 1, rs) > FIX_BUDGET) return false;
     }
+  }
   return true;
 }
 
@@ -786,21 +863,32 @@ fdtd_status configure_passes(fdtd_ctx* c) {
 
 fdtd_status apply_passes(fdtd_ctx* c, int k) {
   fdtd_status st;
-  const int64_t n_rect = (int64_t)c->rects.size() / 4;
-  // zone marks: clear those of the previous depth, set those of the new one
-  if (n_rect > 0 && c->kz_marked != k) {
+  const std::vector<PassRegion> regs = pass_regions(c, k);
+  // zone boxes (one per region: an instance's block or a cluster's bounding box)
+  std::vector<int32_t> zr;
+  for (const PassRegion& g : regs)
+    zr.insert(zr.end(), {(int32_t)g.i0, (int32_t)g.j0, (int32_t)(g.i1 - g.i0), (int32_t)(g.j1 - g.j0)});
+  // zone marks: clear those of the previous depth / regions, set those of the new ones
+  if (c->kz_marked != k || c->zone_marked != zr) {
+    int32_t* dz = nullptr;
+    if ((st = upload(c, &dz, zr)) != FDTD_OK) return st;
+    const int64_t n_old = (int64_t)c->zone_marked.size() / 4, n_new = (int64_t)zr.size() / 4;
     if (c->prec == 64) {
-      fdtd::launch_zone<double>((double*)c->coef[1], (const double*)c->coef[0], c->pitch, c->d_rects, n_rect,
+      fdtd::launch_zone<double>((double*)c->coef[1], (const double*)c->coef[0], c->pitch, c->d_zone_marked, n_old,
                                 c->d.row_begin, ROW0, c->kz_marked, false, c->stream);
-      fdtd::launch_zone<double>((double*)c->coef[1], (const double*)c->coef[0], c->pitch, c->d_rects, n_rect,
-                                c->d.row_begin, ROW0, k, true, c->stream);
+      fdtd::launch_zone<double>((double*)c->coef[1], (const double*)c->coef[0], c->pitch, dz, n_new, c->d.row_begin,
+                                ROW0, k, true, c->stream);
     } else {
-      fdtd::launch_zone<float>((float*)c->coef[1], (const float*)c->coef[0], c->pitch, c->d_rects, n_rect,
+      fdtd::launch_zone<float>((float*)c->coef[1], (const float*)c->coef[0], c->pitch, c->d_zone_marked, n_old,
                                c->d.row_begin, ROW0, c->kz_marked, false, c->stream);
-      fdtd::launch_zone<float>((float*)c->coef[1], (const float*)c->coef[0], c->pitch, c->d_rects, n_rect,
-                               c->d.row_begin, ROW0, k, true, c->stream);
+      fdtd::launch_zone<float>((float*)c->coef[1], (const float*)c->coef[0], c->pitch, dz, n_new, c->d.row_begin,
+                               ROW0, k, true, c->stream);
     }
     CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->d_zone_marked) dfree(c, c->d_zone_marked);
+    c->d_zone_marked = dz;
+    c->zone_marked = zr;
   }
   c->kz_marked = k;
   c->kz = k;
@@ -822,14 +910,15 @@ fdtd_status apply_passes(fdtd_ctx* c, int k) {
       c->pml_marked = want;
     }
   }
-  // batches of consecutive instances of one model (instances are stored grouped by model).  Every
-  // model gets its own region stride and batch size under one shared-memory budget per CTA
-  // (~220 KB: one 512-thread fix-up CTA per SM; 8 instances fill the DMMA's N = 8), so small
-  // models are batched 8 at a time and the largest still fits; the launch uses the largest batch
-  // footprint.
+  // Fix-up batches (K3).  Instances with their own region are batched by model, up to 8
+  // per CTA under one shared-memory budget (~220 KB: one 512-thread fix-up CTA per SM; 8 instances
+  // fill the DMMA's N = 8; a row slab with few instances uses smaller batches so that the fix-up's
+  // CTAs still fill one wave); a cluster is one batch of its members around their shared region;
+  // the instances of large models (order >= FDTD_BIG_Q, default 512) take the cooperative
+  // one-instance-at-a-time path (bigrom_kernel), decided by the model alone so that every slab
+  // decomposition runs the same arithmetic.  Batch order: regular batches, then the large ones.
   {
-    // up to 8 instances per CTA; a row slab with few instances uses smaller batches so that the
-    // fix-up's CTAs still fill one wave (it is latency-bound)
+    const int M = 2 * k - 1;
     const char* env = getenv("FDTD_ROM_BATCH");
     int Bauto = 8;
     if (c->d.nranks > 1) {
@@ -839,30 +928,21 @@ fdtd_status apply_passes(fdtd_ctx* c, int k) {
       while (Bauto > 1 && (int64_t)c->inst_model.size() <= (int64_t)(Bauto / 2) * 2 * nsm) Bauto /= 2;
     }
     const int Bmax = env ? std::max(1, std::min(64, atoi(env))) : Bauto;
-    const size_t budget = 220 * 1024;
-    struct Shape { int B, stride; size_t per; };
-    std::vector<Shape> shp;
-    size_t need1 = 0;
-    for (auto& m : c->models) {
-      const int rs = (fdtd::region_elems(m.bx, m.by, 2 * k - 1) + 3) / 4 * 4;
-      const size_t per = fdtd::post_smem_bytes(c->es, m.q1 + m.q2 + m.nY, m.nY, 1, rs);
-      shp.push_back({1, rs, per});
-      need1 = std::max(need1, per);
-    }
-    const size_t cap = std::max(budget, need1);
-    // Large models (order >= FDTD_BIG_Q, default 512) take the cooperative one-instance-at-a-time
-    // path (bigrom_kernel: the whole GPU on one ROM step), decided by the model alone so that every
-    // slab decomposition runs the same arithmetic; their batches follow the regular ones.
     const char* benv = getenv("FDTD_BIG_Q");
     const int big_q = benv ? atoi(benv) : 512;
-    std::vector<char> big(c->models.size(), 0);
+    const int nm = (int)c->models.size();
+    std::vector<int> rs(nm), Bm(nm);
+    std::vector<char> big(nm, 0);
     size_t big_smem = 0;
     int64_t big_elems = 0;
-    for (size_t mi = 0; mi < c->models.size(); ++mi) {
+    for (int mi = 0; mi < nm; ++mi) {
       const ModelHost& m = c->models[mi];
+      rs[mi] = (fdtd::region_elems(m.bx, m.by, M) + 3) / 4 * 4;
+      const size_t per = batch_smem(c, m, 1, 1, rs[mi]);
+      Bm[mi] = (int)std::max<size_t>(1, std::min<size_t>(Bmax, FIX_BUDGET / per));  // any B <= 8: N = 8, zero-padded
       if (big_q > 0 && m.q1 + m.q2 >= big_q) {
         big[mi] = 1;
-        big_smem = std::max(big_smem, shp[mi].per);
+        big_smem = std::max(big_smem, per);
         big_elems = std::max<int64_t>(big_elems, 3 * (m.q1 + m.q2) + (m.q2 + m.q1 + m.nY) + 2 * m.nY);
       }
     }
@@ -871,51 +951,91 @@ fdtd_status apply_passes(fdtd_ctx* c, int k) {
       c->big_grid = c->prec == 64 ? fdtd::big_grid_size<double>(big_smem, k) : fdtd::big_grid_size<float>(big_smem, k);
       if (c->big_grid <= 0) std::fill(big.begin(), big.end(), 0);  // cannot launch cooperatively: batch path
     }
+    for (int mi = 0; mi < nm; ++mi)
+      if (big[mi]) Bm[mi] = 1;  // bigrom_kernel steps one instance at a time
     c->big_smem = big_smem;
     c->post_smem = 16;
-    for (size_t mi = 0; mi < shp.size(); ++mi) {  // any B <= 8: the DMMA's N = 8 columns (zero-padded)
-      Shape& x = shp[mi];
-      x.B = big[mi] ? 1 : (int)std::max<size_t>(1, std::min<size_t>(Bmax, cap / x.per));
-      if (!big[mi]) c->post_smem = std::max(c->post_smem, x.B * x.per);
-    }
     c->batch_tab.clear();
-    const int n = (int)c->inst_model.size();
-    for (int pass = 0; pass < 2; ++pass) {  // regular batches, then the large models' instances
-      for (int i = 0; i < n;) {
-        const Shape& x = shp[c->inst_model[i]];
-        int e = i;
-        while (e < n && e - i < x.B && c->inst_model[e] == c->inst_model[i]) ++e;
-        if (big[c->inst_model[i]] == pass) c->batch_tab.insert(c->batch_tab.end(), {c->inst_model[i], i, e - i, x.B, x.stride});
-        i = e;
+    c->batch_inst.clear();
+    c->batch_rect.clear();
+    auto add_batch = [&](int model, const std::vector<int>& mem, int B, int stride, int kind, const PassRegion* g) {
+      c->batch_tab.insert(c->batch_tab.end(), {model, (int32_t)c->batch_inst.size(), (int32_t)mem.size(), B, stride, kind});
+      c->batch_inst.insert(c->batch_inst.end(), mem.begin(), mem.end());
+      if (g) c->batch_rect.insert(c->batch_rect.end(), {(int32_t)g->i0, (int32_t)g->j0, (int32_t)(g->i1 - g->i0),
+                                                        (int32_t)(g->j1 - g->j0)});
+      else c->batch_rect.insert(c->batch_rect.end(), {0, 0, 0, 0});
+    };
+    for (int pass = 0; pass < 2; ++pass) {
+      // instances with their own region, grouped by model in instance order
+      std::vector<int> cur;
+      int cur_model = -1;
+      auto flush = [&]() {
+        if (cur.empty()) return;
+        add_batch(cur_model, cur, Bm[cur_model], rs[cur_model], 0, nullptr);
+        if (!pass) c->post_smem = std::max(c->post_smem, batch_smem(c, c->models[cur_model], Bm[cur_model],
+                                                                     Bm[cur_model], rs[cur_model]));
+        cur.clear();
+      };
+      for (const PassRegion& g : regs) {
+        if (g.members.size() != 1 || big[g.model] != pass) continue;
+        if (g.model != cur_model || (int)cur.size() == Bm[g.model]) {
+          flush();
+          cur_model = g.model;
+        }
+        cur.push_back(g.members[0]);
       }
-      if (pass == 0) c->n_batch_reg = (int)(c->batch_tab.size() / 5);
+      flush();
+      if (pass == 0) {  // clusters: one batch per cluster around its shared region
+        for (const PassRegion& g : regs) {
+          if (g.members.size() < 2) continue;
+          const int crs = (fdtd::region_elems((int)(g.i1 - g.i0), (int)(g.j1 - g.j0), M) + 3) / 4 * 4;
+          add_batch(g.model, g.members, (int)g.members.size(), crs, 1, &g);
+          c->post_smem = std::max(c->post_smem, batch_smem(c, c->models[g.model], (int)g.members.size(), 1, crs));
+        }
+        c->n_batch_reg = (int)(c->batch_tab.size() / fdtd::BATCH_FIELDS);
+      }
     }
-    if (c->batch_tab.empty()) c->batch_tab.assign(5, 0);
+    c->n_clusters = 0;
+    for (const PassRegion& g : regs) c->n_clusters += g.members.size() > 1;
+    if (c->batch_tab.empty()) {
+      c->batch_tab.assign(fdtd::BATCH_FIELDS, 0);
+      c->batch_inst.assign(1, 0);
+      c->batch_rect.assign(4, 0);
+    }
+    if ((st = upload(c, &c->d_batch_tab, c->batch_tab)) != FDTD_OK) return st;
+    if ((st = upload(c, &c->d_batch_inst, c->batch_inst)) != FDTD_OK) return st;
+    if ((st = upload(c, &c->d_batch_rect, c->batch_rect)) != FDTD_OK) return st;
+    const int n = (int)c->inst_model.size();
+    c->post_grid = n > 0 ? (int)(c->batch_tab.size() / fdtd::BATCH_FIELDS) : 1;
+    std::vector<double> l1((size_t)KMAX * c->post_grid, 0.0);
+    if ((st = upload(c, &c->d_level1, l1)) != FDTD_OK) return st;
     if (big_elems > 0 && c->big_grid > 0) {
       std::vector<double> z((size_t)big_elems, 0.0);
       if ((st = upload_T(c, &c->d_big, z)) != FDTD_OK) return st;
     }
-    if ((st = upload(c, &c->d_batch_tab, c->batch_tab)) != FDTD_OK) return st;
-    c->post_grid = n > 0 ? (int)(c->batch_tab.size() / 5) : 1;
-    std::vector<double> l1((size_t)KMAX * c->post_grid, 0.0);
-    if ((st = upload(c, &c->d_level1, l1)) != FDTD_OK) return st;
   }
-  // zone probes: probes inside an instance's zone are recorded by its fix-up
+  // zone probes: the probes inside a region's zone (outside every hole) are recorded by its fix-up,
+  // on the region's first member
   {
     const int n = (int)c->inst_model.size();
+    std::vector<std::vector<int32_t>> per(n);
+    if (k >= 2)
+      for (const PassRegion& g : regs)
+        for (int pr = 0; pr < c->n_probe; ++pr) {
+          const int64_t pi = c->probe_ij[2 * pr], pj = c->probe_ij[2 * pr + 1];
+          if (!(pi >= g.i0 - (k - 1) && pi < g.i1 + k && pj >= g.j0 - (k - 1) && pj < g.j1 + k)) continue;
+          bool hole = false;
+          for (int i : g.members) {
+            const int64_t i0 = c->rects[4 * i], j0 = c->rects[4 * i + 1];
+            hole |= pi >= i0 && pi < i0 + c->rects[4 * i + 2] && pj >= j0 && pj < j0 + c->rects[4 * i + 3];
+          }
+          if (!hole) per[g.members[0]].insert(per[g.members[0]].end(), {(int32_t)pi, (int32_t)pj, pr});
+        }
     c->zp_off.assign(n + 1, 0);
     c->zp.clear();
     for (int i = 0; i < n; ++i) {
       c->zp_off[i] = (int32_t)(c->zp.size() / 3);
-      if (k >= 2) {
-        const int64_t i0 = c->rects[4 * i], j0 = c->rects[4 * i + 1], bx = c->rects[4 * i + 2], by = c->rects[4 * i + 3];
-        for (int pr = 0; pr < c->n_probe; ++pr) {
-          const int64_t pi = c->probe_ij[2 * pr], pj = c->probe_ij[2 * pr + 1];
-          const bool hole = pi >= i0 && pi < i0 + bx && pj >= j0 && pj < j0 + by;
-          if (!hole && pi >= i0 - (k - 1) && pi < i0 + bx + k && pj >= j0 - (k - 1) && pj < j0 + by + k)
-            c->zp.insert(c->zp.end(), {(int32_t)pi, (int32_t)pj, pr});
-        }
-      }
+      c->zp.insert(c->zp.end(), per[i].begin(), per[i].end());
     }
     c->zp_off[n] = (int32_t)(c->zp.size() / 3);
     if (c->zp.empty()) c->zp.assign(3, 0);
@@ -1873,6 +1993,9 @@ fdtd_status fdtd_get_info(const fdtd_ctx* c, fdtd_info* o) {
   o->bytes_per_cell_step = 8.0 * (double)c->es / o->steps_per_pass;
   o->sweep_stream = (void*)c->stream;
   o->graph_builds = c->graph_builds;
+  o->fixup_clusters = c->n_clusters;
+  o->big_instances = (int32_t)(c->batch_tab.size() / fdtd::BATCH_FIELDS) - c->n_batch_reg;
+  if (c->inst_model.empty()) o->big_instances = 0;
   return FDTD_OK;
 }
 

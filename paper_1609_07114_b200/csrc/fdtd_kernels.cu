@@ -767,8 +767,8 @@ __device__ __forceinline__ T* rom_end(T* sv, int64_t S, int64_t nYB, int B) {
 // part of W^n (coarse half cells + x~^T R~ x~) of instance b is in eout[b].  Four phases: M1 GEMM |
 // energy + t | Schur solve | M2 GEMM with the base added in its epilogue (fp32: tensor cores).
 template <typename T, bool ENERGY>
-__device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first, int nb, int B, int64_t S, T* sv,
-                         double* eout) {
+__device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, const int32_t* mem, int nb, int B, int64_t S,
+                         T* sv, double* ep) {
   const int nY = m.nY, q1 = m.q1, q2 = m.q2, nx = q1 + q2, m1 = q2 + q1 + nY, m2 = q1 + nY;
   const int tid = threadIdx.x, nt = blockDim.x;
   RomVec<T> v(sv, S);
@@ -792,7 +792,7 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first
       for (int i = lane; i < nx; i += 32) acc += (double)v.sx[i * B + b] * (double)v.so[(m1 + i) * B + b];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
-      if (lane == 0) eout[b] = acc;
+      if (lane == 0) ep[mem[b]] = acc;
     }
   }
   // t = (a_y/c_y) y + (D_l G/c_y) h - L~^T E*
@@ -805,7 +805,7 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, int first
   // U = S_k t (per-instance Schur inverse, L2-resident after the prefetch at the batch start)
   for (int it = tid; it < nY * nb; it += nt) {
     const int i = it % nY, b = it / nY;
-    const T* Sk = p.Sk + p.Sk_off[first + b] + i;
+    const T* Sk = p.Sk + p.Sk_off[mem[b]] + i;
     T a[4] = {T(0), T(0), T(0), T(0)};  // four interleaved partial sums: a quarter of the FMA chain
     int c = 0;
     for (; FDTD_SCHUR16 && c + 15 < nY; c += 16) {  // 16 loads in flight, then their FMAs
@@ -858,8 +858,9 @@ struct BigScratch {
 };
 
 template <typename T, bool ENERGY>
-__device__ void rom_step_big(const PostParams<T>& p, const RomModelDev& m, int first, int s, T* sv, int64_t S,
-                             double* eout, double* part) {
+__device__ void rom_step_big(const PostParams<T>& p, const RomModelDev& m, const int32_t* mem, int s, T* sv,
+                             int64_t S, double* ep, double* part) {
+  const int first = mem[0];
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   const int nY = m.nY, q1 = m.q1, q2 = m.q2, nx = q1 + q2, m1 = q2 + q1 + nY, m2 = q1 + nY;
@@ -927,7 +928,7 @@ __device__ void rom_step_big(const PostParams<T>& p, const RomModelDev& m, int f
     for (int i = lane; i < nx; i += 32) acc += (double)xin[i] * (double)bsc.SO[m1 + i];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
-    if (lane == 0) eout[0] = acc;
+    if (lane == 0) ep[first] = acc;
   }
   {  // t and U = S_k t, in every CTA
     const int64_t po = p.port_off[first];
@@ -975,23 +976,23 @@ __device__ void rom_step_big(const PostParams<T>& p, const RomModelDev& m, int f
 }
 
 template <typename T>
-__device__ void load_rom_state(const PostParams<T>& p, const RomModelDev& m, int first, int nb, int B, T* sv) {
+__device__ void load_rom_state(const PostParams<T>& p, const RomModelDev& m, const int32_t* mem, int nb, int B, T* sv) {
   T* sx = sv;
   const int nx = m.q1 + m.q2;
   for (int it = threadIdx.x; it < nx * nb; it += blockDim.x) {
     const int i = it % nx, b = it / nx;
-    sx[i * B + b] = p.state[p.state_off[first + b] + i];
+    sx[i * B + b] = p.state[p.state_off[mem[b]] + i];
   }
 }
 
 template <typename T>
-__device__ void store_rom(const PostParams<T>& p, const RomModelDev& m, int first, int nb, int B, int64_t S,
+__device__ void store_rom(const PostParams<T>& p, const RomModelDev& m, const int32_t* mem, int nb, int B, int64_t S,
                           const T* sv, T* ex, T* ey) {
   const T* sx = sv;
   const T* sy = sv + S;
   for (int it = threadIdx.x; it < m.nY * nb; it += blockDim.x) {  // S6: scatter y^{n+1}
     const int i = it % m.nY, b = it / m.nY;
-    const int64_t e = p.port_edge[p.port_off[first + b] + i];
+    const int64_t e = p.port_edge[p.port_off[mem[b]] + i];
     FCHK((e & IDX_MASK) >= (int64_t)p.row0 * p.pitch && (e & IDX_MASK) < (int64_t)(p.row0 + p.rows) * p.pitch);
     if (e >> 62) ey[e & IDX_MASK] = sy[i * B + b];
     else ex[e & IDX_MASK] = sy[i * B + b];
@@ -1002,7 +1003,7 @@ __device__ void store_rom(const PostParams<T>& p, const RomModelDev& m, int firs
     const int i = it % nx, b = it / nx;
     const T v = sx[i * B + b];
     bad |= !isfinite(v);
-    p.state[p.state_off[first + b] + i] = v;
+    p.state[p.state_off[mem[b]] + i] = v;
   }
   if (bad) *p.flag = 1;  // non-finite sentinel (a ROM blow-up reaches the state first)
 }
@@ -1043,94 +1044,129 @@ struct Flat {
   }
 };
 
-// per-instance constants of a batch (static shared memory of the fix-up kernel)
-constexpr int MAXB = 64;  // largest batch (FDTD_ROM_BATCH)
+// per-region / per-member constants of a batch (static shared memory of the fix-up kernels)
+constexpr int MAXB = 64;  // largest batch (FDTD_ROM_BATCH; a cluster's members)
 struct BatchShared {
-  int64_t gbase[MAXB];     // device element offset of region cell (0, 0)
+  int64_t gi0[MAXB], gj0[MAXB];        // global cell (column, row) of region cell (0, 0)
+  int64_t gbase[MAXB];                 // its device element offset
   int su[MAXB], sv0[MAXB], sv1[MAXB];  // the source cells in region coordinates (su = -1: none)
-  double zsum[MAXB];
+  int rr[MAXB], bu[MAXB], bv[MAXB];    // member b: its region, its block's lower-left cell there
+  double zsum[MAXB];                   // zone energy per region
 };
 
 // K3: the K-step fix-up of one batch (instances of one model).  The sweep advanced every cell K
-// steps with the interface edges frozen at y^n; here, per instance, the K steps are recomputed
-// on the region [i0-M, i0+bx+M) x [j0-M, j0+by+M), M = Kz + K - 1, from the pass's input buffer
-// with the sweep's own arithmetic (yee_row's device functions), and between the H and E half
-// steps the ROM takes its step (S4 gather, S5 eq:connExplicit, S6 scatter).  Values in the
-// region go wrong from its border inwards by one cell per step, so after K steps every cell
-// within Kz of the block is exact.  Written back: the zone cells (block + Kz - 1 rings, + one
-// more column / row on the right / top, holes excluded) with their bottom Ex and left Ey edges;
-// y^{n+K}; the ROM state.  Their energy (which the sweep skipped) and the zone probes are
-// recorded here for every step of the pass.  Every region phase runs over the whole batch at once.
+// steps with the interface edges frozen at y^n; here the K steps are recomputed on each region
+// from the pass's input buffer with the sweep's own arithmetic (yee_row's device functions), and
+// between the H and E half steps every member's ROM takes its step (S4 gather, S5
+// eq:connExplicit, S6 scatter).  A batch's regions are either one per member (kind 0:
+// [i0-M, i0+bx+M) x [j0-M, j0+by+M), M = Kz + K - 1) or one shared by all members (kind 1: a
+// cluster of instances closer than the pass depth allows; the region is their bounding box + M,
+// DESIGN.md "Pass depth").  Values in a region go wrong from its border inwards by one cell per
+// step, so after K steps every cell within Kz of the blocks is exact.  Written back: the zone of
+// each region (block or bounding box + Kz - 1 rings, + one more column / row on the right / top,
+// holes excluded) with the cells' bottom Ex and left Ey edges; y^{n+K}; the ROM states.  The
+// zones' energy (which the sweep skipped) and the zone probes are recorded here for every step of
+// the pass.  Cells outside the grid (walls) load as dead cells with zero fields.  Every region
+// phase runs over the whole batch at once.
 template <typename T, int K, bool ENERGY, bool BIG = false>
 __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[K], int64_t step, BatchShared& bs,
                             double* part = nullptr) {
-  const int* bt = p.batch_tab + 5 * bi;  // (model, first instance, count, slots B, region stride)
-  const int model = bt[0], first = bt[1], nb = bt[2], B = bt[3], rstride = bt[4];
+  const int* bt = p.batch_tab + BATCH_FIELDS * bi;  // (model, member offset, count, slots B, region stride, kind)
+  const int model = bt[0], nb = bt[2], B = bt[3], rstride = bt[4], kind = bt[5];
+  const int32_t* mem = p.batch_inst + bt[1];
   const RomModelDev m = p.models[model];
   const int nY = m.nY;
   const int64_t S = (int64_t)(m.q1 + m.q2 + nY) * B;  // vector stride of this batch's layout
   const int tid = threadIdx.x, nt = blockDim.x;
   // BIG (one instance on the whole cooperative grid): only CTA 0 holds the region; the others take
-  // part in the ROM step only (nr = 0 empties every region loop of theirs)
+  // part in the ROM step only (nr = nreg = 0 empties every region loop of theirs)
   const bool rg = !BIG || blockIdx.x == 0;
   const int nr = rg ? nb : 0;
+  const int nreg = rg ? (kind ? 1 : nb) : 0;
   const int64_t nYB = (int64_t)nY * B;
   T* reg = rom_end(sv, S, nYB, B);
   const RomConst<T> rc(sv, S, nYB);
   const int Kz = p.Kz, M = Kz + K - 1;
   const int64_t P = p.pitch;
-  // the batch's common region shape (one model)
-  const int bx = p.rects[4 * (int64_t)first + 2], by = p.rects[4 * (int64_t)first + 3];
-  const int Wr = bx + 2 * M, Hr = by + 2 * M, W1 = Wr + 1, n = Hr * Wr;
+  // the members' blocks (one model: bx x by); the region's block: a member's, or the cluster's box
+  const int bx = p.rects[4 * (int64_t)mem[0] + 2], by = p.rects[4 * (int64_t)mem[0] + 3];
+  const int rbx = kind ? p.batch_rect[4 * bi + 2] : bx, rby = kind ? p.batch_rect[4 * bi + 3] : by;
+  const int Wr = rbx + 2 * M, Hr = rby + 2 * M, W1 = Wr + 1, n = Hr * Wr;
   int zu0 = 0, zu1 = 0, zv0 = 0, zv1 = 0;
   if (Kz >= 2) {  // zone rectangle in region coordinates
-    zu0 = M - (Kz - 1); zu1 = M + bx + Kz; zv0 = M - (Kz - 1); zv1 = M + by + Kz;
+    zu0 = M - (Kz - 1); zu1 = M + rbx + Kz; zv0 = M - (Kz - 1); zv1 = M + rby + Kz;
   }
   const int zw = zu1 - zu0, nz = zw * (zv1 - zv0);
-  auto H = [&](int b) { return reg + (int64_t)b * rstride; };
-  auto MA = [&](int b) { return reg + (int64_t)b * rstride + n; };
-  auto MS = [&](int b) { return reg + (int64_t)b * rstride + 2 * n; };
-  auto EX = [&](int b) { return reg + (int64_t)b * rstride + 3 * n; };
-  auto EY = [&](int b) { return reg + (int64_t)b * rstride + 4 * n + Wr; };
-  auto ZE = [&](int b) { return reg + (int64_t)b * rstride + 4 * n + Wr + Hr * W1; };
+  auto H = [&](int r) { return reg + (int64_t)r * rstride; };
+  auto MA = [&](int r) { return reg + (int64_t)r * rstride + n; };
+  auto MS = [&](int r) { return reg + (int64_t)r * rstride + 2 * n; };
+  auto EX = [&](int r) { return reg + (int64_t)r * rstride + 3 * n; };
+  auto EY = [&](int r) { return reg + (int64_t)r * rstride + 4 * n + Wr; };
+  auto ZE = [&](int r) { return reg + (int64_t)r * rstride + 4 * n + Wr + Hr * W1; };
   FCHK(4 * n + Wr + Hr * W1 + nz <= rstride &&
-       (size_t)((char*)(reg + (int64_t)B * rstride) - (char*)sv) <= p.smem_bytes);  // regions inside the launch
+       (size_t)((char*)(reg + (int64_t)(kind ? 1 : B) * rstride) - (char*)sv) <= (BIG ? p.big_smem_bytes : p.smem_bytes));
   for (int64_t k = tid; rg && k < NROMVEC * S; k += nt) sv[k] = T(0);
-  for (int b = tid; b < nr; b += nt) {
-    const int32_t* r = p.rects + 4 * (int64_t)(first + b);
-    const int64_t lr0 = (int64_t)r[1] - M - p.row_begin + p.row0;  // local row of region row 0
-    bs.gbase[b] = lr0 * P + r[0] - M;
-    FCHK(bs.gbase[b] >= 0 && bs.gbase[b] + (int64_t)Hr * P + Wr < p.alloc_elems);  // region rows inside the arrays
-    const int64_t cu = p.src_col - (r[0] - M);
+  for (int r = tid; r < nreg; r += nt) {
+    const int32_t* q = kind ? p.batch_rect + 4 * bi : p.rects + 4 * (int64_t)mem[r];
+    const int64_t i0 = (int64_t)q[0] - M, j0 = (int64_t)q[1] - M;  // global cell of region cell (0, 0)
+    const int64_t lr0 = j0 - p.row_begin + p.row0;                  // its local row
+    bs.gi0[r] = i0;
+    bs.gj0[r] = j0;
+    bs.gbase[r] = lr0 * P + i0;
+    FCHK(lr0 >= 0 || j0 < 0);  // region rows below the slab only where the grid ends
+    const int64_t cu = p.src_col - i0;
     const bool hit = p.src_row >= 0 && cu >= 0 && cu < Wr;
-    bs.su[b] = hit ? (int)cu : -1;
-    bs.sv0[b] = hit ? (int)max(p.src_row - lr0, (int64_t)0) : 0;
-    bs.sv1[b] = hit ? (int)min(p.src_row_end - lr0, (int64_t)Hr) : 0;
+    bs.su[r] = hit ? (int)cu : -1;
+    bs.sv0[r] = hit ? (int)max(p.src_row - lr0, (int64_t)0) : 0;
+    bs.sv1[r] = hit ? (int)min(p.src_row_end - lr0, (int64_t)Hr) : 0;
+  }
+  for (int b = tid; b < nr; b += nt) {  // members: region and block position
+    const int32_t* q = p.rects + 4 * (int64_t)mem[b];
+    const int32_t* o = kind ? p.batch_rect + 4 * bi : q;
+    bs.rr[b] = kind ? 0 : b;
+    bs.bu[b] = q[0] - o[0] + M;
+    bs.bv[b] = q[1] - o[1] + M;
   }
   __syncthreads();  // the zero padding lands before load_rom_state fills the live slots
   T* sy = sv + S;
   T* sh = sv + 2 * S;
   // ---- load the regions: materials and the fields at step n (asynchronous element copies, all in
-  // flight at once: the region rows are not 16-byte aligned)
-  for (Flat f(tid, nt, 0, Wr, 0, Hr); f.b < nr; f.next()) {
-    const int64_t o = bs.gbase[f.b] + (int64_t)f.v * P + f.u;
+  // flight at once: the region rows are not 16-byte aligned).  Outside the grid: dead cells (the
+  // PEC walls), zero fields.
+  const int64_t NX = p.nx, NY = p.ny;
+  for (Flat f(tid, nt, 0, Wr, 0, Hr); f.b < nreg; f.next()) {
     const int t = f.v * Wr + f.u;
-    cp_async_el(MA(f.b) + t, p.mea + o);
-    cp_async_el(MS(f.b) + t, p.msb + o);
-    cp_async_el(H(f.b) + t, p.hz0 + o);
+    const int64_t gi = bs.gi0[f.b] + f.u, gj = bs.gj0[f.b] + f.v;
+    if (gi >= 0 && gi < NX && gj >= 0 && gj < NY) {
+      const int64_t o = bs.gbase[f.b] + (int64_t)f.v * P + f.u;
+      FCHK(o >= 0 && o < p.alloc_elems);
+      cp_async_el(MA(f.b) + t, p.mea + o);
+      cp_async_el(MS(f.b) + t, p.msb + o);
+      cp_async_el(H(f.b) + t, p.hz0 + o);
+    } else {
+      MA(f.b)[t] = T(-1);
+      MS(f.b)[t] = T(0);
+      H(f.b)[t] = T(0);
+    }
   }
-  for (Flat f(tid, nt, 0, Wr, 0, Hr + 1); f.b < nr; f.next())
-    cp_async_el(EX(f.b) + f.v * Wr + f.u, p.ex0 + bs.gbase[f.b] + (int64_t)f.v * P + f.u);
-  for (Flat f(tid, nt, 0, W1, 0, Hr); f.b < nr; f.next())
-    cp_async_el(EY(f.b) + f.v * W1 + f.u, p.ey0 + bs.gbase[f.b] + (int64_t)f.v * P + f.u);
-  if (!BIG) load_rom_state(p, m, first, nb, B, sv);  // (BIG: the ROM step reads x~ from global memory)
+  for (Flat f(tid, nt, 0, Wr, 0, Hr + 1); f.b < nreg; f.next()) {  // Ex edge rows
+    const int64_t gi = bs.gi0[f.b] + f.u, gj = bs.gj0[f.b] + f.v;
+    if (gi >= 0 && gi < NX && gj >= 0 && gj <= NY) cp_async_el(EX(f.b) + f.v * Wr + f.u, p.ex0 + bs.gbase[f.b] + (int64_t)f.v * P + f.u);
+    else EX(f.b)[f.v * Wr + f.u] = T(0);
+  }
+  for (Flat f(tid, nt, 0, W1, 0, Hr); f.b < nreg; f.next()) {  // Ey edge columns
+    const int64_t gi = bs.gi0[f.b] + f.u, gj = bs.gj0[f.b] + f.v;
+    if (gi >= 0 && gi <= NX && gj >= 0 && gj < NY) cp_async_el(EY(f.b) + f.v * W1 + f.u, p.ey0 + bs.gbase[f.b] + (int64_t)f.v * P + f.u);
+    else EY(f.b)[f.v * W1 + f.u] = T(0);
+  }
+  if (!BIG) load_rom_state(p, m, mem, nb, B, sv);  // (BIG: the ROM step reads x~ from global memory)
   for (int it = tid; FDTD_SKPF && it < nr * ((nY * nY + 31) / 32); it += nt) {  // the batch's Schur inverses into L2
-    const int b = it % nb, l = it / nb;
-    prefetch_l2(p.Sk + p.Sk_off[first + b] + l * 32);
+    const int b = it % nr, l = it / nr;
+    prefetch_l2(p.Sk + p.Sk_off[mem[b]] + l * 32);
   }
   for (int it = tid; it < nY * nr; it += nt) {  // per-pass constants of the batch's ports (RomConst)
     const int i = it % nY, b = it / nY;
-    const int64_t po = p.port_off[first + b] + i;
+    const int64_t po = p.port_off[mem[b]] + i;
     rc.eh[i * B + b] = p.ehalf[po];
     rc.cya[i * B + b] = p.cya[po];
     rc.cyg[i * B + b] = p.cyg[po];
@@ -1144,94 +1180,97 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   for (int s = 0; s < K; ++s) {
     const int cw = Wr - 2 * s, ch = Hr - 2 * s;
     // ---- H half-step (+ source, + the zone cells' storage-function terms of W^{n+s})
-    for (Flat f(tid, nt, s, cw, s, ch); f.b < nr; f.next()) {
-      const int u = f.u, v = f.v, b = f.b;
-      const T* ex = EX(b);
-      const T* ey = EY(b);
-      const T* ma = MA(b);
-      T* hz = H(b);
+    for (Flat f(tid, nt, s, cw, s, ch); f.b < nreg; f.next()) {
+      const int u = f.u, v = f.v, r = f.b;
+      const T* ex = EX(r);
+      const T* ey = EY(r);
+      const T* ma = MA(r);
+      T* hz = H(r);
       const int t = v * Wr + u;
       const T h0 = hz[t];
       const T hu = hupd(h0, ex[t + Wr], ex[t], ey[v * W1 + u + 1], ey[v * W1 + u], p.chy, p.chx);
       T h = ma[t] < T(0) ? h0 : hu;  // dead cells keep their Hz (as in yee_row)
-      if (u == bs.su[b] && v >= bs.sv0[b] && v < bs.sv1[b]) h += g[s];
+      if (u == bs.su[r] && v >= bs.sv0[r] && v < bs.sv1[r]) h += g[s];
       if (ENERGY && u >= zu0 && u < zu1 && v >= zv0 && v < zv1) {
         // the zone cell's full storage-function term (row_coef's weights without the zone mask)
-        const T* ms = MS(b);
+        const T* ms = MS(r);
         bool lx, ly;
         T ax, ay, ca, cb;
         edge_coef(ma[t - Wr], ms[t - Wr], ma[t], ms[t], p.idy, ca, cb, ax, lx);
         edge_coef(ma[t - 1], ms[t - 1], ma[t], ms[t], -p.idx, ca, cb, ay, ly);
         const T wx = lx ? mul_rn(p.wxy, ax) : T(0), wy = ly ? mul_rn(p.wxy, ay) : T(0);
         const T hw = ma[t] < T(0) ? T(0) : p.wh;
-        ZE(b)[(v - zv0) * zw + u - zu0] = cell_energy(T(0), ex[t], ey[v * W1 + u], h0, h, wx, wy, hw);
+        ZE(r)[(v - zv0) * zw + u - zu0] = cell_energy(T(0), ex[t], ey[v * W1 + u], h0, h, wx, wy, hw);
       }
       hz[t] = h;
     }
     __syncthreads();
     // ---- zone probes; S4 gather of y^{n+s} (interface edges) and h = Hz^{n+s+1/2} (outside cells)
     for (int b = 0; b < nr; ++b) {
-      const int z0 = p.zp_off[first + b], z1 = p.zp_off[first + b + 1];
+      const int z0 = p.zp_off[mem[b]], z1 = p.zp_off[mem[b] + 1];
       if (z0 == z1) continue;
-      const int32_t* r = p.rects + 4 * (int64_t)(first + b);
+      const int r = bs.rr[b];
       for (int z = z0 + tid; z < z1; z += nt) {
-        const int u = p.zp[3 * z] - (r[0] - M), v = p.zp[3 * z + 1] - (r[1] - M);
+        const int u = (int)(p.zp[3 * z] - bs.gi0[r]), v = (int)(p.zp[3 * z + 1] - bs.gj0[r]);
         FCHK(u >= 0 && u < Wr && v >= 0 && v < Hr && p.zp[3 * z + 2] < p.n_probe);
-        p.probe_ring[(int64_t)p.zp[3 * z + 2] * p.cap + (step + s) % p.cap] = H(b)[v * Wr + u];
+        p.probe_ring[(int64_t)p.zp[3 * z + 2] * p.cap + (step + s) % p.cap] = H(r)[v * Wr + u];
       }
     }
     for (int it = tid; it < nY * nr; it += nt) {
       const int i = it % nY, b = it / nY;
-      const T* ex = EX(b);
-      const T* ey = EY(b);
-      const T* hz = H(b);
+      const int r = bs.rr[b], U0 = bs.bu[b], V0 = bs.bv[b];
+      const T* ex = EX(r);
+      const T* ey = EY(r);
+      const T* hz = H(r);
       T y, h;
-      if (i < bx) {  // S side: Ex edge row M, outside cell row M-1
-        y = ex[M * Wr + M + i]; h = hz[(M - 1) * Wr + M + i];
-      } else if (i < 2 * bx) {  // N side: Ex edge row M+by, outside cell row M+by
-        y = ex[(M + by) * Wr + M + i - bx]; h = hz[(M + by) * Wr + M + i - bx];
-      } else if (i < 2 * bx + by) {  // W side: Ey edge column M, outside cell column M-1
-        const int v = M + i - 2 * bx;
-        y = ey[v * W1 + M]; h = hz[v * Wr + M - 1];
-      } else {  // E side: Ey edge column M+bx, outside cell column M+bx
-        const int v = M + i - 2 * bx - by;
-        y = ey[v * W1 + M + bx]; h = hz[v * Wr + M + bx];
+      if (i < bx) {  // S side: Ex edge row V0, outside cell row V0-1
+        y = ex[V0 * Wr + U0 + i]; h = hz[(V0 - 1) * Wr + U0 + i];
+      } else if (i < 2 * bx) {  // N side: Ex edge row V0+by, outside cell row V0+by
+        y = ex[(V0 + by) * Wr + U0 + i - bx]; h = hz[(V0 + by) * Wr + U0 + i - bx];
+      } else if (i < 2 * bx + by) {  // W side: Ey edge column U0, outside cell column U0-1
+        const int v = V0 + i - 2 * bx;
+        y = ey[v * W1 + U0]; h = hz[v * Wr + U0 - 1];
+      } else {  // E side: Ey edge column U0+bx, outside cell column U0+bx
+        const int v = V0 + i - 2 * bx - by;
+        y = ey[v * W1 + U0 + bx]; h = hz[v * Wr + U0 + bx];
       }
       sy[i * B + b] = y;
       sh[i * B + b] = h;
     }
-    if (ENERGY) {  // zone energy per instance, fixed order (one warp per instance)
+    if (ENERGY) {  // zone energy per region, fixed order (one warp per region)
       const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
-      for (int b = w; b < nr; b += nw) {
-        const T* ze = ZE(b);
+      for (int r = w; r < nreg; r += nw) {
+        const T* ze = ZE(r);
         double acc = 0.0;
         for (int i = lane; i < nz; i += 32) acc += (double)ze[i];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
-        if (lane == 0) bs.zsum[b] = acc;
+        if (lane == 0) bs.zsum[r] = acc;
       }
     }
     __syncthreads();
-    // ---- S5: ROM step n+s -> y^{n+s+1}, x~^{n+s+1}; ROM energy of W^{n+s}
-    double* eout = p.rom_partials + (int64_t)s * p.n_inst + first;
-    if constexpr (BIG) rom_step_big<T, ENERGY>(p, m, first, s, sv, S, eout, part);
-    else rom_step<T, ENERGY>(p, m, first, nb, B, S, sv, eout);
-    if (ENERGY && tid < nr) eout[tid] += bs.zsum[tid];
+    // ---- S5: ROM step n+s -> y^{n+s+1}, x~^{n+s+1}; ROM energy of W^{n+s} (+ the zone energy of
+    // the member's region on its first member)
+    double* ep = p.rom_partials + (int64_t)s * p.n_inst;
+    if constexpr (BIG) rom_step_big<T, ENERGY>(p, m, mem, s, sv, S, ep, part);
+    else rom_step<T, ENERGY>(p, m, mem, nb, B, S, sv, ep);
+    if (ENERGY && tid < nr && (kind == 0 || tid == 0)) ep[mem[tid]] += bs.zsum[bs.rr[tid]];
     // ---- S6: y^{n+s+1} into the regions' interface edges, and in the same phase the E half-step
     // on the regions' live edges (dead edges -- interface, PEC, hole -- keep their value: they are
     // skipped, so the scatter and the update never touch the same edge)
     for (int it = tid; it < nY * nr; it += nt) {
       const int i = it % nY, b = it / nY;
+      const int r = bs.rr[b], U0 = bs.bu[b], V0 = bs.bv[b];
       const T y = sy[i * B + b];
-      T* ex = EX(b);
-      T* ey = EY(b);
-      if (i < bx) ex[M * Wr + M + i] = y;
-      else if (i < 2 * bx) ex[(M + by) * Wr + M + i - bx] = y;
-      else if (i < 2 * bx + by) ey[(M + i - 2 * bx) * W1 + M] = y;
-      else ey[(M + i - 2 * bx - by) * W1 + M + bx] = y;
+      T* ex = EX(r);
+      T* ey = EY(r);
+      if (i < bx) ex[V0 * Wr + U0 + i] = y;
+      else if (i < 2 * bx) ex[(V0 + by) * Wr + U0 + i - bx] = y;
+      else if (i < 2 * bx + by) ey[(V0 + i - 2 * bx) * W1 + U0] = y;
+      else ey[(V0 + i - 2 * bx - by) * W1 + U0 + bx] = y;
     }
-    for (Flat f(tid, nt, s, cw, s + 1, ch - 1); f.b < nr; f.next()) {  // Ex edge rows s+1 .. Hr-s-1,
-      const int t = f.v * Wr + f.u;                                       // columns s .. Wr-s-1
+    for (Flat f(tid, nt, s, cw, s + 1, ch - 1); f.b < nreg; f.next()) {  // Ex edge rows s+1 .. Hr-s-1,
+      const int t = f.v * Wr + f.u;                                         // columns s .. Wr-s-1
       const T* ma = MA(f.b);
       const T* ms = MS(f.b);
       const T* hz = H(f.b);
@@ -1241,8 +1280,8 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       edge_coef(ma[t - Wr], ms[t - Wr], ma[t], ms[t], p.idy, ca, cb, a, l);
       if (l) ex[t] = eupd(ex[t], ca, cb, hz[t] - hz[t - Wr]);
     }
-    for (Flat f(tid, nt, s + 1, cw - 1, s, ch); f.b < nr; f.next()) {  // Ey edge columns s+1 .. Wr-s-1,
-      const int c = f.v * Wr + f.u;                                       // rows s .. Hr-s-1
+    for (Flat f(tid, nt, s + 1, cw - 1, s, ch); f.b < nreg; f.next()) {  // Ey edge columns s+1 .. Wr-s-1,
+      const int c = f.v * Wr + f.u;                                         // rows s .. Hr-s-1
       const T* ma = MA(f.b);
       const T* ms = MS(f.b);
       const T* hz = H(f.b);
@@ -1256,7 +1295,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   }
   // ---- write back the zones: Hz of the live zone cells, their bottom Ex and left Ey edges
   if (nz > 0)
-    for (Flat f(tid, nt, zu0, zw, zv0, zv1 - zv0); f.b < nr; f.next()) {
+    for (Flat f(tid, nt, zu0, zw, zv0, zv1 - zv0); f.b < nreg; f.next()) {
       const int t = f.v * Wr + f.u;
       if (!(MA(f.b)[t] >= T(0))) continue;
       const int64_t o = bs.gbase[f.b] + (int64_t)f.v * P + f.u;
@@ -1272,7 +1311,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     for (int i = tid; i < m.q1 + m.q2; i += nt) sv[i] = xf[i];
     __syncthreads();
   }
-  store_rom(p, m, first, nb, B, S, sv, p.ex1, p.ey1);
+  store_rom(p, m, mem, nb, B, S, sv, p.ex1, p.ey1);
 }
 
 template <typename T, int K, bool ENERGY>
@@ -1295,11 +1334,12 @@ __global__ void __launch_bounds__(512, 1) postk_kernel(const PostParams<T> p) {
   if (b < p.n_batch_reg) fixup_batch<T, K, ENERGY>(p, b, sv, g, step, bs);
   if (ENERGY && b < p.n_batch_reg) {  // this batch's ROM + zone energies, one value per step (level 1)
     __syncthreads();              // rom_partials of this batch written (fixup_batch ends with barriers)
-    const int first = p.batch_tab[5 * b + 1], nb = p.batch_tab[5 * b + 2];
+    const int32_t* mem = p.batch_inst + p.batch_tab[BATCH_FIELDS * b + 1];
+    const int nb = p.batch_tab[BATCH_FIELDS * b + 2];
 #pragma unroll 1
     for (int s = 0; s < K; ++s) {
       double v = 0.0;
-      for (int k = threadIdx.x; k < nb; k += blockDim.x) v += p.rom_partials[(int64_t)s * p.n_inst + first + k];
+      for (int k = threadIdx.x; k < nb; k += blockDim.x) v += p.rom_partials[(int64_t)s * p.n_inst + mem[k]];
       const double tot = block_sum(v, red);
       if (threadIdx.x == 0) p.level1[(int64_t)s * p.n_batch + b] = tot;
     }
@@ -1329,7 +1369,7 @@ __global__ void __launch_bounds__(512, 1) bigrom_kernel(const PostParams<T> p) {
     fixup_batch<T, K, ENERGY, true>(p, b, sv, g, step, bs, part);
     if (ENERGY && blockIdx.x == 0) {
       __syncthreads();
-      const int first = p.batch_tab[5 * b + 1];
+      const int first = p.batch_inst[p.batch_tab[BATCH_FIELDS * b + 1]];
 #pragma unroll 1
       for (int s = 0; s < K; ++s) {
         const double tot = block_sum(threadIdx.x == 0 ? p.rom_partials[(int64_t)s * p.n_inst + first] : 0.0, red);
@@ -1675,11 +1715,11 @@ void sweepk_launch(const SweepParams<T>& q, dim3 grid, int threads, cudaStream_t
   constexpr int V = (sizeof(T) == 4 && K < 4) ? 4 : 2;  // sweep_width
   const size_t smem = (K > 1 && !FDTD_REG_RING) ? (size_t)(threads / 32) * K * NCOEF * 32 * V * sizeof(T) : 0;
   if (q.partials) {
-    if (smem > 48 * 1024)
+    if (smem > 32 * 1024)  // (static shared memory counts against the 48 KB default too)
       cudaFuncSetAttribute(sweepk_kernel<T, K, V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     sweepk_kernel<T, K, V, true><<<grid, threads, smem, s>>>(q);
   } else {
-    if (smem > 48 * 1024)
+    if (smem > 32 * 1024)  // (static shared memory counts against the 48 KB default too)
       cudaFuncSetAttribute(sweepk_kernel<T, K, V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     sweepk_kernel<T, K, V, false><<<grid, threads, smem, s>>>(q);
   }
@@ -1712,11 +1752,11 @@ void postk_launch(const PostParams<T>& p, bool energy, cudaStream_t s) {
   const int grid = p.n_batch_reg;
   if (grid <= 0) return;
   if (energy) {
-    if (smem > 48 * 1024)
+    if (smem > 32 * 1024)  // (static shared memory counts against the 48 KB default too)
       cudaFuncSetAttribute(postk_kernel<T, K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     postk_kernel<T, K, true><<<grid, p.block, smem, s>>>(p);
   } else {
-    if (smem > 48 * 1024)
+    if (smem > 32 * 1024)  // (static shared memory counts against the 48 KB default too)
       cudaFuncSetAttribute(postk_kernel<T, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     postk_kernel<T, K, false><<<grid, p.block, smem, s>>>(p);
   }
@@ -1728,7 +1768,7 @@ template <typename T, int K, bool ENERGY>
 void bigrom_launch(const PostParams<T>& p, cudaStream_t s) {
   auto kern = bigrom_kernel<T, K, ENERGY>;
   const size_t smem = p.big_smem_bytes;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 32 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.big_grid);
   cfg.blockDim = dim3(512);
@@ -1758,7 +1798,7 @@ int big_grid_size(size_t smem, int K) {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   auto kern = K == 1 ? bigrom_kernel<T, 1, true> : bigrom_kernel<T, 2, true>;
   if constexpr (sizeof(T) == 4) if (K == 4) kern = bigrom_kernel<T, 4, true>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 32 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 512, smem) != cudaSuccess || per < 1) return 0;
   return nsm;
 }
@@ -1808,7 +1848,7 @@ void pml_launch(const PmlParams<T>& p, bool energy, cudaStream_t s) {
   const size_t smem = sizeof(T) * ((size_t)5 * Hr * WB + WB + (size_t)2 * Hr * (WB + 1));
   dim3 grid((p.rows + p.chunk - 1) / p.chunk, 2);
   auto kern = energy ? pml_kernel<T, K, true> : pml_kernel<T, K, false>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 32 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<grid, 256, smem, s>>>(p);
 }
 

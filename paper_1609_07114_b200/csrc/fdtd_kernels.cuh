@@ -85,13 +85,16 @@ struct RomModelDev {
 // with the ROM update (S4-S6, eq:connExplicit) between them; the zone cells (the ones the sweep
 // may have got wrong and whose energy it skipped) are written back.  Also: zone probes and the
 // per-batch ROM + zone energies (finalize_kernel sums them with the sweep's).
+constexpr int BATCH_FIELDS = 6;  // batch table entry: model, member offset, count, slots, region stride, kind
 template <typename T>
 struct PostParams {
   int n_inst;
   int n_batch;                     // batches of <= batch instances of one model (level-1 energy slots)
   int n_batch_reg;                 // batches [0, n_batch_reg): postk_kernel; the rest are single
                                    // instances of large models (bigrom_kernel, cooperative)
-  const int32_t* batch_tab;        // per batch: (model, first instance, count, slots B, region stride)
+  const int32_t* batch_tab;        // per batch: (model, member offset, count, slots B, region stride, kind)
+  const int32_t* batch_inst;       // the batches' members (instance indices)
+  const int32_t* batch_rect;       // per batch: the cluster's bounding box (i0, j0, w, h) (kind 1)
   const RomModelDev* models;
   const double* mpool;             // shared model operators (fp64), tiled for the DMMA GEMMs
   const T* Sk; const int64_t* Sk_off;        // per-instance Schur inverses (col-major nY x nY)
@@ -104,6 +107,7 @@ struct PostParams {
   const T* ex0; const T* ey0; const T* hz0;   // input buffer (state at step n)
   const T* mea; const T* msb;
   int64_t pitch, row_begin;
+  int64_t nx, ny;                  // global grid (cells outside load as dead cells)
   int row0;                        // local row of global row row_begin
   int Kz;                          // zone depth of the material marks (>= K)
   const int32_t* rects;            // per instance (i0, j0, bx, by), global

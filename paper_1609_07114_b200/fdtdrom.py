@@ -49,7 +49,8 @@ class Info(C.Structure):
     _fields_ = [("steps_taken", C.c_int64), ("n_instances", C.c_int64), ("kernel_launches", C.c_int64),
                 ("pitch", C.c_int64), ("sweep_ctas", C.c_int64), ("graphs", C.c_int32),
                 ("precision", C.c_int32), ("bytes_per_cell_step", C.c_double), ("steps_per_pass", C.c_int32),
-                ("sweep_stream", C.c_void_p), ("graph_builds", C.c_int64)]
+                ("sweep_stream", C.c_void_p), ("graph_builds", C.c_int64), ("fixup_clusters", C.c_int32),
+                ("big_instances", C.c_int32)]
 
 
 class RomSpec(C.Structure):  # fdtdrom_build.h

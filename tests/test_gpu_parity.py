@@ -194,9 +194,9 @@ def test_k_step_passes_bitwise_equal_one_step(which):
     else:
         s = configs.make("cfg3", n=256)
         s.sigma = np.zeros((s.ny, s.nx))
-    # deepest valid pass: fp64 vectors hold 2 columns; the ragged scene's instances sit 4-5 cells
-    # from the walls (a 4-step fix-up region needs 7)
-    kmax = 2 if (s.precision == 64 or which == "ragged") else 4
+    # deepest valid pass: fp64 vectors hold 2 columns (the ragged scene's instances sit 4-5 cells
+    # from the walls: their fix-up regions reach beyond the walls, where they hold dead cells)
+    kmax = 2 if s.precision == 64 else 4
     runs = []
     for spp in (1, 2, 4):
         g = gpu_from_scene(s)
@@ -417,3 +417,68 @@ def test_big_rom_path_k_bitwise(big_path):
         assert np.array_equal(outs[0][1], x)
         assert np.array_equal(outs[0][2], p)
         np.testing.assert_allclose(e, outs[0][3], rtol=2e-6)
+
+
+# ----------------------------------------------------------------- clusters (no global pass-depth cliff)
+def _dense_scene(precision, n=192, count=50, seed=5, nslabs=1):
+    """SURVEY Q19's placement rule: footprint + one-cell ring inside the grid, rings pairwise disjoint
+    -- instances 2 cells apart and next to the PEC walls, so four-step passes need fix-up clusters
+    and wall-clipped regions."""
+    rng = np.random.default_rng(seed)
+    dx = dy = 1e-3
+    fe, fs = sc.uniform_fill(6, 6, 3, seed, 1, 4, 0, 0.05)
+    m = rg.build_rom(6, 6, 3, dx, dy, fe, fs, 24, 30e9)
+    dt = 0.95 * m["fine_dt_limit"]
+    P = sc.place_blocks(n, n, [(6, 6)], count, seed, nslabs=nslabs, margin=1, clear=1)
+    probes = np.array([[1, 1], [n - 2, n - 2], [n // 2, 3]], np.int32)
+    steps = 400
+    return sc.Scene(name="dense", nx=n, ny=n, dx=dx, dy=dy, dt=dt, eps_r=rng.uniform(1, 3, (n, n)),
+                    sigma=rng.uniform(0, 0.05, (n, n)), precision=precision, steps=steps, source=(n // 3, n // 2 + 1),
+                    samples=sc.gaussian_samples(steps, dt, 30e9, True), probes=probes, models=[m], placements=P)
+
+
+def test_clusters_k4_bitwise_equal_k1():
+    """Dense placement: the deepest pass stays 4 (clusters + wall-clipped regions instead of the
+    round-1 global drop to one step per pass) and reproduces one-step passes bit for bit."""
+    s = _dense_scene(32)
+    outs = []
+    for spp in (1, 2, 4):
+        g = gpu_from_scene(s)
+        g.set_time_blocking(spp)
+        Ex, Ey, Hz, xs = consistent_random_state(s, 13)
+        g.set_window(0, 0, Ex, Ey, Hz)
+        g.set_rom_state(xs)
+        g.record_energy(True)
+        for n in (1, 2, 3, 5, 8, 40, 1, 7):
+            g.step(n)
+        info = g.info()
+        assert info.steps_per_pass == spp, (spp, info.steps_per_pass)
+        if spp > 1:
+            assert info.fixup_clusters >= (3 if spp == 4 else 1), (spp, info.fixup_clusters)
+        outs.append((g.get_window(), g.get_rom_state(), g.probe(), g.energy()))
+        g.close()
+    for (w, x, p, e) in outs[1:]:
+        for a, b in zip(outs[0][0], w):
+            assert np.array_equal(a, b)
+        assert np.array_equal(outs[0][1], x)
+        assert np.array_equal(outs[0][2], p)
+        np.testing.assert_allclose(e, outs[0][3], rtol=2e-6)
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_clusters_parity(precision):
+    s = _dense_scene(precision)
+    _compare(s, 400, 1e-10 if precision == 64 else 1e-4, random_init=5)
+
+
+def test_clusters_energy_non_increasing():
+    s = _dense_scene(32)
+    g = gpu_from_scene(s, source=False)
+    Ex, Ey, Hz, xs = consistent_random_state(s, 21)
+    g.set_window(0, 0, Ex, Ey, Hz)
+    g.set_rom_state(xs)
+    g.record_energy(True)
+    g.step(1000)
+    e = g.energy()
+    assert g.info().fixup_clusters >= 3
+    assert np.all(np.diff(e) <= 1e-6 * e[:-1]), np.max(np.diff(e) / e[:-1])

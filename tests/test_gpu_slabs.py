@@ -158,3 +158,21 @@ def test_literal_models_on_slabs_bitwise(nslab):
     assert np.array_equal(x1, x2)
     assert np.array_equal(p1, p2)
     np.testing.assert_allclose(e2, e1, rtol=1e-12)
+
+
+@pytest.mark.parametrize("nslab", [2, 4])
+def test_dense_clusters_slabs_bitwise_equal_single(nslab):
+    """Clusters and wall-clipped regions on row slabs (SURVEY Q19's placement rule, rings inside the
+    slabs): bit-identical to one context."""
+    from test_gpu_parity import _dense_scene
+
+    s = _dense_scene(32, nslabs=4)
+    assert slabs.check_partition(s.placements, s.models, s.ny, nslab)
+    init = consistent_random_state(s, 3)
+    (W1, x1, p1, e1) = run_single(s, 301, init)
+    (W2, x2, p2, e2) = run_group(s, 301, init, nslab, 4, check_spp=False)
+    for a, b in zip(W1, W2):
+        assert np.array_equal(a, b)
+    assert np.array_equal(x1, x2)
+    assert np.array_equal(p1, p2)
+    np.testing.assert_allclose(e2, e1, rtol=1e-6)

@@ -65,7 +65,12 @@ for a in (*W, x, p):
 print("RESULT " + json.dumps(dict(case=case, k=k, used=g.info().steps_per_pass, err=err, prec=s.precision,
                                   digest=h.hexdigest()[:16])))
 ''' % (ROOT, os.path.join(ROOT, "tests"), case, k, steps)
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    try:
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=240)
+    except subprocess.TimeoutExpired as e:
+        return {"case": case, "k": k, "rc": -9, "threads": threads, "trap": False,
+                "tail": "timeout: " + ((e.stdout or b"")[-300:].decode(errors="replace") if isinstance(e.stdout, bytes)
+                                       else str(e.stdout)[-300:])}
     line = [x for x in r.stdout.splitlines() if x.startswith("RESULT ")]
     out = json.loads(line[-1][7:]) if line else {"case": case, "k": k}
     out.update(rc=r.returncode, threads=threads, trap="FDTD_CHECK" in (r.stdout + r.stderr),
