@@ -919,13 +919,19 @@ fdtd_status apply_passes(fdtd_ctx* c, int k) {
   // decomposition runs the same arithmetic.  Batch order: regular batches, then the large ones.
   {
     const int M = 2 * k - 1;
+    // batch size: the fewest instances per CTA that still need no more waves of one-CTA-per-SM
+    // fix-up CTAs than 8 per CTA would (the phases are latency-bound, so a wave costs about the same
+    // whatever its batches hold; fewer instances per CTA shorten every phase): 4096 instances on
+    // 148 SMs -> 7 (4 waves), a 512-instance slab -> 4 (one wave)
     const char* env = getenv("FDTD_ROM_BATCH");
     int Bauto = 8;
-    if (c->d.nranks > 1) {
+    {
       int nsm = 148, dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-      while (Bauto > 1 && (int64_t)c->inst_model.size() <= (int64_t)(Bauto / 2) * 2 * nsm) Bauto /= 2;
+      const int64_t n = (int64_t)c->inst_model.size();
+      auto waves = [&](int b) { return ((n + b - 1) / b + nsm - 1) / nsm; };
+      while (Bauto > 1 && waves(Bauto - 1) == waves(8)) --Bauto;
     }
     const int Bmax = env ? std::max(1, std::min(64, atoi(env))) : Bauto;
     const char* benv = getenv("FDTD_BIG_Q");
@@ -2029,6 +2035,13 @@ fdtd_status fdtd_halo_plan(int32_t nranks, int32_t rank, int64_t row_begin, int6
     }
   return FDTD_OK;
 }
+
+#if FDTD_PHASES
+int fdtd_debug_phases(long long* out, int n) {  // tuning builds only (tools/phase_times.py)
+  fdtd::debug_phases(out, n);
+  return 0;
+}
+#endif
 
 void fdtd_destroy(fdtd_ctx* c) {
   if (!c) return;

@@ -13,6 +13,7 @@
 //  finalize_kernel   : fixed-order energy sum of the pass and the device step counter.
 #include "fdtd_kernels.cuh"
 
+#include <algorithm>
 #include <climits>
 #include <cstdio>
 
@@ -648,6 +649,26 @@ __device__ double block_sum(double v, double* red) {
 // products and sums are fp64 and only the result is rounded to the state precision (fp32 states
 // get a more accurate ROM update than fp32 FMAs would give).  Each output column depends on that
 // column only, so a batch's composition never changes an instance's values.
+// FDTD_PHASES=1 (a tuning build, tools/phase_times.py): thread 0 of each fix-up CTA stamps
+// clock64() at every phase barrier into g_phase (read back with fdtd_debug_phases)
+#ifndef FDTD_PHASES
+#define FDTD_PHASES 0
+#endif
+#if FDTD_PHASES
+__device__ long long g_phase[4096][72];
+__device__ __forceinline__ int& ph_counter() {
+  __shared__ int ph;
+  return ph;
+}
+#define PHASE()                                                                                      \
+  do {                                                                                               \
+    if (threadIdx.x == 0 && blockIdx.x < 4096 && ph_counter() < 72) g_phase[blockIdx.x][ph_counter()++] = clock64(); \
+  } while (0)
+#else
+#define PHASE() \
+  do {          \
+  } while (0)
+#endif
 #ifndef FDTD_TPW  // dmma_gemm: row tiles per warp sharing a B fragment; A tiles in flight
 #define FDTD_TPW 3
 #endif
@@ -656,6 +677,9 @@ __device__ double block_sum(double v, double* red) {
 #endif
 #ifndef FDTD_SCHUR16  // Schur solve: 16 loads in flight per thread
 #define FDTD_SCHUR16 1
+#endif
+#ifndef FDTD_REGION_LDG  // region loads: register-staged loads (1) or per-element cp.async (0)
+#define FDTD_REGION_LDG 0
 #endif
 #ifndef FDTD_SKPF  // prefetch the batch's Schur inverses into L2 at the batch start
 #define FDTD_SKPF 1
@@ -781,6 +805,7 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, const int
               [&](int r, int c, double x) { so[r * B + c] = (T)x; });
   }
   __syncthreads();
+  PHASE();
   if (ENERGY) {  // x~^T R~ x~ + sum D_l D_l' eps/dt y^2 (storage function, R17); one warp per instance
     const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
     for (int b = w; b < nb; b += nw) {
@@ -802,6 +827,7 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, const int
     v.st[k] = v.so[(q2 + q1 + i) * B + b] + fma_rn(rc.cyg[k], v.sh[k], mul_rn(rc.cya[k], v.sy[k]));
   }
   __syncthreads();
+  PHASE();
   // U = S_k t (per-instance Schur inverse, L2-resident after the prefetch at the batch start)
   for (int it = tid; it < nY * nb; it += nt) {
     const int i = it % nY, b = it / nY;
@@ -822,6 +848,7 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, const int
     v.sU[i * B + b] = (a[0] + a[1]) + (a[2] + a[3]);
   }
   __syncthreads();
+  PHASE();
   // [E~^{n+1}; y^{n+1}] = [E*; L~^T E*] + M2 U (the base added in fp64 in the epilogue; literal:
   // y' = the U rows themselves), and H~^{n+1} = so rows 0 .. q2 copied beside it
   {
@@ -836,6 +863,7 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, const int
     for (int64_t k = tid; k < (int64_t)q2 * B; k += nt) sx[(int64_t)q1 * B + k] = so[k];
   }
   __syncthreads();
+  PHASE();
 }
 
 // ---- the large-model path (one instance at a time on the whole GPU; fdtd_api.cpp "big" models):
@@ -1128,12 +1156,71 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     bs.bv[b] = q[1] - o[1] + M;
   }
   __syncthreads();  // the zero padding lands before load_rom_state fills the live slots
+  PHASE();
   T* sy = sv + S;
   T* sh = sv + 2 * S;
   // ---- load the regions: materials and the fields at step n (asynchronous element copies, all in
   // flight at once: the region rows are not 16-byte aligned).  Outside the grid: dead cells (the
   // PEC walls), zero fields.
   const int64_t NX = p.nx, NY = p.ny;
+#if FDTD_REGION_LDG
+  // loads into registers, RU cells at a time per thread (all in flight), then the stores
+  constexpr int RU = 4;
+  for (Flat f(tid, nt, 0, Wr, 0, Hr); f.b < nreg;) {
+    int64_t o[RU];
+    int tt[RU], rr[RU];
+    bool in[RU];
+#pragma unroll
+    for (int k = 0; k < RU; ++k) {
+      in[k] = false;
+      rr[k] = -1;
+      if (f.b < nreg) {
+        const int64_t gi = bs.gi0[f.b] + f.u, gj = bs.gj0[f.b] + f.v;
+        in[k] = gi >= 0 && gi < NX && gj >= 0 && gj < NY;
+        o[k] = bs.gbase[f.b] + (int64_t)f.v * P + f.u;
+        tt[k] = f.v * Wr + f.u;
+        rr[k] = f.b;
+        f.next();
+      }
+    }
+    T a[RU], b[RU], h[RU];
+#pragma unroll
+    for (int k = 0; k < RU; ++k)
+      if (in[k]) { a[k] = __ldg(p.mea + o[k]); b[k] = __ldg(p.msb + o[k]); h[k] = __ldg(p.hz0 + o[k]); }
+      else { a[k] = T(-1); b[k] = T(0); h[k] = T(0); }
+#pragma unroll
+    for (int k = 0; k < RU; ++k)
+      if (rr[k] >= 0) { MA(rr[k])[tt[k]] = a[k]; MS(rr[k])[tt[k]] = b[k]; H(rr[k])[tt[k]] = h[k]; }
+  }
+  for (int e = 0; e < 2; ++e) {  // Ex edge rows (Hr + 1 rows x Wr), Ey edge columns (Hr rows x Wr + 1)
+    const int cw = e ? W1 : Wr, chh = e ? Hr : Hr + 1, pw = e ? W1 : Wr;
+    const T* src = e ? p.ey0 : p.ex0;
+    for (Flat f(tid, nt, 0, cw, 0, chh); f.b < nreg;) {
+      int64_t o[2 * RU];
+      int tt[2 * RU], rr[2 * RU];
+      bool in[2 * RU];
+#pragma unroll
+      for (int k = 0; k < 2 * RU; ++k) {
+        in[k] = false;
+        rr[k] = -1;
+        if (f.b < nreg) {
+          const int64_t gi = bs.gi0[f.b] + f.u, gj = bs.gj0[f.b] + f.v;
+          in[k] = e ? (gi >= 0 && gi <= NX && gj >= 0 && gj < NY) : (gi >= 0 && gi < NX && gj >= 0 && gj <= NY);
+          o[k] = bs.gbase[f.b] + (int64_t)f.v * P + f.u;
+          tt[k] = f.v * pw + f.u;
+          rr[k] = f.b;
+          f.next();
+        }
+      }
+      T x[2 * RU];
+#pragma unroll
+      for (int k = 0; k < 2 * RU; ++k) x[k] = in[k] ? __ldg(src + o[k]) : T(0);
+#pragma unroll
+      for (int k = 0; k < 2 * RU; ++k)
+        if (rr[k] >= 0) (e ? EY(rr[k]) : EX(rr[k]))[tt[k]] = x[k];
+    }
+  }
+#else
   for (Flat f(tid, nt, 0, Wr, 0, Hr); f.b < nreg; f.next()) {
     const int t = f.v * Wr + f.u;
     const int64_t gi = bs.gi0[f.b] + f.u, gj = bs.gj0[f.b] + f.v;
@@ -1159,7 +1246,10 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     if (gi >= 0 && gi <= NX && gj >= 0 && gj < NY) cp_async_el(EY(f.b) + f.v * W1 + f.u, p.ey0 + bs.gbase[f.b] + (int64_t)f.v * P + f.u);
     else EY(f.b)[f.v * W1 + f.u] = T(0);
   }
+#endif
+  PHASE();
   if (!BIG) load_rom_state(p, m, mem, nb, B, sv);  // (BIG: the ROM step reads x~ from global memory)
+  PHASE();
   for (int it = tid; FDTD_SKPF && it < nr * ((nY * nY + 31) / 32); it += nt) {  // the batch's Schur inverses into L2
     const int b = it % nr, l = it / nr;
     prefetch_l2(p.Sk + p.Sk_off[mem[b]] + l * 32);
@@ -1171,8 +1261,10 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     rc.cya[i * B + b] = p.cya[po];
     rc.cyg[i * B + b] = p.cyg[po];
   }
+  PHASE();
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  PHASE();
   // Values go wrong from the region's border inwards one cell per step, so step s only updates the
   // cone that is still exact: cells [s, Wr - s) x [s, Hr - s) (edges one further in across their
   // normal); the zone, the ROM's gather cells and the write-back all lie inside the last cone.
@@ -1205,6 +1297,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       hz[t] = h;
     }
     __syncthreads();
+    PHASE();
     // ---- zone probes; S4 gather of y^{n+s} (interface edges) and h = Hz^{n+s+1/2} (outside cells)
     for (int b = 0; b < nr; ++b) {
       const int z0 = p.zp_off[mem[b]], z1 = p.zp_off[mem[b] + 1];
@@ -1249,6 +1342,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       }
     }
     __syncthreads();
+    PHASE();
     // ---- S5: ROM step n+s -> y^{n+s+1}, x~^{n+s+1}; ROM energy of W^{n+s} (+ the zone energy of
     // the member's region on its first member)
     double* ep = p.rom_partials + (int64_t)s * p.n_inst;
@@ -1292,6 +1386,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       if (l) ey[f.v * W1 + f.u] = eupd(ey[f.v * W1 + f.u], ca, cb, hz[c] - hz[c - 1]);
     }
     __syncthreads();
+    PHASE();
   }
   // ---- write back the zones: Hz of the live zone cells, their bottom Ex and left Ey edges
   if (nz > 0)
@@ -1310,6 +1405,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     const T* xf = ((K - 1) & 1) ? bsc.X1 : bsc.X0;
     for (int i = tid; i < m.q1 + m.q2; i += nt) sv[i] = xf[i];
     __syncthreads();
+    PHASE();
   }
   store_rom(p, m, mem, nb, B, S, sv, p.ex1, p.ey1);
 }
@@ -1321,6 +1417,10 @@ __global__ void __launch_bounds__(512, 1) postk_kernel(const PostParams<T> p) {
   __shared__ BatchShared bs;
   T* sv = reinterpret_cast<T*>(smem_raw);
   const int b = blockIdx.x;
+#if FDTD_PHASES
+  if (threadIdx.x == 0) ph_counter() = 0;
+  PHASE();
+#endif
   const int64_t step = *p.step;
   T g[K];
 #pragma unroll
@@ -1332,6 +1432,7 @@ __global__ void __launch_bounds__(512, 1) postk_kernel(const PostParams<T> p) {
     }
   }
   if (b < p.n_batch_reg) fixup_batch<T, K, ENERGY>(p, b, sv, g, step, bs);
+  PHASE();
   if (ENERGY && b < p.n_batch_reg) {  // this batch's ROM + zone energies, one value per step (level 1)
     __syncthreads();              // rom_partials of this batch written (fixup_batch ends with barriers)
     const int32_t* mem = p.batch_inst + p.batch_tab[BATCH_FIELDS * b + 1];
@@ -1761,6 +1862,13 @@ void postk_launch(const PostParams<T>& p, bool energy, cudaStream_t s) {
     postk_kernel<T, K, false><<<grid, p.block, smem, s>>>(p);
   }
 }
+
+#if FDTD_PHASES
+void debug_phases(long long* out, int n) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_phase, sizeof(long long) * (size_t)std::min(n, 4096 * 72));
+}
+#endif
 
 void launch_finalize(const FinParams& p, cudaStream_t s) { finalize_kernel<<<p.energy ? FIN_GRID : 1, 256, 0, s>>>(p); }
 

@@ -226,4 +226,8 @@ template <typename T>
 void launch_zone(T* msb, const T* mea, int64_t pitch, const int32_t* rects, int64_t n_rect, int64_t row_begin,
                  int row0, int Kz, bool set, cudaStream_t s);
 
+#if FDTD_PHASES
+void debug_phases(long long* out, int n);  // tuning builds: the fix-up's phase stamps
+#endif
+
 }  // namespace fdtd

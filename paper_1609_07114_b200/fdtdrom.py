@@ -117,6 +117,8 @@ def lib():
         L.fdtd_rom_build.restype = C.c_int
         L.fdtd_rom_build_last_error.argtypes = []
         L.fdtd_rom_build_last_error.restype = C.c_char_p
+        if hasattr(L, "fdtd_debug_phases"):  # tuning builds (FDTD_PHASES)
+            L.fdtd_debug_phases.argtypes = [vp, i32]
         for n in ("create", "add_rom", "set_source", "set_probes", "record_energy", "step", "probe", "energy",
                   "get_window", "set_window", "get_rom_state", "set_rom_state", "sync", "get_info", "set_tuning",
                   "nccl_unique_id", "profile", "profile_read", "step_group", "set_time_blocking",
