@@ -759,6 +759,8 @@ __device__ __forceinline__ void dmma_gemm(const TA* __restrict__ At, int mtiles,
 //   sx = [E~; H~] (q1 + q2), sy = y (nY), sh = h (nY), so = [M1; R~] x (q2 + q1 + nY + q1 + q2, two
 //   slots), st = t (nY), sU = U (nY)
 constexpr int NROMVEC = 7;  // vector slots of one batch (stride S = (q1 + q2 + nY) x B each)
+// the slot stride, rounded up to 4 elements so that the fp64 constants after the slots stay aligned
+__host__ __device__ inline int64_t vec_stride(int nvec, int B) { return ((int64_t)nvec * B + 3) / 4 * 4; }
 template <typename T>
 struct RomVec {
   T *sx, *sy, *sh, *so, *st, *sU;
@@ -1104,7 +1106,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   const int32_t* mem = p.batch_inst + bt[1];
   const RomModelDev m = p.models[model];
   const int nY = m.nY;
-  const int64_t S = (int64_t)(m.q1 + m.q2 + nY) * B;  // vector stride of this batch's layout
+  const int64_t S = vec_stride(m.q1 + m.q2 + nY, B);  // vector stride of this batch's layout
   const int tid = threadIdx.x, nt = blockDim.x;
   // BIG (one instance on the whole cooperative grid): only CTA 0 holds the region; the others take
   // part in the ROM step only (nr = nreg = 0 empties every region loop of theirs)
@@ -1843,8 +1845,8 @@ void launch_sweep(const SweepParams<T>& p, int K, int warps_per_cta, cudaStream_
 
 size_t post_smem_bytes(size_t es, int nvec, int nY, int batch, int region_stride) {
   // ROM vectors, the per-pass port constants (fp64 eh + two T arrays), the zone partials, the regions
-  return es * ((size_t)NROMVEC * nvec * batch + (size_t)(8 / es + 2) * nY * batch + (size_t)batch * ZWARPS * (8 / es) +
-               (size_t)batch * region_stride);
+  return es * ((size_t)NROMVEC * vec_stride(nvec, batch) + (size_t)(8 / es + 2) * nY * batch +
+               (size_t)batch * ZWARPS * (8 / es) + (size_t)batch * region_stride);
 }
 
 template <typename T, int K>
