@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <type_traits>
 #include <cstdio>
 
 #include <cooperative_groups.h>
@@ -179,6 +180,14 @@ template <typename T>
 __device__ __forceinline__ bool cell_dead(T wx) { return signbit(wx); }
 template <typename T>
 __device__ __forceinline__ T cell_hw(T wx, T wy, T wh) { return (signbit(wx) | signbit(wy)) ? T(0) : wh; }
+#ifndef FDTD_EFAST  // sweep energy: cheaper Hz weight and fp32 row sums flushed to fp64 every 16 rows
+#define FDTD_EFAST 0  // measured: no change in the sweep time (it is not issue-bound), one register spill
+#endif
+// The Hz weight of the sweep's packed energy term without a select: wh, or 0 on a zone cell (wy = -0).
+// A dead cell (hole, wall, padding) keeps Hz = 0, so its weight does not matter: wh * 0 * 0 = 0.
+__device__ __forceinline__ F2 cell_hw2(float wy0, float wy1, float hwh) {
+  return fma2(F2{copysignf(1.f, wy0), copysignf(1.f, wy1)}, F2{hwh, hwh}, F2{hwh, hwh});  // hwh = wh / 2
+}
 
 template <typename T, int V>
 __device__ __forceinline__ void row_coef(const T (&ma)[V], const T (&ms)[V], const T (&mb)[V], const T (&sb)[V],
@@ -318,7 +327,11 @@ __device__ __forceinline__ float yee_row_f2(const float (&exb)[V], const float (
 #pragma unroll
     for (int k = 0; k < V; k += 2) {
       const F2 ex2{exb[k], exb[k + 1]}, ey2{ey[k], ey[k + 1]};
+#if FDTD_EFAST
+      const F2 hw = cell_hw2(wy[k], wy[k + 1], 0.5f * p.wh);
+#else
       const F2 hw{cell_hw(wx[k], wy[k], p.wh), cell_hw(wx[k + 1], wy[k + 1], p.wh)};
+#endif
       acc = fma2(mul2(F2{wx[k], wx[k + 1]}, ex2), ex2, acc);
       acc = fma2(mul2(F2{wy[k], wy[k + 1]}, ey2), ey2, acc);
       acc = fma2(mul2(hw, F2{hz[k], hz[k + 1]}), F2{hn[k], hn[k + 1]}, acc);
@@ -412,10 +425,10 @@ __device__ __forceinline__ T yee_any(const T (&exb)[V], const T (&ext)[V], const
     return yee_row<T, V, ENERGY>(exb, ext, ey, hz, hb, cs, p, gsrc, srow, src_k, hn, exo, eyo);
 }
 
-template <typename T, int V, int K, bool ENERGY, bool CHK, int T0>
+template <typename T, int V, int K, bool ENERGY, bool CHK, int T0, typename EA>
 __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCtx<T, V, K>& x, int j, int je,
                                           const RowIn<T, V>& X, RowIn<T, V>& Y, const StageOut<T, V, K>& A,
-                                          StageOut<T, V, K>& B, double (&eacc)[K], RowCoef<T, V> (&rc)[K]) {
+                                          StageOut<T, V, K>& B, EA (&eacc)[K], RowCoef<T, V> (&rc)[K]) {
   // T0 = (j - jb) mod the loop's unroll: the coefficient set of row j - s lives in rc[(T0 - s) mod K]
   // (registers, statically named; FDTD_REG_RING) or in the shared-memory ring
   // CHK: some stage rows may lie outside the chunk [r0, r1) (energy, probes and stores skip them)
@@ -432,7 +445,7 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
     const T en = yee_any<T, V, ENERGY>(Y.ext, X.ext, X.ey, X.hz, A.h[0], CoefRegs<T, V>{cf}, p, x.g[0],
                                        CHK && j >= x.src_r && j < x.src_r1, x.src_k, B.h[0], B.x[0], B.y[0]);
     const bool own = !CHK || (j >= x.r0 && j < x.r1);
-    if (ENERGY && own) eacc[0] += (double)en;
+    if (ENERGY && own) eacc[0] += (EA)en;
     if (CHK && own && x.out) record_probes<T, V>(p, j, B.h[0], x.slot[0], (int32_t)x.c);
   }
   if (j + 1 < je) {  // row j+1 into the buffer of row j-1 (consumed above)
@@ -464,7 +477,7 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
     const T en = yee_any<T, V, ENERGY>(A.x[s - 1], B.x[s - 1], A.y[s - 1], A.h[s - 1], A.h[s], cr, p, x.g[s],
                                        CHK && r >= x.src_r && r < x.src_r1, x.src_k, B.h[s], B.x[s], B.y[s]);
     const bool own = !CHK || (r >= x.r0 && r < x.r1);
-    if (ENERGY && own) eacc[s] += (double)en;
+    if (ENERGY && own) eacc[s] += (EA)en;
     if (CHK && own && x.out) record_probes<T, V>(p, r, B.h[s], x.slot[s], (int32_t)x.c);
   }
   // stage K-1's outputs are the fields at step n+K of row j-K+1
@@ -553,9 +566,16 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   for (int s = 0; s < K; ++s)
 #pragma unroll
     for (int k = 0; k < V; ++k) O0.h[s][k] = O0.x[s][k] = O0.y[s][k] = T(0);
-  double eacc[K];
+  // energy partials: per stage, the rows' sums in EA (fp32 with FDTD_EFAST, flushed into the fp64
+  // dacc every 16 rows) -- fp64 over the chunk
+  using EA = typename std::conditional<FDTD_EFAST && sizeof(T) == 4, float, double>::type;
+  EA eacc[K];
+  double dacc[K];
 #pragma unroll
-  for (int s = 0; s < K; ++s) eacc[s] = 0.0;
+  for (int s = 0; s < K; ++s) {
+    eacc[s] = EA(0);
+    dacc[s] = 0.0;
+  }
   // does this warp's strip hold a probe in the chunk's rows?  (scanned once per warp)
   bool warp_probes = false;
   if (p.probe_rows) {
@@ -603,16 +623,21 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
         if (j + 3 < je) sweep_row<T, V, K, ENERGY, true, 3>(p, x, j + 3, je, R0, R1, O1, O0, eacc, rc);
       }
     }
-  }
-  if (!x.out) {
+    if (ENERGY && sizeof(EA) == 4 && ((j - jb) & 15) == 16 - U) {
 #pragma unroll
-    for (int s = 0; s < K; ++s) eacc[s] = 0.0;
+      for (int s = 0; s < K; ++s) {
+        dacc[s] += (double)eacc[s];
+        eacc[s] = EA(0);
+      }
+    }
   }
+#pragma unroll
+  for (int s = 0; s < K; ++s) dacc[s] = x.out ? dacc[s] + (double)eacc[s] : 0.0;
   if (ENERGY) {
     __shared__ double red[K][32];
 #pragma unroll
     for (int s = 0; s < K; ++s) {
-      double v = eacc[s];
+      double v = dacc[s];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FULL, v, o);
       if (x.lane == 0) red[s][warp] = v;
