@@ -136,9 +136,12 @@ def run_reference(args):
     if rank != 0:
         return 0
     wl = args.workload
-    # warm-up steps then K timed steps, each a step of the bounded sample
+    # warm-up steps, then the timed steps of the bounded sample: at least K and at least ~10 s of
+    # stepping (a 20-step run would time mostly start-up), at most 240 s
     oracle_rate(wl, max(args.warmup, 0), max_seconds=60)
-    v, dt, done, sample, cores = oracle_rate(wl, args.steps, max_seconds=240)
+    v0, dt0, done0, _, _ = oracle_rate(wl, max(args.steps, 8), max_seconds=30)
+    want = max(args.steps, int(10.0 * done0 / max(dt0, 1e-9)))
+    v, dt, done, sample, cores = oracle_rate(wl, want, max_seconds=240)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": done,
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(done, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",

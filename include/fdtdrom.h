@@ -272,6 +272,16 @@ fdtd_status fdtd_set_tuning(fdtd_ctx *c, int32_t rows_per_cta, int32_t warps_per
 fdtd_status fdtd_halo_plan(int32_t nranks, int32_t rank, int64_t row_begin, int64_t row_end, int32_t depth,
                            int32_t pml, int64_t *out, int32_t cap, int32_t *n);
 
+/* Fix-up regions of a `depth`-step pass (the temporal blocking of
+ * north_star (2), no paper counterpart): instances (rects[4k..4k+3] = i0, j0, bx, by; models[k] their
+ * model) whose blocks grown by `depth` cells meet, directly or through others, share one region --
+ * merged into their bounding box until no two regions' boxes grown by `depth` meet.  Host-only.
+ * region[k] receives instance k's region index; boxes (optional, 5 per region) the region's
+ * (i0, j0, width, height, mixed-models flag); *n_regions the count.  depth 1: one region per
+ * instance. */
+fdtd_status fdtd_pass_regions(const int32_t *rects, const int32_t *models, int64_t n, int32_t depth,
+                              int32_t *region, int32_t *boxes, int64_t *n_regions);
+
 /* Fill out[128] with a fresh ncclUniqueId (rank 0 calls it and broadcasts the bytes, e.g. with
  * torch.distributed.broadcast).  FDTD_E_NCCL if libnccl.so.2 cannot be loaded. */
 fdtd_status fdtd_nccl_unique_id(void *out128);

@@ -718,18 +718,19 @@ struct PassRegion {
   int64_t i0 = 0, j0 = 0, i1 = 0, j1 = 0;  // bounding box of the blocks [i0, i1) x [j0, j1)
 };
 
-std::vector<PassRegion> pass_regions(const fdtd_ctx* c, int K) {
+std::vector<PassRegion> pass_regions_of(const std::vector<int32_t>& rects, const std::vector<int32_t>& inst_model,
+                                        int K) {
   // Start from one region per instance and merge any two regions whose boxes, grown by K, meet --
   // with the merged (bounding) boxes, until no pair meets: then no region's box + 2K - 1 reaches
   // into another region, whatever the shape of a cluster.
-  const int n = (int)c->inst_model.size();
+  const int n = (int)inst_model.size();
   std::vector<PassRegion> cur(n);
   for (int i = 0; i < n; ++i) {
     PassRegion& g = cur[i];
-    g.model = c->inst_model[i];
+    g.model = inst_model[i];
     g.members = {i};
-    g.i0 = c->rects[4 * i]; g.j0 = c->rects[4 * i + 1];
-    g.i1 = g.i0 + c->rects[4 * i + 2]; g.j1 = g.j0 + c->rects[4 * i + 3];
+    g.i0 = rects[4 * i]; g.j0 = rects[4 * i + 1];
+    g.i1 = g.i0 + rects[4 * i + 2]; g.j1 = g.j0 + rects[4 * i + 3];
   }
   if (K < 2) return cur;
   for (bool merged = true; merged;) {
@@ -772,6 +773,7 @@ std::vector<PassRegion> pass_regions(const fdtd_ctx* c, int K) {
   }
   return cur;
 }
+std::vector<PassRegion> pass_regions(const fdtd_ctx* c, int K) { return pass_regions_of(c->rects, c->inst_model, K); }
 
 // shared memory of one fix-up batch: B member slots of model m's vectors plus nreg regions of
 // stride rs
@@ -2042,6 +2044,25 @@ int fdtd_debug_phases(long long* out, int n) {  // tuning builds only (tools/pha
   return 0;
 }
 #endif
+
+fdtd_status fdtd_pass_regions(const int32_t* rects, const int32_t* models, int64_t n, int32_t depth, int32_t* region,
+                              int32_t* boxes, int64_t* n_regions) {
+  if (n < 0 || (n > 0 && (!rects || !models || !region)) || depth < 1 || depth > KMAX || !n_regions) return FDTD_E_ARG;
+  std::vector<int32_t> r(rects, rects + 4 * n), m(models, models + n);
+  const std::vector<PassRegion> regs = pass_regions_of(r, m, depth);
+  *n_regions = (int64_t)regs.size();
+  for (size_t g = 0; g < regs.size(); ++g) {
+    for (int i : regs[g].members) region[i] = (int32_t)g;
+    if (boxes) {
+      boxes[5 * g + 0] = (int32_t)regs[g].i0;
+      boxes[5 * g + 1] = (int32_t)regs[g].j0;
+      boxes[5 * g + 2] = (int32_t)(regs[g].i1 - regs[g].i0);
+      boxes[5 * g + 3] = (int32_t)(regs[g].j1 - regs[g].j0);
+      boxes[5 * g + 4] = regs[g].mixed ? 1 : 0;
+    }
+  }
+  return FDTD_OK;
+}
 
 void fdtd_destroy(fdtd_ctx* c) {
   if (!c) return;

@@ -108,6 +108,7 @@ def lib():
         L.fdtd_profile_read.argtypes = [vp, dp, dp, C.POINTER(i64)]
         L.fdtd_nccl_unique_id.argtypes = [vp]
         L.fdtd_halo_plan.argtypes = [i32, i32, i64, i64, i32, i32, vp, i32, C.POINTER(i32)]
+        L.fdtd_pass_regions.argtypes = [vp, vp, i64, i32, vp, vp, C.POINTER(i64)]
         L.fdtd_last_error.argtypes = [vp]
         L.fdtd_last_error.restype = C.c_char_p
         L.fdtd_status_string.restype = C.c_char_p
@@ -122,7 +123,7 @@ def lib():
         for n in ("create", "add_rom", "set_source", "set_probes", "record_energy", "step", "probe", "energy",
                   "get_window", "set_window", "get_rom_state", "set_rom_state", "sync", "get_info", "set_tuning",
                   "nccl_unique_id", "profile", "profile_read", "step_group", "set_time_blocking",
-                  "set_source_line", "set_pml", "halo_plan"):
+                  "set_source_line", "set_pml", "halo_plan", "pass_regions"):
             getattr(L, "fdtd_" + n).restype = C.c_int
         _lib = L
     return _lib
@@ -177,6 +178,20 @@ def halo_plan(nranks, rank, row_begin, row_end, depth, pml=False):
     if st:
         raise FDTDError(st, "fdtd_halo_plan rejected its arguments")
     return out[: n.value]
+
+
+def pass_regions(rects, models, depth):
+    """fdtd_pass_regions: (region index per instance, boxes [n_regions, 5] = i0, j0, w, h, mixed)."""
+    r = np.ascontiguousarray(np.asarray(rects, dtype=np.int32).reshape(-1, 4))
+    m = np.ascontiguousarray(np.asarray(models, dtype=np.int32).reshape(-1))
+    n = r.shape[0]
+    reg = np.zeros(max(n, 1), np.int32)
+    boxes = np.zeros((max(n, 1), 5), np.int32)
+    nr = C.c_int64(0)
+    st = lib().fdtd_pass_regions(_ptr(r), _ptr(m), n, int(depth), _ptr(reg), _ptr(boxes), C.byref(nr))
+    if st:
+        raise FDTDError(st, "fdtd_pass_regions rejected its arguments")
+    return reg[:n], boxes[: nr.value]
 
 
 def nccl_unique_id() -> bytes:
