@@ -706,6 +706,9 @@ __device__ __forceinline__ int& ph_counter() {
 #ifndef FDTD_REGION_LDG  // region loads: register-staged loads (1) or per-element cp.async (0)
 #define FDTD_REGION_LDG 0
 #endif
+#ifndef FDTD_M2PRE  // M2's operator tiles loaded into registers before the Schur phase
+#define FDTD_M2PRE 0  // measured: M2 4 k instead of 6 k cycles, but M1 loses its registers (16 k instead of 10 k)
+#endif
 #ifndef FDTD_SKPF  // prefetch the batch's Schur inverses into L2 at the batch start
 #define FDTD_SKPF 1
 #endif
@@ -855,6 +858,16 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, const int
   }
   __syncthreads();
   PHASE();
+  // M2's operator tiles, when every warp holds at most one of at most 16 k-tiles: loaded now, in
+  // flight during the Schur phase (the M2 phase then waits on no L2 round trip)
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  const bool pre2 = FDTD_M2PRE && m.mt2 <= nwarp && m.kt2 <= 16 && B <= 8;
+  double a2[16];
+  if (pre2) {
+    const double* ap = p.mpool + m.off_M2t + (int64_t)(warp < m.mt2 ? warp : 0) * m.kt2 * 32 + lane;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a2[k] = (k < m.kt2 && warp < m.mt2) ? __ldg(ap + k * 32) : 0.0;
+  }
   // U = S_k t (per-instance Schur inverse, L2-resident after the prefetch at the batch start)
   for (int it = tid; it < nY * nb; it += nt) {
     const int i = it % nY, b = it / nY;
@@ -883,10 +896,29 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, const int
     T* sy = v.sy;
     const T* so = v.so;
     const bool lit = m.literal != 0;
-    dmma_gemm(p.mpool + m.off_M2t, m.mt2, m.kt2, m2, nY, v.sU, B, [&](int r, int c, double x) {
+    auto epi = [&](int r, int c, double x) {
       if (r < q1) sx[r * B + c] = (T)((double)so[(q2 + r) * B + c] + x);
       else sy[(r - q1) * B + c] = (T)((lit ? 0.0 : -(double)so[(q2 + r) * B + c]) + x);
-    });
+    };
+    if (pre2) {
+      if (warp < m.mt2) {  // the same DMMA sequence as dmma_gemm's, from the preloaded tiles
+        const int g = lane >> 2, t4 = lane & 3;
+        double d[2] = {0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (k < m.kt2) {
+            const int kk = k * 4 + t4;
+            mma_f64(d, a2[k], (g < B && kk < nY) ? (double)v.sU[kk * B + g] : 0.0);
+          }
+        const int r = warp * 8 + g, c0 = 2 * t4;
+        if (r < m2) {
+          if (c0 < B) epi(r, c0, d[0]);
+          if (c0 + 1 < B) epi(r, c0 + 1, d[1]);
+        }
+      }
+    } else {
+      dmma_gemm(p.mpool + m.off_M2t, m.mt2, m.kt2, m2, nY, v.sU, B, epi);
+    }
     for (int64_t k = tid; k < (int64_t)q2 * B; k += nt) sx[(int64_t)q1 * B + k] = so[k];
   }
   __syncthreads();
