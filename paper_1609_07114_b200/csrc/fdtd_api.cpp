@@ -273,7 +273,8 @@ fdtd::SweepParams<T> sweep_params(fdtd_ctx* c, int q) {
   p.idx = (T)(1.0 / c->d.dx); p.idy = (T)(1.0 / c->d.dy);
   p.wxy = (T)(c->d.dx * c->d.dy);
   p.wh = (T)(MU0 * c->d.dx * c->d.dy / c->d.dt);
-  p.alloc_elems = alloc_elems(c);
+  p.naf = p.nam = 1;
+  p.alloc_elems_f = p.alloc_elems_m = alloc_elems(c);
   return p;
 }
 

@@ -108,6 +108,9 @@ __device__ __forceinline__ void cp_async_el(T* dst, const T* src) {
 #ifndef FDTD_REG_RING  // sweep: coefficient ring of K rows in registers (1) or shared memory (0)
 #define FDTD_REG_RING 0
 #endif
+#ifndef FDTD_EXP  // sweep diagnostics (tools/sweep_layout_probe.cu only): 1 no ring loads, 4 no stores
+#define FDTD_EXP 0
+#endif
 #ifndef FDTD_PFD
 #define FDTD_PFD 1  // sweep: row distance of the L2 prefetch beyond the register-prefetched row (measured best)
 #endif
@@ -181,7 +184,7 @@ __device__ __forceinline__ bool cell_dead(T wx) { return signbit(wx); }
 template <typename T>
 __device__ __forceinline__ T cell_hw(T wx, T wy, T wh) { return (signbit(wx) | signbit(wy)) ? T(0) : wh; }
 #ifndef FDTD_EFAST  // sweep energy: cheaper Hz weight and fp32 row sums flushed to fp64 every 16 rows
-#define FDTD_EFAST 0  // measured: no change in the sweep time (it is not issue-bound), one register spill
+#define FDTD_EFAST 1  // round 2 measured -2.5 % per sweep pass (cold and power-capped, tools/sweep_layout_probe.cu)
 #endif
 // The Hz weight of the sweep's packed energy term without a select: wh, or 0 on a zone cell (wy = -0).
 // A dead cell (hole, wall, padding) keeps Hz = 0, so its weight does not matter: wh * 0 * 0 = 0.
@@ -222,12 +225,26 @@ struct CoefRegs {
     for (int k = 0; k < V; ++k) { a[k] = c.wx[k]; b[k] = c.wy[k]; }
   }
 };
+#ifndef FDTD_RING128  // fp32 pairs: the ring holds (a, b) vector pairs as one 16-byte LDS / STS each
+#define FDTD_RING128 1
+#endif
+template <typename T, int V>
+__host__ __device__ constexpr bool ring_packed() { return FDTD_RING128 && sizeof(T) == 4 && V == 2; }
 template <typename T, int V>
 struct CoefRing {
-  const T* b;  // this lane's slot: component i at b + i * 32 * V
-  __device__ __forceinline__ void ex(T (&a)[V], T (&c)[V]) const { ldv_s(b, a); ldv_s(b + 32 * V, c); }
-  __device__ __forceinline__ void ey(T (&a)[V], T (&c)[V]) const { ldv_s(b + 2 * 32 * V, a); ldv_s(b + 3 * 32 * V, c); }
-  __device__ __forceinline__ void w(T (&a)[V], T (&c)[V]) const { ldv_s(b + 4 * 32 * V, a); ldv_s(b + 5 * 32 * V, c); }
+  const T* b;  // this lane's slot: component i at b + i * 32 * V (packed: pair i/2 at b + (i/2) * 64 * V)
+  __device__ __forceinline__ void ld2(int i, T (&a)[V], T (&c)[V]) const {
+    if constexpr (ring_packed<T, V>()) {
+      const float4 t = *reinterpret_cast<const float4*>(b + i * 32 * V);
+      a[0] = t.x; a[1] = t.y; c[0] = t.z; c[1] = t.w;
+    } else {
+      ldv_s(b + i * 32 * V, a);
+      ldv_s(b + (i + 1) * 32 * V, c);
+    }
+  }
+  __device__ __forceinline__ void ex(T (&a)[V], T (&c)[V]) const { ld2(0, a, c); }
+  __device__ __forceinline__ void ey(T (&a)[V], T (&c)[V]) const { ld2(2, a, c); }
+  __device__ __forceinline__ void w(T (&a)[V], T (&c)[V]) const { ld2(4, a, c); }
 };
 
 // One Yee step on one row r of a warp's column strip (K1): Hz^{new} of row r from
@@ -376,6 +393,12 @@ __device__ __forceinline__ void record_probes(const SweepParams<T>& p, int r, co
 template <typename T, int V>
 __device__ __forceinline__ void ring_store(T* ring, int slot, const RowCoef<T, V>& cf) {  // ring: this lane's base
   T* b = ring + slot * (NCOEF * 32 * V);
+  if constexpr (ring_packed<T, V>()) {
+    *reinterpret_cast<float4*>(b) = make_float4(cf.cax[0], cf.cax[1], cf.cbx[0], cf.cbx[1]);
+    *reinterpret_cast<float4*>(b + 2 * 32 * V) = make_float4(cf.cay[0], cf.cay[1], cf.cby[0], cf.cby[1]);
+    *reinterpret_cast<float4*>(b + 4 * 32 * V) = make_float4(cf.wx[0], cf.wx[1], cf.wy[0], cf.wy[1]);
+    return;
+  }
   stv_s(b + 0 * 32 * V, cf.cax); stv_s(b + 1 * 32 * V, cf.cbx); stv_s(b + 2 * 32 * V, cf.cay);
   stv_s(b + 3 * 32 * V, cf.cby); stv_s(b + 4 * 32 * V, cf.wx); stv_s(b + 5 * 32 * V, cf.wy);
 }
@@ -399,9 +422,11 @@ struct StageOut {
 
 template <typename T, int V, int K>
 struct SweepCtx {
-  uint32_t c, P;  // this lane's first column (row-0 element offset) and the row pitch: every array
-                  // holds < 2^32 elements (fdtd_create), so element offsets stay 32-bit and each
-                  // address is one wide multiply-add on the array's base pointer
+  uint32_t c;       // this lane's first column
+  uint32_t cf, Pf;  // its element offset in a row of the field pool and that pool's row pitch
+  uint32_t cm, Pm;  // the same in the material pool: every pool holds < 2^32 elements
+                    // (fdtd_create), so offsets stay 32-bit and each address is one wide
+                    // multiply-add on the pool's base pointer (the pools' arrays sit TILE apart)
   T* ring;
   int lane, r0, r1, src_r, src_r1, src_k;  // source rows [src_r, src_r1) in this lane's column src_k
   bool out;
@@ -438,9 +463,14 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
     RowCoef<T, V>& cf = rc[T0 & (K - 1)];
     row_coef<T, V>(X.ma, X.ms, Y.ma, Y.ms, p.idx, p.idy, p.wxy, p.wh, cf);
 #else
+#if FDTD_EXP & 1
+    RowCoef<T, V>& cf = rc[0];
+    row_coef<T, V>(X.ma, X.ms, Y.ma, Y.ms, p.idx, p.idy, p.wxy, p.wh, cf);
+#else
     RowCoef<T, V> cf;
     row_coef<T, V>(X.ma, X.ms, Y.ma, Y.ms, p.idx, p.idy, p.wxy, p.wh, cf);
     if (K > 1) ring_store<T, V>(x.ring, j & (K - 1), cf);
+#endif
 #endif
     const T en = yee_any<T, V, ENERGY>(Y.ext, X.ext, X.ey, X.hz, A.h[0], CoefRegs<T, V>{cf}, p, x.g[0],
                                        CHK && j >= x.src_r && j < x.src_r1, x.src_k, B.h[0], B.x[0], B.y[0]);
@@ -449,21 +479,21 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
     if (CHK && own && x.out) record_probes<T, V>(p, j, B.h[0], x.slot[0], (int32_t)x.c);
   }
   if (j + 1 < je) {  // row j+1 into the buffer of row j-1 (consumed above)
-    const uint32_t o = (uint32_t)(j + 1) * x.P + x.c;
-    FCHK((int64_t)o + x.P + V <= p.alloc_elems && j + 1 >= 0);
-    ldv(p.ex0 + (o + x.P), Y.ext);
+    const uint32_t o = (uint32_t)(j + 1) * x.Pf + x.cf, om = (uint32_t)(j + 1) * x.Pm + x.cm;
+    FCHK((int64_t)o + x.Pf + 2 * TILE + V <= p.alloc_elems_f && (int64_t)om + TILE + V <= p.alloc_elems_m);
+    ldv(p.ex0 + (o + x.Pf), Y.ext);
     ldv(p.ey0 + o, Y.ey);
     ldv(p.hz0 + o, Y.hz);
-    ldv(p.mea + o, Y.ma);
-    ldv(p.msb + o, Y.ms);
+    ldv(p.mea + om, Y.ma);
+    ldv(p.msb + om, Y.ms);
   }
   if (PFD > 0 && j + 1 + PFD < je) {  // pull row j+1+PFD into L2 (no registers held)
-    const uint32_t o = (uint32_t)(j + 1 + PFD) * x.P + x.c;
-    prefetch_l2(p.ex0 + (o + x.P));
+    const uint32_t o = (uint32_t)(j + 1 + PFD) * x.Pf + x.cf, om = (uint32_t)(j + 1 + PFD) * x.Pm + x.cm;
+    prefetch_l2(p.ex0 + (o + x.Pf));
     prefetch_l2(p.ey0 + o);
     prefetch_l2(p.hz0 + o);
-    prefetch_l2(p.mea + o);
-    prefetch_l2(p.msb + o);
+    prefetch_l2(p.mea + om);
+    prefetch_l2(p.msb + om);
   }
   // ---- stage s: step n+s on row j-s, from stage s-1's outputs of rows j-s (A) and j-s+1 (B)
 #pragma unroll
@@ -471,6 +501,8 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
     const int r = j - s;
 #if FDTD_REG_RING
     const CoefRegs<T, V> cr{rc[(T0 - s) & (K - 1)]};
+#elif FDTD_EXP & 1  // diagnostic: no ring loads (wrong coefficients)
+    const CoefRegs<T, V> cr{rc[0]};
 #else
     const CoefRing<T, V> cr{x.ring + (r & (K - 1)) * (NCOEF * 32 * V)};
 #endif
@@ -482,9 +514,9 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
   }
   // stage K-1's outputs are the fields at step n+K of row j-K+1
   const int rs = j - (K - 1);
-  if (x.out && (!CHK || (rs >= x.r0 && rs < x.r1))) {
-    const uint32_t o = (uint32_t)rs * x.P + x.c;
-    FCHK(rs >= p.row0 && rs < p.row0 + p.rows && x.c + V <= x.P);  // stores stay in the owned rows
+  if (!(FDTD_EXP & 4) && x.out && (!CHK || (rs >= x.r0 && rs < x.r1))) {
+    const uint32_t o = (uint32_t)rs * x.Pf + x.cf;
+    FCHK(rs >= p.row0 && rs < p.row0 + p.rows && x.c + V <= p.pitch);  // stores stay in the owned rows
     stv(p.hz1 + o, B.h[K - 1]);
     stv(p.ex1 + o, B.x[K - 1]);
     stv(p.ey1 + o, B.y[K - 1]);
@@ -523,15 +555,19 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   x.lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int wpc = blockDim.x >> 5;
-  x.ring = reinterpret_cast<T*>(smem_raw) + (int64_t)warp * K * NCOEF * 32 * V + x.lane * V;
+  x.ring = reinterpret_cast<T*>(smem_raw) + (int64_t)warp * K * NCOEF * 32 * V + x.lane * V * (ring_packed<T, V>() ? 2 : 1);
   const int64_t colv = (int64_t)(blockIdx.x * wpc + warp) * NOUT + x.lane - HL;
   x.out = colv >= 0 && colv < (p.nx + V - 1) / V && x.lane >= HL && x.lane < 32 - HL;
   const int64_t c = (int64_t)colv * V;
   const int cy = p.chunk0 + blockIdx.y;  // row chunk
   x.r0 = p.row0 + cy * p.chunk;
   x.r1 = min(x.r0 + p.chunk, p.row0 + p.rows);
-  x.P = (uint32_t)p.pitch;
-  x.c = (uint32_t)c;  // c >= -V: row offsets (>= one pitch) keep every element offset non-negative
+  x.c = (uint32_t)c;
+  // pool offsets (c >= -V: row offsets >= one pitch keep every element offset non-negative)
+  x.Pf = (uint32_t)(p.pitch * p.naf);
+  x.Pm = (uint32_t)(p.pitch * p.nam);
+  x.cf = (uint32_t)pool_off(c, p.naf);
+  x.cm = (uint32_t)pool_off(c, p.nam);
   x.step = *p.step;
   const bool src_lane = p.src_row >= 0 && p.src_col >= c && p.src_col < c + V;
   x.src_k = src_lane ? (int)(p.src_col - c) : -1;
@@ -549,17 +585,18 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   const int jb = x.r0 - K, je = x.r1 + K - 1;  // stage-0 rows [jb, je); jb - 1 >= 0 (ROW0 = 2 KMAX)
   RowIn<T, V> R0, R1;  // rows jb-1 (only Ex of edge row jb and the materials are used) and jb
   {
-    const uint32_t o = (uint32_t)(jb - 1) * x.P + x.c;
-    FCHK(jb - 1 >= 0 && (int64_t)o + 2 * x.P + V <= p.alloc_elems);
-    ldv(p.ex0 + (o + x.P), R0.ext);
-    ldv(p.mea + o, R0.ma);
-    ldv(p.msb + o, R0.ms);
-    const uint32_t o1 = o + x.P;
-    ldv(p.ex0 + (o1 + x.P), R1.ext);
+    const uint32_t o = (uint32_t)(jb - 1) * x.Pf + x.cf, om = (uint32_t)(jb - 1) * x.Pm + x.cm;
+    FCHK(jb - 1 >= 0 && (int64_t)o + 2 * x.Pf + 2 * TILE + V <= p.alloc_elems_f &&
+         (int64_t)om + x.Pm + TILE + V <= p.alloc_elems_m);
+    ldv(p.ex0 + (o + x.Pf), R0.ext);
+    ldv(p.mea + om, R0.ma);
+    ldv(p.msb + om, R0.ms);
+    const uint32_t o1 = o + x.Pf, om1 = om + x.Pm;
+    ldv(p.ex0 + (o1 + x.Pf), R1.ext);
     ldv(p.ey0 + o1, R1.ey);
     ldv(p.hz0 + o1, R1.hz);
-    ldv(p.mea + o1, R1.ma);
-    ldv(p.msb + o1, R1.ms);
+    ldv(p.mea + om1, R1.ma);
+    ldv(p.msb + om1, R1.ms);
   }
   StageOut<T, V, K> O0, O1;
 #pragma unroll

@@ -34,6 +34,15 @@ namespace fdtd {
 // ROM interface edges are frozen for the whole pass; the fix-up kernel repairs the zone around
 // every instance.
 constexpr int KMAX = 4;  // deepest pass (ghost rows on each side of a slab)
+// HBM layout: the arrays of a pool are tile-interleaved along each row: a row of a
+// pool of `na` arrays is a sequence of column tiles, tile t holding columns [t TILE, (t+1) TILE)
+// of array 0, then of array 1, ...  Element (row, col) of array a sits at
+// row * na * pitch + pool_off(col, na) + a * TILE (na = 1: the plain row-major array).
+constexpr int TILE = 64;
+__host__ __device__ inline int64_t pool_off(int64_t col, int na) {
+  const int64_t t = col >= 0 ? col / TILE : -((-col + TILE - 1) / TILE);  // floor
+  return t * TILE * na + (col - t * TILE);
+}
 template <typename T>
 struct SweepParams {
   const T* ex0; const T* ey0; const T* hz0;  // fields at step n (E^n, H^{n-1/2})
@@ -41,7 +50,9 @@ struct SweepParams {
   // per cell: mea = eps0 eps_r / (2 dt) (< 0: hole / wall / dead), msb = sigma / 4 with the sign
   // bit set on fix-up zone cells (their energy is added by the fix-up kernel)
   const T* mea; const T* msb;
-  int64_t pitch;   // elements per row (all arrays)
+  int64_t pitch;   // columns per row (a multiple of TILE)
+  int naf, nam;    // arrays per pool: fields (ex, ey, hz of one buffer) and materials (mea, msb);
+                   // 1 = separate row-major arrays
   int64_t nx;      // grid columns (the sweep processes ceil(nx / W) lane vectors per row)
   int rows;        // owned cell rows: local rows row0 .. row0+rows-1
   int row0;        // local row of the first owned row (KMAX ghost rows below)
@@ -62,7 +73,7 @@ struct SweepParams {
   T* probe_ring; int64_t cap;
   T idx, idy;           // 1/dx, 1/dy
   T wxy, wh;            // dx dy, mu0 dx dy / dt (energy weights)
-  int64_t alloc_elems;  // elements of every field / material array incl. its tail (FDTD_CHECK bounds)
+  int64_t alloc_elems_f, alloc_elems_m;  // elements of a field / material pool incl. its tail (FDTD_CHECK)
 };
 
 // Fused per-model operators (column-major, in the model pool), with x = [E~; H~] (q1 + q2):
