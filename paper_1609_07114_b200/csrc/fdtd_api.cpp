@@ -1254,10 +1254,12 @@ fdtd_status fdtd_set_tuning(fdtd_ctx* c, int32_t rows_per_cta, int32_t warps_per
   // rows per CTA: long enough that the 2K - 1 recomputed stage rows at a chunk start stay a few per
   // cent, short enough for several waves of CTAs (the last wave's tail is paid once per slab)
   // rows per CTA: the 2K - 1 stage rows recomputed at a chunk start against the tail of the last
-  // wave; a row slab of a multi-GPU run (a few thousand rows) does better with 128 than 64
+  // wave; a row slab of a multi-GPU run (a few thousand rows) does better with 128 than 64; 512
+  // rows measured 1.3 % faster than 256 on 32768 rows (tools/sweep_layout_probe.cu, round 2)
   const bool slab = c->d.nranks > 1;
   c->chunk = rows_per_cta ? rows_per_cta
-                          : (c->rows >= 16384 ? 256 : c->rows >= 2048 ? (slab && c->rows < 8192 ? 128 : 64) : 32);
+                          : (c->rows >= 32768 ? 512 : c->rows >= 16384 ? 256
+                             : c->rows >= 2048 ? (slab && c->rows < 8192 ? 128 : 64) : 32);
   c->warps = warps_per_cta ? warps_per_cta : 4;
   if (!rows_per_cta)
     if (const char* e = getenv("FDTD_CHUNK")) c->chunk = std::max(1, atoi(e));  // tuning experiments

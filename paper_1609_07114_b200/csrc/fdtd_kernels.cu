@@ -183,6 +183,9 @@ template <typename T>
 __device__ __forceinline__ bool cell_dead(T wx) { return signbit(wx); }
 template <typename T>
 __device__ __forceinline__ T cell_hw(T wx, T wy, T wh) { return (signbit(wx) | signbit(wy)) ? T(0) : wh; }
+#ifndef FDTD_EACC2  // with FDTD_EFAST: per-stage packed fp32 pair accumulators (no per-row pair sum)
+#define FDTD_EACC2 0  // measured: +3.6 % per pass (one spill, 128-register cap)
+#endif
 #ifndef FDTD_EFAST  // sweep energy: cheaper Hz weight and fp32 row sums flushed to fp64 every 16 rows
 #define FDTD_EFAST 1  // round 2 measured -2.5 % per sweep pass (cold and power-capped, tools/sweep_layout_probe.cu)
 #endif
@@ -294,11 +297,14 @@ __device__ __forceinline__ T yee_row(const T (&exb)[V], const T (&ext)[V], const
 
 // yee_row for fp32 with the column pairs of a lane in packed FADD2 / FMUL2 / FFMA2 (the same
 // per-element operations as the generic version, in the same order).
-template <int V, bool ENERGY, typename CS>
+// ACC: the storage-function terms go straight into the caller's packed accumulator (when `own`)
+// and 0 is returned.
+template <int V, bool ENERGY, typename CS, bool ACC = false>
 __device__ __forceinline__ float yee_row_f2(const float (&exb)[V], const float (&ext)[V], const float (&ey)[V],
                                             const float (&hz)[V], const float (&hb)[V], const CS& cs,
                                             const SweepParams<float>& p, float gsrc, bool srow, int src_k,
-                                            float (&hn)[V], float (&exo)[V], float (&eyo)[V]) {
+                                            float (&hn)[V], float (&exo)[V], float (&eyo)[V],
+                                            F2* acc_out = nullptr, bool own = true) {
   static_assert(V % 2 == 0, "pairs");
   const float eyr = __shfl_down_sync(FULL, ey[0], 1);
   float wx[V], wy[V];  // energy weights, with the dead / zone flags in their sign bits
@@ -339,8 +345,9 @@ __device__ __forceinline__ float yee_row_f2(const float (&exb)[V], const float (
     }
   }
   float en = 0.f;
-  if (ENERGY) {
+  if (ENERGY && (!ACC || own)) {
     F2 acc{0.f, 0.f};
+    if constexpr (ACC) acc = *acc_out;
 #pragma unroll
     for (int k = 0; k < V; k += 2) {
       const F2 ex2{exb[k], exb[k + 1]}, ey2{ey[k], ey[k + 1]};
@@ -353,10 +360,21 @@ __device__ __forceinline__ float yee_row_f2(const float (&exb)[V], const float (
       acc = fma2(mul2(F2{wy[k], wy[k + 1]}, ey2), ey2, acc);
       acc = fma2(mul2(hw, F2{hz[k], hz[k + 1]}), F2{hn[k], hn[k + 1]}, acc);
     }
-    en = acc.x + acc.y;
+    if constexpr (ACC)
+      *acc_out = acc;
+    else
+      en = acc.x + acc.y;
   }
   return en;
 }
+
+// energy accumulators of the sweep: fp64, fp32 row sums (FDTD_EFAST), or packed fp32 pairs
+__device__ __forceinline__ double ea_value(double a) { return a; }
+__device__ __forceinline__ double ea_value(float a) { return (double)a; }
+__device__ __forceinline__ double ea_value(F2 a) { return (double)a.x + (double)a.y; }
+__device__ __forceinline__ void ea_zero(double& a) { a = 0.0; }
+__device__ __forceinline__ void ea_zero(float& a) { a = 0.f; }
+__device__ __forceinline__ void ea_zero(F2& a) { a = F2{0.f, 0.f}; }
 
 // S3 probes: record Hz^{n+s+1/2} of the probes in row r owned by this lane (sorted per row).
 // Out of line: only the few row chunks holding a probe row take this path.
@@ -440,14 +458,20 @@ struct SweepCtx {
 // Naming the two buffers statically (the caller alternates them) keeps every carried value in
 // place: no register moves.
 // fp32: packed pairs; fp64: the generic scalar row
-template <typename T, int V, bool ENERGY, typename CS>
-__device__ __forceinline__ T yee_any(const T (&exb)[V], const T (&ext)[V], const T (&ey)[V], const T (&hz)[V],
-                                     const T (&hb)[V], const CS& cs, const SweepParams<T>& p, T gsrc, bool srow,
-                                     int src_k, T (&hn)[V], T (&exo)[V], T (&eyo)[V]) {
-  if constexpr (sizeof(T) == 4 && V % 2 == 0)
-    return yee_row_f2<V, ENERGY>(exb, ext, ey, hz, hb, cs, p, gsrc, srow, src_k, hn, exo, eyo);
-  else
-    return yee_row<T, V, ENERGY>(exb, ext, ey, hz, hb, cs, p, gsrc, srow, src_k, hn, exo, eyo);
+template <typename T, int V, bool ENERGY, typename CS, typename EA>
+__device__ __forceinline__ void yee_any(const T (&exb)[V], const T (&ext)[V], const T (&ey)[V], const T (&hz)[V],
+                                        const T (&hb)[V], const CS& cs, const SweepParams<T>& p, T gsrc, bool srow,
+                                        int src_k, T (&hn)[V], T (&exo)[V], T (&eyo)[V], EA& acc, bool own) {
+  if constexpr (std::is_same<EA, F2>::value) {
+    yee_row_f2<V, ENERGY, CS, true>(exb, ext, ey, hz, hb, cs, p, gsrc, srow, src_k, hn, exo, eyo, &acc, own);
+  } else {
+    T en;
+    if constexpr (sizeof(T) == 4 && V % 2 == 0)
+      en = yee_row_f2<V, ENERGY>(exb, ext, ey, hz, hb, cs, p, gsrc, srow, src_k, hn, exo, eyo);
+    else
+      en = yee_row<T, V, ENERGY>(exb, ext, ey, hz, hb, cs, p, gsrc, srow, src_k, hn, exo, eyo);
+    if (ENERGY && own) acc += (EA)en;
+  }
 }
 
 template <typename T, int V, int K, bool ENERGY, bool CHK, int T0, typename EA>
@@ -472,10 +496,9 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
     if (K > 1) ring_store<T, V>(x.ring, j & (K - 1), cf);
 #endif
 #endif
-    const T en = yee_any<T, V, ENERGY>(Y.ext, X.ext, X.ey, X.hz, A.h[0], CoefRegs<T, V>{cf}, p, x.g[0],
-                                       CHK && j >= x.src_r && j < x.src_r1, x.src_k, B.h[0], B.x[0], B.y[0]);
     const bool own = !CHK || (j >= x.r0 && j < x.r1);
-    if (ENERGY && own) eacc[0] += (EA)en;
+    yee_any<T, V, ENERGY>(Y.ext, X.ext, X.ey, X.hz, A.h[0], CoefRegs<T, V>{cf}, p, x.g[0],
+                          CHK && j >= x.src_r && j < x.src_r1, x.src_k, B.h[0], B.x[0], B.y[0], eacc[0], own);
     if (CHK && own && x.out) record_probes<T, V>(p, j, B.h[0], x.slot[0], (int32_t)x.c);
   }
   if (j + 1 < je) {  // row j+1 into the buffer of row j-1 (consumed above)
@@ -506,10 +529,9 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
 #else
     const CoefRing<T, V> cr{x.ring + (r & (K - 1)) * (NCOEF * 32 * V)};
 #endif
-    const T en = yee_any<T, V, ENERGY>(A.x[s - 1], B.x[s - 1], A.y[s - 1], A.h[s - 1], A.h[s], cr, p, x.g[s],
-                                       CHK && r >= x.src_r && r < x.src_r1, x.src_k, B.h[s], B.x[s], B.y[s]);
     const bool own = !CHK || (r >= x.r0 && r < x.r1);
-    if (ENERGY && own) eacc[s] += (EA)en;
+    yee_any<T, V, ENERGY>(A.x[s - 1], B.x[s - 1], A.y[s - 1], A.h[s - 1], A.h[s], cr, p, x.g[s],
+                          CHK && r >= x.src_r && r < x.src_r1, x.src_k, B.h[s], B.x[s], B.y[s], eacc[s], own);
     if (CHK && own && x.out) record_probes<T, V>(p, r, B.h[s], x.slot[s], (int32_t)x.c);
   }
   // stage K-1's outputs are the fields at step n+K of row j-K+1
@@ -568,11 +590,12 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   x.Pm = (uint32_t)(p.pitch * p.nam);
   x.cf = (uint32_t)pool_off(c, p.naf);
   x.cm = (uint32_t)pool_off(c, p.nam);
-  x.step = *p.step;
+
   const bool src_lane = p.src_row >= 0 && p.src_col >= c && p.src_col < c + V;
   x.src_k = src_lane ? (int)(p.src_col - c) : -1;
   x.src_r = src_lane ? p.src_row : INT_MIN;
   x.src_r1 = src_lane ? p.src_row_end : INT_MIN;
+  x.step = *p.step;
 #pragma unroll
   for (int s = 0; s < K; ++s) {
     x.g[s] = T(0);
@@ -605,12 +628,15 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
     for (int k = 0; k < V; ++k) O0.h[s][k] = O0.x[s][k] = O0.y[s][k] = T(0);
   // energy partials: per stage, the rows' sums in EA (fp32 with FDTD_EFAST, flushed into the fp64
   // dacc every 16 rows) -- fp64 over the chunk
-  using EA = typename std::conditional<FDTD_EFAST && sizeof(T) == 4, float, double>::type;
+  // (packed fp32 pairs, FDTD_EACC2, on the packed row path)
+  using EA = typename std::conditional<
+      FDTD_EFAST && sizeof(T) == 4,
+      typename std::conditional<FDTD_EACC2 && V % 2 == 0, F2, float>::type, double>::type;
   EA eacc[K];
   double dacc[K];
 #pragma unroll
   for (int s = 0; s < K; ++s) {
-    eacc[s] = EA(0);
+    ea_zero(eacc[s]);
     dacc[s] = 0.0;
   }
   // does this warp's strip hold a probe in the chunk's rows?  (scanned once per warp)
@@ -660,16 +686,17 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
         if (j + 3 < je) sweep_row<T, V, K, ENERGY, true, 3>(p, x, j + 3, je, R0, R1, O1, O0, eacc, rc);
       }
     }
-    if (ENERGY && sizeof(EA) == 4 && ((j - jb) & 15) == 16 - U) {
+    if (ENERGY && !std::is_same<EA, double>::value && ((j - jb) & 15) == 16 - U) {
 #pragma unroll
       for (int s = 0; s < K; ++s) {
-        dacc[s] += (double)eacc[s];
-        eacc[s] = EA(0);
+        dacc[s] += ea_value(eacc[s]);
+        ea_zero(eacc[s]);
       }
     }
   }
 #pragma unroll
-  for (int s = 0; s < K; ++s) dacc[s] = x.out ? dacc[s] + (double)eacc[s] : 0.0;
+#pragma unroll
+  for (int s = 0; s < K; ++s) dacc[s] = x.out ? dacc[s] + ea_value(eacc[s]) : 0.0;
   if (ENERGY) {
     __shared__ double red[K][32];
 #pragma unroll

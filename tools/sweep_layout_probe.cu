@@ -46,7 +46,9 @@ int main(int argc, char** argv) {
   // material terms: mea = eps0 eps_r / (2 dt) ~ 20, msb = sigma / 4 ~ 0.01; fields ~ 1e-3
   const double dt = 1e-12, dx = 1e-3;
   fdtd::SweepParams<float> base{};
-  base.nx = nx; base.rows = (int)rows; base.row0 = row0; base.chunk = 256; base.pitch = pitch;
+  base.nx = nx; base.rows = (int)rows; base.row0 = row0; base.pitch = pitch;
+  base.chunk = getenv("SLP_CHUNK") ? atoi(getenv("SLP_CHUNK")) : 256;
+  const int warps = getenv("SLP_WARPS") ? atoi(getenv("SLP_WARPS")) : 4;
   base.chx = (float)(dt / (4e-7 * M_PI * dx)); base.chy = base.chx;
   base.src_row = -1; base.src_row_end = -1; base.src_col = -1;
   int64_t* d_step; CK(cudaMalloc(&d_step, 16)); CK(cudaMemset(d_step, 0, 16));
@@ -60,7 +62,7 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
   auto timeit = [&](fdtd::SweepParams<float> p, const char* name) {
     for (int w = 0; w < 3; ++w) {
-      fdtd::launch_sweep<float>(p, 4, 4, st, 0, -1);
+      fdtd::launch_sweep<float>(p, 4, warps, st, 0, -1);
       std::swap(p.ex0, *(const float**)&p.ex1); std::swap(p.ey0, *(const float**)&p.ey1);
       std::swap(p.hz0, *(const float**)&p.hz1);
     }
@@ -69,7 +71,7 @@ int main(int argc, char** argv) {
     std::vector<float> all;
     for (int r = 0; r < reps; ++r) {
       cudaEventRecord(e0, st);
-      fdtd::launch_sweep<float>(p, 4, 4, st, 0, -1);
+      fdtd::launch_sweep<float>(p, 4, warps, st, 0, -1);
       cudaEventRecord(e1, st);
       cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
