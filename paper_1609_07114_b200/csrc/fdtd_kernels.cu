@@ -42,7 +42,7 @@ __device__ __forceinline__ void ldv(const float* p, float (&v)[2]) {
 __device__ __forceinline__ void stv(float* p, const float (&v)[2]) {
   *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
 }
-__device__ __forceinline__ void ldv_s(const float* p, float (&v)[2]) {
+[[maybe_unused]] __device__ __forceinline__ void ldv_s(const float* p, float (&v)[2]) {
   const float2 x = *reinterpret_cast<const float2*>(p);
   v[0] = x.x; v[1] = x.y;
 }
@@ -371,10 +371,10 @@ __device__ __forceinline__ float yee_row_f2(const float (&exb)[V], const float (
 // energy accumulators of the sweep: fp64, fp32 row sums (FDTD_EFAST), or packed fp32 pairs
 __device__ __forceinline__ double ea_value(double a) { return a; }
 __device__ __forceinline__ double ea_value(float a) { return (double)a; }
-__device__ __forceinline__ double ea_value(F2 a) { return (double)a.x + (double)a.y; }
+[[maybe_unused]] __device__ __forceinline__ double ea_value(F2 a) { return (double)a.x + (double)a.y; }
 __device__ __forceinline__ void ea_zero(double& a) { a = 0.0; }
 __device__ __forceinline__ void ea_zero(float& a) { a = 0.f; }
-__device__ __forceinline__ void ea_zero(F2& a) { a = F2{0.f, 0.f}; }
+[[maybe_unused]] __device__ __forceinline__ void ea_zero(F2& a) { a = F2{0.f, 0.f}; }
 
 // S3 probes: record Hz^{n+s+1/2} of the probes in row r owned by this lane (sorted per row).
 // Out of line: only the few row chunks holding a probe row take this path.
@@ -773,6 +773,9 @@ __device__ __forceinline__ int& ph_counter() {
 #ifndef FDTD_M2PRE  // M2's operator tiles loaded into registers before the Schur phase
 #define FDTD_M2PRE 0  // measured: M2 4 k instead of 6 k cycles, but M1 loses its registers (16 k instead of 10 k)
 #endif
+#ifndef FDTD_FUSE  // fix-up: five barrier phases per step (M1 beside the H half-step, E beside the gather)
+#define FDTD_FUSE 1
+#endif
 #ifndef FDTD_SKPF  // prefetch the batch's Schur inverses into L2 at the batch start
 #define FDTD_SKPF 1
 #endif
@@ -987,6 +990,94 @@ __device__ void rom_step(const PostParams<T>& p, const RomModelDev& m, const int
   }
   __syncthreads();
   PHASE();
+}
+
+// The same ROM step split into the phases the fused fix-up step schedules beside its region work
+// (FDTD_FUSE, K3): rom_m1 (M1 GEMM; needs x~ only), rom_t (energy + t; needs the gathered y
+// and h), rom_schur (U = S_k t), rom_m2 (M2 GEMM, the base added in its epilogue, which also hands
+// each y^{n+1} to scat(port, slot, y) -- the scatter into the region's interface edge -- and H~
+// copied).  The caller puts a barrier between consecutive phases.
+template <typename T, bool ENERGY>
+__device__ __forceinline__ void rom_m1(const PostParams<T>& p, const RomModelDev& m, int B, int64_t S, T* sv) {
+  const int nY = m.nY, q1 = m.q1, q2 = m.q2, nx = q1 + q2, m1 = q2 + q1 + nY;
+  RomVec<T> v(sv, S);
+  T* so = v.so;
+  dmma_gemm(p.mpool + m.off_M1t, ENERGY ? m.mt1 : (m1 + 7) / 8, m.kt1, ENERGY ? m1 + nx : m1, nx, v.sx, B,
+            [&](int r, int c, double x) { so[r * B + c] = (T)x; });
+}
+template <typename T, bool ENERGY>
+__device__ __forceinline__ void rom_t(const RomModelDev& m, const int32_t* mem, int nb, int B, int64_t S, T* sv,
+                                      double* ep) {
+  const int nY = m.nY, q1 = m.q1, q2 = m.q2, nx = q1 + q2, m1 = q2 + q1 + nY;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  RomVec<T> v(sv, S);
+  const RomConst<T> rc(sv, S, (int64_t)nY * B);
+  if (ENERGY) {  // x~^T R~ x~ + sum D_l D_l' eps/dt y^2 (storage function, R17); one warp per instance
+    const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+    for (int b = w; b < nb; b += nw) {
+      double acc = 0.0;
+      for (int i = lane; i < nY; i += 32) {
+        const double y = (double)v.sy[i * B + b];
+        acc += rc.eh[i * B + b] * y * y;
+      }
+      for (int i = lane; i < nx; i += 32) acc += (double)v.sx[i * B + b] * (double)v.so[(m1 + i) * B + b];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
+      if (lane == 0) ep[mem[b]] = acc;
+    }
+  }
+  for (int it = tid; it < nY * nb; it += nt) {  // t = (a_y/c_y) y + (D_l G/c_y) h - L~^T E*
+    const int i = it % nY, b = it / nY;
+    const int k = i * B + b;
+    v.st[k] = v.so[(q2 + q1 + i) * B + b] + fma_rn(rc.cyg[k], v.sh[k], mul_rn(rc.cya[k], v.sy[k]));
+  }
+}
+template <typename T>
+__device__ __forceinline__ void rom_schur(const PostParams<T>& p, const RomModelDev& m, const int32_t* mem, int nb,
+                                          int B, int64_t S, T* sv) {
+  const int nY = m.nY;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  RomVec<T> v(sv, S);
+  for (int it = tid; it < nY * nb; it += nt) {  // U = S_k t (as in rom_step)
+    const int i = it % nY, b = it / nY;
+    const T* Sk = p.Sk + p.Sk_off[mem[b]] + i;
+    T a[4] = {T(0), T(0), T(0), T(0)};
+    int c = 0;
+    for (; c + 15 < nY; c += 16) {
+      T sk[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) sk[u] = __ldg(Sk + (int64_t)(c + u) * nY);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) a[u & 3] = fma_rn(sk[u], v.st[(c + u) * B + b], a[u & 3]);
+    }
+    for (; c + 3 < nY; c += 4)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = fma_rn(__ldg(Sk + (int64_t)(c + u) * nY), v.st[(c + u) * B + b], a[u]);
+    for (; c < nY; ++c) a[0] = fma_rn(__ldg(Sk + (int64_t)c * nY), v.st[c * B + b], a[0]);
+    v.sU[i * B + b] = (a[0] + a[1]) + (a[2] + a[3]);
+  }
+}
+template <typename T, typename Scat>
+__device__ __forceinline__ void rom_m2(const PostParams<T>& p, const RomModelDev& m, int nb, int B, int64_t S, T* sv,
+                                       Scat scat) {
+  const int nY = m.nY, q1 = m.q1, q2 = m.q2, m2 = q1 + nY;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  RomVec<T> v(sv, S);
+  T* sx = v.sx;
+  T* sy = v.sy;
+  const T* so = v.so;
+  const bool lit = m.literal != 0;
+  auto epi = [&](int r, int c, double x) {
+    if (r < q1) {
+      sx[r * B + c] = (T)((double)so[(q2 + r) * B + c] + x);
+    } else {
+      const T y = (T)((lit ? 0.0 : -(double)so[(q2 + r) * B + c]) + x);
+      sy[(r - q1) * B + c] = y;
+      if (c < nb) scat(r - q1, c, y);
+    }
+  };
+  dmma_gemm(p.mpool + m.off_M2t, m.mt2, m.kt2, m2, nY, v.sU, B, epi);
+  for (int64_t k = tid; k < (int64_t)q2 * B; k += nt) sx[(int64_t)q1 * B + k] = so[k];
 }
 
 // ---- the large-model path (one instance at a time on the whole GPU; fdtd_api.cpp "big" models):
@@ -1391,10 +1482,10 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   // Values go wrong from the region's border inwards one cell per step, so step s only updates the
   // cone that is still exact: cells [s, Wr - s) x [s, Hr - s) (edges one further in across their
   // normal); the zone, the ROM's gather cells and the write-back all lie inside the last cone.
-#pragma unroll 1
-  for (int s = 0; s < K; ++s) {
+  // the step's region pieces (K3)
+  // H half-step (+ source, + the zone cells' storage-function terms of W^{n+s}) on the cone of step s
+  auto h_half = [&](int s) {
     const int cw = Wr - 2 * s, ch = Hr - 2 * s;
-    // ---- H half-step (+ source, + the zone cells' storage-function terms of W^{n+s})
     for (Flat f(tid, nt, s, cw, s, ch); f.b < nreg; f.next()) {
       const int u = f.u, v = f.v, r = f.b;
       const T* ex = EX(r);
@@ -1419,9 +1510,10 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       }
       hz[t] = h;
     }
-    __syncthreads();
-    PHASE();
-    // ---- zone probes; S4 gather of y^{n+s} (interface edges) and h = Hz^{n+s+1/2} (outside cells)
+  };
+  // zone probes; S4 gather of y^{n+s} (interface edges) and h = Hz^{n+s+1/2} (outside cells); the
+  // regions' zone energies (fixed order, one warp per region)
+  auto gather = [&](int s) {
     for (int b = 0; b < nr; ++b) {
       const int z0 = p.zp_off[mem[b]], z1 = p.zp_off[mem[b] + 1];
       if (z0 == z1) continue;
@@ -1453,7 +1545,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       sy[i * B + b] = y;
       sh[i * B + b] = h;
     }
-    if (ENERGY) {  // zone energy per region, fixed order (one warp per region)
+    if (ENERGY) {
       const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
       for (int r = w; r < nreg; r += nw) {
         const T* ze = ZE(r);
@@ -1464,28 +1556,21 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
         if (lane == 0) bs.zsum[r] = acc;
       }
     }
-    __syncthreads();
-    PHASE();
-    // ---- S5: ROM step n+s -> y^{n+s+1}, x~^{n+s+1}; ROM energy of W^{n+s} (+ the zone energy of
-    // the member's region on its first member)
-    double* ep = p.rom_partials + (int64_t)s * p.n_inst;
-    if constexpr (BIG) rom_step_big<T, ENERGY>(p, m, mem, s, sv, S, ep, part);
-    else rom_step<T, ENERGY>(p, m, mem, nb, B, S, sv, ep);
-    if (ENERGY && tid < nr && (kind == 0 || tid == 0)) ep[mem[tid]] += bs.zsum[bs.rr[tid]];
-    // ---- S6: y^{n+s+1} into the regions' interface edges, and in the same phase the E half-step
-    // on the regions' live edges (dead edges -- interface, PEC, hole -- keep their value: they are
-    // skipped, so the scatter and the update never touch the same edge)
-    for (int it = tid; it < nY * nr; it += nt) {
-      const int i = it % nY, b = it / nY;
-      const int r = bs.rr[b], U0 = bs.bu[b], V0 = bs.bv[b];
-      const T y = sy[i * B + b];
-      T* ex = EX(r);
-      T* ey = EY(r);
-      if (i < bx) ex[V0 * Wr + U0 + i] = y;
-      else if (i < 2 * bx) ex[(V0 + by) * Wr + U0 + i - bx] = y;
-      else if (i < 2 * bx + by) ey[(V0 + i - 2 * bx) * W1 + U0] = y;
-      else ey[(V0 + i - 2 * bx - by) * W1 + U0 + bx] = y;
-    }
+  };
+  // S6: y into member b's interface edge i
+  auto scatter1 = [&](int i, int b, T y) {
+    const int r = bs.rr[b], U0 = bs.bu[b], V0 = bs.bv[b];
+    T* ex = EX(r);
+    T* ey = EY(r);
+    if (i < bx) ex[V0 * Wr + U0 + i] = y;
+    else if (i < 2 * bx) ex[(V0 + by) * Wr + U0 + i - bx] = y;
+    else if (i < 2 * bx + by) ey[(V0 + i - 2 * bx) * W1 + U0] = y;
+    else ey[(V0 + i - 2 * bx - by) * W1 + U0 + bx] = y;
+  };
+  // E half-step on the regions' live edges (dead edges -- interface, PEC, hole -- keep their value:
+  // they are skipped, so the scatter and the update never touch the same edge)
+  auto e_half = [&](int s) {
+    const int cw = Wr - 2 * s, ch = Hr - 2 * s;
     for (Flat f(tid, nt, s, cw, s + 1, ch - 1); f.b < nreg; f.next()) {  // Ex edge rows s+1 .. Hr-s-1,
       const int t = f.v * Wr + f.u;                                         // columns s .. Wr-s-1
       const T* ma = MA(f.b);
@@ -1508,6 +1593,52 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       edge_coef(ma[c - 1], ms[c - 1], ma[c], ms[c], -p.idx, ca, cb, a, l);
       if (l) ey[f.v * W1 + f.u] = eupd(ey[f.v * W1 + f.u], ca, cb, hz[c] - hz[c - 1]);
     }
+  };
+#pragma unroll 1
+  for (int s = 0; s < K; ++s) {
+    double* ep = p.rom_partials + (int64_t)s * p.n_inst;
+    if constexpr (FDTD_FUSE && !BIG) {
+      // five barrier phases per step instead of seven: the M1 GEMM needs x~ only, so it shares the
+      // H half-step's phase; the live-edge E half-step needs neither y nor the ROM, so it shares the
+      // gather's; the scatter rides in the M2 epilogue
+      h_half(s);
+      rom_m1<T, ENERGY>(p, m, B, S, sv);
+      __syncthreads();
+      PHASE();
+      gather(s);
+      e_half(s);
+      __syncthreads();
+      PHASE();
+      rom_t<T, ENERGY>(m, mem, nb, B, S, sv, ep);
+      __syncthreads();
+      PHASE();
+      // (after the barrier: rom_t's warps have written ep)
+      if (ENERGY && tid < nr && (kind == 0 || tid == 0)) ep[mem[tid]] += bs.zsum[bs.rr[tid]];
+      rom_schur<T>(p, m, mem, nb, B, S, sv);
+      __syncthreads();
+      PHASE();
+      rom_m2<T>(p, m, nb, B, S, sv, scatter1);
+      __syncthreads();
+      PHASE();
+      continue;
+    }
+    h_half(s);
+    __syncthreads();
+    PHASE();
+    gather(s);
+    __syncthreads();
+    PHASE();
+    // ---- S5: ROM step n+s -> y^{n+s+1}, x~^{n+s+1}; ROM energy of W^{n+s} (+ the zone energy of
+    // the member's region on its first member)
+    if constexpr (BIG) rom_step_big<T, ENERGY>(p, m, mem, s, sv, S, ep, part);
+    else rom_step<T, ENERGY>(p, m, mem, nb, B, S, sv, ep);
+    if (ENERGY && tid < nr && (kind == 0 || tid == 0)) ep[mem[tid]] += bs.zsum[bs.rr[tid]];
+    // ---- S6: y^{n+s+1} into the regions' interface edges, and in the same phase the E half-step
+    for (int it = tid; it < nY * nr; it += nt) {
+      const int i = it % nY, b = it / nY;
+      scatter1(i, b, sy[i * B + b]);
+    }
+    e_half(s);
     __syncthreads();
     PHASE();
   }

@@ -30,7 +30,7 @@ __global__ void fill(float* a, size_t n, float base, float amp, uint32_t seed) {
 }
 
 int main(int argc, char** argv) {
-  const int64_t nx = 32768, rows = 32768, pitch = nx + 64;
+  const int64_t nx = getenv("SLP_N") ? atoi(getenv("SLP_N")) : 32768, rows = nx, pitch = nx + 64;
   const int row0 = 8, nrows_alloc = (int)rows + row0 + 4;
   const int reps = argc > 1 ? atoi(argv[1]) : 10;
   const size_t tail = 32 * 1024 / 4;
@@ -54,7 +54,7 @@ int main(int argc, char** argv) {
   int64_t* d_step; CK(cudaMalloc(&d_step, 16)); CK(cudaMemset(d_step, 0, 16));
   base.step = d_step; base.src_meta = d_step;
   double* part; const int64_t npart = 4 * 256 * 1024; CK(cudaMalloc(&part, npart * 8 * 4));
-  base.partials = part; base.pstride = npart;
+  base.partials = getenv("SLP_NOENERGY") ? nullptr : part; base.pstride = npart;
   base.cap = 1;
   base.idx = (float)(1 / dx); base.idy = base.idx; base.wxy = (float)(dx * dx);
   base.wh = (float)(4e-7 * M_PI * dx * dx / dt);
@@ -82,8 +82,8 @@ int main(int argc, char** argv) {
     const cudaError_t e = cudaGetLastError();
     std::vector<float> srt = all;
     std::sort(srt.begin(), srt.end());
-    printf("%-34s best %.3f ms  median %.3f  mean %.3f ms per 4-step pass  (%s)\n", name, best, srt[reps / 2],
-           sum / reps, cudaGetErrorString(e));
+    printf("%-34s best %.3f ms  median %.3f  mean %.3f ms per 4-step pass  (%s)  %.1f G cell-steps/s\n", name, best,
+           srt[reps / 2], sum / reps, cudaGetErrorString(e), 4.0 * nx * rows / (best * 1e-3) / 1e9);
     if (getenv("SLP_ALL")) {
       for (float v : all) printf(" %.2f", v);
       printf("\n");
