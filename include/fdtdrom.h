@@ -72,6 +72,8 @@ typedef enum {
 #define FDTD_NO_GRAPH 0x8u            /* never capture CUDA graphs in fdtd_step        */
 #define FDTD_LOCAL_GROUP 0x10u        /* rank of an in-process slab group (no NCCL; see
                                          fdtd_step_group)                               */
+#define FDTD_NO_WHOLE 0x20u           /* never use the whole-grid path (K3c): small
+                                         grids then also take the sweep + fix-up passes */
 
 typedef struct {
   int64_t nx, ny;          /* global coarse cells                                         */
@@ -223,6 +225,10 @@ typedef struct {
   int32_t fixup_clusters;      /* fix-up regions shared by several instances closer than the pass
                                   depth allows                        */
   int32_t big_instances;       /* instances on the cooperative large-model path                */
+  int32_t whole_grid;          /* 1: fdtd_step runs the whole grid and its ROM instances in one
+                                  CTA, one launch per call (single rank, no CPML, one model of
+                                  fewer than 512 states, <= 64 instances, the grid and the batch
+                                  in one CTA's shared memory; K3c)                   */
 } fdtd_info;
 fdtd_status fdtd_get_info(const fdtd_ctx *c, fdtd_info *out);
 

@@ -146,6 +146,15 @@ struct fdtd_ctx {
   std::vector<int32_t> zone_marked;  // the zone boxes whose cells carry the msb marks (kz_marked deep)
   int32_t* d_zone_marked = nullptr;
   int n_clusters = 0;
+  // whole-grid mode (K3c): the grid and every instance in one CTA, one launch per
+  // fdtd_step call; its batch table (one kind-1 batch around the whole grid) and probe list
+  bool whole = false;
+  size_t whole_smem = 0;
+  int32_t* d_wb_tab = nullptr;
+  int32_t* d_wb_inst = nullptr;
+  int32_t* d_wb_rect = nullptr;
+  int32_t* d_wprobe = nullptr;
+  int n_wprobe = 0;
   int post_grid = 1;
   int n_batch_reg = 0;           // regular fix-up batches; the rest are large-model instances
   void* d_big = nullptr;         // bigrom_kernel scratch
@@ -330,6 +339,13 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
   p.smem_bytes = c->post_smem;
   p.flag = c->d_flag;
   p.alloc_elems = alloc_elems(c); p.rows = c->rows; p.n_probe = c->n_probe;
+  p.energy_ring = c->d_energy_ring;
+  p.wprobe = c->d_wprobe; p.n_wprobe = c->n_wprobe;
+  if (c->whole) {  // the whole-grid batch
+    p.batch_tab = c->d_wb_tab; p.batch_inst = c->d_wb_inst; p.batch_rect = c->d_wb_rect;
+    p.n_batch = p.n_batch_reg = 1;
+    p.smem_bytes = c->whole_smem;
+  }
   return p;
 }
 
@@ -1051,6 +1067,41 @@ fdtd_status apply_passes(fdtd_ctx* c, int k) {
     if ((st = upload(c, &c->d_zp_off, c->zp_off)) != FDTD_OK) return st;
     if ((st = upload(c, &c->d_zp, c->zp)) != FDTD_OK) return st;
   }
+  // whole-grid mode: one rank, no CPML, at least one instance, every instance of one model that is
+  // not on the large-model path, at most MAX_CLUSTER of them, and the grid + one ring of wall cells
+  // with the batch's ROM vectors inside the fix-up's shared memory
+  c->whole = false;
+  {
+    const int n = (int)c->inst_model.size();
+    const char* wenv = getenv("FDTD_WHOLE");
+    bool ok = c->d.nranks == 1 && !(c->d.flags & (FDTD_LOCAL_GROUP | FDTD_NO_WHOLE)) && c->pml_w == 0 && n >= 1 &&
+              n <= MAX_CLUSTER && !(wenv && atoi(wenv) == 0) && c->d.nx <= 4096 && c->d.ny <= 4096;
+    for (int i = 0; ok && i < n; ++i) ok = c->inst_model[i] == c->inst_model[0];
+    if (ok) {
+      const ModelHost& m = c->models[c->inst_model[0]];
+      const char* benv = getenv("FDTD_BIG_Q");
+      const int big_q = benv ? atoi(benv) : 512;
+      ok = !(big_q > 0 && m.q1 + m.q2 >= big_q);
+      const int rs = (fdtd::region_elems((int)c->d.nx, (int)c->d.ny, 1) + 3) / 4 * 4;
+      const size_t smem = batch_smem(c, m, n, 1, rs);
+      if (ok && smem <= FIX_BUDGET) {
+        std::vector<int32_t> tab = {c->inst_model[0], 0, n, n, rs, 1}, inst(n), rect = {0, 0, (int32_t)c->d.nx,
+                                                                                         (int32_t)c->d.ny};
+        for (int i = 0; i < n; ++i) inst[i] = i;
+        std::vector<int32_t> wp;
+        for (int pr = 0; pr < c->n_probe; ++pr)
+          wp.insert(wp.end(), {(int32_t)c->probe_ij[2 * pr], (int32_t)c->probe_ij[2 * pr + 1], pr});
+        c->n_wprobe = c->n_probe;
+        if (wp.empty()) wp.assign(3, 0);
+        if ((st = upload(c, &c->d_wb_tab, tab)) != FDTD_OK) return st;
+        if ((st = upload(c, &c->d_wb_inst, inst)) != FDTD_OK) return st;
+        if ((st = upload(c, &c->d_wb_rect, rect)) != FDTD_OK) return st;
+        if ((st = upload(c, &c->d_wprobe, wp)) != FDTD_OK) return st;
+        c->whole_smem = smem;
+        c->whole = true;
+      }
+    }
+  }
   CK(cudaStreamSynchronize(c->stream));
   c->kz_dirty = false;
   drop_graph(c);
@@ -1659,6 +1710,15 @@ fdtd_status fdtd_step(fdtd_ctx* c, int64_t nsteps) {
                          !c->graph_broken;
   fdtd_status st = configure_passes(c);
   if (st != FDTD_OK) return st;
+  if (c->whole && nsteps > 0) {  // K3c: all the steps in one launch (buffer cur -> 1 - cur)
+    if (c->prec == 64) fdtd::launch_wholegrid<double>(post_params<double>(c, c->cur), nsteps, c->energy_on, c->stream);
+    else fdtd::launch_wholegrid<float>(post_params<float>(c, c->cur), nsteps, c->energy_on, c->stream);
+    c->launches += 1;
+    c->steps += nsteps;
+    c->cur ^= 1;
+    CK(cudaGetLastError());
+    return FDTD_OK;
+  }
   int64_t left = nsteps;
   while (left > 0) {
     const int per = 2 * c->kz;
@@ -2007,6 +2067,7 @@ fdtd_status fdtd_get_info(const fdtd_ctx* c, fdtd_info* o) {
   o->fixup_clusters = c->n_clusters;
   o->big_instances = (int32_t)(c->batch_tab.size() / fdtd::BATCH_FIELDS) - c->n_batch_reg;
   if (c->inst_model.empty()) o->big_instances = 0;
+  o->whole_grid = c->whole ? 1 : 0;
   return FDTD_OK;
 }
 

@@ -1310,9 +1310,14 @@ struct BatchShared {
 // zones' energy (which the sweep skipped) and the zone probes are recorded here for every step of
 // the pass.  Cells outside the grid (walls) load as dead cells with zero fields.  Every region
 // phase runs over the whole batch at once.
-template <typename T, int K, bool ENERGY, bool BIG = false>
+// WHOLE (wholegrid_kernel, K3c): the batch is every instance of the grid around one
+// region that is the whole grid plus a one-cell ring of dead wall cells, so nothing in it goes
+// wrong at its border: nsteps steps run back to back (no cone), every cell is a zone cell (energy,
+// probes from p.wprobe, write-back of every cell and edge), and each step's W^n goes straight to
+// the energy ring.
+template <typename T, int K, bool ENERGY, bool BIG = false, bool WHOLE = false>
 __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[K], int64_t step, BatchShared& bs,
-                            double* part = nullptr) {
+                            double* part = nullptr, int64_t nsteps = K) {
   const int* bt = p.batch_tab + BATCH_FIELDS * bi;  // (model, member offset, count, slots B, region stride, kind)
   const int model = bt[0], nb = bt[2], B = bt[3], rstride = bt[4], kind = bt[5];
   const int32_t* mem = p.batch_inst + bt[1];
@@ -1328,14 +1333,16 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   const int64_t nYB = (int64_t)nY * B;
   T* reg = rom_end(sv, S, nYB, B);
   const RomConst<T> rc(sv, S, nYB);
-  const int Kz = p.Kz, M = Kz + K - 1;
+  const int Kz = p.Kz, M = WHOLE ? 1 : Kz + K - 1;
   const int64_t P = p.pitch;
   // the members' blocks (one model: bx x by); the region's block: a member's, or the cluster's box
   const int bx = p.rects[4 * (int64_t)mem[0] + 2], by = p.rects[4 * (int64_t)mem[0] + 3];
   const int rbx = kind ? p.batch_rect[4 * bi + 2] : bx, rby = kind ? p.batch_rect[4 * bi + 3] : by;
   const int Wr = rbx + 2 * M, Hr = rby + 2 * M, W1 = Wr + 1, n = Hr * Wr;
   int zu0 = 0, zu1 = 0, zv0 = 0, zv1 = 0;
-  if (Kz >= 2) {  // zone rectangle in region coordinates
+  if (WHOLE) {  // every cell of the grid
+    zu0 = M; zu1 = M + rbx; zv0 = M; zv1 = M + rby;
+  } else if (Kz >= 2) {  // zone rectangle in region coordinates
     zu0 = M - (Kz - 1); zu1 = M + rbx + Kz; zv0 = M - (Kz - 1); zv1 = M + rby + Kz;
   }
   const int zw = zu1 - zu0, nz = zw * (zv1 - zv0);
@@ -1483,10 +1490,19 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   // cone that is still exact: cells [s, Wr - s) x [s, Hr - s) (edges one further in across their
   // normal); the zone, the ROM's gather cells and the write-back all lie inside the last cone.
   // the step's region pieces (K3)
+  auto gsrc = [&](int s) -> T {  // soft-source sample of step n+s
+    if constexpr (WHOLE) {
+      const int64_t k = step + s - p.src_meta[0];
+      return (p.src_row >= 0 && k >= 0 && k < p.src_meta[1]) ? (T)p.src_samples[k] : T(0);
+    } else {
+      return g[s];
+    }
+  };
   // H half-step (+ source, + the zone cells' storage-function terms of W^{n+s}) on the cone of step s
   auto h_half = [&](int s) {
-    const int cw = Wr - 2 * s, ch = Hr - 2 * s;
-    for (Flat f(tid, nt, s, cw, s, ch); f.b < nreg; f.next()) {
+    const int sc = WHOLE ? 0 : s;  // (the whole grid has no cone)
+    const int cw = Wr - 2 * sc, ch = Hr - 2 * sc;
+    for (Flat f(tid, nt, sc, cw, sc, ch); f.b < nreg; f.next()) {
       const int u = f.u, v = f.v, r = f.b;
       const T* ex = EX(r);
       const T* ey = EY(r);
@@ -1496,7 +1512,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       const T h0 = hz[t];
       const T hu = hupd(h0, ex[t + Wr], ex[t], ey[v * W1 + u + 1], ey[v * W1 + u], p.chy, p.chx);
       T h = ma[t] < T(0) ? h0 : hu;  // dead cells keep their Hz (as in yee_row)
-      if (u == bs.su[r] && v >= bs.sv0[r] && v < bs.sv1[r]) h += g[s];
+      if (u == bs.su[r] && v >= bs.sv0[r] && v < bs.sv1[r]) h += gsrc(s);
       if (ENERGY && u >= zu0 && u < zu1 && v >= zv0 && v < zv1) {
         // the zone cell's full storage-function term (row_coef's weights without the zone mask)
         const T* ms = MS(r);
@@ -1514,7 +1530,13 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   // zone probes; S4 gather of y^{n+s} (interface edges) and h = Hz^{n+s+1/2} (outside cells); the
   // regions' zone energies (fixed order, one warp per region)
   auto gather = [&](int s) {
-    for (int b = 0; b < nr; ++b) {
+    if constexpr (WHOLE) {  // every probe of the grid
+      for (int z = tid; z < p.n_wprobe; z += nt) {
+        const int u = p.wprobe[3 * z] + M, v = p.wprobe[3 * z + 1] + M;
+        p.probe_ring[(int64_t)p.wprobe[3 * z + 2] * p.cap + (step + s) % p.cap] = H(0)[v * Wr + u];
+      }
+    }
+    for (int b = 0; !WHOLE && b < nr; ++b) {
       const int z0 = p.zp_off[mem[b]], z1 = p.zp_off[mem[b] + 1];
       if (z0 == z1) continue;
       const int r = bs.rr[b];
@@ -1570,8 +1592,9 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   // E half-step on the regions' live edges (dead edges -- interface, PEC, hole -- keep their value:
   // they are skipped, so the scatter and the update never touch the same edge)
   auto e_half = [&](int s) {
-    const int cw = Wr - 2 * s, ch = Hr - 2 * s;
-    for (Flat f(tid, nt, s, cw, s + 1, ch - 1); f.b < nreg; f.next()) {  // Ex edge rows s+1 .. Hr-s-1,
+    const int sc = WHOLE ? 0 : s;
+    const int cw = Wr - 2 * sc, ch = Hr - 2 * sc;
+    for (Flat f(tid, nt, sc, cw, sc + 1, ch - 1); f.b < nreg; f.next()) {  // Ex edge rows s+1 .. Hr-s-1,
       const int t = f.v * Wr + f.u;                                         // columns s .. Wr-s-1
       const T* ma = MA(f.b);
       const T* ms = MS(f.b);
@@ -1582,7 +1605,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       edge_coef(ma[t - Wr], ms[t - Wr], ma[t], ms[t], p.idy, ca, cb, a, l);
       if (l) ex[t] = eupd(ex[t], ca, cb, hz[t] - hz[t - Wr]);
     }
-    for (Flat f(tid, nt, s + 1, cw - 1, s, ch); f.b < nreg; f.next()) {  // Ey edge columns s+1 .. Wr-s-1,
+    for (Flat f(tid, nt, sc + 1, cw - 1, sc, ch); f.b < nreg; f.next()) {  // Ey edge columns s+1 .. Wr-s-1,
       const int c = f.v * Wr + f.u;                                         // rows s .. Hr-s-1
       const T* ma = MA(f.b);
       const T* ms = MS(f.b);
@@ -1595,9 +1618,9 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     }
   };
 #pragma unroll 1
-  for (int s = 0; s < K; ++s) {
-    double* ep = p.rom_partials + (int64_t)s * p.n_inst;
-    if constexpr (FDTD_FUSE && !BIG) {
+  for (int s = 0; s < (WHOLE ? nsteps : K); ++s) {
+    double* ep = p.rom_partials + (int64_t)(WHOLE ? 0 : s) * p.n_inst;
+    if constexpr ((FDTD_FUSE || WHOLE) && !BIG) {
       // five barrier phases per step instead of seven: the M1 GEMM needs x~ only, so it shares the
       // H half-step's phase; the live-edge E half-step needs neither y nor the ROM, so it shares the
       // gather's; the scatter rides in the M2 epilogue
@@ -1614,6 +1637,12 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       PHASE();
       // (after the barrier: rom_t's warps have written ep)
       if (ENERGY && tid < nr && (kind == 0 || tid == 0)) ep[mem[tid]] += bs.zsum[bs.rr[tid]];
+      if (WHOLE && ENERGY && tid == 0) {  // W^{n+s}: the grid's cells (zsum) and every ROM, fixed order
+        double tot = 0.0;
+        for (int b = 0; b < nb; ++b) tot += ep[mem[b]];
+        p.energy_ring[(step + s) % p.cap] = tot;
+        if (!isfinite(tot)) *p.flag = 1;
+      }
       rom_schur<T>(p, m, mem, nb, B, S, sv);
       __syncthreads();
       PHASE();
@@ -1643,7 +1672,22 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     PHASE();
   }
   // ---- write back the zones: Hz of the live zone cells, their bottom Ex and left Ey edges
-  if (nz > 0)
+  if constexpr (WHOLE) {  // every cell and edge of the grid (dead ones included), and a finiteness check
+    bool bad = false;
+    for (Flat f(tid, nt, M, rbx + 1, M, rby + 1); f.b < nreg; f.next()) {
+      const int t = f.v * Wr + f.u;
+      const int64_t o = bs.gbase[f.b] + (int64_t)f.v * P + f.u;
+      const bool cu = f.u < M + rbx, cv = f.v < M + rby;
+      if (cu && cv) {
+        const T h = H(f.b)[t];
+        bad |= !isfinite((double)h);
+        p.hz1[o] = h;
+      }
+      if (cu) p.ex1[o] = EX(f.b)[t];
+      if (cv) p.ey1[o] = EY(f.b)[f.v * W1 + f.u];
+    }
+    if (__syncthreads_or(bad) && tid == 0) *p.flag = 1;
+  } else if (nz > 0)
     for (Flat f(tid, nt, zu0, zw, zv0, zv1 - zv0); f.b < nreg; f.next()) {
       const int t = f.v * Wr + f.u;
       if (!(MA(f.b)[t] >= T(0))) continue;
@@ -1699,6 +1743,24 @@ __global__ void __launch_bounds__(512, 1) postk_kernel(const PostParams<T> p) {
       if (threadIdx.x == 0) p.level1[(int64_t)s * p.n_batch + b] = tot;
     }
   }
+}
+
+// K3c: the whole grid and all its ROM instances in one CTA's shared memory for nsteps steps (small
+// grids: config 1, the degenerate cases); one launch per fdtd_step call.  Advances the device step
+// counter (no finalize kernel: the energy ring is written per step).
+template <typename T, bool ENERGY>
+__global__ void __launch_bounds__(512, 1) wholegrid_kernel(const PostParams<T> p, int64_t nsteps) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ BatchShared bs;
+  T* sv = reinterpret_cast<T*>(smem_raw);
+#if FDTD_PHASES
+  if (threadIdx.x == 0) ph_counter() = 0;
+#endif
+  const int64_t step = *p.step;
+  const T g[1] = {T(0)};
+  fixup_batch<T, 1, ENERGY, false, true>(p, 0, sv, g, step, bs, nullptr, nsteps);
+  __syncthreads();
+  if (threadIdx.x == 0) *const_cast<int64_t*>(p.step) = step + nsteps;  // (the context's counter)
 }
 
 // The large-model fix-up (one instance at a time on a cooperative grid of one CTA per SM): the
@@ -2145,6 +2207,15 @@ void bigrom_launch(const PostParams<T>& p, cudaStream_t s) {
 }
 
 template <typename T>
+void launch_wholegrid(const PostParams<T>& p, int64_t nsteps, bool energy, cudaStream_t s) {
+  if (nsteps <= 0) return;
+  const size_t smem = p.smem_bytes;
+  auto kern = energy ? wholegrid_kernel<T, true> : wholegrid_kernel<T, false>;
+  if (smem > 32 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<1, p.block, smem, s>>>(p, nsteps);
+}
+
+template <typename T>
 void launch_post_big(const PostParams<T>& p, int K, bool energy, cudaStream_t s) {
   if (p.n_batch <= p.n_batch_reg) return;
   if (K == 1) energy ? bigrom_launch<T, 1, true>(p, s) : bigrom_launch<T, 1, false>(p, s);
@@ -2233,6 +2304,7 @@ void launch_band_marks(T* msb, const T* mea, int64_t pitch, int64_t nx, int row0
   template void launch_sweep<T>(const SweepParams<T>&, int, int, cudaStream_t, int, int);         \
   template void launch_post<T>(const PostParams<T>&, int, bool, cudaStream_t);                   \
   template void launch_post_big<T>(const PostParams<T>&, int, bool, cudaStream_t);               \
+  template void launch_wholegrid<T>(const PostParams<T>&, int64_t, bool, cudaStream_t);          \
   template int big_grid_size<T>(size_t, int);                                                     \
   template void launch_materials<T, float>(const float*, const float*, int64_t, int64_t, int64_t, int64_t, \
                                            int64_t, int, int, int64_t, double, T*, T*, cudaStream_t);     \

@@ -135,6 +135,9 @@ struct PostParams {
   T* big;            // bigrom_kernel scratch (x~ twice, [M1; R~] x~, y and h of the largest model)
   size_t big_smem_bytes; int big_grid;
   int64_t alloc_elems; int rows, n_probe;  // FDTD_CHECK bounds: array elements, owned rows, probes
+  // whole-grid mode (wholegrid_kernel): every probe (i, j, probe index) and the energy ring
+  const int32_t* wprobe; int n_wprobe;
+  double* energy_ring;
 };
 
 // End of a pass (finalize_kernel, after the sweep, the CPML bands and the fix-up): W^{n+s} as a
@@ -202,6 +205,10 @@ template <typename T>
 void launch_post(const PostParams<T>& p, int K, bool energy, cudaStream_t s);
 template <typename T>
 void launch_post_big(const PostParams<T>& p, int K, bool energy, cudaStream_t s);
+// K3c: the whole grid in one CTA for nsteps steps (p.n_batch == 1: one batch of every instance
+// around the whole-grid region; p.smem_bytes its shared memory)
+template <typename T>
+void launch_wholegrid(const PostParams<T>& p, int64_t nsteps, bool energy, cudaStream_t s);
 template <typename T>
 int big_grid_size(size_t smem, int K);
 // shared-memory bytes of the fix-up kernel for a given batch (host-side sizing)

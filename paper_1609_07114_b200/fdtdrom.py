@@ -21,6 +21,7 @@ FDTD_MATERIALS_F32 = 0x2
 FDTD_ALLOW_DT_ABOVE_EQ1 = 0x4
 FDTD_NO_GRAPH = 0x8
 FDTD_LOCAL_GROUP = 0x10
+FDTD_NO_WHOLE = 0x20
 
 STATUS = {0: "FDTD_OK", 1: "FDTD_E_ARG", 2: "FDTD_E_STATE", 3: "FDTD_E_PASSIVITY", 4: "FDTD_E_UNSTABLE",
           5: "FDTD_E_CUDA", 6: "FDTD_E_NCCL", 7: "FDTD_E_NOMEM"}
@@ -50,7 +51,7 @@ class Info(C.Structure):
                 ("pitch", C.c_int64), ("sweep_ctas", C.c_int64), ("graphs", C.c_int32),
                 ("precision", C.c_int32), ("bytes_per_cell_step", C.c_double), ("steps_per_pass", C.c_int32),
                 ("sweep_stream", C.c_void_p), ("graph_builds", C.c_int64), ("fixup_clusters", C.c_int32),
-                ("big_instances", C.c_int32)]
+                ("big_instances", C.c_int32), ("whole_grid", C.c_int32)]
 
 
 class RomSpec(C.Structure):  # fdtdrom_build.h
@@ -215,7 +216,7 @@ class Simulation:
 
     def __init__(self, nx, ny, dx, dy, dt, eps_r, sigma, precision=32, device=0, stream=None, rank=0,
                  nranks=1, nccl_id=None, row_begin=0, row_end=None, materials_row0=0, record_capacity=0,
-                 allow_unstable=False, use_graphs=True, torch_allocator=True, local_group=False):
+                 allow_unstable=False, use_graphs=True, torch_allocator=True, local_group=False, whole_grid=True):
         import torch
 
         if not torch.cuda.is_available():
@@ -249,6 +250,8 @@ class Simulation:
             flags |= FDTD_NO_GRAPH
         if local_group:
             flags |= FDTD_LOCAL_GROUP
+        if not whole_grid:
+            flags |= FDTD_NO_WHOLE
         d = GridDesc()
         d.nx, d.ny, d.dx, d.dy, d.dt = self.nx, self.ny, self.dx, self.dy, self.dt
         d.precision, d.flags = self.precision, flags

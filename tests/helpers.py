@@ -37,7 +37,11 @@ def oracle_from_scene(scene, source=True, probes=True):
 
 
 def gpu_from_scene(scene, source=True, probes=True, **kw):
+    """The CUDA path for a scene.  whole_grid defaults to False here: the parity tests exercise the
+    sweep + fix-up passes even on grids small enough for the whole-grid path (K3c), which
+    tests/test_gpu_wholegrid.py covers (and compares with the passes bit for bit)."""
     from paper_1609_07114_b200 import Simulation
+    kw.setdefault("whole_grid", False)
     eps, sig = np_materials(scene)
     sim = Simulation(scene.nx, scene.ny, scene.dx, scene.dy, scene.dt, eps, sig, precision=scene.precision, **kw)
     if "pml" in scene.meta:
