@@ -149,6 +149,7 @@ struct fdtd_ctx {
   // whole-grid mode (K3c): the grid and every instance in one CTA, one launch per
   // fdtd_step call; its batch table (one kind-1 batch around the whole grid) and probe list
   bool whole = false;
+  bool whole_coef = false;
   size_t whole_smem = 0;
   int32_t* d_wb_tab = nullptr;
   int32_t* d_wb_inst = nullptr;
@@ -345,6 +346,7 @@ fdtd::PostParams<T> post_params(fdtd_ctx* c, int q) {
     p.batch_tab = c->d_wb_tab; p.batch_inst = c->d_wb_inst; p.batch_rect = c->d_wb_rect;
     p.n_batch = p.n_batch_reg = 1;
     p.smem_bytes = c->whole_smem;
+    p.whole_coef = c->whole_coef ? 1 : 0;
   }
   return p;
 }
@@ -1097,7 +1099,11 @@ fdtd_status apply_passes(fdtd_ctx* c, int k) {
         if ((st = upload(c, &c->d_wb_inst, inst)) != FDTD_OK) return st;
         if ((st = upload(c, &c->d_wb_rect, rect)) != FDTD_OK) return st;
         if ((st = upload(c, &c->d_wprobe, wp)) != FDTD_OK) return st;
-        c->whole_smem = smem;
+        // every edge's (ca, cb) and energy weight precomputed in shared memory, if they fit
+        const int64_t Wr = c->d.nx + 2, Hr = c->d.ny + 2;
+        const size_t coef = (size_t)(3 * (Hr + 1) * Wr + 3 * Hr * (Wr + 1)) * c->es;
+        c->whole_coef = smem + coef <= FIX_BUDGET;
+        c->whole_smem = smem + (c->whole_coef ? coef : 0);
         c->whole = true;
       }
     }

@@ -1486,6 +1486,35 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   PHASE();
+  // WHOLE with p.whole_coef: every edge's (ca, cb) and energy weight, built once for all the steps
+  // (edge_coef, the functions the per-step code calls; cb == 0 exactly on a dead edge)
+  T *CAX = nullptr, *CBX = nullptr, *WXC = nullptr, *CAY = nullptr, *CBY = nullptr, *WYC = nullptr;
+  if (WHOLE && p.whole_coef) {
+    const int nex = (Hr + 1) * Wr, ney = Hr * W1;
+    CAX = reg + (int64_t)rstride;
+    CBX = CAX + nex;
+    WXC = CBX + nex;
+    CAY = WXC + nex;
+    CBY = CAY + ney;
+    WYC = CBY + ney;
+    const T* ma = MA(0);
+    const T* ms = MS(0);
+    for (int k = tid; k < nex; k += nt) {  // Ex edge rows 1 .. Hr-1 (rows 0 and Hr: dead borders)
+      const int v = k / Wr;
+      T ca = T(1), cb = T(0), a = T(0);
+      bool l = false;
+      if (v >= 1 && v < Hr) edge_coef(ma[k - Wr], ms[k - Wr], ma[k], ms[k], p.idy, ca, cb, a, l);
+      CAX[k] = ca; CBX[k] = l ? cb : T(0); WXC[k] = l ? mul_rn(p.wxy, a) : T(0);
+    }
+    for (int k = tid; k < ney; k += nt) {  // Ey edge columns 1 .. Wr-1
+      const int v = k / W1, u = k % W1;
+      T ca = T(1), cb = T(0), a = T(0);
+      bool l = false;
+      if (u >= 1 && u < Wr) edge_coef(ma[v * Wr + u - 1], ms[v * Wr + u - 1], ma[v * Wr + u], ms[v * Wr + u], -p.idx, ca, cb, a, l);
+      CAY[k] = ca; CBY[k] = l ? cb : T(0); WYC[k] = l ? mul_rn(p.wxy, a) : T(0);
+    }
+    __syncthreads();
+  }
   // Values go wrong from the region's border inwards one cell per step, so step s only updates the
   // cone that is still exact: cells [s, Wr - s) x [s, Hr - s) (edges one further in across their
   // normal); the zone, the ROM's gather cells and the write-back all lie inside the last cone.
@@ -1515,12 +1544,19 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       if (u == bs.su[r] && v >= bs.sv0[r] && v < bs.sv1[r]) h += gsrc(s);
       if (ENERGY && u >= zu0 && u < zu1 && v >= zv0 && v < zv1) {
         // the zone cell's full storage-function term (row_coef's weights without the zone mask)
-        const T* ms = MS(r);
-        bool lx, ly;
-        T ax, ay, ca, cb;
-        edge_coef(ma[t - Wr], ms[t - Wr], ma[t], ms[t], p.idy, ca, cb, ax, lx);
-        edge_coef(ma[t - 1], ms[t - 1], ma[t], ms[t], -p.idx, ca, cb, ay, ly);
-        const T wx = lx ? mul_rn(p.wxy, ax) : T(0), wy = ly ? mul_rn(p.wxy, ay) : T(0);
+        T wx, wy;
+        if (WHOLE && WXC) {
+          wx = WXC[t];
+          wy = WYC[v * W1 + u];
+        } else {
+          const T* ms = MS(r);
+          bool lx, ly;
+          T ax, ay, ca, cb;
+          edge_coef(ma[t - Wr], ms[t - Wr], ma[t], ms[t], p.idy, ca, cb, ax, lx);
+          edge_coef(ma[t - 1], ms[t - 1], ma[t], ms[t], -p.idx, ca, cb, ay, ly);
+          wx = lx ? mul_rn(p.wxy, ax) : T(0);
+          wy = ly ? mul_rn(p.wxy, ay) : T(0);
+        }
         const T hw = ma[t] < T(0) ? T(0) : p.wh;
         ZE(r)[(v - zv0) * zw + u - zu0] = cell_energy(T(0), ex[t], ey[v * W1 + u], h0, h, wx, wy, hw);
       }
@@ -1567,7 +1603,17 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       sy[i * B + b] = y;
       sh[i * B + b] = h;
     }
-    if (ENERGY) {
+    if (ENERGY && WHOLE) {  // one region: every warp sums a fixed slice (per-warp partials in zsum)
+      const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+      const int per = (nz + nw - 1) / nw;
+      const int i0 = w * per, i1 = min(nz, i0 + per);
+      const T* ze = ZE(0);
+      double acc = 0.0;
+      for (int i = i0 + lane; i < i1; i += 32) acc += (double)ze[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
+      if (lane == 0) bs.zsum[w] = acc;
+    } else if (ENERGY) {
       const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
       for (int r = w; r < nreg; r += nw) {
         const T* ze = ZE(r);
@@ -1594,6 +1640,22 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   auto e_half = [&](int s) {
     const int sc = WHOLE ? 0 : s;
     const int cw = Wr - 2 * sc, ch = Hr - 2 * sc;
+    if (WHOLE && CBX) {  // precomputed coefficients (the same values; cb == 0 on dead edges)
+      const T* hz = H(0);
+      T* ex = EX(0);
+      T* ey = EY(0);
+      for (Flat f(tid, nt, 0, Wr, 1, Hr - 1); f.b < nreg; f.next()) {
+        const int t = f.v * Wr + f.u;
+        const T cb = CBX[t];
+        if (cb != T(0)) ex[t] = eupd(ex[t], CAX[t], cb, hz[t] - hz[t - Wr]);
+      }
+      for (Flat f(tid, nt, 1, Wr - 1, 0, Hr); f.b < nreg; f.next()) {
+        const int c = f.v * Wr + f.u, e = f.v * W1 + f.u;
+        const T cb = CBY[e];
+        if (cb != T(0)) ey[e] = eupd(ey[e], CAY[e], cb, hz[c] - hz[c - 1]);
+      }
+      return;
+    }
     for (Flat f(tid, nt, sc, cw, sc + 1, ch - 1); f.b < nreg; f.next()) {  // Ex edge rows s+1 .. Hr-s-1,
       const int t = f.v * Wr + f.u;                                         // columns s .. Wr-s-1
       const T* ma = MA(f.b);
@@ -1636,9 +1698,10 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       __syncthreads();
       PHASE();
       // (after the barrier: rom_t's warps have written ep)
-      if (ENERGY && tid < nr && (kind == 0 || tid == 0)) ep[mem[tid]] += bs.zsum[bs.rr[tid]];
+      if (ENERGY && !WHOLE && tid < nr && (kind == 0 || tid == 0)) ep[mem[tid]] += bs.zsum[bs.rr[tid]];
       if (WHOLE && ENERGY && tid == 0) {  // W^{n+s}: the grid's cells (zsum) and every ROM, fixed order
         double tot = 0.0;
+        for (int w = 0; w < (nt >> 5); ++w) tot += bs.zsum[w];
         for (int b = 0; b < nb; ++b) tot += ep[mem[b]];
         p.energy_ring[(step + s) % p.cap] = tot;
         if (!isfinite(tot)) *p.flag = 1;

@@ -138,6 +138,7 @@ struct PostParams {
   // whole-grid mode (wholegrid_kernel): every probe (i, j, probe index) and the energy ring
   const int32_t* wprobe; int n_wprobe;
   double* energy_ring;
+  int whole_coef;  // 1: every edge's coefficients precomputed in shared memory after the region
 };
 
 // End of a pass (finalize_kernel, after the sweep, the CPML bands and the fix-up): W^{n+s} as a
