@@ -31,7 +31,8 @@ __global__ void fill(float* a, size_t n, float base, float amp, uint32_t seed) {
 
 int main(int argc, char** argv) {
   const int64_t nx = getenv("SLP_N") ? atoi(getenv("SLP_N")) : 32768, rows = nx, pitch = nx + 64;
-  const int row0 = 8, nrows_alloc = (int)rows + row0 + 4;
+  const bool k8 = getenv("SLP_K8") != nullptr;  // experiment: 8 steps per pass (V = 2, 4 halo lanes)
+  const int row0 = k8 ? 16 : 8, nrows_alloc = (int)rows + row0 + 12;
   const int reps = argc > 1 ? atoi(argv[1]) : 10;
   const size_t tail = 32 * 1024 / 4;
   const size_t na1 = (size_t)nrows_alloc * pitch + tail;  // one row-major array
@@ -60,9 +61,21 @@ int main(int argc, char** argv) {
   base.wh = (float)(4e-7 * M_PI * dx * dx / dt);
   cudaStream_t st; CK(cudaStreamCreate(&st));
   cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+  auto launch = [&](const fdtd::SweepParams<float>& p) {
+    if (!k8) {
+      fdtd::launch_sweep<float>(p, 4, warps, st, 0, -1);
+      return;
+    }
+    const int nch = (p.rows + p.chunk - 1) / p.chunk;
+    const int64_t nvec = (p.nx + 1) / 2, nw = (nvec + 23) / 24;
+    dim3 grid((unsigned)((nw + warps - 1) / warps), nch);
+    const size_t smem = (size_t)warps * 8 * fdtd::NCOEF * 32 * 2 * sizeof(float);
+    cudaFuncSetAttribute(fdtd::sweepk_kernel<float, 8, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    fdtd::sweepk_kernel<float, 8, 2, true><<<grid, 32 * warps, smem, st>>>(p);
+  };
   auto timeit = [&](fdtd::SweepParams<float> p, const char* name) {
     for (int w = 0; w < 3; ++w) {
-      fdtd::launch_sweep<float>(p, 4, warps, st, 0, -1);
+      launch(p);
       std::swap(p.ex0, *(const float**)&p.ex1); std::swap(p.ey0, *(const float**)&p.ey1);
       std::swap(p.hz0, *(const float**)&p.hz1);
     }
@@ -71,7 +84,7 @@ int main(int argc, char** argv) {
     std::vector<float> all;
     for (int r = 0; r < reps; ++r) {
       cudaEventRecord(e0, st);
-      fdtd::launch_sweep<float>(p, 4, warps, st, 0, -1);
+      launch(p);
       cudaEventRecord(e1, st);
       cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -83,7 +96,7 @@ int main(int argc, char** argv) {
     std::vector<float> srt = all;
     std::sort(srt.begin(), srt.end());
     printf("%-34s best %.3f ms  median %.3f  mean %.3f ms per 4-step pass  (%s)  %.1f G cell-steps/s\n", name, best,
-           srt[reps / 2], sum / reps, cudaGetErrorString(e), 4.0 * nx * rows / (best * 1e-3) / 1e9);
+           srt[reps / 2], sum / reps, cudaGetErrorString(e), (k8 ? 8.0 : 4.0) * nx * rows / (best * 1e-3) / 1e9);
     if (getenv("SLP_ALL")) {
       for (float v : all) printf(" %.2f", v);
       printf("\n");
