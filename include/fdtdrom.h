@@ -200,6 +200,14 @@ fdtd_status fdtd_get_window(fdtd_ctx *c, int64_t i0, int64_t j0, int64_t w, int6
 fdtd_status fdtd_set_window(fdtd_ctx *c, int64_t i0, int64_t j0, int64_t w, int64_t h,
                             const double *Ex, const double *Ey, const double *Hz);
 
+/* Seeded random initial fields on the device (R26, the random-init state of the tests
+ * at any grid size): every live Hz cell and every live Ex / Ey edge of this rank's rows gets
+ * amplitude * u (E) or amplitude / eta0 * u (H), u in [-1, 1) a hash of (seed, component, global
+ * row, column) -- so every row-slab decomposition gets the same state.  Dead cells and edges (PEC
+ * walls, ROM holes, interface edges) keep their values, so the state stays consistent with the ROM
+ * states (y = L~^T E~).  Asynchronous on the stream; amplitude < 0: FDTD_E_ARG. */
+fdtd_status fdtd_set_random_fields(fdtd_ctx *c, uint64_t seed, double amplitude);
+
 /* ROM states x~ = [E~; H~] (q1 + q2 per instance, instances in the order they were
  * added on this rank), fp64.  Synchronous. */
 fdtd_status fdtd_get_rom_state(fdtd_ctx *c, double *out, int64_t cap, int64_t *n);

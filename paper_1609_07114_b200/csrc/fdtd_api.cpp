@@ -1891,6 +1891,24 @@ fdtd_status fdtd_set_window(fdtd_ctx* c, int64_t i0, int64_t j0, int64_t w, int6
   return window_io(c, i0, j0, w, h, const_cast<double*>(Ex), const_cast<double*>(Ey), const_cast<double*>(Hz), true);
 }
 
+fdtd_status fdtd_set_random_fields(fdtd_ctx* c, uint64_t seed, double amplitude) {
+  if (!c || !(amplitude >= 0.0)) return FDTD_E_ARG;
+  fdtd_status st = check_async(c);
+  if (st != FDTD_OK) return st;
+  const int q = c->cur;
+  const double ah = amplitude / (MU0 * C0);  // |H| ~ |E| / eta0
+  if (c->prec == 64)
+    fdtd::launch_random_fields<double>((double*)c->f[q][0], (double*)c->f[q][1], (double*)c->f[q][2],
+                                       (const double*)c->coef[0], c->pitch, c->d.nx, c->rows, ROW0, c->d.row_begin,
+                                       seed, amplitude, ah, c->stream);
+  else
+    fdtd::launch_random_fields<float>((float*)c->f[q][0], (float*)c->f[q][1], (float*)c->f[q][2],
+                                      (const float*)c->coef[0], c->pitch, c->d.nx, c->rows, ROW0, c->d.row_begin,
+                                      seed, amplitude, ah, c->stream);
+  CK(cudaGetLastError());
+  return FDTD_OK;
+}
+
 fdtd_status fdtd_get_rom_state(fdtd_ctx* c, double* out, int64_t cap, int64_t* n) {
   if (!c || !n) return FDTD_E_ARG;
   fdtd_status st = check_async(c);

@@ -2113,6 +2113,30 @@ __global__ void gather_mat_kernel(const M* eps_r, const M* sigma, int64_t nx, in
   os[k] = (double)sigma[(gj - mat_row0) * nx + gi];
 }
 
+// Seeded random state on the live cells and edges of the owned rows (fdtd_set_random_fields): each
+// value a hash of (seed, array, global row, column) -- independent of the row-slab decomposition;
+// dead cells and edges (PEC, holes, interface edges) keep their values.
+__device__ __forceinline__ double hash_unit(uint64_t seed, uint64_t a, uint64_t j, uint64_t i) {
+  uint64_t z = seed ^ (a << 60) ^ (j << 30) ^ i;
+  z += 0x9e3779b97f4a7c15ull;  // splitmix64
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;  // [-1, 1)
+}
+template <typename T>
+__global__ void random_fields_kernel(T* ex, T* ey, T* hz, const T* mea, int64_t pitch, int64_t nx, int row0,
+                                     int64_t row_begin, uint64_t seed, double ae, double ah) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nx) return;
+  const int64_t jl = row0 + blockIdx.y, gj = row_begin + blockIdx.y;
+  const int64_t o = jl * pitch + i;
+  if (!(mea[o] >= T(0))) return;
+  hz[o] = (T)(ah * hash_unit(seed, 2, gj, i));
+  if (mea[o - pitch] >= T(0)) ex[o] = (T)(ae * hash_unit(seed, 0, gj, i));
+  if (mea[o - 1] >= T(0)) ey[o] = (T)(ae * hash_unit(seed, 1, gj, i));  // (column -1: padding, dead)
+}
+
 template <typename T>
 __global__ void mask_kernel(T* mea, T* f0, T* f1, T* f2, T* f3, T* f4, T* f5, int64_t pitch, const int32_t* rects,
                             int64_t row_begin, int row0, bool zero_iface) {
@@ -2332,6 +2356,14 @@ void launch_mask(T* mea, T* f[6], int64_t pitch, const int32_t* rects, int64_t n
 }
 
 template <typename T>
+void launch_random_fields(T* ex, T* ey, T* hz, const T* mea, int64_t pitch, int64_t nx, int rows, int row0,
+                          int64_t row_begin, uint64_t seed, double ae, double ah, cudaStream_t s) {
+  if (rows <= 0 || nx <= 0) return;
+  random_fields_kernel<T><<<dim3((unsigned)((nx + 255) / 256), rows), 256, 0, s>>>(ex, ey, hz, mea, pitch, nx, row0,
+                                                                                  row_begin, seed, ae, ah);
+}
+
+template <typename T>
 void launch_zone(T* msb, const T* mea, int64_t pitch, const int32_t* rects, int64_t n_rect, int64_t row_begin,
                  int row0, int Kz, bool set, cudaStream_t s) {
   if (n_rect <= 0 || Kz < 2) return;
@@ -2374,6 +2406,8 @@ void launch_band_marks(T* msb, const T* mea, int64_t pitch, int64_t nx, int row0
   template void launch_materials<T, double>(const double*, const double*, int64_t, int64_t, int64_t,      \
                                             int64_t, int64_t, int, int, int64_t, double, T*, T*,          \
                                             cudaStream_t);                                                \
+  template void launch_random_fields<T>(T*, T*, T*, const T*, int64_t, int64_t, int, int, int64_t, uint64_t, \
+                                        double, double, cudaStream_t);                                     \
   template void launch_zone<T>(T*, const T*, int64_t, const int32_t*, int64_t, int64_t, int, int, bool,   \
                                cudaStream_t);                                                             \
   template void launch_pml<T>(const PmlParams<T>&, int, bool, cudaStream_t);                             \

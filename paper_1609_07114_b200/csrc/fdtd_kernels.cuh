@@ -234,6 +234,9 @@ void launch_gather_materials(const M* eps_r, const M* sigma, int64_t nx, int64_t
 template <typename M>
 void launch_min2(const M* a, const M* b, int64_t n, double* out /*2 per block*/, int nblocks, cudaStream_t s);
 template <typename T>
+void launch_random_fields(T* ex, T* ey, T* hz, const T* mea, int64_t pitch, int64_t nx, int rows, int row0,
+                          int64_t row_begin, uint64_t seed, double ae, double ah, cudaStream_t s);
+template <typename T>
 void launch_mask(T* mea, T* fields[6], int64_t pitch, const int32_t* rects, int64_t n_rect, int64_t row_begin,
                  int row0, bool zero_iface, cudaStream_t s);
 // sign bit of msb on the columns [0, ncol) and [nx - ncol, nx) of every owned row (PML bands)

@@ -99,6 +99,7 @@ def lib():
         L.fdtd_energy.argtypes = [vp, vp, i64, C.POINTER(i64)]
         L.fdtd_get_window.argtypes = [vp, i64, i64, i64, i64, vp, vp, vp]
         L.fdtd_set_window.argtypes = [vp, i64, i64, i64, i64, vp, vp, vp]
+        L.fdtd_set_random_fields.argtypes = [vp, C.c_uint64, C.c_double]
         L.fdtd_get_rom_state.argtypes = [vp, vp, i64, C.POINTER(i64)]
         L.fdtd_set_rom_state.argtypes = [vp, vp, i64]
         L.fdtd_sync.argtypes = [vp]
@@ -373,6 +374,11 @@ class Simulation:
         arrs = [None if a is None else _f64(a) for a in (Ex, Ey, Hz)]
         self._ck(lib().fdtd_set_window(self._h, int(i0), int(j0), int(w), int(h), *[_ptr(a) for a in arrs]),
                  "fdtd_set_window")
+
+    def set_random_fields(self, seed, amplitude=1.0):
+        """Seeded random live fields on the device (fdtd_set_random_fields)."""
+        self._ck(lib().fdtd_set_random_fields(self._h, C.c_uint64(int(seed)), C.c_double(float(amplitude))),
+                 "fdtd_set_random_fields")
 
     def get_rom_state(self):
         out = np.zeros(max(self.rom_state_len, 1))

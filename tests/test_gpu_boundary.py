@@ -96,3 +96,75 @@ def test_source_window_keeps_graph():
     assert b.info().graph_builds == 2
     a.close()
     b.close()
+
+
+def _holes(s):
+    """Masks of the ROM hole cells and of the interface edges (Ex rows / Ey columns on a block's rim)."""
+    hz = np.zeros((s.ny, s.nx), bool)
+    ex = np.zeros((s.ny + 1, s.nx), bool)
+    ey = np.zeros((s.ny, s.nx + 1), bool)
+    for k, i0, j0 in s.placements:
+        bx, by = s.models[k]["bx"], s.models[k]["by"]
+        hz[j0:j0 + by, i0:i0 + bx] = True
+        ex[j0:j0 + by + 1, i0:i0 + bx] = True
+        ey[j0:j0 + by, i0:i0 + bx + 1] = True
+    return ex, ey, hz
+
+
+def test_random_fields_state_and_parity():
+    """fdtd_set_random_fields: every live cell and edge populated, holes / interface edges / PEC walls
+    untouched (zero), and the state evolves like the oracle's from the same fields (fp32 1e-4, energy
+    non-increasing source-free)."""
+    from helpers import oracle_from_scene, rel
+    s = configs.make("cfg3", n=256)
+    g = gpu_from_scene(s, source=False)
+    g.set_random_fields(5, 1.0)
+    Ex, Ey, Hz = g.get_window()
+    mx, my, mh = _holes(s)
+    assert not Hz[mh].any() and not Ex[mx].any() and not Ey[my].any()
+    assert not Ex[0].any() and not Ex[-1].any() and not Ey[:, 0].any() and not Ey[:, -1].any()
+    live = ~mh
+    assert np.count_nonzero(Hz[live]) > 0.99 * live.sum()
+    assert 0.5 < np.abs(Ex[1:-1][~mx[1:-1]]).max() <= 1.0
+    assert np.abs(Hz).max() <= 1.0 / 376.0
+    o = oracle_from_scene(s, source=False)
+    o.set_state(Ex, Ey, Hz, None)
+    g.record_energy(True)
+    g.step(500)
+    _, eo = o.step(500, energy=True)
+    eg = g.energy()
+    Exg, Eyg, Hzg = g.get_window()
+    Exo, Eyo, Hzo, _ = o.get_state()
+    errs = dict(Ex=rel(Exg, Exo), Ey=rel(Eyg, Eyo), Hz=rel(Hzg, Hzo), energy=rel(eg, eo))
+    assert max(errs.values()) <= 1e-4, errs
+    assert np.all(np.diff(eg) <= 1e-6 * eg[:-1])
+    g.close()
+
+
+def test_random_fields_decomposition_independent():
+    """The same seed gives the same state on one context and on 3 row slabs."""
+    from paper_1609_07114_b200 import Simulation, slabs
+    s = configs.make("cfg3", n=256)
+    g = gpu_from_scene(s, source=False)
+    g.set_random_fields(11, 2.0)
+    ref = g.get_window()
+    g.close()
+    from helpers import np_materials
+    eps, sig = np_materials(s)
+    acc = [np.zeros_like(a) for a in ref]
+    for k in range(3):
+        rb, re = slabs.slab_rows(s.ny, 3, k)
+        m0, m1 = max(rb - 4, 0), min(re + 4, s.ny)
+        sim = Simulation(s.nx, s.ny, s.dx, s.dy, s.dt, eps[m0:m1], sig[m0:m1], precision=s.precision,
+                         rank=k, nranks=3, row_begin=rb, row_end=re, materials_row0=m0, local_group=True)
+        own = slabs.owned_placements(s.placements, s.models, rb, re)
+        for mk, m in enumerate(s.models):
+            sel = own[own[:, 0] == mk]
+            if len(sel):
+                sim.add_rom(m, sel[:, 1:3])
+        sim.set_random_fields(11, 2.0)
+        for a, b in zip(acc, sim.get_window()):
+            a += b
+        sim.close()
+    for a, b in zip(acc, ref):
+        assert np.array_equal(a, b)

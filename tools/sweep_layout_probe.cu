@@ -105,8 +105,9 @@ int main(int argc, char** argv) {
   {  // separate arrays
     fdtd::SweepParams<float> p = base;
     p.naf = p.nam = 1;
-    p.ex0 = alloc(na1, 0.f, 1e-3f); p.ey0 = alloc(na1, 0.f, 1e-3f); p.hz0 = alloc(na1, 0.f, 1e-3f);
-    p.ex1 = alloc(na1, 0.f, 1e-3f); p.ey1 = alloc(na1, 0.f, 1e-3f); p.hz1 = alloc(na1, 0.f, 1e-3f);
+    const float fa = getenv("SLP_ZERO") ? 0.f : 1e-3f;  // SLP_ZERO: all-zero fields (data-dependent power)
+    p.ex0 = alloc(na1, 0.f, fa); p.ey0 = alloc(na1, 0.f, fa); p.hz0 = alloc(na1, 0.f, fa);
+    p.ex1 = alloc(na1, 0.f, fa); p.ey1 = alloc(na1, 0.f, fa); p.hz1 = alloc(na1, 0.f, fa);
     p.mea = alloc(na1, 20.f, 10.f); p.msb = alloc(na1, 0.01f, 0.01f);
     p.alloc_elems_f = p.alloc_elems_m = (int64_t)na1;
     CK(cudaDeviceSynchronize());
