@@ -169,7 +169,9 @@ fdtd_status fdtd_record_energy(fdtd_ctx *c, int32_t on);
  * H half-step (eq:updateH), source, probes and energy, per-ROM gather / reduced
  * update / scatter (eq:connExplicit), E half-step (eq:updateEx) -- S1..S8 of
  * DESIGN.md.  FDTD_E_STATE if the unread probe/energy records would exceed
- * record_capacity. */
+ * record_capacity.  Large grids run K-step passes (sweep + ROM fix-up, CUDA graphs); a small
+ * single-rank grid with a few instances of one model runs the whole call as one kernel launch
+ * (fdtd_info.whole_grid; FDTD_NO_WHOLE opts out) -- the results are bit-identical either way. */
 fdtd_status fdtd_step(fdtd_ctx *c, int64_t nsteps);
 
 /* In-process slab group (testing the decomposition on one device): contexts created with
