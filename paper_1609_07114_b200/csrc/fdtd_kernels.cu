@@ -1735,19 +1735,18 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     PHASE();
   }
   // ---- write back the zones: Hz of the live zone cells, their bottom Ex and left Ey edges
-  if constexpr (WHOLE) {  // every cell and edge of the grid (dead ones included), and a finiteness check
+  if constexpr (WHOLE) {  // every cell of the grid with its bottom Ex and left Ey edge (dead ones
+                          // included; the top and east wall edges never change), a finiteness check
     bool bad = false;
-    for (Flat f(tid, nt, M, rbx + 1, M, rby + 1); f.b < nreg; f.next()) {
+    for (Flat f(tid, nt, M, rbx, M, rby); f.b < nreg; f.next()) {
       const int t = f.v * Wr + f.u;
       const int64_t o = bs.gbase[f.b] + (int64_t)f.v * P + f.u;
-      const bool cu = f.u < M + rbx, cv = f.v < M + rby;
-      if (cu && cv) {
-        const T h = H(f.b)[t];
-        bad |= !isfinite((double)h);
-        p.hz1[o] = h;
-      }
-      if (cu) p.ex1[o] = EX(f.b)[t];
-      if (cv) p.ey1[o] = EY(f.b)[f.v * W1 + f.u];
+      FCHK(o >= (int64_t)p.row0 * p.pitch && o < (int64_t)(p.row0 + p.rows) * p.pitch);  // owned rows only
+      const T h = H(f.b)[t];
+      bad |= !isfinite((double)h);
+      p.hz1[o] = h;
+      p.ex1[o] = EX(f.b)[t];
+      p.ey1[o] = EY(f.b)[f.v * W1 + f.u];
     }
     if (__syncthreads_or(bad) && tid == 0) *p.flag = 1;
   } else if (nz > 0)

@@ -7,6 +7,7 @@ the sweep, the fix-up region loads / write-backs / scatters, the zone probes, th
 loads and stores trap on a bounds violation, and write-backs must stay in the owned rows), then runs
 small hot-path cases with cudaMalloc'd buffers (no caching allocator), K = 1, 2, 4:
   * parity with the fp64 oracle (fp64 1e-10 / fp32 1e-4);
+  * the whole-grid path (cfg1whole, densewhole: K3c, one launch per call) the same way;
   * determinism: the same run twice, and with the fix-up at 128 / 256 / 512 threads per CTA, must be
     bit-identical -- a shared-memory race or a missing barrier would show as a difference
     (the racecheck / synccheck stand-in).
@@ -36,13 +37,18 @@ elif case == "cfg3crop":
     s = configs.make("cfg3", n=256)
 elif case == "cfg5sub":
     s = configs.make("cfg5", n=512, max_fine=64, min_count=8)
+elif case == "cfg1whole":
+    s = configs.make("cfg1")
+elif case == "densewhole":
+    from test_gpu_wholegrid import _dense_fp32
+    s = _dense_fp32()
 elif case == "literal":
     from test_gpu_parity import _literal_scene
     s = _literal_scene(32, n=128)
 else:
     from test_gpu_pml import channel_scene
     s = channel_scene(32, nx=120, ny=40, rom=True)
-g = gpu_from_scene(s, torch_allocator=False)
+g = gpu_from_scene(s, torch_allocator=False, whole_grid=case.endswith("whole"))
 g.set_time_blocking(k)
 Ex, Ey, Hz, xs = consistent_random_state(s, 3)
 g.set_window(0, 0, Ex, Ey, Hz)
@@ -63,6 +69,7 @@ h = hashlib.sha256()
 for a in (*W, x, p):
     h.update(np.ascontiguousarray(a).tobytes())
 print("RESULT " + json.dumps(dict(case=case, k=k, used=g.info().steps_per_pass, err=err, prec=s.precision,
+                                  whole_grid=int(g.info().whole_grid),
                                   digest=h.hexdigest()[:16])))
 ''' % (ROOT, os.path.join(ROOT, "tests"), case, k, steps)
     try:
@@ -88,7 +95,7 @@ def main():
         from paper_1609_07114_b200 import build
         build.build_checked()
     cases = [("cfg1", 1), ("cfg1", 2), ("cfg3crop", 1), ("cfg3crop", 2), ("cfg3crop", 4), ("pml", 4),
-             ("literal", 4), ("cfg5sub", 4)]
+             ("literal", 4), ("cfg5sub", 4), ("cfg1whole", 2), ("densewhole", 4)]
     res = []
     ok = True
     for case, k in cases:
