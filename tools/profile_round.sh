@@ -9,6 +9,8 @@ OUT=gpurun_out
 mkdir -p $OUT
 python bench.py > $OUT/bench_full_$TAG.log 2>&1; echo "bench=$?"
 python bench.py --impl reference > $OUT/bench_ref_$TAG.log 2>&1; echo "ref=$?"
+python bench.py --init random --no-cpu > $OUT/bench_cfg4_random_$TAG.log 2>&1; echo "bench_random=$?"
+python tools/wholegrid_bench.py --out $OUT/wholegrid_bench_$TAG.json > $OUT/wholegrid_$TAG.log 2>&1; echo "wholegrid=$?"
 for w in cfg2 cfg3 cfg5 cfg4dense; do
   python bench.py --workload $w --no-cpu > $OUT/bench_${w}_$TAG.log 2>&1; echo "bench_$w=$?"
 done
