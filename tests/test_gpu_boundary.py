@@ -111,13 +111,14 @@ def _holes(s):
     return ex, ey, hz
 
 
-def test_random_fields_state_and_parity():
+@pytest.mark.parametrize("name,whole", [("cfg3", False), ("cfg1", False), ("cfg1", True)])
+def test_random_fields_state_and_parity(name, whole):
     """fdtd_set_random_fields: every live cell and edge populated, holes / interface edges / PEC walls
-    untouched (zero), and the state evolves like the oracle's from the same fields (fp32 1e-4, energy
-    non-increasing source-free)."""
+    untouched (zero), and the state evolves like the oracle's from the same fields (fp32 1e-4 / fp64
+    1e-10, energy non-increasing source-free) -- the pass path and the whole-grid path."""
     from helpers import oracle_from_scene, rel
-    s = configs.make("cfg3", n=256)
-    g = gpu_from_scene(s, source=False)
+    s = configs.make("cfg3", n=256) if name == "cfg3" else configs.make(name)
+    g = gpu_from_scene(s, source=False, whole_grid=whole)
     g.set_random_fields(5, 1.0)
     Ex, Ey, Hz = g.get_window()
     mx, my, mh = _holes(s)
@@ -136,7 +137,8 @@ def test_random_fields_state_and_parity():
     Exg, Eyg, Hzg = g.get_window()
     Exo, Eyo, Hzo, _ = o.get_state()
     errs = dict(Ex=rel(Exg, Exo), Ey=rel(Eyg, Eyo), Hz=rel(Hzg, Hzo), energy=rel(eg, eo))
-    assert max(errs.values()) <= 1e-4, errs
+    assert max(errs.values()) <= (1e-4 if s.precision == 32 else 1e-10), errs
+    assert g.info().whole_grid == int(whole)
     assert np.all(np.diff(eg) <= 1e-6 * eg[:-1])
     g.close()
 
