@@ -61,6 +61,7 @@ def main():
     ap.add_argument("--steps", type=int, default=96)
     ap.add_argument("--slabs", default="1,2,4,8")
     ap.add_argument("--workload", default="cfg4")
+    ap.add_argument("--slab-chunk", type=int, default=0, help="rows per CTA on the slab contexts (0: default)")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_slab_overhead.json"))
     a = ap.parse_args()
     scene = configs.make(a.workload, device="cuda")
@@ -69,6 +70,9 @@ def main():
     base = None
     for n in [int(x) for x in a.slabs.split(",")]:
         sims = build(scene, n, stream)
+        if n > 1 and a.slab_chunk:
+            for sim in sims:
+                sim.set_tuning(a.slab_chunk, 0)
         ms = timed(sims, a.steps)
         for sm in sims:
             sm.profile(True)
