@@ -161,3 +161,20 @@ def test_whole_successive_calls_vs_oracle():
     Exo, Eyo, Hzo, _ = o.get_state()
     assert max(rel(Exg, Exo), rel(Eyg, Eyo), rel(Hzg, Hzo)) <= 1e-10
     g.close()
+
+
+def test_whole_line_source_and_probe_in_hole():
+    """A line source across the grid (through an instance's row span) and a probe inside a ROM hole:
+    the whole-grid path equals the passes bit for bit and the oracle to 1e-10."""
+    s = _one_model(40, 36, 64)
+    i0, j0 = int(s.placements[0, 1]), int(s.placements[0, 2])
+    s.meta["source_rows"] = (2, s.ny - 2)
+    s.source = (s.nx - 9, 0)
+    s.probes = np.concatenate([s.probes, np.array([[i0 + 1, j0 + 1]], dtype=np.int32)])
+    calls = (5, 17, 40)
+    a = _run(s, False, calls, spp=2)
+    b = _run(s, True, calls)
+    for x, y in zip(a[0], b[0]):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+    _compare(s, 300, 1e-10, whole_grid=True)
