@@ -776,6 +776,9 @@ __device__ __forceinline__ int& ph_counter() {
 #ifndef FDTD_FUSE  // fix-up: five barrier phases per step (M1 beside the H half-step, E beside the gather)
 #define FDTD_FUSE 1
 #endif
+#ifndef FDTD_FUSE2  // whole-grid path: t formed in the gather, the ROM energy in the Schur phase (4 barriers)
+#define FDTD_FUSE2 1
+#endif
 #ifndef FDTD_SKPF  // prefetch the batch's Schur inverses into L2 at the batch start
 #define FDTD_SKPF 1
 #endif
@@ -1032,6 +1035,34 @@ __device__ __forceinline__ void rom_t(const RomModelDev& m, const int32_t* mem, 
     v.st[k] = v.so[(q2 + q1 + i) * B + b] + fma_rn(rc.cyg[k], v.sh[k], mul_rn(rc.cya[k], v.sy[k]));
   }
 }
+// The storage-function part of rom_t alone (FDTD_FUSE2: t is formed by the gather), one warp per
+// instance; plus z(b) (the zone energy of the member's region, or 0) added by its lane 0 -- the
+// same two fp64 additions rom_t and the zone add make.
+template <typename T, bool ENERGY, typename Z>
+__device__ __forceinline__ void rom_energy(const RomModelDev& m, const int32_t* mem, int nb, int B, int64_t S, T* sv,
+                                           double* ep, Z z) {
+  if (!ENERGY) return;
+  const int nY = m.nY, q1 = m.q1, q2 = m.q2, nx = q1 + q2, m1 = q2 + q1 + nY;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  RomVec<T> v(sv, S);
+  const RomConst<T> rc(sv, S, (int64_t)nY * B);
+  const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+  for (int b = w; b < nb; b += nw) {
+    double acc = 0.0;
+    for (int i = lane; i < nY; i += 32) {
+      const double y = (double)v.sy[i * B + b];
+      acc += rc.eh[i * B + b] * y * y;
+    }
+    for (int i = lane; i < nx; i += 32) acc += (double)v.sx[i * B + b] * (double)v.so[(m1 + i) * B + b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
+    if (lane == 0) {
+      ep[mem[b]] = acc;
+      ep[mem[b]] += z(b);
+    }
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ void rom_schur(const PostParams<T>& p, const RomModelDev& m, const int32_t* mem, int nb,
                                           int B, int64_t S, T* sv) {
@@ -1565,7 +1596,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   };
   // zone probes; S4 gather of y^{n+s} (interface edges) and h = Hz^{n+s+1/2} (outside cells); the
   // regions' zone energies (fixed order, one warp per region)
-  auto gather = [&](int s) {
+  auto gather = [&](int s, bool with_t) {
     if constexpr (WHOLE) {  // every probe of the grid
       for (int z = tid; z < p.n_wprobe; z += nt) {
         const int u = p.wprobe[3 * z] + M, v = p.wprobe[3 * z + 1] + M;
@@ -1602,6 +1633,10 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       }
       sy[i * B + b] = y;
       sh[i * B + b] = h;
+      if (with_t) {  // t = (a_y/c_y) y + (D_l G/c_y) h - L~^T E*, as rom_t forms it (M1 ran in the H phase)
+        const int k = i * B + b;
+        sv[5 * S + k] = sv[3 * S + (m.q2 + m.q1 + i) * B + b] + fma_rn(rc.cyg[k], h, mul_rn(rc.cya[k], y));
+      }
     }
     if (ENERGY && WHOLE) {  // one region: every warp sums a fixed slice (per-warp partials in zsum)
       const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
@@ -1690,10 +1725,33 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
       rom_m1<T, ENERGY>(p, m, B, S, sv);
       __syncthreads();
       PHASE();
-      gather(s);
+      gather(s, FDTD_FUSE2 != 0 && WHOLE);
       e_half(s);
       __syncthreads();
       PHASE();
+      if constexpr (FDTD_FUSE2 != 0 && WHOLE) {
+        // four barrier phases per step: t was formed by the gather, so the storage-function terms
+        // (one warp per instance, the zone energy added by the same lane) share the Schur phase.
+        // Whole grid only: cfg1 7.5 instead of 8.15 us per step; on the batched fix-up the energy
+        // warps lengthen the Schur phase more than the saved barrier gains (0.432 vs 0.419 ms)
+        rom_energy<T, ENERGY>(m, mem, nb, B, S, sv, ep, [&](int b) {
+          return (!WHOLE && (kind == 0 || b == 0)) ? bs.zsum[bs.rr[b]] : 0.0;
+        });
+        rom_schur<T>(p, m, mem, nb, B, S, sv);
+        __syncthreads();
+        PHASE();
+        if (WHOLE && ENERGY && tid == 0) {  // W^{n+s}: the grid's cells (zsum) and every ROM, fixed order
+          double tot = 0.0;
+          for (int w = 0; w < (nt >> 5); ++w) tot += bs.zsum[w];
+          for (int b = 0; b < nb; ++b) tot += ep[mem[b]];
+          p.energy_ring[(step + s) % p.cap] = tot;
+          if (!isfinite(tot)) *p.flag = 1;
+        }
+        rom_m2<T>(p, m, nb, B, S, sv, scatter1);
+        __syncthreads();
+        PHASE();
+        continue;
+      }
       rom_t<T, ENERGY>(m, mem, nb, B, S, sv, ep);
       __syncthreads();
       PHASE();
@@ -1717,7 +1775,7 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
     h_half(s);
     __syncthreads();
     PHASE();
-    gather(s);
+    gather(s, false);
     __syncthreads();
     PHASE();
     // ---- S5: ROM step n+s -> y^{n+s+1}, x~^{n+s+1}; ROM energy of W^{n+s} (+ the zone energy of
