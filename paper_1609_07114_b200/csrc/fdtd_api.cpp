@@ -1307,17 +1307,25 @@ fdtd_status fdtd_create(const fdtd_grid_desc* desc, fdtd_ctx** out) {
 fdtd_status fdtd_set_tuning(fdtd_ctx* c, int32_t rows_per_cta, int32_t warps_per_cta) {
   if (!c) return FDTD_E_ARG;
   if (rows_per_cta < 0 || warps_per_cta < 0 || warps_per_cta > 8) return fail(c, FDTD_E_ARG, "bad tuning");
-  // rows per CTA: long chunks amortise the K-row prologue, short ones keep enough CTAs for ~8 waves
-  // rows per CTA: long enough that the 2K - 1 recomputed stage rows at a chunk start stay a few per
-  // cent, short enough for several waves of CTAs (the last wave's tail is paid once per slab)
   // rows per CTA: the 2K - 1 stage rows recomputed at a chunk start against the tail of the last
   // wave; a row slab of a multi-GPU run (a few thousand rows) does better with 128 than 64; 512
-  // rows measured 1.3 % faster than 256 on 32768 rows (tools/sweep_layout_probe.cu, round 2)
+  // rows measured 1.3 % faster than 256 on 32768 rows (tools/sweep_layout_probe.cu, round 2).
+  // Small grids (< 2048 rows, too few CTAs for one wave): a pass is the latency of one CTA's row
+  // chain, so short chunks of 2-warp CTAs spread it over >= ~600 CTAs (the Sec. VI-A cavity, 500^2
+  // fp64: 43 -> 31 us per step with 4-row chunks)
   const bool slab = c->d.nranks > 1;
   c->chunk = rows_per_cta ? rows_per_cta
                           : (c->rows >= 32768 ? 512 : c->rows >= 16384 ? 256
                              : c->rows >= 2048 ? (slab && c->rows < 8192 ? 128 : 64) : 32);
   c->warps = warps_per_cta ? warps_per_cta : 4;
+  if (!rows_per_cta && !warps_per_cta && c->rows < 2048) {
+    c->warps = 2;
+    int gx2 = 1;
+    for (int K = 1; K <= KMAX; K *= 2) gx2 = std::max(gx2, sweep_gx(c, K));
+    int ch = 32;
+    while (ch > 4 && (int64_t)((c->rows + ch - 1) / ch) * gx2 < 600) ch /= 2;
+    c->chunk = ch;
+  }
   if (!rows_per_cta)
     if (const char* e = getenv("FDTD_CHUNK")) c->chunk = std::max(1, atoi(e));  // tuning experiments
   if (!warps_per_cta)
