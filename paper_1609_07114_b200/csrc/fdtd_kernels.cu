@@ -779,6 +779,9 @@ __device__ __forceinline__ int& ph_counter() {
 #ifndef FDTD_FUSE2  // whole-grid path: t formed in the gather, the ROM energy in the Schur phase (4 barriers)
 #define FDTD_FUSE2 1
 #endif
+#ifndef BIG_TILES  // large-model path: row tiles of [M1; R~] per CTA processed together in phase 1
+#define BIG_TILES 3
+#endif
 #ifndef FDTD_SKPF  // prefetch the batch's Schur inverses into L2 at the batch start
 #define FDTD_SKPF 1
 #endif
@@ -1151,35 +1154,57 @@ __device__ void rom_step_big(const PostParams<T>& p, const RomModelDev& m, const
   // ---- phase 1: SO = [M1; R~] x~ (with ENERGY all m1 + nx rows)
   const int rows1 = ENERGY ? m1 + nx : m1, mt1 = (rows1 + 7) / 8, kt1 = m.kt1;
   if (worker) {
+    // the CTA's row tiles (c1, c1 + G1, ...) BT at a time: warp w takes k-tiles [ka, kb) of every one
+    // of them (each tile's DMMA chain and the fixed-order sum over the warps as one tile alone), so
+    // BT x 8 A-tile loads are in flight per warp instead of 8
+    constexpr int BT = BIG_TILES;
     const int kpw = (kt1 + nw - 1) / nw;
-    for (int tile = c1; tile < mt1; tile += G1) {
-      const int ka = warp * kpw, kb = min(ka + kpw, kt1);
-      const double* ap = mp + m.off_M1t + (int64_t)tile * kt1 * 32 + lane;
-      double d[2] = {0.0, 0.0};
+    const int ka = warp * kpw, kb = min(ka + kpw, kt1);
+    for (int tile0 = c1; tile0 < mt1; tile0 += BT * G1) {
+      const double* ap[BT];
+      bool on[BT];
+      double d[BT][2];
+#pragma unroll
+      for (int j = 0; j < BT; ++j) {
+        const int tile = tile0 + j * G1;
+        on[j] = tile < mt1;
+        ap[j] = mp + m.off_M1t + (int64_t)(on[j] ? tile : 0) * kt1 * 32 + lane;
+        d[j][0] = d[j][1] = 0.0;
+      }
       int kt = ka;
       for (; kt + 8 <= kb; kt += 8) {
-        double a[8], b[8];
+        double a[BT][8], b[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] = (double)__ldg(ap + (kt + u) * 32);
+        for (int j = 0; j < BT; ++j)
+#pragma unroll
+          for (int u = 0; u < 8; ++u) a[j][u] = on[j] ? (double)__ldg(ap[j] + (kt + u) * 32) : 0.0;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int kk = (kt + u) * 4 + t4;
           b[u] = (g == 0 && kk < nx) ? (double)xin[kk] : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) mma_f64(d, a[u], b[u]);
+        for (int j = 0; j < BT; ++j)
+#pragma unroll
+          for (int u = 0; u < 8; ++u) mma_f64(d[j], a[j][u], b[u]);
       }
       for (; kt < kb; ++kt) {
         const int kk = kt * 4 + t4;
-        mma_f64(d, (double)__ldg(ap + kt * 32), (g == 0 && kk < nx) ? (double)xin[kk] : 0.0);
+        const double b = (g == 0 && kk < nx) ? (double)xin[kk] : 0.0;
+#pragma unroll
+        for (int j = 0; j < BT; ++j)
+          if (on[j]) mma_f64(d[j], (double)__ldg(ap[j] + kt * 32), b);
       }
-      if (t4 == 0) part[warp * 8 + g] = d[0];  // column 0 (the instance) of rows tile*8 + g
+#pragma unroll
+      for (int j = 0; j < BT; ++j)
+        if (t4 == 0) part[(warp * BT + j) * 8 + g] = d[j][0];  // column 0 (the instance) of rows tile*8 + g
       __syncthreads();
-      if (tid < 8) {
+      if (tid < 8 * BT) {
+        const int j = tid / 8, r8 = tid % 8;
         double acc = 0.0;
-        for (int w = 0; w < nw; ++w) acc += part[w * 8 + tid];
-        const int r = tile * 8 + tid;
-        if (r < rows1) bsc.SO[r] = (T)acc;
+        for (int w = 0; w < nw; ++w) acc += part[(w * BT + j) * 8 + r8];
+        const int r = (tile0 + j * G1) * 8 + r8;
+        if (tile0 + j * G1 < mt1 && r < rows1) bsc.SO[r] = (T)acc;
       }
       __syncthreads();
     }
@@ -1189,36 +1214,67 @@ __device__ void rom_step_big(const PostParams<T>& p, const RomModelDev& m, const
       bsc.YH[i] = v.sy[i];
       bsc.YH[nY + i] = v.sh[i];
     }
+  PHASE();
   grid.sync();
+  PHASE();
   // ---- phase 2
   const RomConst<T> rc(sv, S, (int64_t)nY);
-  if (ENERGY && rg && warp == 0) {  // storage function of the instance (the batch path's order)
+  // storage function of the instance on the last CTA (it holds no M2 tile; CTA 0 is busiest): every
+  // warp sums a slice of x~^T R~ x~ (global scratch: all loads in flight), the fixed-order sum of
+  // the warps follows the Schur phase's barriers
+  const bool ecta = G > 1 ? cta == G - 1 : true;
+  if (ENERGY && ecta) {
     double acc = 0.0;
-    for (int i = lane; i < nY; i += 32) {
-      const double y = (double)v.sy[i];
-      acc += rc.eh[i] * y * y;
+    if (warp == 0) {
+      const int64_t po = p.port_off[first];
+      for (int i = lane; i < nY; i += 32) {
+        const double y = (double)bsc.YH[i];
+        acc += p.ehalf[po + i] * y * y;
+      }
     }
-    for (int i = lane; i < nx; i += 32) acc += (double)xin[i] * (double)bsc.SO[m1 + i];
+    const int per = (nx + nw - 1) / nw, i0 = warp * per, i1 = min(nx, i0 + per);
+    for (int i = i0 + lane; i < i1; i += 32) acc += (double)xin[i] * (double)bsc.SO[m1 + i];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
-    if (lane == 0) ep[first] = acc;
+    if (lane == 0) part[warp] = acc;
   }
   {  // t and U = S_k t, in every CTA
     const int64_t po = p.port_off[first];
     for (int i = tid; i < nY; i += nt)
       v.st[i] = bsc.SO[q2 + q1 + i] + fma_rn(p.cyg[po + i], bsc.YH[nY + i], mul_rn(p.cya[po + i], bsc.YH[i]));
     __syncthreads();
-    for (int i = tid; i < nY; i += nt) {
-      const T* Sk = p.Sk + p.Sk_off[first] + i;
-      T a[4] = {T(0), T(0), T(0), T(0)};
-      int c = 0;
-      for (; c + 3 < nY; c += 4)
+    // U = S_k t: warp w sums the columns [w cw, (w + 1) cw) for every row (lanes along the rows:
+    // coalesced column loads, all in flight at once), the warps' partials then in a fixed order
+    // (partials in the unused `so` slots of the vector area: 2 S elements)
+    const int pw = max(1, min(nw, (int)((2 * S * (int64_t)sizeof(T)) / (8 * (int64_t)nY))));
+    const int cw = (nY + pw - 1) / pw;
+    double* sp = reinterpret_cast<double*>(v.so);
+    if (warp < pw) {
+      const T* Sk = p.Sk + p.Sk_off[first];
+      const int c0 = warp * cw, c1e = min(nY, c0 + cw);
+      for (int i = lane; i < nY; i += 32) {
+        T a[4] = {T(0), T(0), T(0), T(0)};
+        int c = c0;
+        for (; c + 3 < c1e; c += 4)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) a[u] = fma_rn(__ldg(Sk + (int64_t)(c + u) * nY), v.st[c + u], a[u]);
-      for (; c < nY; ++c) a[0] = fma_rn(__ldg(Sk + (int64_t)c * nY), v.st[c], a[0]);
-      v.sU[i] = (a[0] + a[1]) + (a[2] + a[3]);
+          for (int u = 0; u < 4; ++u) a[u] = fma_rn(__ldg(Sk + (int64_t)(c + u) * nY + i), v.st[c + u], a[u]);
+        for (; c < c1e; ++c) a[0] = fma_rn(__ldg(Sk + (int64_t)c * nY + i), v.st[c], a[0]);
+        sp[warp * nY + i] = (double)((a[0] + a[1]) + (a[2] + a[3]));
+      }
     }
     __syncthreads();
+    for (int i = tid; i < nY; i += nt) {
+      double u = 0.0;
+      for (int w = 0; w < pw; ++w) u += sp[w * nY + i];
+      v.sU[i] = (T)u;
+    }
+    __syncthreads();
+    if (ENERGY && ecta && tid == 0) {  // (part holds the energy warps' sums; reused after the grid barriers)
+      double e = 0.0;
+      for (int w = 0; w < nw; ++w) e += part[w];
+      ep[first] = e;
+    }
+    PHASE();
   }
   // [E~'; y'] = [E*; L~^T E*] + M2 U: the tiles holding y rows on CTA 0 (it scatters y'), the others
   // one warp each on CTAs 1..
@@ -1227,7 +1283,18 @@ __device__ void rom_step_big(const PostParams<T>& p, const RomModelDev& m, const
   auto m2_tile = [&](int tile) {
     const double* ap = mp + m.off_M2t + (int64_t)tile * kt2 * 32 + lane;
     double d[2] = {0.0, 0.0};
-    for (int kt = 0; kt < kt2; ++kt) {
+    int kt = 0;
+    for (; kt + 8 <= kt2; kt += 8) {  // eight A tiles in flight, then their MMAs (the same order)
+      double a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = (double)__ldg(ap + (kt + u) * 32);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int kk = (kt + u) * 4 + t4;
+        mma_f64(d, a[u], (g == 0 && kk < nY) ? (double)v.sU[kk] : 0.0);
+      }
+    }
+    for (; kt < kt2; ++kt) {
       const int kk = kt * 4 + t4;
       mma_f64(d, (double)__ldg(ap + kt * 32), (g == 0 && kk < nY) ? (double)v.sU[kk] : 0.0);
     }
@@ -1245,6 +1312,7 @@ __device__ void rom_step_big(const PostParams<T>& p, const RomModelDev& m, const
     for (int tile = c1 * nw + warp; tile < ty; tile += G1 * nw) m2_tile(tile);
   if (worker)
     for (int r = c1 * nt + tid; r < q2; r += G1 * nt) xout[q1 + r] = bsc.SO[r];
+  PHASE();
   grid.sync();
 }
 
@@ -1890,8 +1958,11 @@ __global__ void __launch_bounds__(512, 1) bigrom_kernel(const PostParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[32];
   __shared__ BatchShared bs;
-  __shared__ double part[16 * 8];  // phase-1 partials: [warp][row]
+  __shared__ double part[16 * 8 * BIG_TILES];  // phase-1 partials: [warp][tile][row]
   T* sv = reinterpret_cast<T*>(smem_raw);
+#if FDTD_PHASES
+  if (threadIdx.x == 0) ph_counter() = 0;
+#endif
   const int64_t step = *p.step;
   T g[K];
 #pragma unroll
