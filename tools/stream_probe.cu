@@ -85,6 +85,49 @@ __global__ void __launch_bounds__(256, 2) walk_il(const float* in, float* out, u
   }
 }
 
+// block-major ("strip") layout: each array stored as [block][row][BW] with BW = the stored width of
+// one warp strip (28 lanes x 2 = 56 columns), so a warp walking its rows reads one contiguous stream
+// per array (lanes 2..29) plus two 8-byte pieces of each neighbour block (its halo lanes).  R rows
+// per block (ny + 16 padded); block -1 and nblk exist (zero) so that the halo lanes of the edge
+// warps load unconditionally.
+template <int PFD>
+__global__ void __launch_bounds__(256, 2) walk_blk(const float* a0, const float* a1, const float* a2, const float* a3,
+                                                  const float* a4, float* o0, float* o1, float* o2, uint32_t R,
+                                                  int rows, int chunk) {
+  constexpr int BW = 56;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpc = blockDim.x >> 5;
+  const int blk = blockIdx.x * wpc + warp + 1;  // +1: block -1 is the front pad
+  const int bl = blk + (lane < 2 ? -1 : lane >= 30 ? 1 : 0);
+  const int off = lane < 2 ? 52 + 2 * lane : lane >= 30 ? 2 * (lane - 30) : 2 * (lane - 2);
+  const uint32_t c = (uint32_t)bl * R * BW + off;  // element of row 0
+  const uint32_t cs = (uint32_t)blk * R * BW + 2 * (lane - 2);
+  const int r0 = blockIdx.y * chunk + 8, r1 = min(r0 + chunk, rows + 8);
+  float2 x0, x1, x2, x3, x4;
+  auto L = [&](int j) {
+    const uint32_t o = (uint32_t)j * BW + c;
+    x0 = ld(a0 + o); x1 = ld(a1 + o); x2 = ld(a2 + o); x3 = ld(a3 + o); x4 = ld(a4 + o);
+  };
+  L(r0 - 4);
+  for (int j = r0 - 4; j < r1; ++j) {
+    float2 y0 = x0, y1 = x1, y2 = x2, y3 = x3, y4 = x4;
+    if (j + 1 < r1) L(j + 1);
+    if (PFD > 0 && j + 1 + PFD < r1) {
+      const uint32_t o = (uint32_t)(j + 1 + PFD) * BW + c;
+      pf(a0 + o); pf(a1 + o); pf(a2 + o); pf(a3 + o); pf(a4 + o);
+    }
+    if (j >= r0 && lane >= 2 && lane < 30) {
+      const uint32_t o = (uint32_t)(j - 3) * BW + cs;
+      float2 s;
+      s.x = y0.x + y1.x * y3.x; s.y = y0.y + y1.y * y3.y;
+      *reinterpret_cast<float2*>(o0 + o) = s;
+      s.x = y2.x * y4.x; s.y = y2.y - y4.y;
+      *reinterpret_cast<float2*>(o1 + o) = s;
+      s.x = y1.x + y2.x; s.y = y3.y + y0.y;
+      *reinterpret_cast<float2*>(o2 + o) = s;
+    }
+  }
+}
+
 __global__ void copyk(const float4* a, float4* b, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) b[i] = a[i];
 }
@@ -149,6 +192,27 @@ int main() {
     time([&] { walk<4, 1><<<g, wpc * 32>>>(buf[0], buf[1], buf[2], buf[3], buf[4], buf[5], buf[6], buf[7], P, ny, chunk, nout); }, "walk V4 pfd1 ch256 w4", bytes);
     time([&] { walk<4, 0><<<g, wpc * 32>>>(buf[0], buf[1], buf[2], buf[3], buf[4], buf[5], buf[6], buf[7], P, ny, chunk, nout); }, "walk V4 pfd0 ch256 w4", bytes);
     time([&] { walk<4, 2><<<g, wpc * 32>>>(buf[0], buf[1], buf[2], buf[3], buf[4], buf[5], buf[6], buf[7], P, ny, chunk, nout); }, "walk V4 pfd2 ch256 w4", bytes);
+  }
+  {  // block-major layout (walk_blk): 32768 / 56 = 586 blocks (+2 pad), R = ny + 16 rows each
+    const int wpc = 4;
+    const uint32_t R = ny + 16, nblk = (nx + 55) / 56;
+    const size_t nb = (size_t)(nblk + 8) * R * 56;  // the grid rounds the blocks up to whole CTAs
+    float* bb[8];
+    for (int i = 0; i < 8; ++i) {
+      if (cudaMalloc(&bb[i], nb * 4) != cudaSuccess) { printf("oom\n"); return 1; }
+      cudaMemset(bb[i], 0, nb * 4);
+    }
+    for (int chunk : {256, 512, 2048}) {
+      dim3 g((nblk + wpc - 1) / wpc, ny / chunk);
+      char nm[64];
+      snprintf(nm, 64, "blk56 pfd1 ch%d w4", chunk);
+      time([&] { walk_blk<1><<<g, wpc * 32>>>(bb[0], bb[1], bb[2], bb[3], bb[4], bb[5], bb[6], bb[7], R, ny, chunk); }, nm, bytes);
+      snprintf(nm, 64, "blk56 pfd2 ch%d w4", chunk);
+      time([&] { walk_blk<2><<<g, wpc * 32>>>(bb[0], bb[1], bb[2], bb[3], bb[4], bb[5], bb[6], bb[7], R, ny, chunk); }, nm, bytes);
+      snprintf(nm, 64, "blk56 pfd0 ch%d w4", chunk);
+      time([&] { walk_blk<0><<<g, wpc * 32>>>(bb[0], bb[1], bb[2], bb[3], bb[4], bb[5], bb[6], bb[7], R, ny, chunk); }, nm, bytes);
+    }
+    for (int i = 0; i < 8; ++i) cudaFree(bb[i]);
   }
   time([&] { copyk<<<148 * 8, 512>>>((const float4*)buf[0], (float4*)buf[5], n / 4); }, "copy (1 in 1 out)", 8.0 * n);
   return 0;
