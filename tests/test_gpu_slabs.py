@@ -176,3 +176,33 @@ def test_dense_clusters_slabs_bitwise_equal_single(nslab):
     assert np.array_equal(x1, x2)
     assert np.array_equal(p1, p2)
     np.testing.assert_allclose(e2, e1, rtol=1e-6)
+
+
+@pytest.mark.parametrize("nslab", [2, 3])
+@pytest.mark.parametrize("precision", [32, 64])
+def test_slabs_match_oracle_directly(nslab, precision):
+    """S8 against the oracle itself (not only against one context): the slabs' halo plan through the
+    in-process transport, K-step passes (K = 4 fp32, 2 fp64), gathered fields, ROM states (global and
+    per instance), probes and the energy vs the undivided fp64 oracle -- 1e-10 fp64, 1e-4 fp32
+    (north_star tolerances)."""
+    from helpers import instance_pairs, oracle_from_scene, per_instance_errors, rel
+
+    s = slab_scene(precision)
+    assert slabs.check_partition(s.placements, s.models, s.ny, nslab)
+    init = consistent_random_state(s, 7)
+    n = 301
+    (Wg, xg, pg, eg) = run_group(s, n, init, nslab, 4)
+    o = oracle_from_scene(s)
+    Ex, Ey, Hz, xs = init
+    o.set_state(Ex, Ey, Hz, xs)
+    po, eo = o.step(n, energy=True)
+    Exo, Eyo, Hzo, xo = o.get_state()
+    tol = 1e-10 if precision == 64 else 1e-4
+    errs = dict(probe=rel(pg, po), Ex=rel(Wg[0], Exo), Ey=rel(Wg[1], Eyo), Hz=rel(Wg[2], Hzo), rom=rel(xg, xo),
+                energy=rel(eg, eo))
+    px, py = instance_pairs(s, Wg, (Exo, Eyo, Hzo), xg, xo)
+    errs["rom_inst"], mx_rom = per_instance_errors(px)
+    errs["y_inst"], mx_y = per_instance_errors(py)
+    print("slabs", nslab, "fp%d" % precision, errs)
+    bad = {k: v for k, v in errs.items() if not v <= tol}
+    assert not bad and mx_rom <= 10 * tol and mx_y <= 10 * tol, (errs, mx_rom, mx_y)
