@@ -563,7 +563,7 @@ __device__ __forceinline__ void sweep_row(const SweepParams<T>& p, const SweepCt
 #ifndef FDTD_SWEEP_MINB  // 2 x 256 threads: <= 128 registers, 16 resident warps per SM
 #define FDTD_SWEEP_MINB (FDTD_REG_RING ? 1 : 2)
 #endif
-template <typename T, int K, int V, bool ENERGY>
+template <typename T, int K, int V, bool ENERGY, int UR = 2>
 #if defined(FDTD_SWEEP_MAXNREG)
 __global__ void __maxnreg__(FDTD_SWEEP_MAXNREG) sweepk_kernel(
 #else
@@ -659,7 +659,10 @@ __global__ void __launch_bounds__(FDTD_SWEEP_THREADS, FDTD_SWEEP_MINB) sweepk_ke
   // chunk's own (the fast body, unless the chunk holds a probe row); [jend, je): the last rows.
   // Pairs of rows keep the ping-pong parity; the generic body checks rows at run time.
   // Groups of U rows keep the ping-pong parity and (register ring) the static coefficient slots.
-  constexpr int U = (FDTD_REG_RING && K > 2) ? K : 2;
+  // UR = 4 (K = 4 fp32 on chunks of >= 256 rows, sweepk_launch): one rotation of the ping-pong
+  // registers per four rows instead of two (-4.6 % instructions in the fast loop; at 64-row chunks
+  // the longer generic head and tail lose)
+  constexpr int U = (FDTD_REG_RING && K > 2) ? K : (UR == 4 ? 4 : 2);
   RowCoef<T, V> rc[K];
 #if FDTD_REG_RING
 #pragma unroll
@@ -2342,19 +2345,28 @@ void launch_min2(const M* a, const M* b, int64_t n, double* out, int nblocks, cu
 template void launch_min2<float>(const float*, const float*, int64_t, double*, int, cudaStream_t);
 template void launch_min2<double>(const double*, const double*, int64_t, double*, int, cudaStream_t);
 
-template <typename T, int K>
-void sweepk_launch(const SweepParams<T>& q, dim3 grid, int threads, cudaStream_t s) {
+#ifndef FDTD_SWEEP_U4_CHUNK  // rows per chunk from which the fp32 K = 4 sweep runs the four-row body
+#define FDTD_SWEEP_U4_CHUNK 256
+#endif
+template <typename T, int K, int UR>
+void sweepk_launch_u(const SweepParams<T>& q, dim3 grid, int threads, cudaStream_t s) {
   constexpr int V = (sizeof(T) == 4 && K < 4) ? 4 : 2;  // sweep_width
   const size_t smem = (K > 1 && !FDTD_REG_RING) ? (size_t)(threads / 32) * K * NCOEF * 32 * V * sizeof(T) : 0;
   if (q.partials) {
     if (smem > 32 * 1024)  // (static shared memory counts against the 48 KB default too)
-      cudaFuncSetAttribute(sweepk_kernel<T, K, V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sweepk_kernel<T, K, V, true><<<grid, threads, smem, s>>>(q);
+      cudaFuncSetAttribute(sweepk_kernel<T, K, V, true, UR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sweepk_kernel<T, K, V, true, UR><<<grid, threads, smem, s>>>(q);
   } else {
     if (smem > 32 * 1024)  // (static shared memory counts against the 48 KB default too)
-      cudaFuncSetAttribute(sweepk_kernel<T, K, V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sweepk_kernel<T, K, V, false><<<grid, threads, smem, s>>>(q);
+      cudaFuncSetAttribute(sweepk_kernel<T, K, V, false, UR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sweepk_kernel<T, K, V, false, UR><<<grid, threads, smem, s>>>(q);
   }
+}
+template <typename T, int K>
+void sweepk_launch(const SweepParams<T>& q, dim3 grid, int threads, cudaStream_t s) {
+  if constexpr (K == 4 && sizeof(T) == 4)
+    if (q.chunk >= FDTD_SWEEP_U4_CHUNK) return sweepk_launch_u<T, K, 4>(q, grid, threads, s);
+  sweepk_launch_u<T, K, 2>(q, grid, threads, s);
 }
 
 template <typename T>

@@ -94,9 +94,10 @@ def test_ragged_fp64(nx, ny):
     _compare(s, s.steps, 1e-10, random_init=5)
 
 
-@pytest.mark.parametrize("tuning", [(1, 1), (3, 2), (7, 8), (64, 4)])
+@pytest.mark.parametrize("tuning", [(1, 1), (3, 2), (7, 8), (64, 4), (256, 4), (512, 2)])
 def test_tuning_is_bitwise_invariant(tuning):
-    """Chunk-start and warp-edge recomputation are bit-identical to the owner's values."""
+    """Chunk-start and warp-edge recomputation are bit-identical to the owner's values; chunks of >= 256
+    rows take the four-row loop body of the fp32 K = 4 sweep (K1)."""
     s = _ragged_scene(301, 203, 32)
     base = gpu_from_scene(s)
     Ex, Ey, Hz, xs = consistent_random_state(s, 9)
