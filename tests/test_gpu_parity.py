@@ -343,16 +343,19 @@ def test_source_and_probes_on_warp_and_chunk_seams(src):
                  sigma=rng.uniform(0, 0.05, (n, n)), precision=32, steps=300, source=src,
                  samples=sc.gaussian_samples(300, dt, 30e9, True), probes=probes, models=[], placements=None)
     outs = []
-    for spp in (1, 4):
+    for spp, tuning in ((1, None), (4, None), (4, (256, 4))):  # (256, 4): the four-row sweep body
         g = gpu_from_scene(s)
         g.set_time_blocking(spp)
+        if tuning:
+            g.set_tuning(*tuning)
         g.step(300)
         assert g.info().steps_per_pass == spp
         outs.append((g.get_window(), g.probe()))
         g.close()
-    for a, b in zip(outs[0][0], outs[1][0]):
-        assert np.array_equal(a, b)
-    assert np.array_equal(outs[0][1], outs[1][1])
+    for o in outs[1:]:
+        for a, b in zip(outs[0][0], o[0]):
+            assert np.array_equal(a, b)
+        assert np.array_equal(outs[0][1], o[1])
     _compare(s, 300, 1e-4)
 
 
