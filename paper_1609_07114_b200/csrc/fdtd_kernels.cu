@@ -1899,13 +1899,39 @@ __device__ void fixup_batch(const PostParams<T>& p, int bi, T* sv, const T (&g)[
   store_rom(p, m, mem, nb, B, S, sv, p.ex1, p.ey1);
 }
 
+#ifndef FDTD_PERSIST  // fix-up: one CTA per SM walking the batches (b, b + grid, ...), the next batch's
+#define FDTD_PERSIST 0    // regions pulled into L2 while the current one runs
+#endif
+// the rows of batch b's regions (materials and the pass's input fields) into L2 (prefetch hints;
+// rows outside this slab's allocated rows are skipped)
+template <typename T, int K>
+__device__ void prefetch_regions(const PostParams<T>& p, int b) {
+  const int* bt = p.batch_tab + BATCH_FIELDS * b;
+  const int nb = bt[2], kind = bt[5];
+  const int32_t* mem = p.batch_inst + bt[1];
+  const int M = p.Kz + K - 1, nreg = kind ? 1 : nb;
+  const int32_t* q0 = p.rects + 4 * (int64_t)mem[0];
+  const int bw = kind ? p.batch_rect[4 * b + 2] : q0[2], bh = kind ? p.batch_rect[4 * b + 3] : q0[3];
+  const int Wr = bw + 2 * M + 1, Hr = bh + 2 * M + 1, lines = (Wr + 31) / 32 + 1;  // 128-byte lines per row
+  const int per = Hr * lines * 5;
+  for (int it = threadIdx.x; it < nreg * per; it += blockDim.x) {
+    const int r = it / per, rem = it % per, a = rem / (Hr * lines), v = (rem / lines) % Hr, l = rem % lines;
+    const int32_t* q = kind ? p.batch_rect + 4 * b : p.rects + 4 * (int64_t)mem[r];
+    const int64_t i0 = (int64_t)q[0] - M, lr = (int64_t)q[1] - M + v - p.row_begin + p.row0;
+    if (lr < 0 || lr >= p.row0 + p.rows + K) continue;
+    const int64_t c = max(i0, (int64_t)0) + 32 * l;
+    if (c >= p.pitch) continue;
+    const T* base = a == 0 ? p.mea : a == 1 ? p.msb : a == 2 ? p.hz0 : a == 3 ? p.ex0 : p.ey0;
+    prefetch_l2(base + lr * p.pitch + c);
+  }
+}
+
 template <typename T, int K, bool ENERGY>
 __global__ void __launch_bounds__(512, 1) postk_kernel(const PostParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[32];
   __shared__ BatchShared bs;
   T* sv = reinterpret_cast<T*>(smem_raw);
-  const int b = blockIdx.x;
 #if FDTD_PHASES
   if (threadIdx.x == 0) ph_counter() = 0;
   PHASE();
@@ -1920,18 +1946,23 @@ __global__ void __launch_bounds__(512, 1) postk_kernel(const PostParams<T> p) {
       if (k >= 0 && k < p.src_meta[1]) g[s] = (T)p.src_samples[k];
     }
   }
-  if (b < p.n_batch_reg) fixup_batch<T, K, ENERGY>(p, b, sv, g, step, bs);
-  PHASE();
-  if (ENERGY && b < p.n_batch_reg) {  // this batch's ROM + zone energies, one value per step (level 1)
-    __syncthreads();              // rom_partials of this batch written (fixup_batch ends with barriers)
-    const int32_t* mem = p.batch_inst + p.batch_tab[BATCH_FIELDS * b + 1];
-    const int nb = p.batch_tab[BATCH_FIELDS * b + 2];
+  for (int b = blockIdx.x; b < (FDTD_PERSIST ? p.n_batch_reg : blockIdx.x + 1); b += gridDim.x) {
+    if (b >= p.n_batch_reg) break;
+    if (FDTD_PERSIST && b != (int)blockIdx.x) __syncthreads();  // the previous batch's readers are done
+    if (FDTD_PERSIST && b + (int)gridDim.x < p.n_batch_reg) prefetch_regions<T, K>(p, b + gridDim.x);
+    fixup_batch<T, K, ENERGY>(p, b, sv, g, step, bs);
+    PHASE();
+    if (ENERGY) {  // this batch's ROM + zone energies, one value per step (level 1)
+      __syncthreads();  // rom_partials of this batch written (fixup_batch ends with barriers)
+      const int32_t* mem = p.batch_inst + p.batch_tab[BATCH_FIELDS * b + 1];
+      const int nb = p.batch_tab[BATCH_FIELDS * b + 2];
 #pragma unroll 1
-    for (int s = 0; s < K; ++s) {
-      double v = 0.0;
-      for (int k = threadIdx.x; k < nb; k += blockDim.x) v += p.rom_partials[(int64_t)s * p.n_inst + mem[k]];
-      const double tot = block_sum(v, red);
-      if (threadIdx.x == 0) p.level1[(int64_t)s * p.n_batch + b] = tot;
+      for (int s = 0; s < K; ++s) {
+        double v = 0.0;
+        for (int k = threadIdx.x; k < nb; k += blockDim.x) v += p.rom_partials[(int64_t)s * p.n_inst + mem[k]];
+        const double tot = block_sum(v, red);
+        if (threadIdx.x == 0) p.level1[(int64_t)s * p.n_batch + b] = tot;
+      }
     }
   }
 }
@@ -2393,7 +2424,13 @@ size_t post_smem_bytes(size_t es, int nvec, int nY, int batch, int region_stride
 template <typename T, int K>
 void postk_launch(const PostParams<T>& p, bool energy, cudaStream_t s) {
   const size_t smem = p.smem_bytes;
-  const int grid = p.n_batch_reg;
+  int grid = p.n_batch_reg;
+  if (FDTD_PERSIST) {  // one CTA per SM (the fix-up CTA fills an SM's registers)
+    int nsm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    grid = std::min(grid, nsm);
+  }
   if (grid <= 0) return;
   if (energy) {
     if (smem > 32 * 1024)  // (static shared memory counts against the 48 KB default too)
