@@ -348,14 +348,16 @@ def test_source_and_probes_on_warp_and_chunk_seams(src):
         g.set_time_blocking(spp)
         if tuning:
             g.set_tuning(*tuning)
+        g.record_energy(True)
         g.step(300)
         assert g.info().steps_per_pass == spp
-        outs.append((g.get_window(), g.probe()))
+        outs.append((g.get_window(), g.probe(), g.energy()))
         g.close()
     for o in outs[1:]:
         for a, b in zip(outs[0][0], o[0]):
             assert np.array_equal(a, b)
         assert np.array_equal(outs[0][1], o[1])
+        np.testing.assert_allclose(o[2], outs[0][2], rtol=1e-6)  # the same terms, summed in another order
     _compare(s, 300, 1e-4)
 
 
