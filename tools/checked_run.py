@@ -33,7 +33,7 @@ from inputs import configs
 case, k, steps = %r, %d, %d
 if case == "cfg1":
     s = configs.make("cfg1")
-elif case == "cfg3crop":
+elif case in ("cfg3crop", "cfg3crop4row"):
     s = configs.make("cfg3", n=256)
 elif case == "cfg5sub":
     s = configs.make("cfg5", n=512, max_fine=64, min_count=8)
@@ -50,6 +50,8 @@ else:
     s = channel_scene(32, nx=120, ny=40, rom=True)
 g = gpu_from_scene(s, torch_allocator=False, whole_grid=case.endswith("whole"))
 g.set_time_blocking(k)
+if case == "cfg3crop4row":
+    g.set_tuning(256, 4)  # one 256-row chunk: the four-row sweep body
 Ex, Ey, Hz, xs = consistent_random_state(s, 3)
 g.set_window(0, 0, Ex, Ey, Hz)
 if xs.size:
@@ -94,7 +96,7 @@ def main():
         sys.path.insert(0, ROOT)
         from paper_1609_07114_b200 import build
         build.build_checked()
-    cases = [("cfg1", 1), ("cfg1", 2), ("cfg3crop", 1), ("cfg3crop", 2), ("cfg3crop", 4), ("pml", 4),
+    cases = [("cfg1", 1), ("cfg1", 2), ("cfg3crop", 1), ("cfg3crop", 2), ("cfg3crop", 4), ("cfg3crop4row", 4), ("pml", 4),
              ("literal", 4), ("cfg5sub", 4), ("cfg1whole", 2), ("densewhole", 4)]
     res = []
     ok = True
@@ -105,7 +107,7 @@ def main():
         good = all(r["rc"] == 0 and not r["trap"] and r.get("err", 1) <= tol for r in runs) and len(digests) == 1
         ok &= good
         res.append(dict(case=case, k=k, ok=good, runs=runs, bitwise_identical_across_runs_and_threads=len(digests) == 1))
-        print("%-9s K=%d used=%s err=%s traps=%s identical=%s -> %s" % (
+        print("%-12s K=%d used=%s err=%s traps=%s identical=%s -> %s" % (
             case, k, runs[0].get("used"), max(r.get("err", float("nan")) for r in runs),
             any(r["trap"] for r in runs), len(digests) == 1, "ok" if good else "FAIL"), flush=True)
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
