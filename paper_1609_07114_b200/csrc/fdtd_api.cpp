@@ -1308,15 +1308,17 @@ fdtd_status fdtd_set_tuning(fdtd_ctx* c, int32_t rows_per_cta, int32_t warps_per
   if (!c) return FDTD_E_ARG;
   if (rows_per_cta < 0 || warps_per_cta < 0 || warps_per_cta > 8) return fail(c, FDTD_E_ARG, "bad tuning");
   // rows per CTA: the 2K - 1 stage rows recomputed at a chunk start against the tail of the last
-  // wave; a row slab of a multi-GPU run (a few thousand rows) does better with 128 than 64; 512
-  // rows measured 1.3 % faster than 256 on 32768 rows (tools/sweep_layout_probe.cu, round 2).
+  // wave; a row slab of a multi-GPU run does better with 128 than 64 below 8192 rows and with 256
+  // from 8192 rows (config 4 on 4 slabs: 495 vs 482 G, on 8 slabs 128 beats 256: 453 vs 423 G;
+  // profiles/r02g_slab_chunks.txt); 512 rows measured 1.3 % faster than 256 on 32768 rows
+  // (tools/sweep_layout_probe.cu, round 2).
   // Small grids (< 2048 rows, too few CTAs for one wave): a pass is the latency of one CTA's row
   // chain, so short chunks of 2-warp CTAs spread it over >= ~600 CTAs (the Sec. VI-A cavity, 500^2
   // fp64: 43 -> 31 us per step with 4-row chunks)
   const bool slab = c->d.nranks > 1;
   c->chunk = rows_per_cta ? rows_per_cta
                           : (c->rows >= 32768 ? 512 : c->rows >= 16384 ? 256
-                             : c->rows >= 2048 ? (slab && c->rows < 8192 ? 128 : 64) : 32);
+                             : c->rows >= 2048 ? (slab ? (c->rows < 8192 ? 128 : 256) : 64) : 32);
   c->warps = warps_per_cta ? warps_per_cta : 4;
   if (!rows_per_cta && !warps_per_cta && c->rows < 2048) {
     c->warps = 2;
