@@ -71,8 +71,10 @@ def test_cpml_k_step_bitwise():
     s = channel_scene(32, rom=True)
     Ex, Ey, Hz, xs = consistent_random_state(s, 8)
     outs = []
-    for spp in (1, 2, 4):
+    for spp, tuning in ((1, None), (2, None), (4, None), (4, (256, 4))):  # (256, 4): four-row sweep body
         g = gpu_from_scene(s)
+        if tuning:
+            g.set_tuning(*tuning)
         g.set_window(0, 0, Ex, Ey, Hz)
         g.set_rom_state(xs)
         g.set_time_blocking(spp)
