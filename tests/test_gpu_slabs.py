@@ -44,7 +44,7 @@ def run_single(s, n, init):
     return out
 
 
-def run_group(s, n, init, nslab, spp=2, check_spp=True):
+def run_group(s, n, init, nslab, spp=2, check_spp=True, tuning=None):
     import torch
 
     from paper_1609_07114_b200 import Simulation, step_group
@@ -76,6 +76,8 @@ def run_group(s, n, init, nslab, spp=2, check_spp=True):
         sim.set_probes(s.probes)
         sim.record_energy(True)
         sim.set_time_blocking(spp)
+        if tuning:
+            sim.set_tuning(*tuning)
         sim.set_window(0, 0, Ex, Ey, Hz)
         idx = [next(t for t, (mm, a, b) in enumerate(glob) if (a, b) == (i0, j0)) for _, i0, j0 in mine]
         if idx:
@@ -206,3 +208,33 @@ def test_slabs_match_oracle_directly(nslab, precision):
     print("slabs", nslab, "fp%d" % precision, errs)
     bad = {k: v for k, v in errs.items() if not v <= tol}
     assert not bad and mx_rom <= 10 * tol and mx_y <= 10 * tol, (errs, mx_rom, mx_y)
+
+
+@pytest.mark.parametrize("nslab", [2, 3])
+def test_tall_slabs_with_long_chunks_bitwise(nslab):
+    """Slabs of several 256-row chunks (the multi-GPU rule for 8,192-16,383-row slabs, four-row sweep
+    body): the interior / slab-edge chunk split with K = 4 passes is bit-identical to one context."""
+    nx, ny = 120, 1600
+    rng = np.random.default_rng(21)
+    dx = dy = 1e-3
+    fe, fs = sc.uniform_fill(3, 2, 3, 1, 1, 4, 0, 0.05)
+    m1 = rg.build_rom(3, 2, 3, dx, dy, fe, fs, 20, 30e9)
+    dt = 0.95 * m1["fine_dt_limit"]
+    src = (60, 799)
+    probes = np.array([[60, 800], [10, 255], [100, 1023], [5, 1599]], dtype=np.int32)
+    P = sc.place_blocks(nx, ny, [(3, 2)], 40, seed=6, nslabs=12, forbid=[src] + [tuple(p) for p in probes])
+    # keep the fix-up regions (block + 7 cells for K = 4) clear of the 2- and 3-slab boundaries
+    cuts = sorted({slabs.slab_rows(ny, n, k)[0] for n in (2, 3) for k in range(1, n)})
+    P = P[[all(not (j0 - 8 <= c < j0 + 2 + 8) for c in cuts) for _, _, j0 in P]]
+    s = sc.Scene(name="tall", nx=nx, ny=ny, dx=dx, dy=dy, dt=dt, eps_r=rng.uniform(1, 4, (ny, nx)),
+                 sigma=rng.uniform(0, 0.05, (ny, nx)), precision=32, steps=200, source=src,
+                 samples=sc.gaussian_samples(200, dt, 30e9, True), probes=probes, models=[m1], placements=P)
+    assert slabs.check_partition(s.placements, s.models, s.ny, nslab)
+    init = consistent_random_state(s, 2)
+    (W1, x1, p1, e1) = run_single(s, 101, init)
+    (W2, x2, p2, e2) = run_group(s, 101, init, nslab, 4, tuning=(256, 4))
+    for a, b in zip(W1, W2):
+        assert np.array_equal(a, b)
+    assert np.array_equal(x1, x2)
+    assert np.array_equal(p1, p2)
+    np.testing.assert_allclose(e2, e1, rtol=1e-6)
